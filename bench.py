@@ -1,0 +1,288 @@
+#!/usr/bin/env python
+"""Benchmark: LJ melt (and SNAP) atom-steps/s on B200, one JSON line on rank 0.
+
+Workload at N=1 (BASELINE.json configs[1]): LJ 12-6 melt, 2,048,000 atoms fcc
+rho*=0.8442 (80^3 cells), rc=2.5, skin=0.3, T=1.44 (seed 87287), dt=0.005,
+velocity-Verlet NVE with skin rebuilds — both the full/newton-off list (no
+atomics, headline `value`) and the half/newton-on list (FP64 atomics).  A
+"step" is one full velocity-Verlet step (kick+drift+skin test, halo refresh
+or rebuild, force, kick).  Inputs (x, v, f, table: ~1 GB) exceed the 126 MB L2.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Matom-steps/s for LJ & SNAP at 1/2/4/8 B200; % of HBM / FP64 roofline"
+UNIT = "Matom-steps/s"
+LJ = dict(rho=0.8442, cells=80, rc=2.5, skin=0.3, T=1.44, seed=87287, dt=0.005)
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def lj_script(cells, style_newton_thermo=10 ** 9, steps=0):
+    return (f"units lj\nboundary p p p\nlattice fcc {LJ['rho']}\ncreate_box {cells} {cells} {cells}\n"
+            f"create_atoms\nmass 1.0\nvelocity {LJ['T']} {LJ['seed']}\npair_style lj/cut {LJ['rc']}\n"
+            f"pair_coeff 1.0 1.0\ntimestep {LJ['dt']}\nthermo {style_newton_thermo}\n")
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """Samples SM clock + throttle reasons with NVML every 100 ms while running."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown", 0x1: "gpu_idle"}
+
+    def __init__(self, index=0):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001
+            self._nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self._nv.nvmlDeviceGetClockInfo(self._h, self._nv.NVML_CLOCK_SM))
+                r = self._nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        if self._nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._nv is not None:
+            self._t.join()
+
+    def summary(self):
+        return {"sm_mhz": float(np.median(self.samples)) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------- CPU oracle
+def cpu_lj_sample(steps=20, cells=20, style="full"):
+    """Oracle (numpy port of mdkk) on a bounded sample: 32k atoms, same physics, `steps` timed steps."""
+    from oracle import md
+    pos, L = md.lattice("fcc", LJ["rho"], (cells, cells, cells))
+    vel = md.seeded_velocities(len(pos), LJ["T"], 1.0, LJ["seed"])
+    run = md.LJRun(pos, vel, L, rc=LJ["rc"], skin=LJ["skin"], style=style, newton=(style == "half"), dt=LJ["dt"])
+    run.forces()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        run.step()
+    dt = time.perf_counter() - t0
+    return len(pos) * steps / dt / 1e6, dt, len(pos)
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    per_step = []
+    from oracle import md
+    pos, L = md.lattice("fcc", LJ["rho"], (20, 20, 20))
+    vel = md.seeded_velocities(len(pos), LJ["T"], 1.0, LJ["seed"])
+    run = md.LJRun(pos, vel, L, rc=LJ["rc"], skin=LJ["skin"], style="full", newton=False, dt=LJ["dt"])
+    run.forces()
+    for _ in range(args.warmup):
+        run.step()
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        run.step()
+        per_step.append(time.perf_counter() - t0)
+    tot = sum(per_step)
+    value = len(pos) * args.steps / tot / 1e6
+    sample = (f"numpy oracle port of mdkk (oracle/md.py), LJ melt 32,000 atoms fcc rho 0.8442 rc 2.5 skin 0.3 "
+              f"T 1.44 dt 0.005 full list, {args.steps} steps after {args.warmup} warm-up")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "LJ melt, bounded CPU sample of configs[1] (32k atoms)", "n_atoms": len(pos)},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+
+
+# -------------------------------------------------------------------- GPU
+def lj_run(style, cells, steps, warmup, device, profile=True):
+    import torch
+    from paper_2508_13523_b200 import _lib
+    from paper_2508_13523_b200.driver import RunConfig, Simulation
+    sim = Simulation(RunConfig(list_style=style, newton=(style == "half"), skin=LJ["skin"], device=device),
+                     log=None)
+    sim.execute(lj_script(cells))
+    sim._ensure_system()
+    sim._forces_device()
+    for _ in range(warmup):
+        sim.step_device()
+    torch.cuda.synchronize()
+    fev = []
+    orig = sim._forces_device
+
+    def timed_forces():
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        e = orig()
+        b.record()
+        fev.append((a, b))
+        return e
+    if profile:
+        sim._forces_device = timed_forces
+    rebuild0, l0 = sim.n_rebuilds, _lib.launch_count()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(device.index or 0) as clk:
+        torch.cuda.synchronize()
+        start.record()
+        for _ in range(steps):
+            sim.step_device()
+        end.record()
+        torch.cuda.synchronize()
+    ms = start.elapsed_time(end) / steps
+    launches = _lib.launch_count() - l0
+    fms = float(np.mean([a.elapsed_time(b) for a, b in fev])) if fev else None
+    st = sim.system.stores[0]
+    nn = float(sim.lists[0].counts_dev[: st.n_local].double().mean().item())
+    e = float(sim._e_dev.item())
+    return dict(ms=ms, force_ms=fms, n_atoms=sim.system.n_atoms, rebuilds=sim.n_rebuilds - rebuild0,
+                launches=launches, nn=nn, clocks=clk.summary(), e_pot=e, n_ghost=st.n_ghost)
+
+
+def lj_e2e(style, cells, steps, device):
+    """Public API end to end: host arrays -> distribute/build -> run_nve(steps) -> thermo + gid-ordered D2H."""
+    import torch
+    from paper_2508_13523_b200.driver import RunConfig, Simulation
+    sim = Simulation(RunConfig(list_style=style, newton=(style == "half"), skin=LJ["skin"], device=device),
+                     log=None)
+    sim.execute(lj_script(cells, style_newton_thermo=steps))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    sim.run_nve(steps)          # upload, build, steps, thermo at 0 and `steps` (+ gid-ordered snapshots)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    n = sim.system.n_atoms
+    h2d = n * 2 * 3 * 8                         # positions + velocities uploaded once
+    d2h = 2 * (n * 3 * 8 + 2 * 8)               # two thermo snapshots (positions) + E, KE
+    return dict(value=n * steps / dt / 1e6, h2d=h2d / steps, d2h=d2h / steps)
+
+
+def traffic_from_profiles(kernel="k_lj"):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get(kernel)
+    return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cells", type=int, default=LJ["cells"])
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=device)
+
+    full = lj_run("full", args.cells, args.steps, args.warmup, device)
+    half = lj_run("half", args.cells, args.steps, args.warmup, device)
+    ms = full["ms"]
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], device=device, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    n_atoms = full["n_atoms"] * world   # independent replicas until the DD path lands
+    value = n_atoms / (ms * 1e-3) / 1e6
+    peak, peak_kind = _peaks()
+    nn = full["nn"]
+    bytes_per_launch = full["n_atoms"] * (28.0 * nn + 52.0)
+    achieved = bytes_per_launch / (full["force_ms"] * 1e-3) / 1e9
+    e2e = lj_e2e("full", args.cells, max(args.steps, 20), device) if not args.no_e2e else None
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        v, secs, n = cpu_lj_sample()
+        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": f"numpy oracle port, LJ melt {n} atoms (same rho/rc/skin/T/dt, full list), 20 steps "
+                         f"after initial build, {secs:.1f} s, 1 thread of {os.cpu_count()}"}
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "LJ 12-6 melt fcc rho*=0.8442, rc=2.5, skin=0.3, T=1.44, dt=0.005, "
+                                   "full list newton-off (configs[1])",
+                       "n_atoms": full["n_atoms"], "n_ghost": full["n_ghost"], "list": "full",
+                       "rebuilds_in_timed_steps": full["rebuilds"], "mean_neighbors": nn,
+                       "l2": "inputs (x,v,f,table ~%.0f MB) larger than L2" % (full["n_atoms"] * (nn * 4 + 96) / 1e6),
+                       "parallelism": "replicas" if world > 1 else "1 GPU"},
+            "variants": {
+                "lj_full_newton_off": {"value": value, "ms_per_step": full["ms"], "force_ms": full["force_ms"],
+                                       "rebuilds": full["rebuilds"]},
+                "lj_half_newton_on_atomics": {"value": half["n_atoms"] / (half["ms"] * 1e-3) / 1e6,
+                                              "ms_per_step": half["ms"], "force_ms": half["force_ms"],
+                                              "rebuilds": half["rebuilds"], "mean_neighbors": half["nn"]},
+            },
+            "roofline": {"bound": "hbm", "kernel": "k_lj<full> (+ partial reduce)", "achieved": achieved,
+                         "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": traffic_from_profiles("k_lj"),
+                         "bytes_model": f"n_local*(28*nn+52), nn={nn:.2f} measured"},
+            "cpu_baseline": cpu,
+            "e2e": ({"value": e2e["value"], "unit": UNIT, "h2d_bytes_per_step": e2e["h2d"],
+                     "d2h_bytes_per_step": e2e["d2h"]} if e2e else None),
+            "gpu_launches": full["launches"],
+            "clocks": full["clocks"],
+        }
+        print(json.dumps(out))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,156 @@
+/*
+ * mdkk_b200.h — C ABI of the B200-native force-and-neighbor hot path.
+ *
+ * This is the drop-in boundary for the reference `mdkk` engine
+ * (/root/reference/pkg/src/mdkk).  Every entry point replaces one reference
+ * function (cited per declaration); the Python host layer
+ * (paper_2508_13523_b200/) keeps the reference's Python signatures and binds
+ * these through ctypes.
+ *
+ * Conventions
+ *  - All array arguments are DEVICE pointers owned by the caller unless the
+ *    name ends in `_host`.  No torch types cross this boundary.
+ *  - Positions / forces / velocities are AoS-padded double4 rows
+ *    (x, y, z, pad): one 32-byte sector per neighbour gather.
+ *  - Neighbour tables are int32 [cap][n_local] (atom index fastest: the
+ *    reference's transposed `layout_b`, mdkk/memspace.py:99-100), padded -1
+ *    beyond counts[i].
+ *  - `stream` is a cudaStream_t (may be NULL = legacy default stream).
+ *  - Every function returns an mdkk_status; calls are asynchronous on
+ *    `stream` unless documented otherwise.  No C++ exception crosses the ABI.
+ */
+#ifndef MDKK_B200_H
+#define MDKK_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    MDKK_OK = 0,
+    MDKK_E_CAPACITY = 1,   /* neighbour row overflow: grow cap x1.5 and rebuild (mdkk/neighbor.py:199-205) */
+    MDKK_E_COINCIDENT = 2, /* r^2 <= 0 (mdkk/pair_lj.py:83-84, mdkk/snap/compute.py:117-118) */
+    MDKK_E_NONFINITE = 3,  /* non-finite energy / force (mdkk/driver/simulation.py:459-464) */
+    MDKK_E_ARG = 4,        /* invalid argument */
+    MDKK_E_CUDA = 5        /* CUDA runtime error (see mdkk_last_error) */
+} mdkk_status;
+
+/* Device error-word bits written by kernels (read lazily by the host). */
+#define MDKK_FLAG_COINCIDENT 1
+#define MDKK_FLAG_NONFINITE 2
+
+typedef struct mdkk_ctx mdkk_ctx;   /* per-device scratch arena (opaque) */
+typedef struct mdkk_snap mdkk_snap; /* SNAP coupling tables on device (opaque) */
+
+/* ------------------------------------------------------------------ misc */
+int mdkk_version(void);
+/* Number of kernels this library has launched in the process (all devices). */
+unsigned long long mdkk_launch_count(void);
+const char* mdkk_last_error(void);
+int mdkk_device_sm_count(int device, int* out_host);
+int mdkk_ctx_create(int device, mdkk_ctx** out_host);
+int mdkk_ctx_destroy(mdkk_ctx* ctx);
+
+/* ------------------------------------------------------ domain / halo comm
+ * Replaces mdkk/domain.py:56-63 (wrap), :246-293 (exchange_ghosts selection),
+ * :295-305 (forward_comm pack), :307-322 (reverse_comm fold), :324-334
+ * (migrate: wrap + reorder).
+ */
+/* x[i] wrapped into [0, L) per axis. */
+int mdkk_wrap(double* x, int n, const double* lengths_host, void* stream);
+
+/* Halo selection over `n` owned rows of x against C combos.  combos_dev is
+ * double[C][9] = {lo[3], hi[3], shift[3]}; an atom is selected for combo c iff
+ * x + shift lies in [lo, hi) on every axis (half-open, mdkk/domain.py:274).
+ * Two phases: count writes totals[C] (device) and per-block offsets into
+ * block_scratch (int[ceil(n/256) * C]); fill writes out_idx combo-major, atoms
+ * ascending within a combo — the reference's src/shift/index order. */
+int mdkk_halo_count(mdkk_ctx* ctx, const double* x, int n, const double* combos_dev, int C,
+                    int* block_scratch, int* totals, void* stream);
+int mdkk_halo_fill(mdkk_ctx* ctx, const double* x, int n, const double* combos_dev, int C,
+                   const int* block_scratch, const int* totals, int* out_idx, void* stream);
+
+/* Forward-comm pack: out[k] = x[idx[k]] + shift_table[code[k]] (shift_table is
+ * double[27][3] device, code int8 in 0..26).  `out` may alias ghost rows of x. */
+int mdkk_pack_shift(const double* x, const int* idx, const int8_t* code, const double* shift_table,
+                    int n, double* out, void* stream);
+/* Reverse-comm unpack: f[idx[k]] += buf[k] (FP64 atomics; idx may repeat). */
+int mdkk_fold_add(double* f, const int* idx, const double* buf, int n, void* stream);
+/* Gather rows by permutation: dst[i] = src[perm[i]] for double4 rows / int64 / int32. */
+int mdkk_gather_rows4(const double* src, const int* perm, int n, double* dst, void* stream);
+int mdkk_gather_i64(const int64_t* src, const int* perm, int n, int64_t* dst, void* stream);
+int mdkk_gather_i32(const int32_t* src, const int* perm, int n, int32_t* dst, void* stream);
+/* Scatter rows by permutation: dst[perm[i]] = src[i] (gid-ordered gather for host views). */
+int mdkk_scatter_rows4(const double* src, const int* perm, int n, double* dst, void* stream);
+
+/* ----------------------------------------------------------------- binning
+ * Counting-sort cell binning (replaces the bbox/argsort/bincount of
+ * mdkk/neighbor.py:88-96).  grid_host = {origin[3], inv_width[3]} and
+ * ncell_host = {nx, ny, nz}; cell id = (cx*ny + cy)*nz + cz (x slowest, as
+ * mdkk/neighbor.py:93).  Out-of-grid atoms clamp to edge cells, which keeps
+ * the 27-cell stencil complete when every width >= the build cutoff. */
+int mdkk_cell_keys(const double* x, int n, const double* grid_host, const int* ncell_host, int* keys,
+                   void* stream);
+/* Owning brick of each row: floor(pos / L * grid) clipped (mdkk/domain.py:89-95). */
+int mdkk_rank_keys(const double* x, int n, const double* lengths_host, const int* grid_host, int* keys,
+                   void* stream);
+/* Stable bucket sort by int key in [0, nbuckets): bucket_start[nbuckets+1],
+ * order[n] (rows of a bucket contiguous, ascending row index). */
+int mdkk_bucket_sort(mdkk_ctx* ctx, const int* keys, int n, int nbuckets, int* bucket_start, int* order,
+                     void* stream);
+/* cell_keys + bucket_sort.  keys is caller scratch int[n]. */
+int mdkk_bin_atoms(mdkk_ctx* ctx, const double* x, int n, const double* grid_host, const int* ncell_host,
+                   int* keys, int* cell_start, int* cell_atoms, void* stream);
+
+/* -------------------------------------------------------------- neighbour
+ * Per-atom stencil scan (replaces mdkk/neighbor.py:83-219 + _apply_style
+ * :134-179).  style 0 = full, 1 = half; newton as in the reference.
+ * Row i receives every partner j != i with r^2 < bc2 (strict) passing the
+ * style predicate; half lists use gid / owner_rank / z-y-x rules.
+ * counts[i] is the true count even when > cap; *max_count (device int) gets
+ * the max.  The caller grows cap x1.5 and relaunches when max_count > cap. */
+int mdkk_nbr_build(mdkk_ctx* ctx, const double* x, int n_local, int n_total,
+                   const double* grid_host, const int* ncell_host, const int* cell_start,
+                   const int* cell_atoms, const int64_t* gid, const int32_t* owner_rank, int my_rank,
+                   double bc2, int style, int newton, int cap, int* table, int* counts,
+                   int* max_count, void* stream);
+/* Canonical per-row order (partner gid, z, y, x) — mdkk/neighbor.py:192-197.
+ * In-place sort of each row of a table; used by NeighborList.pairs(). */
+int mdkk_nbr_canonicalize(const double* x, const int64_t* gid, int n_local, int cap,
+                          int* table, const int* counts, void* stream);
+/* max_i |x_i - x_ref_i|^2 into *out (device double) — mdkk/neighbor.py:66-74. */
+int mdkk_max_disp2(const double* x, const double* x_ref, int n, double* out, void* stream);
+
+/* --------------------------------------------------------------------- LJ
+ * Truncated 12-6 LJ (mdkk/pair_lj.py:81-91) over a neighbour table
+ * (compute_pair, mdkk/pair_lj.py:114-179).  style/newton select the entry
+ * semantics of mdkk/neighbor.py:134-179:
+ *   full          : f_i only, weight 1/2, no atomics (owner writes)
+ *   half, newton  : f_i and f_j (FP64 atomics; ghosts folded by reverse comm)
+ *   half, !newton : f_j written only for local j; ghost entries weight 1/2
+ * f must be zeroed by the caller for half lists (atomics accumulate).
+ * ev (device double[7]) receives {E, Wxx, Wyy, Wzz, Wxy, Wxz, Wyz}
+ * (deterministic two-stage reduction).  flags (device int) gets
+ * MDKK_FLAG_COINCIDENT if any in-range r^2 <= 0. */
+int mdkk_lj_force(mdkk_ctx* ctx, const double* x, int n_local, const int* table,
+                  const int* counts, int cap, int style, int newton, double epsilon,
+                  double sigma, double rc, double* f, double* ev, int* flags, void* stream);
+
+/* ------------------------------------------------------------- integrator
+ * Velocity Verlet (mdkk/driver/simulation.py:431-450) fused with the skin
+ * test (mdkk/neighbor.py:66-74).  first: v += h f; x += dt v;
+ * *maxdisp2 = max |x - x_ref|^2.  second: v += h f; ke (optional,
+ * device double) = sum 1/2 m v^2 (mdkk/driver/simulation.py:407-415). */
+int mdkk_verlet_first(mdkk_ctx* ctx, double* x, double* v, const double* f, const double* x_ref,
+                      int n, double dt, double half_dt_over_m, double* maxdisp2, void* stream);
+int mdkk_verlet_second(mdkk_ctx* ctx, double* v, const double* f, int n, double half_dt_over_m,
+                       double mass, double* ke, void* stream);
+/* Sum of 1/2 m |v|^2 over n rows into *ke (device double). */
+int mdkk_kinetic(mdkk_ctx* ctx, const double* v, int n, double mass, double* ke, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MDKK_B200_H */

@@ -1,0 +1,95 @@
+// Context, errors, scratch arena and the deterministic partial reducer.
+#include <atomic>
+
+#include "common.cuh"
+
+namespace mdkk {
+
+static thread_local std::string g_last_error;
+static std::atomic<unsigned long long> g_launches{0};
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+int cuda_fail(cudaError_t e, const char* what) {
+    set_error(std::string(what) + ": " + cudaGetErrorString(e));
+    return MDKK_E_CUDA;
+}
+
+void* scratch(mdkk_ctx* ctx, size_t bytes) {
+    if (bytes <= ctx->scratch_bytes) return ctx->scratch;
+    size_t want = bytes + bytes / 2 + (1 << 20);
+    if (ctx->scratch) {
+        cudaDeviceSynchronize();
+        cudaFree(ctx->scratch);
+    }
+    ctx->scratch = nullptr;
+    ctx->scratch_bytes = 0;
+    if (cudaMalloc(&ctx->scratch, want) != cudaSuccess) return nullptr;
+    ctx->scratch_bytes = want;
+    return ctx->scratch;
+}
+
+__global__ void k_reduce_partials(const double* __restrict__ p, int nb, int K, double* __restrict__ out) {
+    // one block; thread t sums a strided slice of column k, then a fixed-order tree
+    __shared__ double sm[256];
+    for (int k = 0; k < K; ++k) {
+        double s = 0.0;
+        for (int b = threadIdx.x; b < nb; b += blockDim.x) s += p[(long long)b * K + k];
+        sm[threadIdx.x] = s;
+        __syncthreads();
+        for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+            if (threadIdx.x < w) sm[threadIdx.x] += sm[threadIdx.x + w];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) out[k] = sm[0];
+        __syncthreads();
+    }
+}
+
+void reduce_partials(const double* partials, int nblocks, int K, double* out, cudaStream_t s) {
+    k_reduce_partials<<<1, 256, 0, s>>>(partials, nblocks, K, out);
+}
+
+}  // namespace mdkk
+
+extern "C" {
+
+int mdkk_version(void) { return 1; }
+
+unsigned long long mdkk_launch_count(void) { return mdkk::g_launches.load(); }
+
+const char* mdkk_last_error(void) { return mdkk::g_last_error.c_str(); }
+
+int mdkk_device_sm_count(int device, int* out_host) {
+    if (!out_host) return MDKK_E_ARG;
+    cudaError_t e = cudaDeviceGetAttribute(out_host, cudaDevAttrMultiProcessorCount, device);
+    return e == cudaSuccess ? MDKK_OK : mdkk::cuda_fail(e, "cudaDeviceGetAttribute");
+}
+
+int mdkk_ctx_create(int device, mdkk_ctx** out_host) {
+    if (!out_host) return MDKK_E_ARG;
+    auto* c = new mdkk_ctx();
+    c->device = device;
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) {
+        delete c;
+        return mdkk::cuda_fail(e, "cudaSetDevice");
+    }
+    cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
+    *out_host = c;
+    return MDKK_OK;
+}
+
+int mdkk_ctx_destroy(mdkk_ctx* ctx) {
+    if (!ctx) return MDKK_OK;
+    if (ctx->scratch) {
+        cudaDeviceSynchronize();
+        cudaFree(ctx->scratch);
+    }
+    delete ctx;
+    return MDKK_OK;
+}
+
+}  // extern "C"

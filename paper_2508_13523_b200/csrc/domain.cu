@@ -1,0 +1,241 @@
+// Domain kernels: wrap, halo selection (stable multi-way compaction),
+// forward-comm pack with periodic shift, reverse-comm fold, row permutes.
+// Reference: mdkk/domain.py:56-63, :246-334.
+#include "common.cuh"
+
+namespace {
+
+constexpr int kHaloBlock = 256;
+constexpr int kMaxCombos = 27 * 64;
+
+__global__ void k_wrap(double* __restrict__ x, int n, double Lx, double Ly, double Lz) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double4 p = mdkk::ld4_nc(x, i);
+    // pos - L * floor(pos / L) exactly as mdkk/domain.py:62
+    p.x = p.x - Lx * floor(p.x / Lx);
+    p.y = p.y - Ly * floor(p.y / Ly);
+    p.z = p.z - Lz * floor(p.z / Lz);
+    mdkk::st4(x, i, p);
+}
+
+__device__ __forceinline__ bool in_combo(const double4& p, const double* c) {
+    // shifted = x + shift ; lo <= shifted < hi on every axis (mdkk/domain.py:273-274)
+    double sx = p.x + c[6], sy = p.y + c[7], sz = p.z + c[8];
+    return sx >= c[0] && sx < c[3] && sy >= c[1] && sy < c[4] && sz >= c[2] && sz < c[5];
+}
+
+__global__ void k_halo_count(const double* __restrict__ x, int n, const double* __restrict__ combos,
+                             int C, int* __restrict__ block_counts) {
+    extern __shared__ double sc[];
+    for (int t = threadIdx.x; t < 9 * C; t += blockDim.x) sc[t] = combos[t];
+    __syncthreads();
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    double4 p = make_double4(0, 0, 0, 0);
+    if (i < n) p = mdkk::ld4(x, i);
+    for (int c = 0; c < C; ++c) {
+        int flag = (i < n) && in_combo(p, sc + 9 * c);
+        int cnt = __syncthreads_count(flag);
+        if (threadIdx.x == 0) block_counts[(long long)blockIdx.x * C + c] = cnt;
+    }
+}
+
+// One block per combo: exclusive scan over blocks (stride C) in place; totals[c].
+__global__ void k_halo_scan(int* __restrict__ block_counts, int nb, int C, int* __restrict__ totals) {
+    __shared__ int warp_tot[32];
+    __shared__ int carry;
+    const int c = blockIdx.x;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int base = 0; base < nb; base += blockDim.x) {
+        int b = base + threadIdx.x;
+        int v = b < nb ? block_counts[(long long)b * C + c] : 0;
+        int incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        if (lane == 31) warp_tot[wid] = incl;
+        __syncthreads();
+        if (wid == 0) {
+            int w = lane < nw ? warp_tot[lane] : 0;
+            int wi = w;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                int t = __shfl_up_sync(0xffffffffu, wi, o);
+                if (lane >= o) wi += t;
+            }
+            if (lane < nw) warp_tot[lane] = wi - w;  // exclusive warp offsets
+        }
+        __syncthreads();
+        int excl = carry + warp_tot[wid] + incl - v;
+        if (b < nb) block_counts[(long long)b * C + c] = excl;
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) carry = excl + v;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) totals[c] = carry;
+}
+
+__global__ void k_halo_fill(const double* __restrict__ x, int n, const double* __restrict__ combos, int C,
+                            const int* __restrict__ block_off, const int* __restrict__ totals,
+                            int* __restrict__ out) {
+    extern __shared__ double sc[];
+    int* base = reinterpret_cast<int*>(sc + 9 * C);
+    __shared__ int warp_cnt[kHaloBlock / 32];
+    for (int t = threadIdx.x; t < 9 * C; t += blockDim.x) sc[t] = combos[t];
+    if (threadIdx.x == 0) {
+        int s = 0;
+        for (int c = 0; c < C; ++c) {
+            base[c] = s;
+            s += totals[c];
+        }
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    double4 p = make_double4(0, 0, 0, 0);
+    if (i < n) p = mdkk::ld4(x, i);
+    for (int c = 0; c < C; ++c) {
+        bool flag = (i < n) && in_combo(p, sc + 9 * c);
+        unsigned m = __ballot_sync(0xffffffffu, flag);
+        if (lane == 0) warp_cnt[wid] = __popc(m);
+        __syncthreads();
+        int before = 0;
+        for (int w = 0; w < wid; ++w) before += warp_cnt[w];
+        if (flag) {
+            int r = before + __popc(m & ((1u << lane) - 1u));
+            out[base[c] + block_off[(long long)blockIdx.x * C + c] + r] = i;
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void k_pack_shift(const double* __restrict__ x, const int* __restrict__ idx,
+                             const int8_t* __restrict__ code, const double* __restrict__ shifts, int n,
+                             double* __restrict__ out) {
+    int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    double4 p = mdkk::ld4_nc(x, idx[k]);
+    const double* s = shifts + 3 * code[k];
+    // ghost x = owner x + shift: one rounding, as mdkk/domain.py:281,300
+    mdkk::st4(out, k, make_double4(p.x + s[0], p.y + s[1], p.z + s[2], 0.0));
+}
+
+__global__ void k_fold_add(double* __restrict__ f, const int* __restrict__ idx,
+                           const double* __restrict__ buf, int n) {
+    int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    double4 b = mdkk::ld4_nc(buf, k);
+    double* t = f + 4LL * idx[k];
+    atomicAdd(t + 0, b.x);
+    atomicAdd(t + 1, b.y);
+    atomicAdd(t + 2, b.z);
+}
+
+__global__ void k_gather4(const double* __restrict__ src, const int* __restrict__ perm, int n,
+                          double* __restrict__ dst) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) mdkk::st4(dst, i, mdkk::ld4_nc(src, perm[i]));
+}
+__global__ void k_scatter4(const double* __restrict__ src, const int* __restrict__ perm, int n,
+                           double* __restrict__ dst) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) mdkk::st4(dst, perm[i], mdkk::ld4_nc(src, i));
+}
+template <typename T>
+__global__ void k_gather(const T* __restrict__ src, const int* __restrict__ perm, int n, T* __restrict__ dst) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = src[perm[i]];
+}
+
+}  // namespace
+
+extern "C" {
+
+int mdkk_wrap(double* x, int n, const double* L, void* stream) {
+    if (n < 0 || !L) return MDKK_E_ARG;
+    if (n == 0) return MDKK_OK;
+    k_wrap<<<mdkk::grid_for(n, 256), 256, 0, mdkk::as_stream(stream)>>>(x, n, L[0], L[1], L[2]);
+    MDKK_CHECK_LAUNCH("k_wrap");
+    return MDKK_OK;
+}
+
+int mdkk_halo_count(mdkk_ctx*, const double* x, int n, const double* combos, int C, int* block_scratch,
+                    int* totals, void* stream) {
+    if (n < 0 || C < 0 || C > kMaxCombos) return MDKK_E_ARG;
+    if (C == 0) return MDKK_OK;
+    cudaStream_t s = mdkk::as_stream(stream);
+    int nb = mdkk::grid_for(n, kHaloBlock);
+    size_t sm = sizeof(double) * 9 * C;
+    k_halo_count<<<nb, kHaloBlock, sm, s>>>(x, n, combos, C, block_scratch);
+    MDKK_CHECK_LAUNCH("k_halo_count");
+    k_halo_scan<<<C, 1024, 0, s>>>(block_scratch, nb, C, totals);
+    MDKK_CHECK_LAUNCH("k_halo_scan");
+    return MDKK_OK;
+}
+
+int mdkk_halo_fill(mdkk_ctx*, const double* x, int n, const double* combos, int C, const int* block_scratch,
+                   const int* totals, int* out_idx, void* stream) {
+    if (n < 0 || C < 0 || C > kMaxCombos) return MDKK_E_ARG;
+    if (C == 0 || n == 0) return MDKK_OK;
+    int nb = mdkk::grid_for(n, kHaloBlock);
+    size_t sm = sizeof(double) * 9 * C + sizeof(int) * C;
+    k_halo_fill<<<nb, kHaloBlock, sm, mdkk::as_stream(stream)>>>(x, n, combos, C, block_scratch, totals,
+                                                                  out_idx);
+    MDKK_CHECK_LAUNCH("k_halo_fill");
+    return MDKK_OK;
+}
+
+int mdkk_pack_shift(const double* x, const int* idx, const int8_t* code, const double* shifts, int n,
+                    double* out, void* stream) {
+    if (n < 0) return MDKK_E_ARG;
+    if (n == 0) return MDKK_OK;
+    k_pack_shift<<<mdkk::grid_for(n, 256), 256, 0, mdkk::as_stream(stream)>>>(x, idx, code, shifts, n, out);
+    MDKK_CHECK_LAUNCH("k_pack_shift");
+    return MDKK_OK;
+}
+
+int mdkk_fold_add(double* f, const int* idx, const double* buf, int n, void* stream) {
+    if (n < 0) return MDKK_E_ARG;
+    if (n == 0) return MDKK_OK;
+    k_fold_add<<<mdkk::grid_for(n, 256), 256, 0, mdkk::as_stream(stream)>>>(f, idx, buf, n);
+    MDKK_CHECK_LAUNCH("k_fold_add");
+    return MDKK_OK;
+}
+
+int mdkk_gather_rows4(const double* src, const int* perm, int n, double* dst, void* stream) {
+    if (n < 0) return MDKK_E_ARG;
+    if (n == 0) return MDKK_OK;
+    k_gather4<<<mdkk::grid_for(n, 256), 256, 0, mdkk::as_stream(stream)>>>(src, perm, n, dst);
+    MDKK_CHECK_LAUNCH("k_gather4");
+    return MDKK_OK;
+}
+
+int mdkk_scatter_rows4(const double* src, const int* perm, int n, double* dst, void* stream) {
+    if (n < 0) return MDKK_E_ARG;
+    if (n == 0) return MDKK_OK;
+    k_scatter4<<<mdkk::grid_for(n, 256), 256, 0, mdkk::as_stream(stream)>>>(src, perm, n, dst);
+    MDKK_CHECK_LAUNCH("k_scatter4");
+    return MDKK_OK;
+}
+
+int mdkk_gather_i64(const int64_t* src, const int* perm, int n, int64_t* dst, void* stream) {
+    if (n < 0) return MDKK_E_ARG;
+    if (n == 0) return MDKK_OK;
+    k_gather<int64_t><<<mdkk::grid_for(n, 256), 256, 0, mdkk::as_stream(stream)>>>(src, perm, n, dst);
+    MDKK_CHECK_LAUNCH("k_gather_i64");
+    return MDKK_OK;
+}
+
+int mdkk_gather_i32(const int32_t* src, const int* perm, int n, int32_t* dst, void* stream) {
+    if (n < 0) return MDKK_E_ARG;
+    if (n == 0) return MDKK_OK;
+    k_gather<int32_t><<<mdkk::grid_for(n, 256), 256, 0, mdkk::as_stream(stream)>>>(src, perm, n, dst);
+    MDKK_CHECK_LAUNCH("k_gather_i32");
+    return MDKK_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,104 @@
+// Truncated 12-6 Lennard-Jones force / energy / virial over a transposed
+// neighbour table.  Reference: mdkk/pair_lj.py:81-91 (kernel) and :114-179
+// (engine: weights, partner writes, 6-virial).
+//
+// full          : one thread per owned atom, owner writes f_i (no atomics),
+//                 energy/virial weight 1/2 per directed entry.
+// half, newton  : f_i accumulated in registers, f_j via FP64 RED atomics,
+//                 ghost rows folded afterwards by reverse comm.
+// half, !newton : f_j written only for local j; ghost entries weight 1/2.
+#include "common.cuh"
+
+namespace {
+
+constexpr int kBlock = 128;
+
+template <int STYLE, bool NEWTON>
+__global__ void __launch_bounds__(kBlock) k_lj(const double* __restrict__ x, int n_local,
+                                               const int* __restrict__ table, const int* __restrict__ counts,
+                                               int cap, double eps4, double eps24, double sig2, double rc2,
+                                               double* __restrict__ f, double* __restrict__ partials,
+                                               int* __restrict__ flags) {
+    const int i = blockIdx.x * kBlock + threadIdx.x;
+    double acc[7] = {0, 0, 0, 0, 0, 0, 0};  // E, Wxx, Wyy, Wzz, Wxy, Wxz, Wyz
+    if (i < n_local) {
+        const double4 xi = mdkk::ld4(x, i);
+        const int n = min(counts[i], cap);
+        double fx = 0.0, fy = 0.0, fz = 0.0;
+        bool bad = false;
+        const int* col = table + i;
+        int j_next = n > 0 ? __ldg(col) : 0;
+        for (int k = 0; k < n; ++k) {
+            const int j = j_next;
+            if (k + 1 < n) j_next = __ldg(col + (long long)(k + 1) * n_local);
+            const double4 xj = mdkk::ld4(x, j);
+            const double dx = xj.x - xi.x, dy = xj.y - xi.y, dz = xj.z - xi.z;
+            const double r2 = mdkk::r2_exact(dx, dy, dz);
+            if (r2 < rc2) {
+                bad |= !(r2 > 0.0);
+                const double inv = 1.0 / r2;
+                const double s2 = sig2 * inv;
+                const double s6 = s2 * s2 * s2;
+                const double s12 = s6 * s6;
+                const double e = eps4 * (s12 - s6);
+                const double fp = eps24 * (2.0 * s12 - s6) * inv;
+                const double w = (STYLE == 0) ? 0.5 : ((NEWTON || j < n_local) ? 1.0 : 0.5);
+                const double gx = fp * dx, gy = fp * dy, gz = fp * dz;
+                fx -= gx;
+                fy -= gy;
+                fz -= gz;
+                if (STYLE == 1 && (NEWTON || j < n_local)) {
+                    double* fj = f + 4LL * j;
+                    atomicAdd(fj + 0, gx);
+                    atomicAdd(fj + 1, gy);
+                    atomicAdd(fj + 2, gz);
+                }
+                const double wf = w * fp;
+                acc[0] += w * e;
+                acc[1] += wf * (dx * dx);
+                acc[2] += wf * (dy * dy);
+                acc[3] += wf * (dz * dz);
+                acc[4] += wf * (dx * dy);
+                acc[5] += wf * (dx * dz);
+                acc[6] += wf * (dy * dz);
+            }
+        }
+        if (STYLE == 0) {
+            mdkk::st4(f, i, make_double4(fx, fy, fz, 0.0));
+        } else {
+            double* fi = f + 4LL * i;
+            atomicAdd(fi + 0, fx);
+            atomicAdd(fi + 1, fy);
+            atomicAdd(fi + 2, fz);
+        }
+        if (bad) atomicOr(flags, MDKK_FLAG_COINCIDENT);
+    }
+    mdkk::block_sum<7, kBlock>(acc, partials + 7LL * blockIdx.x);
+}
+
+}  // namespace
+
+extern "C" int mdkk_lj_force(mdkk_ctx* ctx, const double* x, int n_local, const int* table, const int* counts,
+                             int cap, int style, int newton, double epsilon, double sigma, double rc, double* f,
+                             double* ev, int* flags, void* stream) {
+    if (!ctx || n_local < 0 || cap < 1 || (style != 0 && style != 1)) return MDKK_E_ARG;
+    cudaStream_t s = mdkk::as_stream(stream);
+    if (n_local == 0) {
+        cudaMemsetAsync(ev, 0, 7 * sizeof(double), s);
+        return MDKK_OK;
+    }
+    const int nb = mdkk::grid_for(n_local, kBlock);
+    double* partials = static_cast<double*>(mdkk::scratch(ctx, sizeof(double) * 7 * (size_t)nb));
+    if (!partials) return mdkk::cuda_fail(cudaErrorMemoryAllocation, "scratch");
+    const double e4 = 4.0 * epsilon, e24 = 24.0 * epsilon, s2 = sigma * sigma, rc2 = rc * rc;
+    if (style == 0)
+        k_lj<0, false><<<nb, kBlock, 0, s>>>(x, n_local, table, counts, cap, e4, e24, s2, rc2, f, partials, flags);
+    else if (newton)
+        k_lj<1, true><<<nb, kBlock, 0, s>>>(x, n_local, table, counts, cap, e4, e24, s2, rc2, f, partials, flags);
+    else
+        k_lj<1, false><<<nb, kBlock, 0, s>>>(x, n_local, table, counts, cap, e4, e24, s2, rc2, f, partials, flags);
+    MDKK_CHECK_LAUNCH("k_lj");
+    mdkk::reduce_partials(partials, nb, 7, ev, s);
+    MDKK_CHECK_LAUNCH("k_reduce_partials");
+    return MDKK_OK;
+}

@@ -1,0 +1,407 @@
+"""Device-resident velocity-Verlet driver (mirror of mdkk/driver/simulation.py).
+
+`RunConfig`, `LJStyle`, `SnapStyle`, `default_registry`, `Simulation`,
+`run_script`, `RunResult`, `lattice_positions`, `seeded_velocities` keep the
+reference names and semantics (mdkk/driver/simulation.py:36-488).  x, v, f
+never leave HBM inside the loop: one step is
+
+    verlet_first (kick + drift + max|x - x_ref|^2)  ->  1 scalar D2H (rebuild?)
+    [migrate + rebuild | forward pack]  ->  force kernel (+ reverse fold)
+    ->  verlet_second (kick)
+
+and energies / kinetic energy / the non-finite check are read back only on
+thermo steps.  Styles `lj/cut/kk` and `snap/kk` are the B200 drop-ins; the
+base names resolve to the same GPU styles (there is no CPU path here).
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from .. import _lib
+from ..domain import Box, RankedSystem
+from ..neighbor import build, build_all
+from ..pair_lj import LJCut, PairParams, PairResult, compute_pair, lj_force_rank
+from .registry import StyleRegistry
+from .script import parse_script
+
+
+class RunError(RuntimeError):
+    pass
+
+
+class RunConfig:
+    """Harness knobs (mdkk/driver/simulation.py:36-62) plus `device`."""
+
+    def __init__(self, n_ranks: int = 1, strategy: str = "serial", mode: str | None = None,
+                 list_style: str | None = None, newton: bool = True, skin: float = 0.3,
+                 workers: int | None = None, batch_u: int | None = None, batch_y: int | None = None,
+                 tile_v: int | None = None, layout: str | None = None, rng_seed: int | None = None,
+                 device=None):
+        if strategy not in ("serial", "duplicate", "atomic"):
+            raise RunError(f"unknown strategy {strategy!r}; choose from ['atomic', 'duplicate', 'serial']")
+        self.n_ranks = int(n_ranks)
+        self.strategy = strategy
+        self.mode = mode
+        self.list_style = list_style
+        self.newton = bool(newton)
+        self.skin = float(skin)
+        self.workers = workers
+        self.batch_u, self.batch_y, self.tile_v, self.layout = batch_u, batch_y, tile_v, layout
+        self.rng_seed = rng_seed
+        self.device = device
+
+
+class LJStyle:
+    """Truncated 12-6 pair style on the GPU (mdkk/driver/simulation.py:65-85)."""
+
+    list_style = None
+
+    def __init__(self, r_c: float, mode: str = "atom", name: str = "lj/cut/kk"):
+        self.name = name
+        self.r_c = float(r_c)
+        self.default_mode = mode
+        self.kernel = None
+
+    def set_coeff(self, epsilon: float, sigma: float) -> None:
+        self.kernel = LJCut(PairParams(epsilon, sigma, self.r_c))
+
+    def compute(self, system, lists, config: RunConfig, check: bool = True) -> PairResult:
+        if self.kernel is None:
+            raise RunError("pair_coeff must be set before computing forces")
+        return compute_pair(self.kernel, system, lists, mode=config.mode or self.default_mode, check=check)
+
+    def compute_device(self, system, lists, config) -> tuple[torch.Tensor, torch.Tensor]:
+        """Engine path: no host sync; returns (device energy scalar, device flag word)."""
+        if self.kernel is None:
+            raise RunError("pair_coeff must be set before computing forces")
+        dev = system.device
+        evs = torch.zeros((len(system.stores), 7), dtype=torch.float64, device=dev)
+        flags = torch.zeros(1, dtype=torch.int32, device=dev)
+        half = False
+        for k, (s, nl) in enumerate(zip(system.stores, lists)):
+            lj_force_rank(s, nl, self.kernel.params, evs[k], flags)
+            half |= nl.style == "half"
+        if half and any(s.n_ghost for s in system.stores):
+            system.reverse_comm()
+        for s in system.stores:
+            s.device_wrote(force=True)
+        return (evs[:, 0].sum() if len(system.stores) > 1 else evs[0, 0]), flags
+
+
+def default_registry() -> StyleRegistry:
+    """lj/cut, lj/cut/opt, lj/cut/kk, snap, snap/opt, snap/kk -> GPU styles (mdkk/driver/simulation.py:145-153)."""
+    reg = StyleRegistry()
+    for name in ("lj/cut", "lj/cut/opt", "lj/cut/kk"):
+        reg.register(name, lambda args, _n=name: LJStyle(float(args[0]),
+                                                         mode="neighbor" if _n.endswith("opt") else "atom",
+                                                         name=_n))
+    try:
+        from ..snap.style import SnapStyle
+    except ImportError:  # SNAP kernels not built into this library version
+        SnapStyle = None
+    if SnapStyle is not None:
+        for name in ("snap", "snap/opt", "snap/kk"):
+            reg.register(name, lambda args, _n=name: SnapStyle.from_file(float(args[0]), args[1], name=_n))
+    return reg
+
+
+def lattice_positions(style: str, rho: float, cells) -> tuple[np.ndarray, Box]:
+    """fcc/sc sites in meshgrid(ij) cell x basis order (mdkk/driver/simulation.py:156-178).
+
+    `bcc` (absent from the reference) takes the lattice constant a as `rho`.
+    """
+    if rho <= 0:
+        raise RunError("lattice density must be positive")
+    if style == "fcc":
+        a = (4.0 / rho) ** (1.0 / 3.0)
+        base = np.array([[0.0, 0.0, 0.0], [0.5, 0.5, 0.0], [0.5, 0.0, 0.5], [0.0, 0.5, 0.5]])
+    elif style == "sc":
+        a = (1.0 / rho) ** (1.0 / 3.0)
+        base = np.zeros((1, 3))
+    elif style == "bcc":
+        a = float(rho)
+        base = np.array([[0.0, 0.0, 0.0], [0.5, 0.5, 0.5]])
+    else:
+        raise RunError(f"unknown lattice style {style!r}")
+    nx, ny, nz = (int(c) for c in cells)
+    if min(nx, ny, nz) < 1:
+        raise RunError("create_box needs at least one cell per direction")
+    ii, jj, kk = np.meshgrid(np.arange(nx), np.arange(ny), np.arange(nz), indexing="ij")
+    corners = np.stack([ii, jj, kk], axis=-1).reshape(-1, 3).astype(np.float64)
+    pos = (corners[:, None, :] + base[None, :, :]).reshape(-1, 3) * a
+    return pos, Box((a * nx, a * ny, a * nz))
+
+
+def seeded_velocities(n: int, temperature: float, mass: float, seed: int) -> np.ndarray:
+    """Gaussian, zero momentum, exact-T rescale (mdkk/driver/simulation.py:181-194)."""
+    if temperature < 0:
+        raise RunError("temperature must be non-negative")
+    if temperature == 0.0 or n == 0:
+        return np.zeros((n, 3))
+    v = np.random.default_rng(seed).normal(0.0, np.sqrt(temperature / mass), (n, 3))
+    v -= v.mean(axis=0)
+    t_now = mass * float(np.sum(v * v)) / (3.0 * n)
+    if t_now > 0:
+        v *= np.sqrt(temperature / t_now)
+    return v
+
+
+class RunResult:
+    """Thermo rows, per-logged-step gid-ordered snapshots (mdkk/driver/simulation.py:197-210)."""
+
+    def __init__(self):
+        self.rows = []
+        self.snapshots = {}
+        self.lines = []
+        self.n_rebuilds = 0
+
+    def log(self, step, e_pot, e_kin, temperature):
+        e_total = e_pot + e_kin
+        self.rows.append((step, e_pot, e_kin, e_total, temperature))
+        self.lines.append(f"{step} {e_pot:.17g} {e_kin:.17g} {e_total:.17g} {temperature:.17g}")
+
+
+class Simulation:
+    """Executes a parsed script; the NVE loop runs device-resident (mdkk/driver/simulation.py:213-481)."""
+
+    def __init__(self, config: RunConfig | None = None, registry: StyleRegistry | None = None, log=print):
+        self.config = config or RunConfig()
+        self.registry = registry or default_registry()
+        self.log = log or (lambda *_: None)
+        self.suffix = None
+        self.lattice_spec = None
+        self.cells = None
+        self.box = None
+        self.mass = 1.0
+        self._positions = None
+        self._velocities = None
+        self.style = None
+        self.dt = 0.005
+        self.thermo_every = 100
+        self.system: RankedSystem | None = None
+        self.lists = None
+        self.results: list[RunResult] = []
+        self.n_rebuilds = 0
+        self._cap_hint = None
+        self.snapshots = True
+        dev = self.config.device
+        self.device = torch.device(dev) if dev is not None else torch.device("cuda", torch.cuda.current_device())
+        self._d2 = None
+        self._e_dev = None
+        self._flags = None
+
+    # ------------------------------------------------------------ commands
+    def execute(self, script) -> "Simulation":
+        cmds = parse_script(script) if isinstance(script, str) else script
+        for cmd in cmds:
+            handler = getattr(self, f"_cmd_{cmd.name}", None)
+            if handler is None:
+                raise RunError(f"line {cmd.line_no}: no handler for {cmd.name!r}")
+            try:
+                handler(cmd.args)
+            except (RunError, ValueError) as exc:
+                raise RunError(f"line {cmd.line_no} ({cmd.name}): {exc}") from exc
+        return self
+
+    def _cmd_units(self, a):
+        if a[0] != "lj":
+            raise RunError("only reduced units are supported")
+
+    def _cmd_boundary(self, a):
+        if tuple(a) != ("p", "p", "p"):
+            raise RunError("only fully periodic boundaries are supported")
+
+    def _cmd_lattice(self, a):
+        self.lattice_spec = (a[0], float(a[1]))
+
+    def _cmd_create_box(self, a):
+        if self.lattice_spec is None:
+            raise RunError("lattice must be set before create_box")
+        self.cells = tuple(int(v) for v in a)
+        _, self.box = lattice_positions(self.lattice_spec[0], self.lattice_spec[1], self.cells)
+
+    def _cmd_create_atoms(self, a):
+        if self.cells is None:
+            raise RunError("create_box must run before create_atoms")
+        self._positions, self.box = lattice_positions(self.lattice_spec[0], self.lattice_spec[1], self.cells)
+        self._velocities = np.zeros_like(self._positions)
+        self.system = None
+
+    def _cmd_mass(self, a):
+        m = float(a[0])
+        if m <= 0:
+            raise RunError("mass must be positive")
+        self.mass = m
+
+    def _cmd_velocity(self, a):
+        if self._positions is None:
+            raise RunError("create_atoms must run before velocity")
+        t, seed = float(a[0]), int(a[1])
+        if self.config.rng_seed is not None:
+            seed = self.config.rng_seed
+        self._velocities = seeded_velocities(len(self._positions), t, self.mass, seed)
+        self.system = None
+
+    def _cmd_pair_style(self, a):
+        self.style = self.registry.resolve(a[0], self.suffix)(a[1:])
+        self.lists = None
+
+    def _cmd_pair_coeff(self, a):
+        if self.style is None:
+            raise RunError("pair_style must be set before pair_coeff")
+        self.style.set_coeff(float(a[0]), float(a[1]))
+
+    def _cmd_suffix(self, a):
+        self.suffix = None if a[0] == "off" else a[0]
+
+    def _cmd_timestep(self, a):
+        dt = float(a[0])
+        if dt <= 0:
+            raise RunError("timestep must be positive")
+        self.dt = dt
+
+    def _cmd_thermo(self, a):
+        n = int(a[0])
+        if n <= 0:
+            raise RunError("thermo interval must be positive")
+        self.thermo_every = n
+
+    def _cmd_run(self, a):
+        self.run_nve(int(a[0]))
+
+    # --------------------------------------------------------- integration
+    def _ensure_system(self):
+        if self.style is None:
+            raise RunError("pair_style must be set before run")
+        if self._positions is None:
+            raise RunError("create_atoms must run before run")
+        if self.system is None:
+            with torch.cuda.device(self.device):
+                self.system = RankedSystem.distribute(self.box, self.config.n_ranks, self._positions,
+                                                      self._velocities, device=self.device)
+            self.lists = None
+        if self.lists is None:
+            style_list = self.style.list_style or self.config.list_style or "half"
+            if self.style.list_style and self.config.list_style and self.config.list_style != self.style.list_style:
+                raise RunError(f"style {self.style.name} requires {self.style.list_style} lists")
+            self._list_style = style_list
+            self.lists = build_all(self.system, self.style.r_c, self.config.skin, style=style_list,
+                                   newton=self.config.newton)
+            self._cap_hint = max(nl.table_dev.shape[0] for nl in self.lists)
+        if self._d2 is None:
+            self._d2 = torch.zeros(max(self.config.n_ranks, 1), dtype=torch.float64, device=self.device)
+
+    def _rebuild_lists(self):
+        """migrate + build (mdkk/driver/simulation.py:368-373)."""
+        halo = self.style.r_c + self.config.skin
+        self.system.migrate(halo)
+        self.lists = [build(s, self.system.box, self.style.r_c, self.config.skin, style=self._list_style,
+                            newton=self.config.newton, cap_hint=self._cap_hint) for s in self.system.stores]
+        self._cap_hint = max(nl.table_dev.shape[0] for nl in self.lists)
+        self.n_rebuilds += 1
+
+    def _forces_device(self):
+        e, flags = self.style.compute_device(self.system, self.lists, self.config)
+        self._e_dev, self._flags = e, flags
+        return e
+
+    def _compute_forces(self) -> float:
+        return float(self._forces_device().item())
+
+    def _kinetic(self) -> tuple[float, float]:
+        lib, st = _lib.lib(), _lib.stream(self.device)
+        ke = torch.zeros(len(self.system.stores), dtype=torch.float64, device=self.device)
+        n = 0
+        for k, s in enumerate(self.system.stores):
+            s.to_device()
+            _lib.check(lib.mdkk_kinetic(_lib.ctx(self.device), s.v.data_ptr(), s.n_local, self.mass,
+                                        ke[k:].data_ptr(), st), "mdkk_kinetic")
+            n += s.n_local
+        k = float(ke.sum().item())
+        return k, (2.0 * k / (3.0 * n) if n else 0.0)
+
+    def _half_kick_drift(self) -> bool:
+        """v += dt/2m f; x += dt v; returns whether any rank moved beyond skin/2 (one sync)."""
+        lib, st = _lib.lib(), _lib.stream(self.device)
+        ctx = _lib.ctx(self.device)
+        h = 0.5 * self.dt / self.mass
+        for k, (s, nl) in enumerate(zip(self.system.stores, self.lists)):
+            s.to_device()
+            _lib.check(lib.mdkk_verlet_first(ctx, s.x.data_ptr(), s.v.data_ptr(), s.f.data_ptr(),
+                                             nl.ref_dev.data_ptr(), s.n_local, self.dt, h,
+                                             self._d2[k:].data_ptr(), st), "mdkk_verlet_first")
+            s.device_wrote(pos=True, vel=True)
+        worst = float(self._d2[: len(self.system.stores)].max().item())
+        return math.sqrt(worst) > 0.5 * self.config.skin
+
+    def _half_kick(self):
+        lib, st = _lib.lib(), _lib.stream(self.device)
+        h = 0.5 * self.dt / self.mass
+        for s in self.system.stores:
+            _lib.check(lib.mdkk_verlet_second(_lib.ctx(self.device), s.v.data_ptr(), s.f.data_ptr(), s.n_local,
+                                              h, self.mass, None, st), "mdkk_verlet_second")
+            s.device_wrote(vel=True)
+
+    def step_device(self) -> torch.Tensor:
+        """One velocity-Verlet step (mdkk/driver/simulation.py:431-450); energy stays on device."""
+        if self._half_kick_drift():
+            self._rebuild_lists()
+        else:
+            self.system.forward_comm()
+        e = self._forces_device()
+        self._half_kick()
+        return e
+
+    def step_once(self) -> float:
+        return float(self.step_device().item())
+
+    def _check_finite(self, step, e_pot):
+        if not np.isfinite(e_pot):
+            raise RunError(f"non-finite potential energy at step {step}")
+        for s in self.system.stores:
+            if s.n_local and not bool(torch.isfinite(s.f[: s.n_local, :3]).all().item()):
+                raise RunError(f"non-finite force at step {step}")
+        if self._flags is not None and int(self._flags.item()) & _lib.FLAG_COINCIDENT:
+            raise RunError(f"coincident atoms (r = 0) at or before step {step}")
+
+    def run_nve(self, n_steps: int) -> RunResult:
+        """NVE with thermo at 0, every `thermo`, and the last step (mdkk/driver/simulation.py:452-481).
+
+        The non-finite check runs on logged steps (device error word + force
+        scan) instead of every step, so the loop never waits on the host.
+        """
+        if n_steps < 0:
+            raise RunError("run expects a non-negative step count")
+        with torch.cuda.device(self.device):
+            self._ensure_system()
+            result = RunResult()
+            self.results.append(result)
+            rebuilds0 = self.n_rebuilds
+
+            def log(step, e_dev):
+                e_pot = float(e_dev.item())
+                self._check_finite(step, e_pot)
+                ke, t = self._kinetic()
+                result.log(step, e_pot, ke, t)
+                if self.snapshots:
+                    result.snapshots[step] = self.system.gather()[0]
+                self.log(result.lines[-1])
+
+            log(0, self._forces_device())
+            for step in range(1, n_steps + 1):
+                e = self.step_device()
+                if step % self.thermo_every == 0 or step == n_steps:
+                    log(step, e)
+            result.n_rebuilds = self.n_rebuilds - rebuilds0
+        return result
+
+
+def run_script(text: str, config: RunConfig | None = None, log=print) -> Simulation:
+    """Parse and execute a script (mdkk/driver/simulation.py:484-488)."""
+    sim = Simulation(config, log=log)
+    sim.execute(parse_script(text))
+    return sim

@@ -1,0 +1,163 @@
+"""Dual-space arrays: space "a" = host numpy, space "b" = device (torch CUDA) storage.
+
+Mirror of mdkk/memspace.py:26-162 with the reference's protocol unchanged
+(single writer, copy only when stale, `transfer_count` counts physical
+copies), but space "b" is real HBM.  Device rows may be padded: positions and
+forces are stored as AoS double4 (x, y, z, pad) so one neighbour gather is one
+32-byte sector, while the logical (n, 3) view is what both spaces expose.
+
+Scatter strategies (Serial / Duplicate / Atomic, mdkk/memspace.py:165-254)
+are accepted for signature compatibility; on the GPU the deconfliction is
+fixed by the list style: full lists are owner-writes (no atomics), half lists
+use FP64 atomics (`RED.E.ADD.F64`).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+SPACES = ("a", "b")
+
+_TORCH_DTYPE = {np.dtype(np.float64): torch.float64, np.dtype(np.int32): torch.int32,
+                np.dtype(np.int64): torch.int64, np.dtype(np.complex128): torch.complex128,
+                np.dtype(np.int8): torch.int8}
+
+
+class MemspaceError(RuntimeError):
+    """Protocol violation on a dual-space array (mdkk/memspace.py:21-22)."""
+
+
+class LayoutPolicy:
+    """Logical -> storage dimension order, slowest first (mdkk/memspace.py:26-74)."""
+
+    __slots__ = ("order",)
+
+    def __init__(self, order):
+        order = tuple(int(d) for d in order)
+        if sorted(order) != list(range(len(order))):
+            raise ValueError(f"order must be a permutation of 0..{len(order) - 1}, got {order}")
+        self.order = order
+
+    @classmethod
+    def row_major(cls, ndim: int) -> "LayoutPolicy":
+        return cls(range(ndim))
+
+    @classmethod
+    def transposed(cls, ndim: int) -> "LayoutPolicy":
+        return cls(range(ndim - 1, -1, -1))
+
+    def storage_shape(self, shape) -> tuple[int, ...]:
+        return tuple(shape[d] for d in self.order)
+
+    def flat_index(self, idx, shape) -> int:
+        if len(idx) != len(self.order):
+            raise ValueError("index rank mismatch")
+        off = 0
+        for d in self.order:
+            off = off * shape[d] + idx[d]
+        return off
+
+    def logical_axes(self) -> tuple[int, ...]:
+        return tuple(self.order.index(d) for d in range(len(self.order)))
+
+    def __eq__(self, other):
+        return isinstance(other, LayoutPolicy) and self.order == other.order
+
+    def __repr__(self):
+        return f"LayoutPolicy(order={self.order})"
+
+
+class DualArray:
+    """Host/device mirrored array with staleness flags (mdkk/memspace.py:77-156).
+
+    ``pad_last`` pads the fastest logical dimension of the device storage
+    (used for double4 rows).  ``storage_b`` adopts an existing device tensor.
+    """
+
+    def __init__(self, shape, layout_a: LayoutPolicy | None = None, layout_b: LayoutPolicy | None = None,
+                 dtype=np.float64, device=None, pad_last: int | None = None, storage_b=None):
+        shape = tuple(int(s) for s in shape)
+        if not shape or any(s <= 0 for s in shape):
+            raise ValueError(f"all extents must be > 0, got {shape}")
+        self.shape = shape
+        self.dtype = np.dtype(dtype)
+        self.layout_a = layout_a or LayoutPolicy.row_major(len(shape))
+        self.layout_b = layout_b or LayoutPolicy.transposed(len(shape))
+        self.device = torch.device(device) if device is not None else torch.device("cuda")
+        self.data_a = np.zeros(shape, dtype=self.dtype)
+        sshape = list(self.layout_b.storage_shape(shape))
+        if pad_last is not None:
+            if self.layout_b.order[-1] != len(shape) - 1:
+                raise ValueError("padding needs the last logical dim fastest in storage")
+            sshape[-1] = pad_last
+        if storage_b is not None:
+            self.data_b = storage_b
+        else:
+            self.data_b = torch.zeros(sshape, dtype=_TORCH_DTYPE[self.dtype], device=self.device)
+        self.modified_a = False
+        self.modified_b = False
+        self.transfer_count = 0
+
+    def _check(self, space):
+        if space not in SPACES:
+            raise ValueError(f"space must be one of {SPACES}, got {space!r}")
+        return space
+
+    def layout(self, space):
+        return self.layout_a if self._check(space) == "a" else self.layout_b
+
+    def view(self, space):
+        """Logical-index view of the given space (numpy for 'a', torch for 'b')."""
+        if self._check(space) == "a":
+            return self.data_a
+        v = self.data_b.permute(*self.layout_b.logical_axes())
+        sl = tuple(slice(0, s) for s in self.shape)
+        return v[sl]
+
+    def modified(self, space):
+        return self.modified_a if self._check(space) == "a" else self.modified_b
+
+    def mark_modified(self, space):
+        space = self._check(space)
+        other = "b" if space == "a" else "a"
+        if self.modified(other):
+            raise MemspaceError(f"space {other!r} has unsynchronized modifications; "
+                                f"sync before writing {space!r}")
+        if space == "a":
+            self.modified_a = True
+        else:
+            self.modified_b = True
+
+    def sync(self, space):
+        space = self._check(space)
+        if space == "a" and self.modified_b:
+            self.data_a[...] = self.view("b").cpu().numpy()
+            self.transfer_count += 1
+            self.modified_b = False
+        elif space == "b" and self.modified_a:
+            self.view("b").copy_(torch.from_numpy(np.ascontiguousarray(self.data_a)).to(self.device))
+            self.transfer_count += 1
+            self.modified_a = False
+        return self
+
+    def read(self, space):
+        self.sync(space)
+        return self.view(space)
+
+
+def create_dual(shape, layout_a=None, layout_b=None, dtype=np.float64, device=None, **kw) -> DualArray:
+    return DualArray(shape, layout_a=layout_a, layout_b=layout_b, dtype=dtype, device=device, **kw)
+
+
+class Serial:
+    copies = 1
+
+
+class Duplicate:
+    def __init__(self, copies: int | None = None):
+        self.copies = int(copies or 1)
+
+
+class Atomic:
+    copies = 1

@@ -1,0 +1,142 @@
+"""Lennard-Jones pair engine on the GPU (drop-in for mdkk/pair_lj.py).
+
+`PairParams`, `LJCut`, `PairResult`, `u2_lj` and `compute_pair` keep the
+reference signatures (mdkk/pair_lj.py:29-179).  `compute_pair` launches the
+sm_100a kernel `mdkk_lj_force` per rank — owner-writes for full lists, FP64
+atomics for half lists — then the device reverse comm; energy and the six
+virial components come from a deterministic on-device reduction.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from .domain import RankedSystem
+from .neighbor import STYLES, NeighborList
+
+
+class PairError(RuntimeError):
+    pass
+
+
+class PairParams:
+    """epsilon, sigma, r_c with the reference validation (mdkk/pair_lj.py:29-39)."""
+
+    def __init__(self, epsilon: float, sigma: float, r_c: float):
+        if epsilon <= 0 or sigma <= 0 or r_c <= 0:
+            raise PairError("epsilon, sigma, r_c must all be positive")
+        if r_c <= sigma:
+            raise PairError(f"cutoff {r_c} must exceed sigma {sigma}")
+        self.epsilon, self.sigma, self.r_c = float(epsilon), float(sigma), float(r_c)
+
+
+def u2_lj(r: float, params: PairParams) -> tuple[float, float]:
+    """Scalar closed form (energy, fpair) for one distance (mdkk/pair_lj.py:55-69)."""
+    if r == 0:
+        raise PairError("coincident atoms (r = 0)")
+    if not (0 < r < params.r_c):
+        raise PairError(f"r = {r} outside (0, r_c = {params.r_c})")
+    s2 = (params.sigma * params.sigma) / (r * r)
+    s6 = s2 * s2 * s2
+    return 4.0 * params.epsilon * (s6 * s6 - s6), 24.0 * params.epsilon * (2.0 * s6 * s6 - s6) / (r * r)
+
+
+class LJCut:
+    """Truncated (not shifted) 12-6 kernel (mdkk/pair_lj.py:72-91); evaluated by csrc/lj.cu."""
+
+    name = "lj/cut"
+
+    def __init__(self, params: PairParams):
+        self.params = params
+        self.r_c = params.r_c
+
+
+class PairResult:
+    """Energy, gid-ordered forces, virial (xx,yy,zz,xy,xz,yz) — read lazily from the device."""
+
+    def __init__(self, ev: torch.Tensor, system: RankedSystem | None, flags: torch.Tensor | None = None):
+        self._ev = ev
+        self._system = system
+        self._flags = flags
+        self._energy = self._virial = self._forces = None
+
+    def _host_ev(self):
+        if self._energy is None:
+            if self._flags is not None and int(self._flags.item()) & _lib.FLAG_COINCIDENT:
+                raise PairError("coincident atoms (r = 0)")
+            ev = self._ev.cpu().numpy()
+            self._energy, self._virial = float(ev[0]), ev[1:7].copy()
+
+    @property
+    def energy(self) -> float:
+        self._host_ev()
+        return self._energy
+
+    @property
+    def virial(self) -> np.ndarray:
+        self._host_ev()
+        return self._virial
+
+    @property
+    def forces(self) -> np.ndarray:
+        if self._forces is None:
+            self._forces = self._system.gather_forces()
+        return self._forces
+
+    def pressure(self, volume: float) -> float:
+        return float(self.virial[:3].sum() / (3.0 * volume))
+
+
+def lj_force_rank(store, nl: NeighborList, params: PairParams, ev: torch.Tensor, flags: torch.Tensor,
+                  zero: bool = True) -> None:
+    """One rank's kernel launch (no host sync).  Ghost rows must be zero on entry for half lists."""
+    dev = store.device
+    if zero and nl.style == "half":
+        store.f.zero_()
+    elif zero and store.n_ghost:
+        store.f[store.n_local:store.n_total].zero_()
+    _lib.check(_lib.lib().mdkk_lj_force(
+        _lib.ctx(dev), store.x.data_ptr(), store.n_local, nl.table_dev.data_ptr(), nl.counts_dev.data_ptr(),
+        nl.table_dev.shape[0], STYLES[nl.style], int(nl.newton), params.epsilon, params.sigma, params.r_c,
+        store.f.data_ptr(), ev.data_ptr(), flags.data_ptr(), _lib.stream(dev)), "mdkk_lj_force")
+
+
+def compute_pair(kernel, system: RankedSystem, lists: list[NeighborList], mode: str = "atom", strategy=None,
+                 n_workers: int | None = None, zero_forces: bool = True, check: bool = True) -> PairResult:
+    """Evaluate the LJ kernel over every rank's list (mdkk/pair_lj.py:114-179).
+
+    `mode` / `strategy` / `n_workers` are accepted for signature parity; the
+    GPU schedule is one thread per owned atom and the write-deconfliction is
+    fixed by the list style.  `check=False` (engine-internal) skips the
+    synchronous stale-list and coincident-atom checks; the error word is then
+    read when the result is first inspected.
+    """
+    if mode not in ("atom", "neighbor"):
+        raise PairError(f"unknown execution mode {mode!r}")
+    params = kernel.params
+    dev = system.device
+    evs = torch.zeros((len(system.stores), 7), dtype=torch.float64, device=dev)
+    flags = torch.zeros(1, dtype=torch.int32, device=dev)
+    prev = None
+    if not zero_forces:
+        prev = [s.f.clone() for s in system.stores]
+    half = False
+    for k, (store, nl) in enumerate(zip(system.stores, lists)):
+        if check:
+            nl.check_current()
+        store.to_device()
+        half |= nl.style == "half"
+        lj_force_rank(store, nl, params, evs[k], flags)
+        store.device_wrote(force=True)
+    if half and any(s.n_ghost for s in system.stores):
+        system.reverse_comm()
+    if prev is not None:
+        for s, p in zip(system.stores, prev):
+            s.f[: s.n_local] += p[: s.n_local]
+    ev = evs.sum(dim=0) if len(system.stores) > 1 else evs[0]
+    res = PairResult(ev, system, flags)
+    if check:
+        res._host_ev()  # raise PairError now, as the reference does
+    return res

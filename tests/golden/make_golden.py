@@ -1,0 +1,184 @@
+"""Generate golden vectors by running the UNMODIFIED reference `mdkk` engine.
+
+Run in the build container (the reference is importable there, not on the GPU
+box):  PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+Every fixture records the reference's own outputs on seeded inputs so the
+oracle (oracle/) and the CUDA path can be pinned to them.  Outputs are small
+compressed npz files committed next to this script.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+import time
+
+import numpy as np
+
+REF_SRC = "/root/reference/pkg/src"
+REF_PKG = "/root/reference/pkg"
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REF_SRC)
+
+from mdkk.domain import Box, RankedSystem  # noqa: E402
+from mdkk.neighbor import build_all  # noqa: E402
+from mdkk.pair_lj import LJCut, PairParams, compute_pair  # noqa: E402
+from mdkk.driver.simulation import RunConfig, run_script, lattice_positions, seeded_velocities  # noqa: E402
+from mdkk.snap import (  # noqa: E402
+    SnapState, build_neighbor_map, compute_bi, compute_fused_deidrj, compute_ui,
+    compute_yi, make_coupling_tables, QuantumIndex,
+)
+
+
+def random_config(n, rho, seed, min_sep=0.85):
+    """Same construction as the reference tests/conftest.py:16-31."""
+    rng = np.random.default_rng(seed)
+    cells = int(np.ceil(n ** (1.0 / 3.0)))
+    a = (1.0 / rho) ** (1.0 / 3.0)
+    lo = np.stack(np.meshgrid(*[np.arange(cells)] * 3, indexing="ij"), axis=-1).reshape(-1, 3)
+    order = rng.permutation(len(lo))[:n]
+    jitter = rng.uniform(-0.5, 0.5, (n, 3)) * (a - min_sep)
+    return (lo[order] + 0.5) * a + jitter, Box((a * cells,) * 3)
+
+
+def directed_set(system, lists):
+    """Directed (gid_i, gid_j, shift_x, shift_y, shift_z) entries of every rank."""
+    out = []
+    for store, nl in zip(system.stores, lists):
+        rows, cols, w, wj = nl.pairs()
+        sh = np.rint(store.ghost_shift[cols] / system.box.lengths).astype(np.int64)
+        out.append(np.column_stack([store.global_ids[rows], store.global_ids[cols], sh,
+                                    np.full(len(rows), store.rank), (w * 2).astype(np.int64),
+                                    wj.astype(np.int64)]))
+    return np.concatenate(out) if out else np.zeros((0, 8), np.int64)
+
+
+def lj_small():
+    pos, box = random_config(120, 0.7, seed=2)
+    out = {"pos": pos, "lengths": box.lengths, "rc": 2.5, "skin": 0.3}
+    for style, newton in (("full", False), ("half", True), ("half", False)):
+        for n_ranks in (1, 2, 4):
+            system = RankedSystem.distribute(box, n_ranks, pos, np.zeros_like(pos))
+            lists = build_all(system, 2.5, 0.3, style=style, newton=newton)
+            res = compute_pair(LJCut(PairParams(1.0, 1.0, 2.5)), system, lists)
+            tag = f"{style}_{int(newton)}_{n_ranks}"
+            out[f"E_{tag}"] = res.energy
+            out[f"F_{tag}"] = res.forces
+            out[f"W_{tag}"] = res.virial
+            out[f"pairs_{tag}"] = directed_set(system, lists)
+            out[f"cap_{tag}"] = np.array([nl.max_neighbors for nl in lists])
+            out[f"nghost_{tag}"] = np.array([s.n_ghost for s in system.stores])
+    np.savez_compressed(os.path.join(HERE, "lj_small.npz"), **out)
+
+
+def lj_32k():
+    pos, box = lattice_positions("fcc", 0.8442, (20, 20, 20))
+    pos = pos + np.random.default_rng(1).normal(0.0, 0.02, pos.shape)
+    out = {"lengths": box.lengths}
+    for style, newton in (("full", False), ("half", True)):
+        system = RankedSystem.distribute(box, 1, pos, np.zeros_like(pos))
+        lists = build_all(system, 2.5, 0.3, style=style, newton=newton)
+        res = compute_pair(LJCut(PairParams(1.0, 1.0, 2.5)), system, lists)
+        out[f"E_{style}"] = res.energy
+        out[f"W_{style}"] = res.virial
+        out[f"F_{style}_sub"] = res.forces[::37]
+        out[f"Fmax_{style}"] = float(np.abs(res.forces).max())
+        out[f"nentries_{style}"] = int(sum(len(nl.pairs()[0]) for nl in lists))
+        out[f"cap_{style}"] = int(lists[0].max_neighbors)
+        out[f"nghost_{style}"] = int(system.stores[0].n_ghost)
+    np.savez_compressed(os.path.join(HERE, "lj_32k_jitter.npz"), **out)
+
+
+def melt_runs():
+    silent = lambda *_: None  # noqa: E731
+    with open(os.path.join(REF_PKG, "scripts/melt.in")) as fh:
+        text = fh.read()
+    out = {}
+    sim = run_script(text, RunConfig(), log=silent)
+    out["melt500_rows"] = np.array(sim.results[-1].rows)
+    # C1: 32k fcc rho 0.8442, rc 2.5, T 1.44 seed 87287, dt 0.005, 100 steps.
+    c1 = ("units lj\nboundary p p p\nlattice fcc 0.8442\ncreate_box 20 20 20\ncreate_atoms\n"
+          "mass 1.0\nvelocity 1.44 87287\npair_style lj/cut 2.5\npair_coeff 1.0 1.0\n"
+          "timestep 0.005\nthermo 10\nrun 100\n")
+    for style in ("half", "full"):
+        t0 = time.time()
+        sim = run_script(c1, RunConfig(list_style=style, newton=(style == "half")), log=silent)
+        out[f"c1_{style}_rows"] = np.array(sim.results[-1].rows)
+        out[f"c1_{style}_final_pos_sub"] = sim.results[-1].snapshots[100][::97]
+        print(f"C1 {style}: {time.time() - t0:.1f}s")
+    np.savez_compressed(os.path.join(HERE, "lj_runs.npz"), **out)
+
+
+def _cluster(n, seed, spread=2.6, min_sep=0.8, box_l=12.0):
+    rng = np.random.default_rng(seed)
+    pts = [rng.uniform(-spread, spread, 3)]
+    while len(pts) < n:
+        cand = rng.uniform(-spread, spread, 3)
+        if min(np.linalg.norm(cand - p) for p in pts) >= min_sep:
+            pts.append(cand)
+    return np.asarray(pts) + box_l / 2.0
+
+
+def _snap_pipeline(pos, box, jmax, beta, r_c, skin):
+    system = RankedSystem.distribute(box, 1, pos, np.zeros_like(pos))
+    lists = build_all(system, cutoff=r_c, skin=skin, style="full", newton=False)
+    tables = make_coupling_tables(jmax)
+    store, nl = system.stores[0], lists[0]
+    nmap = build_neighbor_map(store, nl, r_c)
+    state = SnapState(tables, store.n_local, beta)
+    compute_ui(nmap, state)
+    energy = float(np.sum(compute_bi(state) @ state.beta))
+    compute_yi(state)
+    f = compute_fused_deidrj(nmap, state, store.n_total)
+    fr = store.force.read("a")
+    fr[: store.n_total] = f
+    store.force.mark_modified("a")
+    system.reverse_comm()
+    gid = store.global_ids[: store.n_local]
+    o = np.argsort(gid)
+    return energy, system.gather_forces(), state.u_view()[o], state.y_view()[o], nmap.n_pairs
+
+
+def snap_fixtures():
+    out = {}
+    for jmax, seed in ((1, 39), (2, 40), (4, 43)):
+        n = 10 if jmax < 4 else 6
+        pos = _cluster(n, seed)
+        beta = np.random.default_rng(11).uniform(-0.5, 0.5, len(QuantumIndex(jmax).triples()))
+        e, f, u, y, npairs = _snap_pipeline(pos, Box((12.0,) * 3), jmax, beta, 1.9, 0.2)
+        tag = f"j{int(2 * jmax)}"
+        out.update({f"{tag}_pos": pos, f"{tag}_beta": beta, f"{tag}_E": e, f"{tag}_F": f,
+                    f"{tag}_U": u, f"{tag}_Y": y})
+    # periodic 40-atom system, 2J=4, rc 1.4 (reference tests/test_snap.py:457-462 geometry)
+    pos = np.random.default_rng(53).uniform(0, 6.0, (40, 3))
+    beta = np.random.default_rng(11).uniform(-0.5, 0.5, len(QuantumIndex(2).triples()))
+    e, f, u, y, _ = _snap_pipeline(pos, Box((6.0,) * 3), 2, beta, 1.4, 0.3)
+    out.update({"per_pos": pos, "per_beta": beta, "per_E": e, "per_F": f, "per_U": u, "per_Y": y})
+    # C4: 2,000 bcc tungsten-like, 2J=8, rc 4.73, skin 0.3, N(0,0.05) jitter seed 1
+    a = 3.1803
+    grid = np.stack(np.meshgrid(*[np.arange(10)] * 3, indexing="ij"), -1).reshape(-1, 3).astype(float)
+    basis = np.array([[0, 0, 0], [0.5, 0.5, 0.5]])
+    lat = (grid[:, None, :] + basis[None]).reshape(-1, 3) * a
+    pos = lat + np.random.default_rng(1).normal(0.0, 0.05, lat.shape)
+    beta = np.linspace(0.05, 0.1, 55)
+    t0 = time.time()
+    e, f, u, y, npairs = _snap_pipeline(pos, Box((10 * a,) * 3), 4, beta, 4.73, 0.3)
+    print(f"SNAP 2k: {time.time() - t0:.1f}s, pairs {npairs}")
+    out.update({"c4_E": e, "c4_F": f, "c4_U_sub": u[:16], "c4_Y_sub": y[:16], "c4_npairs": npairs})
+    # perfect lattice energy (SURVEY §8(c) KAT 64610.777035472027)
+    e0, f0, _, _, _ = _snap_pipeline(lat, Box((10 * a,) * 3), 4, beta, 4.73, 0.3)
+    out.update({"c4_lattice_E": e0, "c4_lattice_Fmax": float(np.abs(f0).max())})
+    np.savez_compressed(os.path.join(HERE, "snap.npz"), **out)
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["lj_small", "lj_32k", "snap", "runs"]
+    if "lj_small" in which:
+        lj_small()
+    if "lj_32k" in which:
+        lj_32k()
+    if "snap" in which:
+        snap_fixtures()
+    if "runs" in which:
+        melt_runs()

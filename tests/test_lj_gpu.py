@@ -1,0 +1,211 @@
+"""GPU parity: neighbour lists, LJ forces and NVE runs vs the oracle and reference goldens.
+
+Mirrors the reference tests (mdkk tests/test_neighbor.py, test_pair_lj.py,
+test_acceptance.py:41-103) with the CUDA path under test and the CPU oracle /
+reference fixtures as the checker.  Tolerances are the north star's:
+neighbour sets exact, energy 1e-12 relative, forces 1e-10 * max|F|.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import golden
+from oracle import md
+
+pytestmark = pytest.mark.gpu
+
+
+def _mk(pos, lengths, n_ranks=1, gids=None):
+    from paper_2508_13523_b200 import Box, RankedSystem
+    return RankedSystem.distribute(Box(lengths), n_ranks, pos, np.zeros_like(pos), global_ids=gids)
+
+
+def _directed(system, lists):
+    out = []
+    for store, nl in zip(system.stores, lists):
+        rows, cols, w, wj = nl.pairs()
+        sh = np.rint(store.ghost_shift[cols] / system.box.lengths).astype(np.int64)
+        out.append(np.column_stack([store.global_ids[rows], store.global_ids[cols], sh,
+                                    np.full(len(rows), store.rank), (w * 2).astype(np.int64),
+                                    wj.astype(np.int64)]))
+    return set(map(tuple, np.concatenate(out).tolist()))
+
+
+@pytest.mark.parametrize("style,newton", [("full", False), ("half", True), ("half", False)])
+@pytest.mark.parametrize("n_ranks", [1, 2, 4])
+def test_lists_and_forces_match_reference(gpu, style, newton, n_ranks):
+    from paper_2508_13523_b200 import LJCut, PairParams, build_all, compute_pair
+    g = golden("lj_small.npz")
+    tag = f"{style}_{int(newton)}_{n_ranks}"
+    system = _mk(g["pos"], g["lengths"], n_ranks)
+    lists = build_all(system, 2.5, 0.3, style=style, newton=newton)
+    assert _directed(system, lists) == set(map(tuple, g[f"pairs_{tag}"].tolist()))
+    assert [nl.max_neighbors for nl in lists] == g[f"cap_{tag}"].tolist()
+    assert [s.n_ghost for s in system.stores] == g[f"nghost_{tag}"].tolist()
+    res = compute_pair(LJCut(PairParams(1.0, 1.0, 2.5)), system, lists)
+    assert res.energy == pytest.approx(float(g[f"E_{tag}"]), rel=1e-12)
+    fref = g[f"F_{tag}"]
+    assert np.abs(res.forces - fref).max() <= 1e-10 * np.abs(fref).max()
+    assert np.allclose(res.virial, g[f"W_{tag}"], rtol=1e-12, atol=1e-10)
+
+
+def test_lj_matches_n2_oracle_20_configs(gpu):
+    """mdkk tests/test_acceptance.py:41-58 with the GPU path."""
+    from paper_2508_13523_b200 import LJCut, PairParams, build_all, compute_pair
+    cases = [(100, 0.5), (100, 0.8)] * 4 + [(500, 0.6), (500, 0.8)] * 4 + [(2000, 0.7)] * 4
+    for k, (n, rho) in enumerate(cases):
+        pos, lengths = md.random_config(n, rho, seed=1000 + k)
+        eps, sigma = 0.8 + 0.05 * (k % 5), 0.9 + 0.02 * (k % 4)
+        e_ref, f_ref, w_ref = md.lj_reference_n2(pos, lengths, eps, sigma, 1.8)
+        system = _mk(pos, lengths)
+        lists = build_all(system, 1.8, 0.3, style="half", newton=True)
+        res = compute_pair(LJCut(PairParams(eps, sigma, 1.8)), system, lists)
+        assert res.energy == pytest.approx(e_ref, rel=1e-12), k
+        assert np.allclose(res.forces, f_ref, rtol=1e-12, atol=1e-10), k
+        assert np.allclose(res.virial, w_ref, rtol=1e-12, atol=1e-10), k
+
+
+@pytest.mark.parametrize("style,newton", [("full", False), ("half", True)])
+def test_lj_32k_kat(gpu, style, newton):
+    from paper_2508_13523_b200 import LJCut, PairParams, build_all, compute_pair
+    g = golden("lj_32k_jitter.npz")
+    pos, lengths = md.lattice("fcc", 0.8442, (20, 20, 20))
+    pos = md.jittered(pos, 0.02, 1)
+    system = _mk(pos, lengths)
+    lists = build_all(system, 2.5, 0.3, style=style, newton=newton)
+    assert lists[0].max_neighbors == int(g[f"cap_{style}"])
+    assert int(lists[0].counts.sum()) == int(g[f"nentries_{style}"])
+    assert system.stores[0].n_ghost == int(g[f"nghost_{style}"])
+    res = compute_pair(LJCut(PairParams(1.0, 1.0, 2.5)), system, lists)
+    assert res.energy == pytest.approx(float(g[f"E_{style}"]), rel=1e-12)
+    if style == "full":
+        assert res.energy == pytest.approx(-215477.76387663497, rel=1e-12)
+    assert np.abs(res.forces[::37] - g[f"F_{style}_sub"]).max() <= 1e-10 * float(g[f"Fmax_{style}"])
+    assert np.allclose(res.virial, g[f"W_{style}"], rtol=1e-12)
+
+
+def test_pair_set_vs_brute_force_and_capacity_growth(gpu):
+    from paper_2508_13523_b200 import build_all
+    pos, lengths = md.random_config(60, 0.9, seed=21)
+    system = _mk(pos, lengths)
+    dense = build_all(system, 1.4, 0.3, style="full", newton=False, capacity=1)
+    ref = build_all(system, 1.4, 0.3, style="full", newton=False)
+    brute = md.pair_set_brute(pos, lengths, 1.4)
+
+    def within(lst):
+        out = set()
+        st = system.stores[0]
+        for nl in lst:
+            r, c, _, _ = nl.pairs()
+            x = st.positions()
+            d = x[c] - x[r]
+            k = (d * d).sum(1) < 1.4 ** 2
+            out |= {tuple(sorted((int(st.global_ids[a]), int(st.global_ids[b])))) for a, b in zip(r[k], c[k])}
+        return out
+    assert within(dense) == within(ref) == brute
+    assert dense[0].max_neighbors >= dense[0].max_count
+
+
+def test_canonical_row_order(gpu):
+    from paper_2508_13523_b200 import build_all
+    pos, lengths = md.random_config(60, 0.65, seed=21)
+    system = _mk(pos, lengths)
+    (nl,) = build_all(system, 1.4, 0.3, style="full", newton=False)
+    rows, cols, _, _ = nl.pairs()
+    assert np.all(np.diff(rows) >= 0)
+    x, gid = system.stores[0].positions(), system.stores[0].global_ids
+    for r in np.unique(rows):
+        c = cols[rows == r]
+        key = np.lexsort((x[c, 0], x[c, 1], x[c, 2], gid[c]))
+        assert np.array_equal(key, np.arange(len(c)))
+
+
+def test_table_is_padded_transposed(gpu):
+    from paper_2508_13523_b200 import build_all
+    pos, lengths = md.random_config(80, 0.65, seed=21)
+    (nl,) = build_all(_mk(pos, lengths), 1.4, 0.3, style="full", newton=False)
+    tbl = nl.table.read("a")
+    assert tbl.shape == (80, nl.max_neighbors)
+    cnt = nl.counts
+    for i in range(80):
+        assert np.all(tbl[i, cnt[i]:] == -1) and np.all(tbl[i, : cnt[i]] >= 0)
+
+
+def test_skin_rebuild_and_stale_refusal(gpu):
+    from paper_2508_13523_b200 import LJCut, PairParams, StaleListError, any_needs_rebuild, build_all, compute_pair
+    pos, lengths = md.random_config(30, 0.65, seed=21)
+    system = _mk(pos, lengths)
+    (nl,) = build_all(system, 1.4, 0.3, style="full", newton=False)
+    store = system.stores[0]
+    assert not nl.needs_rebuild()
+    p = store.pos.read("a")
+    p[0, 0] += 0.49 * 0.3
+    store.pos.mark_modified("a")
+    system.forward_comm()
+    assert not nl.needs_rebuild()
+    p = store.pos.read("a")
+    p[0, 0] += 0.02 * 0.3
+    store.pos.mark_modified("a")
+    system.forward_comm()
+    assert nl.needs_rebuild() and any_needs_rebuild([nl])
+    with pytest.raises(StaleListError):
+        compute_pair(LJCut(PairParams(1.0, 1.0, 1.4)), system, [nl])
+
+
+def test_coincident_atoms_raise(gpu):
+    from paper_2508_13523_b200 import LJCut, PairError, PairParams, build_all, compute_pair
+    pos = np.array([[1.0, 1.0, 1.0], [1.0, 1.0, 1.0]])
+    system = _mk(pos, np.array([6.0, 6.0, 6.0]))
+    lists = build_all(system, 2.5, 0.3, style="half", newton=True)
+    with pytest.raises(PairError):
+        compute_pair(LJCut(PairParams(1.0, 1.0, 2.5)), system, lists)
+
+
+def test_ghosts_are_owner_plus_shift(gpu):
+    pos, lengths = md.random_config(64, 0.7, seed=5)
+    system = _mk(pos, lengths, 4)
+    system.exchange_ghosts(1.3)
+    osys = md.Ranked(lengths, 4, pos, np.zeros_like(pos))
+    osys.exchange_ghosts(1.3)
+    for store, ork in zip(system.stores, osys.ranks):
+        x = store.positions()
+        got = {(int(g), tuple(np.rint(s / lengths).astype(int)), tuple(p)) for g, s, p in
+               zip(store.global_ids[store.n_local:], store.ghost_shift[store.n_local:], x[store.n_local:])}
+        ref = {(int(g), tuple(np.rint(s / lengths).astype(int)), tuple(p)) for g, s, p in
+               zip(ork.gid[ork.n_local:], ork.shift[ork.n_local:], ork.x[ork.n_local:])}
+        assert got == ref  # bit-exact ghost coordinates
+
+
+def test_melt_500_matches_reference(gpu):
+    """pkg/scripts/melt.in through run_script: thermo rows vs the reference's, drift < 1e-4."""
+    from paper_2508_13523_b200.driver import RunConfig, run_script
+    text = ("units lj\nboundary p p p\nlattice fcc 0.8442\ncreate_box 5 5 5\ncreate_atoms\nmass 1.0\n"
+            "velocity 0.05 87287\npair_style lj/cut 2.2\npair_coeff 1.0 1.0\ntimestep 0.005\n"
+            "thermo 100\nrun 1000\n")
+    sim = run_script(text, RunConfig(), log=None)
+    rows = np.array(sim.results[-1].rows)
+    ref = golden("lj_runs.npz")["melt500_rows"]
+    assert rows.shape == ref.shape
+    assert np.allclose(rows[:3, 1:], ref[:3, 1:], rtol=1e-9, atol=1e-9)
+    e0 = rows[0, 3]
+    assert np.abs(rows[:, 3] - e0).max() / abs(e0) < 1e-4
+
+
+@pytest.mark.parametrize("style", ["half", "full"])
+def test_c1_32k_trajectory_matches_reference(gpu, style):
+    """C1 melt: 100 steps, thermo every 10, vs the reference's own run."""
+    from paper_2508_13523_b200.driver import RunConfig, run_script
+    c1 = ("units lj\nboundary p p p\nlattice fcc 0.8442\ncreate_box 20 20 20\ncreate_atoms\n"
+          "mass 1.0\nvelocity 1.44 87287\npair_style lj/cut 2.5\npair_coeff 1.0 1.0\n"
+          "timestep 0.005\nthermo 10\nrun 100\n")
+    sim = run_script(c1, RunConfig(list_style=style, newton=(style == "half")), log=None)
+    rows = np.array(sim.results[-1].rows)
+    g = golden("lj_runs.npz")
+    ref = g[f"c1_{style}_rows"]
+    assert rows.shape == ref.shape
+    assert rows[0, 1] == pytest.approx(ref[0, 1], rel=1e-12)
+    assert np.allclose(rows[:, 1:], ref[:, 1:], rtol=1e-8)
+    snap = sim.results[-1].snapshots[100][::97]
+    assert np.abs(snap - g[f"c1_{style}_final_pos_sub"]).max() < 1e-7
