@@ -31,25 +31,25 @@ void* scratch(mdkk_ctx* ctx, size_t bytes) {
     return ctx->scratch;
 }
 
-__global__ void k_reduce_partials(const double* __restrict__ p, int nb, int K, double* __restrict__ out) {
-    // one block; thread t sums a strided slice of column k, then a fixed-order tree
-    __shared__ double sm[256];
-    for (int k = 0; k < K; ++k) {
-        double s = 0.0;
-        for (int b = threadIdx.x; b < nb; b += blockDim.x) s += p[(long long)b * K + k];
-        sm[threadIdx.x] = s;
-        __syncthreads();
-        for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-            if (threadIdx.x < w) sm[threadIdx.x] += sm[threadIdx.x + w];
-            __syncthreads();
-        }
-        if (threadIdx.x == 0) out[k] = sm[0];
-        __syncthreads();
+// One block per column k: fixed-order strided sums then a fixed tree (deterministic).
+__global__ void __launch_bounds__(1024) k_reduce_partials(const double* __restrict__ p, int nb, int K,
+                                                          double* __restrict__ out) {
+    __shared__ double sm[32];
+    const int k = blockIdx.x;
+    double s = 0.0;
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) s += p[(long long)b * K + k];
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double v = threadIdx.x < (blockDim.x >> 5) ? sm[threadIdx.x] : 0.0;
+        v = warp_sum(v);
+        if (threadIdx.x == 0) out[k] = v;
     }
 }
 
 void reduce_partials(const double* partials, int nblocks, int K, double* out, cudaStream_t s) {
-    k_reduce_partials<<<1, 256, 0, s>>>(partials, nblocks, K, out);
+    k_reduce_partials<<<K, 1024, 0, s>>>(partials, nblocks, K, out);
 }
 
 }  // namespace mdkk

@@ -1,30 +1,28 @@
-// Cell binning (counting sort) and the per-atom stencil neighbour build.
+// Cell binning (counting sort) and the cluster neighbour build.
 // Reference: mdkk/neighbor.py:83-219 (candidate pairs, style rules, table).
+//
+// Build = one warp per 32-atom cluster of cell-sorted owned rows:
+//   1. bounding box of the cluster (warp min/max)
+//   2. union: every row (owned or ghost) in the cells overlapping bbox +/- bc
+//      whose distance to the bbox is < bc, ballot-compacted into union[c]
+//      (positions staged in shared memory)
+//   3. each lane scans the staged union (broadcast reads) and keeps j != i with
+//      r^2 < bc^2 (strict, same rounding as the reference) passing the style
+//      predicate (full / half newton on / off, mdkk/neighbor.py:134-179).
 #include <cub/device/device_scan.cuh>
 
-#include "common.cuh"
+#include "cluster.cuh"
 
 namespace {
 
-struct Grid {
-    double ox, oy, oz;
-    double ix, iy, iz;
-    int nx, ny, nz;
-};
-
-__device__ __forceinline__ int clampi(int v, int hi) { return v < 0 ? 0 : (v >= hi ? hi - 1 : v); }
-
-__device__ __forceinline__ int3 cell_of(const Grid& g, double x, double y, double z) {
-    return make_int3(clampi((int)floor((x - g.ox) * g.ix), g.nx), clampi((int)floor((y - g.oy) * g.iy), g.ny),
-                     clampi((int)floor((z - g.oz) * g.iz), g.nz));
-}
+using mdkk::Grid;
 
 __global__ void k_cell_keys(const double* __restrict__ x, int n, Grid g, int* __restrict__ key) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     double4 p = mdkk::ld4(x, i);
-    int3 c = cell_of(g, p.x, p.y, p.z);
-    key[i] = (c.x * g.ny + c.y) * g.nz + c.z;
+    int3 c = mdkk::cell_of(g, p.x, p.y, p.z);
+    key[i] = mdkk::cell_key(g, c.x, c.y, c.z);
 }
 
 // Owning brick: floor(pos / L * grid) clipped (mdkk/domain.py:89-95).
@@ -33,9 +31,9 @@ __global__ void k_rank_keys(const double* __restrict__ x, int n, double Lx, doub
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     double4 p = mdkk::ld4(x, i);
-    int cx = clampi((int)floor(p.x / Lx * (double)gx), gx);
-    int cy = clampi((int)floor(p.y / Ly * (double)gy), gy);
-    int cz = clampi((int)floor(p.z / Lz * (double)gz), gz);
+    int cx = mdkk::clampi((int)floor(p.x / Lx * (double)gx), gx);
+    int cy = mdkk::clampi((int)floor(p.y / Ly * (double)gy), gy);
+    int cz = mdkk::clampi((int)floor(p.z / Lz * (double)gz), gz);
     key[i] = (cx * gy + cy) * gz + cz;
 }
 
@@ -52,7 +50,7 @@ __global__ void k_cell_scatter(int n, const int* __restrict__ cid, const int* __
     atoms[start[c] + atomicAdd(cursor + c, 1)] = i;
 }
 
-// Deterministic order inside a cell: ascending row index (insertion sort).
+// Deterministic order inside a bucket: ascending row index (insertion sort).
 __global__ void k_cell_sort(int ncell, const int* __restrict__ start, int* __restrict__ atoms) {
     int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= ncell) return;
@@ -67,64 +65,135 @@ __global__ void k_cell_sort(int ncell, const int* __restrict__ start, int* __res
     }
 }
 
-__device__ __forceinline__ bool lex_zyx_less(const double4& a, const double4& b) {
+__device__ __forceinline__ bool lex_zyx_less(double ax, double ay, double az, double bx, double by, double bz) {
     // mdkk/neighbor.py:163-166: z, then y, then x
-    return (a.z < b.z) || (a.z == b.z && (a.y < b.y || (a.y == b.y && a.x < b.x)));
+    return (az < bz) || (az == bz && (ay < by || (ay == by && ax < bx)));
 }
 
+constexpr int kWarps = 4;
+
 template <int STYLE, bool NEWTON>
-__global__ void __launch_bounds__(128) k_nbr_build(const double* __restrict__ x, int n_local, Grid g,
-                                                   const int* __restrict__ cell_start,
-                                                   const int* __restrict__ cell_atoms,
-                                                   const int64_t* __restrict__ gid,
-                                                   const int32_t* __restrict__ owner_rank, int my_rank,
-                                                   double bc2, int cap, int* __restrict__ table,
-                                                   int* __restrict__ counts, int* __restrict__ max_count) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    int cnt = 0;
-    if (i < n_local) {
-        const double4 xi = mdkk::ld4(x, i);
-        const int3 c = cell_of(g, xi.x, xi.y, xi.z);
-        int64_t gi = 0;
-        if (STYLE == 1) gi = gid[i];
-        for (int ax = c.x - 1; ax <= c.x + 1; ++ax) {
-            if (ax < 0 || ax >= g.nx) continue;
-            for (int ay = c.y - 1; ay <= c.y + 1; ++ay) {
-                if (ay < 0 || ay >= g.ny) continue;
-                // cells (ax, ay, c.z-1 .. c.z+1) are contiguous in cell order
-                int z0 = max(c.z - 1, 0), z1 = min(c.z + 1, g.nz - 1);
-                int base = (ax * g.ny + ay) * g.nz;
-                int s0 = cell_start[base + z0], s1 = cell_start[base + z1 + 1];
-                for (int s = s0; s < s1; ++s) {
-                    int j = cell_atoms[s];
-                    if (j == i) continue;
-                    double4 xj = mdkk::ld4(x, j);
-                    double r2 = mdkk::r2_exact(xj.x - xi.x, xj.y - xi.y, xj.z - xi.z);
-                    if (!(r2 < bc2)) continue;
-                    if (STYLE == 1) {
-                        bool keep;
-                        if (j < n_local) {
-                            keep = gi < gid[j];
-                        } else if (NEWTON) {
-                            int orank = owner_rank[j];
-                            keep = orank > my_rank || (orank == my_rank && lex_zyx_less(xi, xj));
-                        } else {
-                            keep = true;
-                        }
-                        if (!keep) continue;
-                    }
-                    if (cnt < cap) table[(long long)cnt * n_local + i] = j;
-                    ++cnt;
+__global__ void __launch_bounds__(kWarps * 32) k_nbr_build(
+    const double* __restrict__ x, int n_local, Grid g, const int* __restrict__ cell_start,
+    const int* __restrict__ cell_atoms, const int64_t* __restrict__ gid, const int32_t* __restrict__ owner_rank,
+    int my_rank, double bc, double bc2, int cap, int ucap, int S, int* __restrict__ uni, int* __restrict__ ucount,
+    uint16_t* __restrict__ table, int* __restrict__ counts, int* __restrict__ maxes) {
+    extern __shared__ double smem[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int c = blockIdx.x * kWarps + w;
+    const int ncl = (n_local + 31) >> 5;
+    if (c >= ncl) return;
+    double* sx = smem + (size_t)w * S * 3;
+    double* sy = sx + S;
+    double* sz = sy + S;
+    int* su = reinterpret_cast<int*>(smem + (size_t)kWarps * S * 3) + (size_t)w * S;
+
+    const int i = c * 32 + lane;
+    const bool valid = i < n_local;
+    double4 xi = mdkk::ld4(x, valid ? i : c * 32);
+    // 1. cluster bounding box
+    double bmin_x = mdkk::warp_min_d(xi.x), bmax_x = mdkk::warp_max(xi.x);
+    double bmin_y = mdkk::warp_min_d(xi.y), bmax_y = mdkk::warp_max(xi.y);
+    double bmin_z = mdkk::warp_min_d(xi.z), bmax_z = mdkk::warp_max(xi.z);
+    const int3 clo = mdkk::cell_of(g, bmin_x - bc, bmin_y - bc, bmin_z - bc);
+    const int3 chi = mdkk::cell_of(g, bmax_x + bc, bmax_y + bc, bmax_z + bc);
+    // 2. union of candidate rows within bc of the bbox
+    int m = 0;
+    int* ug = uni + (long long)c * ucap;
+    for (int cx = clo.x; cx <= chi.x; ++cx) {
+        for (int cy = clo.y; cy <= chi.y; ++cy) {
+            int2 kr = mdkk::zrun_keys(g, cx, cy, clo.z, chi.z);
+            const int s0 = cell_start[kr.x], s1 = cell_start[kr.y + 1];
+            for (int base = s0; base < s1; base += 32) {
+                const int s = base + lane;
+                bool keep = false;
+                int j = 0;
+                double4 p = make_double4(0, 0, 0, 0);
+                if (s < s1) {
+                    j = cell_atoms[s];
+                    p = mdkk::ld4(x, j);
+                    double dx = fmax(0.0, fmax(bmin_x - p.x, p.x - bmax_x));
+                    double dy = fmax(0.0, fmax(bmin_y - p.y, p.y - bmax_y));
+                    double dz = fmax(0.0, fmax(bmin_z - p.z, p.z - bmax_z));
+                    keep = dx * dx + dy * dy + dz * dz < bc2 * (1.0 + 1e-12);
                 }
+                const unsigned mask = __ballot_sync(0xffffffffu, keep);
+                if (keep) {
+                    const int pos = m + __popc(mask & ((1u << lane) - 1u));
+                    if (pos < ucap) ug[pos] = j;
+                    if (pos < S) {
+                        sx[pos] = p.x;
+                        sy[pos] = p.y;
+                        sz[pos] = p.z;
+                        su[pos] = j;
+                    }
+                }
+                m += __popc(mask);
             }
+        }
+    }
+    if (lane == 0) {
+        ucount[c] = m;
+        atomicMax(maxes + 1, m);
+    }
+    __syncwarp();
+    if (m > ucap) return;  // host grows ucap and relaunches
+    // 3. per-lane scan of the union
+    int cnt = 0;
+    if (valid) {
+        const int64_t gi = (STYLE == 1) ? gid[i] : 0;
+        const int capb = cap >> 3;
+        for (int u = 0; u < m; ++u) {
+            int j;
+            double px, py, pz;
+            if (u < S) {
+                j = su[u];
+                px = sx[u];
+                py = sy[u];
+                pz = sz[u];
+            } else {
+                j = ug[u];
+                double4 p = mdkk::ld4(x, j);
+                px = p.x;
+                py = p.y;
+                pz = p.z;
+            }
+            if (j == i) continue;
+            const double r2 = mdkk::r2_exact(px - xi.x, py - xi.y, pz - xi.z);
+            if (!(r2 < bc2)) continue;
+            if (STYLE == 1) {
+                bool keep;
+                if (j < n_local) {
+                    keep = gi < gid[j];
+                } else if (NEWTON) {
+                    const int orank = owner_rank[j];
+                    keep = orank > my_rank ||
+                           (orank == my_rank && lex_zyx_less(xi.x, xi.y, xi.z, px, py, pz));
+                } else {
+                    keep = true;
+                }
+                if (!keep) continue;
+            }
+            if (cnt < cap) table[mdkk::tbl_index(c, capb, cnt, lane)] = (uint16_t)u;
+            ++cnt;
         }
         counts[i] = cnt;
     }
-    // warp max then one atomic per warp
-    int m = cnt;
+    int mc = cnt;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((threadIdx.x & 31) == 0 && m > 0) atomicMax(max_count, m);
+    for (int o = 16; o > 0; o >>= 1) mc = max(mc, __shfl_xor_sync(0xffffffffu, mc, o));
+    if (lane == 0 && mc > 0) atomicMax(maxes, mc);
+}
+
+// Expand a cluster list into a plain int32 [cap_out][n_local] table of row indices.
+__global__ void k_expand(const int* __restrict__ uni, int ucap, const uint16_t* __restrict__ table, int cap,
+                         const int* __restrict__ counts, int n_local, int cap_out, int* __restrict__ out) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_local) return;
+    const int c = i >> 5, lane = i & 31, capb = cap >> 3;
+    const int n = min(counts[i], min(cap, cap_out));
+    for (int k = 0; k < n; ++k) out[(long long)k * n_local + i] = uni[(long long)c * ucap + table[mdkk::tbl_index(c, capb, k, lane)]];
+    for (int k = n; k < cap_out; ++k) out[(long long)k * n_local + i] = -1;
 }
 
 // Canonical per-row order: (gid[j], z_j, y_j, x_j) ascending (mdkk/neighbor.py:192-197).
@@ -163,20 +232,6 @@ __global__ void k_max_disp2(const double* __restrict__ x, const double* __restri
     }
     d2 = mdkk::warp_max(d2);
     if ((threadIdx.x & 31) == 0) mdkk::atomic_max_nonneg(out, d2);
-}
-
-Grid make_grid(const double* gh, const int* nc) {
-    Grid g;
-    g.ox = gh[0];
-    g.oy = gh[1];
-    g.oz = gh[2];
-    g.ix = gh[3];
-    g.iy = gh[4];
-    g.iz = gh[5];
-    g.nx = nc[0];
-    g.ny = nc[1];
-    g.nz = nc[2];
-    return g;
 }
 
 }  // namespace
@@ -218,7 +273,7 @@ int mdkk_cell_keys(const double* x, int n, const double* grid_host, const int* n
                    void* stream) {
     if (n < 0 || !grid_host || !ncell_host) return MDKK_E_ARG;
     if (n == 0) return MDKK_OK;
-    Grid g = make_grid(grid_host, ncell_host);
+    Grid g = mdkk::make_grid(grid_host, ncell_host);
     if (g.nx < 1 || g.ny < 1 || g.nz < 1) return MDKK_E_ARG;
     k_cell_keys<<<mdkk::grid_for(n, 256), 256, 0, mdkk::as_stream(stream)>>>(x, n, g, keys);
     MDKK_CHECK_LAUNCH("k_cell_keys");
@@ -247,23 +302,43 @@ int mdkk_bin_atoms(mdkk_ctx* ctx, const double* x, int n, const double* grid_hos
 
 int mdkk_nbr_build(mdkk_ctx*, const double* x, int n_local, int n_total, const double* grid_host,
                    const int* ncell_host, const int* cell_start, const int* cell_atoms, const int64_t* gid,
-                   const int32_t* owner_rank, int my_rank, double bc2, int style, int newton, int cap,
-                   int* table, int* counts, int* max_count, void* stream) {
-    if (n_local < 0 || n_total < n_local || cap < 1 || (style != 0 && style != 1)) return MDKK_E_ARG;
+                   const int32_t* owner_rank, int my_rank, double bc, int style, int newton, int cap, int ucap,
+                   int stage, int* uni, int* ucount, uint16_t* table, int* counts, int* maxes, void* stream) {
+    if (n_local < 0 || n_total < n_local || cap < 8 || (cap & 7) || ucap < 1 || ucap > 65535 || stage < 32 ||
+        (style != 0 && style != 1))
+        return MDKK_E_ARG;
     if (n_local == 0) return MDKK_OK;
-    Grid g = make_grid(grid_host, ncell_host);
+    Grid g = mdkk::make_grid(grid_host, ncell_host);
     cudaStream_t s = mdkk::as_stream(stream);
-    int nb = mdkk::grid_for(n_local, 128);
+    const int ncl = (n_local + 31) / 32;
+    const int nb = (ncl + kWarps - 1) / kWarps;
+    const size_t sm = (size_t)kWarps * stage * (3 * sizeof(double) + sizeof(int));
+    const double bc2 = bc * bc;
+#define MDKK_BUILD(ST, NW)                                                                                       \
+    do {                                                                                                         \
+        auto kern = k_nbr_build<ST, NW>;                                                                         \
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);                        \
+        kern<<<nb, kWarps * 32, sm, s>>>(x, n_local, g, cell_start, cell_atoms, gid, owner_rank, my_rank, bc, bc2, \
+                                         cap, ucap, stage, uni, ucount, table, counts, maxes);                   \
+    } while (0)
     if (style == 0)
-        k_nbr_build<0, false><<<nb, 128, 0, s>>>(x, n_local, g, cell_start, cell_atoms, gid, owner_rank,
-                                                 my_rank, bc2, cap, table, counts, max_count);
+        MDKK_BUILD(0, false);
     else if (newton)
-        k_nbr_build<1, true><<<nb, 128, 0, s>>>(x, n_local, g, cell_start, cell_atoms, gid, owner_rank,
-                                                my_rank, bc2, cap, table, counts, max_count);
+        MDKK_BUILD(1, true);
     else
-        k_nbr_build<1, false><<<nb, 128, 0, s>>>(x, n_local, g, cell_start, cell_atoms, gid, owner_rank,
-                                                 my_rank, bc2, cap, table, counts, max_count);
+        MDKK_BUILD(1, false);
+#undef MDKK_BUILD
     MDKK_CHECK_LAUNCH("k_nbr_build");
+    return MDKK_OK;
+}
+
+int mdkk_nbr_expand(const int* uni, int ucap, const uint16_t* table, int cap, const int* counts, int n_local,
+                    int cap_out, int* out, void* stream) {
+    if (n_local < 0 || cap < 8 || (cap & 7) || cap_out < 1) return MDKK_E_ARG;
+    if (n_local == 0) return MDKK_OK;
+    k_expand<<<mdkk::grid_for(n_local, 128), 128, 0, mdkk::as_stream(stream)>>>(uni, ucap, table, cap, counts,
+                                                                                n_local, cap_out, out);
+    MDKK_CHECK_LAUNCH("k_expand");
     return MDKK_OK;
 }
 

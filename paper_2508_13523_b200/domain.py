@@ -475,6 +475,15 @@ class RankedSystem:
             s.device_wrote(pos=True, vel=True, force=True)
         self.exchange_ghosts(halo)
 
+    def sort_local(self, width: float) -> None:
+        """Re-order every rank's owned rows into serpentine cell order (drops ghosts; call before exchange)."""
+        for s in self.stores:
+            s.to_device()
+            s.n_ghost = 0
+            self._spatial_sort(s, width, width)
+            s.device_wrote(pos=True, vel=True, force=True)
+        self.lanes = []
+
     def _spatial_sort(self, s: AtomStore, width: float, halo: float):
         """Reorder owned rows by cell so neighbour gathers are local (rows are re-indexed, gids travel)."""
         if s.n_local < 2:

@@ -83,7 +83,7 @@ class LJStyle:
         flags = torch.zeros(1, dtype=torch.int32, device=dev)
         half = False
         for k, (s, nl) in enumerate(zip(system.stores, lists)):
-            lj_force_rank(s, nl, self.kernel.params, evs[k], flags)
+            lj_force_rank(s, nl, self.kernel.params, evs[k], flags, virial=False)
             half |= nl.style == "half"
         if half and any(s.n_ghost for s in system.stores):
             system.reverse_comm()
@@ -187,6 +187,7 @@ class Simulation:
         self.results: list[RunResult] = []
         self.n_rebuilds = 0
         self._cap_hint = None
+        self._ucap_hint = None
         self.snapshots = True
         dev = self.config.device
         self.device = torch.device(dev) if dev is not None else torch.device("cuda", torch.cuda.current_device())
@@ -291,7 +292,8 @@ class Simulation:
             self._list_style = style_list
             self.lists = build_all(self.system, self.style.r_c, self.config.skin, style=style_list,
                                    newton=self.config.newton)
-            self._cap_hint = max(nl.table_dev.shape[0] for nl in self.lists)
+            self._cap_hint = max(nl.alloc_cap for nl in self.lists)
+            self._ucap_hint = max(nl.ucap for nl in self.lists)
         if self._d2 is None:
             self._d2 = torch.zeros(max(self.config.n_ranks, 1), dtype=torch.float64, device=self.device)
 
@@ -300,8 +302,10 @@ class Simulation:
         halo = self.style.r_c + self.config.skin
         self.system.migrate(halo)
         self.lists = [build(s, self.system.box, self.style.r_c, self.config.skin, style=self._list_style,
-                            newton=self.config.newton, cap_hint=self._cap_hint) for s in self.system.stores]
-        self._cap_hint = max(nl.table_dev.shape[0] for nl in self.lists)
+                            newton=self.config.newton, cap_hint=self._cap_hint, ucap_hint=self._ucap_hint)
+                      for s in self.system.stores]
+        self._cap_hint = max(nl.alloc_cap for nl in self.lists)
+        self._ucap_hint = max(nl.ucap for nl in self.lists)
         self.n_rebuilds += 1
 
     def _forces_device(self):

@@ -39,21 +39,41 @@ def grow_capacity(capacity: int, needed: int) -> int:
     return cap
 
 
+STAGE_MAX = 768  # union entries staged in shared memory per 32-atom cluster
+
+
+def _round8(v: int) -> int:
+    return (int(v) + 7) // 8 * 8
+
+
 class NeighborList:
-    """Device neighbour table + counts (mdkk/neighbor.py:38-80)."""
+    """Device cluster neighbour list (mdkk/neighbor.py:38-80).
+
+    Device layout (include/mdkk_b200.h, "cluster list"): owned rows are
+    cell-sorted, cluster c = rows [32c, 32c+32); `uni_dev[c, :ucount[c]]` is
+    the cluster's union of candidate partners and `table_dev` holds uint16
+    local indices into it, 8 per 16-byte lane load.
+    """
 
     def __init__(self, store: AtomStore, style: str, newton: bool, cutoff: float, skin: float,
-                 cap: int, table: torch.Tensor, counts: torch.Tensor, max_count: int):
+                 cap: int, alloc_cap: int, table: torch.Tensor, counts: torch.Tensor, uni: torch.Tensor,
+                 ucount: torch.Tensor, ucap: int, max_count: int, max_union: int):
         self.store = store
         self.style = style
         self.newton = bool(newton)
         self.cutoff = float(cutoff)
         self.skin = float(skin)
         self.n_local = store.n_local
-        self.max_neighbors = int(cap)
+        self.max_neighbors = int(cap)      # reference growth sequence from `capacity`
+        self.alloc_cap = int(alloc_cap)    # physical slots per row (multiple of 8, >= max_count)
         self.max_count = int(max_count)
-        self.table_dev = table          # (>= cap, n_local) int32; rows beyond counts undefined
-        self.counts_dev = counts        # (n_local,) int32
+        self.max_union = int(max_union)
+        self.table_dev = table
+        self.counts_dev = counts
+        self.uni_dev = uni
+        self.ucount_dev = ucount
+        self.ucap = int(ucap)
+        self.stage = max(32, min(STAGE_MAX, (self.max_union + 31) // 32 * 32))
         self.ref_dev = store.x[: max(store.n_local, 1)].clone()
         self._d2 = torch.zeros(1, dtype=torch.float64, device=store.device)
         self._pairs = None
@@ -66,18 +86,24 @@ class NeighborList:
     def counts(self) -> np.ndarray:
         return self.counts_dev[: self.n_local].cpu().numpy()
 
+    def expanded(self, cap: int | None = None) -> torch.Tensor:
+        """int32 [cap][n_local] row-index table, -1 padded (device)."""
+        cap = cap or self.max_neighbors
+        n = max(self.n_local, 1)
+        out = torch.full((cap, n), -1, dtype=torch.int32, device=self.store.device)
+        if self.n_local:
+            _lib.call("mdkk_nbr_expand", self.uni_dev.data_ptr(), self.ucap, self.table_dev.data_ptr(),
+                      self.alloc_cap, self.counts_dev.data_ptr(), self.n_local, cap, out.data_ptr(),
+                      _lib.stream(self.store.device))
+        return out
+
     @property
     def table(self) -> DualArray:
-        """(n_local, cap) int32 DualArray, -1 padded (layout_b transposed = the device storage)."""
-        n, cap = max(self.n_local, 1), self.max_neighbors
-        t = self.table_dev[:cap].clone()
-        if self.n_local:
-            k = torch.arange(cap, device=t.device)[:, None]
-            t[:, : self.n_local][k >= self.counts_dev[None, : self.n_local]] = -1
-        else:
-            t.fill_(-1)
-        d = DualArray((n, cap), layout_b=LayoutPolicy.transposed(2), dtype=np.int32,
-                      device=t.device, storage_b=t[:, :n])
+        """(n_local, cap) int32 DualArray, -1 padded; device storage is [cap][n_local] (layout_b transposed)."""
+        t = self.expanded()
+        n = max(self.n_local, 1)
+        d = DualArray((n, self.max_neighbors), layout_b=LayoutPolicy.transposed(2), dtype=np.int32,
+                      device=t.device, storage_b=t)
         d.mark_modified("b")
         return d
 
@@ -94,7 +120,7 @@ class NeighborList:
             z = np.zeros(0, np.int64)
             return z, z, np.zeros(0), np.zeros(0, bool)
         cap = self.max_neighbors
-        t = self.table_dev[:cap].clone()
+        t = self.expanded(cap)
         st.to_device()
         _lib.call("mdkk_nbr_canonicalize", st.x.data_ptr(), st.gid.data_ptr(), n, cap, t.data_ptr(),
                   self.counts_dev.data_ptr(), _lib.stream(st.device))
@@ -151,12 +177,14 @@ _cache: dict = {}
 
 
 def build(store: AtomStore, box: Box, cutoff: float, skin: float, style: str = "full",
-          newton: bool = True, capacity: int = DEFAULT_CAPACITY, cap_hint: int | None = None) -> NeighborList:
+          newton: bool = True, capacity: int = DEFAULT_CAPACITY, cap_hint: int | None = None,
+          ucap_hint: int | None = None) -> NeighborList:
     """One rank's list from its local + ghost rows (mdkk/neighbor.py:182-219).
 
-    `cap_hint` (engine-internal) sizes the first launch; the reported
-    `max_neighbors` always follows the reference growth sequence from
-    `capacity`.
+    Owned rows must be cell-sorted for compact clusters (RankedSystem keeps
+    them so); any order is still correct.  `cap_hint` / `ucap_hint`
+    (engine-internal) size the first launch; the reported `max_neighbors`
+    always follows the reference growth sequence from `capacity`.
     """
     if style not in STYLES:
         raise NeighborError(f"unknown list style {style!r}")
@@ -179,32 +207,44 @@ def build(store: AtomStore, box: Box, cutoff: float, skin: float, style: str = "
     garr, narr = _lib.dbl3(g), _lib.int_arr(nc)
     _lib.check(lib.mdkk_bin_atoms(ctx, store.x.data_ptr(), n_total, garr, narr, keys.data_ptr(),
                                   cstart.data_ptr(), catoms.data_ptr(), stream), "mdkk_bin_atoms")
-    cap = grow_capacity(capacity, 0)
-    alloc = max(cap, int(cap_hint or 0))
-    counts = torch.empty(max(n_local, 1), dtype=torch.int32, device=dev)
-    mc = torch.zeros(1, dtype=torch.int32, device=dev)
+    ncl = max((n_local + 31) // 32, 1)
+    alloc = _round8(max(grow_capacity(capacity, 0), int(cap_hint or 0)))
+    ucap = int(min(65535, max(256, int(ucap_hint or 1024))))
+    stage = STAGE_MAX
+    counts = torch.empty(ncl * 32, dtype=torch.int32, device=dev)
+    ucount = torch.empty(ncl, dtype=torch.int32, device=dev)
+    maxes = torch.zeros(2, dtype=torch.int32, device=dev)
     while True:
-        table = torch.empty((alloc, max(n_local, 1)), dtype=torch.int32, device=dev)
-        mc.zero_()
+        table = torch.empty(ncl * alloc * 32, dtype=torch.int16, device=dev)
+        uni = torch.empty(ncl * ucap, dtype=torch.int32, device=dev)
+        maxes.zero_()
         _lib.check(lib.mdkk_nbr_build(ctx, store.x.data_ptr(), n_local, n_total, garr, narr, cstart.data_ptr(),
                                       catoms.data_ptr(), store.gid.data_ptr(), store.orank.data_ptr(),
-                                      store.rank, bc * bc, STYLES[style], int(bool(newton)), alloc,
-                                      table.data_ptr(), counts.data_ptr(), mc.data_ptr(), stream),
-                   "mdkk_nbr_build")
-        need = int(mc.item())
-        if need <= alloc:
-            break
-        alloc = grow_capacity(alloc, need)  # never truncate: grow and rebuild
+                                      store.rank, bc, STYLES[style], int(bool(newton)), alloc, ucap, stage,
+                                      uni.data_ptr(), ucount.data_ptr(), table.data_ptr(), counts.data_ptr(),
+                                      maxes.data_ptr(), stream), "mdkk_nbr_build")
+        need, munion = (int(v) for v in maxes.cpu().numpy())
+        if munion > ucap:
+            if munion > 65535:
+                raise NeighborError(f"cluster union of {munion} rows exceeds the uint16 table range")
+            ucap = min(65535, (int(munion * 1.25) + 63) // 64 * 64)
+            continue
+        if need > alloc:
+            alloc = _round8(grow_capacity(alloc, need))  # never truncate: grow and rebuild
+            continue
+        break
     cap = grow_capacity(capacity, need)
-    return NeighborList(store, style, newton, cutoff, skin, cap, table, counts, need)
+    return NeighborList(store, style, newton, cutoff, skin, cap, alloc, table, counts, uni, ucount, ucap,
+                        need, munion)
 
 
 def build_all(system: RankedSystem, cutoff: float, skin: float, style: str = "full",
               newton: bool = True, capacity: int = DEFAULT_CAPACITY) -> list[NeighborList]:
     """Exchange ghosts, then per-rank builds (mdkk/neighbor.py:222-227)."""
-    system.exchange_ghosts(cutoff + skin)
     if system.sort_width is None:
         system.sort_width = cutoff + skin
+        system.sort_local(cutoff + skin)   # cell order -> compact 32-atom clusters
+    system.exchange_ghosts(cutoff + skin)
     return [build(store, system.box, cutoff, skin, style, newton, capacity) for store in system.stores]
 
 

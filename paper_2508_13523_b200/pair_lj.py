@@ -90,7 +90,7 @@ class PairResult:
 
 
 def lj_force_rank(store, nl: NeighborList, params: PairParams, ev: torch.Tensor, flags: torch.Tensor,
-                  zero: bool = True) -> None:
+                  zero: bool = True, virial: bool = True) -> None:
     """One rank's kernel launch (no host sync).  Ghost rows must be zero on entry for half lists."""
     dev = store.device
     if zero and nl.style == "half":
@@ -98,9 +98,10 @@ def lj_force_rank(store, nl: NeighborList, params: PairParams, ev: torch.Tensor,
     elif zero and store.n_ghost:
         store.f[store.n_local:store.n_total].zero_()
     _lib.check(_lib.lib().mdkk_lj_force(
-        _lib.ctx(dev), store.x.data_ptr(), store.n_local, nl.table_dev.data_ptr(), nl.counts_dev.data_ptr(),
-        nl.table_dev.shape[0], STYLES[nl.style], int(nl.newton), params.epsilon, params.sigma, params.r_c,
-        store.f.data_ptr(), ev.data_ptr(), flags.data_ptr(), _lib.stream(dev)), "mdkk_lj_force")
+        _lib.ctx(dev), store.x.data_ptr(), store.n_local, nl.uni_dev.data_ptr(), nl.ucap, nl.ucount_dev.data_ptr(),
+        nl.table_dev.data_ptr(), nl.counts_dev.data_ptr(), nl.alloc_cap, nl.stage, STYLES[nl.style],
+        int(nl.newton), int(virial), params.epsilon, params.sigma, params.r_c, store.f.data_ptr(), ev.data_ptr(),
+        flags.data_ptr(), _lib.stream(dev)), "mdkk_lj_force")
 
 
 def compute_pair(kernel, system: RankedSystem, lists: list[NeighborList], mode: str = "atom", strategy=None,
