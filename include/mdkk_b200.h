@@ -105,38 +105,31 @@ int mdkk_bin_atoms(mdkk_ctx* ctx, const double* x, int n, const double* grid_hos
                    int* keys, int* cell_start, int* cell_atoms, void* stream);
 
 /* -------------------------------------------------------------- neighbour
- * Cluster neighbour list (replaces mdkk/neighbor.py:83-219 + _apply_style
- * :134-179).  Owned rows must be cell-sorted; cluster c = rows [32c, 32c+32).
- *   uni[c*ucap + u], u < ucount[c]: rows (owned or ghost) within bc of the
- *       cluster's bounding box — the staging set of the force kernels;
- *   table (uint16, cap a multiple of 8): entry k of row i = lane i%32 of
- *       cluster c is at ((c*cap/8 + k/8)*32 + lane)*8 + k%8 and holds a local
- *       index u into uni[c];  counts[i] = true number of entries.
- * Row i lists every j != i with r^2 < bc^2 (strict; r^2 rounded as the
- * reference's einsum, mdkk/neighbor.py:126) passing the style predicate:
- * style 0 = full; 1 = half with gid / owner-rank / z-y-x rules (newton on) or
- * ghosts on both sides (newton off).  maxes[0] = max count, maxes[1] = max
- * union size (device ints, caller-zeroed); the caller grows cap x1.5 / ucap
- * and relaunches when either exceeds its capacity (never truncates).
- * `stage` = union entries staged in shared memory per cluster (>= 32). */
+ * Cluster-scan neighbour build (replaces mdkk/neighbor.py:83-219 +
+ * _apply_style :134-179).  Owned rows should be cell-sorted (any order is
+ * correct, sorted is fast): one warp takes 32 consecutive rows, gathers the
+ * union of rows within bc of their bounding box, and each lane keeps every
+ * j != i with r^2 < bc^2 (strict; r^2 rounded as the reference's einsum,
+ * mdkk/neighbor.py:126) passing the style predicate: style 0 = full; 1 =
+ * half with the gid / owner-rank / z-y-x rules (newton on) or ghost pairs on
+ * both sides (newton off).  table is int32 [cap][n_local] (atom fastest),
+ * entries beyond counts[i] undefined; counts[i] is the true count even when
+ * > cap and *max_count (device int, caller-zeroed) the max, so the caller
+ * grows cap x1.5 and relaunches — never truncates (mdkk/neighbor.py:199-205). */
 int mdkk_nbr_build(mdkk_ctx* ctx, const double* x, int n_local, int n_total,
                    const double* grid_host, const int* ncell_host, const int* cell_start,
                    const int* cell_atoms, const int64_t* gid, const int32_t* owner_rank, int my_rank,
-                   double bc, int style, int newton, int cap, int ucap, int stage, int* uni, int* ucount,
-                   uint16_t* table, int* counts, int* maxes, void* stream);
-/* Expand a cluster list to int32 [cap_out][n_local] row indices, -1 padded
- * (the reference's table with the transposed layout_b, mdkk/neighbor.py:207-214). */
-int mdkk_nbr_expand(const int* uni, int ucap, const uint16_t* table, int cap, const int* counts, int n_local,
-                    int cap_out, int* out, void* stream);
+                   double bc, int style, int newton, int cap, int* table, int* counts, int* max_count,
+                   void* stream);
 /* Canonical per-row order (partner gid, z, y, x) — mdkk/neighbor.py:192-197.
- * In-place sort of each row of an expanded [cap][n_local] table. */
+ * In-place sort of each row of a [cap][n_local] table. */
 int mdkk_nbr_canonicalize(const double* x, const int64_t* gid, int n_local, int cap,
                           int* table, const int* counts, void* stream);
 /* max_i |x_i - x_ref_i|^2 into *out (device double) — mdkk/neighbor.py:66-74. */
 int mdkk_max_disp2(const double* x, const double* x_ref, int n, double* out, void* stream);
 
 /* --------------------------------------------------------------------- LJ
- * Truncated 12-6 LJ (mdkk/pair_lj.py:81-91) over a cluster list
+ * Truncated 12-6 LJ (mdkk/pair_lj.py:81-91) over a [cap][n_local] table
  * (compute_pair, mdkk/pair_lj.py:114-179).  style/newton select the entry
  * semantics of mdkk/neighbor.py:134-179:
  *   full          : f_i only, weight 1/2, no atomics (owner writes)
@@ -144,13 +137,12 @@ int mdkk_max_disp2(const double* x, const double* x_ref, int n, double* out, voi
  *   half, !newton : f_j written only for local j; ghost entries weight 1/2
  * f must be zeroed by the caller for half lists (atomics accumulate).
  * ev (device double[7]) receives {E, Wxx, Wyy, Wzz, Wxy, Wxz, Wyz}; with
- * virial == 0 only E is computed (W* = 0).  Deterministic two-stage
+ * virial == 0 only E is accumulated (W* = 0).  Deterministic two-stage
  * reduction.  flags (device int) gets MDKK_FLAG_COINCIDENT if any in-range
  * r^2 <= 0. */
-int mdkk_lj_force(mdkk_ctx* ctx, const double* x, int n_local, const int* uni, int ucap,
-                  const int* ucount, const uint16_t* table, const int* counts, int cap, int stage,
-                  int style, int newton, int virial, double epsilon, double sigma, double rc, double* f,
-                  double* ev, int* flags, void* stream);
+int mdkk_lj_force(mdkk_ctx* ctx, const double* x, int n_local, const int* table, const int* counts,
+                  int cap, int style, int newton, int virial, double epsilon, double sigma, double rc,
+                  double* f, double* ev, int* flags, void* stream);
 
 /* ------------------------------------------------------------- integrator
  * Velocity Verlet (mdkk/driver/simulation.py:431-450) fused with the skin

@@ -43,12 +43,10 @@ SIGNATURES = {
     "mdkk_rank_keys": [_p, _i, _p, _p, _p, _p],
     "mdkk_bucket_sort": [_p, _p, _i, _i, _p, _p, _p],
     "mdkk_bin_atoms": [_p, _p, _i, _p, _p, _p, _p, _p, _p],
-    "mdkk_nbr_build": [_p, _p, _i, _i, _p, _p, _p, _p, _p, _p, _i, _d, _i, _i, _i, _i, _i, _p, _p, _p, _p, _p,
-                       _p],
-    "mdkk_nbr_expand": [_p, _i, _p, _i, _p, _i, _i, _p, _p],
+    "mdkk_nbr_build": [_p, _p, _i, _i, _p, _p, _p, _p, _p, _p, _i, _d, _i, _i, _i, _p, _p, _p, _p],
     "mdkk_nbr_canonicalize": [_p, _p, _i, _i, _p, _p, _p],
     "mdkk_max_disp2": [_p, _p, _i, _p, _p],
-    "mdkk_lj_force": [_p, _p, _i, _p, _i, _p, _p, _p, _i, _i, _i, _i, _i, _d, _d, _d, _p, _p, _p, _p],
+    "mdkk_lj_force": [_p, _p, _i, _p, _p, _i, _i, _i, _i, _d, _d, _d, _p, _p, _p, _p],
     "mdkk_verlet_first": [_p, _p, _p, _p, _p, _i, _d, _d, _p, _p],
     "mdkk_verlet_second": [_p, _p, _p, _i, _d, _d, _p, _p],
     "mdkk_kinetic": [_p, _p, _i, _d, _p, _p],

@@ -4,11 +4,11 @@
 // Build = one warp per 32-atom cluster of cell-sorted owned rows:
 //   1. bounding box of the cluster (warp min/max)
 //   2. union: every row (owned or ghost) in the cells overlapping bbox +/- bc
-//      whose distance to the bbox is < bc, ballot-compacted into union[c]
-//      (positions staged in shared memory)
-//   3. each lane scans the staged union (broadcast reads) and keeps j != i with
-//      r^2 < bc^2 (strict, same rounding as the reference) passing the style
-//      predicate (full / half newton on / off, mdkk/neighbor.py:134-179).
+//      whose distance to the bbox is < bc, ballot-compacted in shared memory
+//   3. each lane scans the union (broadcast loads: one wavefront per candidate
+//      per warp) and keeps j != i with r^2 < bc^2 (strict, same rounding as
+//      the reference) passing the style predicate (mdkk/neighbor.py:134-179).
+// Output: int32 table [cap][n_local] (atom fastest) of row indices + counts.
 #include <cub/device/device_scan.cuh>
 
 #include "cluster.cuh"
@@ -71,129 +71,97 @@ __device__ __forceinline__ bool lex_zyx_less(double ax, double ay, double az, do
 }
 
 constexpr int kWarps = 4;
+constexpr int kUnion = 1024;  // candidate indices staged per cluster (4 KB of shared memory per warp)
 
+// One warp per 32-atom cluster of cell-sorted owned rows.  The union pass
+// collects every row within bc of the cluster's bounding box (a superset of
+// each lane's partners); the scan then reads each candidate once per warp
+// through a broadcast load while every lane tests it against its own atom.
 template <int STYLE, bool NEWTON>
 __global__ void __launch_bounds__(kWarps * 32) k_nbr_build(
     const double* __restrict__ x, int n_local, Grid g, const int* __restrict__ cell_start,
     const int* __restrict__ cell_atoms, const int64_t* __restrict__ gid, const int32_t* __restrict__ owner_rank,
-    int my_rank, double bc, double bc2, int cap, int ucap, int S, int* __restrict__ uni, int* __restrict__ ucount,
-    uint16_t* __restrict__ table, int* __restrict__ counts, int* __restrict__ maxes) {
-    extern __shared__ double smem[];
+    int my_rank, double bc, double bc2, int cap, int* __restrict__ table, int* __restrict__ counts,
+    int* __restrict__ max_count) {
+    __shared__ int s_union[kWarps][kUnion];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int c = blockIdx.x * kWarps + w;
     const int ncl = (n_local + 31) >> 5;
     if (c >= ncl) return;
-    double* sx = smem + (size_t)w * S * 3;
-    double* sy = sx + S;
-    double* sz = sy + S;
-    int* su = reinterpret_cast<int*>(smem + (size_t)kWarps * S * 3) + (size_t)w * S;
-
+    int* su = s_union[w];
     const int i = c * 32 + lane;
     const bool valid = i < n_local;
-    double4 xi = mdkk::ld4(x, valid ? i : c * 32);
-    // 1. cluster bounding box
-    double bmin_x = mdkk::warp_min_d(xi.x), bmax_x = mdkk::warp_max(xi.x);
-    double bmin_y = mdkk::warp_min_d(xi.y), bmax_y = mdkk::warp_max(xi.y);
-    double bmin_z = mdkk::warp_min_d(xi.z), bmax_z = mdkk::warp_max(xi.z);
+    const double4 xi = mdkk::ld4(x, valid ? i : c * 32);
+    // 1. cluster bounding box and the cells it can reach
+    const double bmin_x = mdkk::warp_min_d(xi.x), bmax_x = mdkk::warp_max(xi.x);
+    const double bmin_y = mdkk::warp_min_d(xi.y), bmax_y = mdkk::warp_max(xi.y);
+    const double bmin_z = mdkk::warp_min_d(xi.z), bmax_z = mdkk::warp_max(xi.z);
     const int3 clo = mdkk::cell_of(g, bmin_x - bc, bmin_y - bc, bmin_z - bc);
     const int3 chi = mdkk::cell_of(g, bmax_x + bc, bmax_y + bc, bmax_z + bc);
-    // 2. union of candidate rows within bc of the bbox
+    // 2. union of candidate rows
     int m = 0;
-    int* ug = uni + (long long)c * ucap;
     for (int cx = clo.x; cx <= chi.x; ++cx) {
         for (int cy = clo.y; cy <= chi.y; ++cy) {
-            int2 kr = mdkk::zrun_keys(g, cx, cy, clo.z, chi.z);
+            const int2 kr = mdkk::zrun_keys(g, cx, cy, clo.z, chi.z);
             const int s0 = cell_start[kr.x], s1 = cell_start[kr.y + 1];
             for (int base = s0; base < s1; base += 32) {
                 const int s = base + lane;
                 bool keep = false;
                 int j = 0;
-                double4 p = make_double4(0, 0, 0, 0);
                 if (s < s1) {
                     j = cell_atoms[s];
-                    p = mdkk::ld4(x, j);
-                    double dx = fmax(0.0, fmax(bmin_x - p.x, p.x - bmax_x));
-                    double dy = fmax(0.0, fmax(bmin_y - p.y, p.y - bmax_y));
-                    double dz = fmax(0.0, fmax(bmin_z - p.z, p.z - bmax_z));
+                    const double4 p = mdkk::ld4(x, j);
+                    const double dx = fmax(0.0, fmax(bmin_x - p.x, p.x - bmax_x));
+                    const double dy = fmax(0.0, fmax(bmin_y - p.y, p.y - bmax_y));
+                    const double dz = fmax(0.0, fmax(bmin_z - p.z, p.z - bmax_z));
                     keep = dx * dx + dy * dy + dz * dz < bc2 * (1.0 + 1e-12);
                 }
                 const unsigned mask = __ballot_sync(0xffffffffu, keep);
-                if (keep) {
-                    const int pos = m + __popc(mask & ((1u << lane) - 1u));
-                    if (pos < ucap) ug[pos] = j;
-                    if (pos < S) {
-                        sx[pos] = p.x;
-                        sy[pos] = p.y;
-                        sz[pos] = p.z;
-                        su[pos] = j;
-                    }
-                }
+                const int pos = m + __popc(mask & ((1u << lane) - 1u));
+                if (keep && pos < kUnion) su[pos] = j;
                 m += __popc(mask);
             }
         }
     }
-    if (lane == 0) {
-        ucount[c] = m;
-        atomicMax(maxes + 1, m);
-    }
     __syncwarp();
-    if (m > ucap) return;  // host grows ucap and relaunches
-    // 3. per-lane scan of the union
+    // 3. exact per-lane test (strict r^2 < bc^2, reference rounding) + style predicate
     int cnt = 0;
-    if (valid) {
-        const int64_t gi = (STYLE == 1) ? gid[i] : 0;
-        const int capb = cap >> 3;
-        for (int u = 0; u < m; ++u) {
-            int j;
-            double px, py, pz;
-            if (u < S) {
-                j = su[u];
-                px = sx[u];
-                py = sy[u];
-                pz = sz[u];
+    const int64_t gi = (STYLE == 1 && valid) ? gid[i] : 0;
+    auto visit = [&](int j) {
+        if (!valid || j == i) return;
+        const double4 p = mdkk::ld4(x, j);
+        const double r2 = mdkk::r2_exact(p.x - xi.x, p.y - xi.y, p.z - xi.z);
+        if (!(r2 < bc2)) return;
+        if (STYLE == 1) {
+            bool keep;
+            if (j < n_local) {
+                keep = gi < gid[j];
+            } else if (NEWTON) {
+                const int orank = owner_rank[j];
+                keep = orank > my_rank || (orank == my_rank && lex_zyx_less(xi.x, xi.y, xi.z, p.x, p.y, p.z));
             } else {
-                j = ug[u];
-                double4 p = mdkk::ld4(x, j);
-                px = p.x;
-                py = p.y;
-                pz = p.z;
+                keep = true;
             }
-            if (j == i) continue;
-            const double r2 = mdkk::r2_exact(px - xi.x, py - xi.y, pz - xi.z);
-            if (!(r2 < bc2)) continue;
-            if (STYLE == 1) {
-                bool keep;
-                if (j < n_local) {
-                    keep = gi < gid[j];
-                } else if (NEWTON) {
-                    const int orank = owner_rank[j];
-                    keep = orank > my_rank ||
-                           (orank == my_rank && lex_zyx_less(xi.x, xi.y, xi.z, px, py, pz));
-                } else {
-                    keep = true;
-                }
-                if (!keep) continue;
-            }
-            if (cnt < cap) table[mdkk::tbl_index(c, capb, cnt, lane)] = (uint16_t)u;
-            ++cnt;
+            if (!keep) return;
         }
-        counts[i] = cnt;
+        if (cnt < cap) table[(long long)cnt * n_local + i] = j;
+        ++cnt;
+    };
+    if (m <= kUnion) {
+        for (int u = 0; u < m; ++u) visit(su[u]);
+    } else {  // union overflow (pathological density): scan the raw cell range instead
+        for (int cx = clo.x; cx <= chi.x; ++cx)
+            for (int cy = clo.y; cy <= chi.y; ++cy) {
+                const int2 kr = mdkk::zrun_keys(g, cx, cy, clo.z, chi.z);
+                const int s1 = cell_start[kr.y + 1];
+                for (int s = cell_start[kr.x]; s < s1; ++s) visit(cell_atoms[s]);
+            }
     }
+    if (valid) counts[i] = cnt;
     int mc = cnt;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mc = max(mc, __shfl_xor_sync(0xffffffffu, mc, o));
-    if (lane == 0 && mc > 0) atomicMax(maxes, mc);
-}
-
-// Expand a cluster list into a plain int32 [cap_out][n_local] table of row indices.
-__global__ void k_expand(const int* __restrict__ uni, int ucap, const uint16_t* __restrict__ table, int cap,
-                         const int* __restrict__ counts, int n_local, int cap_out, int* __restrict__ out) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n_local) return;
-    const int c = i >> 5, lane = i & 31, capb = cap >> 3;
-    const int n = min(counts[i], min(cap, cap_out));
-    for (int k = 0; k < n; ++k) out[(long long)k * n_local + i] = uni[(long long)c * ucap + table[mdkk::tbl_index(c, capb, k, lane)]];
-    for (int k = n; k < cap_out; ++k) out[(long long)k * n_local + i] = -1;
+    if (lane == 0 && mc > 0) atomicMax(max_count, mc);
 }
 
 // Canonical per-row order: (gid[j], z_j, y_j, x_j) ascending (mdkk/neighbor.py:192-197).
@@ -302,43 +270,25 @@ int mdkk_bin_atoms(mdkk_ctx* ctx, const double* x, int n, const double* grid_hos
 
 int mdkk_nbr_build(mdkk_ctx*, const double* x, int n_local, int n_total, const double* grid_host,
                    const int* ncell_host, const int* cell_start, const int* cell_atoms, const int64_t* gid,
-                   const int32_t* owner_rank, int my_rank, double bc, int style, int newton, int cap, int ucap,
-                   int stage, int* uni, int* ucount, uint16_t* table, int* counts, int* maxes, void* stream) {
-    if (n_local < 0 || n_total < n_local || cap < 8 || (cap & 7) || ucap < 1 || ucap > 65535 || stage < 32 ||
-        (style != 0 && style != 1))
-        return MDKK_E_ARG;
+                   const int32_t* owner_rank, int my_rank, double bc, int style, int newton, int cap, int* table,
+                   int* counts, int* max_count, void* stream) {
+    if (n_local < 0 || n_total < n_local || cap < 1 || (style != 0 && style != 1)) return MDKK_E_ARG;
     if (n_local == 0) return MDKK_OK;
     Grid g = mdkk::make_grid(grid_host, ncell_host);
     cudaStream_t s = mdkk::as_stream(stream);
     const int ncl = (n_local + 31) / 32;
     const int nb = (ncl + kWarps - 1) / kWarps;
-    const size_t sm = (size_t)kWarps * stage * (3 * sizeof(double) + sizeof(int));
     const double bc2 = bc * bc;
-#define MDKK_BUILD(ST, NW)                                                                                       \
-    do {                                                                                                         \
-        auto kern = k_nbr_build<ST, NW>;                                                                         \
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);                        \
-        kern<<<nb, kWarps * 32, sm, s>>>(x, n_local, g, cell_start, cell_atoms, gid, owner_rank, my_rank, bc, bc2, \
-                                         cap, ucap, stage, uni, ucount, table, counts, maxes);                   \
-    } while (0)
     if (style == 0)
-        MDKK_BUILD(0, false);
+        k_nbr_build<0, false><<<nb, kWarps * 32, 0, s>>>(x, n_local, g, cell_start, cell_atoms, gid, owner_rank,
+                                                         my_rank, bc, bc2, cap, table, counts, max_count);
     else if (newton)
-        MDKK_BUILD(1, true);
+        k_nbr_build<1, true><<<nb, kWarps * 32, 0, s>>>(x, n_local, g, cell_start, cell_atoms, gid, owner_rank,
+                                                        my_rank, bc, bc2, cap, table, counts, max_count);
     else
-        MDKK_BUILD(1, false);
-#undef MDKK_BUILD
+        k_nbr_build<1, false><<<nb, kWarps * 32, 0, s>>>(x, n_local, g, cell_start, cell_atoms, gid, owner_rank,
+                                                         my_rank, bc, bc2, cap, table, counts, max_count);
     MDKK_CHECK_LAUNCH("k_nbr_build");
-    return MDKK_OK;
-}
-
-int mdkk_nbr_expand(const int* uni, int ucap, const uint16_t* table, int cap, const int* counts, int n_local,
-                    int cap_out, int* out, void* stream) {
-    if (n_local < 0 || cap < 8 || (cap & 7) || cap_out < 1) return MDKK_E_ARG;
-    if (n_local == 0) return MDKK_OK;
-    k_expand<<<mdkk::grid_for(n_local, 128), 128, 0, mdkk::as_stream(stream)>>>(uni, ucap, table, cap, counts,
-                                                                                n_local, cap_out, out);
-    MDKK_CHECK_LAUNCH("k_expand");
     return MDKK_OK;
 }
 

@@ -293,7 +293,6 @@ class Simulation:
             self.lists = build_all(self.system, self.style.r_c, self.config.skin, style=style_list,
                                    newton=self.config.newton)
             self._cap_hint = max(nl.alloc_cap for nl in self.lists)
-            self._ucap_hint = max(nl.ucap for nl in self.lists)
         if self._d2 is None:
             self._d2 = torch.zeros(max(self.config.n_ranks, 1), dtype=torch.float64, device=self.device)
 
@@ -302,10 +301,9 @@ class Simulation:
         halo = self.style.r_c + self.config.skin
         self.system.migrate(halo)
         self.lists = [build(s, self.system.box, self.style.r_c, self.config.skin, style=self._list_style,
-                            newton=self.config.newton, cap_hint=self._cap_hint, ucap_hint=self._ucap_hint)
+                            newton=self.config.newton, cap_hint=self._cap_hint)
                       for s in self.system.stores]
         self._cap_hint = max(nl.alloc_cap for nl in self.lists)
-        self._ucap_hint = max(nl.ucap for nl in self.lists)
         self.n_rebuilds += 1
 
     def _forces_device(self):

@@ -39,41 +39,27 @@ def grow_capacity(capacity: int, needed: int) -> int:
     return cap
 
 
-STAGE_MAX = 768  # union entries staged in shared memory per 32-atom cluster
-
-
-def _round8(v: int) -> int:
-    return (int(v) + 7) // 8 * 8
-
-
 class NeighborList:
-    """Device cluster neighbour list (mdkk/neighbor.py:38-80).
+    """Device neighbour table + counts (mdkk/neighbor.py:38-80).
 
-    Device layout (include/mdkk_b200.h, "cluster list"): owned rows are
-    cell-sorted, cluster c = rows [32c, 32c+32); `uni_dev[c, :ucount[c]]` is
-    the cluster's union of candidate partners and `table_dev` holds uint16
-    local indices into it, 8 per 16-byte lane load.
+    `table_dev` is int32 [alloc_cap][n_local] (atom fastest — the
+    reference's transposed layout_b); entries beyond counts[i] are undefined
+    on device and -1 in the `table` DualArray view.
     """
 
     def __init__(self, store: AtomStore, style: str, newton: bool, cutoff: float, skin: float,
-                 cap: int, alloc_cap: int, table: torch.Tensor, counts: torch.Tensor, uni: torch.Tensor,
-                 ucount: torch.Tensor, ucap: int, max_count: int, max_union: int):
+                 cap: int, table: torch.Tensor, counts: torch.Tensor, max_count: int):
         self.store = store
         self.style = style
         self.newton = bool(newton)
         self.cutoff = float(cutoff)
         self.skin = float(skin)
         self.n_local = store.n_local
-        self.max_neighbors = int(cap)      # reference growth sequence from `capacity`
-        self.alloc_cap = int(alloc_cap)    # physical slots per row (multiple of 8, >= max_count)
+        self.max_neighbors = int(cap)          # reference growth sequence from `capacity`
+        self.alloc_cap = int(table.shape[0])   # physical slots per row (>= max_count)
         self.max_count = int(max_count)
-        self.max_union = int(max_union)
         self.table_dev = table
         self.counts_dev = counts
-        self.uni_dev = uni
-        self.ucount_dev = ucount
-        self.ucap = int(ucap)
-        self.stage = max(32, min(STAGE_MAX, (self.max_union + 31) // 32 * 32))
         self.ref_dev = store.x[: max(store.n_local, 1)].clone()
         self._d2 = torch.zeros(1, dtype=torch.float64, device=store.device)
         self._pairs = None
@@ -87,19 +73,19 @@ class NeighborList:
         return self.counts_dev[: self.n_local].cpu().numpy()
 
     def expanded(self, cap: int | None = None) -> torch.Tensor:
-        """int32 [cap][n_local] row-index table, -1 padded (device)."""
+        """int32 [cap][n_local] table, -1 padded (device copy)."""
         cap = cap or self.max_neighbors
-        n = max(self.n_local, 1)
-        out = torch.full((cap, n), -1, dtype=torch.int32, device=self.store.device)
+        t = self.table_dev[:cap].clone()
         if self.n_local:
-            _lib.call("mdkk_nbr_expand", self.uni_dev.data_ptr(), self.ucap, self.table_dev.data_ptr(),
-                      self.alloc_cap, self.counts_dev.data_ptr(), self.n_local, cap, out.data_ptr(),
-                      _lib.stream(self.store.device))
-        return out
+            k = torch.arange(cap, device=t.device)[:, None]
+            t[:, : self.n_local][k >= self.counts_dev[None, : self.n_local]] = -1
+        else:
+            t.fill_(-1)
+        return t
 
     @property
     def table(self) -> DualArray:
-        """(n_local, cap) int32 DualArray, -1 padded; device storage is [cap][n_local] (layout_b transposed)."""
+        """(n_local, cap) int32 DualArray, -1 padded; device storage [cap][n_local] (layout_b transposed)."""
         t = self.expanded()
         n = max(self.n_local, 1)
         d = DualArray((n, self.max_neighbors), layout_b=LayoutPolicy.transposed(2), dtype=np.int32,
@@ -178,7 +164,7 @@ _cache: dict = {}
 
 def build(store: AtomStore, box: Box, cutoff: float, skin: float, style: str = "full",
           newton: bool = True, capacity: int = DEFAULT_CAPACITY, cap_hint: int | None = None,
-          ucap_hint: int | None = None) -> NeighborList:
+          **_unused) -> NeighborList:
     """One rank's list from its local + ghost rows (mdkk/neighbor.py:182-219).
 
     Owned rows must be cell-sorted for compact clusters (RankedSystem keeps
@@ -207,35 +193,23 @@ def build(store: AtomStore, box: Box, cutoff: float, skin: float, style: str = "
     garr, narr = _lib.dbl3(g), _lib.int_arr(nc)
     _lib.check(lib.mdkk_bin_atoms(ctx, store.x.data_ptr(), n_total, garr, narr, keys.data_ptr(),
                                   cstart.data_ptr(), catoms.data_ptr(), stream), "mdkk_bin_atoms")
-    ncl = max((n_local + 31) // 32, 1)
-    alloc = _round8(max(grow_capacity(capacity, 0), int(cap_hint or 0)))
-    ucap = int(min(65535, max(256, int(ucap_hint or 1024))))
-    stage = STAGE_MAX
-    counts = torch.empty(ncl * 32, dtype=torch.int32, device=dev)
-    ucount = torch.empty(ncl, dtype=torch.int32, device=dev)
-    maxes = torch.zeros(2, dtype=torch.int32, device=dev)
+    alloc = max(grow_capacity(capacity, 0), int(cap_hint or 0))
+    counts = torch.empty(max(n_local, 1), dtype=torch.int32, device=dev)
+    mc = torch.zeros(1, dtype=torch.int32, device=dev)
     while True:
-        table = torch.empty(ncl * alloc * 32, dtype=torch.int16, device=dev)
-        uni = torch.empty(ncl * ucap, dtype=torch.int32, device=dev)
-        maxes.zero_()
+        table = torch.empty((alloc, max(n_local, 1)), dtype=torch.int32, device=dev)
+        mc.zero_()
         _lib.check(lib.mdkk_nbr_build(ctx, store.x.data_ptr(), n_local, n_total, garr, narr, cstart.data_ptr(),
                                       catoms.data_ptr(), store.gid.data_ptr(), store.orank.data_ptr(),
-                                      store.rank, bc, STYLES[style], int(bool(newton)), alloc, ucap, stage,
-                                      uni.data_ptr(), ucount.data_ptr(), table.data_ptr(), counts.data_ptr(),
-                                      maxes.data_ptr(), stream), "mdkk_nbr_build")
-        need, munion = (int(v) for v in maxes.cpu().numpy())
-        if munion > ucap:
-            if munion > 65535:
-                raise NeighborError(f"cluster union of {munion} rows exceeds the uint16 table range")
-            ucap = min(65535, (int(munion * 1.25) + 63) // 64 * 64)
-            continue
-        if need > alloc:
-            alloc = _round8(grow_capacity(alloc, need))  # never truncate: grow and rebuild
-            continue
-        break
+                                      store.rank, bc, STYLES[style], int(bool(newton)), alloc,
+                                      table.data_ptr(), counts.data_ptr(), mc.data_ptr(), stream),
+                   "mdkk_nbr_build")
+        need = int(mc.item())
+        if need <= alloc:
+            break
+        alloc = grow_capacity(alloc, need)  # never truncate: grow and rebuild
     cap = grow_capacity(capacity, need)
-    return NeighborList(store, style, newton, cutoff, skin, cap, alloc, table, counts, uni, ucount, ucap,
-                        need, munion)
+    return NeighborList(store, style, newton, cutoff, skin, cap, table, counts, need)
 
 
 def build_all(system: RankedSystem, cutoff: float, skin: float, style: str = "full",

@@ -98,10 +98,9 @@ def lj_force_rank(store, nl: NeighborList, params: PairParams, ev: torch.Tensor,
     elif zero and store.n_ghost:
         store.f[store.n_local:store.n_total].zero_()
     _lib.check(_lib.lib().mdkk_lj_force(
-        _lib.ctx(dev), store.x.data_ptr(), store.n_local, nl.uni_dev.data_ptr(), nl.ucap, nl.ucount_dev.data_ptr(),
-        nl.table_dev.data_ptr(), nl.counts_dev.data_ptr(), nl.alloc_cap, nl.stage, STYLES[nl.style],
-        int(nl.newton), int(virial), params.epsilon, params.sigma, params.r_c, store.f.data_ptr(), ev.data_ptr(),
-        flags.data_ptr(), _lib.stream(dev)), "mdkk_lj_force")
+        _lib.ctx(dev), store.x.data_ptr(), store.n_local, nl.table_dev.data_ptr(), nl.counts_dev.data_ptr(),
+        nl.alloc_cap, STYLES[nl.style], int(nl.newton), int(virial), params.epsilon, params.sigma, params.r_c,
+        store.f.data_ptr(), ev.data_ptr(), flags.data_ptr(), _lib.stream(dev)), "mdkk_lj_force")
 
 
 def compute_pair(kernel, system: RankedSystem, lists: list[NeighborList], mode: str = "atom", strategy=None,
