@@ -12,9 +12,10 @@
  *    name ends in `_host`.  No torch types cross this boundary.
  *  - Positions / forces / velocities are AoS-padded double4 rows
  *    (x, y, z, pad): one 32-byte sector per neighbour gather.
- *  - Neighbour tables are int32 [cap][n_local] (atom index fastest: the
- *    reference's transposed `layout_b`, mdkk/memspace.py:99-100), padded -1
- *    beyond counts[i].
+ *  - Neighbour tables are int32, cluster-blocked [ceil(n_local/32)][cap][32]:
+ *    entry k of row i lives at ((i/32)*cap + k)*32 + i%32 — the reference's
+ *    transposed `layout_b` (atom index fastest, mdkk/memspace.py:99-100)
+ *    tiled by 32 rows so one warp's k-th entries are one 128-byte line.
  *  - `stream` is a cudaStream_t (may be NULL = legacy default stream).
  *  - Every function returns an mdkk_status; calls are asynchronous on
  *    `stream` unless documented otherwise.  No C++ exception crosses the ABI.
@@ -112,8 +113,8 @@ int mdkk_bin_atoms(mdkk_ctx* ctx, const double* x, int n, const double* grid_hos
  * j != i with r^2 < bc^2 (strict; r^2 rounded as the reference's einsum,
  * mdkk/neighbor.py:126) passing the style predicate: style 0 = full; 1 =
  * half with the gid / owner-rank / z-y-x rules (newton on) or ghost pairs on
- * both sides (newton off).  table is int32 [cap][n_local] (atom fastest),
- * entries beyond counts[i] undefined; counts[i] is the true count even when
+ * both sides (newton off).  table is the cluster-blocked int32 layout above
+ * (ceil(n_local/32)*cap*32 ints), entries beyond counts[i] undefined; counts[i] is the true count even when
  * > cap and *max_count (device int, caller-zeroed) the max, so the caller
  * grows cap x1.5 and relaunches — never truncates (mdkk/neighbor.py:199-205). */
 int mdkk_nbr_build(mdkk_ctx* ctx, const double* x, int n_local, int n_total,
@@ -122,14 +123,15 @@ int mdkk_nbr_build(mdkk_ctx* ctx, const double* x, int n_local, int n_total,
                    double bc, int style, int newton, int cap, int* table, int* counts, int* max_count,
                    void* stream);
 /* Canonical per-row order (partner gid, z, y, x) — mdkk/neighbor.py:192-197.
- * In-place sort of each row of a [cap][n_local] table. */
+ * In-place sort of each row of a plain [cap][n_local] table (the host API
+ * transposes the cluster-blocked table into this form first). */
 int mdkk_nbr_canonicalize(const double* x, const int64_t* gid, int n_local, int cap,
                           int* table, const int* counts, void* stream);
 /* max_i |x_i - x_ref_i|^2 into *out (device double) — mdkk/neighbor.py:66-74. */
 int mdkk_max_disp2(const double* x, const double* x_ref, int n, double* out, void* stream);
 
 /* --------------------------------------------------------------------- LJ
- * Truncated 12-6 LJ (mdkk/pair_lj.py:81-91) over a [cap][n_local] table
+ * Truncated 12-6 LJ (mdkk/pair_lj.py:81-91) over a cluster-blocked table
  * (compute_pair, mdkk/pair_lj.py:114-179).  style/newton select the entry
  * semantics of mdkk/neighbor.py:134-179:
  *   full          : f_i only, weight 1/2, no atomics (owner writes)

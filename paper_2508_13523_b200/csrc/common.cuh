@@ -32,21 +32,24 @@ inline int grid_for(long long n, int block, int max_blocks = 1 << 30) {
     return static_cast<int>(g);
 }
 
-// AoS-padded double4 row access as two 16-byte vector loads.
-__device__ __forceinline__ double4 ld4(const double* p, long long i) {
-    const double2* q = reinterpret_cast<const double2*>(p + 4 * i);
-    double2 a = __ldg(q), b = __ldg(q + 1);
-    return make_double4(a.x, a.y, b.x, b.y);
+// AoS-padded double4 row access: one 256-bit load per row (sm_100
+// LDG.E.ENL2.256), i.e. one 32-byte sector per neighbour gather.
+__device__ __forceinline__ double4 ld4(const double* p, long long i) {  // read-only in this kernel
+    double4 v;
+    asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p + 4 * i));
+    return v;
 }
-__device__ __forceinline__ double4 ld4_nc(const double* p, long long i) {  // mutable data
-    const double2* q = reinterpret_cast<const double2*>(p + 4 * i);
-    double2 a = q[0], b = q[1];
-    return make_double4(a.x, a.y, b.x, b.y);
+__device__ __forceinline__ double4 ld4_nc(const double* p, long long i) {  // data this kernel may write
+    double4 v;
+    asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
+                 : "l"(p + 4 * i)
+                 : "memory");
+    return v;
 }
 __device__ __forceinline__ void st4(double* p, long long i, double4 v) {
-    double2* q = reinterpret_cast<double2*>(p + 4 * i);
-    q[0] = make_double2(v.x, v.y);
-    q[1] = make_double2(v.z, v.w);
+    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p + 4 * i), "d"(v.x), "d"(v.y), "d"(v.z), "d"(v.w)
+                 : "memory");
 }
 
 // r^2 with explicit rounding and no FMA contraction.  The reference evaluates

@@ -3,7 +3,8 @@
 // (engine: weights, partner writes, 6-virial).
 //
 // One thread per owned atom (rows cell-sorted, so a warp's partners overlap
-// and the double4 gathers hit L1); table reads are coalesced (atom fastest).
+// and the 256-bit double4 gathers hit L1); the cluster-blocked table
+// [ncl][cap][32] makes every per-k read one coalesced 128-byte line.
 // full          : owner writes f_i (no atomics); energy/virial weight 1/2 per entry
 // half, newton  : f_i in registers, f_j via FP64 RED atomics; ghosts folded by reverse comm
 // half, !newton : f_j written only for local j; ghost entries weight 1/2
@@ -27,11 +28,11 @@ __global__ void __launch_bounds__(kBlock) k_lj(const double* __restrict__ x, int
         const int n = min(counts[i], cap);
         double fx = 0.0, fy = 0.0, fz = 0.0;
         bool bad = false;
-        const int* col = table + i;
+        const int* col = table + ((long long)(i >> 5) * cap) * 32 + (i & 31);
         int j_next = n > 0 ? __ldg(col) : 0;
         for (int k = 0; k < n; ++k) {
             const int j = j_next;
-            if (k + 1 < n) j_next = __ldg(col + (long long)(k + 1) * n_local);
+            if (k + 1 < n) j_next = __ldg(col + (long long)(k + 1) * 32);
             const double4 xj = mdkk::ld4(x, j);
             const double dx = xj.x - xi.x, dy = xj.y - xi.y, dz = xj.z - xi.z;
             const double r2 = mdkk::r2_exact(dx, dy, dz);

@@ -8,7 +8,7 @@
 //   3. each lane scans the union (broadcast loads: one wavefront per candidate
 //      per warp) and keeps j != i with r^2 < bc^2 (strict, same rounding as
 //      the reference) passing the style predicate (mdkk/neighbor.py:134-179).
-// Output: int32 table [cap][n_local] (atom fastest) of row indices + counts.
+// Output: int32 cluster-blocked table [ncl][cap][32] of row indices + counts.
 #include <cub/device/device_scan.cuh>
 
 #include "cluster.cuh"
@@ -71,12 +71,14 @@ __device__ __forceinline__ bool lex_zyx_less(double ax, double ay, double az, do
 }
 
 constexpr int kWarps = 4;
-constexpr int kUnion = 1024;  // candidate indices staged per cluster (4 KB of shared memory per warp)
+constexpr int kUnion = 1024;  // candidate indices per cluster in shared memory (4 KB per warp)
+constexpr int kChunk = 64;    // candidate positions staged per pass (1.5 KB per warp)
 
 // One warp per 32-atom cluster of cell-sorted owned rows.  The union pass
 // collects every row within bc of the cluster's bounding box (a superset of
-// each lane's partners); the scan then reads each candidate once per warp
-// through a broadcast load while every lane tests it against its own atom.
+// each lane's partners); the scan stages union positions in shared memory 64
+// at a time (4 independent loads in flight per lane) and every lane tests
+// each staged candidate against its own atom (broadcast reads).
 template <int STYLE, bool NEWTON>
 __global__ void __launch_bounds__(kWarps * 32) k_nbr_build(
     const double* __restrict__ x, int n_local, Grid g, const int* __restrict__ cell_start,
@@ -84,11 +86,15 @@ __global__ void __launch_bounds__(kWarps * 32) k_nbr_build(
     int my_rank, double bc, double bc2, int cap, int* __restrict__ table, int* __restrict__ counts,
     int* __restrict__ max_count) {
     __shared__ int s_union[kWarps][kUnion];
+    __shared__ double s_pos[kWarps][3][kChunk];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int c = blockIdx.x * kWarps + w;
     const int ncl = (n_local + 31) >> 5;
     if (c >= ncl) return;
     int* su = s_union[w];
+    double* spx = s_pos[w][0];
+    double* spy = s_pos[w][1];
+    double* spz = s_pos[w][2];
     const int i = c * 32 + lane;
     const bool valid = i < n_local;
     const double4 xi = mdkk::ld4(x, valid ? i : c * 32);
@@ -127,10 +133,10 @@ __global__ void __launch_bounds__(kWarps * 32) k_nbr_build(
     // 3. exact per-lane test (strict r^2 < bc^2, reference rounding) + style predicate
     int cnt = 0;
     const int64_t gi = (STYLE == 1 && valid) ? gid[i] : 0;
-    auto visit = [&](int j) {
+    int* trow = table + ((long long)c * cap) * 32 + lane;
+    auto visit = [&](int j, double px, double py, double pz) {
         if (!valid || j == i) return;
-        const double4 p = mdkk::ld4(x, j);
-        const double r2 = mdkk::r2_exact(p.x - xi.x, p.y - xi.y, p.z - xi.z);
+        const double r2 = mdkk::r2_exact(px - xi.x, py - xi.y, pz - xi.z);
         if (!(r2 < bc2)) return;
         if (STYLE == 1) {
             bool keep;
@@ -138,23 +144,38 @@ __global__ void __launch_bounds__(kWarps * 32) k_nbr_build(
                 keep = gi < gid[j];
             } else if (NEWTON) {
                 const int orank = owner_rank[j];
-                keep = orank > my_rank || (orank == my_rank && lex_zyx_less(xi.x, xi.y, xi.z, p.x, p.y, p.z));
+                keep = orank > my_rank || (orank == my_rank && lex_zyx_less(xi.x, xi.y, xi.z, px, py, pz));
             } else {
                 keep = true;
             }
             if (!keep) return;
         }
-        if (cnt < cap) table[(long long)cnt * n_local + i] = j;
+        if (cnt < cap) trow[(long long)cnt * 32] = j;
         ++cnt;
     };
     if (m <= kUnion) {
-        for (int u = 0; u < m; ++u) visit(su[u]);
+        for (int u0 = 0; u0 < m; u0 += kChunk) {
+            const int cn = min(kChunk, m - u0);
+            for (int t = lane; t < cn; t += 32) {
+                const double4 p = mdkk::ld4(x, su[u0 + t]);
+                spx[t] = p.x;
+                spy[t] = p.y;
+                spz[t] = p.z;
+            }
+            __syncwarp();
+            for (int t = 0; t < cn; ++t) visit(su[u0 + t], spx[t], spy[t], spz[t]);
+            __syncwarp();
+        }
     } else {  // union overflow (pathological density): scan the raw cell range instead
         for (int cx = clo.x; cx <= chi.x; ++cx)
             for (int cy = clo.y; cy <= chi.y; ++cy) {
                 const int2 kr = mdkk::zrun_keys(g, cx, cy, clo.z, chi.z);
                 const int s1 = cell_start[kr.y + 1];
-                for (int s = cell_start[kr.x]; s < s1; ++s) visit(cell_atoms[s]);
+                for (int s = cell_start[kr.x]; s < s1; ++s) {
+                    const int j = cell_atoms[s];
+                    const double4 p = mdkk::ld4(x, j);
+                    visit(j, p.x, p.y, p.z);
+                }
             }
     }
     if (valid) counts[i] = cnt;

@@ -42,9 +42,10 @@ def grow_capacity(capacity: int, needed: int) -> int:
 class NeighborList:
     """Device neighbour table + counts (mdkk/neighbor.py:38-80).
 
-    `table_dev` is int32 [alloc_cap][n_local] (atom fastest — the
-    reference's transposed layout_b); entries beyond counts[i] are undefined
-    on device and -1 in the `table` DualArray view.
+    `table_dev` is int32 cluster-blocked [ceil(n_local/32)][alloc_cap][32]
+    (atom fastest within 32-row tiles — the reference's transposed layout_b);
+    entries beyond counts[i] are undefined on device and -1 in the `table`
+    DualArray view.
     """
 
     def __init__(self, store: AtomStore, style: str, newton: bool, cutoff: float, skin: float,
@@ -56,7 +57,7 @@ class NeighborList:
         self.skin = float(skin)
         self.n_local = store.n_local
         self.max_neighbors = int(cap)          # reference growth sequence from `capacity`
-        self.alloc_cap = int(table.shape[0])   # physical slots per row (>= max_count)
+        self.alloc_cap = int(table.shape[1])   # physical slots per row (>= max_count)
         self.max_count = int(max_count)
         self.table_dev = table
         self.counts_dev = counts
@@ -75,7 +76,9 @@ class NeighborList:
     def expanded(self, cap: int | None = None) -> torch.Tensor:
         """int32 [cap][n_local] table, -1 padded (device copy)."""
         cap = cap or self.max_neighbors
-        t = self.table_dev[:cap].clone()
+        ncl = self.table_dev.shape[0]
+        t = self.table_dev.permute(1, 0, 2).reshape(self.alloc_cap, ncl * 32)[:cap, : max(self.n_local, 1)]
+        t = t.contiguous()
         if self.n_local:
             k = torch.arange(cap, device=t.device)[:, None]
             t[:, : self.n_local][k >= self.counts_dev[None, : self.n_local]] = -1
@@ -197,7 +200,7 @@ def build(store: AtomStore, box: Box, cutoff: float, skin: float, style: str = "
     counts = torch.empty(max(n_local, 1), dtype=torch.int32, device=dev)
     mc = torch.zeros(1, dtype=torch.int32, device=dev)
     while True:
-        table = torch.empty((alloc, max(n_local, 1)), dtype=torch.int32, device=dev)
+        table = torch.empty(((n_local + 31) // 32 or 1, alloc, 32), dtype=torch.int32, device=dev)
         mc.zero_()
         _lib.check(lib.mdkk_nbr_build(ctx, store.x.data_ptr(), n_local, n_total, garr, narr, cstart.data_ptr(),
                                       catoms.data_ptr(), store.gid.data_ptr(), store.orank.data_ptr(),
