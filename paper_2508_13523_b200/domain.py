@@ -121,24 +121,29 @@ def decompose(box: Box, n_ranks: int) -> RankSet:
     return RankSet(box, best[1])
 
 
-def _rows4(n: int, device) -> torch.Tensor:
-    return torch.zeros((max(n, 1), 4), dtype=torch.float64, device=device)
+def _rows4(n: int, device, zero: bool = True) -> torch.Tensor:
+    t = torch.empty((max(n, 1), 4), dtype=torch.float64, device=device)
+    return t.zero_() if zero else t
 
 
-def _to4(a: np.ndarray, device) -> torch.Tensor:
-    t = _rows4(len(a), device)
+def _to4(a: np.ndarray, device, cap: int | None = None) -> torch.Tensor:
+    t = _rows4(max(cap or 0, len(a)), device)
     if len(a):
         t[: len(a), :3] = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(device)
     return t
 
 
+_ROW = None
+
+
 class AtomStore:
     """One rank's rows in HBM: n_local owned rows followed by n_ghost ghosts (mdkk/domain.py:126-193).
 
-    Device tensors: ``x``/``f`` (n_total, 4) f64, ``v`` (n_local, 4) f64,
-    ``gid`` int64, ``orank``/``oidx`` int32 per row, ``gcode`` int8 shift code
-    per ghost.  ``pos``/``vel``/``force`` are DualArray views over them
-    (space "a" = host numpy, "b" = these tensors).
+    Device buffers have spare capacity so rebuilds reuse them: ``x``/``f``
+    (cap, 4) f64, ``gid`` int64, ``orank``/``oidx`` int32 per row, ``v``
+    (cap_local, 4).  Rows [0, n_total) are valid.  ``pos``/``vel``/``force``
+    are DualArray views over the valid rows (space "a" = host numpy,
+    "b" = HBM), following the reference's protocol (mdkk/memspace.py:77-156).
     """
 
     def __init__(self, rank: int, device, x: torch.Tensor, v: torch.Tensor, gid: torch.Tensor, n_local: int):
@@ -146,24 +151,48 @@ class AtomStore:
         self.device = torch.device(device)
         self.n_local = int(n_local)
         self.n_ghost = 0
-        self.gid = gid
-        self.orank = torch.full((max(n_local, 1),), self.rank, dtype=torch.int32, device=self.device)
-        self.oidx = torch.arange(max(n_local, 1), dtype=torch.int32, device=self.device)
-        self.gcode = torch.zeros(0, dtype=torch.int8, device=self.device)
-        self._adopt(x, v, torch.zeros_like(x))
+        self.x, self.v, self.gid = x, v, gid
+        cap = x.shape[0]
+        if gid.shape[0] < cap:
+            g = torch.empty(cap, dtype=torch.int64, device=self.device)
+            g[: gid.shape[0]] = gid
+            self.gid = g
+        self.f = torch.zeros_like(x)
+        self.orank = torch.full((cap,), self.rank, dtype=torch.int32, device=self.device)
+        self.oidx = torch.arange(cap, dtype=torch.int32, device=self.device)
         self.lo = self.hi = None  # brick bounds, set by RankedSystem
+        self._lengths = None
+        self._lanes_in = []       # lanes whose ghost rows live here (for ghost_shift)
+        self._alt = None          # double buffers for the spatial sort
+        self._views()
+
+    @property
+    def capacity(self) -> int:
+        return self.x.shape[0]
+
+    def _views(self):
+        nt = max(self.n_total, 1)
+        self.pos = DualArray((nt, 3), device=self.device, pad_last=4, storage_b=self.x[:nt], layout_b=_ROW)
+        self.vel = DualArray((max(self.n_local, 1), 3), device=self.device, pad_last=4,
+                             storage_b=self.v[: max(self.n_local, 1)], layout_b=_ROW)
+        self.force = DualArray((nt, 3), device=self.device, pad_last=4, storage_b=self.f[:nt], layout_b=_ROW)
         self._host_cache = {}
 
-    # -- DualArray plumbing (mdkk/memspace.py protocol) ----------------------
-    def _adopt(self, x, v, f):
-        self.x, self.v, self.f = x, v, f
-        nt = max(self.n_total, 1)
-        self.pos = DualArray((nt, 3), device=self.device, pad_last=4, storage_b=x,
-                             layout_b=_ROW)
-        self.vel = DualArray((max(self.n_local, 1), 3), device=self.device, pad_last=4, storage_b=v,
-                             layout_b=_ROW)
-        self.force = DualArray((nt, 3), device=self.device, pad_last=4, storage_b=f, layout_b=_ROW)
-        self._host_cache = {}
+    def ensure_capacity(self, rows: int) -> None:
+        """Grow the per-row buffers (keeping owned rows) when `rows` exceeds capacity."""
+        if rows <= self.capacity:
+            return
+        cap = int(rows * 1.15) + 64
+        nl = self.n_local
+        x = _rows4(cap, self.device, zero=False)
+        x[:nl] = self.x[:nl]
+        g = torch.empty(cap, dtype=torch.int64, device=self.device)
+        g[:nl] = self.gid[:nl]
+        self.x, self.gid = x, g
+        self.f = torch.zeros((cap, 4), dtype=torch.float64, device=self.device)
+        self.orank = torch.full((cap,), self.rank, dtype=torch.int32, device=self.device)
+        self.oidx = torch.arange(cap, dtype=torch.int32, device=self.device)
+        self._alt = None
 
     def to_device(self):
         """Make device storage current before a kernel reads it."""
@@ -214,14 +243,12 @@ class AtomStore:
     def ghost_shift(self) -> np.ndarray:
         h = self._host_cache.get("shift")
         if h is None:
-            s = np.zeros((self.n_total, 3))
-            if self.n_ghost:
-                s[self.n_local:] = SHIFT_UNITS[self.gcode.cpu().numpy().astype(np.int64)] * self._lengths
-            h = self._host_cache["shift"] = s
+            h = np.zeros((self.n_total, 3))
+            for ln in self._lanes_in:
+                codes = ln.code.cpu().numpy().astype(np.int64)
+                h[ln.start:ln.start + ln.count] = SHIFT_UNITS[codes] * self._lengths
+            self._host_cache["shift"] = h
         return h
-
-
-_ROW = None  # set below (row-major device layout for (n, 3) padded rows)
 
 
 def _init_layout():
@@ -255,10 +282,20 @@ class RankedSystem:
         self.dense_gids = dense_gids
         self.n_atoms = sum(s.n_local for s in stores)
         self._shift_dev = torch.from_numpy(SHIFT_UNITS * box.lengths).to(self.device)
+        self._combo_cache = {}
+        self._scratch = {}
         self.sort_width = None  # spatial-sort bin width (set by the first neighbour build)
         for s in stores:
-            s.lo, s.hi = rankset.lo[s.rank], rankset.hi[s.rank]
-            s._lengths = box.lengths
+            self._attach(s)
+
+    def _attach(self, s: AtomStore):
+        s.lo, s.hi, s._lengths = self.rankset.lo[s.rank], self.rankset.hi[s.rank], self.box.lengths
+
+    def _buf(self, name, n, dtype):
+        t = self._scratch.get(name)
+        if t is None or t.numel() < n:
+            t = self._scratch[name] = torch.empty(max(int(n * 1.15) + 64, 1), dtype=dtype, device=self.device)
+        return t
 
     @property
     def n_ranks(self) -> int:
@@ -279,18 +316,23 @@ class RankedSystem:
         stores = []
         for r in range(rs.n_ranks):
             sel = np.flatnonzero(owner == r)
-            g = torch.zeros(max(len(sel), 1), dtype=torch.int64, device=device)
+            cap = int(len(sel) * 1.3) + 64   # headroom for ghost rows
+            g = torch.zeros(cap, dtype=torch.int64, device=device)
             if len(sel):
                 g[: len(sel)] = torch.from_numpy(gids[sel]).to(device)
-            stores.append(AtomStore(r, device, _to4(pos[sel], device), _to4(vel[sel], device), g, len(sel)))
+            stores.append(AtomStore(r, device, _to4(pos[sel], device, cap), _to4(vel[sel], device), g, len(sel)))
         return cls(box, rs, stores, device, dense)
 
     # ------------------------------------------------------------ ghosts
     def _combos(self, src: int, halo: float):
-        """(dst, code, lo, hi, shift) combos for src, dst-major then shift order (mdkk/domain.py:263-271)."""
+        """(dst, code) combos for src, dst-major then shift order (mdkk/domain.py:263-271) + device table."""
+        key = (src, halo)
+        hit = self._combo_cache.get(key)
+        if hit is not None:
+            return hit
         L = self.box.lengths
         rs = self.rankset
-        out = []
+        meta, rows = [], []
         for dst in range(self.n_ranks):
             lo, hi = rs.lo[dst] - halo, rs.hi[dst] + halo
             for code in range(27):
@@ -301,11 +343,19 @@ class RankedSystem:
                 slo, shi = rs.lo[src] - halo + shift, rs.hi[src] + halo + shift
                 if np.any(shi <= lo) or np.any(slo >= hi):
                     continue
-                out.append((dst, code, lo, hi, shift))
-        return out
+                meta.append((dst, code))
+                rows.append(np.concatenate([lo, hi, shift]))
+        tab = torch.from_numpy(np.array(rows) if rows else np.zeros((0, 9))).to(self.device)
+        codes = torch.tensor([c for _, c in meta], dtype=torch.int8, device=self.device)
+        hit = self._combo_cache[key] = (meta, tab, codes)
+        return hit
 
     def exchange_ghosts(self, halo: float) -> None:
-        """Select ghosts on device and rebuild ghost rows + lanes (mdkk/domain.py:246-293)."""
+        """Select ghosts on device and rebuild ghost rows + lanes (mdkk/domain.py:246-293).
+
+        One host sync (the per-combo totals); everything else is launched
+        asynchronously into reused buffers.
+        """
         if halo <= 0:
             raise DomainError(f"halo must be positive, got {halo}")
         if halo > 0.5 * self.box.min_periodic_length():
@@ -316,78 +366,70 @@ class RankedSystem:
         ctx = _lib.ctx(self.device)
         for s in self.stores:
             s.to_device()
-        # per src: selected indices per combo
-        sel = {}  # (src, dst) -> list of (code, idx_tensor_view, count)
+        plans = []
         for src in self.stores:
-            combos = self._combos(src.rank, halo)
-            C_ = len(combos)
+            meta, tab, codes = self._combos(src.rank, halo)
+            C_ = len(meta)
             if C_ == 0 or src.n_local == 0:
+                plans.append(None)
                 continue
-            tab = np.array([np.concatenate([lo, hi, sh]) for (_, _, lo, hi, sh) in combos])
-            tab_dev = torch.from_numpy(tab).to(self.device)
             nb = (src.n_local + 255) // 256
-            blk = torch.empty(nb * C_, dtype=torch.int32, device=self.device)
-            tot = torch.empty(C_, dtype=torch.int32, device=self.device)
-            _lib.check(lib.mdkk_halo_count(ctx, src.x.data_ptr(), src.n_local, tab_dev.data_ptr(), C_,
+            blk = self._buf(f"blk{src.rank}", nb * C_, torch.int32)
+            tot = self._buf(f"tot{src.rank}", C_, torch.int32)[:C_]
+            _lib.check(lib.mdkk_halo_count(ctx, src.x.data_ptr(), src.n_local, tab.data_ptr(), C_,
                                            blk.data_ptr(), tot.data_ptr(), stream), "mdkk_halo_count")
-            totals = tot.cpu().numpy()
-            idx = torch.empty(max(int(totals.sum()), 1), dtype=torch.int32, device=self.device)
-            _lib.check(lib.mdkk_halo_fill(ctx, src.x.data_ptr(), src.n_local, tab_dev.data_ptr(), C_,
-                                          blk.data_ptr(), tot.data_ptr(), idx.data_ptr(), stream),
-                       "mdkk_halo_fill")
-            off = 0
-            for (dst, code, _, _, _), t in zip(combos, totals):
-                if t:
-                    sel.setdefault((src.rank, dst), []).append((code, idx[off:off + t], int(t)))
-                off += int(t)
+            plans.append((meta, tab, codes, blk, tot))
+        live = [p for p in plans if p is not None]
+        host_tot = torch.cat([p[4] for p in live]).cpu().numpy() if live else np.zeros(0, np.int64)
+        sel = {}   # (src, dst) -> (idx view, code tensor, count)
+        off_all = 0
+        for src, plan in zip(self.stores, plans):
+            if plan is None:
+                continue
+            meta, tab, codes, blk, tot = plan
+            C_ = len(meta)
+            totals = host_tot[off_all:off_all + C_].astype(np.int64)
+            off_all += C_
+            idx = self._buf(f"idx{src.rank}", int(totals.sum()) + 1, torch.int32)
+            _lib.check(lib.mdkk_halo_fill(ctx, src.x.data_ptr(), src.n_local, tab.data_ptr(), C_, blk.data_ptr(),
+                                          tot.data_ptr(), idx.data_ptr(), stream), "mdkk_halo_fill")
+            # combos are dst-major: each (src, dst) lane is one contiguous run of idx
+            start = np.concatenate([[0], np.cumsum(totals)])
+            d_of = np.array([d for d, _ in meta])
+            for d in np.unique(d_of):
+                ks = np.flatnonzero(d_of == d)
+                a, b = int(start[ks[0]]), int(start[ks[-1] + 1])
+                if b > a:
+                    code = torch.repeat_interleave(codes[ks[0]:ks[-1] + 1], tot[ks[0]:ks[-1] + 1].long(),
+                                                   output_size=b - a)
+                    sel[(src.rank, int(d))] = (idx[a:b], code, b - a)
         self.lanes = []
         for dst in self.stores:
             nl = dst.n_local
-            parts = []
-            for src in range(self.n_ranks):
-                for code, ix, t in sel.get((src, dst.rank), []):
-                    parts.append((src, code, ix, t))
-            ng = sum(p[3] for p in parts)
-            x = _rows4(nl + ng, self.device)
-            x[:nl] = dst.x[:nl]
-            gid = torch.empty(max(nl + ng, 1), dtype=torch.int64, device=self.device)
-            gid[:nl] = dst.gid[:nl]
-            orank = torch.empty(max(nl + ng, 1), dtype=torch.int32, device=self.device)
-            orank[:nl] = self.stores[dst.rank].rank
-            oidx = torch.empty(max(nl + ng, 1), dtype=torch.int32, device=self.device)
-            oidx[:nl] = torch.arange(nl, dtype=torch.int32, device=self.device)
-            codes = np.zeros(ng, dtype=np.int8)
+            ng = sum(sel[(s, dst.rank)][2] for s in range(self.n_ranks) if (s, dst.rank) in sel)
+            dst.ensure_capacity(nl + ng)
+            dst._lanes_in = []
             cur = nl
-            lane_src, lane_start, lane_parts = None, 0, []
-            for src, code, ix, t in parts:
-                codes[cur - nl:cur - nl + t] = code
-                orank[cur:cur + t] = src
-                oidx[cur:cur + t] = ix
-                sst = self.stores[src]
-                _lib.check(lib.mdkk_gather_i64(sst.gid.data_ptr(), ix.data_ptr(), t,
-                                               gid[cur:].data_ptr(), stream), "mdkk_gather_i64")
-                if src != lane_src:
-                    if lane_parts:
-                        self._add_lane(lane_src, dst.rank, lane_parts, lane_start)
-                    lane_src, lane_start, lane_parts = src, cur, []
-                lane_parts.append((code, ix, t))
+            for s in range(self.n_ranks):
+                if (s, dst.rank) not in sel:
+                    continue
+                ix, code, t = sel[(s, dst.rank)]
+                sst = self.stores[s]
+                _lib.check(lib.mdkk_gather_i64(sst.gid.data_ptr(), ix.data_ptr(), t, dst.gid[cur:].data_ptr(),
+                                               stream), "mdkk_gather_i64")
+                dst.orank[cur:cur + t].fill_(s)
+                dst.oidx[cur:cur + t].copy_(ix)
+                ln = _Lane(s, dst.rank, ix, code, cur, t)
+                self.lanes.append(ln)
+                dst._lanes_in.append(ln)
                 cur += t
-            if lane_parts:
-                self._add_lane(lane_src, dst.rank, lane_parts, lane_start)
-            gcode = torch.from_numpy(codes).to(self.device)
-            v = dst.v
             dst.n_ghost = ng
-            dst.gid, dst.orank, dst.oidx, dst.gcode = gid, orank, oidx, gcode
-            dst._adopt(x, v, torch.zeros_like(x))
+            if nl:
+                dst.orank[:nl].fill_(dst.rank)
+            dst._views()
         self._pack_all()
         for s in self.stores:
             s.device_wrote(pos=True)
-
-    def _add_lane(self, src, dst, parts, start):
-        idx = torch.cat([p[1] for p in parts]) if len(parts) > 1 else parts[0][1]
-        count = sum(p[2] for p in parts)
-        code = torch.from_numpy(np.concatenate([np.full(p[2], p[0], np.int8) for p in parts])).to(self.device)
-        self.lanes.append(_Lane(src, dst, idx, code, start, count))
 
     def _pack_all(self):
         lib, stream = _lib.lib(), _lib.stream(self.device)
@@ -434,7 +476,7 @@ class RankedSystem:
         if R > 1:
             parts = {}  # dst -> list of (src, order segment)
             for s in self.stores:
-                keys = torch.empty(max(s.n_local, 1), dtype=torch.int32, device=self.device)
+                keys = self._buf(f"rk{s.rank}", s.n_local + 1, torch.int32)
                 start = torch.empty(R + 1, dtype=torch.int32, device=self.device)
                 order = torch.empty(max(s.n_local, 1), dtype=torch.int32, device=self.device)
                 _lib.check(lib.mdkk_rank_keys(s.x.data_ptr(), s.n_local, L, grid, keys.data_ptr(), stream),
@@ -449,8 +491,9 @@ class RankedSystem:
             for d in range(R):
                 segs = parts.get(d, [])
                 n = sum(p[2] for p in segs)
-                x, v = _rows4(n, self.device), _rows4(n, self.device)
-                gid = torch.zeros(max(n, 1), dtype=torch.int64, device=self.device)
+                cap = int(n * 1.3) + 64
+                x, v = _rows4(cap, self.device), _rows4(n, self.device)
+                gid = torch.zeros(cap, dtype=torch.int64, device=self.device)
                 cur = 0
                 for s, o, c in segs:
                     _lib.check(lib.mdkk_gather_rows4(s.x.data_ptr(), o.data_ptr(), c, x[cur:].data_ptr(), stream), "g4")
@@ -458,54 +501,59 @@ class RankedSystem:
                     _lib.check(lib.mdkk_gather_i64(s.gid.data_ptr(), o.data_ptr(), c, gid[cur:].data_ptr(), stream), "g64")
                     cur += c
                 st = AtomStore(d, self.device, x, v, gid, n)
-                st.lo, st.hi, st._lengths = self.rankset.lo[d], self.rankset.hi[d], self.box.lengths
+                self._attach(st)
                 new.append(st)
             self.stores = new
         else:
             s = self.stores[0]
-            st = AtomStore(0, self.device, s.x[: max(s.n_local, 1)].clone(), s.v, s.gid[: max(s.n_local, 1)].clone(),
-                           s.n_local)
-            st.lo, st.hi, st._lengths = s.lo, s.hi, s._lengths
-            self.stores = [st]
+            s.n_ghost = 0
+            s._lanes_in = []
         w = sort_width or self.sort_width
         if w:
             for s in self.stores:
                 self._spatial_sort(s, w, halo)
         for s in self.stores:
+            s.n_ghost = 0
+            s._views()
             s.device_wrote(pos=True, vel=True, force=True)
         self.exchange_ghosts(halo)
+        for s in self.stores:   # the reference resets forces at migration (new AtomStores)
+            s.f[: s.n_total].zero_()
 
     def sort_local(self, width: float) -> None:
         """Re-order every rank's owned rows into serpentine cell order (drops ghosts; call before exchange)."""
         for s in self.stores:
             s.to_device()
             s.n_ghost = 0
+            s._lanes_in = []
             self._spatial_sort(s, width, width)
+            s._views()
             s.device_wrote(pos=True, vel=True, force=True)
         self.lanes = []
 
     def _spatial_sort(self, s: AtomStore, width: float, halo: float):
-        """Reorder owned rows by cell so neighbour gathers are local (rows are re-indexed, gids travel)."""
+        """Reorder owned rows by cell (double-buffered) so neighbour gathers are local; gids travel."""
         if s.n_local < 2:
             return
         lib, stream = _lib.lib(), _lib.stream(self.device)
         ctx = _lib.ctx(self.device)
         g, nc = cell_grid(s.lo, s.hi, halo, width)
         ncell = nc[0] * nc[1] * nc[2]
-        keys = torch.empty(s.n_local, dtype=torch.int32, device=self.device)
-        start = torch.empty(ncell + 1, dtype=torch.int32, device=self.device)
-        order = torch.empty(s.n_local, dtype=torch.int32, device=self.device)
-        _lib.check(lib.mdkk_bin_atoms(ctx, s.x.data_ptr(), s.n_local, _lib.dbl3(g), _lib.int_arr(nc),
+        n = s.n_local
+        keys = self._buf(f"sk{s.rank}", n, torch.int32)
+        start = self._buf(f"ss{s.rank}", ncell + 1, torch.int32)
+        order = self._buf(f"so{s.rank}", n, torch.int32)
+        _lib.check(lib.mdkk_bin_atoms(ctx, s.x.data_ptr(), n, _lib.dbl3(g), _lib.int_arr(nc),
                                       keys.data_ptr(), start.data_ptr(), order.data_ptr(), stream), "bin")
-        x, v = _rows4(s.n_local, self.device), _rows4(s.n_local, self.device)
-        gid = torch.empty(s.n_local, dtype=torch.int64, device=self.device)
-        _lib.check(lib.mdkk_gather_rows4(s.x.data_ptr(), order.data_ptr(), s.n_local, x.data_ptr(), stream), "g4")
-        _lib.check(lib.mdkk_gather_rows4(s.v.data_ptr(), order.data_ptr(), s.n_local, v.data_ptr(), stream), "g4")
-        _lib.check(lib.mdkk_gather_i64(s.gid.data_ptr(), order.data_ptr(), s.n_local, gid.data_ptr(), stream), "g64")
-        s.gid = gid
-        s.orank = torch.full((s.n_local,), s.rank, dtype=torch.int32, device=self.device)
-        s.oidx = torch.arange(s.n_local, dtype=torch.int32, device=self.device)
-        s._adopt(x, v, torch.zeros_like(x))
+        if s._alt is None or s._alt[0].shape[0] != s.capacity or s._alt[1].shape[0] < n:
+            s._alt = (_rows4(s.capacity, self.device, zero=False), _rows4(s.v.shape[0], self.device, zero=False),
+                      torch.empty(s.capacity, dtype=torch.int64, device=self.device))
+        x2, v2, g2 = s._alt
+        _lib.check(lib.mdkk_gather_rows4(s.x.data_ptr(), order.data_ptr(), n, x2.data_ptr(), stream), "g4")
+        _lib.check(lib.mdkk_gather_rows4(s.v.data_ptr(), order.data_ptr(), n, v2.data_ptr(), stream), "g4")
+        _lib.check(lib.mdkk_gather_i64(s.gid.data_ptr(), order.data_ptr(), n, g2.data_ptr(), stream), "g64")
+        s._alt = (s.x, s.v, s.gid)
+        s.x, s.v, s.gid = x2, v2, g2
 
     # -------------------------------------------------------------- gather
     def _gid_order(self, rows_fn, width):
