@@ -87,6 +87,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_nbr_build(
     int* __restrict__ max_count) {
     __shared__ int s_union[kWarps][kUnion];
     __shared__ double s_pos[kWarps][3][kChunk];
+    __shared__ float s_rel[kWarps][3][kChunk];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int c = blockIdx.x * kWarps + w;
     const int ncl = (n_local + 31) >> 5;
@@ -95,6 +96,9 @@ __global__ void __launch_bounds__(kWarps * 32) k_nbr_build(
     double* spx = s_pos[w][0];
     double* spy = s_pos[w][1];
     double* spz = s_pos[w][2];
+    float* sfx = s_rel[w][0];
+    float* sfy = s_rel[w][1];
+    float* sfz = s_rel[w][2];
     const int i = c * 32 + lane;
     const bool valid = i < n_local;
     const double4 xi = mdkk::ld4(x, valid ? i : c * 32);
@@ -130,7 +134,14 @@ __global__ void __launch_bounds__(kWarps * 32) k_nbr_build(
         }
     }
     __syncwarp();
-    // 3. exact per-lane test (strict r^2 < bc^2, reference rounding) + style predicate
+    // 3. per-lane test: FP32 prefilter on cluster-relative coordinates (rejects
+    //    ~85% of candidates at twice the FP64 rate), then the exact FP64 test
+    //    (strict r^2 < bc^2, reference rounding) + style predicate.
+    const double ccx = 0.5 * (bmin_x + bmax_x), ccy = 0.5 * (bmin_y + bmax_y), ccz = 0.5 * (bmin_z + bmax_z);
+    const float fxi = (float)(xi.x - ccx), fyi = (float)(xi.y - ccy), fzi = (float)(xi.z - ccz);
+    // margin >> FP32 rounding: |r2_f - r2| <~ 6 eps_f D^2 with D the farthest cluster-relative coordinate
+    const double hx = 0.5 * (bmax_x - bmin_x) + bc, hy = 0.5 * (bmax_y - bmin_y) + bc, hz = 0.5 * (bmax_z - bmin_z) + bc;
+    const float bc2f = (float)(bc2 * (1.0 + 1e-4) + 4e-6 * (hx * hx + hy * hy + hz * hz));
     int cnt = 0;
     const int64_t gi = (STYLE == 1 && valid) ? gid[i] : 0;
     int* trow = table + ((long long)c * cap) * 32 + lane;
@@ -161,9 +172,15 @@ __global__ void __launch_bounds__(kWarps * 32) k_nbr_build(
                 spx[t] = p.x;
                 spy[t] = p.y;
                 spz[t] = p.z;
+                sfx[t] = (float)(p.x - ccx);
+                sfy[t] = (float)(p.y - ccy);
+                sfz[t] = (float)(p.z - ccz);
             }
             __syncwarp();
-            for (int t = 0; t < cn; ++t) visit(su[u0 + t], spx[t], spy[t], spz[t]);
+            for (int t = 0; t < cn; ++t) {
+                const float dx = sfx[t] - fxi, dy = sfy[t] - fyi, dz = sfz[t] - fzi;
+                if (dx * dx + dy * dy + dz * dz < bc2f) visit(su[u0 + t], spx[t], spy[t], spz[t]);
+            }
             __syncwarp();
         }
     } else {  // union overflow (pathological density): scan the raw cell range instead
