@@ -537,7 +537,7 @@ class RankedSystem:
             return
         lib, stream = _lib.lib(), _lib.stream(self.device)
         ctx = _lib.ctx(self.device)
-        g, nc = cell_grid(s.lo, s.hi, halo, width)
+        g, nc = cell_grid(s.lo, s.hi, 0.0, width)   # bins tile the brick exactly: full cells everywhere
         ncell = nc[0] * nc[1] * nc[2]
         n = s.n_local
         keys = self._buf(f"sk{s.rank}", n, torch.int32)
