@@ -158,6 +158,35 @@ int mdkk_verlet_second(mdkk_ctx* ctx, double* v, const double* f, int n, double 
 /* Sum of 1/2 m |v|^2 over n rows into *ke (device double). */
 int mdkk_kinetic(mdkk_ctx* ctx, const double* v, int n, double mass, double* ke, void* stream);
 
+/* ------------------------------------------------------------------- SNAP
+ * FP64 descriptor pipeline with mdkk's conventions (mdkk/snap/compute.py:
+ * rfac0 0.99, rmin0 0, cosine switch, no self term, full (2j+1)^2 blocks,
+ * full three-slot adjoint).  U, Y are complex128 [n_flat][n_local] (atom
+ * fastest, the reference's layout "b"); n_flat = sum_{tj<=2J} (tj+1)^2.
+ * Pairs are the entries of a FULL cluster-blocked table with r^2 < rc^2.
+ *
+ * mdkk_snap_create copies the output-sorted adjoint contribution list
+ *   Y[f] = sum_{k in [f_start[f], f_start[f+1])} coef[k] * op(U[g[k]]) * U[h[k]],
+ *   op = conj when conj[k] != 0   (mdkk/snap/compute.py:303-340)
+ * built on the host from the exact Clebsch-Gordan terms and beta
+ * (mdkk/snap/coupling.py:106-133); 0 <= 2J <= 8. */
+int mdkk_snap_create(mdkk_ctx* ctx, int twojmax, int n_contrib, const int* f_start_host, const int* g_host,
+                     const int* h_host, const int* conj_host, const double* coef_host, mdkk_snap** out_host);
+int mdkk_snap_destroy(mdkk_snap* snap);
+/* U_i = sum_k f_c(r_ik) u(a_ik, b_ik) (compute_ui, mdkk/snap/compute.py:279-292); flags gets
+ * MDKK_FLAG_COINCIDENT for r = 0 pairs (mdkk/snap/compute.py:117-118). */
+int mdkk_snap_ui(mdkk_snap* snap, const double* x, int n_local, const int* table, const int* counts, int cap,
+                 double rc, double* U, int* flags, void* stream);
+/* Y from U (compute_yi) and *energy (device double) = sum_i Re(Y_i . conj(U_i)) / 3
+ * (energy_from_y, mdkk/snap/compute.py:376-387). */
+int mdkk_snap_yi(mdkk_ctx* ctx, mdkk_snap* snap, const double* U, int n_local, double* Y, double* energy,
+                 void* stream);
+/* Fused 3-direction forces (compute_fused_deidrj, mdkk/snap/compute.py:390-409):
+ * t = Re sum_f Y_i[f] conj(d(f_c u)/d r_ik [f]); f_i += t, f_k -= t (FP64
+ * atomics, f double4 rows incl. ghosts, caller-zeroed; ghosts -> reverse comm). */
+int mdkk_snap_deidrj(mdkk_snap* snap, const double* x, int n_local, const int* table, const int* counts, int cap,
+                     double rc, const double* Y, double* f, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,168 @@
+"""Quantum indexing and Clebsch-Gordan coupling tables (host-side setup, uploaded once).
+
+Mirror of mdkk/snap/indexing.py:24-68 and mdkk/snap/coupling.py:28-137:
+doubled-integer angular momenta, flat (tj, p, q) index with tj slowest,
+coupled triples (tj, tj1, tj2) with tj2 <= tj1 <= tj, exact-rational CG with a
+single final rounding, and per-triple (iz, iu1, iu2, coeff) term lists.  The
+device consumes an output-sorted "contribution" list for the full three-slot
+adjoint (mdkk/snap/compute.py:303-340) built by `adjoint_contributions`.
+"""
+
+from __future__ import annotations
+
+import math
+from fractions import Fraction
+from functools import lru_cache
+
+import numpy as np
+
+
+class SnapIndexError(ValueError):
+    pass
+
+
+def twojmax_of(jmax) -> int:
+    tj = float(2 * jmax)
+    if tj < 0 or abs(tj - round(tj)) > 1e-12:
+        raise SnapIndexError(f"2*jmax must be a non-negative integer, got jmax={jmax}")
+    return int(round(tj))
+
+
+class QuantumIndex:
+    """Bijection (j, m, m') -> flat index, per-j contiguous (tj+1)^2 blocks (mdkk/snap/indexing.py:24-54)."""
+
+    def __init__(self, jmax):
+        self.jmax = float(jmax)
+        self.twojmax = twojmax_of(jmax)
+        sizes = [(t + 1) ** 2 for t in range(self.twojmax + 1)]
+        self.block_offset = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+        self.n_flat = int(self.block_offset[-1])
+
+    def flat(self, tj: int, p: int, q: int) -> int:
+        if not (0 <= tj <= self.twojmax):
+            raise SnapIndexError(f"tj {tj} out of range [0, {self.twojmax}]")
+        if not (0 <= p <= tj and 0 <= q <= tj):
+            raise SnapIndexError(f"(p, q) = ({p}, {q}) out of block range for tj {tj}")
+        return int(self.block_offset[tj] + p * (tj + 1) + q)
+
+    def block(self, tj: int) -> slice:
+        return slice(int(self.block_offset[tj]), int(self.block_offset[tj + 1]))
+
+    def triples(self):
+        """(tj, tj1, tj2): tj2 <= tj1 <= tj, triangle, even sum; tj slowest (mdkk/snap/indexing.py:56-68)."""
+        return [(tj, tj1, tj2) for tj in range(self.twojmax + 1) for tj1 in range(tj + 1)
+                for tj2 in range(tj1 + 1) if tj <= tj1 + tj2 and (tj1 + tj2 - tj) % 2 == 0]
+
+
+def _hf(twice: int) -> int:
+    if twice < 0 or twice % 2:
+        raise SnapIndexError(f"factorial of non-integer or negative half-value {twice}/2")
+    return math.factorial(twice // 2)
+
+
+@lru_cache(maxsize=None)
+def clebsch_gordan(tj1: int, tm1: int, tj2: int, tm2: int, tj: int, tm: int) -> float:
+    """<j1 m1; j2 m2 | j m>, doubled args, Racah sum in exact rationals (mdkk/snap/coupling.py:28-66)."""
+    if tm1 + tm2 != tm or not (abs(tj1 - tj2) <= tj <= tj1 + tj2) or (tj1 + tj2 - tj) % 2:
+        return 0.0
+    if abs(tm1) > tj1 or abs(tm2) > tj2 or abs(tm) > tj:
+        return 0.0
+    if (tj1 + tm1) % 2 or (tj2 + tm2) % 2 or (tj + tm) % 2:
+        return 0.0
+    pref = Fraction((tj + 1) * _hf(tj1 + tj2 - tj) * _hf(tj1 - tj2 + tj) * _hf(tj2 - tj1 + tj)
+                    * _hf(tj1 + tm1) * _hf(tj1 - tm1) * _hf(tj2 + tm2) * _hf(tj2 - tm2)
+                    * _hf(tj + tm) * _hf(tj - tm), _hf(tj1 + tj2 + tj + 2))
+    acc = Fraction(0)
+    for k in range(max(0, (tj2 - tj - tm1) // 2, (tj1 - tj + tm2) // 2),
+                   min((tj1 + tj2 - tj) // 2, (tj1 - tm1) // 2, (tj2 + tm2) // 2) + 1):
+        den = (math.factorial(k) * _hf(tj1 + tj2 - tj - 2 * k) * _hf(tj1 - tm1 - 2 * k)
+               * _hf(tj2 + tm2 - 2 * k) * _hf(tj - tj2 + tm1 + 2 * k) * _hf(tj - tj1 - tm2 + 2 * k))
+        acc += Fraction((-1) ** k, den)
+    if acc == 0:
+        return 0.0
+    return math.copysign(math.sqrt(float(acc * acc * pref)), float(acc))
+
+
+class CouplingTables:
+    """Per-triple term lists (iz, iu1, iu2, coeff) for every coupled triple (mdkk/snap/coupling.py:136)."""
+
+    def __init__(self, jmax):
+        self.index = QuantumIndex(jmax)
+        self.triples = self.index.triples()
+        off = self.index.block_offset
+        self.terms = []
+        for (tj, tj1, tj2) in self.triples:
+            cg = np.zeros((tj1 + 1, tj2 + 1))
+            for p1 in range(tj1 + 1):
+                for p2 in range(tj2 + 1):
+                    tm = (2 * p1 - tj1) + (2 * p2 - tj2)
+                    if abs(tm) <= tj:
+                        cg[p1, p2] = clebsch_gordan(tj1, 2 * p1 - tj1, tj2, 2 * p2 - tj2, tj, tm)
+            sh = (tj1 + tj2 - tj) // 2
+            p1, p2, q1, q2 = (v.ravel() for v in np.meshgrid(np.arange(tj1 + 1), np.arange(tj2 + 1),
+                                                             np.arange(tj1 + 1), np.arange(tj2 + 1),
+                                                             indexing="ij"))
+            p, q = p1 + p2 - sh, q1 + q2 - sh
+            c = cg[p1, p2] * cg[q1, q2]
+            k = (p >= 0) & (p <= tj) & (q >= 0) & (q <= tj) & (c != 0.0)
+            self.terms.append((off[tj] + p[k] * (tj + 1) + q[k], off[tj1] + p1[k] * (tj1 + 1) + q1[k],
+                               off[tj2] + p2[k] * (tj2 + 1) + q2[k], c[k]))
+
+    @property
+    def n_terms(self) -> int:
+        return sum(len(t[3]) for t in self.terms)
+
+
+def make_coupling_tables(jmax) -> CouplingTables:
+    return CouplingTables(jmax)
+
+
+def adjoint_contributions(tables: CouplingTables, beta):
+    """Output-sorted list for Y[f] = sum coef * op(U[g]) * U[h] (mdkk/snap/compute.py:303-340).
+
+    Each term of triple t contributes to three slots:
+      Y[iz]  += b c U[iu1] U[iu2]        -> (f=iz,  g=iu1, h=iu2, conj=0)
+      Y[iu1] += b c conj(U[iu2]) U[iz]   -> (f=iu1, g=iu2, h=iz,  conj=1)
+      Y[iu2] += b c conj(U[iu1]) U[iz]   -> (f=iu2, g=iu1, h=iz,  conj=1)
+    identical (f, g, h, conj) keys are merged (U[g]U[h] commutes, so conj=0
+    keys use g <= h).  Returns f_start[n_flat+1], g, h, conj (int32) and coef (f64).
+    """
+    beta = np.asarray(beta, dtype=np.float64)
+    acc: dict = {}
+    for bt, (iz, i1, i2, c) in zip(beta, tables.terms):
+        if bt == 0.0:
+            continue
+        bc = bt * c
+        for z, a, b, v in zip(iz.tolist(), i1.tolist(), i2.tolist(), bc.tolist()):
+            for key in ((z, min(a, b), max(a, b), 0), (a, b, z, 1), (b, a, z, 1)):
+                acc[key] = acc.get(key, 0.0) + v
+    keys = sorted(acc)
+    n_flat = tables.index.n_flat
+    f = np.array([k[0] for k in keys], dtype=np.int64)
+    f_start = np.searchsorted(f, np.arange(n_flat + 1)).astype(np.int32)
+    g = np.array([k[1] for k in keys], dtype=np.int32)
+    h = np.array([k[2] for k in keys], dtype=np.int32)
+    cj = np.array([k[3] for k in keys], dtype=np.int32)
+    coef = np.array([acc[k] for k in keys], dtype=np.float64)
+    return f_start, g, h, cj, coef
+
+
+def read_coeff_file(path):
+    """First token jmax, then one beta per triple, '#' comments (mdkk/snap/compute.py:439-464)."""
+    from .compute import SnapError
+    tokens = []
+    with open(path) as fh:
+        for line in fh:
+            tokens.extend(line.split("#", 1)[0].split())
+    if not tokens:
+        raise SnapError(f"coefficient file {path} is empty")
+    try:
+        values = [float(t) for t in tokens]
+    except ValueError as exc:
+        raise SnapError(f"coefficient file {path}: {exc}") from None
+    jmax = values[0]
+    need = len(QuantumIndex(jmax).triples())
+    beta = np.asarray(values[1:], dtype=np.float64)
+    if len(beta) != need:
+        raise SnapError(f"coefficient file {path}: expected {need} beta values for jmax {jmax}, got {len(beta)}")
+    return jmax, beta

@@ -1,0 +1,140 @@
+"""GPU parity for the SNAP pipeline vs the reference goldens and the CPU oracle.
+
+Mirrors mdkk tests/test_snap.py (closed forms, cluster invariants, periodic
+force balance) and SURVEY §8(c)'s C4 KAT.  Tolerances: energy 1e-12
+relative, forces 1e-10 * max|F|, U / Y 1e-12 relative.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import golden
+from oracle import md, snap as osnap
+
+pytestmark = pytest.mark.gpu
+
+
+def _pipeline(pos, lengths, jmax, beta, rc, skin):
+    from paper_2508_13523_b200 import Box, RankedSystem, build_all
+    from paper_2508_13523_b200.snap import (SnapState, build_neighbor_map, compute_fused_deidrj, compute_ui,
+                                            compute_yi, energy_from_y, make_coupling_tables)
+    system = RankedSystem.distribute(Box(lengths), 1, pos, np.zeros_like(pos))
+    (nl,) = build_all(system, rc, skin, style="full", newton=False)
+    store = system.stores[0]
+    nmap = build_neighbor_map(store, nl, rc)
+    state = SnapState(make_coupling_tables(jmax), store.n_local, beta)
+    compute_ui(nmap, state)
+    compute_yi(state)
+    f = compute_fused_deidrj(nmap, state, store.n_total)
+    fr = store.force.read("a")
+    fr[: store.n_total] = f
+    store.force.mark_modified("a")
+    system.reverse_comm()
+    o = np.argsort(store.global_ids[: store.n_local])
+    return energy_from_y(state), system.gather_forces(), state.u_view()[o], state.y_view()[o]
+
+
+@pytest.mark.parametrize("tag,jmax", [("j2", 1), ("j4", 2), ("j8", 4)])
+def test_cluster_matches_reference(gpu, tag, jmax):
+    g = golden("snap.npz")
+    e, f, u, y = _pipeline(g[f"{tag}_pos"], np.array([12.0] * 3), jmax, g[f"{tag}_beta"], 1.9, 0.2)
+    assert e == pytest.approx(float(g[f"{tag}_E"]), rel=1e-12)
+    assert np.allclose(u, g[f"{tag}_U"], rtol=1e-12, atol=1e-14)
+    assert np.allclose(y, g[f"{tag}_Y"], rtol=1e-11, atol=1e-13)
+    scale = max(1.0, np.abs(g[f"{tag}_F"]).max())
+    assert np.abs(f - g[f"{tag}_F"]).max() / scale < 1e-10
+
+
+def test_periodic_matches_reference_and_balances(gpu):
+    g = golden("snap.npz")
+    e, f, _, _ = _pipeline(g["per_pos"], np.array([6.0] * 3), 2, g["per_beta"], 1.4, 0.3)
+    assert e == pytest.approx(float(g["per_E"]), rel=1e-12)
+    assert np.abs(f - g["per_F"]).max() < 1e-10 * max(1.0, np.abs(g["per_F"]).max())
+    assert np.abs(f.sum(axis=0)).max() < 1e-10
+
+
+def test_c4_2000_bcc_matches_reference(gpu):
+    """SURVEY §8(c) KAT (3): E = 65509.51457722162 on jittered 2k bcc, 2J=8, rc 4.73."""
+    g = golden("snap.npz")
+    pos, lengths = md.lattice("bcc", 3.1803, (10, 10, 10))
+    pos = md.jittered(pos, 0.05, 1)
+    e, f, u, y = _pipeline(pos, lengths, 4, np.linspace(0.05, 0.1, 55), 4.73, 0.3)
+    assert e == pytest.approx(float(g["c4_E"]), rel=1e-12)
+    assert e == pytest.approx(65509.51457722162, rel=1e-12)
+    assert np.abs(f - g["c4_F"]).max() <= 1e-10 * np.abs(g["c4_F"]).max()
+    assert np.allclose(u[:16], g["c4_U_sub"], rtol=1e-12, atol=1e-12)
+    assert np.allclose(y[:16], g["c4_Y_sub"], rtol=1e-11, atol=1e-11)
+
+
+def test_c4_perfect_lattice_energy(gpu):
+    g = golden("snap.npz")
+    pos, lengths = md.lattice("bcc", 3.1803, (10, 10, 10))
+    e, f, _, _ = _pipeline(pos, lengths, 4, np.linspace(0.05, 0.1, 55), 4.73, 0.3)
+    assert e == pytest.approx(float(g["c4_lattice_E"]), rel=1e-12)
+    assert e == pytest.approx(64610.777035472027, rel=1e-12)
+    assert np.abs(f).max() < 1e-9
+
+
+def test_single_pair_closed_form(gpu):
+    """mdkk tests/test_snap.py:375-395 (jmax 1/2: B = (fc^3, 2 fc^3))."""
+    d, rc = 1.3, 1.9
+    pos = np.array([[5.0, 5.0, 5.0], [5.0 + d, 5.0, 5.0]])
+    beta = np.array([0.37, -0.21])
+    e, f, u, y = _pipeline(pos, np.array([12.0] * 3), 0.5, beta, rc, 0.2)
+    fc = 0.5 * (1 + np.cos(np.pi * d / rc))
+    dfc = -np.pi / (2 * rc) * np.sin(np.pi * d / rc)
+    assert e == pytest.approx(2 * (beta[0] + 2 * beta[1]) * fc ** 3, rel=1e-12)
+    assert u[0, 0] == pytest.approx(fc, rel=1e-14)
+    assert y[0, 0] == pytest.approx(3 * beta[0] * fc ** 2 + 2 * beta[1] * fc ** 2, rel=1e-12)
+    assert f[0] == pytest.approx([2 * (beta[0] + 2 * beta[1]) * 3 * fc ** 2 * dfc, 0.0, 0.0], abs=1e-12)
+
+
+def test_zero_distance_raises(gpu):
+    from paper_2508_13523_b200.snap import SnapError
+    with pytest.raises(SnapError):
+        from paper_2508_13523_b200 import Box, RankedSystem, build_all
+        from paper_2508_13523_b200.snap import (SnapState, build_neighbor_map, compute_ui, make_coupling_tables)
+        from paper_2508_13523_b200.snap.compute import check_flags
+        system = RankedSystem.distribute(Box((12.0,) * 3), 1, np.full((2, 3), 5.0), np.zeros((2, 3)))
+        (nl,) = build_all(system, 1.9, 0.2, style="full", newton=False)
+        st = SnapState(make_coupling_tables(1), 2, np.zeros(5))
+        compute_ui(build_neighbor_map(system.stores[0], nl, 1.9), st)
+        check_flags(st)
+
+
+def test_snap_style_nve_matches_oracle(gpu, tmp_path):
+    """snap/kk through run_script vs the oracle's SNAP NVE (same lattice, velocities, dt)."""
+    from paper_2508_13523_b200.driver import RunConfig, run_script
+    coeff = tmp_path / "w.coeff"
+    beta = np.linspace(0.05, 0.1, 14)
+    coeff.write_text("2\n" + "\n".join(f"{b!r}" for b in beta) + "\n")
+    script = (f"units lj\nboundary p p p\nlattice bcc 3.1803\ncreate_box 4 4 4\ncreate_atoms\nmass 1.0\n"
+              f"velocity 0.5 4928459\nsuffix kk\npair_style snap 4.73 {coeff}\ntimestep 0.001\nthermo 5\nrun 10\n")
+    sim = run_script(script, RunConfig(), log=None)
+    rows = np.array(sim.results[-1].rows)
+    # oracle: same physics through oracle/snap.py
+    pos, L = md.lattice("bcc", 3.1803, (4, 4, 4))
+    vel = md.seeded_velocities(len(pos), 0.5, 1.0, 4928459)
+    so = osnap.SnapOracle(4, beta, 4.73)
+    sys_ = md.Ranked(L, 1, pos, vel)
+    lists = md.build_all(sys_, 4.73, 0.3, "full", False)
+    e0, _ = osnap.snap_compute(sys_, lists, so)
+    ref = [e0]
+    h = 0.5 * 0.001
+    for step in range(1, 11):
+        for r in sys_.ranks:
+            r.v += h * r.f[: r.n_local]
+            r.x[: r.n_local] += 0.001 * r.v
+        if any(nl.needs_rebuild() for nl in lists):
+            sys_.migrate(5.03)
+            lists = [md.build(r, L, 4.73, 0.3, "full", False) for r in sys_.ranks]
+        else:
+            sys_.forward()
+        e, _ = osnap.snap_compute(sys_, lists, so)
+        for r in sys_.ranks:
+            r.v += h * r.f[: r.n_local]
+        if step % 5 == 0:
+            ref.append(e)
+    assert np.allclose(rows[:, 1], ref, rtol=1e-10)
