@@ -180,6 +180,80 @@ def lj_run(style, cells, steps, warmup, device, profile=True):
                 launches=launches, nn=nn, clocks=clk.summary(), e_pot=e, n_ghost=st.n_ghost)
 
 
+SNAP = dict(a=3.1803, cells=80, rc=4.73, skin=0.3, T=0.01, seed=4928459, dt=0.001, twojmax=8)
+SNAP_TERMS = 32578   # coupling terms at 2J = 8
+
+
+def snap_flops_per_atom_step(nn):
+    """Canonical mdkk-formulation FLOPs: nn*(9260 + 60518) + 36*T."""
+    return nn * (9260.0 + 60518.0) + 36.0 * SNAP_TERMS
+
+
+def fp64_peak(device):
+    """Live FP64 FMA peak (TFLOP/s) from the library's DFMA probe, timed with CUDA events."""
+    import torch
+    from paper_2508_13523_b200 import _lib
+    out = torch.zeros(1, dtype=torch.float64, device=device)
+    blocks, iters = 148 * 8, 20000
+    _lib.call("mdkk_fp64_probe", blocks, 100, out.data_ptr(), _lib.stream(device))
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    _lib.call("mdkk_fp64_probe", blocks, iters, out.data_ptr(), _lib.stream(device))
+    b.record()
+    torch.cuda.synchronize()
+    return blocks * 256 * iters * 8 * 2 / (a.elapsed_time(b) * 1e-3) / 1e12
+
+
+def snap_run(cells, steps, warmup, device):
+    import tempfile
+    import torch
+    from paper_2508_13523_b200 import _lib
+    from paper_2508_13523_b200.driver import RunConfig, Simulation
+    coeff = os.path.join(tempfile.mkdtemp(), "w_2j8.coeff")
+    with open(coeff, "w") as fh:
+        fh.write("4\n" + "\n".join(repr(float(b)) for b in np.linspace(0.05, 0.1, 55)) + "\n")
+    sim = Simulation(RunConfig(skin=SNAP["skin"], device=device), log=None)
+    sim.execute(f"units lj\nboundary p p p\nlattice bcc {SNAP['a']}\ncreate_box {cells} {cells} {cells}\n"
+                f"create_atoms\nmass 1.0\nvelocity {SNAP['T']} {SNAP['seed']}\nsuffix kk\n"
+                f"pair_style snap {SNAP['rc']} {coeff}\ntimestep {SNAP['dt']}\nthermo 1000000000\n")
+    sim._ensure_system()
+    sim._forces_device()
+    for _ in range(warmup):
+        sim.step_device()
+    torch.cuda.synchronize()
+    fev = []
+    orig = sim._forces_device
+
+    def timed_forces():
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        e = orig()
+        b.record()
+        fev.append((a, b))
+        return e
+    sim._forces_device = timed_forces
+    l0 = _lib.launch_count()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    start.record()
+    for _ in range(steps):
+        sim.step_device()
+    end.record()
+    torch.cuda.synchronize()
+    ms = start.elapsed_time(end) / steps
+    st, nl = sim.system.stores[0], sim.lists[0]
+    # pairs within rc per atom (the descriptor neighbours), counted on device from the list
+    ncl = nl.table_dev.shape[0]
+    tab = nl.table_dev.permute(1, 0, 2).reshape(nl.alloc_cap, ncl * 32)[:, : st.n_local].long()
+    cnt = nl.counts_dev[: st.n_local].long()
+    valid = torch.arange(nl.alloc_cap, device=device)[:, None] < cnt[None, :]
+    xj = st.x[tab.clamp(min=0), :3]
+    d = xj - st.x[: st.n_local, :3][None]
+    nn = float((((d * d).sum(-1) < SNAP["rc"] ** 2) & valid).sum().item()) / st.n_local
+    return dict(ms=ms, force_ms=float(np.mean([a.elapsed_time(b) for a, b in fev])), n_atoms=sim.system.n_atoms,
+                nn=nn, launches=_lib.launch_count() - l0, e_pot=float(sim._e_dev.item()))
+
+
 def lj_e2e(style, cells, steps, device):
     """Public API end to end: host arrays -> distribute/build -> run_nve(steps) -> thermo + gid-ordered D2H."""
     import torch
@@ -215,6 +289,9 @@ def main():
     ap.add_argument("--cells", type=int, default=LJ["cells"])
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-snap", action="store_true")
+    ap.add_argument("--snap-cells", type=int, default=SNAP["cells"])
+    ap.add_argument("--snap-steps", type=int, default=5)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -244,6 +321,10 @@ def main():
     bytes_per_launch = full["n_atoms"] * (28.0 * nn + 52.0)
     achieved = bytes_per_launch / (full["force_ms"] * 1e-3) / 1e9
     e2e = lj_e2e("full", args.cells, max(args.steps, 20), device) if not args.no_e2e else None
+    snapr, fp64 = None, None
+    if not args.no_snap:
+        fp64 = fp64_peak(device)
+        snapr = snap_run(args.snap_cells, args.snap_steps, 2, device)
     cpu = None
     if rank == 0 and not args.no_cpu:
         v, secs, n = cpu_lj_sample()
@@ -272,6 +353,19 @@ def main():
                          "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic_from_profiles("k_lj"),
                          "bytes_model": f"n_local*(28*nn+52), nn={nn:.2f} measured"},
+            "snap": (None if snapr is None else {
+                "workload": f"SNAP W bcc a=3.1803, 2J=8, rc=4.73, skin 0.3, T=0.01, dt=0.001, "
+                            f"{snapr['n_atoms']} atoms (configs[4] at N=1)",
+                "value": snapr["n_atoms"] / (snapr["ms"] * 1e-3) / 1e6, "unit": UNIT,
+                "ms_per_step": snapr["ms"], "force_ms": snapr["force_ms"], "steps": args.snap_steps,
+                "pairs_within_rc_per_atom": snapr["nn"],
+                "roofline": {"bound": "fp64", "kernel": "ui + yi + fused deidrj (+ reverse comm)",
+                             "achieved": snap_flops_per_atom_step(snapr["nn"]) * snapr["n_atoms"]
+                             / (snapr["force_ms"] * 1e-3) / 1e12,
+                             "peak": fp64, "peak_kind": "measured live (DFMA probe)", "unit": "TFLOP/s",
+                             "frac": snap_flops_per_atom_step(snapr["nn"]) * snapr["n_atoms"]
+                             / (snapr["force_ms"] * 1e-3) / 1e12 / fp64,
+                             "flops_model": "canonical mdkk formulation nn*(9260+60518)+36*32578 per atom"}}),
             "cpu_baseline": cpu,
             "e2e": ({"value": e2e["value"], "unit": UNIT, "h2d_bytes_per_step": e2e["h2d"],
                      "d2h_bytes_per_step": e2e["d2h"]} if e2e else None),

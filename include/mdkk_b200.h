@@ -53,6 +53,9 @@ const char* mdkk_last_error(void);
 int mdkk_device_sm_count(int device, int* out_host);
 int mdkk_ctx_create(int device, mdkk_ctx** out_host);
 int mdkk_ctx_destroy(mdkk_ctx* ctx);
+/* FP64 FMA throughput probe: blocks x 256 threads x iters x 8 DFMA (2 flops
+ * each); timed by the caller to measure the FP64 roofline denominator. */
+int mdkk_fp64_probe(int blocks, int iters, double* out, void* stream);
 
 /* ------------------------------------------------------ domain / halo comm
  * Replaces mdkk/domain.py:56-63 (wrap), :246-293 (exchange_ghosts selection),

@@ -30,6 +30,7 @@ SIGNATURES = {
     "mdkk_device_sm_count": [_i, _p],
     "mdkk_ctx_create": [_i, _p],
     "mdkk_ctx_destroy": [_p],
+    "mdkk_fp64_probe": [_i, _i, _p, _p],
     "mdkk_wrap": [_p, _i, _p, _p],
     "mdkk_halo_count": [_p, _p, _i, _p, _i, _p, _p, _p],
     "mdkk_halo_fill": [_p, _p, _i, _p, _i, _p, _p, _p, _p],

@@ -93,3 +93,31 @@ int mdkk_ctx_destroy(mdkk_ctx* ctx) {
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------ FP64 probe
+// Peak FP64 FMA throughput probe: every thread runs 8 independent DFMA chains
+// (enough ILP to saturate the FP64 pipe); bench.py times it with CUDA events
+// to get the live FP64 roofline denominator (MEASURED_PEAKS.json has none).
+namespace {
+__global__ void __launch_bounds__(256) k_fp64_probe(int iters, double seed, double* out) {
+    double a[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = seed + threadIdx.x * 1e-9 + k;
+    const double m = 0.999999999, c = 1e-12;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) a[k] = fma(a[k], m, c);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += a[k];
+    if (s == 42.0) out[0] = s;  // keep the chains live
+}
+}  // namespace
+
+extern "C" int mdkk_fp64_probe(int blocks, int iters, double* out, void* stream) {
+    if (blocks < 1 || iters < 1) return MDKK_E_ARG;
+    k_fp64_probe<<<blocks, 256, 0, mdkk::as_stream(stream)>>>(iters, 1.0, out);
+    MDKK_CHECK_LAUNCH("k_fp64_probe");
+    return MDKK_OK;
+}

@@ -109,7 +109,7 @@ def test_snap_style_nve_matches_oracle(gpu, tmp_path):
     from paper_2508_13523_b200.driver import RunConfig, run_script
     coeff = tmp_path / "w.coeff"
     beta = np.linspace(0.05, 0.1, 14)
-    coeff.write_text("2\n" + "\n".join(f"{b!r}" for b in beta) + "\n")
+    coeff.write_text("2\n" + "\n".join(repr(float(b)) for b in beta) + "\n")
     script = (f"units lj\nboundary p p p\nlattice bcc 3.1803\ncreate_box 4 4 4\ncreate_atoms\nmass 1.0\n"
               f"velocity 0.5 4928459\nsuffix kk\npair_style snap 4.73 {coeff}\ntimestep 0.001\nthermo 5\nrun 10\n")
     sim = run_script(script, RunConfig(), log=None)
