@@ -247,7 +247,7 @@ def snap_run(cells, steps, warmup, device):
     tab = nl.table_dev.permute(1, 0, 2).reshape(nl.alloc_cap, ncl * 32)[:, : st.n_local].long()
     cnt = nl.counts_dev[: st.n_local].long()
     valid = torch.arange(nl.alloc_cap, device=device)[:, None] < cnt[None, :]
-    xj = st.x[tab.clamp(min=0), :3]
+    xj = st.x[torch.where(valid, tab, 0), :3]
     d = xj - st.x[: st.n_local, :3][None]
     nn = float((((d * d).sum(-1) < SNAP["rc"] ** 2) & valid).sum().item()) / st.n_local
     return dict(ms=ms, force_ms=float(np.mean([a.elapsed_time(b) for a, b in fev])), n_atoms=sim.system.n_atoms,
