@@ -164,8 +164,8 @@ int mdkk_kinetic(mdkk_ctx* ctx, const double* v, int n, double mass, double* ke,
 /* ------------------------------------------------------------------- SNAP
  * FP64 descriptor pipeline with mdkk's conventions (mdkk/snap/compute.py:
  * rfac0 0.99, rmin0 0, cosine switch, no self term, full (2j+1)^2 blocks,
- * full three-slot adjoint).  U, Y are complex128 [n_flat][n_local] (atom
- * fastest, the reference's layout "b"); n_flat = sum_{tj<=2J} (tj+1)^2.
+ * full three-slot adjoint).  U, Y are complex128 row-major [n_local][n_flat]
+ * (the reference's layout "a"); n_flat = sum_{tj<=2J} (tj+1)^2.
  * Pairs are the entries of a FULL cluster-blocked table with r^2 < rc^2.
  *
  * mdkk_snap_create copies the output-sorted adjoint contribution list
@@ -185,7 +185,8 @@ int mdkk_snap_ui(mdkk_snap* snap, const double* x, int n_local, const int* table
 int mdkk_snap_yi(mdkk_ctx* ctx, mdkk_snap* snap, const double* U, int n_local, double* Y, double* energy,
                  void* stream);
 /* Fused 3-direction forces (compute_fused_deidrj, mdkk/snap/compute.py:390-409):
- * t = Re sum_f Y_i[f] conj(d(f_c u)/d r_ik [f]); f_i += t, f_k -= t (FP64
+ * t = Re sum_f Y_i[f] conj(d(f_c u)/d r_ik [f]) evaluated in reverse mode (u
+ * forward, adjoint backward, 4 complex partials per pair); f_i += t, f_k -= t (FP64
  * atomics, f double4 rows incl. ghosts, caller-zeroed; ghosts -> reverse comm). */
 int mdkk_snap_deidrj(mdkk_snap* snap, const double* x, int n_local, const int* table, const int* counts, int cap,
                      double rc, const double* Y, double* f, void* stream);

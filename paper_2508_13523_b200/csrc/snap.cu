@@ -5,16 +5,16 @@
 // rmin0 = 0, plain cosine switch, no self term, full (tj+1)^2 blocks and the
 // full three-slot adjoint Y.
 //
-// Data: U, Y are complex128 [n_flat][n_atoms] (atom fastest — the reference's
-// transposed layout "b"), double2 = (re, im).
+// Data: U, Y are complex128 row-major [n_atoms][n_flat] (the reference's
+// layout "a"), double2 = (re, im).
 //
 // compute_ui / fused deidrj: one warp per atom, its neighbours processed one
 // at a time; the warp computes each level of the Wigner-U recursion with the
 // level's elements spread over lanes (element idx -> lane idx%32, slot idx/32)
 // and the previous level in shared memory.  Each lane keeps its 14 slots of
 // U_i (ui) or Y_i (deidrj) in registers, so the per-atom sums need no atomics.
-// compute_yi: one thread per atom walking an output-sorted contribution list
-// (uniform across the warp -> broadcast table reads, coalesced U reads).
+// compute_yi: one warp per atom over an output-sorted contribution list staged
+// through shared memory; compute_fused_deidrj in reverse mode (see below).
 #include <algorithm>
 #include <cmath>
 #include <vector>
@@ -26,7 +26,7 @@ struct mdkk_snap {
     int n_flat = 0;
     int n_contrib = 0;
     int* f_start = nullptr;     // [n_flat + 1]
-    int4* contrib = nullptr;    // {g, h, conj, 0}
+    int4* contrib = nullptr;    // {g, h, conj, f}
     double* coef = nullptr;     // [n_contrib]
 };
 
@@ -57,73 +57,62 @@ __device__ __forceinline__ cplx cscale(double s, cplx a) { return {s * a.re, s *
 __device__ __forceinline__ cplx cneg(cplx a) { return {-a.re, -a.im}; }
 
 // Recursion weights of element (P, Q) of level tj (mdkk/snap/compute.py:130-147):
-// w[0] = sqrt(PQ)/tj (a * prev[P-1][Q-1]), w[1] = sqrt(P(tj-Q))/tj (b * prev[P-1][Q]),
-// w[2] = sqrt((tj-P)Q)/tj (-conj(b) * prev[P][Q-1]), w[3] = sqrt((tj-P)(tj-Q))/tj (conj(a) * prev[P][Q]).
-__constant__ double c_w[block_offset(kMaxTwoJ + 1)][4];
+// w0 = sqrt(PQ)/tj (a * prev[P-1][Q-1]), w1 = sqrt(P(tj-Q))/tj (b * prev[P-1][Q]),
+// w2 = sqrt((tj-P)Q)/tj (-conj(b) * prev[P][Q-1]), w3 = sqrt((tj-P)(tj-Q))/tj (conj(a) * prev[P][Q]).
+// Stored SoA in global memory and staged per CTA in shared memory (lanes read
+// different elements: constant memory would serialise).
+__device__ double g_w[4][block_offset(kMaxTwoJ + 1)];
+
+struct SW {
+    double w[4][block_offset(kMaxTwoJ + 1)];
+};
+
+__device__ __forceinline__ void stage_weights(SW& sw, int n_flat) {
+    for (int t = threadIdx.x; t < 4 * n_flat; t += blockDim.x) sw.w[t / n_flat][t % n_flat] = g_w[t / n_flat][t % n_flat];
+    __syncthreads();
+}
 
 struct PairGeo {
     cplx a, b;
     double fc, dfc, r;
-    cplx da[3], db[3];
 };
 
-// a, b, f_c, f_c' (mdkk/snap/compute.py:27-45) and optionally d a / d dr, d b / d dr (:48-63).
-template <bool GRAD>
-__device__ __forceinline__ void pair_geometry(double dx, double dy, double dz, double r2, double rc, PairGeo& g) {
+// a, b, f_c, f_c' (mdkk/snap/compute.py:27-45).
+__device__ __forceinline__ void pair_geometry(double dx, double dy, double dz, double r2, double rc, PairGeo& g,
+                                              double& z0, double& r0) {
     const double r = sqrt(r2);
     const double ct = 0.99 * kPi / rc;
-    const double z0 = r / tan(ct * r);
-    const double r0 = sqrt(r * r + z0 * z0);
+    z0 = r / tan(ct * r);
+    r0 = sqrt(r * r + z0 * z0);
     g.r = r;
     g.a = {z0 / r0, -dz / r0};
     g.b = {dy / r0, -dx / r0};
     g.fc = 0.5 * (1.0 + cos(kPi * r / rc));
     g.dfc = -kPi / (2.0 * rc) * sin(kPi * r / rc);
-    if (GRAD) {
-        const double dz0_dr = z0 / r - ct * (r * r + z0 * z0) / r;
-        const double d[3] = {dx, dy, dz};
+}
+
+// d a / d dr_k, d b / d dr_k (mdkk/snap/compute.py:48-63).
+__device__ __forceinline__ void pair_grads(const double d[3], const PairGeo& g, double rc, double z0, double r0,
+                                           cplx da[3], cplx db[3]) {
+    const double r = g.r, ct = 0.99 * kPi / rc;
+    const double dz0_dr = z0 / r - ct * (r * r + z0 * z0) / r;
 #pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            const double dz0 = dz0_dr * (d[k] / r);
-            const double dr0 = (d[k] + z0 * dz0) / r0;
-            // da = (dz0 + unit_z*(-i)) / r0 - a dr0 / r0
-            g.da[k] = {dz0 / r0 - g.a.re * dr0 / r0, (k == 2 ? -1.0 / r0 : 0.0) - g.a.im * dr0 / r0};
-            // db = unit_b / r0 - b dr0 / r0,  unit_b = (-i, 1, 0)
-            g.db[k] = {(k == 1 ? 1.0 / r0 : 0.0) - g.b.re * dr0 / r0, (k == 0 ? -1.0 / r0 : 0.0) - g.b.im * dr0 / r0};
-        }
+    for (int k = 0; k < 3; ++k) {
+        const double dz0 = dz0_dr * (d[k] / r);
+        const double dr0 = (d[k] + z0 * dz0) / r0;
+        da[k] = {dz0 / r0 - g.a.re * dr0 / r0, (k == 2 ? -1.0 / r0 : 0.0) - g.a.im * dr0 / r0};
+        db[k] = {(k == 1 ? 1.0 / r0 : 0.0) - g.b.re * dr0 / r0, (k == 0 ? -1.0 / r0 : 0.0) - g.b.im * dr0 / r0};
     }
 }
 
-// One element of level tj from the previous level stored row-major (tj x tj) in `prev`.
-__device__ __forceinline__ cplx level_elem(const cplx* prev, int tj, int P, int Q, const double* w, cplx a, cplx b) {
+// One element (P, Q) of level tj from the previous level stored row-major (tj x tj) at `prev`.
+__device__ __forceinline__ cplx level_elem(const cplx* prev, int tj, int P, int Q, double w0, double w1, double w2,
+                                          double w3, cplx a, cplx b) {
     cplx v = {0.0, 0.0};
-    if (P >= 1 && Q >= 1) v = cadd(v, cscale(w[0], cmul(prev[(P - 1) * tj + (Q - 1)], a)));
-    if (P >= 1 && Q <= tj - 1) v = cadd(v, cscale(w[1], cmul(prev[(P - 1) * tj + Q], b)));
-    if (P <= tj - 1 && Q >= 1) v = cadd(v, cscale(w[2], cmul(prev[P * tj + (Q - 1)], cneg(cconj(b)))));
-    if (P <= tj - 1 && Q <= tj - 1) v = cadd(v, cscale(w[3], cmul(prev[P * tj + Q], cconj(a))));
-    return v;
-}
-
-// Product-rule companion (mdkk/snap/compute.py:150-162).
-__device__ __forceinline__ cplx level_elem_d(const cplx* prev, const cplx* dprev, int tj, int P, int Q,
-                                             const double* w, cplx a, cplx b, cplx da, cplx db) {
-    cplx v = {0.0, 0.0};
-    if (P >= 1 && Q >= 1) {
-        const int k = (P - 1) * tj + (Q - 1);
-        v = cadd(v, cscale(w[0], cadd(cmul(dprev[k], a), cmul(prev[k], da))));
-    }
-    if (P >= 1 && Q <= tj - 1) {
-        const int k = (P - 1) * tj + Q;
-        v = cadd(v, cscale(w[1], cadd(cmul(dprev[k], b), cmul(prev[k], db))));
-    }
-    if (P <= tj - 1 && Q >= 1) {
-        const int k = P * tj + (Q - 1);
-        v = cadd(v, cscale(w[2], cadd(cmul(dprev[k], cneg(cconj(b))), cmul(prev[k], cneg(cconj(db))))));
-    }
-    if (P <= tj - 1 && Q <= tj - 1) {
-        const int k = P * tj + Q;
-        v = cadd(v, cscale(w[3], cadd(cmul(dprev[k], cconj(a)), cmul(prev[k], cconj(da)))));
-    }
+    if (P >= 1 && Q >= 1) v = cadd(v, cscale(w0, cmul(prev[(P - 1) * tj + (Q - 1)], a)));
+    if (P >= 1 && Q <= tj - 1) v = cadd(v, cscale(w1, cmul(prev[(P - 1) * tj + Q], b)));
+    if (P <= tj - 1 && Q >= 1) v = cadd(v, cscale(w2, cmul(prev[P * tj + (Q - 1)], cneg(cconj(b)))));
+    if (P <= tj - 1 && Q <= tj - 1) v = cadd(v, cscale(w3, cmul(prev[P * tj + Q], cconj(a))));
     return v;
 }
 
@@ -139,12 +128,16 @@ __device__ __forceinline__ bool neighbour(const double* x, const int* table, int
 }
 
 // ---------------------------------------------------------------- compute_ui
+// U row-major [n_local][n_flat] (the reference's layout "a").
 template <int TWOJ>
 __global__ void __launch_bounds__(kWarps * 32) k_snap_ui(const double* __restrict__ x, int n_local,
                                                          const int* __restrict__ table,
                                                          const int* __restrict__ counts, int cap, double rc,
                                                          double2* __restrict__ U, int* __restrict__ flags) {
+    constexpr int NF = block_offset(TWOJ + 1);
+    __shared__ SW sw;
     __shared__ cplx s_lvl[kWarps][2][kLevelMax];
+    stage_weights(sw, NF);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int i = blockIdx.x * kWarps + w;
     if (i >= n_local) return;
@@ -157,11 +150,11 @@ __global__ void __launch_bounds__(kWarps * 32) k_snap_ui(const double* __restric
     bool bad = false;
     for (int k = 0; k < n; ++k) {
         int j;
-        double dx, dy, dz, r2;
+        double dx, dy, dz, r2, z0, r0;
         if (!neighbour(x, table, cap, i, k, xi, rc2, j, dx, dy, dz, r2)) continue;
         bad |= !(r2 > 0.0);
         PairGeo g;
-        pair_geometry<false>(dx, dy, dz, r2, rc, g);
+        pair_geometry(dx, dy, dz, r2, rc, g, z0, r0);
         if (lane == 0) {
             s_lvl[w][0][0] = {1.0, 0.0};
             acc[0].re += g.fc;
@@ -175,8 +168,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_snap_ui(const double* __restric
             for (int s = 0; s < level_slots(tj); ++s) {
                 const int idx = lane + 32 * s;
                 if (idx < level_size(tj)) {
-                    const int P = idx / (tj + 1), Q = idx % (tj + 1);
-                    const cplx v = level_elem(prev, tj, P, Q, c_w[block_offset(tj) + idx], g.a, g.b);
+                    const int P = idx / (tj + 1), Q = idx % (tj + 1), e = block_offset(tj) + idx;
+                    const cplx v = level_elem(prev, tj, P, Q, sw.w[0][e], sw.w[1][e], sw.w[2][e], sw.w[3][e], g.a, g.b);
                     cur[idx] = v;
                     acc[slot_base(tj) + s] = cadd(acc[slot_base(tj) + s], cscale(g.fc, v));
                 }
@@ -185,62 +178,123 @@ __global__ void __launch_bounds__(kWarps * 32) k_snap_ui(const double* __restric
         }
     }
     if (bad && lane == 0) atomicOr(flags, MDKK_FLAG_COINCIDENT);
+    double2* Ui = U + (long long)i * NF;
 #pragma unroll
     for (int tj = 0; tj <= TWOJ; ++tj)
 #pragma unroll
         for (int s = 0; s < level_slots(tj); ++s) {
             const int idx = lane + 32 * s;
             if (idx < level_size(tj))
-                U[(long long)(block_offset(tj) + idx) * n_local + i] =
-                    make_double2(acc[slot_base(tj) + s].re, acc[slot_base(tj) + s].im);
+                Ui[block_offset(tj) + idx] = make_double2(acc[slot_base(tj) + s].re, acc[slot_base(tj) + s].im);
         }
 }
 
 // ---------------------------------------------------------------- compute_yi
-// Y[f] = sum_k coef_k * op(U[g_k]) * U[h_k]  (op = conj for slot-1/2 terms);
-// e_atom = Re sum_f Y[f] conj(U[f]) / 3 (energy_from_y, mdkk/snap/compute.py:376-387).
-__global__ void __launch_bounds__(128) k_snap_yi(const double2* __restrict__ U, int n, int n_flat,
-                                                 const int* __restrict__ f_start, const int4* __restrict__ contrib,
-                                                 const double* __restrict__ coef, double2* __restrict__ Y,
-                                                 double* __restrict__ partials) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    double e[1] = {0.0};
-    if (i < n) {
-        for (int f = 0; f < n_flat; ++f) {
+// Y_i[f] = sum_k coef_k op(U_i[g_k]) U_i[h_k] (op = conj for slot-1/2 terms) and
+// e_i = Re sum_f Y_i[f] conj(U_i[f]) / 3 (energy_from_y, mdkk/snap/compute.py:376-387).
+// One warp per atom (8 atoms per CTA).  U_i and the Y_i accumulator live in
+// shared memory; the contribution table is streamed through shared memory in
+// chunks shared by the CTA's 8 atoms.  Lane l takes 32 consecutive entries of a
+// chunk (stored transposed -> conflict-free) and flushes its running sum with a
+// shared-memory atomic only when the output index f changes.
+constexpr int kYWarps = 8;
+constexpr int kYChunk = 1024;
+
+template <int NF>
+__global__ void __launch_bounds__(kYWarps * 32) k_snap_yi(const double2* __restrict__ U, int n, int n_contrib,
+                                                          const int4* __restrict__ contrib,
+                                                          const double* __restrict__ coef, double2* __restrict__ Y,
+                                                          double* __restrict__ partials) {
+    extern __shared__ double4 s_dyn[];  // dynamic: > 48 KB
+    auto s_t = reinterpret_cast<int4(*)[33]>(s_dyn);                       // [32][33] entry-in-lane x lane
+    auto s_c = reinterpret_cast<double(*)[33]>(s_t + 32);                  // [32][33]
+    auto s_u = reinterpret_cast<double2(*)[NF]>(s_c + 32);                 // [kYWarps][NF]
+    auto s_yr = reinterpret_cast<double(*)[NF]>(s_u + kYWarps);            // [kYWarps][NF]
+    auto s_yi = reinterpret_cast<double(*)[NF]>(s_yr + kYWarps);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int i = blockIdx.x * kYWarps + w;
+    const bool valid = i < n;
+    for (int f = lane; f < NF; f += 32) {
+        s_u[w][f] = valid ? U[(long long)i * NF + f] : make_double2(0.0, 0.0);
+        s_yr[w][f] = 0.0;
+        s_yi[w][f] = 0.0;
+    }
+    for (int base = 0; base < n_contrib; base += kYChunk) {
+        __syncthreads();
+        for (int t = threadIdx.x; t < kYChunk; t += blockDim.x) {
+            const int k = base + t;
+            const int l = t >> 5, p = t & 31;  // entry t belongs to lane l, position p
+            s_t[p][l] = k < n_contrib ? __ldg(contrib + k) : make_int4(0, 0, 0, -1);
+            s_c[p][l] = k < n_contrib ? __ldg(coef + k) : 0.0;
+        }
+        __syncthreads();
+        if (valid) {
+            int cur = -1;
             double are = 0.0, aim = 0.0;
-            const int k1 = __ldg(f_start + f + 1);
-            for (int k = __ldg(f_start + f); k < k1; ++k) {
-                const int4 t = __ldg(contrib + k);
-                const double c = __ldg(coef + k);
-                const double2 ug = U[(long long)t.x * n + i];
-                const double2 uh = U[(long long)t.y * n + i];
-                const double gi = t.z ? -ug.y : ug.y;
-                // c * (g * h)
-                are += c * (ug.x * uh.x - gi * uh.y);
-                aim += c * (ug.x * uh.y + gi * uh.x);
+#pragma unroll 4
+            for (int p = 0; p < 32; ++p) {
+                const int4 t = s_t[p][lane];
+                if (t.w != cur) {
+                    if (cur >= 0) {
+                        atomicAdd(&s_yr[w][cur], are);
+                        atomicAdd(&s_yi[w][cur], aim);
+                    }
+                    cur = t.w;
+                    are = aim = 0.0;
+                }
+                if (t.w >= 0) {
+                    const double c = s_c[p][lane];
+                    const double2 ug = s_u[w][t.x];
+                    const double2 uh = s_u[w][t.y];
+                    const double gi = t.z ? -ug.y : ug.y;
+                    are += c * (ug.x * uh.x - gi * uh.y);
+                    aim += c * (ug.x * uh.y + gi * uh.x);
+                }
             }
-            Y[(long long)f * n + i] = make_double2(are, aim);
-            const double2 uf = U[(long long)f * n + i];
-            e[0] += are * uf.x + aim * uf.y;  // Re(Y conj(U))
+            if (cur >= 0) {
+                atomicAdd(&s_yr[w][cur], are);
+                atomicAdd(&s_yi[w][cur], aim);
+            }
+        }
+    }
+    __syncthreads();
+    double e[1] = {0.0};
+    if (valid) {
+        for (int f = lane; f < NF; f += 32) {
+            const double yr = s_yr[w][f], yi = s_yi[w][f];
+            Y[(long long)i * NF + f] = make_double2(yr, yi);
+            e[0] += yr * s_u[w][f].x + yi * s_u[w][f].y;  // Re(Y conj(U))
         }
         e[0] /= 3.0;
     }
-    mdkk::block_sum<1, 128>(e, partials + blockIdx.x);
+    mdkk::block_sum<1, kYWarps * 32>(e, partials + blockIdx.x);
 }
 
 // ------------------------------------------------------- compute_fused_deidrj
+// Reverse-mode form of compute_fused_deidrj (mdkk/snap/compute.py:390-409).
+// For one pair the reference evaluates t_d = Re sum_f Y[f] conj(d(f_c u[f])/d dr_d)
+// with a forward derivative recursion per direction.  Here u is run forward
+// (all levels kept in shared memory) and the adjoint lambda_tj = Y_tj +
+// M_{tj+1}^H lambda_{tj+1} backward, accumulating G_c = sum_f Y[f] conj(du[f]/dc)
+// for c in {a, a*, b, b*}; then
+//   t_d = f_c' rhat_d Re sum Y conj(u) + f_c Re(G_a conj(da_d) + G_a* da_d + G_b conj(db_d) + G_b* db_d).
+// Same quantity (equal to rounding), 12 instead of 28 complex MACs per element.
 template <int TWOJ>
 __global__ void __launch_bounds__(kWarps * 32) k_snap_deidrj(const double* __restrict__ x, int n_local,
                                                              const int* __restrict__ table,
                                                              const int* __restrict__ counts, int cap, double rc,
                                                              const double2* __restrict__ Y,
                                                              double* __restrict__ f) {
-    __shared__ cplx s_u[kWarps][2][kLevelMax];
-    __shared__ cplx s_du[kWarps][2][3][kLevelMax];
+    constexpr int NF = block_offset(TWOJ + 1);
+    __shared__ SW sw;
+    __shared__ cplx s_u[kWarps][NF];
+    __shared__ cplx s_l[kWarps][2][kLevelMax];
+    stage_weights(sw, NF);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int i = blockIdx.x * kWarps + w;
     if (i >= n_local) return;
     cplx y[kSlots];
+    const double2* Yi = Y + (long long)i * NF;
 #pragma unroll
     for (int tj = 0; tj <= TWOJ; ++tj)
 #pragma unroll
@@ -248,60 +302,102 @@ __global__ void __launch_bounds__(kWarps * 32) k_snap_deidrj(const double* __res
             const int idx = lane + 32 * s;
             y[slot_base(tj) + s] = {0.0, 0.0};
             if (idx < level_size(tj)) {
-                const double2 v = Y[(long long)(block_offset(tj) + idx) * n_local + i];
+                const double2 v = Yi[block_offset(tj) + idx];
                 y[slot_base(tj) + s] = {v.x, v.y};
             }
         }
+    cplx* ul = s_u[w];
     const double4 xi = mdkk::ld4(x, i);
     const int n = min(counts[i], cap);
     const double rc2 = rc * rc;
     double fi[3] = {0.0, 0.0, 0.0};
     for (int k = 0; k < n; ++k) {
         int j;
-        double dx, dy, dz, r2;
+        double dx, dy, dz, r2, z0, r0;
         if (!neighbour(x, table, cap, i, k, xi, rc2, j, dx, dy, dz, r2)) continue;
         PairGeo g;
-        pair_geometry<true>(dx, dy, dz, r2, rc, g);
-        const double rh[3] = {dx / g.r, dy / g.r, dz / g.r};
-        double t[3] = {0.0, 0.0, 0.0};
+        pair_geometry(dx, dy, dz, r2, rc, g, z0, r0);
+        // forward: all levels of u, and S = Re sum Y conj(u)
+        double S = 0.0;
         if (lane == 0) {
-            s_u[w][0][0] = {1.0, 0.0};
-#pragma unroll
-            for (int d = 0; d < 3; ++d) {
-                s_du[w][0][d][0] = {0.0, 0.0};
-                // level 0: wdu = dfc * rhat * 1 -> Re(Y0 * conj(.))
-                t[d] += y[0].re * g.dfc * rh[d];
-            }
+            ul[0] = {1.0, 0.0};
+            S = y[0].re;
         }
         __syncwarp();
 #pragma unroll
         for (int tj = 1; tj <= TWOJ; ++tj) {
-            const int pb = (tj - 1) & 1, cb = tj & 1;
 #pragma unroll
             for (int s = 0; s < level_slots(tj); ++s) {
                 const int idx = lane + 32 * s;
                 if (idx < level_size(tj)) {
-                    const int P = idx / (tj + 1), Q = idx % (tj + 1);
-                    const double* wt = c_w[block_offset(tj) + idx];
-                    const cplx u = level_elem(s_u[w][pb], tj, P, Q, wt, g.a, g.b);
-                    s_u[w][cb][idx] = u;
+                    const int P = idx / (tj + 1), Q = idx % (tj + 1), e = block_offset(tj) + idx;
+                    const cplx v = level_elem(ul + block_offset(tj - 1), tj, P, Q, sw.w[0][e], sw.w[1][e], sw.w[2][e],
+                                              sw.w[3][e], g.a, g.b);
+                    ul[e] = v;
                     const cplx yv = y[slot_base(tj) + s];
+                    S += yv.re * v.re + yv.im * v.im;
+                }
+            }
+            __syncwarp();
+        }
+        // backward: lambda_TWOJ = Y_TWOJ, then G_c and lambda_{tj-1}
+        cplx Ga = {0, 0}, Gas = {0, 0}, Gb = {0, 0}, Gbs = {0, 0};
 #pragma unroll
-                    for (int d = 0; d < 3; ++d) {
-                        const cplx du =
-                            level_elem_d(s_u[w][pb], s_du[w][pb][d], tj, P, Q, wt, g.a, g.b, g.da[d], g.db[d]);
-                        s_du[w][cb][d][idx] = du;
-                        // wdu = fc du + dfc rhat u ; t += Re(Y conj(wdu))
-                        const double wre = g.fc * du.re + g.dfc * rh[d] * u.re;
-                        const double wim = g.fc * du.im + g.dfc * rh[d] * u.im;
-                        t[d] += yv.re * wre + yv.im * wim;
+        for (int s = 0; s < level_slots(TWOJ); ++s) {
+            const int idx = lane + 32 * s;
+            if (idx < level_size(TWOJ)) s_l[w][TWOJ & 1][idx] = y[slot_base(TWOJ) + s];
+        }
+        __syncwarp();
+#pragma unroll
+        for (int tj = TWOJ; tj >= 1; --tj) {
+            const cplx* lam = s_l[w][tj & 1];
+            const cplx* up = ul + block_offset(tj - 1);  // u_{tj-1}, row-major tj x tj
+            // (a) G_c += lambda_tj[P][Q] conj(d(local)/dc)
+#pragma unroll
+            for (int s = 0; s < level_slots(tj); ++s) {
+                const int idx = lane + 32 * s;
+                if (idx < level_size(tj)) {
+                    const int P = idx / (tj + 1), Q = idx % (tj + 1), e = block_offset(tj) + idx;
+                    const cplx l = lam[idx];
+                    if (P >= 1 && Q >= 1) Ga = cadd(Ga, cscale(sw.w[0][e], cmul(l, cconj(up[(P - 1) * tj + (Q - 1)]))));
+                    if (P >= 1 && Q <= tj - 1) Gb = cadd(Gb, cscale(sw.w[1][e], cmul(l, cconj(up[(P - 1) * tj + Q]))));
+                    if (P <= tj - 1 && Q >= 1) Gbs = cadd(Gbs, cscale(-sw.w[2][e], cmul(l, cconj(up[P * tj + (Q - 1)]))));
+                    if (P <= tj - 1 && Q <= tj - 1) Gas = cadd(Gas, cscale(sw.w[3][e], cmul(l, cconj(up[P * tj + Q]))));
+                }
+            }
+            // (b) lambda_{tj-1}[P][Q] = Y[P][Q] + sum of conj(coef) * w * lambda_tj over the 4 users
+            if (tj >= 2) {
+                cplx* ln = s_l[w][(tj - 1) & 1];
+                const int eo = block_offset(tj);
+#pragma unroll
+                for (int s = 0; s < level_slots(tj - 1); ++s) {
+                    const int idx = lane + 32 * s;
+                    if (idx < level_size(tj - 1)) {
+                        const int P = idx / tj, Q = idx % tj;
+                        const int e11 = (P + 1) * (tj + 1) + (Q + 1), e10 = (P + 1) * (tj + 1) + Q;
+                        const int e01 = P * (tj + 1) + (Q + 1), e00 = P * (tj + 1) + Q;
+                        cplx v = y[slot_base(tj - 1) + s];
+                        v = cadd(v, cscale(sw.w[0][eo + e11], cmul(lam[e11], cconj(g.a))));
+                        v = cadd(v, cscale(sw.w[1][eo + e10], cmul(lam[e10], cconj(g.b))));
+                        v = cadd(v, cscale(-sw.w[2][eo + e01], cmul(lam[e01], g.b)));
+                        v = cadd(v, cscale(sw.w[3][eo + e00], cmul(lam[e00], g.a)));
+                        ln[idx] = v;
                     }
                 }
             }
             __syncwarp();
         }
+        // t_d per lane (linear in the lane's partial sums), then one warp reduction
+        cplx da[3], db[3];
+        const double d[3] = {dx, dy, dz};
+        pair_grads(d, g, rc, z0, r0, da, db);
+        double t[3];
 #pragma unroll
-        for (int d = 0; d < 3; ++d) t[d] = mdkk::warp_sum(t[d]);
+        for (int q = 0; q < 3; ++q) {
+            const double re = (Ga.re * da[q].re + Ga.im * da[q].im) + (Gas.re * da[q].re - Gas.im * da[q].im) +
+                              (Gb.re * db[q].re + Gb.im * db[q].im) + (Gbs.re * db[q].re - Gbs.im * db[q].im);
+            t[q] = mdkk::warp_sum(g.dfc * (d[q] / g.r) * S + g.fc * re);
+        }
         if (lane == 0) {
             fi[0] += t[0];
             fi[1] += t[1];
@@ -323,17 +419,17 @@ __global__ void __launch_bounds__(kWarps * 32) k_snap_deidrj(const double* __res
 void upload_weights() {
     static bool done = false;
     if (done) return;
-    double h[block_offset(kMaxTwoJ + 1)][4] = {};
+    static double h[4][block_offset(kMaxTwoJ + 1)] = {};
     for (int tj = 1; tj <= kMaxTwoJ; ++tj)
         for (int P = 0; P <= tj; ++P)
             for (int Q = 0; Q <= tj; ++Q) {
-                double* wv = h[block_offset(tj) + P * (tj + 1) + Q];
-                wv[0] = std::sqrt((double)(P * Q)) / tj;
-                wv[1] = std::sqrt((double)(P * (tj - Q))) / tj;
-                wv[2] = std::sqrt((double)((tj - P) * Q)) / tj;
-                wv[3] = std::sqrt((double)((tj - P) * (tj - Q))) / tj;
+                const int e = block_offset(tj) + P * (tj + 1) + Q;
+                h[0][e] = std::sqrt((double)(P * Q)) / tj;
+                h[1][e] = std::sqrt((double)(P * (tj - Q))) / tj;
+                h[2][e] = std::sqrt((double)((tj - P) * Q)) / tj;
+                h[3][e] = std::sqrt((double)((tj - P) * (tj - Q))) / tj;
             }
-    cudaMemcpyToSymbol(c_w, h, sizeof(h));
+    cudaMemcpyToSymbol(g_w, h, sizeof(h));
     done = true;
 }
 
@@ -366,7 +462,8 @@ int mdkk_snap_create(mdkk_ctx* ctx, int twojmax, int n_contrib, const int* f_sta
     s->n_flat = block_offset(twojmax + 1);
     s->n_contrib = n_contrib;
     std::vector<int4> c(std::max(n_contrib, 1));
-    for (int k = 0; k < n_contrib; ++k) c[k] = make_int4(g_host[k], h_host[k], conj_host[k], 0);
+    for (int f = 0; f < s->n_flat; ++f)
+        for (int k = f_start_host[f]; k < f_start_host[f + 1]; ++k) c[k] = make_int4(g_host[k], h_host[k], conj_host[k], f);
     cudaError_t e = cudaMalloc(&s->f_start, sizeof(int) * (s->n_flat + 1));
     if (e == cudaSuccess) e = cudaMalloc(&s->contrib, sizeof(int4) * c.size());
     if (e == cudaSuccess) e = cudaMalloc(&s->coef, sizeof(double) * c.size());
@@ -414,11 +511,24 @@ int mdkk_snap_yi(mdkk_ctx* ctx, mdkk_snap* s, const double* U, int n_local, doub
         cudaMemsetAsync(energy, 0, sizeof(double), st);
         return MDKK_OK;
     }
-    const int nb = mdkk::grid_for(n_local, 128);
+    const int nb = (n_local + kYWarps - 1) / kYWarps;
     double* partials = static_cast<double*>(mdkk::scratch(ctx, sizeof(double) * (size_t)nb));
     if (!partials) return mdkk::cuda_fail(cudaErrorMemoryAllocation, "scratch");
-    k_snap_yi<<<nb, 128, 0, st>>>(reinterpret_cast<const double2*>(U), n_local, s->n_flat, s->f_start, s->contrib,
-                                  s->coef, reinterpret_cast<double2*>(Y), partials);
+    const double2* u = reinterpret_cast<const double2*>(U);
+    double2* y = reinterpret_cast<double2*>(Y);
+    switch (s->twojmax) {
+#define MDKK_YI(TJ)                                                                                              \
+    case TJ: {                                                                                                   \
+        constexpr int NF = block_offset(TJ + 1);                                                                 \
+        const size_t sm = 32 * 33 * (sizeof(int4) + sizeof(double)) + kYWarps * NF * (sizeof(double2) + 2 * sizeof(double)); \
+        cudaFuncSetAttribute(k_snap_yi<NF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);              \
+        k_snap_yi<NF><<<nb, kYWarps * 32, sm, st>>>(u, n_local, s->n_contrib, s->contrib, s->coef, y, partials); \
+        break;                                                                                                   \
+    }
+        MDKK_YI(0) MDKK_YI(1) MDKK_YI(2) MDKK_YI(3) MDKK_YI(4) MDKK_YI(5) MDKK_YI(6) MDKK_YI(7) MDKK_YI(8)
+#undef MDKK_YI
+        default: return MDKK_E_ARG;
+    }
     MDKK_CHECK_LAUNCH("k_snap_yi");
     mdkk::reduce_partials(partials, nb, 1, energy, st);
     MDKK_CHECK_LAUNCH("k_reduce_partials");

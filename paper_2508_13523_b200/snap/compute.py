@@ -3,7 +3,7 @@
 `build_neighbor_map`, `SnapState`, `compute_ui`, `compute_yi`,
 `compute_fused_deidrj`, `compute_energy`, `energy_from_y` keep the reference
 signatures (mdkk/snap/compute.py:105-436).  U and Y live in HBM as complex128
-[n_flat][n_atoms] (atom fastest — the reference's layout "b"); the
+row-major [n_atoms][n_flat] (the reference's layout "a"); the
 `layout` / `batch_u` / `batch_y` / `tile_v` knobs are accepted for signature
 parity (the reference guarantees they never change results,
 mdkk/snap/compute.py:238-276) and do not change the GPU schedule.
@@ -89,11 +89,11 @@ class SnapState:
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         nf = self.index.n_flat
         shape = (max(1, self.n_atoms), nf)
-        tr = LayoutPolicy.transposed(2)
-        self.U_dev = torch.zeros((nf, max(1, self.n_atoms)), dtype=torch.complex128, device=self.device)
+        rm = LayoutPolicy.row_major(2)   # device rows are atoms: one warp streams one atom's 285 entries
+        self.U_dev = torch.zeros(shape, dtype=torch.complex128, device=self.device)
         self.Y_dev = torch.zeros_like(self.U_dev)
-        self.U = DualArray(shape, layout_b=tr, dtype=np.complex128, device=self.device, storage_b=self.U_dev)
-        self.Y = DualArray(shape, layout_b=tr, dtype=np.complex128, device=self.device, storage_b=self.Y_dev)
+        self.U = DualArray(shape, layout_b=rm, dtype=np.complex128, device=self.device, storage_b=self.U_dev)
+        self.Y = DualArray(shape, layout_b=rm, dtype=np.complex128, device=self.device, storage_b=self.Y_dev)
         self.energy_dev = torch.zeros(1, dtype=torch.float64, device=self.device)
         self.flags = torch.zeros(1, dtype=torch.int32, device=self.device)
         self._handle = None
