@@ -168,13 +168,17 @@ int mdkk_kinetic(mdkk_ctx* ctx, const double* v, int n, double mass, double* ke,
  * (the reference's layout "a"); n_flat = sum_{tj<=2J} (tj+1)^2.
  * Pairs are the entries of a FULL cluster-blocked table with r^2 < rc^2.
  *
- * mdkk_snap_create copies the output-sorted adjoint contribution list
- *   Y[f] = sum_{k in [f_start[f], f_start[f+1])} coef[k] * op(U[g[k]]) * U[h[k]],
- *   op = conj when conj[k] != 0   (mdkk/snap/compute.py:303-340)
- * built on the host from the exact Clebsch-Gordan terms and beta
- * (mdkk/snap/coupling.py:106-133); 0 <= 2J <= 8. */
-int mdkk_snap_create(mdkk_ctx* ctx, int twojmax, int n_contrib, const int* f_start_host, const int* g_host,
-                     const int* h_host, const int* conj_host, const double* coef_host, mdkk_snap** out_host);
+ * mdkk_snap_create copies the half-block adjoint table built on the host from
+ * the exact Clebsch-Gordan terms and beta (mdkk/snap/coupling.py:106-133,
+ * mdkk/snap/compute.py:303-340):
+ *   Y[f] = sum_k coef[k] * op(U[g_k]) * U[h_k]   (op = conj for slot-1/2 terms)
+ * for the n_half outputs with 2p < tj or (2p == tj, 2q <= tj), in rows of 32
+ * entries sharing one output (row_f[r] = its half index), gh[k] = g | h << 12 |
+ * conj << 24; the other outputs follow from Y[tj-p][tj-q] = (-1)^(p+q)
+ * conj(Y[p][q]) via fmap[f] = half index | mirrored << 16 | odd sign << 17.
+ * 0 <= 2J <= 8. */
+int mdkk_snap_create(mdkk_ctx* ctx, int twojmax, int n_rows, const int* row_f_host, const int* gh_host,
+                     const double* coef_host, int n_half, const int* fmap_host, mdkk_snap** out_host);
 int mdkk_snap_destroy(mdkk_snap* snap);
 /* U_i = sum_k f_c(r_ik) u(a_ik, b_ik) (compute_ui, mdkk/snap/compute.py:279-292); flags gets
  * MDKK_FLAG_COINCIDENT for r = 0 pairs (mdkk/snap/compute.py:117-118). */

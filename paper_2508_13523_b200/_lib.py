@@ -51,7 +51,7 @@ SIGNATURES = {
     "mdkk_verlet_first": [_p, _p, _p, _p, _p, _i, _d, _d, _p, _p],
     "mdkk_verlet_second": [_p, _p, _p, _i, _d, _d, _p, _p],
     "mdkk_kinetic": [_p, _p, _i, _d, _p, _p],
-    "mdkk_snap_create": [_p, _i, _i, _p, _p, _p, _p, _p, _p],
+    "mdkk_snap_create": [_p, _i, _i, _p, _p, _p, _i, _p, _p],
     "mdkk_snap_destroy": [_p],
     "mdkk_snap_ui": [_p, _p, _i, _p, _p, _i, _d, _p, _p, _p],
     "mdkk_snap_yi": [_p, _p, _p, _i, _p, _p, _p],

@@ -24,10 +24,12 @@
 struct mdkk_snap {
     int twojmax = 0;
     int n_flat = 0;
-    int n_contrib = 0;
-    int* f_start = nullptr;     // [n_flat + 1]
-    int4* contrib = nullptr;    // {g, h, conj, f}
-    double* coef = nullptr;     // [n_contrib]
+    int n_half = 0;
+    int n_rows = 0;
+    int* row_f = nullptr;   // [n_rows] half-block output of each 32-entry row
+    int* gh = nullptr;      // [n_rows*32] g | h << 12 | conj << 24
+    double* coef = nullptr; // [n_rows*32]
+    int* fmap = nullptr;    // [n_flat] half index | mirrored << 16 | odd sign << 17
 };
 
 namespace {
@@ -190,84 +192,82 @@ __global__ void __launch_bounds__(kWarps * 32) k_snap_ui(const double* __restric
 }
 
 // ---------------------------------------------------------------- compute_yi
-// Y_i[f] = sum_k coef_k op(U_i[g_k]) U_i[h_k] (op = conj for slot-1/2 terms) and
-// e_i = Re sum_f Y_i[f] conj(U_i[f]) / 3 (energy_from_y, mdkk/snap/compute.py:376-387).
-// One warp per atom (8 atoms per CTA).  U_i and the Y_i accumulator live in
-// shared memory; the contribution table is streamed through shared memory in
-// chunks shared by the CTA's 8 atoms.  Lane l takes 32 consecutive entries of a
-// chunk (stored transposed -> conflict-free) and flushes its running sum with a
-// shared-memory atomic only when the output index f changes.
+// Y_i[f] = sum_k coef_k op(U_i[g_k]) U_i[h_k] (op = conj for slot-1/2 terms,
+// mdkk/snap/compute.py:303-340) for the half-block outputs only; the mirror
+// half follows from Y[tj-p][tj-q] = (-1)^(p+q) conj(Y[p][q]).  Also
+// e_i = Re sum_f Y_i[f] conj(U_i[f]) / 3 (energy_from_y, :376-387).
+// One warp per atom, 8 atoms per CTA; the contribution table is streamed
+// through shared memory in rows of 32 entries that share one output, sorted by
+// (g, h) so the lanes' U_i reads fall on neighbouring banks; each output is
+// one warp reduction (no atomics).
 constexpr int kYWarps = 8;
-constexpr int kYChunk = 1024;
+constexpr int kYRows = 32;
 
-template <int NF>
-__global__ void __launch_bounds__(kYWarps * 32) k_snap_yi(const double2* __restrict__ U, int n, int n_contrib,
-                                                          const int4* __restrict__ contrib,
-                                                          const double* __restrict__ coef, double2* __restrict__ Y,
+template <int NF, int NH>
+__global__ void __launch_bounds__(kYWarps * 32) k_snap_yi(const double2* __restrict__ U, int n, int n_rows,
+                                                          const int* __restrict__ row_f, const int* __restrict__ gh,
+                                                          const double* __restrict__ coef,
+                                                          const int* __restrict__ fmap, double2* __restrict__ Y,
                                                           double* __restrict__ partials) {
-    extern __shared__ double4 s_dyn[];  // dynamic: > 48 KB
-    auto s_t = reinterpret_cast<int4(*)[33]>(s_dyn);                       // [32][33] entry-in-lane x lane
-    auto s_c = reinterpret_cast<double(*)[33]>(s_t + 32);                  // [32][33]
-    auto s_u = reinterpret_cast<double2(*)[NF]>(s_c + 32);                 // [kYWarps][NF]
-    auto s_yr = reinterpret_cast<double(*)[NF]>(s_u + kYWarps);            // [kYWarps][NF]
-    auto s_yi = reinterpret_cast<double(*)[NF]>(s_yr + kYWarps);
+    extern __shared__ double2 s_dyn2[];
+    auto s_u = reinterpret_cast<double2(*)[NF]>(s_dyn2);                  // [kYWarps][NF]
+    auto s_yh = reinterpret_cast<double2(*)[NH]>(s_u + kYWarps);          // [kYWarps][NH]
+    auto s_cf = reinterpret_cast<double(*)[32]>(s_yh + kYWarps);          // [kYRows][32]
+    auto s_gh = reinterpret_cast<int(*)[32]>(s_cf + kYRows);              // [kYRows][32]
+    int* s_rf = reinterpret_cast<int*>(s_gh + kYRows);                    // [kYRows]
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int i = blockIdx.x * kYWarps + w;
     const bool valid = i < n;
-    for (int f = lane; f < NF; f += 32) {
-        s_u[w][f] = valid ? U[(long long)i * NF + f] : make_double2(0.0, 0.0);
-        s_yr[w][f] = 0.0;
-        s_yi[w][f] = 0.0;
-    }
-    for (int base = 0; base < n_contrib; base += kYChunk) {
+    for (int f = lane; f < NF; f += 32) s_u[w][f] = valid ? U[(long long)i * NF + f] : make_double2(0.0, 0.0);
+    int cur = -1;
+    double are = 0.0, aim = 0.0;
+    for (int base = 0; base < n_rows; base += kYRows) {
+        const int nr = min(kYRows, n_rows - base);
         __syncthreads();
-        for (int t = threadIdx.x; t < kYChunk; t += blockDim.x) {
-            const int k = base + t;
-            const int l = t >> 5, p = t & 31;  // entry t belongs to lane l, position p
-            s_t[p][l] = k < n_contrib ? __ldg(contrib + k) : make_int4(0, 0, 0, -1);
-            s_c[p][l] = k < n_contrib ? __ldg(coef + k) : 0.0;
+        for (int t = threadIdx.x; t < nr * 32; t += blockDim.x) {
+            s_gh[t >> 5][t & 31] = __ldg(gh + (long long)base * 32 + t);
+            s_cf[t >> 5][t & 31] = __ldg(coef + (long long)base * 32 + t);
         }
+        for (int t = threadIdx.x; t < nr; t += blockDim.x) s_rf[t] = __ldg(row_f + base + t);
         __syncthreads();
-        if (valid) {
-            int cur = -1;
-            double are = 0.0, aim = 0.0;
-#pragma unroll 4
-            for (int p = 0; p < 32; ++p) {
-                const int4 t = s_t[p][lane];
-                if (t.w != cur) {
-                    if (cur >= 0) {
-                        atomicAdd(&s_yr[w][cur], are);
-                        atomicAdd(&s_yi[w][cur], aim);
-                    }
-                    cur = t.w;
-                    are = aim = 0.0;
+        if (!valid) continue;
+        for (int r = 0; r < nr; ++r) {
+            const int fr = s_rf[r];
+            if (fr != cur) {  // warp-uniform
+                if (cur >= 0) {
+                    const double sr = mdkk::warp_sum(are), si = mdkk::warp_sum(aim);
+                    if (lane == 0) s_yh[w][cur] = make_double2(sr, si);
                 }
-                if (t.w >= 0) {
-                    const double c = s_c[p][lane];
-                    const double2 ug = s_u[w][t.x];
-                    const double2 uh = s_u[w][t.y];
-                    const double gi = t.z ? -ug.y : ug.y;
-                    are += c * (ug.x * uh.x - gi * uh.y);
-                    aim += c * (ug.x * uh.y + gi * uh.x);
-                }
+                cur = fr;
+                are = aim = 0.0;
             }
-            if (cur >= 0) {
-                atomicAdd(&s_yr[w][cur], are);
-                atomicAdd(&s_yi[w][cur], aim);
-            }
+            const int e = s_gh[r][lane];
+            const double c = s_cf[r][lane];
+            const double2 ug = s_u[w][e & 0xfff];
+            const double2 uh = s_u[w][(e >> 12) & 0xfff];
+            const double gi = (e >> 24) ? -ug.y : ug.y;
+            are += c * (ug.x * uh.x - gi * uh.y);
+            aim += c * (ug.x * uh.y + gi * uh.x);
         }
     }
-    __syncthreads();
-    double e[1] = {0.0};
+    double en[1] = {0.0};
     if (valid) {
-        for (int f = lane; f < NF; f += 32) {
-            const double yr = s_yr[w][f], yi = s_yi[w][f];
-            Y[(long long)i * NF + f] = make_double2(yr, yi);
-            e[0] += yr * s_u[w][f].x + yi * s_u[w][f].y;  // Re(Y conj(U))
+        if (cur >= 0) {
+            const double sr = mdkk::warp_sum(are), si = mdkk::warp_sum(aim);
+            if (lane == 0) s_yh[w][cur] = make_double2(sr, si);
         }
-        e[0] /= 3.0;
+        __syncwarp();
+        for (int f = lane; f < NF; f += 32) {
+            const int m = __ldg(fmap + f);
+            double2 v = s_yh[w][m & 0xffff];
+            if ((m >> 16) & 1) v.y = -v.y;
+            if ((m >> 17) & 1) v = make_double2(-v.x, -v.y);
+            Y[(long long)i * NF + f] = v;
+            en[0] += v.x * s_u[w][f].x + v.y * s_u[w][f].y;  // Re(Y conj(U))
+        }
+        en[0] /= 3.0;
     }
-    mdkk::block_sum<1, kYWarps * 32>(e, partials + blockIdx.x);
+    mdkk::block_sum<1, kYWarps * 32>(en, partials + blockIdx.x);
 }
 
 // ------------------------------------------------------- compute_fused_deidrj
@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(kYWarps * 32) k_snap_yi(const double2* __restr
 //   t_d = f_c' rhat_d Re sum Y conj(u) + f_c Re(G_a conj(da_d) + G_a* da_d + G_b conj(db_d) + G_b* db_d).
 // Same quantity (equal to rounding), 12 instead of 28 complex MACs per element.
 template <int TWOJ>
-__global__ void __launch_bounds__(kWarps * 32) k_snap_deidrj(const double* __restrict__ x, int n_local,
+__global__ void __launch_bounds__(kWarps * 32, 3) k_snap_deidrj(const double* __restrict__ x, int n_local,
                                                              const int* __restrict__ table,
                                                              const int* __restrict__ counts, int cap, double rc,
                                                              const double2* __restrict__ Y,
@@ -451,30 +451,32 @@ void upload_weights() {
 
 extern "C" {
 
-int mdkk_snap_create(mdkk_ctx* ctx, int twojmax, int n_contrib, const int* f_start_host, const int* g_host,
-                     const int* h_host, const int* conj_host, const double* coef_host, mdkk_snap** out_host) {
-    if (!ctx || !out_host || twojmax < 0 || twojmax > kMaxTwoJ || n_contrib < 0) {
+int mdkk_snap_create(mdkk_ctx* ctx, int twojmax, int n_rows, const int* row_f_host, const int* gh_host,
+                     const double* coef_host, int n_half, const int* fmap_host, mdkk_snap** out_host) {
+    static const int kHalf[kMaxTwoJ + 1] = {1, 3, 8, 16, 29, 47, 72, 104, 145};
+    if (!ctx || !out_host || twojmax < 0 || twojmax > kMaxTwoJ || n_rows < 0 || n_half != kHalf[twojmax]) {
         mdkk::set_error("mdkk_snap_create: 2J must be in [0, 8]");
         return MDKK_E_ARG;
     }
     auto* s = new mdkk_snap();
     s->twojmax = twojmax;
     s->n_flat = block_offset(twojmax + 1);
-    s->n_contrib = n_contrib;
-    std::vector<int4> c(std::max(n_contrib, 1));
-    for (int f = 0; f < s->n_flat; ++f)
-        for (int k = f_start_host[f]; k < f_start_host[f + 1]; ++k) c[k] = make_int4(g_host[k], h_host[k], conj_host[k], f);
-    cudaError_t e = cudaMalloc(&s->f_start, sizeof(int) * (s->n_flat + 1));
-    if (e == cudaSuccess) e = cudaMalloc(&s->contrib, sizeof(int4) * c.size());
-    if (e == cudaSuccess) e = cudaMalloc(&s->coef, sizeof(double) * c.size());
-    if (e == cudaSuccess) e = cudaMemcpy(s->f_start, f_start_host, sizeof(int) * (s->n_flat + 1), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess && n_contrib)
-        e = cudaMemcpy(s->contrib, c.data(), sizeof(int4) * n_contrib, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess && n_contrib) e = cudaMemcpy(s->coef, coef_host, sizeof(double) * n_contrib, cudaMemcpyHostToDevice);
+    s->n_half = n_half;
+    s->n_rows = n_rows;
+    const size_t ne = (size_t)std::max(n_rows, 1) * 32;
+    cudaError_t e = cudaMalloc(&s->row_f, sizeof(int) * std::max(n_rows, 1));
+    if (e == cudaSuccess) e = cudaMalloc(&s->gh, sizeof(int) * ne);
+    if (e == cudaSuccess) e = cudaMalloc(&s->coef, sizeof(double) * ne);
+    if (e == cudaSuccess) e = cudaMalloc(&s->fmap, sizeof(int) * s->n_flat);
+    if (e == cudaSuccess && n_rows) e = cudaMemcpy(s->row_f, row_f_host, sizeof(int) * n_rows, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && n_rows) e = cudaMemcpy(s->gh, gh_host, sizeof(int) * n_rows * 32, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && n_rows) e = cudaMemcpy(s->coef, coef_host, sizeof(double) * n_rows * 32, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(s->fmap, fmap_host, sizeof(int) * s->n_flat, cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
-        cudaFree(s->f_start);
-        cudaFree(s->contrib);
+        cudaFree(s->row_f);
+        cudaFree(s->gh);
         cudaFree(s->coef);
+        cudaFree(s->fmap);
         delete s;
         return mdkk::cuda_fail(e, "mdkk_snap_create");
     }
@@ -485,9 +487,10 @@ int mdkk_snap_create(mdkk_ctx* ctx, int twojmax, int n_contrib, const int* f_sta
 
 int mdkk_snap_destroy(mdkk_snap* s) {
     if (!s) return MDKK_OK;
-    cudaFree(s->f_start);
-    cudaFree(s->contrib);
+    cudaFree(s->row_f);
+    cudaFree(s->gh);
     cudaFree(s->coef);
+    cudaFree(s->fmap);
     delete s;
     return MDKK_OK;
 }
@@ -517,15 +520,18 @@ int mdkk_snap_yi(mdkk_ctx* ctx, mdkk_snap* s, const double* U, int n_local, doub
     const double2* u = reinterpret_cast<const double2*>(U);
     double2* y = reinterpret_cast<double2*>(Y);
     switch (s->twojmax) {
-#define MDKK_YI(TJ)                                                                                              \
+#define MDKK_YI(TJ, NH)                                                                                          \
     case TJ: {                                                                                                   \
         constexpr int NF = block_offset(TJ + 1);                                                                 \
-        const size_t sm = 32 * 33 * (sizeof(int4) + sizeof(double)) + kYWarps * NF * (sizeof(double2) + 2 * sizeof(double)); \
-        cudaFuncSetAttribute(k_snap_yi<NF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);              \
-        k_snap_yi<NF><<<nb, kYWarps * 32, sm, st>>>(u, n_local, s->n_contrib, s->contrib, s->coef, y, partials); \
+        const size_t sm = kYWarps * (NF + NH) * sizeof(double2) + kYRows * 32 * (sizeof(double) + sizeof(int)) + \
+                          kYRows * sizeof(int);                                                                 \
+        cudaFuncSetAttribute(k_snap_yi<NF, NH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);          \
+        k_snap_yi<NF, NH><<<nb, kYWarps * 32, sm, st>>>(u, n_local, s->n_rows, s->row_f, s->gh, s->coef, s->fmap, \
+                                                        y, partials);                                           \
         break;                                                                                                   \
     }
-        MDKK_YI(0) MDKK_YI(1) MDKK_YI(2) MDKK_YI(3) MDKK_YI(4) MDKK_YI(5) MDKK_YI(6) MDKK_YI(7) MDKK_YI(8)
+        MDKK_YI(0, 1) MDKK_YI(1, 3) MDKK_YI(2, 8) MDKK_YI(3, 16) MDKK_YI(4, 29) MDKK_YI(5, 47) MDKK_YI(6, 72)
+        MDKK_YI(7, 104) MDKK_YI(8, 145)
 #undef MDKK_YI
         default: return MDKK_E_ARG;
     }

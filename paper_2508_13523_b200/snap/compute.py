@@ -18,7 +18,7 @@ import torch
 
 from .. import _lib
 from ..memspace import DualArray, LayoutPolicy
-from .coupling import CouplingTables, adjoint_contributions
+from .coupling import CouplingTables, adjoint_rows
 
 
 class SnapError(RuntimeError):
@@ -54,14 +54,14 @@ class _Handle:
     """Device copy of the adjoint contribution table (mdkk_snap_create)."""
 
     def __init__(self, tables: CouplingTables, beta: np.ndarray, device):
-        fs, g, h, cj, coef = adjoint_contributions(tables, beta)
+        row_f, gh, coef, fmap, n_half = adjoint_rows(tables, beta)
         out = C.c_void_p()
         with torch.cuda.device(device):
             _lib.check(_lib.lib().mdkk_snap_create(
-                _lib.ctx(device), tables.index.twojmax, len(coef), fs.ctypes.data, g.ctypes.data, h.ctypes.data,
-                cj.ctypes.data, coef.ctypes.data, C.byref(out)), "mdkk_snap_create")
+                _lib.ctx(device), tables.index.twojmax, len(row_f), row_f.ctypes.data, gh.ctypes.data,
+                coef.ctypes.data, n_half, fmap.ctypes.data, C.byref(out)), "mdkk_snap_create")
         self.ptr = out.value
-        self.n_contrib = len(coef)
+        self.n_contrib = int((coef != 0).sum())
 
     def __del__(self):
         try:

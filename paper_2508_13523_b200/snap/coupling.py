@@ -166,3 +166,57 @@ def read_coeff_file(path):
     if len(beta) != need:
         raise SnapError(f"coefficient file {path}: expected {need} beta values for jmax {jmax}, got {len(beta)}")
     return jmax, beta
+
+
+def half_block_outputs(twojmax: int):
+    """Flat indices with 2p < tj, or 2p == tj and 2q <= tj: one of each mirror pair.
+
+    Every U/Y block obeys X[tj-p][tj-q] = (-1)^(p+q) conj(X[p][q]) (SURVEY §7,
+    verified on mdkk's U and full adjoint Y), so the other half follows.
+    """
+    off = QuantumIndex(twojmax / 2.0).block_offset
+    keep, fmap = [], []
+    for tj in range(twojmax + 1):
+        for p in range(tj + 1):
+            for q in range(tj + 1):
+                if 2 * p < tj or (2 * p == tj and 2 * q <= tj):
+                    keep.append(int(off[tj] + p * (tj + 1) + q))
+    pos = {f: k for k, f in enumerate(keep)}
+    for tj in range(twojmax + 1):
+        for p in range(tj + 1):
+            for q in range(tj + 1):
+                f = int(off[tj] + p * (tj + 1) + q)
+                if f in pos:
+                    fmap.append(pos[f])
+                else:
+                    m = int(off[tj] + (tj - p) * (tj + 1) + (tj - q))
+                    fmap.append(pos[m] | (1 << 16) | ((((p + q) & 1)) << 17))
+    return np.array(keep, dtype=np.int32), np.array(fmap, dtype=np.int32)
+
+
+def adjoint_rows(tables: CouplingTables, beta, width: int = 32):
+    """Device table for the half-block adjoint: rows of `width` contributions sharing one output.
+
+    Returns (row_f, gh, coef, fmap): row_f[r] is the half-block index of row r's
+    output, gh packs g | h << 12 | conj << 24, coef is zero on padding entries,
+    and fmap maps every flat index to (half index | mirrored << 16 | odd-sign << 17).
+    Contributions inside an output are sorted by (g, h) so a warp's 32 lanes read
+    neighbouring U entries.
+    """
+    f_start, g, h, cj, coef = adjoint_contributions(tables, beta)
+    keep, fmap = half_block_outputs(tables.index.twojmax)
+    row_f, gh, cf = [], [], []
+    for k, f in enumerate(keep):
+        a, b = int(f_start[f]), int(f_start[f + 1])
+        o = np.lexsort((h[a:b], g[a:b])) + a
+        n = b - a
+        pad = (-n) % width
+        if n == 0:
+            continue
+        gh.append(np.concatenate([g[o] | (h[o] << 12) | (cj[o] << 24), np.zeros(pad, np.int32)]))
+        cf.append(np.concatenate([coef[o], np.zeros(pad)]))
+        row_f.extend([k] * ((n + pad) // width))
+    if not row_f:
+        return (np.zeros(0, np.int32), np.zeros(0, np.int32), np.zeros(0), fmap, len(keep))
+    return (np.array(row_f, dtype=np.int32), np.concatenate(gh).astype(np.int32), np.concatenate(cf),
+            fmap, len(keep))
