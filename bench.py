@@ -40,7 +40,8 @@ def _peaks():
 
 
 def lj_script(cells, style_newton_thermo=10 ** 9, steps=0):
-    return (f"units lj\nboundary p p p\nlattice fcc {LJ['rho']}\ncreate_box {cells} {cells} {cells}\n"
+    cx, cy, cz = cells if isinstance(cells, tuple) else (cells, cells, cells)
+    return (f"units lj\nboundary p p p\nlattice fcc {LJ['rho']}\ncreate_box {cx} {cy} {cz}\n"
             f"create_atoms\nmass 1.0\nvelocity {LJ['T']} {LJ['seed']}\npair_style lj/cut {LJ['rc']}\n"
             f"pair_coeff 1.0 1.0\ntimestep {LJ['dt']}\nthermo {style_newton_thermo}\n")
 
@@ -137,12 +138,12 @@ def run_reference(args):
 
 
 # -------------------------------------------------------------------- GPU
-def lj_run(style, cells, steps, warmup, device, profile=True):
+def lj_run(style, cells, steps, warmup, device, profile=True, distributed=False):
     import torch
     from paper_2508_13523_b200 import _lib
     from paper_2508_13523_b200.driver import RunConfig, Simulation
-    sim = Simulation(RunConfig(list_style=style, newton=(style == "half"), skin=LJ["skin"], device=device),
-                     log=None)
+    sim = Simulation(RunConfig(list_style=style, newton=(style == "half"), skin=LJ["skin"], device=device,
+                               distributed=distributed), log=None)
     sim.execute(lj_script(cells))
     sim._ensure_system()
     sim._forces_device()
@@ -165,11 +166,16 @@ def lj_run(style, cells, steps, warmup, device, profile=True):
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(device.index or 0) as clk:
         torch.cuda.synchronize()
+        if distributed:
+            import torch.distributed as dist
+            dist.barrier()
         start.record()
         for _ in range(steps):
             sim.step_device()
         end.record()
         torch.cuda.synchronize()
+        if distributed:
+            dist.barrier()
     ms = start.elapsed_time(end) / steps
     launches = _lib.launch_count() - l0
     fms = float(np.mean([a.elapsed_time(b) for a, b in fev])) if fev else None
@@ -254,12 +260,12 @@ def snap_run(cells, steps, warmup, device):
                 nn=nn, launches=_lib.launch_count() - l0, e_pot=float(sim._e_dev.item()))
 
 
-def lj_e2e(style, cells, steps, device):
+def lj_e2e(style, cells, steps, device, distributed=False):
     """Public API end to end: host arrays -> distribute/build -> run_nve(steps) -> thermo + gid-ordered D2H."""
     import torch
     from paper_2508_13523_b200.driver import RunConfig, Simulation
-    sim = Simulation(RunConfig(list_style=style, newton=(style == "half"), skin=LJ["skin"], device=device),
-                     log=None)
+    sim = Simulation(RunConfig(list_style=style, newton=(style == "half"), skin=LJ["skin"], device=device,
+                               distributed=distributed), log=None)
     sim.execute(lj_script(cells, style_newton_thermo=steps))
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -306,27 +312,39 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=device)
 
-    full = lj_run("full", args.cells, args.steps, args.warmup, device)
-    half = lj_run("half", args.cells, args.steps, args.warmup, device)
-    ms = full["ms"]
-    if world > 1:
+    # weak scaling: an 80^3-cell fcc brick (2,048,000 atoms) per GPU, bricks tiled by decompose(N)
+    from paper_2508_13523_b200.domain import Box as _Box, decompose as _decompose
+    grid = _decompose(_Box((1.0, 1.0, 1.0)), world).grid
+    cells = tuple(args.cells * g for g in grid)
+    distributed = world > 1
+
+    def max_over_ranks(v):
+        if not distributed:
+            return v
         import torch.distributed as dist
-        t = torch.tensor([ms], device=device, dtype=torch.float64)
+        t = torch.tensor([v], device=device, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    n_atoms = full["n_atoms"] * world   # independent replicas until the DD path lands
+        return float(t.item())
+
+    full = lj_run("full", cells, args.steps, args.warmup, device, distributed=distributed)
+    half = lj_run("half", cells, args.steps, args.warmup, device, distributed=distributed)
+    ms = max_over_ranks(full["ms"])
+    half_ms = max_over_ranks(half["ms"])
+    n_atoms = full["n_atoms"]           # global atom count (all bricks)
     value = n_atoms / (ms * 1e-3) / 1e6
     peak, peak_kind = _peaks()
     nn = full["nn"]
-    bytes_per_launch = full["n_atoms"] * (28.0 * nn + 52.0)
+    bytes_per_launch = full["n_atoms"] / world * (28.0 * nn + 52.0)
     achieved = bytes_per_launch / (full["force_ms"] * 1e-3) / 1e9
-    e2e = lj_e2e("full", args.cells, max(args.steps, 20), device) if not args.no_e2e else None
+    e2e = lj_e2e("full", cells, max(args.steps, 20), device, distributed) if not args.no_e2e else None
+    if e2e is not None and distributed:
+        e2e["value"] = n_atoms * max(args.steps, 20) / max_over_ranks(n_atoms * max(args.steps, 20) / e2e["value"])
     snapr, fp64 = None, None
-    if not args.no_snap:
+    if not args.no_snap and not distributed:
         fp64 = fp64_peak(device)
         snapr = snap_run(args.snap_cells, args.snap_steps, 2, device)
     cpu = None
-    if rank == 0 and not args.no_cpu:
+    if rank == 0 and not args.no_cpu and not distributed:
         v, secs, n = cpu_lj_sample()
         cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "port",
                "sample": f"numpy oracle port, LJ melt {n} atoms (same rho/rc/skin/T/dt, full list), 20 steps "
@@ -337,16 +355,18 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "LJ 12-6 melt fcc rho*=0.8442, rc=2.5, skin=0.3, T=1.44, dt=0.005, "
-                                   "full list newton-off (configs[1])",
-                       "n_atoms": full["n_atoms"], "n_ghost": full["n_ghost"], "list": "full",
+                                   "full list newton-off (configs[1]; weak scaling: 80^3 fcc cells per GPU)",
+                       "n_atoms": full["n_atoms"], "n_ghost_rank0": full["n_ghost"], "list": "full",
+                       "grid": list(grid),
                        "rebuilds_in_timed_steps": full["rebuilds"], "mean_neighbors": nn,
                        "l2": "inputs (x,v,f,table ~%.0f MB) larger than L2" % (full["n_atoms"] * (nn * 4 + 96) / 1e6),
-                       "parallelism": "replicas" if world > 1 else "1 GPU"},
+                       "parallelism": (f"spatial DD {grid[0]}x{grid[1]}x{grid[2]}, NCCL halo exchange"
+                                       if world > 1 else "1 GPU")},
             "variants": {
                 "lj_full_newton_off": {"value": value, "ms_per_step": full["ms"], "force_ms": full["force_ms"],
                                        "rebuilds": full["rebuilds"]},
-                "lj_half_newton_on_atomics": {"value": half["n_atoms"] / (half["ms"] * 1e-3) / 1e6,
-                                              "ms_per_step": half["ms"], "force_ms": half["force_ms"],
+                "lj_half_newton_on_atomics": {"value": half["n_atoms"] / (half_ms * 1e-3) / 1e6,
+                                              "ms_per_step": half_ms, "force_ms": half["force_ms"],
                                               "rebuilds": half["rebuilds"], "mean_neighbors": half["nn"]},
             },
             "roofline": {"bound": "hbm", "kernel": "k_lj<full> (+ partial reduce)", "achieved": achieved,

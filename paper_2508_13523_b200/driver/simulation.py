@@ -40,7 +40,7 @@ class RunConfig:
                  list_style: str | None = None, newton: bool = True, skin: float = 0.3,
                  workers: int | None = None, batch_u: int | None = None, batch_y: int | None = None,
                  tile_v: int | None = None, layout: str | None = None, rng_seed: int | None = None,
-                 device=None):
+                 device=None, distributed: bool = False):
         if strategy not in ("serial", "duplicate", "atomic"):
             raise RunError(f"unknown strategy {strategy!r}; choose from ['atomic', 'duplicate', 'serial']")
         self.n_ranks = int(n_ranks)
@@ -53,6 +53,8 @@ class RunConfig:
         self.batch_u, self.batch_y, self.tile_v, self.layout = batch_u, batch_y, tile_v, layout
         self.rng_seed = rng_seed
         self.device = device
+        # one brick per process over torch.distributed (NCCL) instead of in-process logical ranks
+        self.distributed = bool(distributed)
 
 
 class LJStyle:
@@ -85,7 +87,7 @@ class LJStyle:
         for k, (s, nl) in enumerate(zip(system.stores, lists)):
             lj_force_rank(s, nl, self.kernel.params, evs[k], flags, virial=False)
             half |= nl.style == "half"
-        if half and any(s.n_ghost for s in system.stores):
+        if half:   # collective in the distributed system: every rank calls it
             system.reverse_comm()
         for s in system.stores:
             s.device_wrote(force=True)
@@ -282,8 +284,13 @@ class Simulation:
             raise RunError("create_atoms must run before run")
         if self.system is None:
             with torch.cuda.device(self.device):
-                self.system = RankedSystem.distribute(self.box, self.config.n_ranks, self._positions,
-                                                      self._velocities, device=self.device)
+                if self.config.distributed:
+                    from ..dist import DistSystem
+                    self.system = DistSystem.distribute(self.box, self._positions, self._velocities,
+                                                        device=self.device)
+                else:
+                    self.system = RankedSystem.distribute(self.box, self.config.n_ranks, self._positions,
+                                                          self._velocities, device=self.device)
             self.lists = None
         if self.lists is None:
             style_list = self.style.list_style or self.config.list_style or "half"
@@ -323,8 +330,14 @@ class Simulation:
             _lib.check(lib.mdkk_kinetic(_lib.ctx(self.device), s.v.data_ptr(), s.n_local, self.mass,
                                         ke[k:].data_ptr(), st), "mdkk_kinetic")
             n += s.n_local
-        k = float(ke.sum().item())
+        tot = torch.stack([ke.sum(), torch.tensor(float(n), dtype=torch.float64, device=self.device)])
+        k, n = (float(v) for v in self._global_sum(tot).cpu().numpy())
         return k, (2.0 * k / (3.0 * n) if n else 0.0)
+
+    def _global_sum(self, t: torch.Tensor) -> torch.Tensor:
+        if self.config.distributed:
+            return self.system.allreduce_sum(t.clone())
+        return t
 
     def _half_kick_drift(self) -> bool:
         """v += dt/2m f; x += dt v; returns whether any rank moved beyond skin/2 (one sync)."""
@@ -337,8 +350,10 @@ class Simulation:
                                              nl.ref_dev.data_ptr(), s.n_local, self.dt, h,
                                              self._d2[k:].data_ptr(), st), "mdkk_verlet_first")
             s.device_wrote(pos=True, vel=True)
-        worst = float(self._d2[: len(self.system.stores)].max().item())
-        return math.sqrt(worst) > 0.5 * self.config.skin
+        worst = self._d2[: len(self.system.stores)].max()
+        if self.config.distributed:   # any rank over skin/2 -> every rank rebuilds (mdkk/neighbor.py:230)
+            worst = self.system.allreduce_max(worst.reshape(1))
+        return math.sqrt(float(worst.item())) > 0.5 * self.config.skin
 
     def _half_kick(self):
         lib, st = _lib.lib(), _lib.stream(self.device)
@@ -385,7 +400,7 @@ class Simulation:
             rebuilds0 = self.n_rebuilds
 
             def log(step, e_dev):
-                e_pot = float(e_dev.item())
+                e_pot = float(self._global_sum(e_dev.reshape(1)).item())
                 self._check_finite(step, e_pot)
                 ke, t = self._kinetic()
                 result.log(step, e_pot, ke, t)

@@ -209,3 +209,24 @@ def test_c1_32k_trajectory_matches_reference(gpu, style):
     assert np.allclose(rows[:, 1:], ref[:, 1:], rtol=1e-8)
     snap = sim.results[-1].snapshots[100][::97]
     assert np.abs(snap - g[f"c1_{style}_final_pos_sub"]).max() < 1e-7
+
+
+def test_distributed_system_single_rank_nccl_matches_in_process(gpu):
+    """DistSystem (one brick per process, NCCL) at world_size 1 == RankedSystem, through run_script."""
+    import os
+    import torch.distributed as dist
+    from paper_2508_13523_b200.driver import RunConfig, run_script
+    c1 = ("units lj\nboundary p p p\nlattice fcc 0.8442\ncreate_box 8 8 8\ncreate_atoms\n"
+          "mass 1.0\nvelocity 1.44 87287\npair_style lj/cut 2.5\npair_coeff 1.0 1.0\n"
+          "timestep 0.005\nthermo 10\nrun 40\n")
+    ref = np.array(run_script(c1, RunConfig(list_style="full", newton=False), log=None).results[-1].rows)
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        for style in ("full", "half"):
+            rows = np.array(run_script(c1, RunConfig(list_style=style, newton=(style == "half"), distributed=True),
+                                       log=None).results[-1].rows)
+            assert np.allclose(rows[:, 1:], ref[:, 1:], rtol=1e-9)
+    finally:
+        dist.destroy_process_group()
