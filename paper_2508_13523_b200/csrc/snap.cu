@@ -132,7 +132,7 @@ __device__ __forceinline__ bool neighbour(const double* x, const int* table, int
 // ---------------------------------------------------------------- compute_ui
 // U row-major [n_local][n_flat] (the reference's layout "a").
 template <int TWOJ>
-__global__ void __launch_bounds__(kWarps * 32) k_snap_ui(const double* __restrict__ x, int n_local,
+__global__ void __launch_bounds__(kWarps * 32, 4) k_snap_ui(const double* __restrict__ x, int n_local,
                                                          const int* __restrict__ table,
                                                          const int* __restrict__ counts, int cap, double rc,
                                                          double2* __restrict__ U, int* __restrict__ flags) {
@@ -280,32 +280,29 @@ __global__ void __launch_bounds__(kYWarps * 32) k_snap_yi(const double2* __restr
 //   t_d = f_c' rhat_d Re sum Y conj(u) + f_c Re(G_a conj(da_d) + G_a* da_d + G_b conj(db_d) + G_b* db_d).
 // Same quantity (equal to rounding), 12 instead of 28 complex MACs per element.
 template <int TWOJ>
-__global__ void __launch_bounds__(kWarps * 32, 3) k_snap_deidrj(const double* __restrict__ x, int n_local,
+__global__ void __launch_bounds__(kWarps * 32, 4) k_snap_deidrj(const double* __restrict__ x, int n_local,
                                                              const int* __restrict__ table,
                                                              const int* __restrict__ counts, int cap, double rc,
                                                              const double2* __restrict__ Y,
                                                              double* __restrict__ f) {
     constexpr int NF = block_offset(TWOJ + 1);
-    __shared__ SW sw;
-    __shared__ cplx s_u[kWarps][NF];
-    __shared__ cplx s_l[kWarps][2][kLevelMax];
+    extern __shared__ double s_dyn_d[];  // > 48 KB: weights | u levels | Y_i | lambda
+    SW& sw = *reinterpret_cast<SW*>(s_dyn_d);
+    auto s_u = reinterpret_cast<cplx(*)[NF]>(reinterpret_cast<char*>(s_dyn_d) + sizeof(SW));
+    auto s_y = s_u + kWarps;
+    auto s_l = reinterpret_cast<cplx(*)[2][kLevelMax]>(s_y + kWarps);
     stage_weights(sw, NF);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int i = blockIdx.x * kWarps + w;
     if (i >= n_local) return;
-    cplx y[kSlots];
+    // Y_i lives in shared memory (frees ~56 registers per lane -> 4 CTAs / SM)
+    cplx* sy = s_y[w];
     const double2* Yi = Y + (long long)i * NF;
-#pragma unroll
-    for (int tj = 0; tj <= TWOJ; ++tj)
-#pragma unroll
-        for (int s = 0; s < level_slots(tj); ++s) {
-            const int idx = lane + 32 * s;
-            y[slot_base(tj) + s] = {0.0, 0.0};
-            if (idx < level_size(tj)) {
-                const double2 v = Yi[block_offset(tj) + idx];
-                y[slot_base(tj) + s] = {v.x, v.y};
-            }
-        }
+    for (int e = lane; e < NF; e += 32) {
+        const double2 v = Yi[e];
+        sy[e] = {v.x, v.y};
+    }
+    __syncwarp();
     cplx* ul = s_u[w];
     const double4 xi = mdkk::ld4(x, i);
     const int n = min(counts[i], cap);
@@ -321,7 +318,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_snap_deidrj(const double* __
         double S = 0.0;
         if (lane == 0) {
             ul[0] = {1.0, 0.0};
-            S = y[0].re;
+            S = sy[0].re;
         }
         __syncwarp();
 #pragma unroll
@@ -334,7 +331,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_snap_deidrj(const double* __
                     const cplx v = level_elem(ul + block_offset(tj - 1), tj, P, Q, sw.w[0][e], sw.w[1][e], sw.w[2][e],
                                               sw.w[3][e], g.a, g.b);
                     ul[e] = v;
-                    const cplx yv = y[slot_base(tj) + s];
+                    const cplx yv = sy[e];
                     S += yv.re * v.re + yv.im * v.im;
                 }
             }
@@ -345,7 +342,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_snap_deidrj(const double* __
 #pragma unroll
         for (int s = 0; s < level_slots(TWOJ); ++s) {
             const int idx = lane + 32 * s;
-            if (idx < level_size(TWOJ)) s_l[w][TWOJ & 1][idx] = y[slot_base(TWOJ) + s];
+            if (idx < level_size(TWOJ)) s_l[w][TWOJ & 1][idx] = sy[block_offset(TWOJ) + idx];
         }
         __syncwarp();
 #pragma unroll
@@ -376,7 +373,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_snap_deidrj(const double* __
                         const int P = idx / tj, Q = idx % tj;
                         const int e11 = (P + 1) * (tj + 1) + (Q + 1), e10 = (P + 1) * (tj + 1) + Q;
                         const int e01 = P * (tj + 1) + (Q + 1), e00 = P * (tj + 1) + Q;
-                        cplx v = y[slot_base(tj - 1) + s];
+                        cplx v = sy[block_offset(tj - 1) + idx];
                         v = cadd(v, cscale(sw.w[0][eo + e11], cmul(lam[e11], cconj(g.a))));
                         v = cadd(v, cscale(sw.w[1][eo + e10], cmul(lam[e10], cconj(g.b))));
                         v = cadd(v, cscale(-sw.w[2][eo + e01], cmul(lam[e01], g.b)));
@@ -547,8 +544,19 @@ int mdkk_snap_deidrj(mdkk_snap* s, const double* x, int n_local, const int* tabl
     if (n_local == 0) return MDKK_OK;
     upload_weights();
     const int nb = (n_local + kWarps - 1) / kWarps;
-    MDKK_SNAP_DISPATCH(s->twojmax, k_snap_deidrj, nb, kWarps * 32, mdkk::as_stream(stream), x, n_local, table,
-                       counts, cap, rc, reinterpret_cast<const double2*>(Y), f);
+    switch (s->twojmax) {
+#define MDKK_DE(TJ)                                                                                          \
+    case TJ: {                                                                                               \
+        const size_t sm = sizeof(SW) + kWarps * (2 * block_offset(TJ + 1) + 2 * kLevelMax) * sizeof(cplx);   \
+        cudaFuncSetAttribute(k_snap_deidrj<TJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);      \
+        k_snap_deidrj<TJ><<<nb, kWarps * 32, sm, mdkk::as_stream(stream)>>>(                                 \
+            x, n_local, table, counts, cap, rc, reinterpret_cast<const double2*>(Y), f);                     \
+        break;                                                                                               \
+    }
+        MDKK_DE(0) MDKK_DE(1) MDKK_DE(2) MDKK_DE(3) MDKK_DE(4) MDKK_DE(5) MDKK_DE(6) MDKK_DE(7) MDKK_DE(8)
+#undef MDKK_DE
+        default: return MDKK_E_ARG;
+    }
     MDKK_CHECK_LAUNCH("k_snap_deidrj");
     return MDKK_OK;
 }
