@@ -129,8 +129,76 @@ __device__ __forceinline__ bool neighbour(const double* x, const int* table, int
     return r2 < rc2;  // mdkk/snap/compute.py:114-115 (strict)
 }
 
+// ---------------------------------------------- half-block helpers (both kernels)
+// Every level obeys X[tj-P][tj-Q] = (-1)^(P+Q) conj(X[P][Q]) (u, U, Y and the
+// adjoint lambda), so only the half set H_tj = {2P < tj, or 2P == tj
+// and 2Q <= tj} is computed: it is the row-major prefix P*(tj+1)+Q < half_size.
+__host__ __device__ constexpr int half_size(int tj) {
+    return (tj & 1) ? (tj + 1) * (tj + 1) / 2 : (tj / 2) * (tj + 1) + tj / 2 + 1;
+}
+__host__ __device__ constexpr int half_offset(int tj) {
+    int s = 0;
+    for (int t = 0; t < tj; ++t) s += half_size(t);
+    return s;
+}
+__host__ __device__ constexpr int half_slots(int tj) { return (half_size(tj) + 15) / 16; }
+__host__ __device__ constexpr int hslot_base(int tj) {
+    int s = 0;
+    for (int t = 0; t < tj; ++t) s += half_slots(t);
+    return s;
+}
+constexpr int kHSlots = hslot_base(kMaxTwoJ + 1);        // 14 per half-warp lane at 2J = 8
+constexpr int kHalfMax = half_size(kMaxTwoJ);            // 41
+constexpr int kHalfAll = half_offset(kMaxTwoJ + 1);      // 145
+
+// X[P][Q] of level tj from its stored half (row-major, stride tj+1).
+__device__ __forceinline__ cplx hget(const cplx* L, int tj, int P, int Q) {
+    const int idx = P * (tj + 1) + Q;
+    if (idx < half_size(tj)) return L[idx];
+    cplx v = L[(tj - P) * (tj + 1) + (tj - Q)];
+    v.im = -v.im;
+    return ((P + Q) & 1) ? cneg(v) : v;
+}
+
+// Element (P, Q) of level tj from the half-stored previous level (mdkk/snap/compute.py:138-147).
+__device__ __forceinline__ cplx level_elem_h(const cplx* prev, int tj, int P, int Q, const SW& sw, int e, cplx a,
+                                            cplx b) {
+    cplx v = {0.0, 0.0};
+    if (P >= 1 && Q >= 1) v = cadd(v, cscale(sw.w[0][e], cmul(hget(prev, tj - 1, P - 1, Q - 1), a)));
+    if (P >= 1 && Q <= tj - 1) v = cadd(v, cscale(sw.w[1][e], cmul(hget(prev, tj - 1, P - 1, Q), b)));
+    if (P <= tj - 1 && Q >= 1) v = cadd(v, cscale(sw.w[2][e], cmul(hget(prev, tj - 1, P, Q - 1), cneg(cconj(b)))));
+    if (P <= tj - 1 && Q <= tj - 1) v = cadd(v, cscale(sw.w[3][e], cmul(hget(prev, tj - 1, P, Q), cconj(a))));
+    return v;
+}
+
+struct NbPair {
+    double dx, dy, dz, r2;
+    int j, pad;
+};
+
+// Compact the in-range partners (r^2 < rc^2, mdkk/snap/compute.py:114-115) of
+// table entries [k0, k0+32) of row i into s_nb; returns their count.
+__device__ __forceinline__ int compact_pairs(const double* x, const int* table, int cap, int i, int k0, int n,
+                                             double4 xi, double rc2, NbPair* s_nb, bool& bad) {
+    const int lane = threadIdx.x & 31, k = k0 + lane;
+    int j = 0;
+    double dx = 0, dy = 0, dz = 0, r2 = 0;
+    const bool ok = k < n && neighbour(x, table, cap, i, k, xi, rc2, j, dx, dy, dz, r2);
+    const unsigned m = __ballot_sync(0xffffffffu, ok);
+    if (ok) {
+        bad |= !(r2 > 0.0);
+        s_nb[__popc(m & ((1u << lane) - 1u))] = {dx, dy, dz, r2, j, 0};
+    }
+    __syncwarp();
+    return __popc(m);
+}
+
 // ---------------------------------------------------------------- compute_ui
-// U row-major [n_local][n_flat] (the reference's layout "a").
+// U_i = sum_k f_c u(a_k, b_k) (mdkk/snap/compute.py:279-292), row-major U.
+// One warp per atom, two neighbours at a time (half-warp each); each half
+// computes the half set H_tj of every level (16 lanes, previous level in
+// shared memory), accumulates f_c u in registers, and the full U_i row is
+// written from the half set and its mirror.
 template <int TWOJ>
 __global__ void __launch_bounds__(kWarps * 32, 4) k_snap_ui(const double* __restrict__ x, int n_local,
                                                          const int* __restrict__ table,
@@ -138,56 +206,76 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_snap_ui(const double* __rest
                                                          double2* __restrict__ U, int* __restrict__ flags) {
     constexpr int NF = block_offset(TWOJ + 1);
     __shared__ SW sw;
-    __shared__ cplx s_lvl[kWarps][2][kLevelMax];
+    __shared__ NbPair s_nb[kWarps][32];
+    __shared__ cplx s_lvl[kWarps][2][2][kHalfMax];
     stage_weights(sw, NF);
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, hl = lane & 15, hh = lane >> 4;
     const int i = blockIdx.x * kWarps + w;
     if (i >= n_local) return;
-    cplx acc[kSlots];
+    cplx acc[kHSlots];
 #pragma unroll
-    for (int s = 0; s < kSlots; ++s) acc[s] = {0.0, 0.0};
+    for (int s = 0; s < kHSlots; ++s) acc[s] = {0.0, 0.0};
     const double4 xi = mdkk::ld4(x, i);
     const int n = min(counts[i], cap);
     const double rc2 = rc * rc;
     bool bad = false;
-    for (int k = 0; k < n; ++k) {
-        int j;
-        double dx, dy, dz, r2, z0, r0;
-        if (!neighbour(x, table, cap, i, k, xi, rc2, j, dx, dy, dz, r2)) continue;
-        bad |= !(r2 > 0.0);
-        PairGeo g;
-        pair_geometry(dx, dy, dz, r2, rc, g, z0, r0);
-        if (lane == 0) {
-            s_lvl[w][0][0] = {1.0, 0.0};
-            acc[0].re += g.fc;
-        }
-        __syncwarp();
-#pragma unroll
-        for (int tj = 1; tj <= TWOJ; ++tj) {
-            const cplx* prev = s_lvl[w][(tj - 1) & 1];
-            cplx* cur = s_lvl[w][tj & 1];
-#pragma unroll
-            for (int s = 0; s < level_slots(tj); ++s) {
-                const int idx = lane + 32 * s;
-                if (idx < level_size(tj)) {
-                    const int P = idx / (tj + 1), Q = idx % (tj + 1), e = block_offset(tj) + idx;
-                    const cplx v = level_elem(prev, tj, P, Q, sw.w[0][e], sw.w[1][e], sw.w[2][e], sw.w[3][e], g.a, g.b);
-                    cur[idx] = v;
-                    acc[slot_base(tj) + s] = cadd(acc[slot_base(tj) + s], cscale(g.fc, v));
-                }
+    for (int k0 = 0; k0 < n; k0 += 32) {
+        const int m = compact_pairs(x, table, cap, i, k0, n, xi, rc2, s_nb[w], bad);
+        for (int t = 0; t < m; t += 2) {
+            const int pi = t + hh;
+            const NbPair nb = s_nb[w][pi < m ? pi : t];
+            PairGeo g;
+            double z0, r0;
+            pair_geometry(nb.dx, nb.dy, nb.dz, nb.r2, rc, g, z0, r0);
+            const double fc = pi < m ? g.fc : 0.0;
+            cplx(*L)[kHalfMax] = s_lvl[w][hh];
+            if (hl == 0) {
+                L[0][0] = {1.0, 0.0};
+                acc[0].re += fc;
             }
             __syncwarp();
+#pragma unroll
+            for (int tj = 1; tj <= TWOJ; ++tj) {
+                const cplx* prev = L[(tj - 1) & 1];
+                cplx* cur = L[tj & 1];
+#pragma unroll
+                for (int s = 0; s < half_slots(tj); ++s) {
+                    const int h = hl + 16 * s;
+                    if (h < half_size(tj)) {
+                        const int P = h / (tj + 1), Q = h % (tj + 1);
+                        const cplx v = level_elem_h(prev, tj, P, Q, sw, block_offset(tj) + h, g.a, g.b);
+                        cur[h] = v;
+                        acc[hslot_base(tj) + s] = cadd(acc[hslot_base(tj) + s], cscale(fc, v));
+                    }
+                }
+                __syncwarp();
+            }
         }
     }
     if (bad && lane == 0) atomicOr(flags, MDKK_FLAG_COINCIDENT);
+    // both halves own the same elements: fold the odd half onto the even one
+#pragma unroll
+    for (int s = 0; s < kHSlots; ++s) {
+        acc[s].re += __shfl_xor_sync(0xffffffffu, acc[s].re, 16);
+        acc[s].im += __shfl_xor_sync(0xffffffffu, acc[s].im, 16);
+    }
+    if (hh) return;
     double2* Ui = U + (long long)i * NF;
 #pragma unroll
     for (int tj = 0; tj <= TWOJ; ++tj)
 #pragma unroll
-        for (int s = 0; s < level_slots(tj); ++s) {
-            const int idx = lane + 32 * s;
-            if (idx < level_size(tj))
-                Ui[block_offset(tj) + idx] = make_double2(acc[slot_base(tj) + s].re, acc[slot_base(tj) + s].im);
+        for (int s = 0; s < half_slots(tj); ++s) {
+            const int h = hl + 16 * s;
+            if (h < half_size(tj)) {
+                const int P = h / (tj + 1), Q = h % (tj + 1);
+                const cplx v = acc[hslot_base(tj) + s];
+                Ui[block_offset(tj) + h] = make_double2(v.re, v.im);
+                const int hm = (tj - P) * (tj + 1) + (tj - Q);
+                if (hm != h) {
+                    const double sg = ((P + Q) & 1) ? -1.0 : 1.0;
+                    Ui[block_offset(tj) + hm] = make_double2(sg * v.re, -sg * v.im);
+                }
+            }
         }
 }
 
@@ -272,139 +360,151 @@ __global__ void __launch_bounds__(kYWarps * 32) k_snap_yi(const double2* __restr
 
 // ------------------------------------------------------- compute_fused_deidrj
 // Reverse-mode form of compute_fused_deidrj (mdkk/snap/compute.py:390-409).
-// For one pair the reference evaluates t_d = Re sum_f Y[f] conj(d(f_c u[f])/d dr_d)
-// with a forward derivative recursion per direction.  Here u is run forward
-// (all levels kept in shared memory) and the adjoint lambda_tj = Y_tj +
+// The reference evaluates t_d = Re sum_f Y[f] conj(d(f_c u[f])/d dr_d) with a
+// forward derivative recursion per direction.  Here u runs forward (half sets
+// of all levels kept in shared memory) and the adjoint lambda_tj = Y_tj +
 // M_{tj+1}^H lambda_{tj+1} backward, accumulating G_c = sum_f Y[f] conj(du[f]/dc)
-// for c in {a, a*, b, b*}; then
-//   t_d = f_c' rhat_d Re sum Y conj(u) + f_c Re(G_a conj(da_d) + G_a* da_d + G_b conj(db_d) + G_b* db_d).
-// Same quantity (equal to rounding), 12 instead of 28 complex MACs per element.
+// for c in {a, a*, b, b*}.  The mirror symmetry gives G_{a*} = conj(G_a),
+// G_{b*} = conj(G_b), so with half sets only
+//   t_d = f_c' rhat_d S + 2 f_c Re(G_a conj(da_d) + G_b conj(db_d)),   S = Re sum_f Y conj(u).
+// Same quantity (equal to rounding) for ~1/4 of the reference's complex MACs.
+// One warp per atom, two neighbours at a time (one per half-warp).
 template <int TWOJ>
-__global__ void __launch_bounds__(kWarps * 32, 4) k_snap_deidrj(const double* __restrict__ x, int n_local,
+__global__ void __launch_bounds__(kWarps * 32, 3) k_snap_deidrj(const double* __restrict__ x, int n_local,
                                                              const int* __restrict__ table,
                                                              const int* __restrict__ counts, int cap, double rc,
                                                              const double2* __restrict__ Y,
                                                              double* __restrict__ f) {
     constexpr int NF = block_offset(TWOJ + 1);
-    extern __shared__ double s_dyn_d[];  // > 48 KB: weights | u levels | Y_i | lambda
+    constexpr int NH = half_offset(TWOJ + 1);
+    extern __shared__ double s_dyn_d[];  // > 48 KB: weights | pairs | Y_i half | u half levels | lambda
     SW& sw = *reinterpret_cast<SW*>(s_dyn_d);
-    auto s_u = reinterpret_cast<cplx(*)[NF]>(reinterpret_cast<char*>(s_dyn_d) + sizeof(SW));
-    auto s_y = s_u + kWarps;
-    auto s_l = reinterpret_cast<cplx(*)[2][kLevelMax]>(s_y + kWarps);
+    auto s_nb = reinterpret_cast<NbPair(*)[32]>(reinterpret_cast<char*>(s_dyn_d) + sizeof(SW));
+    auto s_y = reinterpret_cast<cplx(*)[NH]>(s_nb + kWarps);
+    auto s_u = reinterpret_cast<cplx(*)[2][NH]>(s_y + kWarps);
+    auto s_l = reinterpret_cast<cplx(*)[2][2][kHalfMax]>(s_u + kWarps);
     stage_weights(sw, NF);
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, hl = lane & 15, hh = lane >> 4;
     const int i = blockIdx.x * kWarps + w;
     if (i >= n_local) return;
-    // Y_i lives in shared memory (frees ~56 registers per lane -> 4 CTAs / SM)
-    cplx* sy = s_y[w];
     const double2* Yi = Y + (long long)i * NF;
-    for (int e = lane; e < NF; e += 32) {
-        const double2 v = Yi[e];
-        sy[e] = {v.x, v.y};
-    }
+#pragma unroll
+    for (int tj = 0; tj <= TWOJ; ++tj)
+        for (int h = lane; h < half_size(tj); h += 32) {
+            const double2 v = Yi[block_offset(tj) + h];
+            s_y[w][half_offset(tj) + h] = {v.x, v.y};
+        }
     __syncwarp();
-    cplx* ul = s_u[w];
+    const cplx* sy = s_y[w];
+    cplx* ul = s_u[w][hh];
+    cplx(*lam)[kHalfMax] = s_l[w][hh];
     const double4 xi = mdkk::ld4(x, i);
     const int n = min(counts[i], cap);
     const double rc2 = rc * rc;
     double fi[3] = {0.0, 0.0, 0.0};
-    for (int k = 0; k < n; ++k) {
-        int j;
-        double dx, dy, dz, r2, z0, r0;
-        if (!neighbour(x, table, cap, i, k, xi, rc2, j, dx, dy, dz, r2)) continue;
-        PairGeo g;
-        pair_geometry(dx, dy, dz, r2, rc, g, z0, r0);
-        // forward: all levels of u, and S = Re sum Y conj(u)
-        double S = 0.0;
-        if (lane == 0) {
-            ul[0] = {1.0, 0.0};
-            S = sy[0].re;
-        }
-        __syncwarp();
-#pragma unroll
-        for (int tj = 1; tj <= TWOJ; ++tj) {
-#pragma unroll
-            for (int s = 0; s < level_slots(tj); ++s) {
-                const int idx = lane + 32 * s;
-                if (idx < level_size(tj)) {
-                    const int P = idx / (tj + 1), Q = idx % (tj + 1), e = block_offset(tj) + idx;
-                    const cplx v = level_elem(ul + block_offset(tj - 1), tj, P, Q, sw.w[0][e], sw.w[1][e], sw.w[2][e],
-                                              sw.w[3][e], g.a, g.b);
-                    ul[e] = v;
-                    const cplx yv = sy[e];
-                    S += yv.re * v.re + yv.im * v.im;
-                }
+    bool bad = false;
+    for (int k0 = 0; k0 < n; k0 += 32) {
+        const int m = compact_pairs(x, table, cap, i, k0, n, xi, rc2, s_nb[w], bad);
+        for (int t = 0; t < m; t += 2) {
+            const int pi = t + hh;
+            const bool active = pi < m;
+            const NbPair nb = s_nb[w][active ? pi : t];
+            PairGeo g;
+            double z0, r0;
+            pair_geometry(nb.dx, nb.dy, nb.dz, nb.r2, rc, g, z0, r0);
+            // forward: half sets of all levels, S = Re sum_f Y conj(u) (mirror pairs counted twice)
+            double S = 0.0;
+            if (hl == 0) {
+                ul[0] = {1.0, 0.0};
+                S = sy[0].re;
             }
             __syncwarp();
-        }
-        // backward: lambda_TWOJ = Y_TWOJ, then G_c and lambda_{tj-1}
-        cplx Ga = {0, 0}, Gas = {0, 0}, Gb = {0, 0}, Gbs = {0, 0};
 #pragma unroll
-        for (int s = 0; s < level_slots(TWOJ); ++s) {
-            const int idx = lane + 32 * s;
-            if (idx < level_size(TWOJ)) s_l[w][TWOJ & 1][idx] = sy[block_offset(TWOJ) + idx];
-        }
-        __syncwarp();
+            for (int tj = 1; tj <= TWOJ; ++tj) {
 #pragma unroll
-        for (int tj = TWOJ; tj >= 1; --tj) {
-            const cplx* lam = s_l[w][tj & 1];
-            const cplx* up = ul + block_offset(tj - 1);  // u_{tj-1}, row-major tj x tj
-            // (a) G_c += lambda_tj[P][Q] conj(d(local)/dc)
-#pragma unroll
-            for (int s = 0; s < level_slots(tj); ++s) {
-                const int idx = lane + 32 * s;
-                if (idx < level_size(tj)) {
-                    const int P = idx / (tj + 1), Q = idx % (tj + 1), e = block_offset(tj) + idx;
-                    const cplx l = lam[idx];
-                    if (P >= 1 && Q >= 1) Ga = cadd(Ga, cscale(sw.w[0][e], cmul(l, cconj(up[(P - 1) * tj + (Q - 1)]))));
-                    if (P >= 1 && Q <= tj - 1) Gb = cadd(Gb, cscale(sw.w[1][e], cmul(l, cconj(up[(P - 1) * tj + Q]))));
-                    if (P <= tj - 1 && Q >= 1) Gbs = cadd(Gbs, cscale(-sw.w[2][e], cmul(l, cconj(up[P * tj + (Q - 1)]))));
-                    if (P <= tj - 1 && Q <= tj - 1) Gas = cadd(Gas, cscale(sw.w[3][e], cmul(l, cconj(up[P * tj + Q]))));
-                }
-            }
-            // (b) lambda_{tj-1}[P][Q] = Y[P][Q] + sum of conj(coef) * w * lambda_tj over the 4 users
-            if (tj >= 2) {
-                cplx* ln = s_l[w][(tj - 1) & 1];
-                const int eo = block_offset(tj);
-#pragma unroll
-                for (int s = 0; s < level_slots(tj - 1); ++s) {
-                    const int idx = lane + 32 * s;
-                    if (idx < level_size(tj - 1)) {
-                        const int P = idx / tj, Q = idx % tj;
-                        const int e11 = (P + 1) * (tj + 1) + (Q + 1), e10 = (P + 1) * (tj + 1) + Q;
-                        const int e01 = P * (tj + 1) + (Q + 1), e00 = P * (tj + 1) + Q;
-                        cplx v = sy[block_offset(tj - 1) + idx];
-                        v = cadd(v, cscale(sw.w[0][eo + e11], cmul(lam[e11], cconj(g.a))));
-                        v = cadd(v, cscale(sw.w[1][eo + e10], cmul(lam[e10], cconj(g.b))));
-                        v = cadd(v, cscale(-sw.w[2][eo + e01], cmul(lam[e01], g.b)));
-                        v = cadd(v, cscale(sw.w[3][eo + e00], cmul(lam[e00], g.a)));
-                        ln[idx] = v;
+                for (int s = 0; s < half_slots(tj); ++s) {
+                    const int h = hl + 16 * s;
+                    if (h < half_size(tj)) {
+                        const int P = h / (tj + 1), Q = h % (tj + 1);
+                        const cplx v = level_elem_h(ul + half_offset(tj - 1), tj, P, Q, sw, block_offset(tj) + h,
+                                                    g.a, g.b);
+                        ul[half_offset(tj) + h] = v;
+                        const cplx yv = sy[half_offset(tj) + h];
+                        const double c = (2 * P == tj && 2 * Q == tj) ? 1.0 : 2.0;
+                        S += c * (yv.re * v.re + yv.im * v.im);
                     }
                 }
+                __syncwarp();
             }
+            // backward: lambda_TWOJ = Y_TWOJ; G_a, G_b over the half sets; lambda_{tj-1}
+            cplx Ga = {0, 0}, Gb = {0, 0};
+            for (int h = hl; h < half_size(TWOJ); h += 16) lam[TWOJ & 1][h] = sy[half_offset(TWOJ) + h];
             __syncwarp();
-        }
-        // t_d per lane (linear in the lane's partial sums), then one warp reduction
-        cplx da[3], db[3];
-        const double d[3] = {dx, dy, dz};
-        pair_grads(d, g, rc, z0, r0, da, db);
-        double t[3];
 #pragma unroll
-        for (int q = 0; q < 3; ++q) {
-            const double re = (Ga.re * da[q].re + Ga.im * da[q].im) + (Gas.re * da[q].re - Gas.im * da[q].im) +
-                              (Gb.re * db[q].re + Gb.im * db[q].im) + (Gbs.re * db[q].re - Gbs.im * db[q].im);
-            t[q] = mdkk::warp_sum(g.dfc * (d[q] / g.r) * S + g.fc * re);
-        }
-        if (lane == 0) {
-            fi[0] += t[0];
-            fi[1] += t[1];
-            fi[2] += t[2];
-            double* fj = f + 4LL * j;
-            atomicAdd(fj + 0, -t[0]);
-            atomicAdd(fj + 1, -t[1]);
-            atomicAdd(fj + 2, -t[2]);
+            for (int tj = TWOJ; tj >= 1; --tj) {
+                const cplx* lt = lam[tj & 1];
+                const cplx* up = ul + half_offset(tj - 1);
+#pragma unroll
+                for (int s = 0; s < half_slots(tj); ++s) {
+                    const int h = hl + 16 * s;
+                    if (h < half_size(tj)) {
+                        const int P = h / (tj + 1), Q = h % (tj + 1), e = block_offset(tj) + h;
+                        const cplx l = lt[h];
+                        cplx ca = {0, 0}, cas = {0, 0}, cb = {0, 0}, cbs = {0, 0};
+                        if (P >= 1 && Q >= 1) ca = cscale(sw.w[0][e], cmul(l, cconj(hget(up, tj - 1, P - 1, Q - 1))));
+                        if (P <= tj - 1 && Q <= tj - 1) cas = cscale(sw.w[3][e], cmul(l, cconj(hget(up, tj - 1, P, Q))));
+                        if (P >= 1 && Q <= tj - 1) cb = cscale(sw.w[1][e], cmul(l, cconj(hget(up, tj - 1, P - 1, Q))));
+                        if (P <= tj - 1 && Q >= 1) cbs = cscale(-sw.w[2][e], cmul(l, cconj(hget(up, tj - 1, P, Q - 1))));
+                        const double mw = (2 * P == tj && 2 * Q == tj) ? 0.5 : 1.0;
+                        Ga = cadd(Ga, cscale(mw, cadd(ca, cconj(cas))));
+                        Gb = cadd(Gb, cscale(mw, cadd(cb, cconj(cbs))));
+                    }
+                }
+                if (tj >= 2) {
+                    cplx* ln = lam[(tj - 1) & 1];
+                    const int eo = block_offset(tj);
+#pragma unroll
+                    for (int s = 0; s < half_slots(tj - 1); ++s) {
+                        const int h = hl + 16 * s;
+                        if (h < half_size(tj - 1)) {
+                            const int P = h / tj, Q = h % tj;
+                            cplx v = sy[half_offset(tj - 1) + h];
+                            v = cadd(v, cscale(sw.w[0][eo + (P + 1) * (tj + 1) + (Q + 1)],
+                                               cmul(hget(lt, tj, P + 1, Q + 1), cconj(g.a))));
+                            v = cadd(v, cscale(sw.w[1][eo + (P + 1) * (tj + 1) + Q], cmul(hget(lt, tj, P + 1, Q), cconj(g.b))));
+                            v = cadd(v, cscale(-sw.w[2][eo + P * (tj + 1) + (Q + 1)], cmul(hget(lt, tj, P, Q + 1), g.b)));
+                            v = cadd(v, cscale(sw.w[3][eo + P * (tj + 1) + Q], cmul(hget(lt, tj, P, Q), g.a)));
+                            ln[h] = v;
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+            cplx da[3], db[3];
+            const double d[3] = {nb.dx, nb.dy, nb.dz};
+            pair_grads(d, g, rc, z0, r0, da, db);
+            double tt[3];
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                double v = g.dfc * (d[q] / g.r) * S +
+                           2.0 * g.fc * ((Ga.re * da[q].re + Ga.im * da[q].im) + (Gb.re * db[q].re + Gb.im * db[q].im));
+#pragma unroll
+                for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                tt[q] = v;
+            }
+            if (hl == 0 && active) {
+                fi[0] += tt[0];
+                fi[1] += tt[1];
+                fi[2] += tt[2];
+                double* fj = f + 4LL * nb.j;
+                atomicAdd(fj + 0, -tt[0]);
+                atomicAdd(fj + 1, -tt[1]);
+                atomicAdd(fj + 2, -tt[2]);
+            }
         }
     }
+#pragma unroll
+    for (int q = 0; q < 3; ++q) fi[q] += __shfl_xor_sync(0xffffffffu, fi[q], 16);
     if (lane == 0) {
         double* p = f + 4LL * i;
         atomicAdd(p + 0, fi[0]);
@@ -547,7 +647,8 @@ int mdkk_snap_deidrj(mdkk_snap* s, const double* x, int n_local, const int* tabl
     switch (s->twojmax) {
 #define MDKK_DE(TJ)                                                                                          \
     case TJ: {                                                                                               \
-        const size_t sm = sizeof(SW) + kWarps * (2 * block_offset(TJ + 1) + 2 * kLevelMax) * sizeof(cplx);   \
+        const size_t sm = sizeof(SW) + kWarps * (32 * sizeof(NbPair) +                                       \
+                                                 (3 * half_offset(TJ + 1) + 4 * kHalfMax) * sizeof(cplx));  \
         cudaFuncSetAttribute(k_snap_deidrj<TJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);      \
         k_snap_deidrj<TJ><<<nb, kWarps * 32, sm, mdkk::as_stream(stream)>>>(                                 \
             x, n_local, table, counts, cap, rc, reinterpret_cast<const double2*>(Y), f);                     \
