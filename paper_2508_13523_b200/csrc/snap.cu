@@ -160,6 +160,14 @@ __device__ __forceinline__ cplx hget(const cplx* L, int tj, int P, int Q) {
     return ((P + Q) & 1) ? cneg(v) : v;
 }
 
+// Store element (P, Q) of a full row-major (tj+1)^2 level and its mirror.
+__device__ __forceinline__ void store_mirrored(cplx* L, int tj, int P, int Q, cplx v) {
+    L[P * (tj + 1) + Q] = v;
+    const int hm = (tj - P) * (tj + 1) + (tj - Q);
+    const double sg = ((P + Q) & 1) ? -1.0 : 1.0;
+    L[hm] = {sg * v.re, -sg * v.im};  // the center element writes itself twice (same value)
+}
+
 // Element (P, Q) of level tj from the half-stored previous level (mdkk/snap/compute.py:138-147).
 __device__ __forceinline__ cplx level_elem_h(const cplx* prev, int tj, int P, int Q, const SW& sw, int e, cplx a,
                                             cplx b) {
@@ -207,7 +215,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_snap_ui(const double* __rest
     constexpr int NF = block_offset(TWOJ + 1);
     __shared__ SW sw;
     __shared__ NbPair s_nb[kWarps][32];
-    __shared__ cplx s_lvl[kWarps][2][2][kHalfMax];
+    __shared__ cplx s_lvl[kWarps][2][2][kLevelMax];
     stage_weights(sw, NF);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, hl = lane & 15, hh = lane >> 4;
     const int i = blockIdx.x * kWarps + w;
@@ -228,7 +236,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_snap_ui(const double* __rest
             double z0, r0;
             pair_geometry(nb.dx, nb.dy, nb.dz, nb.r2, rc, g, z0, r0);
             const double fc = pi < m ? g.fc : 0.0;
-            cplx(*L)[kHalfMax] = s_lvl[w][hh];
+            cplx(*L)[kLevelMax] = s_lvl[w][hh];
             if (hl == 0) {
                 L[0][0] = {1.0, 0.0};
                 acc[0].re += fc;
@@ -242,9 +250,10 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_snap_ui(const double* __rest
                 for (int s = 0; s < half_slots(tj); ++s) {
                     const int h = hl + 16 * s;
                     if (h < half_size(tj)) {
-                        const int P = h / (tj + 1), Q = h % (tj + 1);
-                        const cplx v = level_elem_h(prev, tj, P, Q, sw, block_offset(tj) + h, g.a, g.b);
-                        cur[h] = v;
+                        const int P = h / (tj + 1), Q = h % (tj + 1), e = block_offset(tj) + h;
+                        const cplx v = level_elem(prev, tj, P, Q, sw.w[0][e], sw.w[1][e], sw.w[2][e], sw.w[3][e],
+                                                  g.a, g.b);
+                        store_mirrored(cur, tj, P, Q, v);
                         acc[hslot_base(tj) + s] = cadd(acc[hslot_base(tj) + s], cscale(fc, v));
                     }
                 }
@@ -381,8 +390,8 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_snap_deidrj(const double* __
     SW& sw = *reinterpret_cast<SW*>(s_dyn_d);
     auto s_nb = reinterpret_cast<NbPair(*)[32]>(reinterpret_cast<char*>(s_dyn_d) + sizeof(SW));
     auto s_y = reinterpret_cast<cplx(*)[NH]>(s_nb + kWarps);
-    auto s_u = reinterpret_cast<cplx(*)[2][NH]>(s_y + kWarps);
-    auto s_l = reinterpret_cast<cplx(*)[2][2][kHalfMax]>(s_u + kWarps);
+    auto s_u = reinterpret_cast<cplx(*)[2][NF]>(s_y + kWarps);
+    auto s_l = reinterpret_cast<cplx(*)[2][2][kLevelMax]>(s_u + kWarps);
     stage_weights(sw, NF);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, hl = lane & 15, hh = lane >> 4;
     const int i = blockIdx.x * kWarps + w;
@@ -397,7 +406,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_snap_deidrj(const double* __
     __syncwarp();
     const cplx* sy = s_y[w];
     cplx* ul = s_u[w][hh];
-    cplx(*lam)[kHalfMax] = s_l[w][hh];
+    cplx(*lam)[kLevelMax] = s_l[w][hh];
     const double4 xi = mdkk::ld4(x, i);
     const int n = min(counts[i], cap);
     const double rc2 = rc * rc;
@@ -426,9 +435,10 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_snap_deidrj(const double* __
                     const int h = hl + 16 * s;
                     if (h < half_size(tj)) {
                         const int P = h / (tj + 1), Q = h % (tj + 1);
-                        const cplx v = level_elem_h(ul + half_offset(tj - 1), tj, P, Q, sw, block_offset(tj) + h,
-                                                    g.a, g.b);
-                        ul[half_offset(tj) + h] = v;
+                        const int e = block_offset(tj) + h;
+                        const cplx v = level_elem(ul + block_offset(tj - 1), tj, P, Q, sw.w[0][e], sw.w[1][e],
+                                                  sw.w[2][e], sw.w[3][e], g.a, g.b);
+                        store_mirrored(ul + block_offset(tj), tj, P, Q, v);
                         const cplx yv = sy[half_offset(tj) + h];
                         const double c = (2 * P == tj && 2 * Q == tj) ? 1.0 : 2.0;
                         S += c * (yv.re * v.re + yv.im * v.im);
@@ -438,12 +448,13 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_snap_deidrj(const double* __
             }
             // backward: lambda_TWOJ = Y_TWOJ; G_a, G_b over the half sets; lambda_{tj-1}
             cplx Ga = {0, 0}, Gb = {0, 0};
-            for (int h = hl; h < half_size(TWOJ); h += 16) lam[TWOJ & 1][h] = sy[half_offset(TWOJ) + h];
+            for (int h = hl; h < half_size(TWOJ); h += 16)
+                store_mirrored(lam[TWOJ & 1], TWOJ, h / (TWOJ + 1), h % (TWOJ + 1), sy[half_offset(TWOJ) + h]);
             __syncwarp();
 #pragma unroll
             for (int tj = TWOJ; tj >= 1; --tj) {
                 const cplx* lt = lam[tj & 1];
-                const cplx* up = ul + half_offset(tj - 1);
+                const cplx* up = ul + block_offset(tj - 1);
 #pragma unroll
                 for (int s = 0; s < half_slots(tj); ++s) {
                     const int h = hl + 16 * s;
@@ -451,10 +462,10 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_snap_deidrj(const double* __
                         const int P = h / (tj + 1), Q = h % (tj + 1), e = block_offset(tj) + h;
                         const cplx l = lt[h];
                         cplx ca = {0, 0}, cas = {0, 0}, cb = {0, 0}, cbs = {0, 0};
-                        if (P >= 1 && Q >= 1) ca = cscale(sw.w[0][e], cmul(l, cconj(hget(up, tj - 1, P - 1, Q - 1))));
-                        if (P <= tj - 1 && Q <= tj - 1) cas = cscale(sw.w[3][e], cmul(l, cconj(hget(up, tj - 1, P, Q))));
-                        if (P >= 1 && Q <= tj - 1) cb = cscale(sw.w[1][e], cmul(l, cconj(hget(up, tj - 1, P - 1, Q))));
-                        if (P <= tj - 1 && Q >= 1) cbs = cscale(-sw.w[2][e], cmul(l, cconj(hget(up, tj - 1, P, Q - 1))));
+                        if (P >= 1 && Q >= 1) ca = cscale(sw.w[0][e], cmul(l, cconj(up[(P - 1) * tj + (Q - 1)])));
+                        if (P <= tj - 1 && Q <= tj - 1) cas = cscale(sw.w[3][e], cmul(l, cconj(up[P * tj + Q])));
+                        if (P >= 1 && Q <= tj - 1) cb = cscale(sw.w[1][e], cmul(l, cconj(up[(P - 1) * tj + Q])));
+                        if (P <= tj - 1 && Q >= 1) cbs = cscale(-sw.w[2][e], cmul(l, cconj(up[P * tj + (Q - 1)])));
                         const double mw = (2 * P == tj && 2 * Q == tj) ? 0.5 : 1.0;
                         Ga = cadd(Ga, cscale(mw, cadd(ca, cconj(cas))));
                         Gb = cadd(Gb, cscale(mw, cadd(cb, cconj(cbs))));
@@ -469,12 +480,13 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_snap_deidrj(const double* __
                         if (h < half_size(tj - 1)) {
                             const int P = h / tj, Q = h % tj;
                             cplx v = sy[half_offset(tj - 1) + h];
-                            v = cadd(v, cscale(sw.w[0][eo + (P + 1) * (tj + 1) + (Q + 1)],
-                                               cmul(hget(lt, tj, P + 1, Q + 1), cconj(g.a))));
-                            v = cadd(v, cscale(sw.w[1][eo + (P + 1) * (tj + 1) + Q], cmul(hget(lt, tj, P + 1, Q), cconj(g.b))));
-                            v = cadd(v, cscale(-sw.w[2][eo + P * (tj + 1) + (Q + 1)], cmul(hget(lt, tj, P, Q + 1), g.b)));
-                            v = cadd(v, cscale(sw.w[3][eo + P * (tj + 1) + Q], cmul(hget(lt, tj, P, Q), g.a)));
-                            ln[h] = v;
+                            const int e11 = (P + 1) * (tj + 1) + (Q + 1), e10 = (P + 1) * (tj + 1) + Q;
+                            const int e01 = P * (tj + 1) + (Q + 1), e00 = P * (tj + 1) + Q;
+                            v = cadd(v, cscale(sw.w[0][eo + e11], cmul(lt[e11], cconj(g.a))));
+                            v = cadd(v, cscale(sw.w[1][eo + e10], cmul(lt[e10], cconj(g.b))));
+                            v = cadd(v, cscale(-sw.w[2][eo + e01], cmul(lt[e01], g.b)));
+                            v = cadd(v, cscale(sw.w[3][eo + e00], cmul(lt[e00], g.a)));
+                            store_mirrored(ln, tj - 1, P, Q, v);
                         }
                     }
                 }
@@ -648,7 +660,7 @@ int mdkk_snap_deidrj(mdkk_snap* s, const double* x, int n_local, const int* tabl
 #define MDKK_DE(TJ)                                                                                          \
     case TJ: {                                                                                               \
         const size_t sm = sizeof(SW) + kWarps * (32 * sizeof(NbPair) +                                       \
-                                                 (3 * half_offset(TJ + 1) + 4 * kHalfMax) * sizeof(cplx));  \
+            (half_offset(TJ + 1) + 2 * block_offset(TJ + 1) + 4 * kLevelMax) * sizeof(cplx));                \
         cudaFuncSetAttribute(k_snap_deidrj<TJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);      \
         k_snap_deidrj<TJ><<<nb, kWarps * 32, sm, mdkk::as_stream(stream)>>>(                                 \
             x, n_local, table, counts, cap, rc, reinterpret_cast<const double2*>(Y), f);                     \
