@@ -336,9 +336,11 @@ def main():
     nn = full["nn"]
     bytes_per_launch = full["n_atoms"] / world * (28.0 * nn + 52.0)
     achieved = bytes_per_launch / (full["force_ms"] * 1e-3) / 1e9
-    e2e = lj_e2e("full", cells, max(args.steps, 20), device, distributed) if not args.no_e2e else None
+    # e2e: the user's call `run 100` (the configs' run length) from host arrays, thermo + snapshots back
+    e2e_steps = 100
+    e2e = lj_e2e("full", cells, e2e_steps, device, distributed) if not args.no_e2e else None
     if e2e is not None and distributed:
-        e2e["value"] = n_atoms * max(args.steps, 20) / max_over_ranks(n_atoms * max(args.steps, 20) / e2e["value"])
+        e2e["value"] = n_atoms * e2e_steps / max_over_ranks(n_atoms * e2e_steps / e2e["value"])
     snapr, fp64 = None, None
     if not args.no_snap and not distributed:
         fp64 = fp64_peak(device)
@@ -388,7 +390,10 @@ def main():
                              "flops_model": "canonical mdkk formulation nn*(9260+60518)+36*32578 per atom"}}),
             "cpu_baseline": cpu,
             "e2e": ({"value": e2e["value"], "unit": UNIT, "h2d_bytes_per_step": e2e["h2d"],
-                     "d2h_bytes_per_step": e2e["d2h"]} if e2e else None),
+                     "d2h_bytes_per_step": e2e["d2h"],
+                     "what": f"Simulation.run_nve({e2e_steps}) from host positions/velocities: upload, distribute, "
+                             "first build, steps, thermo at 0 and end with gid-ordered position snapshots"}
+                    if e2e else None),
             "gpu_launches": full["launches"],
             "clocks": full["clocks"],
         }

@@ -13,9 +13,10 @@ __global__ void k_wrap(double* __restrict__ x, int n, double Lx, double Ly, doub
     if (i >= n) return;
     double4 p = mdkk::ld4_nc(x, i);
     // pos - L * floor(pos / L) exactly as mdkk/domain.py:62
-    p.x = p.x - Lx * floor(p.x / Lx);
-    p.y = p.y - Ly * floor(p.y / Ly);
-    p.z = p.z - Lz * floor(p.z / Lz);
+    // (explicit roundings: no FMA contraction, bit-identical to numpy)
+    p.x = __dsub_rn(p.x, __dmul_rn(Lx, floor(p.x / Lx)));
+    p.y = __dsub_rn(p.y, __dmul_rn(Ly, floor(p.y / Ly)));
+    p.z = __dsub_rn(p.z, __dmul_rn(Lz, floor(p.z / Lz)));
     mdkk::st4(x, i, p);
 }
 

@@ -9,6 +9,7 @@
 //      per warp) and keeps j != i with r^2 < bc^2 (strict, same rounding as
 //      the reference) passing the style predicate (mdkk/neighbor.py:134-179).
 // Output: int32 cluster-blocked table [ncl][cap][32] of row indices + counts.
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include "cluster.cuh"
@@ -244,10 +245,50 @@ __global__ void k_max_disp2(const double* __restrict__ x, const double* __restri
 
 extern "C" {
 
+__global__ void k_iota(int n, int* __restrict__ v) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) v[i] = i;
+}
+
+// Few buckets (rank partitions): a stable LSD radix sort of (key, row) over
+// ceil(log2(nbuckets)) bits.  The scatter + per-bucket insertion sort below
+// is only linear when buckets are small (cells); with R buckets of ~n/R rows
+// its inversion count would be O(n^2).
+static int bucket_sort_radix(mdkk_ctx* ctx, const int* keys, int n, int nbuckets, int* bucket_start, int* order,
+                             cudaStream_t s) {
+    int bits = 1;
+    while ((1 << bits) < nbuckets) ++bits;
+    size_t sort_bytes = 0, scan_bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, (const int*)nullptr, (int*)nullptr, (const int*)nullptr,
+                                    (int*)nullptr, n, 0, bits, s);
+    cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (int*)nullptr, (int*)nullptr, nbuckets + 1, s);
+    auto al = [](size_t v) { return (v + 255) & ~size_t(255); };
+    const size_t off_cnt = 0;
+    const size_t off_ko = al(off_cnt + sizeof(int) * ((size_t)nbuckets + 64));
+    const size_t off_vi = al(off_ko + sizeof(int) * (size_t)n);
+    const size_t off_tmp = al(off_vi + sizeof(int) * (size_t)n);
+    char* base = static_cast<char*>(mdkk::scratch(ctx, off_tmp + std::max(sort_bytes, scan_bytes) + 256));
+    if (!base) return mdkk::cuda_fail(cudaErrorMemoryAllocation, "scratch");
+    int* cnt = reinterpret_cast<int*>(base + off_cnt);
+    int* kout = reinterpret_cast<int*>(base + off_ko);
+    int* vin = reinterpret_cast<int*>(base + off_vi);
+    void* tmp = base + off_tmp;
+    cudaMemsetAsync(cnt, 0, sizeof(int) * ((size_t)nbuckets + 1), s);
+    k_key_count<<<mdkk::grid_for(n, 256), 256, 0, s>>>(n, keys, cnt);
+    MDKK_CHECK_LAUNCH("k_key_count");
+    cub::DeviceScan::ExclusiveSum(tmp, scan_bytes, cnt, bucket_start, nbuckets + 1, s);
+    k_iota<<<mdkk::grid_for(n, 256), 256, 0, s>>>(n, vin);
+    MDKK_CHECK_LAUNCH("k_iota");
+    cub::DeviceRadixSort::SortPairs(tmp, sort_bytes, keys, kout, vin, order, n, 0, bits, s);
+    MDKK_CHECK_LAUNCH("cub radix sort");
+    return MDKK_OK;
+}
+
 int mdkk_bucket_sort(mdkk_ctx* ctx, const int* keys, int n, int nbuckets, int* bucket_start, int* order,
                      void* stream) {
     if (!ctx || n < 0 || nbuckets < 1 || nbuckets > (1 << 30)) return MDKK_E_ARG;
     cudaStream_t s = mdkk::as_stream(stream);
+    if (n > 0 && nbuckets <= 64) return bucket_sort_radix(ctx, keys, n, nbuckets, bucket_start, order, s);
     size_t cub_bytes = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, cub_bytes, (int*)nullptr, (int*)nullptr, nbuckets + 1, s);
     size_t off_cnt = 0;

@@ -31,7 +31,8 @@ import torch
 import torch.distributed as dist
 
 from . import _lib
-from .domain import SHIFT_UNITS, AtomStore, Box, RankSet, _rows4, _to4, cell_grid, decompose, wrap_positions
+from .domain import (SHIFT_UNITS, AtomStore, Box, RankSet, _rows4, _to4, cell_grid, decompose,
+                     _dense_ids, wrap_positions)
 
 
 class CudaOps:
@@ -152,18 +153,32 @@ class DistSystem:
         """Every process passes the same initial arrays and keeps its own brick (mdkk/domain.py:220-235)."""
         rank, world = dist.get_rank(group), dist.get_world_size(group)
         device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-        pos = wrap_positions(np.asarray(positions, dtype=np.float64).reshape(-1, 3), box)
-        vel = np.asarray(velocities, dtype=np.float64).reshape(-1, 3)
+        pos = np.ascontiguousarray(np.asarray(positions, dtype=np.float64).reshape(-1, 3))
+        vel = np.ascontiguousarray(np.asarray(velocities, dtype=np.float64).reshape(-1, 3))
         n = len(pos)
-        gids = np.arange(n, dtype=np.int64) if global_ids is None else np.asarray(global_ids, dtype=np.int64)
         rs = decompose(box, world)
-        sel = np.flatnonzero(rs.rank_of(pos) == rank)
-        cap = int(len(sel) * 1.3) + 64
-        g = torch.zeros(cap, dtype=torch.int64, device=device)
-        if len(sel):
-            g[: len(sel)] = torch.from_numpy(gids[sel]).to(device)
-        store = AtomStore(rank, device, _to4(pos[sel], device, cap), _to4(vel[sel], device), g, len(sel))
-        dense = bool(n == 0 or (gids.min() == 0 and gids.max() == n - 1 and len(np.unique(gids)) == n))
+        ops = ops or CudaOps(device)
+        # one upload of the whole input, wrap + stable owner partition on the device
+        x, v = _to4(pos, device), _to4(vel, device)
+        if global_ids is None:
+            dense, gid = True, torch.arange(max(n, 1), dtype=torch.int64, device=device)
+        else:
+            g_host = np.asarray(global_ids, dtype=np.int64).reshape(-1)
+            dense = _dense_ids(g_host, n)
+            gid = torch.from_numpy(g_host).to(device) if n else torch.zeros(1, dtype=torch.int64, device=device)
+        ops.wrap(x, n, box.lengths)
+        start, order = ops.owner_partition(x, n, box.lengths, rs.grid, world)
+        a, b = int(start[rank]), int(start[rank + 1])
+        c = b - a
+        cap = int(c * 1.3) + 64
+        xr, vr = _rows4(cap, device), _rows4(c, device)
+        gr = torch.zeros(cap, dtype=torch.int64, device=device)
+        if c:
+            o = order[a:b]
+            ops.gather_rows(x, o, c, xr)
+            ops.gather_rows(v, o, c, vr)
+            ops.gather_i64(gid, o, c, gr)
+        store = AtomStore(rank, device, xr, vr, gr, c)
         return cls(box, rs, store, device, group, ops, n, dense)
 
     # ------------------------------------------------------------ helpers
@@ -430,6 +445,10 @@ class DistSystem:
         pos, gid = self._gather_rows(self.store.x, 3)
         vel, _ = self._gather_rows(self.store.v, 3)
         return pos, vel, gid
+
+    def gather_positions(self) -> np.ndarray:
+        self.store.to_device()
+        return self._gather_rows(self.store.x, 3)[0]
 
     def gather_forces(self) -> np.ndarray:
         self.store.force.sync("b")

@@ -133,6 +133,75 @@ def _to4(a: np.ndarray, device, cap: int | None = None) -> torch.Tensor:
     return t
 
 
+def _dense_ids(gids: np.ndarray, n: int) -> bool:
+    """gids is a permutation of 0..n-1 (O(n), no sort)."""
+    if n == 0:
+        return True
+    if gids.min() != 0 or gids.max() != n - 1:
+        return False
+    seen = np.zeros(n, dtype=bool)
+    seen[gids] = True
+    return bool(seen.all())
+
+
+def device_partition(box: Box, rs: RankSet, positions, velocities, global_ids, device, ranks=None):
+    """Upload once, wrap and assign owners on the device (mdkk/domain.py:220-235).
+
+    Returns ({rank: (x rows4 with ghost headroom, v rows4, gid int64, n)}, dense).
+    Rows of each brick keep the input order (the reference's
+    ``np.flatnonzero(owner == r)``): the owner partition is a stable radix
+    sort.  Wrap is bit-identical to mdkk/domain.py:62.
+    """
+    pos = np.ascontiguousarray(np.asarray(positions, dtype=np.float64).reshape(-1, 3))
+    vel = np.ascontiguousarray(np.asarray(velocities, dtype=np.float64).reshape(-1, 3))
+    n = len(pos)
+    if global_ids is None:
+        dense = True
+        gid = torch.arange(max(n, 1), dtype=torch.int64, device=device)
+    else:
+        g_host = np.asarray(global_ids, dtype=np.int64).reshape(-1)
+        dense = _dense_ids(g_host, n)
+        gid = torch.from_numpy(g_host).to(device) if n else torch.zeros(1, dtype=torch.int64, device=device)
+    R = rs.n_ranks
+    ranks = range(R) if ranks is None else ranks
+    lib, stream = _lib.lib(), _lib.stream(device)
+    cap_all = int(n * 1.3) + 64 if R == 1 else n
+    x = _rows4(cap_all, device)
+    v = _rows4(n, device)
+    if n:
+        x[:n, :3] = torch.from_numpy(pos).to(device)
+        v[:n, :3] = torch.from_numpy(vel).to(device)
+        _lib.check(lib.mdkk_wrap(x.data_ptr(), n, _lib.dbl3(box.lengths), stream), "mdkk_wrap")
+    if R == 1:
+        g = torch.zeros(cap_all, dtype=torch.int64, device=device)
+        g[:n] = gid[:n]
+        return {0: (x, v, g, n)}, dense
+    ctx = _lib.ctx(device)
+    keys = torch.empty(max(n, 1), dtype=torch.int32, device=device)
+    start = torch.zeros(R + 1, dtype=torch.int32, device=device)
+    order = torch.empty(max(n, 1), dtype=torch.int32, device=device)
+    if n:
+        _lib.check(lib.mdkk_rank_keys(x.data_ptr(), n, _lib.dbl3(box.lengths), _lib.int_arr(rs.grid),
+                                      keys.data_ptr(), stream), "mdkk_rank_keys")
+        _lib.check(lib.mdkk_bucket_sort(ctx, keys.data_ptr(), n, R, start.data_ptr(), order.data_ptr(), stream),
+                   "mdkk_bucket_sort")
+    st = start.cpu().numpy().astype(np.int64)
+    out = {}
+    for r in ranks:
+        a, b = int(st[r]), int(st[r + 1])
+        c = b - a
+        cap = int(c * 1.3) + 64
+        xr, vr = _rows4(cap, device), _rows4(c, device)
+        gr = torch.zeros(cap, dtype=torch.int64, device=device)
+        if c:
+            o = order[a:b]
+            _lib.check(lib.mdkk_gather_rows4(x.data_ptr(), o.data_ptr(), c, xr.data_ptr(), stream), "g4")
+            _lib.check(lib.mdkk_gather_rows4(v.data_ptr(), o.data_ptr(), c, vr.data_ptr(), stream), "g4")
+            _lib.check(lib.mdkk_gather_i64(gid.data_ptr(), o.data_ptr(), c, gr.data_ptr(), stream), "g64")
+        out[r] = (xr, vr, gr, c)
+    return out, dense
+
+
 _ROW = None
 
 
@@ -165,6 +234,7 @@ class AtomStore:
         self._lanes_in = []       # lanes whose ghost rows live here (for ghost_shift)
         self._alt = None          # double buffers for the spatial sort
         self._views()
+        self.device_wrote(pos=True, vel=True)   # the rows were uploaded: HBM holds the current data
 
     @property
     def capacity(self) -> int:
@@ -304,23 +374,11 @@ class RankedSystem:
     @classmethod
     def distribute(cls, box: Box, n_ranks: int, positions, velocities, global_ids=None,
                    device=None) -> "RankedSystem":
-        """Wrap, assign owners, upload (mdkk/domain.py:220-235).  Setup is host-side, as in the reference."""
+        """Wrap, assign owners, upload (mdkk/domain.py:220-235); one upload, owners assigned on device."""
         device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-        pos = wrap_positions(np.asarray(positions, dtype=np.float64).reshape(-1, 3), box)
-        vel = np.asarray(velocities, dtype=np.float64).reshape(-1, 3)
-        n = len(pos)
-        gids = np.arange(n, dtype=np.int64) if global_ids is None else np.asarray(global_ids, dtype=np.int64)
-        dense = bool(n == 0 or (gids.min() == 0 and gids.max() == n - 1 and len(np.unique(gids)) == n))
         rs = decompose(box, n_ranks)
-        owner = rs.rank_of(pos)
-        stores = []
-        for r in range(rs.n_ranks):
-            sel = np.flatnonzero(owner == r)
-            cap = int(len(sel) * 1.3) + 64   # headroom for ghost rows
-            g = torch.zeros(cap, dtype=torch.int64, device=device)
-            if len(sel):
-                g[: len(sel)] = torch.from_numpy(gids[sel]).to(device)
-            stores.append(AtomStore(r, device, _to4(pos[sel], device, cap), _to4(vel[sel], device), g, len(sel)))
+        parts, dense = device_partition(box, rs, positions, velocities, global_ids, device)
+        stores = [AtomStore(r, device, *parts[r]) for r in range(rs.n_ranks)]
         return cls(box, rs, stores, device, dense)
 
     # ------------------------------------------------------------ ghosts
@@ -567,7 +625,7 @@ class RankedSystem:
                     gi = s.gid[: s.n_local].to(torch.int32)
                     _lib.check(lib.mdkk_scatter_rows4(rows_fn(s).data_ptr(), gi.data_ptr(), s.n_local,
                                                       out.data_ptr(), stream), "scatter")
-            return out[:n, :width].cpu().numpy()
+            return out[:n, :width].contiguous().cpu().numpy()
         rows = np.concatenate([rows_fn(s)[: s.n_local, :width].cpu().numpy() for s in self.stores])
         gid = np.concatenate([s.global_ids[: s.n_local] for s in self.stores])
         return rows[np.argsort(gid, kind="stable")]
@@ -578,8 +636,17 @@ class RankedSystem:
             s.to_device()
         pos = self._gid_order(lambda s: s.x, 3)
         vel = self._gid_order(lambda s: s.v, 3)
-        gid = np.sort(np.concatenate([s.global_ids[: s.n_local] for s in self.stores]), kind="stable")
+        if self.dense_gids:
+            gid = np.arange(self.n_atoms, dtype=np.int64)
+        else:
+            gid = np.sort(np.concatenate([s.global_ids[: s.n_local] for s in self.stores]), kind="stable")
         return pos, vel, gid
+
+    def gather_positions(self) -> np.ndarray:
+        """Owned positions in global-id order (the thermo snapshot; no velocity read-back)."""
+        for s in self.stores:
+            s.to_device()
+        return self._gid_order(lambda s: s.x, 3)
 
     def gather_forces(self) -> np.ndarray:
         """Owned forces in global-id order (mdkk/domain.py:344-348)."""

@@ -405,7 +405,7 @@ class Simulation:
                 ke, t = self._kinetic()
                 result.log(step, e_pot, ke, t)
                 if self.snapshots:
-                    result.snapshots[step] = self.system.gather()[0]
+                    result.snapshots[step] = self.system.gather_positions()
                 self.log(result.lines[-1])
 
             log(0, self._forces_device())
