@@ -164,36 +164,42 @@ int mdkk_kinetic(mdkk_ctx* ctx, const double* v, int n, double mass, double* ke,
 /* ------------------------------------------------------------------- SNAP
  * FP64 descriptor pipeline with mdkk's conventions (mdkk/snap/compute.py:
  * rfac0 0.99, rmin0 0, cosine switch, no self term, full (2j+1)^2 blocks,
- * full three-slot adjoint).  U, Y are complex128 row-major [n_local][n_flat]
- * (the reference's layout "a"); n_flat = sum_{tj<=2J} (tj+1)^2.
+ * full three-slot adjoint).  U is complex128 row-major [n_local][n_flat]
+ * (the reference's layout "a"), n_flat = sum_{tj<=2J} (tj+1)^2.  The engine
+ * keeps Y as its half set (2p < tj, or 2p == tj and 2q <= tj; n_half entries,
+ * the rest follows from Y[tj-p][tj-q] = (-1)^(p+q) conj(Y[p][q])) transposed,
+ * Yh[e][i] with leading dimension ld >= n_local; mdkk_snap_y_expand /
+ * _compress convert to / from the reference layout.
  * Pairs are the entries of a FULL cluster-blocked table with r^2 < rc^2.
  *
- * mdkk_snap_create copies the half-block adjoint table built on the host from
- * the exact Clebsch-Gordan terms and beta (mdkk/snap/coupling.py:106-133,
- * mdkk/snap/compute.py:303-340):
- *   Y[f] = sum_k coef[k] * op(U[g_k]) * U[h_k]   (op = conj for slot-1/2 terms)
- * for the n_half outputs with 2p < tj or (2p == tj, 2q <= tj), in rows of 32
- * entries sharing one output (row_f[r] = its half index), gh[k] = g | h << 12 |
- * conj << 24; the other outputs follow from Y[tj-p][tj-q] = (-1)^(p+q)
- * conj(Y[p][q]) via fmap[f] = half index | mirrored << 16 | odd sign << 17.
- * 0 <= 2J <= 8. */
-int mdkk_snap_create(mdkk_ctx* ctx, int twojmax, int n_rows, const int* row_f_host, const int* gh_host,
-                     const double* coef_host, int n_half, const int* fmap_host, mdkk_snap** out_host);
+ * mdkk_snap_create copies the product list built on the host from the exact
+ * Clebsch-Gordan terms and beta (mdkk/snap/coupling.py:106-133; the Z-list form
+ * of mdkk/snap/compute.py:303-340, see snap/coupling.py zlist_entries):
+ *   Yh[f] = sum_k coef[k] * op_g(U[g_k]) * op_h(U[h_k])      (half indices)
+ * code[k] = g | h << 8 | f << 16 | conj_g << 24 | conj_h << 25 | last << 26 |
+ * center << 27, sorted by output f, `last` on the final product of each output,
+ * `center` when f is its own mirror; fmap[flat] = half index | mirrored << 16 |
+ * odd sign << 17.  0 <= 2J <= 8. */
+int mdkk_snap_create(mdkk_ctx* ctx, int twojmax, int n_entries, const double* coef_host, const int* code_host,
+                     int n_half, const int* fmap_host, mdkk_snap** out_host);
 int mdkk_snap_destroy(mdkk_snap* snap);
 /* U_i = sum_k f_c(r_ik) u(a_ik, b_ik) (compute_ui, mdkk/snap/compute.py:279-292); flags gets
  * MDKK_FLAG_COINCIDENT for r = 0 pairs (mdkk/snap/compute.py:117-118). */
 int mdkk_snap_ui(mdkk_snap* snap, const double* x, int n_local, const int* table, const int* counts, int cap,
                  double rc, double* U, int* flags, void* stream);
-/* Y from U (compute_yi) and *energy (device double) = sum_i Re(Y_i . conj(U_i)) / 3
- * (energy_from_y, mdkk/snap/compute.py:376-387). */
-int mdkk_snap_yi(mdkk_ctx* ctx, mdkk_snap* snap, const double* U, int n_local, double* Y, double* energy,
+/* Yh from U (compute_yi, mdkk/snap/compute.py:303-340) and *energy (device double)
+ * = sum_i Re(Y_i . conj(U_i)) / 3 (energy_from_y, mdkk/snap/compute.py:376-387). */
+int mdkk_snap_yi(mdkk_ctx* ctx, mdkk_snap* snap, const double* U, int n_local, double* Yh, int ld, double* energy,
                  void* stream);
+/* Reference layout: Y[i][flat] (complex128 row-major) from Yh, and back. */
+int mdkk_snap_y_expand(mdkk_snap* snap, const double* Yh, int ld, int n_local, double* Y, void* stream);
+int mdkk_snap_y_compress(mdkk_snap* snap, const double* Y, int n_local, double* Yh, int ld, void* stream);
 /* Fused 3-direction forces (compute_fused_deidrj, mdkk/snap/compute.py:390-409):
  * t = Re sum_f Y_i[f] conj(d(f_c u)/d r_ik [f]) evaluated in reverse mode (u
  * forward, adjoint backward, 4 complex partials per pair); f_i += t, f_k -= t (FP64
  * atomics, f double4 rows incl. ghosts, caller-zeroed; ghosts -> reverse comm). */
 int mdkk_snap_deidrj(mdkk_snap* snap, const double* x, int n_local, const int* table, const int* counts, int cap,
-                     double rc, const double* Y, double* f, void* stream);
+                     double rc, const double* Yh, int ld, double* f, void* stream);
 
 #ifdef __cplusplus
 }

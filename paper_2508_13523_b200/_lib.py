@@ -51,11 +51,13 @@ SIGNATURES = {
     "mdkk_verlet_first": [_p, _p, _p, _p, _p, _i, _d, _d, _p, _p],
     "mdkk_verlet_second": [_p, _p, _p, _i, _d, _d, _p, _p],
     "mdkk_kinetic": [_p, _p, _i, _d, _p, _p],
-    "mdkk_snap_create": [_p, _i, _i, _p, _p, _p, _i, _p, _p],
+    "mdkk_snap_create": [_p, _i, _i, _p, _p, _i, _p, _p],
     "mdkk_snap_destroy": [_p],
     "mdkk_snap_ui": [_p, _p, _i, _p, _p, _i, _d, _p, _p, _p],
-    "mdkk_snap_yi": [_p, _p, _p, _i, _p, _p, _p],
-    "mdkk_snap_deidrj": [_p, _p, _i, _p, _p, _i, _d, _p, _p, _p],
+    "mdkk_snap_yi": [_p, _p, _p, _i, _p, _i, _p, _p],
+    "mdkk_snap_y_expand": [_p, _p, _i, _i, _p, _p],
+    "mdkk_snap_y_compress": [_p, _p, _i, _p, _i, _p],
+    "mdkk_snap_deidrj": [_p, _p, _i, _p, _p, _i, _d, _p, _i, _p, _p],
 }
 _RESTYPE = {"mdkk_last_error": C.c_char_p, "mdkk_launch_count": C.c_ulonglong}
 

@@ -21,15 +21,20 @@
 
 #include "common.cuh"
 
+struct ZEntry {      // one U*U product of the Z-list adjoint (16 B, read as a warp broadcast)
+    double coef;
+    int code;        // g | h << 8 | f << 16 | conj_g << 24 | conj_h << 25 | last-of-output << 26 | center << 27
+    int pad;
+};
+
 struct mdkk_snap {
     int twojmax = 0;
     int n_flat = 0;
     int n_half = 0;
-    int n_rows = 0;
-    int* row_f = nullptr;   // [n_rows] half-block output of each 32-entry row
-    int* gh = nullptr;      // [n_rows*32] g | h << 12 | conj << 24
-    double* coef = nullptr; // [n_rows*32]
-    int* fmap = nullptr;    // [n_flat] half index | mirrored << 16 | odd sign << 17
+    int n_entries = 0;
+    ZEntry* ent = nullptr;   // [n_entries], sorted by output
+    int* chunk = nullptr;    // [kYW + 1] per-warp entry ranges (output-aligned, balanced)
+    int* fmap = nullptr;     // [n_flat] half index | mirrored << 16 | odd sign << 17
 };
 
 namespace {
@@ -289,82 +294,93 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_snap_ui(const double* __rest
 }
 
 // ---------------------------------------------------------------- compute_yi
-// Y_i[f] = sum_k coef_k op(U_i[g_k]) U_i[h_k] (op = conj for slot-1/2 terms,
-// mdkk/snap/compute.py:303-340) for the half-block outputs only; the mirror
-// half follows from Y[tj-p][tj-q] = (-1)^(p+q) conj(Y[p][q]).  Also
-// e_i = Re sum_f Y_i[f] conj(U_i[f]) / 3 (energy_from_y, :376-387).
-// One warp per atom, 8 atoms per CTA; the contribution table is streamed
-// through shared memory in rows of 32 entries that share one output, sorted by
-// (g, h) so the lanes' U_i reads fall on neighbouring banks; each output is
-// one warp reduction (no atomics).
-constexpr int kYWarps = 8;
-constexpr int kYRows = 32;
+// Half-block Y (outputs 2p < tj, or 2p == tj and 2q <= tj) as a list of U*U
+// products, the Z-list form of the reference's three-slot adjoint
+// (mdkk/snap/compute.py:303-340; equivalence: snap/coupling.py zlist_entries):
+//   Y[f] = sum_k coef_k * op_g(U[g_k]) * op_h(U[h_k]),  op = identity or conj.
+// Atoms run across lanes (32 per CTA, one per lane) and the product list is
+// uniform across the warp: every lane reads U of its own atom from a
+// shared-memory tile [half index][atom] (row stride 33: conflict-free stores
+// and reads), the entry itself is one broadcast.  Each warp owns a contiguous,
+// output-aligned slice of the list, so every output is one register sum
+// (no atomics, deterministic) written coalesced to Yh[f][atom] (the engine's
+// half/transposed layout; the reference layout comes from mdkk_snap_y_expand).
+// Also e_i = Re sum_f Y_i[f] conj(U_i[f]) / 3 (energy_from_y, :376-387) from
+// the half set with mirror weight 2.
+constexpr int kYW = 16;                      // warps per CTA (2 CTAs per SM: 32 warps)
+constexpr int kUS = 33;                      // tile row stride (double2)
+
+__constant__ short c_hflat[kHalfAll];       // half index -> flat index
 
 template <int NF, int NH>
-__global__ void __launch_bounds__(kYWarps * 32) k_snap_yi(const double2* __restrict__ U, int n, int n_rows,
-                                                          const int* __restrict__ row_f, const int* __restrict__ gh,
-                                                          const double* __restrict__ coef,
-                                                          const int* __restrict__ fmap, double2* __restrict__ Y,
-                                                          double* __restrict__ partials) {
+__global__ void __launch_bounds__(kYW * 32, 2) k_snap_yi(const double2* __restrict__ U, int n,
+                                                         const ZEntry* __restrict__ ent,
+                                                         const int* __restrict__ chunk, double2* __restrict__ Yh,
+                                                         int ld, double* __restrict__ partials) {
     extern __shared__ double2 s_dyn2[];
-    auto s_u = reinterpret_cast<double2(*)[NF]>(s_dyn2);                  // [kYWarps][NF]
-    auto s_yh = reinterpret_cast<double2(*)[NH]>(s_u + kYWarps);          // [kYWarps][NH]
-    auto s_cf = reinterpret_cast<double(*)[32]>(s_yh + kYWarps);          // [kYRows][32]
-    auto s_gh = reinterpret_cast<int(*)[32]>(s_cf + kYRows);              // [kYRows][32]
-    int* s_rf = reinterpret_cast<int*>(s_gh + kYRows);                    // [kYRows]
+    double2* s_u = s_dyn2;                                                   // [NH][kUS]
+    ZEntry* s_e = reinterpret_cast<ZEntry*>(s_u + NH * kUS);                  // [kYW][32]
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int i = blockIdx.x * kYWarps + w;
-    const bool valid = i < n;
-    for (int f = lane; f < NF; f += 32) s_u[w][f] = valid ? U[(long long)i * NF + f] : make_double2(0.0, 0.0);
-    int cur = -1;
-    double are = 0.0, aim = 0.0;
-    for (int base = 0; base < n_rows; base += kYRows) {
-        const int nr = min(kYRows, n_rows - base);
-        __syncthreads();
-        for (int t = threadIdx.x; t < nr * 32; t += blockDim.x) {
-            s_gh[t >> 5][t & 31] = __ldg(gh + (long long)base * 32 + t);
-            s_cf[t >> 5][t & 31] = __ldg(coef + (long long)base * 32 + t);
-        }
-        for (int t = threadIdx.x; t < nr; t += blockDim.x) s_rf[t] = __ldg(row_f + base + t);
-        __syncthreads();
-        if (!valid) continue;
-        for (int r = 0; r < nr; ++r) {
-            const int fr = s_rf[r];
-            if (fr != cur) {  // warp-uniform
-                if (cur >= 0) {
-                    const double sr = mdkk::warp_sum(are), si = mdkk::warp_sum(aim);
-                    if (lane == 0) s_yh[w][cur] = make_double2(sr, si);
-                }
-                cur = fr;
+    const int a0 = blockIdx.x * 32;
+    for (int t = threadIdx.x; t < 32 * NH; t += blockDim.x) {
+        const int a = t / NH, e = t - a * NH;
+        s_u[e * kUS + a] = (a0 + a < n) ? U[(long long)(a0 + a) * NF + c_hflat[e]] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+    const bool valid = a0 + lane < n;
+    const int beg = chunk[w], end = chunk[w + 1];
+    ZEntry* se = s_e + w * 32;
+    double are = 0.0, aim = 0.0, en = 0.0;
+    for (int base = beg; base < end; base += 32) {
+        if (base + lane < end) se[lane] = ent[base + lane];
+        __syncwarp();
+        const int cnt = min(32, end - base);
+        for (int j = 0; j < cnt; ++j) {
+            const double c = se[j].coef;
+            const int code = se[j].code;
+            double2 ug = s_u[(code & 255) * kUS + lane];
+            double2 uh = s_u[((code >> 8) & 255) * kUS + lane];
+            if (code & (1 << 24)) ug.y = -ug.y;
+            if (code & (1 << 25)) uh.y = -uh.y;
+            const double tre = ug.x * uh.x - ug.y * uh.y;
+            const double tim = ug.x * uh.y + ug.y * uh.x;
+            are = fma(c, tre, are);
+            aim = fma(c, tim, aim);
+            if (code & (1 << 26)) {   // warp-uniform: output complete
+                const int f = (code >> 16) & 255;
+                if (valid) Yh[(long long)f * ld + a0 + lane] = make_double2(are, aim);
+                const double2 u = s_u[f * kUS + lane];
+                en += ((code & (1 << 27)) ? 1.0 : 2.0) * (are * u.x + aim * u.y);
                 are = aim = 0.0;
             }
-            const int e = s_gh[r][lane];
-            const double c = s_cf[r][lane];
-            const double2 ug = s_u[w][e & 0xfff];
-            const double2 uh = s_u[w][(e >> 12) & 0xfff];
-            const double gi = (e >> 24) ? -ug.y : ug.y;
-            are += c * (ug.x * uh.x - gi * uh.y);
-            aim += c * (ug.x * uh.y + gi * uh.x);
-        }
-    }
-    double en[1] = {0.0};
-    if (valid) {
-        if (cur >= 0) {
-            const double sr = mdkk::warp_sum(are), si = mdkk::warp_sum(aim);
-            if (lane == 0) s_yh[w][cur] = make_double2(sr, si);
         }
         __syncwarp();
-        for (int f = lane; f < NF; f += 32) {
-            const int m = __ldg(fmap + f);
-            double2 v = s_yh[w][m & 0xffff];
-            if ((m >> 16) & 1) v.y = -v.y;
-            if ((m >> 17) & 1) v = make_double2(-v.x, -v.y);
-            Y[(long long)i * NF + f] = v;
-            en[0] += v.x * s_u[w][f].x + v.y * s_u[w][f].y;  // Re(Y conj(U))
-        }
-        en[0] /= 3.0;
     }
-    mdkk::block_sum<1, kYWarps * 32>(en, partials + blockIdx.x);
+    double v[1] = {valid ? en / 3.0 : 0.0};
+    mdkk::block_sum<1, kYW * 32>(v, partials + blockIdx.x);
+}
+
+// Reference layout "a": full Y rows [n][NF] from the half/transposed Yh, using
+// Y[tj-p][tj-q] = (-1)^(p+q) conj(Y[p][q]).
+__global__ void k_snap_y_expand(const double2* __restrict__ Yh, int ld, int n, int nf,
+                                const int* __restrict__ fmap, double2* __restrict__ Y) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (long long)n * nf) return;
+    const int i = (int)(t / nf), f = (int)(t - (long long)i * nf);
+    const int m = __ldg(fmap + f);
+    double2 v = Yh[(long long)(m & 0xffff) * ld + i];
+    if ((m >> 16) & 1) v.y = -v.y;
+    if ((m >> 17) & 1) v = make_double2(-v.x, -v.y);
+    Y[t] = v;
+}
+
+// Inverse of the expansion (a host-written reference-layout Y -> engine layout).
+__global__ void k_snap_y_compress(const double2* __restrict__ Y, int n, int nf, int nh, double2* __restrict__ Yh,
+                                  int ld) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (long long)n * nh) return;
+    const int e = (int)(t / n), i = (int)(t - (long long)e * n);
+    Yh[(long long)e * ld + i] = Y[(long long)i * nf + c_hflat[e]];
 }
 
 // ------------------------------------------------------- compute_fused_deidrj
@@ -382,7 +398,7 @@ template <int TWOJ>
 __global__ void __launch_bounds__(kWarps * 32, 3) k_snap_deidrj(const double* __restrict__ x, int n_local,
                                                              const int* __restrict__ table,
                                                              const int* __restrict__ counts, int cap, double rc,
-                                                             const double2* __restrict__ Y,
+                                                             const double2* __restrict__ Yh, int ld,
                                                              double* __restrict__ f) {
     constexpr int NF = block_offset(TWOJ + 1);
     constexpr int NH = half_offset(TWOJ + 1);
@@ -396,13 +412,10 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_snap_deidrj(const double* __
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, hl = lane & 15, hh = lane >> 4;
     const int i = blockIdx.x * kWarps + w;
     if (i >= n_local) return;
-    const double2* Yi = Y + (long long)i * NF;
-#pragma unroll
-    for (int tj = 0; tj <= TWOJ; ++tj)
-        for (int h = lane; h < half_size(tj); h += 32) {
-            const double2 v = Yi[block_offset(tj) + h];
-            s_y[w][half_offset(tj) + h] = {v.x, v.y};
-        }
+    for (int e = lane; e < NH; e += 32) {
+        const double2 v = Yh[(long long)e * ld + i];
+        s_y[w][e] = {v.x, v.y};
+    }
     __syncwarp();
     const cplx* sy = s_y[w];
     cplx* ul = s_u[w][hh];
@@ -539,6 +552,10 @@ void upload_weights() {
                 h[3][e] = std::sqrt((double)((tj - P) * (tj - Q))) / tj;
             }
     cudaMemcpyToSymbol(g_w, h, sizeof(h));
+    static short hf[kHalfAll];
+    for (int tj = 0; tj <= kMaxTwoJ; ++tj)
+        for (int k = 0; k < half_size(tj); ++k) hf[half_offset(tj) + k] = (short)(block_offset(tj) + k);
+    cudaMemcpyToSymbol(c_hflat, hf, sizeof(hf));
     done = true;
 }
 
@@ -560,31 +577,52 @@ void upload_weights() {
 
 extern "C" {
 
-int mdkk_snap_create(mdkk_ctx* ctx, int twojmax, int n_rows, const int* row_f_host, const int* gh_host,
-                     const double* coef_host, int n_half, const int* fmap_host, mdkk_snap** out_host) {
-    static const int kHalf[kMaxTwoJ + 1] = {1, 3, 8, 16, 29, 47, 72, 104, 145};
-    if (!ctx || !out_host || twojmax < 0 || twojmax > kMaxTwoJ || n_rows < 0 || n_half != kHalf[twojmax]) {
-        mdkk::set_error("mdkk_snap_create: 2J must be in [0, 8]");
+int mdkk_snap_create(mdkk_ctx* ctx, int twojmax, int n_entries, const double* coef_host, const int* code_host,
+                     int n_half, const int* fmap_host, mdkk_snap** out_host) {
+    if (!ctx || !out_host || twojmax < 0 || twojmax > kMaxTwoJ || n_entries < 1 || !coef_host || !code_host ||
+        n_half != half_offset(twojmax + 1)) {
+        mdkk::set_error("mdkk_snap_create: 2J must be in [0, 8] with a non-empty product list");
         return MDKK_E_ARG;
+    }
+    // host copy of the list + output-aligned per-warp chunks balanced on entry counts
+    std::vector<ZEntry> h(n_entries);
+    std::vector<int> ends;  // entry index one past each output
+    for (int k = 0; k < n_entries; ++k) {
+        h[k].coef = coef_host[k];
+        h[k].code = code_host[k];
+        h[k].pad = 0;
+        if (code_host[k] & (1 << 26)) ends.push_back(k + 1);
+    }
+    if (ends.empty() || ends.back() != n_entries) {
+        mdkk::set_error("mdkk_snap_create: product list must end on an output boundary");
+        return MDKK_E_ARG;
+    }
+    std::vector<int> chunk(kYW + 1, n_entries);
+    chunk[0] = 0;
+    {
+        size_t o = 0;
+        for (int w = 1; w < kYW; ++w) {
+            const double target = (double)n_entries * w / kYW;
+            while (o < ends.size() && ends[o] < target) ++o;
+            chunk[w] = o < ends.size() ? std::max(chunk[w - 1], ends[o]) : n_entries;
+            if (o < ends.size() && o > 0 && (ends[o] - target) > (target - ends[o - 1]))
+                chunk[w] = std::max(chunk[w - 1], ends[o - 1]);
+        }
     }
     auto* s = new mdkk_snap();
     s->twojmax = twojmax;
     s->n_flat = block_offset(twojmax + 1);
     s->n_half = n_half;
-    s->n_rows = n_rows;
-    const size_t ne = (size_t)std::max(n_rows, 1) * 32;
-    cudaError_t e = cudaMalloc(&s->row_f, sizeof(int) * std::max(n_rows, 1));
-    if (e == cudaSuccess) e = cudaMalloc(&s->gh, sizeof(int) * ne);
-    if (e == cudaSuccess) e = cudaMalloc(&s->coef, sizeof(double) * ne);
+    s->n_entries = n_entries;
+    cudaError_t e = cudaMalloc(&s->ent, sizeof(ZEntry) * n_entries);
+    if (e == cudaSuccess) e = cudaMalloc(&s->chunk, sizeof(int) * (kYW + 1));
     if (e == cudaSuccess) e = cudaMalloc(&s->fmap, sizeof(int) * s->n_flat);
-    if (e == cudaSuccess && n_rows) e = cudaMemcpy(s->row_f, row_f_host, sizeof(int) * n_rows, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess && n_rows) e = cudaMemcpy(s->gh, gh_host, sizeof(int) * n_rows * 32, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess && n_rows) e = cudaMemcpy(s->coef, coef_host, sizeof(double) * n_rows * 32, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(s->ent, h.data(), sizeof(ZEntry) * n_entries, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(s->chunk, chunk.data(), sizeof(int) * (kYW + 1), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(s->fmap, fmap_host, sizeof(int) * s->n_flat, cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
-        cudaFree(s->row_f);
-        cudaFree(s->gh);
-        cudaFree(s->coef);
+        cudaFree(s->ent);
+        cudaFree(s->chunk);
         cudaFree(s->fmap);
         delete s;
         return mdkk::cuda_fail(e, "mdkk_snap_create");
@@ -596,9 +634,8 @@ int mdkk_snap_create(mdkk_ctx* ctx, int twojmax, int n_rows, const int* row_f_ho
 
 int mdkk_snap_destroy(mdkk_snap* s) {
     if (!s) return MDKK_OK;
-    cudaFree(s->row_f);
-    cudaFree(s->gh);
-    cudaFree(s->coef);
+    cudaFree(s->ent);
+    cudaFree(s->chunk);
     cudaFree(s->fmap);
     delete s;
     return MDKK_OK;
@@ -616,31 +653,30 @@ int mdkk_snap_ui(mdkk_snap* s, const double* x, int n_local, const int* table, c
     return MDKK_OK;
 }
 
-int mdkk_snap_yi(mdkk_ctx* ctx, mdkk_snap* s, const double* U, int n_local, double* Y, double* energy, void* stream) {
-    if (!ctx || !s || n_local < 0) return MDKK_E_ARG;
+int mdkk_snap_yi(mdkk_ctx* ctx, mdkk_snap* s, const double* U, int n_local, double* Yh, int ld, double* energy,
+                 void* stream) {
+    if (!ctx || !s || n_local < 0 || ld < n_local) return MDKK_E_ARG;
     cudaStream_t st = mdkk::as_stream(stream);
     if (n_local == 0) {
         cudaMemsetAsync(energy, 0, sizeof(double), st);
         return MDKK_OK;
     }
-    const int nb = (n_local + kYWarps - 1) / kYWarps;
+    upload_weights();
+    const int nb = (n_local + 31) / 32;
     double* partials = static_cast<double*>(mdkk::scratch(ctx, sizeof(double) * (size_t)nb));
     if (!partials) return mdkk::cuda_fail(cudaErrorMemoryAllocation, "scratch");
     const double2* u = reinterpret_cast<const double2*>(U);
-    double2* y = reinterpret_cast<double2*>(Y);
+    double2* y = reinterpret_cast<double2*>(Yh);
     switch (s->twojmax) {
-#define MDKK_YI(TJ, NH)                                                                                          \
-    case TJ: {                                                                                                   \
-        constexpr int NF = block_offset(TJ + 1);                                                                 \
-        const size_t sm = kYWarps * (NF + NH) * sizeof(double2) + kYRows * 32 * (sizeof(double) + sizeof(int)) + \
-                          kYRows * sizeof(int);                                                                 \
-        cudaFuncSetAttribute(k_snap_yi<NF, NH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);          \
-        k_snap_yi<NF, NH><<<nb, kYWarps * 32, sm, st>>>(u, n_local, s->n_rows, s->row_f, s->gh, s->coef, s->fmap, \
-                                                        y, partials);                                           \
-        break;                                                                                                   \
+#define MDKK_YI(TJ)                                                                                             \
+    case TJ: {                                                                                                  \
+        constexpr int NF = block_offset(TJ + 1), NH = half_offset(TJ + 1);                                      \
+        const size_t sm = NH * kUS * sizeof(double2) + kYW * 32 * sizeof(ZEntry);                               \
+        cudaFuncSetAttribute(k_snap_yi<NF, NH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);         \
+        k_snap_yi<NF, NH><<<nb, kYW * 32, sm, st>>>(u, n_local, s->ent, s->chunk, y, ld, partials);             \
+        break;                                                                                                  \
     }
-        MDKK_YI(0, 1) MDKK_YI(1, 3) MDKK_YI(2, 8) MDKK_YI(3, 16) MDKK_YI(4, 29) MDKK_YI(5, 47) MDKK_YI(6, 72)
-        MDKK_YI(7, 104) MDKK_YI(8, 145)
+        MDKK_YI(0) MDKK_YI(1) MDKK_YI(2) MDKK_YI(3) MDKK_YI(4) MDKK_YI(5) MDKK_YI(6) MDKK_YI(7) MDKK_YI(8)
 #undef MDKK_YI
         default: return MDKK_E_ARG;
     }
@@ -650,9 +686,30 @@ int mdkk_snap_yi(mdkk_ctx* ctx, mdkk_snap* s, const double* U, int n_local, doub
     return MDKK_OK;
 }
 
+int mdkk_snap_y_expand(mdkk_snap* s, const double* Yh, int ld, int n_local, double* Y, void* stream) {
+    if (!s || n_local < 0 || ld < n_local) return MDKK_E_ARG;
+    if (n_local == 0) return MDKK_OK;
+    const long long tot = (long long)n_local * s->n_flat;
+    k_snap_y_expand<<<(unsigned)((tot + 255) / 256), 256, 0, mdkk::as_stream(stream)>>>(
+        reinterpret_cast<const double2*>(Yh), ld, n_local, s->n_flat, s->fmap, reinterpret_cast<double2*>(Y));
+    MDKK_CHECK_LAUNCH("k_snap_y_expand");
+    return MDKK_OK;
+}
+
+int mdkk_snap_y_compress(mdkk_snap* s, const double* Y, int n_local, double* Yh, int ld, void* stream) {
+    if (!s || n_local < 0 || ld < n_local) return MDKK_E_ARG;
+    if (n_local == 0) return MDKK_OK;
+    upload_weights();
+    const long long tot = (long long)n_local * s->n_half;
+    k_snap_y_compress<<<(unsigned)((tot + 255) / 256), 256, 0, mdkk::as_stream(stream)>>>(
+        reinterpret_cast<const double2*>(Y), n_local, s->n_flat, s->n_half, reinterpret_cast<double2*>(Yh), ld);
+    MDKK_CHECK_LAUNCH("k_snap_y_compress");
+    return MDKK_OK;
+}
+
 int mdkk_snap_deidrj(mdkk_snap* s, const double* x, int n_local, const int* table, const int* counts, int cap,
-                     double rc, const double* Y, double* f, void* stream) {
-    if (!s || n_local < 0 || cap < 1) return MDKK_E_ARG;
+                     double rc, const double* Yh, int ld, double* f, void* stream) {
+    if (!s || n_local < 0 || cap < 1 || ld < n_local) return MDKK_E_ARG;
     if (n_local == 0) return MDKK_OK;
     upload_weights();
     const int nb = (n_local + kWarps - 1) / kWarps;
@@ -663,7 +720,7 @@ int mdkk_snap_deidrj(mdkk_snap* s, const double* x, int n_local, const int* tabl
             (half_offset(TJ + 1) + 2 * block_offset(TJ + 1) + 4 * kLevelMax) * sizeof(cplx));                \
         cudaFuncSetAttribute(k_snap_deidrj<TJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);      \
         k_snap_deidrj<TJ><<<nb, kWarps * 32, sm, mdkk::as_stream(stream)>>>(                                 \
-            x, n_local, table, counts, cap, rc, reinterpret_cast<const double2*>(Y), f);                     \
+            x, n_local, table, counts, cap, rc, reinterpret_cast<const double2*>(Yh), ld, f);                \
         break;                                                                                               \
     }
         MDKK_DE(0) MDKK_DE(1) MDKK_DE(2) MDKK_DE(3) MDKK_DE(4) MDKK_DE(5) MDKK_DE(6) MDKK_DE(7) MDKK_DE(8)

@@ -2,11 +2,13 @@
 
 `build_neighbor_map`, `SnapState`, `compute_ui`, `compute_yi`,
 `compute_fused_deidrj`, `compute_energy`, `energy_from_y` keep the reference
-signatures (mdkk/snap/compute.py:105-436).  U and Y live in HBM as complex128
-row-major [n_atoms][n_flat] (the reference's layout "a"); the
-`layout` / `batch_u` / `batch_y` / `tile_v` knobs are accepted for signature
-parity (the reference guarantees they never change results,
-mdkk/snap/compute.py:238-276) and do not change the GPU schedule.
+signatures (mdkk/snap/compute.py:105-436).  U lives in HBM as complex128
+row-major [n_atoms][n_flat] (the reference's layout "a"); the engine keeps Y
+as its half set, transposed (`Yh_dev[e][i]`, atoms fastest), and expands the
+reference-layout `state.Y` only when it is read.  The `layout` / `batch_u` /
+`batch_y` / `tile_v` knobs are accepted for signature parity (the reference
+guarantees they never change results, mdkk/snap/compute.py:238-276) and do
+not change the GPU schedule.
 """
 
 from __future__ import annotations
@@ -18,7 +20,7 @@ import torch
 
 from .. import _lib
 from ..memspace import DualArray, LayoutPolicy
-from .coupling import CouplingTables, adjoint_rows
+from .coupling import CouplingTables, device_product_list
 
 
 class SnapError(RuntimeError):
@@ -51,17 +53,18 @@ def build_neighbor_map(store, nlist, r_c: float) -> NeighborMap:
 
 
 class _Handle:
-    """Device copy of the adjoint contribution table (mdkk_snap_create)."""
+    """Device copy of the Z-list product table (mdkk_snap_create)."""
 
     def __init__(self, tables: CouplingTables, beta: np.ndarray, device):
-        row_f, gh, coef, fmap, n_half = adjoint_rows(tables, beta)
+        coef, code, n_half, fmap = device_product_list(tables, beta)
         out = C.c_void_p()
         with torch.cuda.device(device):
             _lib.check(_lib.lib().mdkk_snap_create(
-                _lib.ctx(device), tables.index.twojmax, len(row_f), row_f.ctypes.data, gh.ctypes.data,
-                coef.ctypes.data, n_half, fmap.ctypes.data, C.byref(out)), "mdkk_snap_create")
+                _lib.ctx(device), tables.index.twojmax, len(coef), coef.ctypes.data, code.ctypes.data,
+                n_half, fmap.ctypes.data, C.byref(out)), "mdkk_snap_create")
         self.ptr = out.value
-        self.n_contrib = int((coef != 0).sum())
+        self.n_half = n_half
+        self.n_products = int((coef != 0).sum())
 
     def __del__(self):
         try:
@@ -92,6 +95,11 @@ class SnapState:
         rm = LayoutPolicy.row_major(2)   # device rows are atoms: one warp streams one atom's 285 entries
         self.U_dev = torch.zeros(shape, dtype=torch.complex128, device=self.device)
         self.Y_dev = torch.zeros_like(self.U_dev)
+        n_half = sum((t + 1) ** 2 // 2 if t & 1 else (t // 2) * (t + 1) + t // 2 + 1
+                     for t in range(self.index.twojmax + 1))
+        self.ld = max(32, (self.n_atoms + 31) // 32 * 32)
+        self.Yh_dev = torch.zeros((n_half, self.ld), dtype=torch.complex128, device=self.device)
+        self._y_expanded = True   # Y_dev agrees with Yh_dev
         self.U = DualArray(shape, layout_b=rm, dtype=np.complex128, device=self.device, storage_b=self.U_dev)
         self.Y = DualArray(shape, layout_b=rm, dtype=np.complex128, device=self.device, storage_b=self.Y_dev)
         self.energy_dev = torch.zeros(1, dtype=torch.float64, device=self.device)
@@ -107,7 +115,27 @@ class SnapState:
         return self.U.read("a")[: self.n_atoms]
 
     def y_view(self) -> np.ndarray:
+        self.expand_y()
         return self.Y.read("a")[: self.n_atoms]
+
+    def expand_y(self) -> None:
+        """Reference layout Y (n, n_flat) from the engine's half/transposed Yh (after compute_yi)."""
+        if self._y_expanded:
+            return
+        _lib.check(_lib.lib().mdkk_snap_y_expand(self.handle().ptr, self.Yh_dev.data_ptr(), self.ld, self.n_atoms,
+                                                 self.Y_dev.data_ptr(), _lib.stream(self.device)),
+                   "mdkk_snap_y_expand")
+        self.Y.modified_a = False
+        self.Y.mark_modified("b")
+        self._y_expanded = True
+
+    def sync_yh(self) -> None:
+        """Engine Yh current: a host-written reference-layout Y is compressed into it."""
+        if self.Y.modified_a:
+            self.Y.sync("b")
+            _lib.check(_lib.lib().mdkk_snap_y_compress(self.handle().ptr, self.Y_dev.data_ptr(), self.n_atoms,
+                                                       self.Yh_dev.data_ptr(), self.ld, _lib.stream(self.device)),
+                       "mdkk_snap_y_compress")
 
 
 def compute_ui(nmap: NeighborMap, state: SnapState) -> None:
@@ -131,10 +159,11 @@ def compute_yi(state: SnapState) -> None:
     """Full three-slot adjoint Y and the per-atom energy sum (mdkk/snap/compute.py:303-340, :376-387)."""
     state.U.sync("b")
     _lib.check(_lib.lib().mdkk_snap_yi(_lib.ctx(state.device), state.handle().ptr, state.U_dev.data_ptr(),
-                                       state.n_atoms, state.Y_dev.data_ptr(), state.energy_dev.data_ptr(),
-                                       _lib.stream(state.device)), "mdkk_snap_yi")
+                                       state.n_atoms, state.Yh_dev.data_ptr(), state.ld,
+                                       state.energy_dev.data_ptr(), _lib.stream(state.device)), "mdkk_snap_yi")
     state.Y.modified_a = False
-    state.Y.mark_modified("b")
+    state.Y.modified_b = False
+    state._y_expanded = False
 
 
 def energy_from_y(state: SnapState) -> float:
@@ -150,10 +179,10 @@ def compute_energy(state: SnapState) -> float:
 def deidrj_device(nmap: NeighborMap, state: SnapState, f: torch.Tensor) -> None:
     """Launch the fused force kernel, accumulating into device rows f (n_total, 4) (must be zeroed)."""
     st, nl = nmap.store, nmap.nlist
-    state.Y.sync("b")
+    state.sync_yh()
     _lib.check(_lib.lib().mdkk_snap_deidrj(state.handle().ptr, st.x.data_ptr(), st.n_local, nl.table_dev.data_ptr(),
                                            nl.counts_dev.data_ptr(), nl.alloc_cap, nmap.r_c,
-                                           state.Y_dev.data_ptr(), f.data_ptr(), _lib.stream(st.device)),
+                                           state.Yh_dev.data_ptr(), state.ld, f.data_ptr(), _lib.stream(st.device)),
                "mdkk_snap_deidrj")
 
 

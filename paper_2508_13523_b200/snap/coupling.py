@@ -4,8 +4,8 @@ Mirror of mdkk/snap/indexing.py:24-68 and mdkk/snap/coupling.py:28-137:
 doubled-integer angular momenta, flat (tj, p, q) index with tj slowest,
 coupled triples (tj, tj1, tj2) with tj2 <= tj1 <= tj, exact-rational CG with a
 single final rounding, and per-triple (iz, iu1, iu2, coeff) term lists.  The
-device consumes an output-sorted "contribution" list for the full three-slot
-adjoint (mdkk/snap/compute.py:303-340) built by `adjoint_contributions`.
+device consumes an output-sorted product list for the half-block adjoint (the
+Z-list form of mdkk/snap/compute.py:303-340) built by `zlist_entries`.
 """
 
 from __future__ import annotations
@@ -194,29 +194,131 @@ def half_block_outputs(twojmax: int):
     return np.array(keep, dtype=np.int32), np.array(fmap, dtype=np.int32)
 
 
-def adjoint_rows(tables: CouplingTables, beta, width: int = 32):
-    """Device table for the half-block adjoint: rows of `width` contributions sharing one output.
+def _half_index(twojmax: int):
+    """(tj, p, q) -> (half-set index, mirrored?, odd sign?) with X[m] = (-1)^(p+q) conj(X[half])."""
+    off, hidx = 0, {}
+    for tj in range(twojmax + 1):
+        hs = (tj + 1) * (tj + 1) // 2 if tj & 1 else (tj // 2) * (tj + 1) + tj // 2 + 1
+        for h in range(hs):
+            hidx[(tj, h // (tj + 1), h % (tj + 1))] = off + h
+        off += hs
+    out = {}
+    for tj in range(twojmax + 1):
+        for p in range(tj + 1):
+            for q in range(tj + 1):
+                if (tj, p, q) in hidx:
+                    out[(tj, p, q)] = (hidx[(tj, p, q)], 0, 0)
+                else:
+                    out[(tj, p, q)] = (hidx[(tj, tj - p, tj - q)], 1, (p + q) & 1)
+    return out, off
 
-    Returns (row_f, gh, coef, fmap): row_f[r] is the half-block index of row r's
-    output, gh packs g | h << 12 | conj << 24, coef is zero on padding entries,
-    and fmap maps every flat index to (half index | mirrored << 16 | odd-sign << 17).
-    Contributions inside an output are sorted by (g, h) so a warp's 32 lanes read
-    neighbouring U entries.
+
+def zlist_entries(tables: CouplingTables, beta):
+    """Half-block Y as a list of U*U products (the Z-list form of the adjoint).
+
+    Y_tj = sum over every coupled (tj1 >= tj2, tj) of beta' * Z_{tj1,tj2->tj}
+    with Z[P,Q] = sum cg[p1,p2] cg[q1,q2] U_tj1[p1,q1] U_tj2[p2,q2] and beta'
+    the triple's beta scaled by the multiplicity / dimension ratio of the
+    coupling symmetry B_{j1 j2 j} = (j+1)/(j1+1) B_{j j2 j1} (for tj >= tj1:
+    x2 or x3 when indices coincide; otherwise (tj1+1)/(tj+1)).  This equals
+    the reference's three-slot adjoint (mdkk/snap/compute.py:303-340)
+    element-wise (checked against it to ~1e-15 relative in tests), with U*U
+    products only.  Operands outside the half set are mirrored,
+    U[m] = (-1)^(p+q) conj(U[half]); the sign folds into the coefficient.
+
+    Returns (f, g, h, conj_g, conj_h, coef), sorted by output f (half index),
+    with identical keys merged and every output present at least once.
     """
-    f_start, g, h, cj, coef = adjoint_contributions(tables, beta)
-    keep, fmap = half_block_outputs(tables.index.twojmax)
-    row_f, gh, cf = [], [], []
-    for k, f in enumerate(keep):
-        a, b = int(f_start[f]), int(f_start[f + 1])
-        o = np.lexsort((h[a:b], g[a:b])) + a
-        n = b - a
-        pad = (-n) % width
-        if n == 0:
-            continue
-        gh.append(np.concatenate([g[o] | (h[o] << 12) | (cj[o] << 24), np.zeros(pad, np.int32)]))
-        cf.append(np.concatenate([coef[o], np.zeros(pad)]))
-        row_f.extend([k] * ((n + pad) // width))
-    if not row_f:
-        return (np.zeros(0, np.int32), np.zeros(0, np.int32), np.zeros(0), fmap, len(keep))
-    return (np.array(row_f, dtype=np.int32), np.concatenate(gh).astype(np.int32), np.concatenate(cf),
-            fmap, len(keep))
+    beta = np.asarray(beta, dtype=np.float64)
+    twojmax = tables.index.twojmax
+    hmap, n_half = _half_index(twojmax)
+    bidx = {t: i for i, t in enumerate(tables.triples)}
+    acc: dict = {}
+    for tj1 in range(twojmax + 1):
+        for tj2 in range(tj1 + 1):
+            for tj in range(tj1 - tj2, min(twojmax, tj1 + tj2) + 1, 2):
+                if tj >= tj1:
+                    b = beta[bidx[(tj, tj1, tj2)]]
+                    fac = (3.0 if tj2 == tj else 2.0) if tj1 == tj else 1.0
+                elif tj >= tj2:
+                    b = beta[bidx[(tj1, tj, tj2)]]
+                    fac = (2.0 if tj2 == tj else 1.0) * (tj1 + 1) / (tj + 1)
+                else:
+                    b = beta[bidx[(tj1, tj2, tj)]]
+                    fac = (tj1 + 1) / (tj + 1)
+                if b == 0.0:
+                    continue
+                bf = b * fac
+                sh = (tj1 + tj2 - tj) // 2
+                cg = np.zeros((tj1 + 1, tj2 + 1))
+                for p1 in range(tj1 + 1):
+                    for p2 in range(tj2 + 1):
+                        tm = (2 * p1 - tj1) + (2 * p2 - tj2)
+                        if abs(tm) <= tj:
+                            cg[p1, p2] = clebsch_gordan(tj1, 2 * p1 - tj1, tj2, 2 * p2 - tj2, tj, tm)
+                for (t_, P, Q), (fo, mir, _) in hmap.items():
+                    if t_ != tj or mir:
+                        continue
+                    for p1 in range(tj1 + 1):
+                        p2 = P - p1 + sh
+                        if p2 < 0 or p2 > tj2 or cg[p1, p2] == 0.0:
+                            continue
+                        for q1 in range(tj1 + 1):
+                            q2 = Q - q1 + sh
+                            if q2 < 0 or q2 > tj2 or cg[q1, q2] == 0.0:
+                                continue
+                            g, cgj, sg = hmap[(tj1, p1, q1)]
+                            h, chj, shh = hmap[(tj2, p2, q2)]
+                            c = bf * cg[p1, p2] * cg[q1, q2] * (-1.0 if sg ^ shh else 1.0)
+                            a, d = (g, cgj), (h, chj)
+                            if d < a:
+                                a, d = d, a
+                            key = (fo, a[0], d[0], a[1], d[1])
+                            acc[key] = acc.get(key, 0.0) + c
+    present = {k[0] for k in acc}
+    for fo in range(n_half):
+        if fo not in present:
+            acc[(fo, 0, 0, 0, 0)] = 0.0
+    keys = sorted(acc)
+    arr = np.array(keys, dtype=np.int64).reshape(-1, 5)
+    coef = np.array([acc[k] for k in keys], dtype=np.float64)
+    return arr[:, 0], arr[:, 1], arr[:, 2], arr[:, 3], arr[:, 4], coef
+
+
+def zlist_apply(U: np.ndarray, twojmax: int, entries) -> np.ndarray:
+    """Host emulation of the device yi on full U rows -> full Y rows (test helper for the table)."""
+    f, g, h, cg_, ch_, coef = entries
+    hmap, n_half = _half_index(twojmax)
+    off = QuantumIndex(twojmax / 2.0).block_offset
+    half_flat = np.zeros(n_half, dtype=np.int64)
+    for (tj, p, q), (k, mir, _) in hmap.items():
+        if not mir:
+            half_flat[k] = off[tj] + p * (tj + 1) + q
+    Uh = U[:, half_flat]
+    ug = np.where(cg_ == 1, np.conj(Uh[:, g]), Uh[:, g])
+    uh = np.where(ch_ == 1, np.conj(Uh[:, h]), Uh[:, h])
+    Yh = np.zeros((len(U), n_half), complex)
+    np.add.at(Yh.T, f, (coef * ug * uh).T)
+    Y = np.zeros_like(U)
+    for (tj, p, q), (k, mir, odd) in hmap.items():
+        v = Yh[:, k]
+        if mir:
+            v = np.conj(v) * (-1.0 if odd else 1.0)
+        Y[:, off[tj] + p * (tj + 1) + q] = v
+    return Y
+
+
+def device_product_list(tables: CouplingTables, beta):
+    """Packed (coef, code, n_half, fmap) for mdkk_snap_create (include/mdkk_b200.h)."""
+    f, g, h, cg_, ch_, coef = zlist_entries(tables, beta)
+    hmap, n_half = _half_index(tables.index.twojmax)
+    center = np.zeros(n_half, dtype=np.int64)
+    for (tj, p, q), (k, mir, _) in hmap.items():
+        if not mir and (tj - p, tj - q) == (p, q):
+            center[k] = 1
+    last = np.ones(len(f), dtype=np.int64)
+    last[:-1] = f[1:] != f[:-1]
+    code = g | (h << 8) | (f << 16) | (cg_ << 24) | (ch_ << 25) | (last << 26) | (center[f] << 27)
+    _, fmap = half_block_outputs(tables.index.twojmax)
+    return (np.ascontiguousarray(coef, dtype=np.float64), np.ascontiguousarray(code, dtype=np.int32), n_half,
+            np.ascontiguousarray(fmap, dtype=np.int32))
