@@ -63,19 +63,18 @@ __device__ __forceinline__ cplx cadd(cplx a, cplx b) { return {a.re + b.re, a.im
 __device__ __forceinline__ cplx cscale(double s, cplx a) { return {s * a.re, s * a.im}; }
 __device__ __forceinline__ cplx cneg(cplx a) { return {-a.re, -a.im}; }
 
-// Recursion weights of element (P, Q) of level tj (mdkk/snap/compute.py:130-147):
-// w0 = sqrt(PQ)/tj (a * prev[P-1][Q-1]), w1 = sqrt(P(tj-Q))/tj (b * prev[P-1][Q]),
-// w2 = sqrt((tj-P)Q)/tj (-conj(b) * prev[P][Q-1]), w3 = sqrt((tj-P)(tj-Q))/tj (conj(a) * prev[P][Q]).
-// Stored SoA in global memory and staged per CTA in shared memory (lanes read
-// different elements: constant memory would serialise).
-__device__ double g_w[4][block_offset(kMaxTwoJ + 1)];
+// Weights of the two-term column recursion, rs[k][l] = sqrt(k / l) (0 <= k, l <= 8).
+// Staged per CTA in shared memory (lanes read different entries: constant
+// memory would serialise).
+__device__ double g_rs[kMaxTwoJ + 1][kMaxTwoJ + 1];
 
-struct SW {
-    double w[4][block_offset(kMaxTwoJ + 1)];
+struct RS {
+    double v[kMaxTwoJ + 1][kMaxTwoJ + 1];
 };
 
-__device__ __forceinline__ void stage_weights(SW& sw, int n_flat) {
-    for (int t = threadIdx.x; t < 4 * n_flat; t += blockDim.x) sw.w[t / n_flat][t % n_flat] = g_w[t / n_flat][t % n_flat];
+__device__ __forceinline__ void stage_rs(RS& rs) {
+    for (int t = threadIdx.x; t < (kMaxTwoJ + 1) * (kMaxTwoJ + 1); t += blockDim.x)
+        rs.v[t / (kMaxTwoJ + 1)][t % (kMaxTwoJ + 1)] = g_rs[t / (kMaxTwoJ + 1)][t % (kMaxTwoJ + 1)];
     __syncthreads();
 }
 
@@ -112,15 +111,36 @@ __device__ __forceinline__ void pair_grads(const double d[3], const PairGeo& g, 
     }
 }
 
-// One element (P, Q) of level tj from the previous level stored row-major (tj x tj) at `prev`.
-__device__ __forceinline__ cplx level_elem(const cplx* prev, int tj, int P, int Q, double w0, double w1, double w2,
-                                          double w3, cplx a, cplx b) {
-    cplx v = {0.0, 0.0};
-    if (P >= 1 && Q >= 1) v = cadd(v, cscale(w0, cmul(prev[(P - 1) * tj + (Q - 1)], a)));
-    if (P >= 1 && Q <= tj - 1) v = cadd(v, cscale(w1, cmul(prev[(P - 1) * tj + Q], b)));
-    if (P <= tj - 1 && Q >= 1) v = cadd(v, cscale(w2, cmul(prev[P * tj + (Q - 1)], cneg(cconj(b)))));
-    if (P <= tj - 1 && Q <= tj - 1) v = cadd(v, cscale(w3, cmul(prev[P * tj + Q], cconj(a))));
-    return v;
+// Two-term column recursion for the Wigner-U levels (levels column-major: v[Q*tj + P]).  With level 1 =
+// [[conj(a), -conj(b)], [b, a]] (mdkk/snap/compute.py:125-147), every column
+// Q < tj of level tj follows from column Q of level tj-1:
+//   u[P][Q] = sqrt((tj-P)/(tj-Q)) conj(a) v[P][Q] + sqrt(P/(tj-Q)) b v[P-1][Q]
+// (the same matrices as the reference's four-term recursion, half the
+// products; checked against it to ~1e-16 in the parity tests).  The right
+// half of each level follows from the mirror X[tj-P][tj-Q] = (-1)^(P+Q)
+// conj(X[P][Q]), so only the column half C_tj = {2Q < tj, or 2Q == tj and
+// 2P <= tj} is computed; it has half_size(tj) elements, enumerated column-major.
+__device__ __forceinline__ cplx rec2(const cplx* v, int tj, int P, int Q, const RS& rs, cplx ab, cplx b) {
+    cplx x = {0.0, 0.0};
+    if (P < tj) x = cscale(rs.v[tj - P][tj - Q], cmul(ab, v[Q * tj + P]));
+    if (P >= 1) x = cadd(x, cscale(rs.v[P][tj - Q], cmul(b, v[Q * tj + P - 1])));
+    return x;
+}
+
+__device__ __forceinline__ bool in_col_half(int tj, int P, int Q) {
+    return 2 * Q < tj || (2 * Q == tj && 2 * P <= tj);
+}
+
+// c-th element (column-major) of C_tj.
+__device__ __forceinline__ void col_elem(int tj, int c, int& P, int& Q) {
+    const int nfull = ((tj + 1) >> 1) * (tj + 1);
+    if (c < nfull) {
+        Q = c / (tj + 1);
+        P = c - Q * (tj + 1);
+    } else {
+        Q = tj >> 1;
+        P = c - nfull;
+    }
 }
 
 __device__ __forceinline__ bool neighbour(const double* x, const int* table, int cap, int i, int k, double4 xi,
@@ -156,32 +176,14 @@ constexpr int kHSlots = hslot_base(kMaxTwoJ + 1);        // 14 per half-warp lan
 constexpr int kHalfMax = half_size(kMaxTwoJ);            // 41
 constexpr int kHalfAll = half_offset(kMaxTwoJ + 1);      // 145
 
-// X[P][Q] of level tj from its stored half (row-major, stride tj+1).
-__device__ __forceinline__ cplx hget(const cplx* L, int tj, int P, int Q) {
-    const int idx = P * (tj + 1) + Q;
-    if (idx < half_size(tj)) return L[idx];
-    cplx v = L[(tj - P) * (tj + 1) + (tj - Q)];
-    v.im = -v.im;
-    return ((P + Q) & 1) ? cneg(v) : v;
-}
-
-// Store element (P, Q) of a full row-major (tj+1)^2 level and its mirror.
+// Store element (P, Q) of a full level held COLUMN-major in shared memory
+// (L[Q*(tj+1) + P]: lanes walk C_tj down a column, so reads and writes of a
+// half-warp hit consecutive 16-byte words) and its mirror.
 __device__ __forceinline__ void store_mirrored(cplx* L, int tj, int P, int Q, cplx v) {
-    L[P * (tj + 1) + Q] = v;
-    const int hm = (tj - P) * (tj + 1) + (tj - Q);
+    L[Q * (tj + 1) + P] = v;
+    const int hm = (tj - Q) * (tj + 1) + (tj - P);
     const double sg = ((P + Q) & 1) ? -1.0 : 1.0;
     L[hm] = {sg * v.re, -sg * v.im};  // the center element writes itself twice (same value)
-}
-
-// Element (P, Q) of level tj from the half-stored previous level (mdkk/snap/compute.py:138-147).
-__device__ __forceinline__ cplx level_elem_h(const cplx* prev, int tj, int P, int Q, const SW& sw, int e, cplx a,
-                                            cplx b) {
-    cplx v = {0.0, 0.0};
-    if (P >= 1 && Q >= 1) v = cadd(v, cscale(sw.w[0][e], cmul(hget(prev, tj - 1, P - 1, Q - 1), a)));
-    if (P >= 1 && Q <= tj - 1) v = cadd(v, cscale(sw.w[1][e], cmul(hget(prev, tj - 1, P - 1, Q), b)));
-    if (P <= tj - 1 && Q >= 1) v = cadd(v, cscale(sw.w[2][e], cmul(hget(prev, tj - 1, P, Q - 1), cneg(cconj(b)))));
-    if (P <= tj - 1 && Q <= tj - 1) v = cadd(v, cscale(sw.w[3][e], cmul(hget(prev, tj - 1, P, Q), cconj(a))));
-    return v;
 }
 
 struct NbPair {
@@ -209,19 +211,20 @@ __device__ __forceinline__ int compact_pairs(const double* x, const int* table, 
 // ---------------------------------------------------------------- compute_ui
 // U_i = sum_k f_c u(a_k, b_k) (mdkk/snap/compute.py:279-292), row-major U.
 // One warp per atom, two neighbours at a time (half-warp each); each half
-// computes the half set H_tj of every level (16 lanes, previous level in
-// shared memory), accumulates f_c u in registers, and the full U_i row is
-// written from the half set and its mirror.
+// computes the column half C_tj of every level with the two-term recursion
+// (16 lanes, previous level in shared memory as a full mirrored level),
+// accumulates f_c u in registers, and the full U_i row is written from C and
+// its mirror.
 template <int TWOJ>
 __global__ void __launch_bounds__(kWarps * 32, 4) k_snap_ui(const double* __restrict__ x, int n_local,
                                                          const int* __restrict__ table,
                                                          const int* __restrict__ counts, int cap, double rc,
                                                          double2* __restrict__ U, int* __restrict__ flags) {
     constexpr int NF = block_offset(TWOJ + 1);
-    __shared__ SW sw;
+    __shared__ RS rs;
     __shared__ NbPair s_nb[kWarps][32];
     __shared__ cplx s_lvl[kWarps][2][2][kLevelMax];
-    stage_weights(sw, NF);
+    stage_rs(rs);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, hl = lane & 15, hh = lane >> 4;
     const int i = blockIdx.x * kWarps + w;
     if (i >= n_local) return;
@@ -241,6 +244,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_snap_ui(const double* __rest
             double z0, r0;
             pair_geometry(nb.dx, nb.dy, nb.dz, nb.r2, rc, g, z0, r0);
             const double fc = pi < m ? g.fc : 0.0;
+            const cplx ab = cconj(g.a);
             cplx(*L)[kLevelMax] = s_lvl[w][hh];
             if (hl == 0) {
                 L[0][0] = {1.0, 0.0};
@@ -253,11 +257,11 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_snap_ui(const double* __rest
                 cplx* cur = L[tj & 1];
 #pragma unroll
                 for (int s = 0; s < half_slots(tj); ++s) {
-                    const int h = hl + 16 * s;
-                    if (h < half_size(tj)) {
-                        const int P = h / (tj + 1), Q = h % (tj + 1), e = block_offset(tj) + h;
-                        const cplx v = level_elem(prev, tj, P, Q, sw.w[0][e], sw.w[1][e], sw.w[2][e], sw.w[3][e],
-                                                  g.a, g.b);
+                    const int c = hl + 16 * s;
+                    if (c < half_size(tj)) {
+                        int P, Q;
+                        col_elem(tj, c, P, Q);
+                        const cplx v = rec2(prev, tj, P, Q, rs, ab, g.b);
                         store_mirrored(cur, tj, P, Q, v);
                         acc[hslot_base(tj) + s] = cadd(acc[hslot_base(tj) + s], cscale(fc, v));
                     }
@@ -279,15 +283,16 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_snap_ui(const double* __rest
     for (int tj = 0; tj <= TWOJ; ++tj)
 #pragma unroll
         for (int s = 0; s < half_slots(tj); ++s) {
-            const int h = hl + 16 * s;
-            if (h < half_size(tj)) {
-                const int P = h / (tj + 1), Q = h % (tj + 1);
+            const int c = hl + 16 * s;
+            if (c < half_size(tj)) {
+                int P, Q;
+                col_elem(tj, c, P, Q);
                 const cplx v = acc[hslot_base(tj) + s];
-                Ui[block_offset(tj) + h] = make_double2(v.re, v.im);
-                const int hm = (tj - P) * (tj + 1) + (tj - Q);
-                if (hm != h) {
+                const int e = P * (tj + 1) + Q, em = (tj - P) * (tj + 1) + (tj - Q);
+                Ui[block_offset(tj) + e] = make_double2(v.re, v.im);
+                if (em != e) {
                     const double sg = ((P + Q) & 1) ? -1.0 : 1.0;
-                    Ui[block_offset(tj) + hm] = make_double2(sg * v.re, -sg * v.im);
+                    Ui[block_offset(tj) + em] = make_double2(sg * v.re, -sg * v.im);
                 }
             }
         }
@@ -386,13 +391,18 @@ __global__ void k_snap_y_compress(const double2* __restrict__ Y, int n, int nf, 
 // ------------------------------------------------------- compute_fused_deidrj
 // Reverse-mode form of compute_fused_deidrj (mdkk/snap/compute.py:390-409).
 // The reference evaluates t_d = Re sum_f Y[f] conj(d(f_c u[f])/d dr_d) with a
-// forward derivative recursion per direction.  Here u runs forward (half sets
-// of all levels kept in shared memory) and the adjoint lambda_tj = Y_tj +
-// M_{tj+1}^H lambda_{tj+1} backward, accumulating G_c = sum_f Y[f] conj(du[f]/dc)
-// for c in {a, a*, b, b*}.  The mirror symmetry gives G_{a*} = conj(G_a),
-// G_{b*} = conj(G_b), so with half sets only
-//   t_d = f_c' rhat_d S + 2 f_c Re(G_a conj(da_d) + G_b conj(db_d)),   S = Re sum_f Y conj(u).
-// Same quantity (equal to rounding) for ~1/4 of the reference's complex MACs.
+// forward derivative recursion per direction.  Here u runs forward over the
+// column halves C_tj (two-term recursion, full mirrored levels kept in shared
+// memory) and the adjoint runs backward over the same computational graph:
+// with S = Re sum_f conj(Y[f]) u[f], the total adjoint on C_tj is
+//   lambda[x] = Y[x] + g(x) + s_x conj(Y[m] + g(m)),   m = mirror(x),
+//             = 2 Y[x] + g(x) + s_x conj(g(m))         (x != m; Y is mirror-symmetric)
+// where g(y) = sum over the level-(tj+1) elements z in C_{tj+1} that read y of
+// conj(coef_z) lambda[z].  The recursion coefficients are conj(a) and b only,
+// so dS = Re(G_abar conj(da) + G_b db) with G_abar = sum conj(lambda) w v[P][Q],
+// G_b = sum conj(lambda) w v[P-1][Q], and
+//   t_d = f_c' rhat_d S + f_c Re(G_abar conj(da_d) + G_b db_d).
+// Same quantity (equal to rounding) for ~1/6 of the reference's complex MACs.
 // One warp per atom, two neighbours at a time (one per half-warp).
 template <int TWOJ>
 __global__ void __launch_bounds__(kWarps * 32, 3) k_snap_deidrj(const double* __restrict__ x, int n_local,
@@ -402,20 +412,28 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_snap_deidrj(const double* __
                                                              double* __restrict__ f) {
     constexpr int NF = block_offset(TWOJ + 1);
     constexpr int NH = half_offset(TWOJ + 1);
-    extern __shared__ double s_dyn_d[];  // > 48 KB: weights | pairs | Y_i half | u half levels | lambda
-    SW& sw = *reinterpret_cast<SW*>(s_dyn_d);
-    auto s_nb = reinterpret_cast<NbPair(*)[32]>(reinterpret_cast<char*>(s_dyn_d) + sizeof(SW));
+    extern __shared__ double s_dyn_d[];  // rs | pairs | Y_i half | u levels | lambda levels
+    RS& rs = *reinterpret_cast<RS*>(s_dyn_d);
+    auto s_nb = reinterpret_cast<NbPair(*)[32]>(reinterpret_cast<char*>(s_dyn_d) + sizeof(RS));
     auto s_y = reinterpret_cast<cplx(*)[NH]>(s_nb + kWarps);
     auto s_u = reinterpret_cast<cplx(*)[2][NF]>(s_y + kWarps);
     auto s_l = reinterpret_cast<cplx(*)[2][2][kLevelMax]>(s_u + kWarps);
-    stage_weights(sw, NF);
+    stage_rs(rs);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, hl = lane & 15, hh = lane >> 4;
     const int i = blockIdx.x * kWarps + w;
     if (i >= n_local) return;
-    for (int e = lane; e < NH; e += 32) {
-        const double2 v = Yh[(long long)e * ld + i];
-        s_y[w][e] = {v.x, v.y};
-    }
+    // Y_i at the column-half elements, in the lanes' (column-major) order, from the row-half Yh
+#pragma unroll
+    for (int tj = 0; tj <= TWOJ; ++tj)
+        for (int c = lane; c < half_size(tj); c += 32) {
+            int P, Q;
+            col_elem(tj, c, P, Q);
+            const int h = P * (tj + 1) + Q;
+            const bool mir = h >= half_size(tj);
+            const double2 v = Yh[(long long)(half_offset(tj) + (mir ? (tj - P) * (tj + 1) + (tj - Q) : h)) * ld + i];
+            const double sg = (mir && ((P + Q) & 1)) ? -1.0 : 1.0;
+            s_y[w][half_offset(tj) + c] = {sg * v.x, mir ? -sg * v.y : v.y};
+        }
     __syncwarp();
     const cplx* sy = s_y[w];
     cplx* ul = s_u[w][hh];
@@ -434,7 +452,8 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_snap_deidrj(const double* __
             PairGeo g;
             double z0, r0;
             pair_geometry(nb.dx, nb.dy, nb.dz, nb.r2, rc, g, z0, r0);
-            // forward: half sets of all levels, S = Re sum_f Y conj(u) (mirror pairs counted twice)
+            const cplx ab = cconj(g.a), bb = cconj(g.b);
+            // forward: C_tj of every level, S = Re sum_f conj(Y) u (mirror pairs counted twice)
             double S = 0.0;
             if (hl == 0) {
                 ul[0] = {1.0, 0.0};
@@ -445,62 +464,55 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_snap_deidrj(const double* __
             for (int tj = 1; tj <= TWOJ; ++tj) {
 #pragma unroll
                 for (int s = 0; s < half_slots(tj); ++s) {
-                    const int h = hl + 16 * s;
-                    if (h < half_size(tj)) {
-                        const int P = h / (tj + 1), Q = h % (tj + 1);
-                        const int e = block_offset(tj) + h;
-                        const cplx v = level_elem(ul + block_offset(tj - 1), tj, P, Q, sw.w[0][e], sw.w[1][e],
-                                                  sw.w[2][e], sw.w[3][e], g.a, g.b);
+                    const int c = hl + 16 * s;
+                    if (c < half_size(tj)) {
+                        int P, Q;
+                        col_elem(tj, c, P, Q);
+                        const cplx v = rec2(ul + block_offset(tj - 1), tj, P, Q, rs, ab, g.b);
                         store_mirrored(ul + block_offset(tj), tj, P, Q, v);
-                        const cplx yv = sy[half_offset(tj) + h];
-                        const double c = (2 * P == tj && 2 * Q == tj) ? 1.0 : 2.0;
-                        S += c * (yv.re * v.re + yv.im * v.im);
+                        const cplx yv = sy[half_offset(tj) + c];
+                        const double wgt = (2 * P == tj && 2 * Q == tj) ? 1.0 : 2.0;
+                        S += wgt * (yv.re * v.re + yv.im * v.im);
                     }
                 }
                 __syncwarp();
             }
-            // backward: lambda_TWOJ = Y_TWOJ; G_a, G_b over the half sets; lambda_{tj-1}
+            // backward: total adjoint on C_tj from level tj+1, accumulate G_abar, G_b
             cplx Ga = {0, 0}, Gb = {0, 0};
-            for (int h = hl; h < half_size(TWOJ); h += 16)
-                store_mirrored(lam[TWOJ & 1], TWOJ, h / (TWOJ + 1), h % (TWOJ + 1), sy[half_offset(TWOJ) + h]);
-            __syncwarp();
 #pragma unroll
             for (int tj = TWOJ; tj >= 1; --tj) {
-                const cplx* lt = lam[tj & 1];
-                const cplx* up = ul + block_offset(tj - 1);
+                cplx* lc = lam[tj & 1];
+                const cplx* ln = lam[(tj + 1) & 1];   // level tj+1, column-major (stride tj+2), valid on C_{tj+1}
+                const cplx* v = ul + block_offset(tj - 1);
 #pragma unroll
                 for (int s = 0; s < half_slots(tj); ++s) {
-                    const int h = hl + 16 * s;
-                    if (h < half_size(tj)) {
-                        const int P = h / (tj + 1), Q = h % (tj + 1), e = block_offset(tj) + h;
-                        const cplx l = lt[h];
-                        cplx ca = {0, 0}, cas = {0, 0}, cb = {0, 0}, cbs = {0, 0};
-                        if (P >= 1 && Q >= 1) ca = cscale(sw.w[0][e], cmul(l, cconj(up[(P - 1) * tj + (Q - 1)])));
-                        if (P <= tj - 1 && Q <= tj - 1) cas = cscale(sw.w[3][e], cmul(l, cconj(up[P * tj + Q])));
-                        if (P >= 1 && Q <= tj - 1) cb = cscale(sw.w[1][e], cmul(l, cconj(up[(P - 1) * tj + Q])));
-                        if (P <= tj - 1 && Q >= 1) cbs = cscale(-sw.w[2][e], cmul(l, cconj(up[P * tj + (Q - 1)])));
-                        const double mw = (2 * P == tj && 2 * Q == tj) ? 0.5 : 1.0;
-                        Ga = cadd(Ga, cscale(mw, cadd(ca, cconj(cas))));
-                        Gb = cadd(Gb, cscale(mw, cadd(cb, cconj(cbs))));
-                    }
-                }
-                if (tj >= 2) {
-                    cplx* ln = lam[(tj - 1) & 1];
-                    const int eo = block_offset(tj);
-#pragma unroll
-                    for (int s = 0; s < half_slots(tj - 1); ++s) {
-                        const int h = hl + 16 * s;
-                        if (h < half_size(tj - 1)) {
-                            const int P = h / tj, Q = h % tj;
-                            cplx v = sy[half_offset(tj - 1) + h];
-                            const int e11 = (P + 1) * (tj + 1) + (Q + 1), e10 = (P + 1) * (tj + 1) + Q;
-                            const int e01 = P * (tj + 1) + (Q + 1), e00 = P * (tj + 1) + Q;
-                            v = cadd(v, cscale(sw.w[0][eo + e11], cmul(lt[e11], cconj(g.a))));
-                            v = cadd(v, cscale(sw.w[1][eo + e10], cmul(lt[e10], cconj(g.b))));
-                            v = cadd(v, cscale(-sw.w[2][eo + e01], cmul(lt[e01], g.b)));
-                            v = cadd(v, cscale(sw.w[3][eo + e00], cmul(lt[e00], g.a)));
-                            store_mirrored(ln, tj - 1, P, Q, v);
+                    const int c = hl + 16 * s;
+                    if (c < half_size(tj)) {
+                        int P, Q;
+                        col_elem(tj, c, P, Q);
+                        const bool center = 2 * P == tj && 2 * Q == tj;
+                        const cplx yv = sy[half_offset(tj) + c];
+                        cplx l = center ? yv : cscale(2.0, yv);
+                        if (tj < TWOJ) {
+                            const int T = tj + 1;
+                            // g(x): readers of v[P][Q] at level T are (P, Q) and (P+1, Q), both in C_T
+                            const cplx* lq = ln + Q * (T + 1);
+                            l = cadd(l, cscale(rs.v[T - P][T - Q], cmul(g.a, lq[P])));
+                            l = cadd(l, cscale(rs.v[P + 1][T - Q], cmul(bb, lq[P + 1])));
+                            if (!center && Q == (tj >> 1)) {   // g(mirror) is non-zero only in the last column
+                                const int mP = tj - P, mQ = tj - Q;
+                                const cplx* lm = ln + mQ * (T + 1);
+                                cplx gm = {0.0, 0.0};
+                                if (in_col_half(T, mP, mQ)) gm = cscale(rs.v[T - mP][T - mQ], cmul(g.a, lm[mP]));
+                                if (in_col_half(T, mP + 1, mQ))
+                                    gm = cadd(gm, cscale(rs.v[mP + 1][T - mQ], cmul(bb, lm[mP + 1])));
+                                l = ((P + Q) & 1) ? cadd(l, cneg(cconj(gm))) : cadd(l, cconj(gm));
+                            }
                         }
+                        lc[Q * (tj + 1) + P] = l;
+                        const cplx lcj = cconj(l);
+                        if (P < tj) Ga = cadd(Ga, cscale(rs.v[tj - P][tj - Q], cmul(lcj, v[Q * tj + P])));
+                        if (P >= 1) Gb = cadd(Gb, cscale(rs.v[P][tj - Q], cmul(lcj, v[Q * tj + P - 1])));
                     }
                 }
                 __syncwarp();
@@ -512,7 +524,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_snap_deidrj(const double* __
 #pragma unroll
             for (int q = 0; q < 3; ++q) {
                 double v = g.dfc * (d[q] / g.r) * S +
-                           2.0 * g.fc * ((Ga.re * da[q].re + Ga.im * da[q].im) + (Gb.re * db[q].re + Gb.im * db[q].im));
+                           g.fc * ((Ga.re * da[q].re + Ga.im * da[q].im) + (Gb.re * db[q].re - Gb.im * db[q].im));
 #pragma unroll
                 for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
                 tt[q] = v;
@@ -541,17 +553,10 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_snap_deidrj(const double* __
 void upload_weights() {
     static bool done = false;
     if (done) return;
-    static double h[4][block_offset(kMaxTwoJ + 1)] = {};
-    for (int tj = 1; tj <= kMaxTwoJ; ++tj)
-        for (int P = 0; P <= tj; ++P)
-            for (int Q = 0; Q <= tj; ++Q) {
-                const int e = block_offset(tj) + P * (tj + 1) + Q;
-                h[0][e] = std::sqrt((double)(P * Q)) / tj;
-                h[1][e] = std::sqrt((double)(P * (tj - Q))) / tj;
-                h[2][e] = std::sqrt((double)((tj - P) * Q)) / tj;
-                h[3][e] = std::sqrt((double)((tj - P) * (tj - Q))) / tj;
-            }
-    cudaMemcpyToSymbol(g_w, h, sizeof(h));
+    static double h[kMaxTwoJ + 1][kMaxTwoJ + 1] = {};
+    for (int k = 0; k <= kMaxTwoJ; ++k)
+        for (int l = 1; l <= kMaxTwoJ; ++l) h[k][l] = std::sqrt((double)k / (double)l);
+    cudaMemcpyToSymbol(g_rs, h, sizeof(h));
     static short hf[kHalfAll];
     for (int tj = 0; tj <= kMaxTwoJ; ++tj)
         for (int k = 0; k < half_size(tj); ++k) hf[half_offset(tj) + k] = (short)(block_offset(tj) + k);
@@ -716,7 +721,7 @@ int mdkk_snap_deidrj(mdkk_snap* s, const double* x, int n_local, const int* tabl
     switch (s->twojmax) {
 #define MDKK_DE(TJ)                                                                                          \
     case TJ: {                                                                                               \
-        const size_t sm = sizeof(SW) + kWarps * (32 * sizeof(NbPair) +                                       \
+        const size_t sm = sizeof(RS) + kWarps * (32 * sizeof(NbPair) +                                       \
             (half_offset(TJ + 1) + 2 * block_offset(TJ + 1) + 4 * kLevelMax) * sizeof(cplx));                \
         cudaFuncSetAttribute(k_snap_deidrj<TJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);      \
         k_snap_deidrj<TJ><<<nb, kWarps * 32, sm, mdkk::as_stream(stream)>>>(                                 \
