@@ -120,11 +120,14 @@ __device__ __forceinline__ void pair_grads(const double d[3], const PairGeo& g, 
 // half of each level follows from the mirror X[tj-P][tj-Q] = (-1)^(P+Q)
 // conj(X[P][Q]), so only the column half C_tj = {2Q < tj, or 2Q == tj and
 // 2P <= tj} is computed; it has half_size(tj) elements, enumerated column-major.
+// Branch-free at the column ends: the weights vanish there (sqrt(0) for P == tj
+// resp. P == 0) and the out-of-column operand is a finite neighbour (clamped
+// index, buffers zero-initialised), so both terms are always evaluated.
 __device__ __forceinline__ cplx rec2(const cplx* v, int tj, int P, int Q, const RS& rs, cplx ab, cplx b) {
-    cplx x = {0.0, 0.0};
-    if (P < tj) x = cscale(rs.v[tj - P][tj - Q], cmul(ab, v[Q * tj + P]));
-    if (P >= 1) x = cadd(x, cscale(rs.v[P][tj - Q], cmul(b, v[Q * tj + P - 1])));
-    return x;
+    const cplx v0 = v[Q * tj + P], v1 = v[max(Q * tj + P - 1, 0)];
+    const cplx t0 = cmul(ab, v0), t1 = cmul(b, v1);
+    const double w0 = rs.v[tj - P][tj - Q], w1 = rs.v[P][tj - Q];
+    return {fma(w0, t0.re, w1 * t1.re), fma(w0, t0.im, w1 * t1.im)};
 }
 
 __device__ __forceinline__ bool in_col_half(int tj, int P, int Q) {
@@ -224,6 +227,8 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_snap_ui(const double* __rest
     __shared__ RS rs;
     __shared__ NbPair s_nb[kWarps][32];
     __shared__ cplx s_lvl[kWarps][2][2][kLevelMax];
+    for (int t = threadIdx.x; t < kWarps * 4 * kLevelMax; t += blockDim.x)
+        (&s_lvl[0][0][0][0])[t] = {0.0, 0.0};   // rec2 reads finite neighbours at the column ends
     stage_rs(rs);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, hl = lane & 15, hh = lane >> 4;
     const int i = blockIdx.x * kWarps + w;
@@ -404,20 +409,25 @@ __global__ void k_snap_y_compress(const double2* __restrict__ Y, int n, int nf, 
 //   t_d = f_c' rhat_d S + f_c Re(G_abar conj(da_d) + G_b db_d).
 // Same quantity (equal to rounding) for ~1/6 of the reference's complex MACs.
 // One warp per atom, two neighbours at a time (one per half-warp).
+constexpr int kLamMax = 41;   // half_size(8): lambda levels keep only their column-major C prefix
+
 template <int TWOJ>
-__global__ void __launch_bounds__(kWarps * 32, 3) k_snap_deidrj(const double* __restrict__ x, int n_local,
+__global__ void __launch_bounds__(kWarps * 32, 4) k_snap_deidrj(const double* __restrict__ x, int n_local,
                                                              const int* __restrict__ table,
                                                              const int* __restrict__ counts, int cap, double rc,
                                                              const double2* __restrict__ Yh, int ld,
                                                              double* __restrict__ f) {
-    constexpr int NF = block_offset(TWOJ + 1);
+    constexpr int NU = block_offset(TWOJ) > 0 ? block_offset(TWOJ) : 1;   // levels 0..TWOJ-1 (the top is never re-read)
     constexpr int NH = half_offset(TWOJ + 1);
-    extern __shared__ double s_dyn_d[];  // rs | pairs | Y_i half | u levels | lambda levels
+    extern __shared__ double s_dyn_d[];  // rs | pairs | Y_i (C order) | u levels | lambda C prefixes
     RS& rs = *reinterpret_cast<RS*>(s_dyn_d);
     auto s_nb = reinterpret_cast<NbPair(*)[32]>(reinterpret_cast<char*>(s_dyn_d) + sizeof(RS));
     auto s_y = reinterpret_cast<cplx(*)[NH]>(s_nb + kWarps);
-    auto s_u = reinterpret_cast<cplx(*)[2][NF]>(s_y + kWarps);
-    auto s_l = reinterpret_cast<cplx(*)[2][2][kLevelMax]>(s_u + kWarps);
+    auto s_u = reinterpret_cast<cplx(*)[2][NU]>(s_y + kWarps);
+    auto s_l = reinterpret_cast<cplx(*)[2][2][kLamMax]>(s_u + kWarps);
+    // zero the level buffers once: the branch-free edges read finite neighbours
+    for (int t = threadIdx.x; t < kWarps * 2 * (NU + 2 * kLamMax); t += blockDim.x)
+        reinterpret_cast<cplx*>(s_u)[t] = {0.0, 0.0};
     stage_rs(rs);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, hl = lane & 15, hh = lane >> 4;
     const int i = blockIdx.x * kWarps + w;
@@ -437,7 +447,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_snap_deidrj(const double* __
     __syncwarp();
     const cplx* sy = s_y[w];
     cplx* ul = s_u[w][hh];
-    cplx(*lam)[kLevelMax] = s_l[w][hh];
+    cplx(*lam)[kLamMax] = s_l[w][hh];
     const double4 xi = mdkk::ld4(x, i);
     const int n = min(counts[i], cap);
     const double rc2 = rc * rc;
@@ -469,7 +479,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_snap_deidrj(const double* __
                         int P, Q;
                         col_elem(tj, c, P, Q);
                         const cplx v = rec2(ul + block_offset(tj - 1), tj, P, Q, rs, ab, g.b);
-                        store_mirrored(ul + block_offset(tj), tj, P, Q, v);
+                        if (tj < TWOJ) store_mirrored(ul + block_offset(tj), tj, P, Q, v);
                         const cplx yv = sy[half_offset(tj) + c];
                         const double wgt = (2 * P == tj && 2 * Q == tj) ? 1.0 : 2.0;
                         S += wgt * (yv.re * v.re + yv.im * v.im);
@@ -510,9 +520,12 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_snap_deidrj(const double* __
                             }
                         }
                         lc[Q * (tj + 1) + P] = l;
+                        // zero weights at the column ends (see rec2): no branches
                         const cplx lcj = cconj(l);
-                        if (P < tj) Ga = cadd(Ga, cscale(rs.v[tj - P][tj - Q], cmul(lcj, v[Q * tj + P])));
-                        if (P >= 1) Gb = cadd(Gb, cscale(rs.v[P][tj - Q], cmul(lcj, v[Q * tj + P - 1])));
+                        const cplx t0 = cmul(lcj, v[Q * tj + P]), t1 = cmul(lcj, v[max(Q * tj + P - 1, 0)]);
+                        const double w0 = rs.v[tj - P][tj - Q], w1 = rs.v[P][tj - Q];
+                        Ga = {fma(w0, t0.re, Ga.re), fma(w0, t0.im, Ga.im)};
+                        Gb = {fma(w1, t1.re, Gb.re), fma(w1, t1.im, Gb.im)};
                     }
                 }
                 __syncwarp();
@@ -722,7 +735,8 @@ int mdkk_snap_deidrj(mdkk_snap* s, const double* x, int n_local, const int* tabl
 #define MDKK_DE(TJ)                                                                                          \
     case TJ: {                                                                                               \
         const size_t sm = sizeof(RS) + kWarps * (32 * sizeof(NbPair) +                                       \
-            (half_offset(TJ + 1) + 2 * block_offset(TJ + 1) + 4 * kLevelMax) * sizeof(cplx));                \
+            (half_offset(TJ + 1) + 2 * (block_offset(TJ) > 0 ? block_offset(TJ) : 1) + 4 * kLamMax) *         \
+            sizeof(cplx));                                                                                   \
         cudaFuncSetAttribute(k_snap_deidrj<TJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);      \
         k_snap_deidrj<TJ><<<nb, kWarps * 32, sm, mdkk::as_stream(stream)>>>(                                 \
             x, n_local, table, counts, cap, rc, reinterpret_cast<const double2*>(Yh), ld, f);                \
