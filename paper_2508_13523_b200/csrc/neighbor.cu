@@ -178,9 +178,19 @@ __global__ void __launch_bounds__(kWarps * 32) k_nbr_build(
                 sfz[t] = (float)(p.z - ccz);
             }
             __syncwarp();
+            // branch-free prefilter into a per-lane bit mask, then each lane visits only
+            // its own survivors (in candidate order): the warp runs max-popcount exact
+            // tests per chunk instead of one divergent test per candidate
+            unsigned long long bits = 0ull;
+#pragma unroll 8
             for (int t = 0; t < cn; ++t) {
                 const float dx = sfx[t] - fxi, dy = sfy[t] - fyi, dz = sfz[t] - fzi;
-                if (dx * dx + dy * dy + dz * dz < bc2f) visit(su[u0 + t], spx[t], spy[t], spz[t]);
+                bits |= (unsigned long long)(dx * dx + dy * dy + dz * dz < bc2f) << t;
+            }
+            while (bits) {
+                const int t = __ffsll((long long)bits) - 1;
+                bits &= bits - 1ull;
+                visit(su[u0 + t], spx[t], spy[t], spz[t]);
             }
             __syncwarp();
         }
