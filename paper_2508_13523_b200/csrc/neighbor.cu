@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_nbr_build(
     int* __restrict__ max_count) {
     __shared__ int s_union[kWarps][kUnion];
     __shared__ double s_pos[kWarps][3][kChunk];
-    __shared__ float s_rel[kWarps][3][kChunk];
+    __shared__ float4 s_rel[kWarps][kChunk];   // cluster-relative FP32 (x, y, z, -): one broadcast LDS.128
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int c = blockIdx.x * kWarps + w;
     const int ncl = (n_local + 31) >> 5;
@@ -97,9 +97,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_nbr_build(
     double* spx = s_pos[w][0];
     double* spy = s_pos[w][1];
     double* spz = s_pos[w][2];
-    float* sfx = s_rel[w][0];
-    float* sfy = s_rel[w][1];
-    float* sfz = s_rel[w][2];
+    float4* sf = s_rel[w];
     const int i = c * 32 + lane;
     const bool valid = i < n_local;
     const double4 xi = mdkk::ld4(x, valid ? i : c * 32);
@@ -173,24 +171,26 @@ __global__ void __launch_bounds__(kWarps * 32) k_nbr_build(
                 spx[t] = p.x;
                 spy[t] = p.y;
                 spz[t] = p.z;
-                sfx[t] = (float)(p.x - ccx);
-                sfy[t] = (float)(p.y - ccy);
-                sfz[t] = (float)(p.z - ccz);
+                sf[t] = make_float4((float)(p.x - ccx), (float)(p.y - ccy), (float)(p.z - ccz), 0.f);
             }
             __syncwarp();
             // branch-free prefilter into a per-lane bit mask, then each lane visits only
             // its own survivors (in candidate order): the warp runs max-popcount exact
             // tests per chunk instead of one divergent test per candidate
-            unsigned long long bits = 0ull;
-#pragma unroll 8
-            for (int t = 0; t < cn; ++t) {
-                const float dx = sfx[t] - fxi, dy = sfy[t] - fyi, dz = sfz[t] - fzi;
-                bits |= (unsigned long long)(dx * dx + dy * dy + dz * dz < bc2f) << t;
-            }
-            while (bits) {
-                const int t = __ffsll((long long)bits) - 1;
-                bits &= bits - 1ull;
-                visit(su[u0 + t], spx[t], spy[t], spz[t]);
+            for (int h0 = 0; h0 < cn; h0 += 32) {   // 32 candidates per mask: compile-time bit positions
+                unsigned bits = 0u;
+#pragma unroll
+                for (int t = 0; t < 32; ++t) {
+                    const float4 q = sf[h0 + t];     // entries past cn are stale but masked below
+                    const float dx = q.x - fxi, dy = q.y - fyi, dz = q.z - fzi;
+                    bits |= (dx * dx + dy * dy + dz * dz < bc2f) ? (1u << t) : 0u;
+                }
+                if (cn - h0 < 32) bits &= (1u << (cn - h0)) - 1u;
+                while (bits) {
+                    const int t = h0 + __ffs(bits) - 1;
+                    bits &= bits - 1u;
+                    visit(su[u0 + t], spx[t], spy[t], spz[t]);
+                }
             }
             __syncwarp();
         }

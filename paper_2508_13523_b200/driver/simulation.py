@@ -16,6 +16,7 @@ base names resolve to the same GPU styles (there is no CPU path here).
 
 from __future__ import annotations
 
+import gc
 import math
 
 import numpy as np
@@ -81,8 +82,14 @@ class LJStyle:
         if self.kernel is None:
             raise RunError("pair_coeff must be set before computing forces")
         dev = system.device
-        evs = torch.zeros((len(system.stores), 7), dtype=torch.float64, device=dev)
-        flags = torch.zeros(1, dtype=torch.int32, device=dev)
+        # persistent per-system buffers: the kernels overwrite ev; the flag word is
+        # sticky (checked on thermo steps: "at or before step N")
+        key = (id(system), len(system.stores), str(dev))
+        if getattr(self, "_bufkey", None) != key:
+            self._bufkey = key
+            self._evs = torch.zeros((len(system.stores), 7), dtype=torch.float64, device=dev)
+            self._flags = torch.zeros(1, dtype=torch.int32, device=dev)
+        evs, flags = self._evs, self._flags
         half = False
         for k, (s, nl) in enumerate(zip(system.stores, lists)):
             lj_force_rank(s, nl, self.kernel.params, evs[k], flags, virial=False)
@@ -194,6 +201,7 @@ class Simulation:
         dev = self.config.device
         self.device = torch.device(dev) if dev is not None else torch.device("cuda", torch.cuda.current_device())
         self._d2 = None
+        self._d2_host = None
         self._e_dev = None
         self._flags = None
 
@@ -307,9 +315,12 @@ class Simulation:
         """migrate + build (mdkk/driver/simulation.py:368-373)."""
         halo = self.style.r_c + self.config.skin
         self.system.migrate(halo)
+        old = self.lists if self.lists is not None and len(self.lists) == len(self.system.stores) else None
+        self.lists = None   # the old lists are dead: their buffers are recycled
         self.lists = [build(s, self.system.box, self.style.r_c, self.config.skin, style=self._list_style,
-                            newton=self.config.newton, cap_hint=self._cap_hint)
-                      for s in self.system.stores]
+                            newton=self.config.newton, cap_hint=self._cap_hint,
+                            recycle=old[k] if old is not None else None)
+                      for k, s in enumerate(self.system.stores)]
         self._cap_hint = max(nl.alloc_cap for nl in self.lists)
         self.n_rebuilds += 1
 
@@ -350,10 +361,16 @@ class Simulation:
                                              nl.ref_dev.data_ptr(), s.n_local, self.dt, h,
                                              self._d2[k:].data_ptr(), st), "mdkk_verlet_first")
             s.device_wrote(pos=True, vel=True)
-        worst = self._d2[: len(self.system.stores)].max()
+        n = len(self.system.stores)
+        worst = self._d2[0:1] if n == 1 else self._d2[:n].max().reshape(1)
         if self.config.distributed:   # any rank over skin/2 -> every rank rebuilds (mdkk/neighbor.py:230)
-            worst = self.system.allreduce_max(worst.reshape(1))
-        return math.sqrt(float(worst.item())) > 0.5 * self.config.skin
+            worst = self.system.allreduce_max(worst)
+        # the step's one host sync: a pinned 8-byte read-back, no reduction kernel for one rank
+        if self._d2_host is None:
+            self._d2_host = torch.zeros(1, dtype=torch.float64, pin_memory=True)
+        self._d2_host.copy_(worst, non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        return math.sqrt(float(self._d2_host[0])) > 0.5 * self.config.skin
 
     def _half_kick(self):
         lib, st = _lib.lib(), _lib.stream(self.device)
@@ -375,6 +392,25 @@ class Simulation:
 
     def step_once(self) -> float:
         return float(self.step_device().item())
+
+    def advance(self, n_steps: int) -> torch.Tensor | None:
+        """n velocity-Verlet steps without thermo; returns the last step's device energy.
+
+        The cyclic garbage collector is paused for the loop: the per-step host
+        objects are acyclic (freed by reference counting), and a full
+        collection over the interpreter's heap would stall the launch queue
+        for milliseconds.
+        """
+        was = gc.isenabled()
+        gc.disable()
+        try:
+            e = None
+            for _ in range(n_steps):
+                e = self.step_device()
+            return e
+        finally:
+            if was:
+                gc.enable()
 
     def _check_finite(self, step, e_pot):
         if not np.isfinite(e_pot):
@@ -409,10 +445,12 @@ class Simulation:
                 self.log(result.lines[-1])
 
             log(0, self._forces_device())
-            for step in range(1, n_steps + 1):
-                e = self.step_device()
-                if step % self.thermo_every == 0 or step == n_steps:
-                    log(step, e)
+            step = 0
+            while step < n_steps:   # device-resident stretches between thermo steps
+                k = min(self.thermo_every - step % self.thermo_every, n_steps - step)
+                e = self.advance(k)
+                step += k
+                log(step, e)
             result.n_rebuilds = self.n_rebuilds - rebuilds0
         return result
 

@@ -49,7 +49,7 @@ class NeighborList:
     """
 
     def __init__(self, store: AtomStore, style: str, newton: bool, cutoff: float, skin: float,
-                 cap: int, table: torch.Tensor, counts: torch.Tensor, max_count: int):
+                 cap: int, table: torch.Tensor, counts: torch.Tensor, max_count: int, ref_buf=None):
         self.store = store
         self.style = style
         self.newton = bool(newton)
@@ -61,7 +61,7 @@ class NeighborList:
         self.max_count = int(max_count)
         self.table_dev = table
         self.counts_dev = counts
-        self.ref_dev = store.x[: max(store.n_local, 1)].clone()
+        self.ref_dev = store.x[: max(store.n_local, 1)].clone() if ref_buf is None else _ref_into(ref_buf, store)
         self._d2 = torch.zeros(1, dtype=torch.float64, device=store.device)
         self._pairs = None
 
@@ -149,6 +149,25 @@ class NeighborList:
                 f"exceeds skin/2 = {0.5 * self.skin:.4g}")
 
 
+def _ref_into(buf: torch.Tensor, store: AtomStore) -> torch.Tensor:
+    n = max(store.n_local, 1)
+    if buf.shape[0] < n or buf.device != store.device:
+        return store.x[:n].clone()
+    out = buf[:n]
+    out.copy_(store.x[:n])
+    return out
+
+
+def _recycled(t: torch.Tensor | None, shape, dtype, device) -> torch.Tensor:
+    """View of a dead list's storage when it is large enough (engine rebuilds), else a new tensor."""
+    numel = 1
+    for d in shape:
+        numel *= d
+    if t is not None and t.dtype == dtype and t.device == device and t.is_contiguous() and t.numel() >= numel:
+        return t.reshape(-1)[:numel].view(shape)
+    return torch.empty(shape, dtype=dtype, device=device)
+
+
 class _BuildCache:
     """Per-store reusable device buffers for binning / building."""
 
@@ -167,13 +186,15 @@ _cache: dict = {}
 
 def build(store: AtomStore, box: Box, cutoff: float, skin: float, style: str = "full",
           newton: bool = True, capacity: int = DEFAULT_CAPACITY, cap_hint: int | None = None,
-          **_unused) -> NeighborList:
+          recycle: NeighborList | None = None, **_unused) -> NeighborList:
     """One rank's list from its local + ghost rows (mdkk/neighbor.py:182-219).
 
     Owned rows must be cell-sorted for compact clusters (RankedSystem keeps
     them so); any order is still correct.  `cap_hint` / `ucap_hint`
     (engine-internal) size the first launch; the reported `max_neighbors`
     always follows the reference growth sequence from `capacity`.
+    `recycle` (engine-internal) is a list that is dead after this call: its
+    device buffers are reused instead of allocating a new ~GB table.
     """
     if style not in STYLES:
         raise NeighborError(f"unknown list style {style!r}")
@@ -197,10 +218,11 @@ def build(store: AtomStore, box: Box, cutoff: float, skin: float, style: str = "
     _lib.check(lib.mdkk_bin_atoms(ctx, store.x.data_ptr(), n_total, garr, narr, keys.data_ptr(),
                                   cstart.data_ptr(), catoms.data_ptr(), stream), "mdkk_bin_atoms")
     alloc = max(grow_capacity(capacity, 0), int(cap_hint or 0))
-    counts = torch.empty(max(n_local, 1), dtype=torch.int32, device=dev)
+    old_t = recycle.table_dev if recycle is not None else None
+    counts = _recycled(recycle.counts_dev if recycle is not None else None, (max(n_local, 1),), torch.int32, dev)
     mc = torch.zeros(1, dtype=torch.int32, device=dev)
     while True:
-        table = torch.empty(((n_local + 31) // 32 or 1, alloc, 32), dtype=torch.int32, device=dev)
+        table = _recycled(old_t, ((n_local + 31) // 32 or 1, alloc, 32), torch.int32, dev)
         mc.zero_()
         _lib.check(lib.mdkk_nbr_build(ctx, store.x.data_ptr(), n_local, n_total, garr, narr, cstart.data_ptr(),
                                       catoms.data_ptr(), store.gid.data_ptr(), store.orank.data_ptr(),
@@ -212,7 +234,8 @@ def build(store: AtomStore, box: Box, cutoff: float, skin: float, style: str = "
             break
         alloc = grow_capacity(alloc, need)  # never truncate: grow and rebuild
     cap = grow_capacity(capacity, need)
-    return NeighborList(store, style, newton, cutoff, skin, cap, table, counts, need)
+    return NeighborList(store, style, newton, cutoff, skin, cap, table, counts, need,
+                        ref_buf=recycle.ref_dev if recycle is not None else None)
 
 
 def build_all(system: RankedSystem, cutoff: float, skin: float, style: str = "full",

@@ -91,12 +91,16 @@ class PairResult:
 
 def lj_force_rank(store, nl: NeighborList, params: PairParams, ev: torch.Tensor, flags: torch.Tensor,
                   zero: bool = True, virial: bool = True) -> None:
-    """One rank's kernel launch (no host sync).  Ghost rows must be zero on entry for half lists."""
+    """One rank's kernel launch (no host sync).
+
+    Ghost force rows are zero outside a force evaluation (migrate zeroes all
+    rows, reverse comm zeroes ghosts, full-list kernels write owner rows
+    only), so only the half list (owner rows accumulate with atomics) needs
+    a clear.
+    """
     dev = store.device
     if zero and nl.style == "half":
         store.f.zero_()
-    elif zero and store.n_ghost:
-        store.f[store.n_local:store.n_total].zero_()
     _lib.check(_lib.lib().mdkk_lj_force(
         _lib.ctx(dev), store.x.data_ptr(), store.n_local, nl.table_dev.data_ptr(), nl.counts_dev.data_ptr(),
         nl.alloc_cap, STYLES[nl.style], int(nl.newton), int(virial), params.epsilon, params.sigma, params.r_c,

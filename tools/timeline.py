@@ -1,0 +1,59 @@
+"""GPU busy/idle timeline of the bench's LJ step loop (torch.profiler / CUPTI; no nsys needed).
+
+Prints total wall, summed kernel time, and the largest idle gaps with the
+CPU-side op that was running when each gap ended.
+"""
+import json, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from torch.profiler import profile, ProfilerActivity
+import bench
+from paper_2508_13523_b200.driver import RunConfig, Simulation
+
+style = sys.argv[1] if len(sys.argv) > 1 else "full"
+steps = int(sys.argv[2]) if len(sys.argv) > 2 else 30
+dev = torch.device("cuda", 0)
+sim = Simulation(RunConfig(list_style=style, newton=(style == "half"), device=dev), log=None)
+sim.execute(bench.lj_script(80))
+sim._ensure_system(); sim._forces_device()
+for _ in range(5):
+    sim.step_device()
+torch.cuda.synchronize()
+with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA], with_stack=False) as prof:
+    r0 = sim.n_rebuilds
+    for _ in range(steps):
+        sim.step_device()
+    torch.cuda.synchronize()
+path = "gpurun_out/timeline.json"
+os.makedirs("gpurun_out", exist_ok=True)
+prof.export_chrome_trace(path)
+ev = json.load(open(path))["traceEvents"]
+k = sorted([e for e in ev if e.get("cat") in ("kernel", "gpu_memset", "gpu_memcpy") and "dur" in e], key=lambda e: e["ts"])
+t0, t1 = k[0]["ts"], k[-1]["ts"] + k[-1]["dur"]
+busy = sum(e["dur"] for e in k)
+print(f"{style}: steps={steps} rebuilds={sim.n_rebuilds - r0} wall(first->last kernel)={(t1 - t0) / 1e3:.3f} ms "
+      f"kernel-busy={busy / 1e3:.3f} ms idle={(t1 - t0 - busy) / 1e3:.3f} ms")
+gaps = []
+for a, b in zip(k, k[1:]):
+    g = b["ts"] - (a["ts"] + a["dur"])
+    if g > 0:
+        gaps.append((g, a["name"][:40], b["name"][:40]))
+gaps.sort(reverse=True)
+tot = sum(g for g, *_ in gaps)
+import collections
+by = collections.Counter()
+for g, a, b in gaps:
+    by[(a, b)] += g
+print("idle by (prev kernel -> next kernel), top 15:")
+for (a, b), g in by.most_common(15):
+    print(f"  {g / 1e3:8.3f} ms  {a} -> {b}")
+cpu = collections.Counter()
+for e in ev:
+    if e.get("cat") == "cpu_op" and "dur" in e:
+        cpu[e["name"][:50]] += e["dur"]
+print("cpu ops (total us), top 15:")
+for n, d in cpu.most_common(15):
+    print(f"  {d / 1e3:8.3f} ms  {n}")
+print("last 40 GPU ops (gap before, duration, name):")
+for a, b in list(zip(k, k[1:]))[-40:]:
+    print(f"  gap {(b['ts'] - a['ts'] - a['dur']):8.1f} us  dur {b['dur']:8.1f} us  {b['name'][:70]}")
