@@ -29,11 +29,7 @@ __global__ void __launch_bounds__(kBlock) k_lj(const double* __restrict__ x, int
         double fx = 0.0, fy = 0.0, fz = 0.0;
         bool bad = false;
         const int* col = table + ((long long)(i >> 5) * cap) * 32 + (i & 31);
-        int j_next = n > 0 ? __ldg(col) : 0;
-        for (int k = 0; k < n; ++k) {
-            const int j = j_next;
-            if (k + 1 < n) j_next = __ldg(col + (long long)(k + 1) * 32);
-            const double4 xj = mdkk::ld4(x, j);
+        auto pair = [&](int j, const double4& xj) {
             const double dx = xj.x - xi.x, dy = xj.y - xi.y, dz = xj.z - xi.z;
             const double r2 = mdkk::r2_exact(dx, dy, dz);
             if (r2 < rc2) {
@@ -66,7 +62,30 @@ __global__ void __launch_bounds__(kBlock) k_lj(const double* __restrict__ x, int
                     acc[6] += wf * (dy * dz);
                 }
             }
+        };
+        // Gathers in batches of kB with the next batch's indices already in
+        // flight: kB independent x_j loads per wait (the loop is L2-latency
+        // bound otherwise).  Pair order (k ascending) is unchanged.
+        constexpr int kB = 4;
+        int jn[kB];
+#pragma unroll
+        for (int b = 0; b < kB; ++b) jn[b] = b < n ? __ldg(col + (long long)b * 32) : i;
+        int k = 0;
+        for (; k + kB <= n; k += kB) {
+            int jc[kB];
+            double4 xc[kB];
+#pragma unroll
+            for (int b = 0; b < kB; ++b) jc[b] = jn[b];
+#pragma unroll
+            for (int b = 0; b < kB; ++b) xc[b] = mdkk::ld4(x, jc[b]);
+#pragma unroll
+            for (int b = 0; b < kB; ++b) jn[b] = (k + kB + b < n) ? __ldg(col + (long long)(k + kB + b) * 32) : i;
+#pragma unroll
+            for (int b = 0; b < kB; ++b) pair(jc[b], xc[b]);
         }
+#pragma unroll
+        for (int b = 0; b < kB; ++b)
+            if (k + b < n) pair(jn[b], mdkk::ld4(x, jn[b]));
         if (STYLE == 0) {
             mdkk::st4(f, i, make_double4(fx, fy, fz, 0.0));
         } else {
