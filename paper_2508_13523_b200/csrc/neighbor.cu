@@ -141,6 +141,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_nbr_build(
     // margin >> FP32 rounding: |r2_f - r2| <~ 6 eps_f D^2 with D the farthest cluster-relative coordinate
     const double hx = 0.5 * (bmax_x - bmin_x) + bc, hy = 0.5 * (bmax_y - bmin_y) + bc, hz = 0.5 * (bmax_z - bmin_z) + bc;
     const float bc2f = (float)(bc2 * (1.0 + 1e-4) + 4e-6 * (hx * hx + hy * hy + hz * hz));
+    const float lo2f = (float)(bc2 * (1.0 - 1e-4) - 4e-6 * (hx * hx + hy * hy + hz * hz));  // certainly inside
     int cnt = 0;
     const int64_t gi = (STYLE == 1 && valid) ? gid[i] : 0;
     int* trow = table + ((long long)c * cap) * 32 + lane;
@@ -171,7 +172,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_nbr_build(
                 spx[t] = p.x;
                 spy[t] = p.y;
                 spz[t] = p.z;
-                sf[t] = make_float4((float)(p.x - ccx), (float)(p.y - ccy), (float)(p.z - ccz), 0.f);
+                sf[t] = make_float4((float)(p.x - ccx), (float)(p.y - ccy), (float)(p.z - ccz),
+                                    __int_as_float(su[u0 + t]));
             }
             __syncwarp();
             // branch-free prefilter into a per-lane bit mask, then each lane visits only
@@ -179,13 +181,32 @@ __global__ void __launch_bounds__(kWarps * 32) k_nbr_build(
             // tests per chunk instead of one divergent test per candidate
             for (int h0 = 0; h0 < cn; h0 += 32) {   // 32 candidates per mask: compile-time bit positions
                 unsigned bits = 0u;
+                const int lim = cn - h0;
+                if (STYLE == 0) {
+                    // full list: two-sided FP32 test; certain members are stored right here
+                    // (predicated, candidate order), only the thin shell around bc goes to
+                    // the exact FP64 test below
 #pragma unroll
-                for (int t = 0; t < 32; ++t) {
-                    const float4 q = sf[h0 + t];     // entries past cn are stale but masked below
-                    const float dx = q.x - fxi, dy = q.y - fyi, dz = q.z - fzi;
-                    bits |= (dx * dx + dy * dy + dz * dz < bc2f) ? (1u << t) : 0u;
+                    for (int t = 0; t < 32; ++t) {
+                        const float4 q = sf[h0 + t];     // entries past cn are stale but masked below
+                        const float dx = q.x - fxi, dy = q.y - fyi, dz = q.z - fzi;
+                        const float r2f = dx * dx + dy * dy + dz * dz;
+                        const int j = __float_as_int(q.w);
+                        if (t < lim && valid && r2f < lo2f && j != i) {
+                            if (cnt < cap) trow[(long long)cnt * 32] = j;
+                            ++cnt;
+                        }
+                        bits |= (r2f < bc2f && !(r2f < lo2f)) ? (1u << t) : 0u;
+                    }
+                } else {
+#pragma unroll
+                    for (int t = 0; t < 32; ++t) {
+                        const float4 q = sf[h0 + t];     // entries past cn are stale but masked below
+                        const float dx = q.x - fxi, dy = q.y - fyi, dz = q.z - fzi;
+                        bits |= (dx * dx + dy * dy + dz * dz < bc2f) ? (1u << t) : 0u;
+                    }
                 }
-                if (cn - h0 < 32) bits &= (1u << (cn - h0)) - 1u;
+                if (lim < 32) bits &= (1u << lim) - 1u;
                 while (bits) {
                     const int t = h0 + __ffs(bits) - 1;
                     bits &= bits - 1u;

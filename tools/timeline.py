@@ -54,6 +54,25 @@ for e in ev:
 print("cpu ops (total us), top 15:")
 for n, d in cpu.most_common(15):
     print(f"  {d / 1e3:8.3f} ms  {n}")
-print("last 40 GPU ops (gap before, duration, name):")
-for a, b in list(zip(k, k[1:]))[-40:]:
-    print(f"  gap {(b['ts'] - a['ts'] - a['dur']):8.1f} us  dur {b['dur']:8.1f} us  {b['name'][:70]}")
+# per step: ops from one k_verlet_first to the next
+starts = [n for n, e in enumerate(k) if "k_verlet_first" in e["name"]]
+rows = []
+for a, b in zip(starts, starts[1:]):
+    ops = k[a:b]
+    idle = sum(max(0.0, y["ts"] - (x["ts"] + x["dur"])) for x, y in zip(ops, ops[1:] + [k[b]]))
+    busy = sum(e["dur"] for e in ops)
+    rebuild = any("nbr_build" in e["name"] for e in ops)
+    rows.append((rebuild, busy, idle, a, b))
+for reb in (False, True):
+    sel = [r for r in rows if r[0] == reb]
+    if sel:
+        print(f"{'rebuild' if reb else 'plain'} steps: n={len(sel)} busy={sum(r[1] for r in sel)/len(sel):.1f} us "
+              f"idle={sum(r[2] for r in sel)/len(sel):.1f} us")
+for reb in (False, True):
+    sel = [r for r in rows if r[0] == reb]
+    if not sel:
+        continue
+    _, _, _, a, b = sel[-1]
+    print(("rebuild" if reb else "plain") + " step op sequence (gap before, duration, name):")
+    for x, y in zip(k[a - 1:b], k[a:b + 1]):
+        print(f"  gap {(y['ts'] - x['ts'] - x['dur']):8.1f} us  dur {y['dur']:8.1f} us  {y['name'][:70]}")
