@@ -201,6 +201,33 @@ int mdkk_snap_y_compress(mdkk_snap* snap, const double* Y, int n_local, double* 
 int mdkk_snap_deidrj(mdkk_snap* snap, const double* x, int n_local, const int* table, const int* counts, int cap,
                      double rc, const double* Yh, int ld, double* f, void* stream);
 
+/* --- SNAP API-parity stages (not on the engine path; csrc/snap_aux.cu) ---
+ * Neighbour map (build_neighbor_map / NeighborMap, mdkk/snap/compute.py:66-119):
+ * per-row in-range pair counts npair[n_local+1] and their exclusive scan
+ * offsets[n_local+1] (offsets[n_local] = total pairs P), then the pairs in
+ * (row, dz, dy, dx) order: rows/cols int32 [P], dr f64 [P][3], r [P],
+ * a/b complex128 [P], fc/dfc [P]. */
+int mdkk_snap_pair_count(mdkk_ctx* ctx, const double* x, int n_local, const int* table, const int* counts, int cap,
+                         double rc, int* npair, int* offsets, int* flags, void* stream);
+int mdkk_snap_pair_fill(const double* x, int n_local, const int* table, const int* counts, int cap, double rc,
+                        const int* offsets, int* rows, int* cols, double* dr, double* r, double* a, double* b,
+                        double* fc, double* dfc, void* stream);
+/* Staged force path (compute_duidrj / compute_deidrj, mdkk/snap/compute.py:412-436):
+ * wdu complex128 [P][3][n_flat] = f_c du/d dr_d + f_c' (dr_d / r) u; then
+ * f[row] += t, f[col] -= t with t_d = Re sum_f Y[row][f] conj(wdu[p][d][f]) (Y in the
+ * reference layout, f double4 rows, caller-zeroed). */
+int mdkk_snap_duidrj(mdkk_snap* snap, int n_pairs, const double* dr, double rc, double* wdu, void* stream);
+int mdkk_snap_deidrj_staged(mdkk_snap* snap, int n_pairs, const int* rows, const int* cols, const double* Y,
+                            const double* wdu, double* f, void* stream);
+/* Descriptors (compute_bi_complex, mdkk/snap/compute.py:354-373): B complex128
+ * [n_local][n_tri], B_t = sum c * op(U[g]) op(U[h]) op(U[z]) over the triple's
+ * terms (half indices; code = g | h << 8 | z << 16 | conj_g << 24 | conj_h << 25 |
+ * conj_z << 26 | last-of-triple << 27; tri[k] = triple of term k; chunk[w] =
+ * first term of warp w, output-aligned, mdkk_snap_bi_warps() + 1 entries). */
+int mdkk_snap_bi(mdkk_snap* snap, const double* U, int n_local, const double* coef, const int* code, const int* tri,
+                 const int* chunk, int n_tri, double* B, void* stream);
+int mdkk_snap_bi_warps(void);
+
 #ifdef __cplusplus
 }
 #endif

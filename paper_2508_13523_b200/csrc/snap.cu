@@ -15,201 +15,9 @@
 // U_i (ui) or Y_i (deidrj) in registers, so the per-atom sums need no atomics.
 // compute_yi: one warp per atom over an output-sorted contribution list staged
 // through shared memory; compute_fused_deidrj in reverse mode (see below).
-#include <algorithm>
-#include <cmath>
-#include <vector>
-
-#include "common.cuh"
-
-struct ZEntry {      // one U*U product of the Z-list adjoint (16 B, read as a warp broadcast)
-    double coef;
-    int code;        // g | h << 8 | f << 16 | conj_g << 24 | conj_h << 25 | last-of-output << 26 | center << 27
-    int pad;
-};
-
-struct mdkk_snap {
-    int twojmax = 0;
-    int n_flat = 0;
-    int n_half = 0;
-    int n_entries = 0;
-    ZEntry* ent = nullptr;   // [n_entries], sorted by output
-    int* chunk = nullptr;    // [kYW + 1] per-warp entry ranges (output-aligned, balanced)
-    int* fmap = nullptr;     // [n_flat] half index | mirrored << 16 | odd sign << 17
-};
+#include "snap_common.cuh"
 
 namespace {
-
-constexpr int kMaxTwoJ = 8;
-constexpr int kLevelMax = (kMaxTwoJ + 1) * (kMaxTwoJ + 1);  // 81
-constexpr int kSlots = 14;                                   // sum_tj ceil((tj+1)^2 / 32) for 2J = 8
-constexpr int kWarps = 4;
-constexpr double kPi = 3.141592653589793;
-
-__host__ __device__ constexpr int level_size(int tj) { return (tj + 1) * (tj + 1); }
-__host__ __device__ constexpr int level_slots(int tj) { return (level_size(tj) + 31) / 32; }
-__host__ __device__ constexpr int block_offset(int tj) { return tj * (tj + 1) * (2 * tj + 1) / 6; }
-__host__ __device__ constexpr int slot_base(int tj) {
-    int s = 0;
-    for (int t = 0; t < tj; ++t) s += level_slots(t);
-    return s;
-}
-
-struct cplx {
-    double re, im;
-};
-__device__ __forceinline__ cplx cmul(cplx a, cplx b) { return {a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re}; }
-__device__ __forceinline__ cplx cconj(cplx a) { return {a.re, -a.im}; }
-__device__ __forceinline__ cplx cadd(cplx a, cplx b) { return {a.re + b.re, a.im + b.im}; }
-__device__ __forceinline__ cplx cscale(double s, cplx a) { return {s * a.re, s * a.im}; }
-__device__ __forceinline__ cplx cneg(cplx a) { return {-a.re, -a.im}; }
-
-// Weights of the two-term column recursion, rs[k][l] = sqrt(k / l) (0 <= k, l <= 8).
-// Staged per CTA in shared memory (lanes read different entries: constant
-// memory would serialise).
-__device__ double g_rs[kMaxTwoJ + 1][kMaxTwoJ + 1];
-
-struct RS {
-    double v[kMaxTwoJ + 1][kMaxTwoJ + 1];
-};
-
-__device__ __forceinline__ void stage_rs(RS& rs) {
-    for (int t = threadIdx.x; t < (kMaxTwoJ + 1) * (kMaxTwoJ + 1); t += blockDim.x)
-        rs.v[t / (kMaxTwoJ + 1)][t % (kMaxTwoJ + 1)] = g_rs[t / (kMaxTwoJ + 1)][t % (kMaxTwoJ + 1)];
-    __syncthreads();
-}
-
-struct PairGeo {
-    cplx a, b;
-    double fc, dfc, r;
-};
-
-// a, b, f_c, f_c' (mdkk/snap/compute.py:27-45).
-__device__ __forceinline__ void pair_geometry(double dx, double dy, double dz, double r2, double rc, PairGeo& g,
-                                              double& z0, double& r0) {
-    const double r = sqrt(r2);
-    const double ct = 0.99 * kPi / rc;
-    z0 = r / tan(ct * r);
-    r0 = sqrt(r * r + z0 * z0);
-    g.r = r;
-    g.a = {z0 / r0, -dz / r0};
-    g.b = {dy / r0, -dx / r0};
-    g.fc = 0.5 * (1.0 + cos(kPi * r / rc));
-    g.dfc = -kPi / (2.0 * rc) * sin(kPi * r / rc);
-}
-
-// d a / d dr_k, d b / d dr_k (mdkk/snap/compute.py:48-63).
-__device__ __forceinline__ void pair_grads(const double d[3], const PairGeo& g, double rc, double z0, double r0,
-                                           cplx da[3], cplx db[3]) {
-    const double r = g.r, ct = 0.99 * kPi / rc;
-    const double dz0_dr = z0 / r - ct * (r * r + z0 * z0) / r;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        const double dz0 = dz0_dr * (d[k] / r);
-        const double dr0 = (d[k] + z0 * dz0) / r0;
-        da[k] = {dz0 / r0 - g.a.re * dr0 / r0, (k == 2 ? -1.0 / r0 : 0.0) - g.a.im * dr0 / r0};
-        db[k] = {(k == 1 ? 1.0 / r0 : 0.0) - g.b.re * dr0 / r0, (k == 0 ? -1.0 / r0 : 0.0) - g.b.im * dr0 / r0};
-    }
-}
-
-// Two-term column recursion for the Wigner-U levels (levels column-major: v[Q*tj + P]).  With level 1 =
-// [[conj(a), -conj(b)], [b, a]] (mdkk/snap/compute.py:125-147), every column
-// Q < tj of level tj follows from column Q of level tj-1:
-//   u[P][Q] = sqrt((tj-P)/(tj-Q)) conj(a) v[P][Q] + sqrt(P/(tj-Q)) b v[P-1][Q]
-// (the same matrices as the reference's four-term recursion, half the
-// products; checked against it to ~1e-16 in the parity tests).  The right
-// half of each level follows from the mirror X[tj-P][tj-Q] = (-1)^(P+Q)
-// conj(X[P][Q]), so only the column half C_tj = {2Q < tj, or 2Q == tj and
-// 2P <= tj} is computed; it has half_size(tj) elements, enumerated column-major.
-// Branch-free at the column ends: the weights vanish there (sqrt(0) for P == tj
-// resp. P == 0) and the out-of-column operand is a finite neighbour (clamped
-// index, buffers zero-initialised), so both terms are always evaluated.
-__device__ __forceinline__ cplx rec2(const cplx* v, int tj, int P, int Q, const RS& rs, cplx ab, cplx b) {
-    const cplx v0 = v[Q * tj + P], v1 = v[max(Q * tj + P - 1, 0)];
-    const cplx t0 = cmul(ab, v0), t1 = cmul(b, v1);
-    const double w0 = rs.v[tj - P][tj - Q], w1 = rs.v[P][tj - Q];
-    return {fma(w0, t0.re, w1 * t1.re), fma(w0, t0.im, w1 * t1.im)};
-}
-
-__device__ __forceinline__ bool in_col_half(int tj, int P, int Q) {
-    return 2 * Q < tj || (2 * Q == tj && 2 * P <= tj);
-}
-
-// c-th element (column-major) of C_tj.
-__device__ __forceinline__ void col_elem(int tj, int c, int& P, int& Q) {
-    const int nfull = ((tj + 1) >> 1) * (tj + 1);
-    if (c < nfull) {
-        Q = c / (tj + 1);
-        P = c - Q * (tj + 1);
-    } else {
-        Q = tj >> 1;
-        P = c - nfull;
-    }
-}
-
-__device__ __forceinline__ bool neighbour(const double* x, const int* table, int cap, int i, int k, double4 xi,
-                                          double rc2, int& j, double& dx, double& dy, double& dz, double& r2) {
-    j = table[((long long)(i >> 5) * cap + k) * 32 + (i & 31)];
-    const double4 xj = mdkk::ld4(x, j);
-    dx = xj.x - xi.x;
-    dy = xj.y - xi.y;
-    dz = xj.z - xi.z;
-    r2 = mdkk::r2_exact(dx, dy, dz);
-    return r2 < rc2;  // mdkk/snap/compute.py:114-115 (strict)
-}
-
-// ---------------------------------------------- half-block helpers (both kernels)
-// Every level obeys X[tj-P][tj-Q] = (-1)^(P+Q) conj(X[P][Q]) (u, U, Y and the
-// adjoint lambda), so only the half set H_tj = {2P < tj, or 2P == tj
-// and 2Q <= tj} is computed: it is the row-major prefix P*(tj+1)+Q < half_size.
-__host__ __device__ constexpr int half_size(int tj) {
-    return (tj & 1) ? (tj + 1) * (tj + 1) / 2 : (tj / 2) * (tj + 1) + tj / 2 + 1;
-}
-__host__ __device__ constexpr int half_offset(int tj) {
-    int s = 0;
-    for (int t = 0; t < tj; ++t) s += half_size(t);
-    return s;
-}
-__host__ __device__ constexpr int half_slots(int tj) { return (half_size(tj) + 15) / 16; }
-__host__ __device__ constexpr int hslot_base(int tj) {
-    int s = 0;
-    for (int t = 0; t < tj; ++t) s += half_slots(t);
-    return s;
-}
-constexpr int kHSlots = hslot_base(kMaxTwoJ + 1);        // 14 per half-warp lane at 2J = 8
-constexpr int kHalfMax = half_size(kMaxTwoJ);            // 41
-constexpr int kHalfAll = half_offset(kMaxTwoJ + 1);      // 145
-
-// Store element (P, Q) of a full level held COLUMN-major in shared memory
-// (L[Q*(tj+1) + P]: lanes walk C_tj down a column, so reads and writes of a
-// half-warp hit consecutive 16-byte words) and its mirror.
-__device__ __forceinline__ void store_mirrored(cplx* L, int tj, int P, int Q, cplx v) {
-    L[Q * (tj + 1) + P] = v;
-    const int hm = (tj - Q) * (tj + 1) + (tj - P);
-    const double sg = ((P + Q) & 1) ? -1.0 : 1.0;
-    L[hm] = {sg * v.re, -sg * v.im};  // the center element writes itself twice (same value)
-}
-
-struct NbPair {
-    double dx, dy, dz, r2;
-    int j, pad;
-};
-
-// Compact the in-range partners (r^2 < rc^2, mdkk/snap/compute.py:114-115) of
-// table entries [k0, k0+32) of row i into s_nb; returns their count.
-__device__ __forceinline__ int compact_pairs(const double* x, const int* table, int cap, int i, int k0, int n,
-                                             double4 xi, double rc2, NbPair* s_nb, bool& bad) {
-    const int lane = threadIdx.x & 31, k = k0 + lane;
-    int j = 0;
-    double dx = 0, dy = 0, dz = 0, r2 = 0;
-    const bool ok = k < n && neighbour(x, table, cap, i, k, xi, rc2, j, dx, dy, dz, r2);
-    const unsigned m = __ballot_sync(0xffffffffu, ok);
-    if (ok) {
-        bad |= !(r2 > 0.0);
-        s_nb[__popc(m & ((1u << lane) - 1u))] = {dx, dy, dz, r2, j, 0};
-    }
-    __syncwarp();
-    return __popc(m);
-}
 
 // ---------------------------------------------------------------- compute_ui
 // U_i = sum_k f_c u(a_k, b_k) (mdkk/snap/compute.py:279-292), row-major U.
@@ -320,7 +128,6 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_snap_ui(const double* __rest
 constexpr int kYW = 16;                      // warps per CTA (2 CTAs per SM: 32 warps)
 constexpr int kUS = 33;                      // tile row stride (double2)
 
-__constant__ short c_hflat[kHalfAll];       // half index -> flat index
 
 template <int NF, int NH>
 __global__ void __launch_bounds__(kYW * 32, 2) k_snap_yi(const double2* __restrict__ U, int n,
@@ -562,34 +369,6 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_snap_deidrj(const double* __
         atomicAdd(p + 2, fi[2]);
     }
 }
-
-void upload_weights() {
-    static bool done = false;
-    if (done) return;
-    static double h[kMaxTwoJ + 1][kMaxTwoJ + 1] = {};
-    for (int k = 0; k <= kMaxTwoJ; ++k)
-        for (int l = 1; l <= kMaxTwoJ; ++l) h[k][l] = std::sqrt((double)k / (double)l);
-    cudaMemcpyToSymbol(g_rs, h, sizeof(h));
-    static short hf[kHalfAll];
-    for (int tj = 0; tj <= kMaxTwoJ; ++tj)
-        for (int k = 0; k < half_size(tj); ++k) hf[half_offset(tj) + k] = (short)(block_offset(tj) + k);
-    cudaMemcpyToSymbol(c_hflat, hf, sizeof(hf));
-    done = true;
-}
-
-// Launch a kernel template for the runtime 2J (0..8).
-#define MDKK_SNAP_DISPATCH(TWOJ_RT, KERNEL, GRID, BLOCK, STREAM, ...)                     \
-    switch (TWOJ_RT) {                                                                  \
-        case 0: KERNEL<0><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__); break;              \
-        case 1: KERNEL<1><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__); break;              \
-        case 2: KERNEL<2><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__); break;              \
-        case 3: KERNEL<3><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__); break;              \
-        case 4: KERNEL<4><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__); break;              \
-        case 5: KERNEL<5><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__); break;              \
-        case 6: KERNEL<6><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__); break;              \
-        case 7: KERNEL<7><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__); break;              \
-        default: KERNEL<8><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__); break;             \
-    }
 
 }  // namespace
 

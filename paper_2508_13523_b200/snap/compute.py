@@ -20,7 +20,7 @@ import torch
 
 from .. import _lib
 from ..memspace import DualArray, LayoutPolicy
-from .coupling import CouplingTables, device_product_list
+from .coupling import CouplingTables, bi_entries, device_product_list
 
 
 class SnapError(RuntimeError):
@@ -28,19 +28,68 @@ class SnapError(RuntimeError):
 
 
 class NeighborMap:
-    """The pairs of a full list with r < r_c, evaluated on the fly by the kernels (mdkk/snap/compute.py:66-119)."""
+    """The pairs of a full list with r < r_c (mdkk/snap/compute.py:66-119).
+
+    The engine kernels evaluate the pairs on the fly from the list; the
+    reference's per-pair arrays (`rows`, `cols`, `dr`, `r`, `a`, `b`, `fc`,
+    `dfc`, (row, dz, dy, dx) order) are materialised on the device on first
+    access (mdkk_snap_pair_count / _fill) for the staged path and for callers
+    that inspect them.
+    """
+
+    _FIELDS = ("rows", "cols", "dr", "r", "a", "b", "fc", "dfc")
 
     def __init__(self, store, nlist, r_c: float):
         self.store, self.nlist, self.r_c = store, nlist, float(r_c)
+        self._dev = None
+        self._host = {}
+
+    def device_arrays(self) -> dict:
+        """Per-pair device tensors (int32 rows/cols, f64 dr (P,3), r, complex128 a/b, fc, dfc)."""
+        if self._dev is None:
+            st, nl = self.store, self.nlist
+            dev = st.device
+            st.to_device()
+            n = st.n_local
+            npair = torch.zeros(n + 1, dtype=torch.int32, device=dev)
+            offs = torch.zeros(n + 1, dtype=torch.int32, device=dev)
+            flags = torch.zeros(1, dtype=torch.int32, device=dev)
+            lib, stream = _lib.lib(), _lib.stream(dev)
+            _lib.check(lib.mdkk_snap_pair_count(_lib.ctx(dev), st.x.data_ptr(), n, nl.table_dev.data_ptr(),
+                                                nl.counts_dev.data_ptr(), nl.alloc_cap, self.r_c,
+                                                npair.data_ptr(), offs.data_ptr(), flags.data_ptr(), stream),
+                       "mdkk_snap_pair_count")
+            if int(flags.item()) & _lib.FLAG_COINCIDENT:
+                raise SnapError("neighbor at zero distance")
+            P = int(offs[n].item())
+            m = max(P, 1)
+            d = dict(rows=torch.empty(m, dtype=torch.int32, device=dev),
+                     cols=torch.empty(m, dtype=torch.int32, device=dev),
+                     dr=torch.empty((m, 3), dtype=torch.float64, device=dev),
+                     r=torch.empty(m, dtype=torch.float64, device=dev),
+                     a=torch.empty(m, dtype=torch.complex128, device=dev),
+                     b=torch.empty(m, dtype=torch.complex128, device=dev),
+                     fc=torch.empty(m, dtype=torch.float64, device=dev),
+                     dfc=torch.empty(m, dtype=torch.float64, device=dev))
+            _lib.check(lib.mdkk_snap_pair_fill(st.x.data_ptr(), n, nl.table_dev.data_ptr(), nl.counts_dev.data_ptr(),
+                                               nl.alloc_cap, self.r_c, offs.data_ptr(),
+                                               *[d[k].data_ptr() for k in self._FIELDS], stream),
+                       "mdkk_snap_pair_fill")
+            self._dev = {k: v[:P] for k, v in d.items()}
+        return self._dev
 
     @property
     def n_pairs(self) -> int:
-        """Pairs within r_c (diagnostic, host sync)."""
-        st, nl = self.store, self.nlist
-        x = st.positions()
-        rows, cols, _, _ = nl.pairs()
-        d = x[cols] - x[rows]
-        return int((np.einsum("ij,ij->i", d, d) < self.r_c ** 2).sum())
+        return int(self.device_arrays()["rows"].shape[0])
+
+    def __getattr__(self, name):
+        if name in NeighborMap._FIELDS:
+            h = self._host.get(name)
+            if h is None:
+                t = self.device_arrays()[name].cpu().numpy()
+                h = self._host[name] = t.astype(np.int64) if name in ("rows", "cols") else t
+            return h
+        raise AttributeError(name)
 
 
 def build_neighbor_map(store, nlist, r_c: float) -> NeighborMap:
@@ -166,14 +215,44 @@ def compute_yi(state: SnapState) -> None:
     state._y_expanded = False
 
 
+def compute_bi_complex(state: SnapState) -> np.ndarray:
+    """Scalar invariants per atom and triple, complex (mdkk/snap/compute.py:354-367), on the GPU."""
+    B = _bi_device(state)
+    return B.cpu().numpy()
+
+
+def compute_bi(state: SnapState) -> np.ndarray:
+    """Descriptor vector: real part of the invariants (mdkk/snap/compute.py:370-373)."""
+    return compute_bi_complex(state).real
+
+
+def _bi_device(state: SnapState) -> torch.Tensor:
+    n_tri = len(state.tables.triples)
+    B = torch.zeros((max(state.n_atoms, 1), n_tri), dtype=torch.complex128, device=state.device)
+    if state.n_atoms == 0:
+        return B[:0]
+    tab = getattr(state, "_bi_tab", None)
+    if tab is None:
+        coef, code, tri, chunk = bi_entries(state.tables, int(_lib.lib().mdkk_snap_bi_warps()))
+        tab = state._bi_tab = [torch.from_numpy(v).to(state.device) for v in (coef, code, tri, chunk)]
+    state.U.sync("b")
+    _lib.check(_lib.lib().mdkk_snap_bi(state.handle().ptr, state.U_dev.data_ptr(), state.n_atoms,
+                                       *[t.data_ptr() for t in tab], n_tri, B.data_ptr(),
+                                       _lib.stream(state.device)), "mdkk_snap_bi")
+    return B[: state.n_atoms]
+
+
 def energy_from_y(state: SnapState) -> float:
     """Re(sum Y : conj(U)) / 3, accumulated by the yi kernel (mdkk/snap/compute.py:376-387)."""
     return float(state.energy_dev.item()) if state.n_atoms else 0.0
 
 
 def compute_energy(state: SnapState) -> float:
-    """E = sum beta . B; equal to the adjoint route to 1e-12 (mdkk tests/test_snap.py:364-372)."""
-    return energy_from_y(state)
+    """E = sum over atoms of beta . B, the descriptor route (mdkk/snap/compute.py:376-380)."""
+    if not state.n_atoms:
+        return 0.0
+    beta = torch.from_numpy(state.beta).to(state.device)
+    return float((_bi_device(state).real @ beta).sum().item())
 
 
 def deidrj_device(nmap: NeighborMap, state: SnapState, f: torch.Tensor) -> None:
@@ -190,4 +269,35 @@ def compute_fused_deidrj(nmap: NeighborMap, state: SnapState, n_total: int) -> n
     """All three force components in one pass over pairs (mdkk/snap/compute.py:390-409); host copy returned."""
     f = torch.zeros((max(n_total, 1), 4), dtype=torch.float64, device=state.device)
     deidrj_device(nmap, state, f)
+    return f[:n_total, :3].cpu().numpy()
+
+
+def compute_duidrj(nmap: NeighborMap, state: SnapState) -> np.ndarray:
+    """Staged path: d(f_c u)/d dr for every pair, (n_pairs, 3, n_flat) (mdkk/snap/compute.py:412-422)."""
+    return _duidrj_device(nmap, state).cpu().numpy()
+
+
+def _duidrj_device(nmap: NeighborMap, state: SnapState) -> torch.Tensor:
+    d = nmap.device_arrays()
+    P = d["rows"].shape[0]
+    out = torch.empty((max(P, 1), 3, state.index.n_flat), dtype=torch.complex128, device=state.device)
+    _lib.check(_lib.lib().mdkk_snap_duidrj(state.handle().ptr, P, d["dr"].data_ptr(), nmap.r_c, out.data_ptr(),
+                                           _lib.stream(state.device)), "mdkk_snap_duidrj")
+    return out[:P]
+
+
+def compute_deidrj(nmap: NeighborMap, state: SnapState, du, n_total: int) -> np.ndarray:
+    """Staged contraction of the derivatives against Y (mdkk/snap/compute.py:425-436)."""
+    d = nmap.device_arrays()
+    P = d["rows"].shape[0]
+    du_t = du if isinstance(du, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(du))
+    du_t = du_t.to(device=state.device, dtype=torch.complex128).contiguous()
+    if du_t.shape != (P, 3, state.index.n_flat):
+        raise SnapError(f"derivative block has shape {tuple(du_t.shape)}; expected {(P, 3, state.index.n_flat)}")
+    state.expand_y()
+    state.Y.sync("b")
+    f = torch.zeros((max(n_total, 1), 4), dtype=torch.float64, device=state.device)
+    _lib.check(_lib.lib().mdkk_snap_deidrj_staged(state.handle().ptr, P, d["rows"].data_ptr(), d["cols"].data_ptr(),
+                                                  state.Y_dev.data_ptr(), du_t.data_ptr(), f.data_ptr(),
+                                                  _lib.stream(state.device)), "mdkk_snap_deidrj_staged")
     return f[:n_total, :3].cpu().numpy()

@@ -322,3 +322,48 @@ def device_product_list(tables: CouplingTables, beta):
     _, fmap = half_block_outputs(tables.index.twojmax)
     return (np.ascontiguousarray(coef, dtype=np.float64), np.ascontiguousarray(code, dtype=np.int32), n_half,
             np.ascontiguousarray(fmap, dtype=np.int32))
+
+
+def bi_entries(tables: CouplingTables, n_warps: int):
+    """Descriptor terms for mdkk_snap_bi (include/mdkk_b200.h), per triple in storage order.
+
+    B_t = sum c U[iu1] U[iu2] conj(U[iz]) (mdkk/snap/compute.py:354-373) with
+    every operand on the half set: U[m] = s conj(U[half]); signs fold into c.
+    Returns (coef, code, tri, chunk) with chunk[w] the first term of warp w
+    (triple-aligned, balanced on term counts).
+    """
+    hmap, _ = _half_index(tables.index.twojmax)
+    off = tables.index.block_offset
+    inv = {}
+    for (tj, p, q), v in hmap.items():
+        inv[int(off[tj] + p * (tj + 1) + q)] = v
+    coef, code, tri = [], [], []
+    for t, (iz, i1, i2, c) in enumerate(tables.terms):
+        n = len(c)
+        for k in range(n):
+            g, cg_, sg = inv[int(i1[k])]
+            h, ch_, sh = inv[int(i2[k])]
+            z, mz, sz = inv[int(iz[k])]
+            cz = 0 if mz else 1          # conj(U[z]) = s U[half] when z is mirrored
+            sign = -1.0 if (sg ^ sh ^ sz) else 1.0
+            coef.append(sign * float(c[k]))
+            code.append(g | (h << 8) | (z << 16) | (cg_ << 24) | (ch_ << 25) | (cz << 26) | ((k == n - 1) << 27))
+            tri.append(t)
+        if n == 0:   # keep every triple's output written
+            coef.append(0.0)
+            code.append(1 << 27)
+            tri.append(t)
+    coef = np.asarray(coef, dtype=np.float64)
+    code = np.asarray(code, dtype=np.int64).astype(np.int32)
+    tri = np.asarray(tri, dtype=np.int32)
+    ends = np.flatnonzero((code >> 27) & 1) + 1
+    chunk = [0]
+    for w in range(1, n_warps):
+        target = len(coef) * w / n_warps
+        k = int(np.searchsorted(ends, target))
+        e = int(ends[min(k, len(ends) - 1)])
+        if k > 0 and abs(int(ends[k - 1]) - target) < abs(e - target):
+            e = int(ends[k - 1])
+        chunk.append(max(chunk[-1], e))
+    chunk.append(len(coef))
+    return coef, code, tri, np.asarray(chunk, dtype=np.int32)

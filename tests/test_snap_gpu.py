@@ -138,3 +138,77 @@ def test_snap_style_nve_matches_oracle(gpu, tmp_path):
         if step % 5 == 0:
             ref.append(e)
     assert np.allclose(rows[:, 1], ref, rtol=1e-10)
+
+
+# ---------------------------------------------------------------- API-parity stages
+def _state_for(pos, lengths, jmax, beta, rc, skin):
+    from paper_2508_13523_b200 import Box, RankedSystem, build_all
+    from paper_2508_13523_b200.snap import SnapState, build_neighbor_map, compute_ui, compute_yi, make_coupling_tables
+    system = RankedSystem.distribute(Box(lengths), 1, pos, np.zeros_like(pos))
+    (nl,) = build_all(system, rc, skin, style="full", newton=False)
+    store = system.stores[0]
+    nmap = build_neighbor_map(store, nl, rc)
+    state = SnapState(make_coupling_tables(jmax), store.n_local, beta)
+    compute_ui(nmap, state)
+    compute_yi(state)
+    return system, store, nmap, state
+
+
+def test_neighbor_map_arrays_match_reference_order(gpu):
+    """Pairs within r_c in (row, dz, dy, dx) order with unit-sphere a, b (mdkk tests/test_snap.py:305-323)."""
+    g = golden("snap.npz")
+    pos = g["j4_pos"]
+    system, store, nmap, _ = _state_for(pos, np.array([12.0] * 3), 2, g["j4_beta"], 1.9, 0.2)
+    o = osnap.SnapOracle(4, g["j4_beta"], 1.9)
+    rows, cols, _, _ = nmap.nlist.pairs()
+    x = store.positions()
+    r_rows, r_cols, r_dr = o.pairs_from_list(x, rows, cols)
+    assert nmap.n_pairs == len(r_rows)
+    assert np.array_equal(nmap.rows, r_rows) and np.array_equal(nmap.cols, r_cols)
+    assert np.array_equal(nmap.dr, r_dr)
+    assert np.all(nmap.r <= 1.9) and np.all(nmap.r > 0)
+    assert np.allclose(np.abs(nmap.a) ** 2 + np.abs(nmap.b) ** 2, 1.0, atol=1e-12)
+    r, a, b, fc, dfc, _, _ = osnap.pair_params(r_dr, 1.9)
+    assert np.allclose(nmap.a, a, rtol=0, atol=1e-14) and np.allclose(nmap.b, b, rtol=0, atol=1e-14)
+    assert np.allclose(nmap.fc, fc, rtol=1e-13, atol=1e-15) and np.allclose(nmap.dfc, dfc, rtol=1e-13, atol=1e-15)
+
+
+def test_staged_path_matches_oracle_and_fused(gpu):
+    """compute_duidrj == the reference's per-pair d(f_c u)/dr; staged == fused forces (mdkk tests/test_snap.py:465-478)."""
+    from paper_2508_13523_b200.snap import compute_deidrj, compute_duidrj, compute_fused_deidrj
+    g = golden("snap.npz")
+    bcc, L = md.lattice("bcc", 3.1803, (4, 4, 4))
+    cases = ((g["j4_pos"], np.array([12.0] * 3), 2, g["j4_beta"], 1.9, 0.2),
+             (md.jittered(bcc, 0.05, 2), L, 4, np.linspace(0.05, 0.1, 55), 4.73, 0.3))
+    for pos, lengths, jmax, beta, rc, skin in cases:
+        system, store, nmap, state = _state_for(pos, lengths, jmax, beta, rc, skin)
+        assert nmap.n_pairs > 0
+        du = compute_duidrj(nmap, state)
+        dr = nmap.dr
+        r, a, b, fc, dfc, z0, r0 = osnap.pair_params(dr, rc)
+        da, db = osnap.pair_grads(dr, r, rc, a, b, z0, r0)
+        u, dun = osnap.pair_levels(a, b, 2 * jmax, da, db)
+        wdu = fc[:, None, None] * dun + (dfc[:, None] * dr / r[:, None])[:, :, None] * u[:, None, :]
+        assert np.abs(du - wdu).max() <= 1e-12 * np.abs(wdu).max()
+        fused = compute_fused_deidrj(nmap, state, store.n_total)
+        staged = compute_deidrj(nmap, state, du, store.n_total)
+        assert np.abs(staged - fused).max() <= 1e-12 * max(1.0, np.abs(fused).max())
+
+
+def test_descriptors_and_energy_routes(gpu):
+    """compute_bi_complex vs the oracle's invariants; descriptor and adjoint energies agree
+    (mdkk tests/test_snap.py:328-372); imaginary residue negligible."""
+    from paper_2508_13523_b200.snap import compute_bi, compute_bi_complex, compute_energy, energy_from_y
+    pos, lengths = md.lattice("bcc", 3.1803, (10, 10, 10))
+    pos = md.jittered(pos, 0.05, 1)
+    beta = np.linspace(0.05, 0.1, 55)
+    system, store, nmap, state = _state_for(pos, lengths, 4, beta, 4.73, 0.3)
+    bc = compute_bi_complex(state)
+    o = osnap.SnapOracle(8, beta, 4.73)
+    U = state.u_view()
+    ref = np.stack([((c * U[:, i1]) * U[:, i2] * np.conj(U[:, iz])).sum(axis=1) for (iz, i1, i2, c) in o.terms], 1)
+    assert np.abs(bc - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max())
+    assert np.abs(bc.imag).max() < 1e-10 * max(1.0, np.abs(bc.real).max())
+    assert np.array_equal(compute_bi(state), bc.real)
+    assert compute_energy(state) == pytest.approx(energy_from_y(state), rel=1e-12)
+    assert compute_energy(state) == pytest.approx(65509.51457722162, rel=1e-12)   # SURVEY §8(c) KAT (3)
