@@ -148,6 +148,12 @@ int mdkk_max_disp2(const double* x, const double* x_ref, int n, double* out, voi
 int mdkk_lj_force(mdkk_ctx* ctx, const double* x, int n_local, const int* table, const int* counts,
                   int cap, int style, int newton, int virial, double epsilon, double sigma, double rc,
                   double* f, double* ev, int* flags, void* stream);
+/* Neighbour-parallel LJ (mode "neighbor", lj/cut/opt; mdkk/pair_lj.py:118-143): a
+ * team of 8 lanes per atom splits its list and reduces the partials; same
+ * arguments and results (to rounding) as mdkk_lj_force. */
+int mdkk_lj_force_neighbor(mdkk_ctx* ctx, const double* x, int n_local, const int* table, const int* counts,
+                           int cap, int style, int newton, int virial, double epsilon, double sigma, double rc,
+                           double* f, double* ev, int* flags, void* stream);
 
 /* ------------------------------------------------------------- integrator
  * Velocity Verlet (mdkk/driver/simulation.py:431-450) fused with the skin

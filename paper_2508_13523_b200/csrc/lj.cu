@@ -104,7 +104,121 @@ __global__ void __launch_bounds__(kBlock) k_lj(const double* __restrict__ x, int
     }
 }
 
+// Neighbour-parallel variant (mode "neighbor", the lj/cut/opt default,
+// mdkk/pair_lj.py:118-143 and mdkk/driver/simulation.py:148-149): a team of T
+// lanes per atom splits the atom's list (lane l takes entries l, l+T, ...)
+// and the partial force / energy / virial are reduced with shuffles.  T times
+// more threads for the same pairs: the small-N / low-occupancy regime.
+template <int STYLE, bool NEWTON, bool VIR, int T>
+__global__ void __launch_bounds__(kBlock) k_lj_team(const double* __restrict__ x, int n_local,
+                                                    const int* __restrict__ table, const int* __restrict__ counts,
+                                                    int cap, double eps4, double eps24, double sig2, double rc2,
+                                                    double* __restrict__ f, double* __restrict__ partials,
+                                                    int* __restrict__ flags) {
+    const int t = blockIdx.x * kBlock + threadIdx.x;
+    const int i = t / T, l = t % T;
+    double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+    double fx = 0.0, fy = 0.0, fz = 0.0;
+    const bool valid = i < n_local;
+    bool bad = false;
+    if (valid) {
+        const double4 xi = mdkk::ld4(x, i);
+        const int n = min(counts[i], cap);
+        const int* col = table + ((long long)(i >> 5) * cap) * 32 + (i & 31);
+        for (int k = l; k < n; k += T) {
+            const int j = __ldg(col + (long long)k * 32);
+            const double4 xj = mdkk::ld4(x, j);
+            const double dx = xj.x - xi.x, dy = xj.y - xi.y, dz = xj.z - xi.z;
+            const double r2 = mdkk::r2_exact(dx, dy, dz);
+            if (r2 < rc2) {
+                bad |= !(r2 > 0.0);
+                const double inv = 1.0 / r2;
+                const double s2 = sig2 * inv;
+                const double s6 = s2 * s2 * s2;
+                const double s12 = s6 * s6;
+                const double fp = eps24 * (2.0 * s12 - s6) * inv;
+                const bool wj = (STYLE == 1) && (NEWTON || j < n_local);
+                const double wgt = (STYLE == 0) ? 0.5 : ((NEWTON || j < n_local) ? 1.0 : 0.5);
+                const double gx = fp * dx, gy = fp * dy, gz = fp * dz;
+                fx -= gx;
+                fy -= gy;
+                fz -= gz;
+                if (wj) {
+                    double* fj = f + 4LL * j;
+                    atomicAdd(fj + 0, gx);
+                    atomicAdd(fj + 1, gy);
+                    atomicAdd(fj + 2, gz);
+                }
+                acc[0] += wgt * (eps4 * (s12 - s6));
+                if (VIR) {
+                    const double wf = wgt * fp;
+                    acc[1] += wf * (dx * dx);
+                    acc[2] += wf * (dy * dy);
+                    acc[3] += wf * (dz * dz);
+                    acc[4] += wf * (dx * dy);
+                    acc[5] += wf * (dx * dz);
+                    acc[6] += wf * (dy * dz);
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int o = T / 2; o > 0; o >>= 1) {   // team reduction of the partial force
+        fx += __shfl_xor_sync(0xffffffffu, fx, o);
+        fy += __shfl_xor_sync(0xffffffffu, fy, o);
+        fz += __shfl_xor_sync(0xffffffffu, fz, o);
+    }
+    if (valid && l == 0) {
+        if (STYLE == 0) {
+            mdkk::st4(f, i, make_double4(fx, fy, fz, 0.0));
+        } else {
+            double* fi = f + 4LL * i;
+            atomicAdd(fi + 0, fx);
+            atomicAdd(fi + 1, fy);
+            atomicAdd(fi + 2, fz);
+        }
+    }
+    if (bad) atomicOr(flags, MDKK_FLAG_COINCIDENT);
+    if (VIR) {
+        mdkk::block_sum<7, kBlock>(acc, partials + 7LL * blockIdx.x);
+    } else {
+        double e1[1] = {acc[0]};
+        mdkk::block_sum<1, kBlock>(e1, partials + blockIdx.x);
+    }
+}
+
 }  // namespace
+
+extern "C" int mdkk_lj_force_neighbor(mdkk_ctx* ctx, const double* x, int n_local, const int* table,
+                                      const int* counts, int cap, int style, int newton, int virial, double epsilon,
+                                      double sigma, double rc, double* f, double* ev, int* flags, void* stream) {
+    if (!ctx || n_local < 0 || cap < 1 || (style != 0 && style != 1)) return MDKK_E_ARG;
+    cudaStream_t s = mdkk::as_stream(stream);
+    if (n_local == 0) {
+        cudaMemsetAsync(ev, 0, 7 * sizeof(double), s);
+        return MDKK_OK;
+    }
+    constexpr int T = 8;
+    const int nb = mdkk::grid_for((long long)n_local * T, kBlock);
+    double* partials = static_cast<double*>(mdkk::scratch(ctx, sizeof(double) * 7 * (size_t)nb));
+    if (!partials) return mdkk::cuda_fail(cudaErrorMemoryAllocation, "scratch");
+    const double e4 = 4.0 * epsilon, e24 = 24.0 * epsilon, s2 = sigma * sigma, rc2 = rc * rc;
+#define MDKK_LJT(ST, NW, VR) \
+    k_lj_team<ST, NW, VR, T><<<nb, kBlock, 0, s>>>(x, n_local, table, counts, cap, e4, e24, s2, rc2, f, partials, flags)
+    if (style == 0) {
+        if (virial) MDKK_LJT(0, false, true); else MDKK_LJT(0, false, false);
+    } else if (newton) {
+        if (virial) MDKK_LJT(1, true, true); else MDKK_LJT(1, true, false);
+    } else {
+        if (virial) MDKK_LJT(1, false, true); else MDKK_LJT(1, false, false);
+    }
+#undef MDKK_LJT
+    MDKK_CHECK_LAUNCH("k_lj_team");
+    if (!virial) cudaMemsetAsync(ev, 0, 7 * sizeof(double), s);
+    mdkk::reduce_partials(partials, nb, virial ? 7 : 1, ev, s);
+    MDKK_CHECK_LAUNCH("k_reduce_partials");
+    return MDKK_OK;
+}
 
 extern "C" int mdkk_lj_force(mdkk_ctx* ctx, const double* x, int n_local, const int* table, const int* counts,
                              int cap, int style, int newton, int virial, double epsilon, double sigma, double rc,

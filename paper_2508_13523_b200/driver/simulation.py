@@ -92,7 +92,8 @@ class LJStyle:
         evs, flags = self._evs, self._flags
         half = False
         for k, (s, nl) in enumerate(zip(system.stores, lists)):
-            lj_force_rank(s, nl, self.kernel.params, evs[k], flags, virial=False)
+            lj_force_rank(s, nl, self.kernel.params, evs[k], flags, virial=False,
+                          mode=config.mode or self.default_mode)
             half |= nl.style == "half"
         if half:   # collective in the distributed system: every rank calls it
             system.reverse_comm()

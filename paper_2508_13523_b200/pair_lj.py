@@ -90,7 +90,7 @@ class PairResult:
 
 
 def lj_force_rank(store, nl: NeighborList, params: PairParams, ev: torch.Tensor, flags: torch.Tensor,
-                  zero: bool = True, virial: bool = True) -> None:
+                  zero: bool = True, virial: bool = True, mode: str = "atom") -> None:
     """One rank's kernel launch (no host sync).
 
     Ghost force rows are zero outside a force evaluation (migrate zeroes all
@@ -101,19 +101,24 @@ def lj_force_rank(store, nl: NeighborList, params: PairParams, ev: torch.Tensor,
     dev = store.device
     if zero and nl.style == "half":
         store.f.zero_()
-    _lib.check(_lib.lib().mdkk_lj_force(
+    # mode "atom": one thread per owned atom; "neighbor": a team of lanes per atom
+    # splitting its list (mdkk/pair_lj.py:118-143)
+    fn = "mdkk_lj_force_neighbor" if mode == "neighbor" else "mdkk_lj_force"
+    _lib.check(getattr(_lib.lib(), fn)(
         _lib.ctx(dev), store.x.data_ptr(), store.n_local, nl.table_dev.data_ptr(), nl.counts_dev.data_ptr(),
         nl.alloc_cap, STYLES[nl.style], int(nl.newton), int(virial), params.epsilon, params.sigma, params.r_c,
-        store.f.data_ptr(), ev.data_ptr(), flags.data_ptr(), _lib.stream(dev)), "mdkk_lj_force")
+        store.f.data_ptr(), ev.data_ptr(), flags.data_ptr(), _lib.stream(dev)), fn)
 
 
 def compute_pair(kernel, system: RankedSystem, lists: list[NeighborList], mode: str = "atom", strategy=None,
                  n_workers: int | None = None, zero_forces: bool = True, check: bool = True) -> PairResult:
     """Evaluate the LJ kernel over every rank's list (mdkk/pair_lj.py:114-179).
 
-    `mode` / `strategy` / `n_workers` are accepted for signature parity; the
-    GPU schedule is one thread per owned atom and the write-deconfliction is
-    fixed by the list style.  `check=False` (engine-internal) skips the
+    `mode` picks the GPU schedule: "atom" = one thread per owned atom,
+    "neighbor" = a team of lanes per atom over its list (the reference's
+    mid-row split).  `strategy` / `n_workers` are accepted for signature
+    parity; the write-deconfliction is fixed by the list style (owner writes
+    for full lists, FP64 atomics for half lists).  `check=False` (engine-internal) skips the
     synchronous stale-list and coincident-atom checks; the error word is then
     read when the result is first inspected.
     """
@@ -132,7 +137,7 @@ def compute_pair(kernel, system: RankedSystem, lists: list[NeighborList], mode: 
             nl.check_current()
         store.to_device()
         half |= nl.style == "half"
-        lj_force_rank(store, nl, params, evs[k], flags)
+        lj_force_rank(store, nl, params, evs[k], flags, mode=mode)
         store.device_wrote(force=True)
     if half and any(s.n_ghost for s in system.stores):
         system.reverse_comm()

@@ -261,3 +261,41 @@ def test_large_multirank_partition_and_migrate(gpu):
     t_mig = time.perf_counter() - t0
     assert sum(s.n_local for s in system.stores) == len(pos)
     assert t_dist < 5.0 and t_mig < 5.0, (t_dist, t_mig)
+
+
+def test_configuration_grid_modes_styles_ranks(gpu):
+    """mdkk tests/test_acceptance.py:62-89: every (mode, list style, newton, ranks)
+    combination agrees with the O(N^2) oracle (E, F, W at 1e-12)."""
+    from paper_2508_13523_b200 import LJCut, PairParams, build_all, compute_pair
+    pos, lengths = md.random_config(700, 0.75, seed=4242)
+    e_ref, f_ref, w_ref = md.lj_reference_n2(pos, lengths, 1.0, 1.0, 2.0)
+    for mode in ("atom", "neighbor"):
+        for style, newton in (("full", False), ("full", True), ("half", True), ("half", False)):
+            for ranks in (1, 2, 4):
+                system = _mk(pos, lengths, ranks)
+                lists = build_all(system, 2.0, 0.3, style=style, newton=newton)
+                res = compute_pair(LJCut(PairParams(1.0, 1.0, 2.0)), system, lists, mode=mode)
+                tag = (mode, style, newton, ranks)
+                assert res.energy == pytest.approx(e_ref, rel=1e-12), tag
+                assert np.allclose(res.forces, f_ref, rtol=1e-12, atol=1e-10), tag
+                assert np.allclose(res.virial, w_ref, rtol=1e-12, atol=1e-10), tag
+
+
+def test_lj_cut_opt_style_runs_neighbor_mode(gpu):
+    """lj/cut/opt resolves to the neighbour-parallel schedule and reproduces lj/cut's run."""
+    from paper_2508_13523_b200.driver import RunConfig, run_script
+    base = ("units lj\nboundary p p p\nlattice fcc 0.8442\ncreate_box 6 6 6\ncreate_atoms\nmass 1.0\n"
+            "velocity 1.44 87287\npair_style {}\npair_coeff 1.0 1.0\ntimestep 0.005\nthermo 10\nrun 30\n")
+    a = run_script(base.format("lj/cut 2.5"), RunConfig(), log=None)
+    b = run_script(base.format("lj/cut/opt 2.5"), RunConfig(), log=None)
+    assert b.style.name == "lj/cut/opt" and b.style.default_mode == "neighbor"
+    assert np.allclose(np.array(b.results[-1].rows)[:, 1:], np.array(a.results[-1].rows)[:, 1:], rtol=1e-10)
+
+
+def test_saturation_harness_small_sizes(gpu):
+    """The saturation harness (mdkk/driver/bench.py:105-148) runs both potentials on the GPU
+    and reports positive, size-ordered rows (the full sweep is tools/saturation.py)."""
+    from paper_2508_13523_b200.driver.bench import bench_saturation
+    for pot in ("lj", "snap"):
+        res = bench_saturation(pot, [1000, 4096], reps=1, target_time=0.02)
+        assert list(res.sizes) == [1000, 4096] and np.all(res.rates > 0)
