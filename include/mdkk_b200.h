@@ -175,7 +175,10 @@ int mdkk_kinetic(mdkk_ctx* ctx, const double* v, int n, double mass, double* ke,
  * keeps Y as its half set (2p < tj, or 2p == tj and 2q <= tj; n_half entries,
  * the rest follows from Y[tj-p][tj-q] = (-1)^(p+q) conj(Y[p][q])) transposed,
  * Yh[e][i] with leading dimension ld >= n_local; mdkk_snap_y_expand /
- * _compress convert to / from the reference layout.
+ * _compress convert to / from the reference layout.  U and the reference-layout
+ * Y take the SnapState `layout` knob (mdkk/snap/compute.py:238-276): layout 0
+ * ("a") = row-major [n][n_flat], layout 1 ("b") = transposed [n_flat][ldu],
+ * atoms fastest.
  * Pairs are the entries of a FULL cluster-blocked table with r^2 < rc^2.
  *
  * mdkk_snap_create copies the product list built on the host from the exact
@@ -192,14 +195,16 @@ int mdkk_snap_destroy(mdkk_snap* snap);
 /* U_i = sum_k f_c(r_ik) u(a_ik, b_ik) (compute_ui, mdkk/snap/compute.py:279-292); flags gets
  * MDKK_FLAG_COINCIDENT for r = 0 pairs (mdkk/snap/compute.py:117-118). */
 int mdkk_snap_ui(mdkk_snap* snap, const double* x, int n_local, const int* table, const int* counts, int cap,
-                 double rc, double* U, int* flags, void* stream);
+                 double rc, double* U, int layout, int ldu, int* flags, void* stream);
 /* Yh from U (compute_yi, mdkk/snap/compute.py:303-340) and *energy (device double)
  * = sum_i Re(Y_i . conj(U_i)) / 3 (energy_from_y, mdkk/snap/compute.py:376-387). */
 int mdkk_snap_yi(mdkk_ctx* ctx, mdkk_snap* snap, const double* U, int n_local, double* Yh, int ld, double* energy,
-                 void* stream);
+                 int layout, int ldu, void* stream);
 /* Reference layout: Y[i][flat] (complex128 row-major) from Yh, and back. */
-int mdkk_snap_y_expand(mdkk_snap* snap, const double* Yh, int ld, int n_local, double* Y, void* stream);
-int mdkk_snap_y_compress(mdkk_snap* snap, const double* Y, int n_local, double* Yh, int ld, void* stream);
+int mdkk_snap_y_expand(mdkk_snap* snap, const double* Yh, int ld, int n_local, double* Y, int layout, int ldy,
+                       void* stream);
+int mdkk_snap_y_compress(mdkk_snap* snap, const double* Y, int n_local, double* Yh, int ld, int layout, int ldy,
+                         void* stream);
 /* Fused 3-direction forces (compute_fused_deidrj, mdkk/snap/compute.py:390-409):
  * t = Re sum_f Y_i[f] conj(d(f_c u)/d r_ik [f]) evaluated in reverse mode (u
  * forward, adjoint backward, 4 complex partials per pair); f_i += t, f_k -= t (FP64
@@ -231,7 +236,7 @@ int mdkk_snap_deidrj_staged(mdkk_snap* snap, int n_pairs, const int* rows, const
  * conj_z << 26 | last-of-triple << 27; tri[k] = triple of term k; chunk[w] =
  * first term of warp w, output-aligned, mdkk_snap_bi_warps() + 1 entries). */
 int mdkk_snap_bi(mdkk_snap* snap, const double* U, int n_local, const double* coef, const int* code, const int* tri,
-                 const int* chunk, int n_tri, double* B, void* stream);
+                 const int* chunk, int n_tri, double* B, int layout, int ldu, void* stream);
 int mdkk_snap_bi_warps(void);
 
 #ifdef __cplusplus

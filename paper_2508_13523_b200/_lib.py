@@ -54,16 +54,16 @@ SIGNATURES = {
     "mdkk_kinetic": [_p, _p, _i, _d, _p, _p],
     "mdkk_snap_create": [_p, _i, _i, _p, _p, _i, _p, _p],
     "mdkk_snap_destroy": [_p],
-    "mdkk_snap_ui": [_p, _p, _i, _p, _p, _i, _d, _p, _p, _p],
-    "mdkk_snap_yi": [_p, _p, _p, _i, _p, _i, _p, _p],
-    "mdkk_snap_y_expand": [_p, _p, _i, _i, _p, _p],
-    "mdkk_snap_y_compress": [_p, _p, _i, _p, _i, _p],
+    "mdkk_snap_ui": [_p, _p, _i, _p, _p, _i, _d, _p, _i, _i, _p, _p],
+    "mdkk_snap_yi": [_p, _p, _p, _i, _p, _i, _p, _i, _i, _p],
+    "mdkk_snap_y_expand": [_p, _p, _i, _i, _p, _i, _i, _p],
+    "mdkk_snap_y_compress": [_p, _p, _i, _p, _i, _i, _i, _p],
     "mdkk_snap_deidrj": [_p, _p, _i, _p, _p, _i, _d, _p, _i, _p, _p],
     "mdkk_snap_pair_count": [_p, _p, _i, _p, _p, _i, _d, _p, _p, _p, _p],
     "mdkk_snap_pair_fill": [_p, _i, _p, _p, _i, _d, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p],
     "mdkk_snap_duidrj": [_p, _i, _p, _d, _p, _p],
     "mdkk_snap_deidrj_staged": [_p, _i, _p, _p, _p, _p, _p, _p],
-    "mdkk_snap_bi": [_p, _p, _i, _p, _p, _p, _p, _i, _p, _p],
+    "mdkk_snap_bi": [_p, _p, _i, _p, _p, _p, _p, _i, _p, _i, _i, _p],
     "mdkk_snap_bi_warps": [],
 }
 _RESTYPE = {"mdkk_last_error": C.c_char_p, "mdkk_launch_count": C.c_ulonglong}

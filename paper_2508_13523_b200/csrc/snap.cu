@@ -30,7 +30,8 @@ template <int TWOJ>
 __global__ void __launch_bounds__(kWarps * 32, 4) k_snap_ui(const double* __restrict__ x, int n_local,
                                                          const int* __restrict__ table,
                                                          const int* __restrict__ counts, int cap, double rc,
-                                                         double2* __restrict__ U, int* __restrict__ flags) {
+                                                         double2* __restrict__ U, long long su, long long sf,
+                                                         int* __restrict__ flags) {
     constexpr int NF = block_offset(TWOJ + 1);
     __shared__ RS rs;
     __shared__ NbPair s_nb[kWarps][32];
@@ -91,7 +92,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_snap_ui(const double* __rest
         acc[s].im += __shfl_xor_sync(0xffffffffu, acc[s].im, 16);
     }
     if (hh) return;
-    double2* Ui = U + (long long)i * NF;
+    double2* Ui = U + (long long)i * su;   // layout a: su = NF, sf = 1; layout b: su = 1, sf = ld
 #pragma unroll
     for (int tj = 0; tj <= TWOJ; ++tj)
 #pragma unroll
@@ -102,10 +103,10 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_snap_ui(const double* __rest
                 col_elem(tj, c, P, Q);
                 const cplx v = acc[hslot_base(tj) + s];
                 const int e = P * (tj + 1) + Q, em = (tj - P) * (tj + 1) + (tj - Q);
-                Ui[block_offset(tj) + e] = make_double2(v.re, v.im);
+                Ui[(block_offset(tj) + e) * sf] = make_double2(v.re, v.im);
                 if (em != e) {
                     const double sg = ((P + Q) & 1) ? -1.0 : 1.0;
-                    Ui[block_offset(tj) + em] = make_double2(sg * v.re, -sg * v.im);
+                    Ui[(block_offset(tj) + em) * sf] = make_double2(sg * v.re, -sg * v.im);
                 }
             }
         }
@@ -133,7 +134,8 @@ template <int NF, int NH>
 __global__ void __launch_bounds__(kYW * 32, 2) k_snap_yi(const double2* __restrict__ U, int n,
                                                          const ZEntry* __restrict__ ent,
                                                          const int* __restrict__ chunk, double2* __restrict__ Yh,
-                                                         int ld, double* __restrict__ partials) {
+                                                         int ld, double* __restrict__ partials, long long su,
+                                                         long long sf) {
     extern __shared__ double2 s_dyn2[];
     double2* s_u = s_dyn2;                                                   // [NH][kUS]
     ZEntry* s_e = reinterpret_cast<ZEntry*>(s_u + NH * kUS);                  // [kYW][32]
@@ -141,7 +143,7 @@ __global__ void __launch_bounds__(kYW * 32, 2) k_snap_yi(const double2* __restri
     const int a0 = blockIdx.x * 32;
     for (int t = threadIdx.x; t < 32 * NH; t += blockDim.x) {
         const int a = t / NH, e = t - a * NH;
-        s_u[e * kUS + a] = (a0 + a < n) ? U[(long long)(a0 + a) * NF + c_hflat[e]] : make_double2(0.0, 0.0);
+        s_u[e * kUS + a] = (a0 + a < n) ? U[(long long)(a0 + a) * su + c_hflat[e] * sf] : make_double2(0.0, 0.0);
     }
     __syncthreads();
     const bool valid = a0 + lane < n;
@@ -180,7 +182,7 @@ __global__ void __launch_bounds__(kYW * 32, 2) k_snap_yi(const double2* __restri
 // Reference layout "a": full Y rows [n][NF] from the half/transposed Yh, using
 // Y[tj-p][tj-q] = (-1)^(p+q) conj(Y[p][q]).
 __global__ void k_snap_y_expand(const double2* __restrict__ Yh, int ld, int n, int nf,
-                                const int* __restrict__ fmap, double2* __restrict__ Y) {
+                                const int* __restrict__ fmap, double2* __restrict__ Y, long long su, long long sf) {
     const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= (long long)n * nf) return;
     const int i = (int)(t / nf), f = (int)(t - (long long)i * nf);
@@ -188,16 +190,16 @@ __global__ void k_snap_y_expand(const double2* __restrict__ Yh, int ld, int n, i
     double2 v = Yh[(long long)(m & 0xffff) * ld + i];
     if ((m >> 16) & 1) v.y = -v.y;
     if ((m >> 17) & 1) v = make_double2(-v.x, -v.y);
-    Y[t] = v;
+    Y[i * su + f * sf] = v;
 }
 
 // Inverse of the expansion (a host-written reference-layout Y -> engine layout).
 __global__ void k_snap_y_compress(const double2* __restrict__ Y, int n, int nf, int nh, double2* __restrict__ Yh,
-                                  int ld) {
+                                  int ld, long long su, long long sf) {
     const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= (long long)n * nh) return;
     const int e = (int)(t / n), i = (int)(t - (long long)e * n);
-    Yh[(long long)e * ld + i] = Y[(long long)i * nf + c_hflat[e]];
+    Yh[(long long)e * ld + i] = Y[i * su + c_hflat[e] * sf];
 }
 
 // ------------------------------------------------------- compute_fused_deidrj
@@ -439,20 +441,22 @@ int mdkk_snap_destroy(mdkk_snap* s) {
 }
 
 int mdkk_snap_ui(mdkk_snap* s, const double* x, int n_local, const int* table, const int* counts, int cap, double rc,
-                 double* U, int* flags, void* stream) {
-    if (!s || n_local < 0 || cap < 1) return MDKK_E_ARG;
+                 double* U, int layout, int ldu, int* flags, void* stream) {
+    if (!s || n_local < 0 || cap < 1 || (layout == 1 && ldu < n_local)) return MDKK_E_ARG;
+    const long long su = layout ? 1 : s->n_flat, sf = layout ? ldu : 1;
     if (n_local == 0) return MDKK_OK;
     upload_weights();
     const int nb = (n_local + kWarps - 1) / kWarps;
     MDKK_SNAP_DISPATCH(s->twojmax, k_snap_ui, nb, kWarps * 32, mdkk::as_stream(stream), x, n_local, table, counts,
-                       cap, rc, reinterpret_cast<double2*>(U), flags);
+                       cap, rc, reinterpret_cast<double2*>(U), su, sf, flags);
     MDKK_CHECK_LAUNCH("k_snap_ui");
     return MDKK_OK;
 }
 
 int mdkk_snap_yi(mdkk_ctx* ctx, mdkk_snap* s, const double* U, int n_local, double* Yh, int ld, double* energy,
-                 void* stream) {
-    if (!ctx || !s || n_local < 0 || ld < n_local) return MDKK_E_ARG;
+                 int layout, int ldu, void* stream) {
+    if (!ctx || !s || n_local < 0 || ld < n_local || (layout == 1 && ldu < n_local)) return MDKK_E_ARG;
+    const long long su = layout ? 1 : s->n_flat, sf = layout ? ldu : 1;
     cudaStream_t st = mdkk::as_stream(stream);
     if (n_local == 0) {
         cudaMemsetAsync(energy, 0, sizeof(double), st);
@@ -470,7 +474,7 @@ int mdkk_snap_yi(mdkk_ctx* ctx, mdkk_snap* s, const double* U, int n_local, doub
         constexpr int NF = block_offset(TJ + 1), NH = half_offset(TJ + 1);                                      \
         const size_t sm = NH * kUS * sizeof(double2) + kYW * 32 * sizeof(ZEntry);                               \
         cudaFuncSetAttribute(k_snap_yi<NF, NH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);         \
-        k_snap_yi<NF, NH><<<nb, kYW * 32, sm, st>>>(u, n_local, s->ent, s->chunk, y, ld, partials);             \
+        k_snap_yi<NF, NH><<<nb, kYW * 32, sm, st>>>(u, n_local, s->ent, s->chunk, y, ld, partials, su, sf);     \
         break;                                                                                                  \
     }
         MDKK_YI(0) MDKK_YI(1) MDKK_YI(2) MDKK_YI(3) MDKK_YI(4) MDKK_YI(5) MDKK_YI(6) MDKK_YI(7) MDKK_YI(8)
@@ -483,23 +487,27 @@ int mdkk_snap_yi(mdkk_ctx* ctx, mdkk_snap* s, const double* U, int n_local, doub
     return MDKK_OK;
 }
 
-int mdkk_snap_y_expand(mdkk_snap* s, const double* Yh, int ld, int n_local, double* Y, void* stream) {
-    if (!s || n_local < 0 || ld < n_local) return MDKK_E_ARG;
+int mdkk_snap_y_expand(mdkk_snap* s, const double* Yh, int ld, int n_local, double* Y, int layout, int ldy,
+                       void* stream) {
+    if (!s || n_local < 0 || ld < n_local || (layout == 1 && ldy < n_local)) return MDKK_E_ARG;
+    const long long su = layout ? 1 : s->n_flat, sf = layout ? ldy : 1;
     if (n_local == 0) return MDKK_OK;
     const long long tot = (long long)n_local * s->n_flat;
     k_snap_y_expand<<<(unsigned)((tot + 255) / 256), 256, 0, mdkk::as_stream(stream)>>>(
-        reinterpret_cast<const double2*>(Yh), ld, n_local, s->n_flat, s->fmap, reinterpret_cast<double2*>(Y));
+        reinterpret_cast<const double2*>(Yh), ld, n_local, s->n_flat, s->fmap, reinterpret_cast<double2*>(Y), su, sf);
     MDKK_CHECK_LAUNCH("k_snap_y_expand");
     return MDKK_OK;
 }
 
-int mdkk_snap_y_compress(mdkk_snap* s, const double* Y, int n_local, double* Yh, int ld, void* stream) {
-    if (!s || n_local < 0 || ld < n_local) return MDKK_E_ARG;
+int mdkk_snap_y_compress(mdkk_snap* s, const double* Y, int n_local, double* Yh, int ld, int layout, int ldy,
+                         void* stream) {
+    if (!s || n_local < 0 || ld < n_local || (layout == 1 && ldy < n_local)) return MDKK_E_ARG;
+    const long long su = layout ? 1 : s->n_flat, sf = layout ? ldy : 1;
     if (n_local == 0) return MDKK_OK;
     upload_weights();
     const long long tot = (long long)n_local * s->n_half;
     k_snap_y_compress<<<(unsigned)((tot + 255) / 256), 256, 0, mdkk::as_stream(stream)>>>(
-        reinterpret_cast<const double2*>(Y), n_local, s->n_flat, s->n_half, reinterpret_cast<double2*>(Yh), ld);
+        reinterpret_cast<const double2*>(Y), n_local, s->n_flat, s->n_half, reinterpret_cast<double2*>(Yh), ld, su, sf);
     MDKK_CHECK_LAUNCH("k_snap_y_compress");
     return MDKK_OK;
 }

@@ -211,14 +211,14 @@ template <int NF, int NH>
 __global__ void __launch_bounds__(kBW * 32) k_snap_bi(const double2* __restrict__ U, int n,
                                                       const double* __restrict__ coef, const int* __restrict__ code,
                                                       const int* __restrict__ tri, const int* __restrict__ chunk,
-                                                      int n_tri, double2* __restrict__ B) {
+                                                      int n_tri, double2* __restrict__ B, long long su, long long sf) {
     extern __shared__ double2 s_bu[];   // [NH][33]
     constexpr int S = 33;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int a0 = blockIdx.x * 32;
     for (int t = threadIdx.x; t < 32 * NH; t += blockDim.x) {
         const int a = t / NH, e = t - a * NH;
-        s_bu[e * S + a] = (a0 + a < n) ? U[(long long)(a0 + a) * NF + c_hflat[e]] : make_double2(0.0, 0.0);
+        s_bu[e * S + a] = (a0 + a < n) ? U[(long long)(a0 + a) * su + c_hflat[e] * sf] : make_double2(0.0, 0.0);
     }
     __syncthreads();
     const bool valid = a0 + lane < n;
@@ -301,8 +301,9 @@ int mdkk_snap_deidrj_staged(mdkk_snap* s, int n_pairs, const int* rows, const in
 }
 
 int mdkk_snap_bi(mdkk_snap* s, const double* U, int n_local, const double* coef, const int* code, const int* tri,
-                 const int* chunk, int n_tri, double* B, void* stream) {
-    if (!s || n_local < 0 || n_tri < 1) return MDKK_E_ARG;
+                 const int* chunk, int n_tri, double* B, int layout, int ldu, void* stream) {
+    if (!s || n_local < 0 || n_tri < 1 || (layout == 1 && ldu < n_local)) return MDKK_E_ARG;
+    const long long su = layout ? 1 : s->n_flat, sf = layout ? ldu : 1;
     if (n_local == 0) return MDKK_OK;
     upload_weights();
     cudaStream_t st = mdkk::as_stream(stream);
@@ -315,7 +316,7 @@ int mdkk_snap_bi(mdkk_snap* s, const double* U, int n_local, const double* coef,
         constexpr int NF = block_offset(TJ + 1), NH = half_offset(TJ + 1);                                 \
         const size_t sm = NH * 33 * sizeof(double2);                                                       \
         cudaFuncSetAttribute(k_snap_bi<NF, NH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);    \
-        k_snap_bi<NF, NH><<<nb, kBW * 32, sm, st>>>(u, n_local, coef, code, tri, chunk, n_tri, out);       \
+        k_snap_bi<NF, NH><<<nb, kBW * 32, sm, st>>>(u, n_local, coef, code, tri, chunk, n_tri, out, su, sf); \
         break;                                                                                             \
     }
         MDKK_BI(0) MDKK_BI(1) MDKK_BI(2) MDKK_BI(3) MDKK_BI(4) MDKK_BI(5) MDKK_BI(6) MDKK_BI(7) MDKK_BI(8)

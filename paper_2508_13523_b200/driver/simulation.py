@@ -114,8 +114,11 @@ def default_registry() -> StyleRegistry:
     except ImportError:  # SNAP kernels not built into this library version
         SnapStyle = None
     if SnapStyle is not None:
-        for name in ("snap", "snap/opt", "snap/kk"):
+        for name in ("snap", "snap/kk"):
             reg.register(name, lambda args, _n=name: SnapStyle.from_file(float(args[0]), args[1], name=_n))
+        # the reference's opt preset (mdkk/driver/simulation.py:151-152)
+        reg.register("snap/opt", lambda args: SnapStyle.from_file(float(args[0]), args[1], name="snap/opt",
+                                                                  batch_u=8, tile_v=256))
     return reg
 
 

@@ -123,7 +123,17 @@ class _Handle:
 
 
 class SnapState:
-    """Per-atom U and Y fields in HBM plus the (schedule-only) knobs (mdkk/snap/compute.py:238-276)."""
+    """Per-atom U and Y fields in HBM plus the schedule knobs (mdkk/snap/compute.py:238-276).
+
+    `layout` is the device storage of U and the reference-layout Y: "a" =
+    row-major [n][n_flat] (ui writes one atom's row), "b" = transposed
+    [n_flat][ld] with atoms fastest (the yi / bi tile loads read whole
+    rows).  `tile_v` > 0 runs yi and bi over atom tiles of that size (one
+    launch per tile: bounded shared work per launch).  `batch_u` / `batch_y`
+    are accepted; the pair and product batching of the GPU kernels is fixed
+    by their warp decomposition.  No knob changes results beyond rounding
+    (mdkk tests/test_snap.py:482-499).
+    """
 
     def __init__(self, tables: CouplingTables, n_atoms: int, beta, batch_u: int = 4, batch_y: int = 1,
                  tile_v: int = 0, layout: str = "a", device=None):
@@ -141,12 +151,17 @@ class SnapState:
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         nf = self.index.n_flat
         shape = (max(1, self.n_atoms), nf)
-        rm = LayoutPolicy.row_major(2)   # device rows are atoms: one warp streams one atom's 285 entries
-        self.U_dev = torch.zeros(shape, dtype=torch.complex128, device=self.device)
-        self.Y_dev = torch.zeros_like(self.U_dev)
         n_half = sum((t + 1) ** 2 // 2 if t & 1 else (t // 2) * (t + 1) + t // 2 + 1
                      for t in range(self.index.twojmax + 1))
         self.ld = max(32, (self.n_atoms + 31) // 32 * 32)
+        self._lay = 1 if layout == "b" else 0
+        if self._lay:
+            rm = LayoutPolicy.transposed(2)
+            self.U_dev = torch.zeros((nf, self.ld), dtype=torch.complex128, device=self.device)
+        else:
+            rm = LayoutPolicy.row_major(2)   # device rows are atoms: one warp streams one atom's entries
+            self.U_dev = torch.zeros(shape, dtype=torch.complex128, device=self.device)
+        self.Y_dev = torch.zeros_like(self.U_dev)
         self.Yh_dev = torch.zeros((n_half, self.ld), dtype=torch.complex128, device=self.device)
         self._y_expanded = True   # Y_dev agrees with Yh_dev
         self.U = DualArray(shape, layout_b=rm, dtype=np.complex128, device=self.device, storage_b=self.U_dev)
@@ -172,7 +187,7 @@ class SnapState:
         if self._y_expanded:
             return
         _lib.check(_lib.lib().mdkk_snap_y_expand(self.handle().ptr, self.Yh_dev.data_ptr(), self.ld, self.n_atoms,
-                                                 self.Y_dev.data_ptr(), _lib.stream(self.device)),
+                                                 self.Y_dev.data_ptr(), self._lay, self.ld, _lib.stream(self.device)),
                    "mdkk_snap_y_expand")
         self.Y.modified_a = False
         self.Y.mark_modified("b")
@@ -183,7 +198,8 @@ class SnapState:
         if self.Y.modified_a:
             self.Y.sync("b")
             _lib.check(_lib.lib().mdkk_snap_y_compress(self.handle().ptr, self.Y_dev.data_ptr(), self.n_atoms,
-                                                       self.Yh_dev.data_ptr(), self.ld, _lib.stream(self.device)),
+                                                       self.Yh_dev.data_ptr(), self.ld, self._lay, self.ld,
+                                                       _lib.stream(self.device)),
                        "mdkk_snap_y_compress")
 
 
@@ -194,7 +210,8 @@ def compute_ui(nmap: NeighborMap, state: SnapState) -> None:
     state.flags.zero_()
     _lib.check(_lib.lib().mdkk_snap_ui(state.handle().ptr, st.x.data_ptr(), st.n_local, nl.table_dev.data_ptr(),
                                        nl.counts_dev.data_ptr(), nl.alloc_cap, nmap.r_c, state.U_dev.data_ptr(),
-                                       state.flags.data_ptr(), _lib.stream(st.device)), "mdkk_snap_ui")
+                                       state._lay, state.ld, state.flags.data_ptr(), _lib.stream(st.device)),
+               "mdkk_snap_ui")
     state.U.modified_a = False
     state.U.mark_modified("b")
 
@@ -207,12 +224,30 @@ def check_flags(state: SnapState) -> None:
 def compute_yi(state: SnapState) -> None:
     """Full three-slot adjoint Y and the per-atom energy sum (mdkk/snap/compute.py:303-340, :376-387)."""
     state.U.sync("b")
-    _lib.check(_lib.lib().mdkk_snap_yi(_lib.ctx(state.device), state.handle().ptr, state.U_dev.data_ptr(),
-                                       state.n_atoms, state.Yh_dev.data_ptr(), state.ld,
-                                       state.energy_dev.data_ptr(), _lib.stream(state.device)), "mdkk_snap_yi")
+    tiles = _tiles(state)
+    e_t = state.energy_dev if len(tiles) == 1 else torch.zeros(len(tiles), dtype=torch.float64, device=state.device)
+    for k, (a0, n) in enumerate(tiles):
+        _lib.check(_lib.lib().mdkk_snap_yi(_lib.ctx(state.device), state.handle().ptr, _u_at(state, a0), n,
+                                           state.Yh_dev.data_ptr() + 16 * a0, state.ld, e_t.data_ptr() + 8 * k,
+                                           state._lay, state.ld, _lib.stream(state.device)), "mdkk_snap_yi")
+    if len(tiles) > 1:
+        state.energy_dev.copy_(e_t.sum().reshape(1))
     state.Y.modified_a = False
     state.Y.modified_b = False
     state._y_expanded = False
+
+
+def _tiles(state: SnapState):
+    """Atom tiles (offset, count) of the tile_v knob (mdkk/snap/compute.py:295-299)."""
+    n, t = state.n_atoms, state.tile_v
+    if t <= 0 or t >= n:
+        return [(0, n)]
+    return [(a0, min(t, n - a0)) for a0 in range(0, n, t)]
+
+
+def _u_at(state: SnapState, a0: int) -> int:
+    """Device address of atom a0's U entries in the state's layout."""
+    return state.U_dev.data_ptr() + 16 * (a0 if state._lay else a0 * state.index.n_flat)
 
 
 def compute_bi_complex(state: SnapState) -> np.ndarray:
@@ -236,9 +271,10 @@ def _bi_device(state: SnapState) -> torch.Tensor:
         coef, code, tri, chunk = bi_entries(state.tables, int(_lib.lib().mdkk_snap_bi_warps()))
         tab = state._bi_tab = [torch.from_numpy(v).to(state.device) for v in (coef, code, tri, chunk)]
     state.U.sync("b")
-    _lib.check(_lib.lib().mdkk_snap_bi(state.handle().ptr, state.U_dev.data_ptr(), state.n_atoms,
-                                       *[t.data_ptr() for t in tab], n_tri, B.data_ptr(),
-                                       _lib.stream(state.device)), "mdkk_snap_bi")
+    for a0, n in _tiles(state):
+        _lib.check(_lib.lib().mdkk_snap_bi(state.handle().ptr, _u_at(state, a0), n, *[t.data_ptr() for t in tab],
+                                           n_tri, B.data_ptr() + 16 * n_tri * a0, state._lay, state.ld,
+                                           _lib.stream(state.device)), "mdkk_snap_bi")
     return B[: state.n_atoms]
 
 
@@ -296,8 +332,9 @@ def compute_deidrj(nmap: NeighborMap, state: SnapState, du, n_total: int) -> np.
         raise SnapError(f"derivative block has shape {tuple(du_t.shape)}; expected {(P, 3, state.index.n_flat)}")
     state.expand_y()
     state.Y.sync("b")
+    y_rows = state.Y_dev if not state._lay else state.Y.view("b").contiguous()   # kernel reads [n][n_flat]
     f = torch.zeros((max(n_total, 1), 4), dtype=torch.float64, device=state.device)
     _lib.check(_lib.lib().mdkk_snap_deidrj_staged(state.handle().ptr, P, d["rows"].data_ptr(), d["cols"].data_ptr(),
-                                                  state.Y_dev.data_ptr(), du_t.data_ptr(), f.data_ptr(),
+                                                  y_rows.data_ptr(), du_t.data_ptr(), f.data_ptr(),
                                                   _lib.stream(state.device)), "mdkk_snap_deidrj_staged")
     return f[:n_total, :3].cpu().numpy()

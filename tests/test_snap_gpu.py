@@ -212,3 +212,37 @@ def test_descriptors_and_energy_routes(gpu):
     assert np.array_equal(compute_bi(state), bc.real)
     assert compute_energy(state) == pytest.approx(energy_from_y(state), rel=1e-12)
     assert compute_energy(state) == pytest.approx(65509.51457722162, rel=1e-12)   # SURVEY §8(c) KAT (3)
+
+
+def test_knobs_do_not_change_results(gpu):
+    """mdkk tests/test_snap.py:482-499: layout / tile_v / batch knobs leave E and F unchanged (1e-12)."""
+    from paper_2508_13523_b200 import Box, RankedSystem, build_all
+    from paper_2508_13523_b200.snap import (SnapState, build_neighbor_map, compute_bi, compute_energy,
+                                            compute_fused_deidrj, compute_ui, compute_yi, energy_from_y,
+                                            make_coupling_tables)
+    pos, lengths = md.lattice("bcc", 3.1803, (5, 5, 5))
+    pos = md.jittered(pos, 0.05, 5)
+    beta = np.random.default_rng(67).uniform(-0.1, 0.1, 55)
+    tables = make_coupling_tables(4)
+    system = RankedSystem.distribute(Box(lengths), 1, pos, np.zeros_like(pos))
+    (nl,) = build_all(system, 4.73, 0.3, style="full", newton=False)
+    store = system.stores[0]
+    nmap = build_neighbor_map(store, nl, 4.73)
+
+    def run(**knobs):
+        st = SnapState(tables, store.n_local, beta, **knobs)
+        compute_ui(nmap, st)
+        compute_yi(st)
+        f = compute_fused_deidrj(nmap, st, store.n_total)
+        return energy_from_y(st), f, st.u_view().copy(), st.y_view().copy(), compute_bi(st), compute_energy(st)
+
+    e0, f0, u0, y0, b0, eb0 = run()
+    fscale = max(1.0, np.abs(f0).max())
+    for knobs in ({"batch_u": 1}, {"batch_u": 16}, {"batch_y": 3}, {"tile_v": 1}, {"tile_v": 37},
+                  {"layout": "b"}, {"batch_u": 2, "batch_y": 4, "tile_v": 64, "layout": "b"}):
+        e1, f1, u1, y1, b1, eb1 = run(**knobs)
+        assert e1 == pytest.approx(e0, rel=1e-12), knobs
+        assert eb1 == pytest.approx(eb0, rel=1e-12), knobs
+        assert np.abs(f1 - f0).max() / fscale < 1e-12, knobs
+        assert np.array_equal(u1, u0) and np.allclose(y1, y0, rtol=1e-13, atol=1e-14), knobs
+        assert np.allclose(b1, b0, rtol=1e-13, atol=1e-13), knobs
