@@ -239,6 +239,35 @@ int mdkk_snap_bi(mdkk_snap* snap, const double* U, int n_local, const double* co
                  const int* chunk, int n_tri, double* B, int layout, int ldu, void* stream);
 int mdkk_snap_bi_warps(void);
 
+/* ------------------------------------------------------------------- QEq
+ * Charge equilibration (mdkk/qeq.py): over-allocated CSR with int64 row
+ * offsets = exclusive scan of capacities min(counts, cap) + 1 (caps scratch
+ * [n+1], offsets [n+1]); values f64 / columns int32 / row_nnz int32; diagonal
+ * eta first, then list partners within the cutoff, value (r^3 + gamma^-3)^(-1/3),
+ * column = owner index (mdkk/qeq.py:41-133).  SpMV: y1 = H x1 and, when x2 is
+ * non-NULL, y2 = H x2 in the same traversal; dots (optional, device [2]) gets
+ * x1.y1 and x2.y2.  All reductions fixed-order: a fused two-system CG is
+ * bit-identical to two sequential solves (mdkk/qeq.py:233-274). */
+int mdkk_qeq_offsets(mdkk_ctx* ctx, const int* counts, int n, int cap, long long* caps, long long* offsets,
+                     void* stream);
+int mdkk_qeq_build(const double* x, int n_local, const int* table, const int* counts, int cap, const int* oidx,
+                   const long long* offsets, double eta, double gamma, double cutoff, double* values, int* columns,
+                   int* row_nnz, void* stream);
+int mdkk_qeq_spmv(mdkk_ctx* ctx, const long long* offsets, const double* values, const int* columns,
+                  const int* row_nnz, int n, const double* x1, const double* x2, double* y1, double* y2,
+                  double* dots, void* stream);
+/* Gershgorin guard (mdkk/qeq.py:180-194): *bad_row (device, caller-set to INT_MAX)
+ * gets the first row with diag <= sum |offdiag|; diag / offsum per row. */
+int mdkk_qeq_gershgorin(const long long* offsets, const double* values, const int* columns, const int* row_nnz, int n,
+                        int* bad_row, double* diag, double* offsum, void* stream);
+/* *out = a . b (device), fixed order. */
+int mdkk_dot(mdkk_ctx* ctx, const double* a, const double* b, int n, double* out, void* stream);
+/* CG stages (mdkk/qeq.py:197-207): alpha = *rr / *pap; x += alpha p; r -= alpha Ap;
+ * *rr_new = r . r; then p = r + (*rr_new / *rr) p. */
+int mdkk_cg_update(mdkk_ctx* ctx, int n, double* x, double* r, const double* p, const double* ap, const double* rr,
+                   const double* pap, double* rr_new, void* stream);
+int mdkk_cg_direction(int n, const double* r, double* p, const double* rr, const double* rr_new, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

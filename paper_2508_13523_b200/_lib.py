@@ -65,6 +65,13 @@ SIGNATURES = {
     "mdkk_snap_deidrj_staged": [_p, _i, _p, _p, _p, _p, _p, _p],
     "mdkk_snap_bi": [_p, _p, _i, _p, _p, _p, _p, _i, _p, _i, _i, _p],
     "mdkk_snap_bi_warps": [],
+    "mdkk_qeq_offsets": [_p, _p, _i, _i, _p, _p, _p],
+    "mdkk_qeq_build": [_p, _i, _p, _p, _i, _p, _p, _d, _d, _d, _p, _p, _p, _p],
+    "mdkk_qeq_spmv": [_p, _p, _p, _p, _p, _i, _p, _p, _p, _p, _p, _p],
+    "mdkk_qeq_gershgorin": [_p, _p, _p, _p, _i, _p, _p, _p, _p],
+    "mdkk_dot": [_p, _p, _p, _i, _p, _p],
+    "mdkk_cg_update": [_p, _i, _p, _p, _p, _p, _p, _p, _p, _p],
+    "mdkk_cg_direction": [_i, _p, _p, _p, _p, _p],
 }
 _RESTYPE = {"mdkk_last_error": C.c_char_p, "mdkk_launch_count": C.c_ulonglong}
 

@@ -13,7 +13,7 @@ import difflib
 
 COMMANDS = {"units": 1, "boundary": 3, "lattice": 2, "create_box": 3, "create_atoms": 0, "mass": 1,
             "velocity": 2, "pair_style": None, "pair_coeff": 2, "suffix": 1, "timestep": 1, "thermo": 1,
-            "run": 1}
+            "run": 1, "qeq": None}
 
 
 class ParseError(ValueError):
@@ -58,4 +58,20 @@ def _command(tokens, line_no):
         raise ParseError(line_no, f"{name} expects {n} argument(s), got {len(args)}")
     if name == "pair_style" and not args:
         raise ParseError(line_no, "pair_style expects a style name")
+    if name == "qeq":   # 'qeq off' | 'qeq on gamma eta chi cutoff' (mdkk/driver/script.py:102-120)
+        if not args:
+            raise ParseError(line_no, "qeq expects 'on <params>' or 'off'")
+        if args[0] == "off":
+            if len(args) != 1:
+                raise ParseError(line_no, "qeq off takes no parameters")
+        elif args[0] != "on":
+            raise ParseError(line_no, f"qeq: expected 'on' or 'off', got {args[0]!r}")
+        elif len(args) != 5:
+            raise ParseError(line_no, f"qeq on expects 4 parameter(s), got {len(args) - 1}")
+        else:
+            for tok in args[1:]:
+                try:
+                    float(tok)
+                except ValueError:
+                    raise ParseError(line_no, f"qeq: {tok!r} is not a number") from None
     return Command(name, args, line_no)

@@ -169,6 +169,7 @@ class RunResult:
     def __init__(self):
         self.rows = []
         self.snapshots = {}
+        self.qeq_log = []         # (step, iters_s, iters_t, sum_q, energy) (mdkk/driver/simulation.py:203)
         self.lines = []
         self.n_rebuilds = 0
 
@@ -206,6 +207,7 @@ class Simulation:
         self.device = torch.device(dev) if dev is not None else torch.device("cuda", torch.cuda.current_device())
         self._d2 = None
         self._d2_host = None
+        self.qeq = None
         self._e_dev = None
         self._flags = None
 
@@ -269,6 +271,29 @@ class Simulation:
         if self.style is None:
             raise RunError("pair_style must be set before pair_coeff")
         self.style.set_coeff(float(a[0]), float(a[1]))
+
+    def _cmd_qeq(self, a):
+        """`qeq off` | `qeq on gamma eta chi cutoff` (mdkk/driver/simulation.py:306-311)."""
+        from ..qeq import QeqParams
+        if a[0] == "off":
+            self.qeq = None
+            return
+        gamma, eta, chi, cutoff = (float(v) for v in a[1:])
+        self.qeq = QeqParams(gamma=gamma, eta=eta, chi=chi, cutoff=cutoff)
+
+    def _qeq_diagnostic(self, step: int, result: RunResult) -> None:
+        """Charges on a one-rank copy at thermo steps (mdkk/driver/simulation.py:417-429), solved on the GPU."""
+        if self.qeq is None:
+            return
+        from ..qeq import QeqSystem, build_matrix, qeq_energy, solve_qeq
+        gp, gv, _ = self.system.gather()
+        solo = RankedSystem.distribute(self.system.box, 1, gp, gv, device=self.device)
+        qlists = build_all(solo, self.qeq.cutoff, self.config.skin, style="full", newton=False)
+        store = solo.stores[0]
+        H = build_matrix(store, qlists[0], self.qeq)
+        qsys = QeqSystem(H, np.full(store.n_local, self.qeq.chi))
+        q = solve_qeq(qsys)
+        result.qeq_log.append((step, *qsys.iterations, float(q.sum()), qeq_energy(qsys)))
 
     def _cmd_suffix(self, a):
         self.suffix = None if a[0] == "off" else a[0]
@@ -446,6 +471,7 @@ class Simulation:
                 result.log(step, e_pot, ke, t)
                 if self.snapshots:
                     result.snapshots[step] = self.system.gather_positions()
+                self._qeq_diagnostic(step, result)
                 self.log(result.lines[-1])
 
             log(0, self._forces_device())

@@ -172,8 +172,34 @@ def snap_fixtures():
     np.savez_compressed(os.path.join(HERE, "snap.npz"), **out)
 
 
+def qeq_fixtures():
+    """Reference QEq on the reference tests' configuration (mdkk tests/test_qeq.py:17-40)."""
+    from mdkk.qeq import QeqParams, QeqSystem, build_matrix, qeq_energy, solve_qeq
+    out = {}
+    for tag, n, rho, seed in (("a", 60, 0.5, 12), ("b", 200, 0.6, 5)):
+        pos, box = random_config(n, rho, seed)
+        L = box.lengths
+        params = QeqParams(gamma=0.8, eta=20.0, chi=-0.35, cutoff=2.0)
+        system = RankedSystem.distribute(box, 1, pos, np.zeros((n, 3)))
+        lists = build_all(system, params.cutoff, 0.3, style="full", newton=False)
+        H = build_matrix(system.stores[0], lists[0], params)
+        # uniform chi (the reference's setup) gives q = 0; a seeded spread makes the charges non-trivial
+        chi = params.chi + 0.1 * np.random.default_rng(seed + 1).normal(size=n)
+        qs = QeqSystem(H, chi, tol=1e-10)
+        out[f"{tag}_chi"] = chi
+        q = solve_qeq(qs)
+        gathered = system.gather()[0]
+        out[f"{tag}_pos"] = gathered
+        out[f"{tag}_L"] = np.asarray(L, dtype=np.float64)
+        out[f"{tag}_H"] = H.to_dense()
+        out[f"{tag}_q"] = q
+        out[f"{tag}_E"] = qeq_energy(qs)
+        out[f"{tag}_iters"] = np.array(qs.iterations)
+    np.savez_compressed(os.path.join(HERE, "qeq.npz"), **out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["lj_small", "lj_32k", "snap", "runs"]
+    which = sys.argv[1:] or ["lj_small", "lj_32k", "snap", "runs", "qeq"]
     if "lj_small" in which:
         lj_small()
     if "lj_32k" in which:
@@ -182,3 +208,5 @@ if __name__ == "__main__":
         snap_fixtures()
     if "runs" in which:
         melt_runs()
+    if "qeq" in which:
+        qeq_fixtures()

@@ -139,3 +139,16 @@ def test_snap_c4_matches_reference():
     assert e == pytest.approx(float(g["c4_E"]), rel=1e-12)
     assert e == pytest.approx(65509.51457722162, rel=1e-12)
     assert np.abs(f - g["c4_F"]).max() <= 1e-10 * np.abs(g["c4_F"]).max()
+
+
+def test_qeq_oracle_pinned_to_reference():
+    """oracle/qeq.py vs the unmodified reference's QEq outputs (tests/golden/qeq.npz)."""
+    from oracle import qeq as oq
+    g = golden("qeq.npz")
+    for tag in ("a", "b"):
+        H = oq.dense_matrix(g[f"{tag}_pos"], g[f"{tag}_L"], 0.8, 20.0, 2.0)
+        assert np.abs(H - g[f"{tag}_H"]).max() <= 1e-13
+        q, e = oq.solve_qeq(H, g[f"{tag}_chi"], tol=1e-10)
+        assert np.allclose(q, g[f"{tag}_q"], rtol=1e-8, atol=1e-12)
+        assert e == pytest.approx(float(g[f"{tag}_E"]), rel=1e-8)
+        assert np.allclose(oq.kkt_charges(H, g[f"{tag}_chi"]), g[f"{tag}_q"], rtol=1e-6, atol=1e-9)
