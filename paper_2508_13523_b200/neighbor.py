@@ -217,6 +217,12 @@ def build(store: AtomStore, box: Box, cutoff: float, skin: float, style: str = "
     garr, narr = _lib.dbl3(g), _lib.int_arr(nc)
     _lib.check(lib.mdkk_bin_atoms(ctx, store.x.data_ptr(), n_total, garr, narr, keys.data_ptr(),
                                   cstart.data_ptr(), catoms.data_ptr(), stream), "mdkk_bin_atoms")
+    if cap_hint is None and n_local:
+        # first build: size the table from the density (mean partners 4/3 pi bc^3 rho,
+        # halved for half lists, +25 % for fluctuations) instead of growing by retries
+        vol = float(np.prod(np.asarray(hi, dtype=np.float64) - np.asarray(lo, dtype=np.float64)))
+        mean = n_local / max(vol, 1e-300) * (4.0 / 3.0) * math.pi * bc ** 3 * (0.5 if style == "half" else 1.0)
+        cap_hint = grow_capacity(capacity, int(1.25 * mean) + 8)
     alloc = max(grow_capacity(capacity, 0), int(cap_hint or 0))
     old_t = recycle.table_dev if recycle is not None else None
     counts = _recycled(recycle.counts_dev if recycle is not None else None, (max(n_local, 1),), torch.int32, dev)
