@@ -625,7 +625,13 @@ class RankedSystem:
                     gi = s.gid[: s.n_local].to(torch.int32)
                     _lib.check(lib.mdkk_scatter_rows4(rows_fn(s).data_ptr(), gi.data_ptr(), s.n_local,
                                                       out.data_ptr(), stream), "scatter")
-            return out[:n, :width].contiguous().cpu().numpy()
+            # device -> pinned staging (full-rate DMA) -> fresh host array
+            pin = self._scratch.get("pin")
+            if pin is None or pin.numel() < n * width:
+                pin = self._scratch["pin"] = torch.empty(max(n * width, 1), dtype=torch.float64, pin_memory=True)
+            stage = pin[: n * width].view(n, width)
+            stage.copy_(out[:n, :width])
+            return stage.numpy().copy()
         rows = np.concatenate([rows_fn(s)[: s.n_local, :width].cpu().numpy() for s in self.stores])
         gid = np.concatenate([s.global_ids[: s.n_local] for s in self.stores])
         return rows[np.argsort(gid, kind="stable")]

@@ -207,6 +207,7 @@ class Simulation:
         self.device = torch.device(dev) if dev is not None else torch.device("cuda", torch.cuda.current_device())
         self._d2 = None
         self._d2_host = None
+        self._packed = False
         self.qeq = None
         self._e_dev = None
         self._flags = None
@@ -398,6 +399,11 @@ class Simulation:
         if self._d2_host is None:
             self._d2_host = torch.zeros(1, dtype=torch.float64, pin_memory=True)
         self._d2_host.copy_(worst, non_blocking=True)
+        if not self.config.distributed:
+            # speculative halo refresh, queued behind the read-back: a plain step needs
+            # it next, and a rebuild simply overwrites the ghost rows
+            self.system.forward_comm()
+            self._packed = True
         torch.cuda.current_stream(self.device).synchronize()
         return math.sqrt(float(self._d2_host[0])) > 0.5 * self.config.skin
 
@@ -411,9 +417,10 @@ class Simulation:
 
     def step_device(self) -> torch.Tensor:
         """One velocity-Verlet step (mdkk/driver/simulation.py:431-450); energy stays on device."""
+        self._packed = False
         if self._half_kick_drift():
             self._rebuild_lists()
-        else:
+        elif not self._packed:
             self.system.forward_comm()
         e = self._forces_device()
         self._half_kick()
