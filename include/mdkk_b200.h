@@ -158,10 +158,12 @@ int mdkk_lj_force_neighbor(mdkk_ctx* ctx, const double* x, int n_local, const in
 /* ------------------------------------------------------------- integrator
  * Velocity Verlet (mdkk/driver/simulation.py:431-450) fused with the skin
  * test (mdkk/neighbor.py:66-74).  first: v += h f; x += dt v;
- * *maxdisp2 = max |x - x_ref|^2.  second: v += h f; ke (optional,
- * device double) = sum 1/2 m v^2 (mdkk/driver/simulation.py:407-415). */
+ * *maxdisp2 = max |x - x_ref|^2; pending_kick != 0 first applies the previous
+ * step's deferred closing v += h f (same f; bit-identical to calling second
+ * then first).  second: v += h f; ke (optional, device double) = sum 1/2 m v^2
+ * (mdkk/driver/simulation.py:407-415). */
 int mdkk_verlet_first(mdkk_ctx* ctx, double* x, double* v, const double* f, const double* x_ref,
-                      int n, double dt, double half_dt_over_m, double* maxdisp2, void* stream);
+                      int n, double dt, double half_dt_over_m, double* maxdisp2, int pending_kick, void* stream);
 int mdkk_verlet_second(mdkk_ctx* ctx, double* v, const double* f, int n, double half_dt_over_m,
                        double mass, double* ke, void* stream);
 /* Sum of 1/2 m |v|^2 over n rows into *ke (device double). */

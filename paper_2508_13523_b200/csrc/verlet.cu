@@ -7,6 +7,10 @@ namespace {
 
 constexpr int kBlock = 256;
 
+// PENDING: the previous step's closing half-kick was deferred into this pass
+// (same force, applied first with its own rounding: bit-identical to running
+// k_verlet_second then this kernel).
+template <bool PENDING>
 __global__ void __launch_bounds__(kBlock) k_verlet_first(double* __restrict__ x, double* __restrict__ v,
                                                          const double* __restrict__ f,
                                                          const double* __restrict__ xr, int n, double dt,
@@ -15,6 +19,11 @@ __global__ void __launch_bounds__(kBlock) k_verlet_first(double* __restrict__ x,
     double d2 = 0.0;
     if (i < n) {
         double4 vi = mdkk::ld4_nc(v, i), fi = mdkk::ld4_nc(f, i), xi = mdkk::ld4_nc(x, i);
+        if (PENDING) {
+            vi.x += h * fi.x;
+            vi.y += h * fi.y;
+            vi.z += h * fi.z;
+        }
         vi.x += h * fi.x;
         vi.y += h * fi.y;
         vi.z += h * fi.z;
@@ -63,12 +72,15 @@ __global__ void k_scale(double* p, double s) { *p *= s; }
 extern "C" {
 
 int mdkk_verlet_first(mdkk_ctx*, double* x, double* v, const double* f, const double* x_ref, int n, double dt,
-                      double h, double* maxdisp2, void* stream) {
+                      double h, double* maxdisp2, int pending_kick, void* stream) {
     if (n < 0) return MDKK_E_ARG;
     cudaStream_t s = mdkk::as_stream(stream);
     cudaMemsetAsync(maxdisp2, 0, sizeof(double), s);
     if (n == 0) return MDKK_OK;
-    k_verlet_first<<<mdkk::grid_for(n, kBlock), kBlock, 0, s>>>(x, v, f, x_ref, n, dt, h, maxdisp2);
+    if (pending_kick)
+        k_verlet_first<true><<<mdkk::grid_for(n, kBlock), kBlock, 0, s>>>(x, v, f, x_ref, n, dt, h, maxdisp2);
+    else
+        k_verlet_first<false><<<mdkk::grid_for(n, kBlock), kBlock, 0, s>>>(x, v, f, x_ref, n, dt, h, maxdisp2);
     MDKK_CHECK_LAUNCH("k_verlet_first");
     return MDKK_OK;
 }

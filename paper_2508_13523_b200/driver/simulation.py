@@ -208,6 +208,7 @@ class Simulation:
         self._d2 = None
         self._d2_host = None
         self._packed = False
+        self._kick_pending = False
         self.qeq = None
         self._e_dev = None
         self._flags = None
@@ -389,8 +390,10 @@ class Simulation:
             s.to_device()
             _lib.check(lib.mdkk_verlet_first(ctx, s.x.data_ptr(), s.v.data_ptr(), s.f.data_ptr(),
                                              nl.ref_dev.data_ptr(), s.n_local, self.dt, h,
-                                             self._d2[k:].data_ptr(), st), "mdkk_verlet_first")
+                                             self._d2[k:].data_ptr(), int(self._kick_pending), st),
+                       "mdkk_verlet_first")
             s.device_wrote(pos=True, vel=True)
+        self._kick_pending = False
         n = len(self.system.stores)
         worst = self._d2[0:1] if n == 1 else self._d2[:n].max().reshape(1)
         if self.config.distributed:   # any rank over skin/2 -> every rank rebuilds (mdkk/neighbor.py:230)
@@ -415,16 +418,30 @@ class Simulation:
                                               h, self.mass, None, st), "mdkk_verlet_second")
             s.device_wrote(vel=True)
 
-    def step_device(self) -> torch.Tensor:
-        """One velocity-Verlet step (mdkk/driver/simulation.py:431-450); energy stays on device."""
+    def step_device(self, defer_kick: bool = False) -> torch.Tensor:
+        """One velocity-Verlet step (mdkk/driver/simulation.py:431-450); energy stays on device.
+
+        `defer_kick` leaves the closing half-kick pending: the next step's
+        opening pass applies it (one fewer pass over v and f per step inside
+        `advance`); `flush_kick()` completes it before velocities are read.
+        """
         self._packed = False
         if self._half_kick_drift():
             self._rebuild_lists()
         elif not self._packed:
             self.system.forward_comm()
         e = self._forces_device()
-        self._half_kick()
+        if defer_kick:
+            self._kick_pending = True
+        else:
+            self._half_kick()
         return e
+
+    def flush_kick(self) -> None:
+        """Apply a deferred closing half-kick (velocities complete afterwards)."""
+        if self._kick_pending:
+            self._half_kick()
+            self._kick_pending = False
 
     def step_once(self) -> float:
         return float(self.step_device().item())
@@ -442,7 +459,8 @@ class Simulation:
         try:
             e = None
             for _ in range(n_steps):
-                e = self.step_device()
+                e = self.step_device(defer_kick=True)
+            self.flush_kick()
             return e
         finally:
             if was:
