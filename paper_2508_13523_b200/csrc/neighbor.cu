@@ -71,6 +71,28 @@ __device__ __forceinline__ bool lex_zyx_less(double ax, double ay, double az, do
     return (az < bz) || (az == bz && (ay < by || (ay == by && ax < bx)));
 }
 
+// Packed FP32 pair arithmetic (sm_100 FADD2 / FMUL2 / FFMA2): r^2 of two
+// staged candidates against one atom in 6 instructions.
+__device__ __forceinline__ unsigned long long f32x2(float a, float b) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void r2_pair(const float* px, const float* py, const float* pz, unsigned long long xi2,
+                                        unsigned long long yi2, unsigned long long zi2, float& r0, float& r1) {
+    const unsigned long long x = *reinterpret_cast<const unsigned long long*>(px);
+    const unsigned long long y = *reinterpret_cast<const unsigned long long*>(py);
+    const unsigned long long z = *reinterpret_cast<const unsigned long long*>(pz);
+    unsigned long long dx, dy, dz, r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(dx) : "l"(x), "l"(xi2));
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(dy) : "l"(y), "l"(yi2));
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(dz) : "l"(z), "l"(zi2));
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(dx), "l"(dx));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(dy), "l"(dy), "l"(r));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(dz), "l"(dz), "l"(r));
+    asm("mov.b64 {%0,%1}, %2;" : "=f"(r0), "=f"(r1) : "l"(r));
+}
+
 constexpr int kWarps = 4;
 constexpr int kUnion = 1024;  // candidate indices per cluster in shared memory (4 KB per warp)
 constexpr int kChunk = 64;    // candidate positions staged per pass (1.5 KB per warp)
@@ -88,7 +110,9 @@ __global__ void __launch_bounds__(kWarps * 32) k_nbr_build(
     int* __restrict__ max_count) {
     __shared__ int s_union[kWarps][kUnion];
     __shared__ double s_pos[kWarps][3][kChunk];
-    __shared__ float4 s_rel[kWarps][kChunk];   // cluster-relative FP32 (x, y, z, -): one broadcast LDS.128
+    // cluster-relative FP32 coordinates, SoA: an aligned float2 = two candidates for the packed
+    // FFMA2/FADD2 prefilter (one broadcast LDS.64 per coordinate and candidate pair)
+    __shared__ __align__(16) float s_rel[kWarps][3][kChunk];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int c = blockIdx.x * kWarps + w;
     const int ncl = (n_local + 31) >> 5;
@@ -97,7 +121,9 @@ __global__ void __launch_bounds__(kWarps * 32) k_nbr_build(
     double* spx = s_pos[w][0];
     double* spy = s_pos[w][1];
     double* spz = s_pos[w][2];
-    float4* sf = s_rel[w];
+    float* sfx = s_rel[w][0];
+    float* sfy = s_rel[w][1];
+    float* sfz = s_rel[w][2];
     const int i = c * 32 + lane;
     const bool valid = i < n_local;
     const double4 xi = mdkk::ld4(x, valid ? i : c * 32);
@@ -138,6 +164,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_nbr_build(
     //    (strict r^2 < bc^2, reference rounding) + style predicate.
     const double ccx = 0.5 * (bmin_x + bmax_x), ccy = 0.5 * (bmin_y + bmax_y), ccz = 0.5 * (bmin_z + bmax_z);
     const float fxi = (float)(xi.x - ccx), fyi = (float)(xi.y - ccy), fzi = (float)(xi.z - ccz);
+    const unsigned long long fxi2 = f32x2(fxi, fxi), fyi2 = f32x2(fyi, fyi), fzi2 = f32x2(fzi, fzi);
     // margin >> FP32 rounding: |r2_f - r2| <~ 6 eps_f D^2 with D the farthest cluster-relative coordinate
     const double hx = 0.5 * (bmax_x - bmin_x) + bc, hy = 0.5 * (bmax_y - bmin_y) + bc, hz = 0.5 * (bmax_z - bmin_z) + bc;
     const float bc2f = (float)(bc2 * (1.0 + 1e-4) + 4e-6 * (hx * hx + hy * hy + hz * hz));
@@ -172,8 +199,9 @@ __global__ void __launch_bounds__(kWarps * 32) k_nbr_build(
                 spx[t] = p.x;
                 spy[t] = p.y;
                 spz[t] = p.z;
-                sf[t] = make_float4((float)(p.x - ccx), (float)(p.y - ccy), (float)(p.z - ccz),
-                                    __int_as_float(su[u0 + t]));
+                sfx[t] = (float)(p.x - ccx);
+                sfy[t] = (float)(p.y - ccy);
+                sfz[t] = (float)(p.z - ccz);
             }
             __syncwarp();
             // branch-free prefilter into a per-lane bit mask, then each lane visits only
@@ -186,24 +214,32 @@ __global__ void __launch_bounds__(kWarps * 32) k_nbr_build(
                     // full list: two-sided FP32 test; certain members are stored right here
                     // (predicated, candidate order), only the thin shell around bc goes to
                     // the exact FP64 test below
+                    unsigned in_bits = 0u;
 #pragma unroll
-                    for (int t = 0; t < 32; ++t) {
-                        const float4 q = sf[h0 + t];     // entries past cn are stale but masked below
-                        const float dx = q.x - fxi, dy = q.y - fyi, dz = q.z - fzi;
-                        const float r2f = dx * dx + dy * dy + dz * dz;
-                        const int j = __float_as_int(q.w);
-                        if (t < lim && valid && r2f < lo2f && j != i) {
+                    for (int t = 0; t < 32; t += 2) {   // entries past cn are stale but masked below
+                        float r0, r1;
+                        r2_pair(sfx + h0 + t, sfy + h0 + t, sfz + h0 + t, fxi2, fyi2, fzi2, r0, r1);
+                        in_bits |= ((r0 < lo2f) ? (1u << t) : 0u) | ((r1 < lo2f) ? (2u << t) : 0u);
+                        bits |= ((r0 < bc2f) ? (1u << t) : 0u) | ((r1 < bc2f) ? (2u << t) : 0u);
+                    }
+                    if (lim < 32) in_bits &= (1u << lim) - 1u;
+                    if (!valid) in_bits = 0u;
+                    bits &= ~in_bits;                    // the exact test only for the shell
+                    while (in_bits) {                    // certain members, candidate order
+                        const int t = __ffs(in_bits) - 1;
+                        in_bits &= in_bits - 1u;
+                        const int j = su[u0 + h0 + t];
+                        if (j != i) {
                             if (cnt < cap) trow[(long long)cnt * 32] = j;
                             ++cnt;
                         }
-                        bits |= (r2f < bc2f && !(r2f < lo2f)) ? (1u << t) : 0u;
                     }
                 } else {
 #pragma unroll
-                    for (int t = 0; t < 32; ++t) {
-                        const float4 q = sf[h0 + t];     // entries past cn are stale but masked below
-                        const float dx = q.x - fxi, dy = q.y - fyi, dz = q.z - fzi;
-                        bits |= (dx * dx + dy * dy + dz * dz < bc2f) ? (1u << t) : 0u;
+                    for (int t = 0; t < 32; t += 2) {   // entries past cn are stale but masked below
+                        float r0, r1;
+                        r2_pair(sfx + h0 + t, sfy + h0 + t, sfz + h0 + t, fxi2, fyi2, fzi2, r0, r1);
+                        bits |= ((r0 < bc2f) ? (1u << t) : 0u) | ((r1 < bc2f) ? (2u << t) : 0u);
                     }
                 }
                 if (lim < 32) bits &= (1u << lim) - 1u;
