@@ -35,6 +35,31 @@ from .domain import (SHIFT_UNITS, AtomStore, Box, RankSet, _rows4, _to4, cell_gr
                      _dense_ids, wrap_positions)
 
 
+def _staged(group) -> bool:
+    """gloo moves host memory only: CUDA tensors are staged through the host (single-GPU
+    multi-process tests); NCCL (the product path) sends device buffers directly."""
+    return dist.get_backend(group) == "gloo"
+
+
+def _all_reduce(t: torch.Tensor, op, group) -> None:
+    if t.is_cuda and _staged(group):
+        h = t.cpu()
+        dist.all_reduce(h, op=op, group=group)
+        t.copy_(h)
+    else:
+        dist.all_reduce(t, op=op, group=group)
+
+
+def _all_gather(out: list, t: torch.Tensor, group) -> None:
+    if t.is_cuda and _staged(group):
+        hs = [torch.empty_like(o, device="cpu") for o in out]
+        dist.all_gather(hs, t.cpu(), group=group)
+        for o, h in zip(out, hs):
+            o.copy_(h)
+    else:
+        dist.all_gather(out, t, group=group)
+
+
 class CudaOps:
     """Kernel entry points of libmdkk_b200 used by the distributed system."""
 
@@ -183,26 +208,36 @@ class DistSystem:
 
     # ------------------------------------------------------------ helpers
     def allreduce_max(self, t: torch.Tensor) -> torch.Tensor:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+        _all_reduce(t, dist.ReduceOp.MAX, self.group)
         return t
 
     def allreduce_sum(self, t: torch.Tensor) -> torch.Tensor:
-        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+        _all_reduce(t, dist.ReduceOp.SUM, self.group)
         return t
 
     def _p2p(self, sends, recvs):
         """One batched group of isend/irecv (tensor, peer) pairs; waits for completion."""
+        staged = _staged(self.group) and any(t.is_cuda for t, _ in list(sends) + list(recvs))
+        if staged:
+            sends = [(t.cpu(), p) for t, p in sends]
+            host_recvs = [(torch.empty_like(t, device="cpu"), p) for t, p in recvs]
+        else:
+            host_recvs = recvs
         ops = [dist.P2POp(dist.isend, t, p, self.group) for t, p in sends if t.numel()]
-        ops += [dist.P2POp(dist.irecv, t, p, self.group) for t, p in recvs if t.numel()]
+        ops += [dist.P2POp(dist.irecv, t, p, self.group) for t, p in host_recvs if t.numel()]
         if ops:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
+        if staged:
+            for (t, _), (h, _) in zip(recvs, host_recvs):
+                if t.numel():
+                    t.copy_(h)
 
     def _counts_matrix(self, mine: np.ndarray) -> np.ndarray:
         """All-gather of every rank's per-destination counts -> [src][dst]."""
         t = torch.as_tensor(mine, dtype=torch.int64, device=self.device)
         out = [torch.empty_like(t) for _ in range(self.world)]
-        dist.all_gather(out, t, group=self.group)
+        _all_gather(out, t, self.group)
         return torch.stack(out).cpu().numpy()
 
     def _combos(self, halo):
@@ -423,7 +458,7 @@ class DistSystem:
         s = self.store
         n = torch.tensor([s.n_local], dtype=torch.int64, device=self.device)
         ns = [torch.empty_like(n) for _ in range(self.world)]
-        dist.all_gather(ns, n, group=self.group)
+        _all_gather(ns, n, self.group)
         ns = [int(v.item()) for v in ns]
         m = max(ns) if ns else 0
         rows = torch.zeros((max(m, 1), width), dtype=t.dtype, device=self.device)
@@ -432,8 +467,8 @@ class DistSystem:
         gid[: s.n_local] = s.gid[: s.n_local]
         R = [torch.empty_like(rows) for _ in range(self.world)]
         G = [torch.empty_like(gid) for _ in range(self.world)]
-        dist.all_gather(R, rows, group=self.group)
-        dist.all_gather(G, gid, group=self.group)
+        _all_gather(R, rows, self.group)
+        _all_gather(G, gid, self.group)
         rows = np.concatenate([r[:k].cpu().numpy() for r, k in zip(R, ns)])
         gids = np.concatenate([g[:k].cpu().numpy() for g, k in zip(G, ns)])
         o = np.argsort(gids, kind="stable")
