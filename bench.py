@@ -304,6 +304,8 @@ def main():
     ap.add_argument("--no-snap", action="store_true")
     ap.add_argument("--snap-cells", type=int, default=SNAP["cells"])
     ap.add_argument("--snap-steps", type=int, default=5)
+    ap.add_argument("--strong", action="store_true",
+                    help="configs[2]: a fixed 160^3-cell (16,384,000-atom) melt split over the N GPUs")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -321,7 +323,11 @@ def main():
     # weak scaling: an 80^3-cell fcc brick (2,048,000 atoms) per GPU, bricks tiled by decompose(N)
     from paper_2508_13523_b200.domain import Box as _Box, decompose as _decompose
     grid = _decompose(_Box((1.0, 1.0, 1.0)), world).grid
-    cells = tuple(args.cells * g for g in grid)
+    cells = (160, 160, 160) if args.strong else tuple(args.cells * g for g in grid)
+    scaling = "strong" if args.strong else "weak"
+    workload = ("LJ 12-6 melt fcc rho*=0.8442, rc=2.5, skin=0.3, T=1.44, dt=0.005, full list newton-off "
+                + ("(configs[2]: 16,384,000 atoms, strong scaling over the GPUs)" if args.strong else
+                   "(configs[1]; weak scaling: 80^3 fcc cells per GPU)"))
     distributed = world > 1
 
     def max_over_ranks(v):
@@ -363,10 +369,9 @@ def main():
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "LJ 12-6 melt fcc rho*=0.8442, rc=2.5, skin=0.3, T=1.44, dt=0.005, "
-                                   "full list newton-off (configs[1]; weak scaling: 80^3 fcc cells per GPU)",
+            "config": {"workload": workload,
                        "n_atoms": full["n_atoms"], "n_ghost_rank0": full["n_ghost"], "list": "full",
                        "grid": list(grid),
                        "rebuilds_in_timed_steps": full["rebuilds"], "mean_neighbors": nn,
