@@ -58,6 +58,13 @@ class LayoutPolicy:
             off = off * shape[d] + idx[d]
         return off
 
+    def view(self, flat, shape):
+        """Logical-index view of flat storage (numpy or torch) laid out in this order."""
+        shape = tuple(int(s) for s in shape)
+        st = flat.reshape(self.storage_shape(shape))
+        axes = self.logical_axes()
+        return st.transpose(axes) if isinstance(st, np.ndarray) else st.permute(*axes)
+
     def logical_axes(self) -> tuple[int, ...]:
         return tuple(self.order.index(d) for d in range(len(self.order)))
 
@@ -114,6 +121,10 @@ class DualArray:
         v = self.data_b.permute(*self.layout_b.logical_axes())
         sl = tuple(slice(0, s) for s in self.shape)
         return v[sl]
+
+    def storage(self, space):
+        """The raw storage of a space (numpy for 'a', torch for 'b'), flattened."""
+        return self.data_a.reshape(-1) if self._check(space) == "a" else self.data_b.reshape(-1)
 
     def modified(self, space):
         return self.modified_a if self._check(space) == "a" else self.modified_b
