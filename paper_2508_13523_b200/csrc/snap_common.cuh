@@ -70,31 +70,37 @@ struct PairGeo {
     double fc, dfc, r;
 };
 
-// a, b, f_c, f_c' (mdkk/snap/compute.py:27-45).
+// a, b, f_c, f_c' (mdkk/snap/compute.py:27-45).  One sincospi per angle and one
+// reciprocal of r0 instead of tan / cos / sin and four divisions (equal to the
+// reference's expressions to a few ulp).
 __device__ __forceinline__ void pair_geometry(double dx, double dy, double dz, double r2, double rc, PairGeo& g,
                                               double& z0, double& r0) {
     const double r = sqrt(r2);
-    const double ct = 0.99 * kPi / rc;
-    z0 = r / tan(ct * r);
+    double s1, c1, s2, c2;
+    sincospi(0.99 * r / rc, &s1, &c1);   // z0 = r / tan(0.99 pi r / rc)
+    sincospi(r / rc, &s2, &c2);
+    z0 = r * c1 / s1;
     r0 = sqrt(r * r + z0 * z0);
+    const double ir0 = 1.0 / r0;
     g.r = r;
-    g.a = {z0 / r0, -dz / r0};
-    g.b = {dy / r0, -dx / r0};
-    g.fc = 0.5 * (1.0 + cos(kPi * r / rc));
-    g.dfc = -kPi / (2.0 * rc) * sin(kPi * r / rc);
+    g.a = {z0 * ir0, -dz * ir0};
+    g.b = {dy * ir0, -dx * ir0};
+    g.fc = 0.5 * (1.0 + c2);
+    g.dfc = -kPi / (2.0 * rc) * s2;
 }
 
-// d a / d dr_k, d b / d dr_k (mdkk/snap/compute.py:48-63).
+// d a / d dr_k, d b / d dr_k (mdkk/snap/compute.py:48-63), with reciprocals of r and r0.
 __device__ __forceinline__ void pair_grads(const double d[3], const PairGeo& g, double rc, double z0, double r0,
                                            cplx da[3], cplx db[3]) {
     const double r = g.r, ct = 0.99 * kPi / rc;
-    const double dz0_dr = z0 / r - ct * (r * r + z0 * z0) / r;
+    const double ir = 1.0 / r, ir0 = 1.0 / r0;
+    const double dz0_dr = (z0 - ct * (r * r + z0 * z0)) * ir;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-        const double dz0 = dz0_dr * (d[k] / r);
-        const double dr0 = (d[k] + z0 * dz0) / r0;
-        da[k] = {dz0 / r0 - g.a.re * dr0 / r0, (k == 2 ? -1.0 / r0 : 0.0) - g.a.im * dr0 / r0};
-        db[k] = {(k == 1 ? 1.0 / r0 : 0.0) - g.b.re * dr0 / r0, (k == 0 ? -1.0 / r0 : 0.0) - g.b.im * dr0 / r0};
+        const double dz0 = dz0_dr * (d[k] * ir);
+        const double t = (d[k] + z0 * dz0) * ir0 * ir0;   // dr0 / r0
+        da[k] = {dz0 * ir0 - g.a.re * t, (k == 2 ? -ir0 : 0.0) - g.a.im * t};
+        db[k] = {(k == 1 ? ir0 : 0.0) - g.b.re * t, (k == 0 ? -ir0 : 0.0) - g.b.im * t};
     }
 }
 
