@@ -34,7 +34,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_snap_ui(const double* __rest
                                                          int* __restrict__ flags) {
     constexpr int NF = block_offset(TWOJ + 1);
     __shared__ RS rs;
-    __shared__ NbPair s_nb[kWarps][32];
+    __shared__ NbPair s_nb[kWarps][kNbChunk];
     __shared__ cplx s_lvl[kWarps][2][2][kLevelMax];
     for (int t = threadIdx.x; t < kWarps * 4 * kLevelMax; t += blockDim.x)
         (&s_lvl[0][0][0][0])[t] = {0.0, 0.0};   // rec2 reads finite neighbours at the column ends
@@ -49,14 +49,14 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_snap_ui(const double* __rest
     const int n = min(counts[i], cap);
     const double rc2 = rc * rc;
     bool bad = false;
-    for (int k0 = 0; k0 < n; k0 += 32) {
-        const int m = compact_pairs(x, table, cap, i, k0, n, xi, rc2, s_nb[w], bad);
+    for (int k0 = 0; k0 < n; k0 += kNbChunk) {
+        const int m = compact_pairs(x, table, cap, i, k0, n, xi, rc2, rc, s_nb[w], bad);
         for (int t = 0; t < m; t += 2) {
             const int pi = t + hh;
             const NbPair nb = s_nb[w][pi < m ? pi : t];
             PairGeo g;
             double z0, r0;
-            pair_geometry(nb.dx, nb.dy, nb.dz, nb.r2, rc, g, z0, r0);
+            geo_of(nb, g, z0, r0);
             const double fc = pi < m ? g.fc : 0.0;
             const cplx ab = cconj(g.a);
             cplx(*L)[kLevelMax] = s_lvl[w][hh];
@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_snap_deidrj(const double* __
     constexpr int NH = half_offset(TWOJ + 1);
     extern __shared__ double s_dyn_d[];  // rs | pairs | Y_i (C order) | u levels | lambda C prefixes
     RS& rs = *reinterpret_cast<RS*>(s_dyn_d);
-    auto s_nb = reinterpret_cast<NbPair(*)[32]>(reinterpret_cast<char*>(s_dyn_d) + sizeof(RS));
+    auto s_nb = reinterpret_cast<NbPair(*)[kNbChunk]>(reinterpret_cast<char*>(s_dyn_d) + sizeof(RS));
     auto s_y = reinterpret_cast<cplx(*)[NH]>(s_nb + kWarps);
     auto s_u = reinterpret_cast<cplx(*)[2][NU]>(s_y + kWarps);
     auto s_l = reinterpret_cast<cplx(*)[2][2][kLamMax]>(s_u + kWarps);
@@ -262,15 +262,15 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_snap_deidrj(const double* __
     const double rc2 = rc * rc;
     double fi[3] = {0.0, 0.0, 0.0};
     bool bad = false;
-    for (int k0 = 0; k0 < n; k0 += 32) {
-        const int m = compact_pairs(x, table, cap, i, k0, n, xi, rc2, s_nb[w], bad);
+    for (int k0 = 0; k0 < n; k0 += kNbChunk) {
+        const int m = compact_pairs(x, table, cap, i, k0, n, xi, rc2, rc, s_nb[w], bad);
         for (int t = 0; t < m; t += 2) {
             const int pi = t + hh;
             const bool active = pi < m;
             const NbPair nb = s_nb[w][active ? pi : t];
             PairGeo g;
             double z0, r0;
-            pair_geometry(nb.dx, nb.dy, nb.dz, nb.r2, rc, g, z0, r0);
+            geo_of(nb, g, z0, r0);
             const cplx ab = cconj(g.a), bb = cconj(g.b);
             // forward: C_tj of every level, S = Re sum_f conj(Y) u (mirror pairs counted twice)
             double S = 0.0;
@@ -521,7 +521,7 @@ int mdkk_snap_deidrj(mdkk_snap* s, const double* x, int n_local, const int* tabl
     switch (s->twojmax) {
 #define MDKK_DE(TJ)                                                                                          \
     case TJ: {                                                                                               \
-        const size_t sm = sizeof(RS) + kWarps * (32 * sizeof(NbPair) +                                       \
+        const size_t sm = sizeof(RS) + kWarps * (kNbChunk * sizeof(NbPair) +                                 \
             (half_offset(TJ + 1) + 2 * (block_offset(TJ) > 0 ? block_offset(TJ) : 1) + 4 * kLamMax) *         \
             sizeof(cplx));                                                                                   \
         cudaFuncSetAttribute(k_snap_deidrj<TJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);      \

@@ -182,26 +182,45 @@ __device__ __forceinline__ void store_mirrored(cplx* L, int tj, int P, int Q, cp
     L[hm] = {sg * v.re, -sg * v.im};  // the center element writes itself twice (same value)
 }
 
+// One in-range partner with its hypersphere geometry, computed once by the
+// compaction lane (not by every lane of the half-warp that expands it).
 struct NbPair {
-    double dx, dy, dz, r2;
+    double dx, dy, dz, r;
+    double ar, ai, br, bi;   // a, b
+    double fc, dfc, z0, r0;
     int j, pad;
 };
+constexpr int kNbChunk = 16;   // table entries compacted per pass (s_nb holds kNbChunk pairs)
 
 // Compact the in-range partners (r^2 < rc^2, mdkk/snap/compute.py:114-115) of
-// table entries [k0, k0+32) of row i into s_nb; returns their count.
+// table entries [k0, k0+16) of row i into s_nb with their geometry; returns their count.
 __device__ __forceinline__ int compact_pairs(const double* x, const int* table, int cap, int i, int k0, int n,
-                                             double4 xi, double rc2, NbPair* s_nb, bool& bad) {
+                                             double4 xi, double rc2, double rc, NbPair* s_nb, bool& bad) {
     const int lane = threadIdx.x & 31, k = k0 + lane;
     int j = 0;
     double dx = 0, dy = 0, dz = 0, r2 = 0;
-    const bool ok = k < n && neighbour(x, table, cap, i, k, xi, rc2, j, dx, dy, dz, r2);
+    const bool ok = lane < kNbChunk && k < n && neighbour(x, table, cap, i, k, xi, rc2, j, dx, dy, dz, r2);
     const unsigned m = __ballot_sync(0xffffffffu, ok);
     if (ok) {
         bad |= !(r2 > 0.0);
-        s_nb[__popc(m & ((1u << lane) - 1u))] = {dx, dy, dz, r2, j, 0};
+        PairGeo g;
+        double z0, r0;
+        pair_geometry(dx, dy, dz, r2, rc, g, z0, r0);
+        s_nb[__popc(m & ((1u << lane) - 1u))] = {dx, dy, dz, g.r, g.a.re, g.a.im, g.b.re, g.b.im,
+                                                 g.fc, g.dfc, z0, r0, j, 0};
     }
     __syncwarp();
     return __popc(m);
+}
+
+__device__ __forceinline__ void geo_of(const NbPair& nb, PairGeo& g, double& z0, double& r0) {
+    g.r = nb.r;
+    g.a = {nb.ar, nb.ai};
+    g.b = {nb.br, nb.bi};
+    g.fc = nb.fc;
+    g.dfc = nb.dfc;
+    z0 = nb.z0;
+    r0 = nb.r0;
 }
 
 __constant__ short c_hflat[kHalfAll];       // half index -> flat index
