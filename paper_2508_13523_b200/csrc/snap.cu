@@ -130,10 +130,15 @@ constexpr int kYW = 16;                      // warps per CTA (2 CTAs per SM: 32
 constexpr int kUS = 33;                      // tile row stride (double2)
 
 
+__device__ __forceinline__ double flip_sign(double v, unsigned mask) {   // mask: 0 or 0x80000000
+    return __hiloint2double(__double2hiint(v) ^ (int)mask, __double2loint(v));
+}
+
 template <int NF, int NH>
 __global__ void __launch_bounds__(kYW * 32, 2) k_snap_yi(const double2* __restrict__ U, int n,
                                                          const ZEntry* __restrict__ ent,
-                                                         const int* __restrict__ chunk, double2* __restrict__ Yh,
+                                                         const int* __restrict__ chunk,
+                                                         const int* __restrict__ chunkf, double2* __restrict__ Yh,
                                                          int ld, double* __restrict__ partials, long long su,
                                                          long long sf) {
     extern __shared__ double2 s_dyn2[];
@@ -148,6 +153,8 @@ __global__ void __launch_bounds__(kYW * 32, 2) k_snap_yi(const double2* __restri
     __syncthreads();
     const bool valid = a0 + lane < n;
     const int beg = chunk[w], end = chunk[w + 1];
+    int f = chunkf[w];   // outputs are consecutive inside a warp's range
+    const char* su_l = reinterpret_cast<const char*>(s_u + lane);
     ZEntry* se = s_e + w * 32;
     double are = 0.0, aim = 0.0, en = 0.0;
     for (int base = beg; base < end; base += 32) {
@@ -155,22 +162,21 @@ __global__ void __launch_bounds__(kYW * 32, 2) k_snap_yi(const double2* __restri
         __syncwarp();
         const int cnt = min(32, end - base);
         for (int j = 0; j < cnt; ++j) {
-            const double c = se[j].coef;
-            const int code = se[j].code;
-            double2 ug = s_u[(code & 255) * kUS + lane];
-            double2 uh = s_u[((code >> 8) & 255) * kUS + lane];
-            if (code & (1 << 24)) ug.y = -ug.y;
-            if (code & (1 << 25)) uh.y = -uh.y;
-            const double tre = ug.x * uh.x - ug.y * uh.y;
-            const double tim = ug.x * uh.y + ug.y * uh.x;
-            are = fma(c, tre, are);
-            aim = fma(c, tim, aim);
-            if (code & (1 << 26)) {   // warp-uniform: output complete
-                const int f = (code >> 16) & 255;
+            const ZEntry e = se[j];
+            const double2 ug = *reinterpret_cast<const double2*>(su_l + e.goff);
+            const double2 uh = *reinterpret_cast<const double2*>(su_l + (e.hcode & 0xfffff));
+            const double gy = flip_sign(ug.y, ((unsigned)e.hcode << 11) & 0x80000000u);   // conj_g
+            const double hy = flip_sign(uh.y, ((unsigned)e.hcode << 10) & 0x80000000u);   // conj_h
+            const double tre = ug.x * uh.x - gy * hy;
+            const double tim = ug.x * hy + gy * uh.x;
+            are = fma(e.coef, tre, are);
+            aim = fma(e.coef, tim, aim);
+            if (e.hcode & (1 << 22)) {   // warp-uniform: output f complete
                 if (valid) Yh[(long long)f * ld + a0 + lane] = make_double2(are, aim);
                 const double2 u = s_u[f * kUS + lane];
-                en += ((code & (1 << 27)) ? 1.0 : 2.0) * (are * u.x + aim * u.y);
+                en += ((e.hcode & (1 << 23)) ? 1.0 : 2.0) * (are * u.x + aim * u.y);
                 are = aim = 0.0;
+                ++f;
             }
         }
         __syncwarp();
@@ -386,11 +392,16 @@ int mdkk_snap_create(mdkk_ctx* ctx, int twojmax, int n_entries, const double* co
     // host copy of the list + output-aligned per-warp chunks balanced on entry counts
     std::vector<ZEntry> h(n_entries);
     std::vector<int> ends;  // entry index one past each output
+    std::vector<int> fout(n_entries);
     for (int k = 0; k < n_entries; ++k) {
+        const int c = code_host[k];
+        const int g = c & 255, hh = (c >> 8) & 255;
+        fout[k] = (c >> 16) & 255;
         h[k].coef = coef_host[k];
-        h[k].code = code_host[k];
-        h[k].pad = 0;
-        if (code_host[k] & (1 << 26)) ends.push_back(k + 1);
+        h[k].goff = g * kUS * (int)sizeof(double2);
+        h[k].hcode = hh * kUS * (int)sizeof(double2) | ((c >> 24) & 1) << 20 | ((c >> 25) & 1) << 21 |
+                     ((c >> 26) & 1) << 22 | ((c >> 27) & 1) << 23;
+        if (c & (1 << 26)) ends.push_back(k + 1);
     }
     if (ends.empty() || ends.back() != n_entries) {
         mdkk::set_error("mdkk_snap_create: product list must end on an output boundary");
@@ -408,6 +419,8 @@ int mdkk_snap_create(mdkk_ctx* ctx, int twojmax, int n_entries, const double* co
                 chunk[w] = std::max(chunk[w - 1], ends[o - 1]);
         }
     }
+    std::vector<int> chunkf(kYW);
+    for (int w = 0; w < kYW; ++w) chunkf[w] = chunk[w] < n_entries ? fout[chunk[w]] : 0;
     auto* s = new mdkk_snap();
     s->twojmax = twojmax;
     s->n_flat = block_offset(twojmax + 1);
@@ -415,13 +428,16 @@ int mdkk_snap_create(mdkk_ctx* ctx, int twojmax, int n_entries, const double* co
     s->n_entries = n_entries;
     cudaError_t e = cudaMalloc(&s->ent, sizeof(ZEntry) * n_entries);
     if (e == cudaSuccess) e = cudaMalloc(&s->chunk, sizeof(int) * (kYW + 1));
+    if (e == cudaSuccess) e = cudaMalloc(&s->chunkf, sizeof(int) * kYW);
     if (e == cudaSuccess) e = cudaMalloc(&s->fmap, sizeof(int) * s->n_flat);
     if (e == cudaSuccess) e = cudaMemcpy(s->ent, h.data(), sizeof(ZEntry) * n_entries, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(s->chunk, chunk.data(), sizeof(int) * (kYW + 1), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(s->chunkf, chunkf.data(), sizeof(int) * kYW, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(s->fmap, fmap_host, sizeof(int) * s->n_flat, cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
         cudaFree(s->ent);
         cudaFree(s->chunk);
+        cudaFree(s->chunkf);
         cudaFree(s->fmap);
         delete s;
         return mdkk::cuda_fail(e, "mdkk_snap_create");
@@ -435,6 +451,7 @@ int mdkk_snap_destroy(mdkk_snap* s) {
     if (!s) return MDKK_OK;
     cudaFree(s->ent);
     cudaFree(s->chunk);
+    cudaFree(s->chunkf);
     cudaFree(s->fmap);
     delete s;
     return MDKK_OK;
@@ -474,7 +491,8 @@ int mdkk_snap_yi(mdkk_ctx* ctx, mdkk_snap* s, const double* U, int n_local, doub
         constexpr int NF = block_offset(TJ + 1), NH = half_offset(TJ + 1);                                      \
         const size_t sm = NH * kUS * sizeof(double2) + kYW * 32 * sizeof(ZEntry);                               \
         cudaFuncSetAttribute(k_snap_yi<NF, NH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);         \
-        k_snap_yi<NF, NH><<<nb, kYW * 32, sm, st>>>(u, n_local, s->ent, s->chunk, y, ld, partials, su, sf);     \
+        k_snap_yi<NF, NH><<<nb, kYW * 32, sm, st>>>(u, n_local, s->ent, s->chunk, s->chunkf, y, ld, partials,   \
+                                                        su, sf);                                                \
         break;                                                                                                  \
     }
         MDKK_YI(0) MDKK_YI(1) MDKK_YI(2) MDKK_YI(3) MDKK_YI(4) MDKK_YI(5) MDKK_YI(6) MDKK_YI(7) MDKK_YI(8)

@@ -8,10 +8,10 @@
 
 #include "common.cuh"
 
-struct ZEntry {      // one U*U product of the Z-list adjoint (16 B, read as a warp broadcast)
+struct ZEntry {      // one U*U product of the Z-list adjoint (16 B, one broadcast LDS.128)
     double coef;
-    int code;        // g | h << 8 | f << 16 | conj_g << 24 | conj_h << 25 | last-of-output << 26 | center << 27
-    int pad;
+    int goff;        // byte offset of U[g] in the shared tile (g * row stride)
+    int hcode;       // byte offset of U[h] | conj_g << 20 | conj_h << 21 | last-of-output << 22 | center << 23
 };
 
 struct mdkk_snap {
@@ -21,6 +21,7 @@ struct mdkk_snap {
     int n_entries = 0;
     ZEntry* ent = nullptr;   // [n_entries], sorted by output
     int* chunk = nullptr;    // [kYW + 1] per-warp entry ranges (output-aligned, balanced)
+    int* chunkf = nullptr;   // [kYW] first output (half index) of each warp's range
     int* fmap = nullptr;     // [n_flat] half index | mirrored << 16 | odd sign << 17
 };
 
