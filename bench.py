@@ -121,7 +121,11 @@ def run_reference(args):
         return
     per_step = []
     from oracle import md
-    pos, L = md.lattice("fcc", LJ["rho"], (20, 20, 20))
+    # bounded sample: 20^3 cells (32,000 atoms, ~0.3 s per step on one core) for up to
+    # 200 timed steps, smaller cubes beyond so the whole run stays within a few minutes
+    total = max(1, args.steps + args.warmup)
+    cells = 20 if total <= 200 else max(6, int(20 * (200.0 / total) ** (1.0 / 3.0)))
+    pos, L = md.lattice("fcc", LJ["rho"], (cells, cells, cells))
     vel = md.seeded_velocities(len(pos), LJ["T"], 1.0, LJ["seed"])
     run = md.LJRun(pos, vel, L, rc=LJ["rc"], skin=LJ["skin"], style="full", newton=False, dt=LJ["dt"])
     run.forces()
@@ -133,13 +137,14 @@ def run_reference(args):
         per_step.append(time.perf_counter() - t0)
     tot = sum(per_step)
     value = len(pos) * args.steps / tot / 1e6
-    sample = (f"numpy oracle port of mdkk (oracle/md.py), LJ melt 32,000 atoms fcc rho 0.8442 rc 2.5 skin 0.3 "
-              f"T 1.44 dt 0.005 full list, {args.steps} steps after {args.warmup} warm-up")
+    sample = (f"numpy oracle port of mdkk (oracle/md.py), LJ melt {len(pos):,} atoms fcc rho 0.8442 rc 2.5 "
+              f"skin 0.3 T 1.44 dt 0.005 full list, {args.steps} steps after {args.warmup} warm-up")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "LJ melt, bounded CPU sample of configs[1] (32k atoms)", "n_atoms": len(pos)},
+        "config": {"workload": f"LJ melt, bounded CPU sample of configs[1] ({len(pos):,} atoms)",
+                   "n_atoms": len(pos)},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
 
