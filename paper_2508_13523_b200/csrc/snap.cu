@@ -26,32 +26,34 @@ namespace {
 // (16 lanes, previous level in shared memory as a full mirrored level),
 // accumulates f_c u in registers, and the full U_i row is written from C and
 // its mirror.
-template <int TWOJ>
-__global__ void __launch_bounds__(kWarps * 32, 4) k_snap_ui(const double* __restrict__ x, int n_local,
+template <int TWOJ, int TEAM, int DW>
+__global__ void __launch_bounds__(DW * 32, (TEAM == 16 ? 4 : 8 / DW)) k_snap_ui(const double* __restrict__ x, int n_local,
                                                          const int* __restrict__ table,
                                                          const int* __restrict__ counts, int cap, double rc,
                                                          double2* __restrict__ U, long long su, long long sf,
                                                          int* __restrict__ flags) {
     constexpr int NF = block_offset(TWOJ + 1);
+    constexpr int PPW = 32 / TEAM;                       // pairs in flight per warp
+    constexpr int NS = tslot_base<TEAM>(kMaxTwoJ + 1);   // accumulator slots per lane
     __shared__ RS rs;
-    __shared__ NbPair s_nb[kWarps][kNbChunk];
-    __shared__ cplx s_lvl[kWarps][2][2][kLevelMax];
-    for (int t = threadIdx.x; t < kWarps * 4 * kLevelMax; t += blockDim.x)
+    __shared__ NbPair s_nb[DW][kNbChunk];
+    __shared__ cplx s_lvl[DW][PPW][2][kLevelMax];
+    for (int t = threadIdx.x; t < DW * PPW * 2 * kLevelMax; t += blockDim.x)
         (&s_lvl[0][0][0][0])[t] = {0.0, 0.0};   // rec2 reads finite neighbours at the column ends
     stage_rs(rs);
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, hl = lane & 15, hh = lane >> 4;
-    const int i = blockIdx.x * kWarps + w;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, hl = lane & (TEAM - 1), hh = lane / TEAM;
+    const int i = blockIdx.x * DW + w;
     if (i >= n_local) return;
-    cplx acc[kHSlots];
+    cplx acc[NS];
 #pragma unroll
-    for (int s = 0; s < kHSlots; ++s) acc[s] = {0.0, 0.0};
+    for (int s = 0; s < NS; ++s) acc[s] = {0.0, 0.0};
     const double4 xi = mdkk::ld4(x, i);
     const int n = min(counts[i], cap);
     const double rc2 = rc * rc;
     bool bad = false;
     for (int k0 = 0; k0 < n; k0 += kNbChunk) {
         const int m = compact_pairs(x, table, cap, i, k0, n, xi, rc2, rc, s_nb[w], bad);
-        for (int t = 0; t < m; t += 2) {
+        for (int t = 0; t < m; t += PPW) {
             const int pi = t + hh;
             const NbPair nb = s_nb[w][pi < m ? pi : t];
             PairGeo g;
@@ -70,14 +72,14 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_snap_ui(const double* __rest
                 const cplx* prev = L[(tj - 1) & 1];
                 cplx* cur = L[tj & 1];
 #pragma unroll
-                for (int s = 0; s < half_slots(tj); ++s) {
-                    const int c = hl + 16 * s;
+                for (int s = 0; s < tslots<TEAM>(tj); ++s) {
+                    const int c = hl + TEAM * s;
                     if (c < half_size(tj)) {
                         int P, Q;
                         col_elem(tj, c, P, Q);
                         const cplx v = rec2(prev, tj, P, Q, rs, ab, g.b);
                         store_mirrored(cur, tj, P, Q, v);
-                        acc[hslot_base(tj) + s] = cadd(acc[hslot_base(tj) + s], cscale(fc, v));
+                        acc[tslot_base<TEAM>(tj) + s] = cadd(acc[tslot_base<TEAM>(tj) + s], cscale(fc, v));
                     }
                 }
                 __syncwarp();
@@ -85,23 +87,25 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_snap_ui(const double* __rest
         }
     }
     if (bad && lane == 0) atomicOr(flags, MDKK_FLAG_COINCIDENT);
-    // both halves own the same elements: fold the odd half onto the even one
+    // every team owns the same elements: fold the teams onto team 0
 #pragma unroll
-    for (int s = 0; s < kHSlots; ++s) {
-        acc[s].re += __shfl_xor_sync(0xffffffffu, acc[s].re, 16);
-        acc[s].im += __shfl_xor_sync(0xffffffffu, acc[s].im, 16);
-    }
+    for (int s = 0; s < NS; ++s)
+#pragma unroll
+        for (int o = 16; o >= TEAM; o >>= 1) {
+            acc[s].re += __shfl_xor_sync(0xffffffffu, acc[s].re, o);
+            acc[s].im += __shfl_xor_sync(0xffffffffu, acc[s].im, o);
+        }
     if (hh) return;
     double2* Ui = U + (long long)i * su;   // layout a: su = NF, sf = 1; layout b: su = 1, sf = ld
 #pragma unroll
     for (int tj = 0; tj <= TWOJ; ++tj)
 #pragma unroll
-        for (int s = 0; s < half_slots(tj); ++s) {
-            const int c = hl + 16 * s;
+        for (int s = 0; s < tslots<TEAM>(tj); ++s) {
+            const int c = hl + TEAM * s;
             if (c < half_size(tj)) {
                 int P, Q;
                 col_elem(tj, c, P, Q);
-                const cplx v = acc[hslot_base(tj) + s];
+                const cplx v = acc[tslot_base<TEAM>(tj) + s];
                 const int e = P * (tj + 1) + Q, em = (tj - P) * (tj + 1) + (tj - Q);
                 Ui[(block_offset(tj) + e) * sf] = make_double2(v.re, v.im);
                 if (em != e) {
@@ -111,6 +115,12 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_snap_ui(const double* __rest
             }
         }
 }
+
+#ifndef MDKK_UI_TEAM
+#define MDKK_UI_TEAM 16
+#endif
+constexpr int kUiTeam = MDKK_UI_TEAM;              // lanes per pair in k_snap_ui
+constexpr int kUiWarps = kUiTeam == 16 ? 4 : 2;    // atoms (warps) per CTA
 
 // ---------------------------------------------------------------- compute_yi
 // Half-block Y (outputs 2p < tj, or 2p == tj and 2q <= tj) as a list of U*U
@@ -225,27 +235,37 @@ __global__ void k_snap_y_compress(const double2* __restrict__ Y, int n, int nf, 
 // Same quantity (equal to rounding) for ~1/6 of the reference's complex MACs.
 // One warp per atom, two neighbours at a time (one per half-warp).
 constexpr int kLamMax = 41;   // half_size(8): lambda levels keep only their column-major C prefix
+#ifndef MDKK_DE_TEAM
+#define MDKK_DE_TEAM 8
+#endif
+#ifndef MDKK_DE_WARPS
+#define MDKK_DE_WARPS 2
+#endif
+constexpr int kDeTeam = MDKK_DE_TEAM;     // lanes per pair in k_snap_deidrj (4 pairs per warp at 8)
+constexpr int kDeWarps = MDKK_DE_WARPS;   // atoms (warps) per CTA
 
-template <int TWOJ>
-__global__ void __launch_bounds__(kWarps * 32, 4) k_snap_deidrj(const double* __restrict__ x, int n_local,
+// TEAM lanes expand one pair (32 / TEAM pairs per warp), DW warps (atoms) per CTA.
+template <int TWOJ, int TEAM, int DW>
+__global__ void __launch_bounds__(DW * 32, (TEAM == 16 ? 4 : 10 / DW)) k_snap_deidrj(const double* __restrict__ x, int n_local,
                                                              const int* __restrict__ table,
                                                              const int* __restrict__ counts, int cap, double rc,
                                                              const double2* __restrict__ Yh, int ld,
                                                              double* __restrict__ f) {
     constexpr int NU = block_offset(TWOJ) > 0 ? block_offset(TWOJ) : 1;   // levels 0..TWOJ-1 (the top is never re-read)
     constexpr int NH = half_offset(TWOJ + 1);
+    constexpr int PPW = 32 / TEAM;   // pairs in flight per warp
     extern __shared__ double s_dyn_d[];  // rs | pairs | Y_i (C order) | u levels | lambda C prefixes
     RS& rs = *reinterpret_cast<RS*>(s_dyn_d);
     auto s_nb = reinterpret_cast<NbPair(*)[kNbChunk]>(reinterpret_cast<char*>(s_dyn_d) + sizeof(RS));
-    auto s_y = reinterpret_cast<cplx(*)[NH]>(s_nb + kWarps);
-    auto s_u = reinterpret_cast<cplx(*)[2][NU]>(s_y + kWarps);
-    auto s_l = reinterpret_cast<cplx(*)[2][2][kLamMax]>(s_u + kWarps);
+    auto s_y = reinterpret_cast<cplx(*)[NH]>(s_nb + DW);
+    auto s_u = reinterpret_cast<cplx(*)[PPW][NU]>(s_y + DW);
+    auto s_l = reinterpret_cast<cplx(*)[PPW][2][kLamMax]>(s_u + DW);
     // zero the level buffers once: the branch-free edges read finite neighbours
-    for (int t = threadIdx.x; t < kWarps * 2 * (NU + 2 * kLamMax); t += blockDim.x)
+    for (int t = threadIdx.x; t < DW * PPW * (NU + 2 * kLamMax); t += blockDim.x)
         reinterpret_cast<cplx*>(s_u)[t] = {0.0, 0.0};
     stage_rs(rs);
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, hl = lane & 15, hh = lane >> 4;
-    const int i = blockIdx.x * kWarps + w;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, hl = lane & (TEAM - 1), hh = lane / TEAM;
+    const int i = blockIdx.x * DW + w;
     if (i >= n_local) return;
     // Y_i at the column-half elements, in the lanes' (column-major) order, from the row-half Yh
 #pragma unroll
@@ -270,7 +290,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_snap_deidrj(const double* __
     bool bad = false;
     for (int k0 = 0; k0 < n; k0 += kNbChunk) {
         const int m = compact_pairs(x, table, cap, i, k0, n, xi, rc2, rc, s_nb[w], bad);
-        for (int t = 0; t < m; t += 2) {
+        for (int t = 0; t < m; t += PPW) {
             const int pi = t + hh;
             const bool active = pi < m;
             const NbPair nb = s_nb[w][active ? pi : t];
@@ -288,8 +308,8 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_snap_deidrj(const double* __
 #pragma unroll
             for (int tj = 1; tj <= TWOJ; ++tj) {
 #pragma unroll
-                for (int s = 0; s < half_slots(tj); ++s) {
-                    const int c = hl + 16 * s;
+                for (int s = 0; s < tslots<TEAM>(tj); ++s) {
+                    const int c = hl + TEAM * s;
                     if (c < half_size(tj)) {
                         int P, Q;
                         col_elem(tj, c, P, Q);
@@ -310,8 +330,8 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_snap_deidrj(const double* __
                 const cplx* ln = lam[(tj + 1) & 1];   // level tj+1, column-major (stride tj+2), valid on C_{tj+1}
                 const cplx* v = ul + block_offset(tj - 1);
 #pragma unroll
-                for (int s = 0; s < half_slots(tj); ++s) {
-                    const int c = hl + 16 * s;
+                for (int s = 0; s < tslots<TEAM>(tj); ++s) {
+                    const int c = hl + TEAM * s;
                     if (c < half_size(tj)) {
                         int P, Q;
                         col_elem(tj, c, P, Q);
@@ -354,7 +374,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_snap_deidrj(const double* __
                 double v = g.dfc * (d[q] / g.r) * S +
                            g.fc * ((Ga.re * da[q].re + Ga.im * da[q].im) + (Gb.re * db[q].re - Gb.im * db[q].im));
 #pragma unroll
-                for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                for (int o = TEAM / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
                 tt[q] = v;
             }
             if (hl == 0 && active) {
@@ -369,7 +389,9 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_snap_deidrj(const double* __
         }
     }
 #pragma unroll
-    for (int q = 0; q < 3; ++q) fi[q] += __shfl_xor_sync(0xffffffffu, fi[q], 16);
+    for (int q = 0; q < 3; ++q)
+#pragma unroll
+        for (int o = 16; o >= TEAM; o >>= 1) fi[q] += __shfl_xor_sync(0xffffffffu, fi[q], o);
     if (lane == 0) {
         double* p = f + 4LL * i;
         atomicAdd(p + 0, fi[0]);
@@ -463,9 +485,19 @@ int mdkk_snap_ui(mdkk_snap* s, const double* x, int n_local, const int* table, c
     const long long su = layout ? 1 : s->n_flat, sf = layout ? ldu : 1;
     if (n_local == 0) return MDKK_OK;
     upload_weights();
-    const int nb = (n_local + kWarps - 1) / kWarps;
-    MDKK_SNAP_DISPATCH(s->twojmax, k_snap_ui, nb, kWarps * 32, mdkk::as_stream(stream), x, n_local, table, counts,
-                       cap, rc, reinterpret_cast<double2*>(U), su, sf, flags);
+    const int nb = (n_local + kUiWarps - 1) / kUiWarps;
+    cudaStream_t st = mdkk::as_stream(stream);
+    double2* u = reinterpret_cast<double2*>(U);
+    switch (s->twojmax) {
+#define MDKK_UI(TJ)                                                                                          \
+    case TJ:                                                                                                 \
+        k_snap_ui<TJ, kUiTeam, kUiWarps><<<nb, kUiWarps * 32, 0, st>>>(x, n_local, table, counts, cap, rc, u,  \
+                                                                      su, sf, flags);                        \
+        break;
+        MDKK_UI(0) MDKK_UI(1) MDKK_UI(2) MDKK_UI(3) MDKK_UI(4) MDKK_UI(5) MDKK_UI(6) MDKK_UI(7) MDKK_UI(8)
+#undef MDKK_UI
+        default: return MDKK_E_ARG;
+    }
     MDKK_CHECK_LAUNCH("k_snap_ui");
     return MDKK_OK;
 }
@@ -535,15 +567,16 @@ int mdkk_snap_deidrj(mdkk_snap* s, const double* x, int n_local, const int* tabl
     if (!s || n_local < 0 || cap < 1 || ld < n_local) return MDKK_E_ARG;
     if (n_local == 0) return MDKK_OK;
     upload_weights();
-    const int nb = (n_local + kWarps - 1) / kWarps;
     switch (s->twojmax) {
 #define MDKK_DE(TJ)                                                                                          \
     case TJ: {                                                                                               \
-        const size_t sm = sizeof(RS) + kWarps * (kNbChunk * sizeof(NbPair) +                                 \
-            (half_offset(TJ + 1) + 2 * (block_offset(TJ) > 0 ? block_offset(TJ) : 1) + 4 * kLamMax) *         \
+        constexpr int TEAM = kDeTeam, DW = kDeWarps, PPW = 32 / TEAM;                                        \
+        const size_t sm = sizeof(RS) + DW * (kNbChunk * sizeof(NbPair) +                                     \
+            (half_offset(TJ + 1) + PPW * ((block_offset(TJ) > 0 ? block_offset(TJ) : 1) + 2 * kLamMax)) *    \
             sizeof(cplx));                                                                                   \
-        cudaFuncSetAttribute(k_snap_deidrj<TJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);      \
-        k_snap_deidrj<TJ><<<nb, kWarps * 32, sm, mdkk::as_stream(stream)>>>(                                 \
+        cudaFuncSetAttribute(k_snap_deidrj<TJ, TEAM, DW>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
+                             (int)sm);                                                                       \
+        k_snap_deidrj<TJ, TEAM, DW><<<(n_local + DW - 1) / DW, DW * 32, sm, mdkk::as_stream(stream)>>>(      \
             x, n_local, table, counts, cap, rc, reinterpret_cast<const double2*>(Yh), ld, f);                \
         break;                                                                                               \
     }

@@ -169,6 +169,15 @@ __host__ __device__ constexpr int hslot_base(int tj) {
     for (int t = 0; t < tj; ++t) s += half_slots(t);
     return s;
 }
+// slots of a TEAM-lane team over the column halves (level tj) and their prefix
+template <int TEAM>
+__host__ __device__ constexpr int tslots(int tj) { return (half_size(tj) + TEAM - 1) / TEAM; }
+template <int TEAM>
+__host__ __device__ constexpr int tslot_base(int tj) {
+    int s = 0;
+    for (int t = 0; t < tj; ++t) s += tslots<TEAM>(t);
+    return s;
+}
 constexpr int kHSlots = hslot_base(kMaxTwoJ + 1);        // 14 per half-warp lane at 2J = 8
 constexpr int kHalfMax = half_size(kMaxTwoJ);            // 41
 constexpr int kHalfAll = half_offset(kMaxTwoJ + 1);      // 145
