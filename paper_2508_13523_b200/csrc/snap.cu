@@ -167,13 +167,18 @@ __global__ void __launch_bounds__(kYW * 32, 2) k_snap_yi(const double2* __restri
     const char* su_l = reinterpret_cast<const char*>(s_u + lane);
     ZEntry* se = s_e + w * 32;
     double are = 0.0, aim = 0.0, en = 0.0;
+    int last_g = -1;      // products are sorted by g inside an output: half reuse the previous U[g]
+    double2 ug = make_double2(0.0, 0.0);
     for (int base = beg; base < end; base += 32) {
         if (base + lane < end) se[lane] = ent[base + lane];
         __syncwarp();
         const int cnt = min(32, end - base);
         for (int j = 0; j < cnt; ++j) {
             const ZEntry e = se[j];
-            const double2 ug = *reinterpret_cast<const double2*>(su_l + e.goff);
+            if (e.goff != last_g) {   // warp-uniform
+                ug = *reinterpret_cast<const double2*>(su_l + e.goff);
+                last_g = e.goff;
+            }
             const double2 uh = *reinterpret_cast<const double2*>(su_l + (e.hcode & 0xfffff));
             const double gy = flip_sign(ug.y, ((unsigned)e.hcode << 11) & 0x80000000u);   // conj_g
             const double hy = flip_sign(uh.y, ((unsigned)e.hcode << 10) & 0x80000000u);   // conj_h

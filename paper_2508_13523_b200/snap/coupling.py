@@ -308,9 +308,44 @@ def zlist_apply(U: np.ndarray, twojmax: int, entries) -> np.ndarray:
     return Y
 
 
+def _reuse_order(f, g, h, cg_, ch_):
+    """Order the products of each output into runs sharing their first operand.
+
+    The yi kernel keeps the last U[g] in registers, so a product whose g equals
+    the previous one costs one shared-memory load instead of two.  Greedy cover
+    per output: repeatedly take the operand that appears in most remaining
+    products, orient those products so it is g (U[g] U[h] commutes; each
+    operand keeps its own conj flag), emit them sorted by h.
+    """
+    order, swap = [], np.zeros(len(f), dtype=bool)
+    starts = np.flatnonzero(np.r_[True, f[1:] != f[:-1]])
+    ends = np.r_[starts[1:], len(f)]
+    for a, b in zip(starts, ends):
+        remaining = list(range(a, b))
+        while remaining:
+            cnt: dict = {}
+            for k in remaining:
+                cnt[g[k]] = cnt.get(g[k], 0) + 1
+                if h[k] != g[k]:
+                    cnt[h[k]] = cnt.get(h[k], 0) + 1
+            best = max(sorted(cnt), key=lambda o: cnt[o])
+            take = [k for k in remaining if g[k] == best or h[k] == best]
+            for k in take:
+                swap[k] = g[k] != best
+            take.sort(key=lambda k: (g[k] if swap[k] else h[k]))
+            order.extend(take)
+            remaining = [k for k in remaining if not (g[k] == best or h[k] == best)]
+    order = np.asarray(order, dtype=np.int64)
+    g2, h2 = np.where(swap, h, g), np.where(swap, g, h)
+    c2g, c2h = np.where(swap, ch_, cg_), np.where(swap, cg_, ch_)
+    return order, g2, h2, c2g, c2h
+
+
 def device_product_list(tables: CouplingTables, beta):
     """Packed (coef, code, n_half, fmap) for mdkk_snap_create (include/mdkk_b200.h)."""
     f, g, h, cg_, ch_, coef = zlist_entries(tables, beta)
+    order, g, h, cg_, ch_ = _reuse_order(f, g, h, cg_, ch_)
+    f, g, h, cg_, ch_, coef = f[order], g[order], h[order], cg_[order], ch_[order], coef[order]
     hmap, n_half = _half_index(tables.index.twojmax)
     center = np.zeros(n_half, dtype=np.int64)
     for (tj, p, q), (k, mir, _) in hmap.items():

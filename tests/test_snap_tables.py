@@ -147,3 +147,17 @@ def test_reverse_mode_pair_force_matches_forward_mode(tjm):
         t_ref = np.einsum("f,df->d", Y, np.conj(wdu[0])).real
         t = _pair_force_reverse(d, Y, tjm, 4.73)
         assert np.abs(t - t_ref).max() <= 1e-13 * np.abs(t_ref).max()
+
+
+def test_packed_reuse_ordered_list_still_equals_adjoint():
+    """The device list (greedy operand-reuse order, operands swapped where needed) computes
+    the same Y as the canonical Z-list, and is ordered for U[g] reuse."""
+    tjm = 8
+    beta = np.linspace(0.05, 0.1, 55)
+    o, U = _u_field(tjm, beta, 21)
+    coef, code, n_half, _ = device_product_list(make_coupling_tables(4.0), beta)
+    dec = (code >> 16) & 255, code & 255, (code >> 8) & 255, (code >> 24) & 1, (code >> 25) & 1, coef
+    Y = o.compute_y(U)
+    assert np.abs(zlist_apply(U, tjm, dec) - Y).max() <= 1e-13 * np.abs(Y).max()
+    f, g = dec[0], dec[1]
+    assert np.sum((f[1:] == f[:-1]) & (g[1:] == g[:-1])) > 0.65 * len(f)
