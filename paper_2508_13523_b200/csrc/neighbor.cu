@@ -113,6 +113,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_nbr_build(
     // cluster-relative FP32 coordinates, SoA: an aligned float2 = two candidates for the packed
     // FFMA2/FADD2 prefilter (one broadcast LDS.64 per coordinate and candidate pair)
     __shared__ __align__(16) float s_rel[kWarps][3][kChunk];
+    __shared__ int64_t s_gid[STYLE == 1 ? kWarps : 1][kChunk];      // half lists: the style predicate's
+    __shared__ int s_rank[(STYLE == 1 && NEWTON) ? kWarps : 1][kChunk];  // gids / owner ranks, staged
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int c = blockIdx.x * kWarps + w;
     const int ncl = (n_local + 31) >> 5;
@@ -124,6 +126,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_nbr_build(
     float* sfx = s_rel[w][0];
     float* sfy = s_rel[w][1];
     float* sfz = s_rel[w][2];
+    int64_t* sgid = s_gid[STYLE == 1 ? w : 0];
+    int* srk = s_rank[(STYLE == 1 && NEWTON) ? w : 0];
     const int i = c * 32 + lane;
     const bool valid = i < n_local;
     const double4 xi = mdkk::ld4(x, valid ? i : c * 32);
@@ -172,16 +176,18 @@ __global__ void __launch_bounds__(kWarps * 32) k_nbr_build(
     int cnt = 0;
     const int64_t gi = (STYLE == 1 && valid) ? gid[i] : 0;
     int* trow = table + ((long long)c * cap) * 32 + lane;
-    auto visit = [&](int j, double px, double py, double pz) {
+    // jgid / jrank: the candidate's global id and owner rank (staged in shared memory
+    // for the union scan; read from global memory on the overflow path)
+    auto visit = [&](int j, double px, double py, double pz, int64_t jgid, int jrank) {
         if (!valid || j == i) return;
         const double r2 = mdkk::r2_exact(px - xi.x, py - xi.y, pz - xi.z);
         if (!(r2 < bc2)) return;
         if (STYLE == 1) {
             bool keep;
             if (j < n_local) {
-                keep = gi < gid[j];
+                keep = gi < jgid;
             } else if (NEWTON) {
-                const int orank = owner_rank[j];
+                const int orank = jrank;
                 keep = orank > my_rank || (orank == my_rank && lex_zyx_less(xi.x, xi.y, xi.z, px, py, pz));
             } else {
                 keep = true;
@@ -202,6 +208,11 @@ __global__ void __launch_bounds__(kWarps * 32) k_nbr_build(
                 sfx[t] = (float)(p.x - ccx);
                 sfy[t] = (float)(p.y - ccy);
                 sfz[t] = (float)(p.z - ccz);
+                if (STYLE == 1) {
+                    const int j = su[u0 + t];
+                    sgid[t] = gid[j];
+                    if (NEWTON) srk[t] = owner_rank[j];
+                }
             }
             __syncwarp();
             // branch-free prefilter into a per-lane bit mask, then each lane visits only
@@ -246,7 +257,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_nbr_build(
                 while (bits) {
                     const int t = h0 + __ffs(bits) - 1;
                     bits &= bits - 1u;
-                    visit(su[u0 + t], spx[t], spy[t], spz[t]);
+                    visit(su[u0 + t], spx[t], spy[t], spz[t], STYLE == 1 ? sgid[t] : 0,
+                          (STYLE == 1 && NEWTON) ? srk[t] : 0);
                 }
             }
             __syncwarp();
@@ -259,7 +271,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_nbr_build(
                 for (int s = cell_start[kr.x]; s < s1; ++s) {
                     const int j = cell_atoms[s];
                     const double4 p = mdkk::ld4(x, j);
-                    visit(j, p.x, p.y, p.z);
+                    visit(j, p.x, p.y, p.z, STYLE == 1 ? gid[j] : 0,
+                          (STYLE == 1 && NEWTON && j >= n_local) ? owner_rank[j] : 0);
                 }
             }
     }
