@@ -469,6 +469,13 @@ class DistSystem:
         G = [torch.empty_like(gid) for _ in range(self.world)]
         _all_gather(R, rows, self.group)
         _all_gather(G, gid, self.group)
+        if self.dense_gids and sum(ns) == self.n_atoms:
+            # gids are 0..N-1: place rows by gid on the device, one read-back
+            out = torch.empty((max(self.n_atoms, 1), width), dtype=t.dtype, device=self.device)
+            for r, g, k in zip(R, G, ns):
+                if k:
+                    out[g[:k]] = r[:k]
+            return out[: self.n_atoms].cpu().numpy(), np.arange(self.n_atoms, dtype=np.int64)
         rows = np.concatenate([r[:k].cpu().numpy() for r, k in zip(R, ns)])
         gids = np.concatenate([g[:k].cpu().numpy() for g, k in zip(G, ns)])
         o = np.argsort(gids, kind="stable")
