@@ -161,14 +161,25 @@ class SnapState:
         else:
             rm = LayoutPolicy.row_major(2)   # device rows are atoms: one warp streams one atom's entries
             self.U_dev = torch.zeros(shape, dtype=torch.complex128, device=self.device)
-        self.Y_dev = torch.zeros_like(self.U_dev)
         self.Yh_dev = torch.zeros((n_half, self.ld), dtype=torch.complex128, device=self.device)
-        self._y_expanded = True   # Y_dev agrees with Yh_dev
+        self._y_expanded = True   # the reference-layout Y (if any) agrees with Yh_dev
         self.U = DualArray(shape, layout_b=rm, dtype=np.complex128, device=self.device, storage_b=self.U_dev)
-        self.Y = DualArray(shape, layout_b=rm, dtype=np.complex128, device=self.device, storage_b=self.Y_dev)
+        # the reference-layout Y (n x n_flat, as large as U) exists only once something reads
+        # or writes it: the engine itself works on the half set Yh
+        self._shape, self._rm = shape, rm
+        self._Y = None
+        self.Y_dev = None
         self.energy_dev = torch.zeros(1, dtype=torch.float64, device=self.device)
         self.flags = torch.zeros(1, dtype=torch.int32, device=self.device)
         self._handle = None
+
+    @property
+    def Y(self) -> DualArray:
+        if self._Y is None:
+            self.Y_dev = torch.zeros_like(self.U_dev)
+            self._Y = DualArray(self._shape, layout_b=self._rm, dtype=np.complex128, device=self.device,
+                                storage_b=self.Y_dev)
+        return self._Y
 
     def handle(self) -> _Handle:
         if self._handle is None:
@@ -184,18 +195,19 @@ class SnapState:
 
     def expand_y(self) -> None:
         """Reference layout Y (n, n_flat) from the engine's half/transposed Yh (after compute_yi)."""
-        if self._y_expanded:
+        if self._y_expanded and self._Y is not None:
             return
+        Y = self.Y   # allocated on first use
         _lib.check(_lib.lib().mdkk_snap_y_expand(self.handle().ptr, self.Yh_dev.data_ptr(), self.ld, self.n_atoms,
                                                  self.Y_dev.data_ptr(), self._lay, self.ld, _lib.stream(self.device)),
                    "mdkk_snap_y_expand")
-        self.Y.modified_a = False
-        self.Y.mark_modified("b")
+        Y.modified_a = False
+        Y.mark_modified("b")
         self._y_expanded = True
 
     def sync_yh(self) -> None:
         """Engine Yh current: a host-written reference-layout Y is compressed into it."""
-        if self.Y.modified_a:
+        if self._Y is not None and self._Y.modified_a:
             self.Y.sync("b")
             _lib.check(_lib.lib().mdkk_snap_y_compress(self.handle().ptr, self.Y_dev.data_ptr(), self.n_atoms,
                                                        self.Yh_dev.data_ptr(), self.ld, self._lay, self.ld,
@@ -232,8 +244,9 @@ def compute_yi(state: SnapState) -> None:
                                            state._lay, state.ld, _lib.stream(state.device)), "mdkk_snap_yi")
     if len(tiles) > 1:
         state.energy_dev.copy_(e_t.sum().reshape(1))
-    state.Y.modified_a = False
-    state.Y.modified_b = False
+    if state._Y is not None:
+        state._Y.modified_a = False
+        state._Y.modified_b = False
     state._y_expanded = False
 
 
