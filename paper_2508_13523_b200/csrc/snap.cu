@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(DW * 32, (TEAM == 16 ? 4 : 8 / DW)) k_snap_ui(
                         int P, Q;
                         col_elem(tj, c, P, Q);
                         const cplx v = rec2(prev, tj, P, Q, rs, ab, g.b);
-                        store_mirrored(cur, tj, P, Q, v);
+                        if (tj < TWOJ) store_mirrored(cur, tj, P, Q, v);   // the top level is never re-read
                         acc[tslot_base<TEAM>(tj) + s] = cadd(acc[tslot_base<TEAM>(tj) + s], cscale(fc, v));
                     }
                 }
