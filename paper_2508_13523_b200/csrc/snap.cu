@@ -5,16 +5,15 @@
 // rmin0 = 0, plain cosine switch, no self term, full (tj+1)^2 blocks and the
 // full three-slot adjoint Y.
 //
-// Data: U, Y are complex128 row-major [n_atoms][n_flat] (the reference's
-// layout "a"), double2 = (re, im).
+// Data: U complex128 in the state's layout (a: [n][n_flat], b: [n_flat][ld]);
+// the engine's Y is the half set, transposed (Yh[e][i]); double2 = (re, im).
 //
-// compute_ui / fused deidrj: one warp per atom, its neighbours processed one
-// at a time; the warp computes each level of the Wigner-U recursion with the
-// level's elements spread over lanes (element idx -> lane idx%32, slot idx/32)
-// and the previous level in shared memory.  Each lane keeps its 14 slots of
-// U_i (ui) or Y_i (deidrj) in registers, so the per-atom sums need no atomics.
-// compute_yi: one warp per atom over an output-sorted contribution list staged
-// through shared memory; compute_fused_deidrj in reverse mode (see below).
+// compute_ui: one warp per atom; each team of lanes expands one neighbour at a
+// time with the two-term column recursion over the column halves C_tj (the
+// previous level mirrored into shared memory), keeping its slots of U_i in
+// registers (no atomics).  compute_yi: atoms across lanes over a shared U tile,
+// the Z-list product stream as warp broadcasts.  compute_fused_deidrj: reverse
+// mode over the same recursion (u forward, adjoint backward), 8-lane teams.
 #include "snap_common.cuh"
 
 namespace {

@@ -29,18 +29,10 @@ namespace {
 
 constexpr int kMaxTwoJ = 8;
 constexpr int kLevelMax = (kMaxTwoJ + 1) * (kMaxTwoJ + 1);  // 81
-constexpr int kSlots = 14;                                   // sum_tj ceil((tj+1)^2 / 32) for 2J = 8
 constexpr int kWarps = 4;
 constexpr double kPi = 3.141592653589793;
 
-__host__ __device__ constexpr int level_size(int tj) { return (tj + 1) * (tj + 1); }
-__host__ __device__ constexpr int level_slots(int tj) { return (level_size(tj) + 31) / 32; }
 __host__ __device__ constexpr int block_offset(int tj) { return tj * (tj + 1) * (2 * tj + 1) / 6; }
-__host__ __device__ constexpr int slot_base(int tj) {
-    int s = 0;
-    for (int t = 0; t < tj; ++t) s += level_slots(t);
-    return s;
-}
 
 struct cplx {
     double re, im;
@@ -163,12 +155,6 @@ __host__ __device__ constexpr int half_offset(int tj) {
     for (int t = 0; t < tj; ++t) s += half_size(t);
     return s;
 }
-__host__ __device__ constexpr int half_slots(int tj) { return (half_size(tj) + 15) / 16; }
-__host__ __device__ constexpr int hslot_base(int tj) {
-    int s = 0;
-    for (int t = 0; t < tj; ++t) s += half_slots(t);
-    return s;
-}
 // slots of a TEAM-lane team over the column halves (level tj) and their prefix
 template <int TEAM>
 __host__ __device__ constexpr int tslots(int tj) { return (half_size(tj) + TEAM - 1) / TEAM; }
@@ -178,8 +164,6 @@ __host__ __device__ constexpr int tslot_base(int tj) {
     for (int t = 0; t < tj; ++t) s += tslots<TEAM>(t);
     return s;
 }
-constexpr int kHSlots = hslot_base(kMaxTwoJ + 1);        // 14 per half-warp lane at 2J = 8
-constexpr int kHalfMax = half_size(kMaxTwoJ);            // 41
 constexpr int kHalfAll = half_offset(kMaxTwoJ + 1);      // 145
 
 // Store element (P, Q) of a full level held COLUMN-major in shared memory
