@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(DW * 32, (TEAM == 16 ? 4 : 8 / DW)) k_snap_ui(
                         int P, Q;
                         col_elem(tj, c, P, Q);
                         const cplx v = rec2(prev, tj, P, Q, rs, ab, g.b);
-                        if (tj < TWOJ) store_mirrored(cur, tj, P, Q, v);   // the top level is never re-read
+                        if (tj < TWOJ) store_for_next(cur, tj, P, Q, v);   // the top level is never re-read
                         acc[tslot_base<TEAM>(tj) + s] = cadd(acc[tslot_base<TEAM>(tj) + s], cscale(fc, v));
                     }
                 }
@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(DW * 32, (TEAM == 16 ? 4 : 10 / DW)) k_snap_de
                         int P, Q;
                         col_elem(tj, c, P, Q);
                         const cplx v = rec2(ul + block_offset(tj - 1), tj, P, Q, rs, ab, g.b);
-                        if (tj < TWOJ) store_mirrored(ul + block_offset(tj), tj, P, Q, v);
+                        if (tj < TWOJ) store_for_next(ul + block_offset(tj), tj, P, Q, v);
                         const cplx yv = sy[half_offset(tj) + c];
                         const double wgt = (2 * P == tj && 2 * Q == tj) ? 1.0 : 2.0;
                         S += wgt * (yv.re * v.re + yv.im * v.im);

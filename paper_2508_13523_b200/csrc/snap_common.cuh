@@ -169,6 +169,17 @@ constexpr int kHalfAll = half_offset(kMaxTwoJ + 1);      // 145
 // Store element (P, Q) of a full level held COLUMN-major in shared memory
 // (L[Q*(tj+1) + P]: lanes walk C_tj down a column, so reads and writes of a
 // half-warp hit consecutive 16-byte words) and its mirror.
+// Store (P, Q) of C_tj for the next level's recursion: the next level reads
+// columns 0..(tj+1)>>1 only, i.e. C_tj plus the mirror image of C_tj's last
+// column (Q == tj>>1), so only that column writes its mirror.
+__device__ __forceinline__ void store_for_next(cplx* L, int tj, int P, int Q, cplx v) {
+    L[Q * (tj + 1) + P] = v;
+    if (Q == (tj >> 1)) {
+        const double sg = ((P + Q) & 1) ? -1.0 : 1.0;
+        L[(tj - Q) * (tj + 1) + (tj - P)] = {sg * v.re, -sg * v.im};
+    }
+}
+
 __device__ __forceinline__ void store_mirrored(cplx* L, int tj, int P, int Q, cplx v) {
     L[Q * (tj + 1) + P] = v;
     const int hm = (tj - Q) * (tj + 1) + (tj - P);
