@@ -255,7 +255,8 @@ __global__ void __launch_bounds__(DW * 32, (TEAM == 16 ? 4 : 10 / DW)) k_snap_de
                                                              const int* __restrict__ counts, int cap, double rc,
                                                              const double2* __restrict__ Yh, int ld,
                                                              double* __restrict__ f) {
-    constexpr int NU = block_offset(TWOJ) > 0 ? block_offset(TWOJ) : 1;   // levels 0..TWOJ-1 (the top is never re-read)
+    // levels 0..TWOJ-1 in compact storage (the top is never re-read), +pad for the clamped edge reads
+    constexpr int NU = lvl_offset(TWOJ) + TWOJ + 1;
     constexpr int NH = half_offset(TWOJ + 1);
     constexpr int PPW = 32 / TEAM;   // pairs in flight per warp
     extern __shared__ double s_dyn_d[];  // rs | pairs | Y_i (C order) | u levels | lambda C prefixes
@@ -317,8 +318,8 @@ __global__ void __launch_bounds__(DW * 32, (TEAM == 16 ? 4 : 10 / DW)) k_snap_de
                     if (c < half_size(tj)) {
                         int P, Q;
                         col_elem(tj, c, P, Q);
-                        const cplx v = rec2(ul + block_offset(tj - 1), tj, P, Q, rs, ab, g.b);
-                        if (tj < TWOJ) store_for_next(ul + block_offset(tj), tj, P, Q, v);
+                        const cplx v = rec2(ul + lvl_offset(tj - 1), tj, P, Q, rs, ab, g.b);
+                        if (tj < TWOJ) store_for_next(ul + lvl_offset(tj), tj, P, Q, v);
                         const cplx yv = sy[half_offset(tj) + c];
                         const double wgt = (2 * P == tj && 2 * Q == tj) ? 1.0 : 2.0;
                         S += wgt * (yv.re * v.re + yv.im * v.im);
@@ -332,7 +333,7 @@ __global__ void __launch_bounds__(DW * 32, (TEAM == 16 ? 4 : 10 / DW)) k_snap_de
             for (int tj = TWOJ; tj >= 1; --tj) {
                 cplx* lc = lam[tj & 1];
                 const cplx* ln = lam[(tj + 1) & 1];   // level tj+1, column-major (stride tj+2), valid on C_{tj+1}
-                const cplx* v = ul + block_offset(tj - 1);
+                const cplx* v = ul + lvl_offset(tj - 1);
 #pragma unroll
                 for (int s = 0; s < tslots<TEAM>(tj); ++s) {
                     const int c = hl + TEAM * s;
@@ -576,7 +577,7 @@ int mdkk_snap_deidrj(mdkk_snap* s, const double* x, int n_local, const int* tabl
     case TJ: {                                                                                               \
         constexpr int TEAM = kDeTeam, DW = kDeWarps, PPW = 32 / TEAM;                                        \
         const size_t sm = sizeof(RS) + DW * (kNbChunk * sizeof(NbPair) +                                     \
-            (half_offset(TJ + 1) + PPW * ((block_offset(TJ) > 0 ? block_offset(TJ) : 1) + 2 * kLamMax)) *    \
+            (half_offset(TJ + 1) + PPW * (lvl_offset(TJ) + TJ + 1 + 2 * kLamMax)) *                           \
             sizeof(cplx));                                                                                   \
         cudaFuncSetAttribute(k_snap_deidrj<TJ, TEAM, DW>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
                              (int)sm);                                                                       \

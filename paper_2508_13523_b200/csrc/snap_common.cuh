@@ -155,6 +155,15 @@ __host__ __device__ constexpr int half_offset(int tj) {
     for (int t = 0; t < tj; ++t) s += half_size(t);
     return s;
 }
+// Compact column-major level storage for the recursion: level t keeps columns
+// 0..(t+1)>>1 (all the next level reads: C_t plus the mirror of its last column).
+__host__ __device__ constexpr int lvl_size(int t) { return (t + 1) * (((t + 1) >> 1) + 1); }
+__host__ __device__ constexpr int lvl_offset(int t) {
+    int s = 0;
+    for (int k = 0; k < t; ++k) s += lvl_size(k);
+    return s;
+}
+
 // slots of a TEAM-lane team over the column halves (level tj) and their prefix
 template <int TEAM>
 __host__ __device__ constexpr int tslots(int tj) { return (half_size(tj) + TEAM - 1) / TEAM; }
