@@ -26,18 +26,46 @@ __device__ __forceinline__ bool in_combo(const double4& p, const double* c) {
     return sx >= c[0] && sx < c[3] && sy >= c[1] && sy < c[4] && sz >= c[2] && sz < c[5];
 }
 
+// Per-thread bit mask of the combos (<= 64 per call) the atom falls in, and the
+// block-wide OR: blocks of cell-sorted rows are compact, so most of them touch no
+// halo at all and skip every per-combo block reduction.
+__device__ __forceinline__ unsigned long long combo_mask(const double4& p, const double* sc, int c0, int C,
+                                                         bool valid) {
+    unsigned long long m = 0ull;
+    if (valid)
+        for (int c = c0; c < min(C, c0 + 64); ++c)
+            if (in_combo(p, sc + 9 * c)) m |= 1ull << (c - c0);
+    return m;
+}
+
+__device__ __forceinline__ unsigned long long block_or(unsigned long long m, unsigned long long* s_or) {
+    if (threadIdx.x == 0) *s_or = 0ull;
+    __syncthreads();
+    for (int o = 16; o > 0; o >>= 1) m |= __shfl_xor_sync(0xffffffffu, m, o);
+    if ((threadIdx.x & 31) == 0 && m) atomicOr(s_or, m);
+    __syncthreads();
+    return *s_or;
+}
+
 __global__ void k_halo_count(const double* __restrict__ x, int n, const double* __restrict__ combos,
                              int C, int* __restrict__ block_counts) {
     extern __shared__ double sc[];
+    __shared__ unsigned long long s_or;
     for (int t = threadIdx.x; t < 9 * C; t += blockDim.x) sc[t] = combos[t];
     __syncthreads();
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     double4 p = make_double4(0, 0, 0, 0);
     if (i < n) p = mdkk::ld4(x, i);
-    for (int c = 0; c < C; ++c) {
-        int flag = (i < n) && in_combo(p, sc + 9 * c);
-        int cnt = __syncthreads_count(flag);
-        if (threadIdx.x == 0) block_counts[(long long)blockIdx.x * C + c] = cnt;
+    for (int c0 = 0; c0 < C; c0 += 64) {   // combos in groups of 64 (one mask word)
+        const unsigned long long mine = combo_mask(p, sc, c0, C, i < n);
+        const unsigned long long any = block_or(mine, &s_or);
+        for (int c = c0; c < min(C, c0 + 64); ++c) {
+            int cnt = 0;
+            if ((any >> (c - c0)) & 1ull)   // block-uniform branch
+                cnt = __syncthreads_count((int)((mine >> (c - c0)) & 1ull));
+            if (threadIdx.x == 0) block_counts[(long long)blockIdx.x * C + c] = cnt;
+        }
+        __syncthreads();
     }
 }
 
@@ -86,6 +114,7 @@ __global__ void k_halo_fill(const double* __restrict__ x, int n, const double* _
     extern __shared__ double sc[];
     int* base = reinterpret_cast<int*>(sc + 9 * C);
     __shared__ int warp_cnt[kHaloBlock / 32];
+    __shared__ unsigned long long s_or;
     for (int t = threadIdx.x; t < 9 * C; t += blockDim.x) sc[t] = combos[t];
     if (threadIdx.x == 0) {
         int s = 0;
@@ -99,8 +128,14 @@ __global__ void k_halo_fill(const double* __restrict__ x, int n, const double* _
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     double4 p = make_double4(0, 0, 0, 0);
     if (i < n) p = mdkk::ld4(x, i);
-    for (int c = 0; c < C; ++c) {
-        bool flag = (i < n) && in_combo(p, sc + 9 * c);
+    for (int c0 = 0; c0 < C; c0 += 64) {   // combos in groups of 64 (one mask word)
+    const unsigned long long mine = combo_mask(p, sc, c0, C, i < n);
+    unsigned long long any = block_or(mine, &s_or);
+    while (any) {   // block-uniform: only the combos some row of this block falls in
+        const int cb = __ffsll((long long)any) - 1;
+        const int c = c0 + cb;
+        any &= any - 1ull;
+        const bool flag = (mine >> cb) & 1ull;
         unsigned m = __ballot_sync(0xffffffffu, flag);
         if (lane == 0) warp_cnt[wid] = __popc(m);
         __syncthreads();
@@ -112,7 +147,9 @@ __global__ void k_halo_fill(const double* __restrict__ x, int n, const double* _
         }
         __syncthreads();
     }
+    }
 }
+
 
 __global__ void k_pack_shift(const double* __restrict__ x, const int* __restrict__ idx,
                              const int8_t* __restrict__ code, const double* __restrict__ shifts, int n,
