@@ -32,7 +32,7 @@ import torch.distributed as dist
 
 from . import _lib
 from .domain import (SHIFT_UNITS, AtomStore, Box, RankSet, _rows4, _to4, cell_grid, decompose,
-                     _dense_ids, wrap_positions)
+                     _dense_ids)
 
 
 def _staged(group) -> bool:

@@ -16,9 +16,7 @@ Mirror of mdkk/domain.py (Box :22-42, minimum_image :45-53, wrap_positions
 
 from __future__ import annotations
 
-import ctypes as C
 import itertools
-import math
 
 import numpy as np
 import torch

@@ -13,7 +13,7 @@ import numpy as np
 import pytest
 
 from conftest import golden
-from oracle import md, qeq as oq
+from oracle import qeq as oq
 
 pytestmark = pytest.mark.gpu
 

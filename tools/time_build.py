@@ -4,7 +4,6 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 from paper_2508_13523_b200 import _lib
 from paper_2508_13523_b200.driver import RunConfig, Simulation
-from paper_2508_13523_b200 import neighbor as nbm
 import bench
 
 dev = torch.device("cuda", 0)
