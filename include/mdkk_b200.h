@@ -70,11 +70,14 @@ int mdkk_wrap(double* x, int n, const double* lengths_host, void* stream);
  * x + shift lies in [lo, hi) on every axis (half-open, mdkk/domain.py:274).
  * Two phases: count writes totals[C] (device) and per-block offsets into
  * block_scratch (int[ceil(n/256) * C]); fill writes out_idx combo-major, atoms
- * ascending within a combo — the reference's src/shift/index order. */
+ * ascending within a combo — the reference's src/shift/index order; with
+ * out_code (optional, int8[total]) each selected row also gets its combo's
+ * shift code combo_code[c] (device int8[C]). */
 int mdkk_halo_count(mdkk_ctx* ctx, const double* x, int n, const double* combos_dev, int C,
                     int* block_scratch, int* totals, void* stream);
 int mdkk_halo_fill(mdkk_ctx* ctx, const double* x, int n, const double* combos_dev, int C,
-                   const int* block_scratch, const int* totals, int* out_idx, void* stream);
+                   const int* block_scratch, const int* totals, int* out_idx, const int8_t* combo_code,
+                   int8_t* out_code, void* stream);
 
 /* Forward-comm pack: out[k] = x[idx[k]] + shift_table[code[k]] (shift_table is
  * double[27][3] device, code int8 in 0..26).  `out` may alias ghost rows of x. */
@@ -154,6 +157,16 @@ int mdkk_lj_force(mdkk_ctx* ctx, const double* x, int n_local, const int* table,
 int mdkk_lj_force_neighbor(mdkk_ctx* ctx, const double* x, int n_local, const int* table, const int* counts,
                            int cap, int style, int newton, int virial, double epsilon, double sigma, double rc,
                            double* f, double* ev, int* flags, void* stream);
+/* Speculative step launch (engine-internal pipelining): as mdkk_lj_force (mode 0) or
+ * mdkk_lj_force_neighbor (mode 1), but the kernel does nothing when
+ * sqrt(*maxdisp2) > half_skin -- the step's skin test, evaluated on the device in the
+ * host's FP64 operations, so the launch can be queued before the host has read the
+ * rebuild decision; a rebuilding step relaunches after its rebuild.  ev is then
+ * undefined until that relaunch. */
+int mdkk_lj_force_gated(mdkk_ctx* ctx, const double* x, int n_local, const int* table, const int* counts,
+                        int cap, int style, int newton, int virial, int mode, double epsilon, double sigma,
+                        double rc, double* f, double* ev, int* flags, const double* maxdisp2, double half_skin,
+                        void* stream);
 
 /* ------------------------------------------------------------- integrator
  * Velocity Verlet (mdkk/driver/simulation.py:431-450) fused with the skin
@@ -213,6 +226,14 @@ int mdkk_snap_y_compress(mdkk_snap* snap, const double* Y, int n_local, double* 
  * atomics, f double4 rows incl. ghosts, caller-zeroed; ghosts -> reverse comm). */
 int mdkk_snap_deidrj(mdkk_snap* snap, const double* x, int n_local, const int* table, const int* counts, int cap,
                      double rc, const double* Yh, int ld, double* f, void* stream);
+/* The whole per-step pipeline in one call (SnapStyle.compute, mdkk/driver/simulation.py:123-142):
+ * ui -> yi -> fused deidrj on one stream.  U ([n_local][n_flat] complex, layout a) and Yh
+ * ([n_half][n_local] complex) are optional dumps: pass both NULL to use a workspace owned by
+ * the handle (grown on demand, freed by mdkk_snap_destroy).  f as mdkk_snap_deidrj (caller
+ * zeroed, ghost rows -> reverse comm); *energy (device) and *flags as mdkk_snap_yi / _ui. */
+int mdkk_snap_compute(mdkk_ctx* ctx, mdkk_snap* snap, const double* x, int n_local, const int* table,
+                      const int* counts, int cap, double rc, double* U, double* Yh, double* f, double* energy,
+                      int* flags, void* stream);
 
 /* --- SNAP API-parity stages (not on the engine path; csrc/snap_aux.cu) ---
  * Neighbour map (build_neighbor_map / NeighborMap, mdkk/snap/compute.py:66-119):

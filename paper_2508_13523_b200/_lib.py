@@ -33,7 +33,7 @@ SIGNATURES = {
     "mdkk_fp64_probe": [_i, _i, _p, _p],
     "mdkk_wrap": [_p, _i, _p, _p],
     "mdkk_halo_count": [_p, _p, _i, _p, _i, _p, _p, _p],
-    "mdkk_halo_fill": [_p, _p, _i, _p, _i, _p, _p, _p, _p],
+    "mdkk_halo_fill": [_p, _p, _i, _p, _i, _p, _p, _p, _p, _p, _p],
     "mdkk_pack_shift": [_p, _p, _p, _p, _i, _p, _p],
     "mdkk_fold_add": [_p, _p, _p, _i, _p],
     "mdkk_gather_rows4": [_p, _p, _i, _p, _p],
@@ -48,6 +48,7 @@ SIGNATURES = {
     "mdkk_nbr_canonicalize": [_p, _p, _i, _i, _p, _p, _p],
     "mdkk_max_disp2": [_p, _p, _i, _p, _p],
     "mdkk_lj_force": [_p, _p, _i, _p, _p, _i, _i, _i, _i, _d, _d, _d, _p, _p, _p, _p],
+    "mdkk_lj_force_gated": [_p, _p, _i, _p, _p, _i, _i, _i, _i, _i, _d, _d, _d, _p, _p, _p, _p, _d, _p],
     "mdkk_lj_force_neighbor": [_p, _p, _i, _p, _p, _i, _i, _i, _i, _d, _d, _d, _p, _p, _p, _p],
     "mdkk_verlet_first": [_p, _p, _p, _p, _p, _i, _d, _d, _p, _i, _p],
     "mdkk_verlet_second": [_p, _p, _p, _i, _d, _d, _p, _p],
@@ -59,6 +60,7 @@ SIGNATURES = {
     "mdkk_snap_y_expand": [_p, _p, _i, _i, _p, _i, _i, _p],
     "mdkk_snap_y_compress": [_p, _p, _i, _p, _i, _i, _i, _p],
     "mdkk_snap_deidrj": [_p, _p, _i, _p, _p, _i, _d, _p, _i, _p, _p],
+    "mdkk_snap_compute": [_p, _p, _p, _i, _p, _p, _i, _d, _p, _p, _p, _p, _p, _p],
     "mdkk_snap_pair_count": [_p, _p, _i, _p, _p, _i, _d, _p, _p, _p, _p],
     "mdkk_snap_pair_fill": [_p, _i, _p, _p, _i, _d, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p],
     "mdkk_snap_duidrj": [_p, _i, _p, _d, _p, _p],

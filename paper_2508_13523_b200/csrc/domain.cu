@@ -110,7 +110,8 @@ __global__ void k_halo_scan(int* __restrict__ block_counts, int nb, int C, int* 
 
 __global__ void k_halo_fill(const double* __restrict__ x, int n, const double* __restrict__ combos, int C,
                             const int* __restrict__ block_off, const int* __restrict__ totals,
-                            int* __restrict__ out) {
+                            int* __restrict__ out, const int8_t* __restrict__ combo_code,
+                            int8_t* __restrict__ out_code) {
     extern __shared__ double sc[];
     int* base = reinterpret_cast<int*>(sc + 9 * C);
     __shared__ int warp_cnt[kHaloBlock / 32];
@@ -143,7 +144,9 @@ __global__ void k_halo_fill(const double* __restrict__ x, int n, const double* _
         for (int w = 0; w < wid; ++w) before += warp_cnt[w];
         if (flag) {
             int r = before + __popc(m & ((1u << lane) - 1u));
-            out[base[c] + block_off[(long long)blockIdx.x * C + c] + r] = i;
+            const int o = base[c] + block_off[(long long)blockIdx.x * C + c] + r;
+            out[o] = i;
+            if (out_code) out_code[o] = combo_code[c];
         }
         __syncthreads();
     }
@@ -216,13 +219,13 @@ int mdkk_halo_count(mdkk_ctx*, const double* x, int n, const double* combos, int
 }
 
 int mdkk_halo_fill(mdkk_ctx*, const double* x, int n, const double* combos, int C, const int* block_scratch,
-                   const int* totals, int* out_idx, void* stream) {
-    if (n < 0 || C < 0 || C > kMaxCombos) return MDKK_E_ARG;
+                   const int* totals, int* out_idx, const int8_t* combo_code, int8_t* out_code, void* stream) {
+    if (n < 0 || C < 0 || C > kMaxCombos || (out_code && !combo_code)) return MDKK_E_ARG;
     if (C == 0 || n == 0) return MDKK_OK;
     int nb = mdkk::grid_for(n, kHaloBlock);
     size_t sm = sizeof(double) * 9 * C + sizeof(int) * C;
     k_halo_fill<<<nb, kHaloBlock, sm, mdkk::as_stream(stream)>>>(x, n, combos, C, block_scratch, totals,
-                                                                  out_idx);
+                                                                  out_idx, combo_code, out_code);
     MDKK_CHECK_LAUNCH("k_halo_fill");
     return MDKK_OK;
 }

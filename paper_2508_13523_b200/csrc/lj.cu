@@ -15,12 +15,21 @@ namespace {
 
 constexpr int kBlock = 128;
 
+// Speculative launch gate: the step's skin test (mdkk/neighbor.py:73-74, the host's
+// sqrt(maxdisp2) > skin/2 in the same FP64 operations) read on the device, so the
+// force launch can be queued before the host has seen the rebuild decision.
+__device__ __forceinline__ bool gated_off(const double* gate, double limit) {
+    return gate != nullptr && sqrt(*gate) > limit;
+}
+
 template <int STYLE, bool NEWTON, bool VIR>
 __global__ void __launch_bounds__(kBlock) k_lj(const double* __restrict__ x, int n_local,
                                                const int* __restrict__ table, const int* __restrict__ counts,
                                                int cap, double eps4, double eps24, double sig2, double rc2,
                                                double* __restrict__ f, double* __restrict__ partials,
-                                               int* __restrict__ flags) {
+                                               int* __restrict__ flags, const double* __restrict__ gate,
+                                               double gate_limit) {
+    if (gated_off(gate, gate_limit)) return;   // block-uniform: the step rebuilds and relaunches
     const int i = blockIdx.x * kBlock + threadIdx.x;
     double acc[7] = {0, 0, 0, 0, 0, 0, 0};  // E, Wxx, Wyy, Wzz, Wxy, Wxz, Wyz
     if (i < n_local) {
@@ -114,7 +123,9 @@ __global__ void __launch_bounds__(kBlock) k_lj_team(const double* __restrict__ x
                                                     const int* __restrict__ table, const int* __restrict__ counts,
                                                     int cap, double eps4, double eps24, double sig2, double rc2,
                                                     double* __restrict__ f, double* __restrict__ partials,
-                                                    int* __restrict__ flags) {
+                                                    int* __restrict__ flags, const double* __restrict__ gate,
+                                                    double gate_limit) {
+    if (gated_off(gate, gate_limit)) return;
     const int t = blockIdx.x * kBlock + threadIdx.x;
     const int i = t / T, l = t % T;
     double acc[7] = {0, 0, 0, 0, 0, 0, 0};
@@ -189,11 +200,12 @@ __global__ void __launch_bounds__(kBlock) k_lj_team(const double* __restrict__ x
 
 }  // namespace
 
-extern "C" int mdkk_lj_force_neighbor(mdkk_ctx* ctx, const double* x, int n_local, const int* table,
-                                      const int* counts, int cap, int style, int newton, int virial, double epsilon,
-                                      double sigma, double rc, double* f, double* ev, int* flags, void* stream) {
+namespace {
+
+int lj_team_launch(mdkk_ctx* ctx, const double* x, int n_local, const int* table, const int* counts, int cap,
+                   int style, int newton, int virial, double epsilon, double sigma, double rc, double* f, double* ev,
+                   int* flags, const double* gate, double gate_limit, cudaStream_t s) {
     if (!ctx || n_local < 0 || cap < 1 || (style != 0 && style != 1)) return MDKK_E_ARG;
-    cudaStream_t s = mdkk::as_stream(stream);
     if (n_local == 0) {
         cudaMemsetAsync(ev, 0, 7 * sizeof(double), s);
         return MDKK_OK;
@@ -203,8 +215,9 @@ extern "C" int mdkk_lj_force_neighbor(mdkk_ctx* ctx, const double* x, int n_loca
     double* partials = static_cast<double*>(mdkk::scratch(ctx, sizeof(double) * 7 * (size_t)nb));
     if (!partials) return mdkk::cuda_fail(cudaErrorMemoryAllocation, "scratch");
     const double e4 = 4.0 * epsilon, e24 = 24.0 * epsilon, s2 = sigma * sigma, rc2 = rc * rc;
-#define MDKK_LJT(ST, NW, VR) \
-    k_lj_team<ST, NW, VR, T><<<nb, kBlock, 0, s>>>(x, n_local, table, counts, cap, e4, e24, s2, rc2, f, partials, flags)
+#define MDKK_LJT(ST, NW, VR)                                                                                   \
+    k_lj_team<ST, NW, VR, T><<<nb, kBlock, 0, s>>>(x, n_local, table, counts, cap, e4, e24, s2, rc2, f, partials, \
+                                                    flags, gate, gate_limit)
     if (style == 0) {
         if (virial) MDKK_LJT(0, false, true); else MDKK_LJT(0, false, false);
     } else if (newton) {
@@ -220,11 +233,10 @@ extern "C" int mdkk_lj_force_neighbor(mdkk_ctx* ctx, const double* x, int n_loca
     return MDKK_OK;
 }
 
-extern "C" int mdkk_lj_force(mdkk_ctx* ctx, const double* x, int n_local, const int* table, const int* counts,
-                             int cap, int style, int newton, int virial, double epsilon, double sigma, double rc,
-                             double* f, double* ev, int* flags, void* stream) {
+int lj_launch(mdkk_ctx* ctx, const double* x, int n_local, const int* table, const int* counts, int cap, int style,
+              int newton, int virial, double epsilon, double sigma, double rc, double* f, double* ev, int* flags,
+              const double* gate, double gate_limit, cudaStream_t s) {
     if (!ctx || n_local < 0 || cap < 1 || (style != 0 && style != 1)) return MDKK_E_ARG;
-    cudaStream_t s = mdkk::as_stream(stream);
     if (n_local == 0) {
         cudaMemsetAsync(ev, 0, 7 * sizeof(double), s);
         return MDKK_OK;
@@ -233,8 +245,9 @@ extern "C" int mdkk_lj_force(mdkk_ctx* ctx, const double* x, int n_local, const 
     double* partials = static_cast<double*>(mdkk::scratch(ctx, sizeof(double) * 7 * (size_t)nb));
     if (!partials) return mdkk::cuda_fail(cudaErrorMemoryAllocation, "scratch");
     const double e4 = 4.0 * epsilon, e24 = 24.0 * epsilon, s2 = sigma * sigma, rc2 = rc * rc;
-#define MDKK_LJ(ST, NW, VR) \
-    k_lj<ST, NW, VR><<<nb, kBlock, 0, s>>>(x, n_local, table, counts, cap, e4, e24, s2, rc2, f, partials, flags)
+#define MDKK_LJ(ST, NW, VR)                                                                                    \
+    k_lj<ST, NW, VR><<<nb, kBlock, 0, s>>>(x, n_local, table, counts, cap, e4, e24, s2, rc2, f, partials, flags, \
+                                           gate, gate_limit)
     if (style == 0) {
         if (virial) MDKK_LJ(0, false, true); else MDKK_LJ(0, false, false);
     } else if (newton) {
@@ -248,4 +261,30 @@ extern "C" int mdkk_lj_force(mdkk_ctx* ctx, const double* x, int n_local, const 
     mdkk::reduce_partials(partials, nb, virial ? 7 : 1, ev, s);
     MDKK_CHECK_LAUNCH("k_reduce_partials");
     return MDKK_OK;
+}
+
+}  // namespace
+
+extern "C" int mdkk_lj_force_neighbor(mdkk_ctx* ctx, const double* x, int n_local, const int* table,
+                                      const int* counts, int cap, int style, int newton, int virial, double epsilon,
+                                      double sigma, double rc, double* f, double* ev, int* flags, void* stream) {
+    return lj_team_launch(ctx, x, n_local, table, counts, cap, style, newton, virial, epsilon, sigma, rc, f, ev,
+                          flags, nullptr, 0.0, mdkk::as_stream(stream));
+}
+
+extern "C" int mdkk_lj_force(mdkk_ctx* ctx, const double* x, int n_local, const int* table, const int* counts,
+                             int cap, int style, int newton, int virial, double epsilon, double sigma, double rc,
+                             double* f, double* ev, int* flags, void* stream) {
+    return lj_launch(ctx, x, n_local, table, counts, cap, style, newton, virial, epsilon, sigma, rc, f, ev, flags,
+                     nullptr, 0.0, mdkk::as_stream(stream));
+}
+
+extern "C" int mdkk_lj_force_gated(mdkk_ctx* ctx, const double* x, int n_local, const int* table,
+                                   const int* counts, int cap, int style, int newton, int virial, int mode,
+                                   double epsilon, double sigma, double rc, double* f, double* ev, int* flags,
+                                   const double* maxdisp2, double half_skin, void* stream) {
+    if (!maxdisp2 || (mode != 0 && mode != 1)) return MDKK_E_ARG;
+    return (mode == 0 ? lj_launch : lj_team_launch)(ctx, x, n_local, table, counts, cap, style, newton, virial,
+                                                    epsilon, sigma, rc, f, ev, flags, maxdisp2, half_skin,
+                                                    mdkk::as_stream(stream));
 }

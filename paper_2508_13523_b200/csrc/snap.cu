@@ -480,6 +480,7 @@ int mdkk_snap_destroy(mdkk_snap* s) {
     cudaFree(s->chunk);
     cudaFree(s->chunkf);
     cudaFree(s->fmap);
+    cudaFree(s->work);
     delete s;
     return MDKK_OK;
 }
@@ -591,6 +592,31 @@ int mdkk_snap_deidrj(mdkk_snap* s, const double* x, int n_local, const int* tabl
     }
     MDKK_CHECK_LAUNCH("k_snap_deidrj");
     return MDKK_OK;
+}
+
+int mdkk_snap_compute(mdkk_ctx* ctx, mdkk_snap* s, const double* x, int n_local, const int* table, const int* counts,
+                      int cap, double rc, double* U, double* Yh, double* f, double* energy, int* flags,
+                      void* stream) {
+    if (!ctx || !s || n_local < 0 || cap < 1 || !f || !energy || !flags) return MDKK_E_ARG;
+    if ((U == nullptr) != (Yh == nullptr)) return MDKK_E_ARG;
+    if (!U) {   // handle-owned workspace, grown on demand and kept for the next step
+        const size_t need = (size_t)n_local * (s->n_flat + s->n_half) * sizeof(double2);
+        if (need > s->work_bytes) {
+            cudaFree(s->work);
+            s->work = nullptr;
+            s->work_bytes = 0;
+            cudaError_t e = cudaMalloc(&s->work, need + need / 4);
+            if (e != cudaSuccess) return mdkk::cuda_fail(e, "mdkk_snap_compute workspace");
+            s->work_bytes = need + need / 4;
+        }
+        U = s->work;
+        Yh = s->work + (size_t)n_local * s->n_flat * 2;
+    }
+    int rc_ = mdkk_snap_ui(s, x, n_local, table, counts, cap, rc, U, 0, 0, flags, stream);
+    if (rc_ != MDKK_OK) return rc_;
+    rc_ = mdkk_snap_yi(ctx, s, U, n_local, Yh, n_local, energy, 0, 0, stream);
+    if (rc_ != MDKK_OK) return rc_;
+    return mdkk_snap_deidrj(s, x, n_local, table, counts, cap, rc, Yh, n_local, f, stream);
 }
 
 }  // extern "C"

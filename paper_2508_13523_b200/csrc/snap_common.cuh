@@ -23,6 +23,8 @@ struct mdkk_snap {
     int* chunk = nullptr;    // [kYW + 1] per-warp entry ranges (output-aligned, balanced)
     int* chunkf = nullptr;   // [kYW] first output (half index) of each warp's range
     int* fmap = nullptr;     // [n_flat] half index | mirrored << 16 | odd sign << 17
+    double* work = nullptr;  // mdkk_snap_compute workspace: U [n][n_flat] then Yh [n_half][n] (complex)
+    size_t work_bytes = 0;
 };
 
 namespace {

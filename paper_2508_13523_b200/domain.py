@@ -447,8 +447,10 @@ class RankedSystem:
             totals = host_tot[off_all:off_all + C_].astype(np.int64)
             off_all += C_
             idx = self._buf(f"idx{src.rank}", int(totals.sum()) + 1, torch.int32)
+            cds = self._buf(f"cds{src.rank}", int(totals.sum()) + 1, torch.int8)
             _lib.check(lib.mdkk_halo_fill(ctx, src.x.data_ptr(), src.n_local, tab.data_ptr(), C_, blk.data_ptr(),
-                                          tot.data_ptr(), idx.data_ptr(), stream), "mdkk_halo_fill")
+                                          tot.data_ptr(), idx.data_ptr(), codes.data_ptr(), cds.data_ptr(),
+                                          stream), "mdkk_halo_fill")
             # combos are dst-major: each (src, dst) lane is one contiguous run of idx
             start = np.concatenate([[0], np.cumsum(totals)])
             d_of = np.array([d for d, _ in meta])
@@ -456,9 +458,7 @@ class RankedSystem:
                 ks = np.flatnonzero(d_of == d)
                 a, b = int(start[ks[0]]), int(start[ks[-1] + 1])
                 if b > a:
-                    code = torch.repeat_interleave(codes[ks[0]:ks[-1] + 1], tot[ks[0]:ks[-1] + 1].long(),
-                                                   output_size=b - a)
-                    sel[(src.rank, int(d))] = (idx[a:b], code, b - a)
+                    sel[(src.rank, int(d))] = (idx[a:b], cds[a:b], b - a)
         self.lanes = []
         for dst in self.stores:
             nl = dst.n_local

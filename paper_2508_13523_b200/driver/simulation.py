@@ -62,6 +62,7 @@ class LJStyle:
     """Truncated 12-6 pair style on the GPU (mdkk/driver/simulation.py:65-85)."""
 
     list_style = None
+    supports_gate = True     # compute_device can be launched speculatively (see Simulation._half_kick_drift)
 
     def __init__(self, r_c: float, mode: str = "atom", name: str = "lj/cut/kk"):
         self.name = name
@@ -77,8 +78,10 @@ class LJStyle:
             raise RunError("pair_coeff must be set before computing forces")
         return compute_pair(self.kernel, system, lists, mode=config.mode or self.default_mode, check=check)
 
-    def compute_device(self, system, lists, config) -> tuple[torch.Tensor, torch.Tensor]:
-        """Engine path: no host sync; returns (device energy scalar, device flag word)."""
+    def compute_device(self, system, lists, config, gate=None, gate_limit: float = 0.0
+                       ) -> tuple[torch.Tensor, torch.Tensor]:
+        """Engine path: no host sync; returns (device energy scalar, device flag word).
+        With `gate` the launch is speculative (a no-op when sqrt(gate) > gate_limit)."""
         if self.kernel is None:
             raise RunError("pair_coeff must be set before computing forces")
         dev = system.device
@@ -93,7 +96,7 @@ class LJStyle:
         half = False
         for k, (s, nl) in enumerate(zip(system.stores, lists)):
             lj_force_rank(s, nl, self.kernel.params, evs[k], flags, virial=False,
-                          mode=config.mode or self.default_mode)
+                          mode=config.mode or self.default_mode, gate=gate, gate_limit=gate_limit)
             half |= nl.style == "half"
         if half:   # collective in the distributed system: every rank calls it
             system.reverse_comm()
@@ -207,6 +210,8 @@ class Simulation:
         self.device = torch.device(dev) if dev is not None else torch.device("cuda", torch.cuda.current_device())
         self._d2 = None
         self._d2_host = None
+        self._d2_ready = None      # event after the skin-test read-back
+        self._spec_e = None        # energy of a speculatively launched force evaluation
         self._packed = False
         self._kick_pending = False
         self.qeq = None
@@ -355,8 +360,11 @@ class Simulation:
         self._cap_hint = max(nl.alloc_cap for nl in self.lists)
         self.n_rebuilds += 1
 
-    def _forces_device(self):
-        e, flags = self.style.compute_device(self.system, self.lists, self.config)
+    def _forces_device(self, gate=None, gate_limit: float = 0.0):
+        if gate is not None:
+            e, flags = self.style.compute_device(self.system, self.lists, self.config, gate, gate_limit)
+        else:
+            e, flags = self.style.compute_device(self.system, self.lists, self.config)
         self._e_dev, self._flags = e, flags
         return e
 
@@ -402,12 +410,23 @@ class Simulation:
         if self._d2_host is None:
             self._d2_host = torch.zeros(1, dtype=torch.float64, pin_memory=True)
         self._d2_host.copy_(worst, non_blocking=True)
-        if not self.config.distributed:
+        if self.config.distributed:
+            torch.cuda.current_stream(self.device).synchronize()
+        else:
+            if self._d2_ready is None:
+                self._d2_ready = torch.cuda.Event()
+            self._d2_ready.record(torch.cuda.current_stream(self.device))
             # speculative halo refresh, queued behind the read-back: a plain step needs
             # it next, and a rebuild simply overwrites the ghost rows
             self.system.forward_comm()
             self._packed = True
-        torch.cuda.current_stream(self.device).synchronize()
+            if getattr(self.style, "supports_gate", False):
+                # speculative force launch, gated on the device by the same skin test:
+                # the GPU runs it while the host reads the decision (no idle gap), and
+                # it is a no-op on a rebuilding step (relaunched after the rebuild)
+                self._gate = worst
+                self._spec_e = self._forces_device(gate=worst, gate_limit=0.5 * self.config.skin)
+            self._d2_ready.synchronize()
         return math.sqrt(float(self._d2_host[0])) > 0.5 * self.config.skin
 
     def _half_kick(self):
@@ -426,11 +445,15 @@ class Simulation:
         `advance`); `flush_kick()` completes it before velocities are read.
         """
         self._packed = False
+        self._spec_e = None
         if self._half_kick_drift():
             self._rebuild_lists()
-        elif not self._packed:
-            self.system.forward_comm()
-        e = self._forces_device()
+            e = self._forces_device()
+        else:
+            if not self._packed:
+                self.system.forward_comm()
+            e = self._spec_e if self._spec_e is not None else self._forces_device()
+        self._spec_e = None
         if defer_kick:
             self._kick_pending = True
         else:

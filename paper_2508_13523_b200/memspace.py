@@ -92,7 +92,7 @@ class DualArray:
         self.layout_a = layout_a or LayoutPolicy.row_major(len(shape))
         self.layout_b = layout_b or LayoutPolicy.transposed(len(shape))
         self.device = torch.device(device) if device is not None else torch.device("cuda")
-        self.data_a = np.zeros(shape, dtype=self.dtype)
+        self._data_a = None    # host storage materialises on first host access
         sshape = list(self.layout_b.storage_shape(shape))
         if pad_last is not None:
             if self.layout_b.order[-1] != len(shape) - 1:
@@ -105,6 +105,16 @@ class DualArray:
         self.modified_a = False
         self.modified_b = False
         self.transfer_count = 0
+
+    @property
+    def data_a(self) -> np.ndarray:
+        if self._data_a is None:
+            self._data_a = np.zeros(self.shape, dtype=self.dtype)
+        return self._data_a
+
+    @data_a.setter
+    def data_a(self, value) -> None:
+        self._data_a = value
 
     def _check(self, space):
         if space not in SPACES:

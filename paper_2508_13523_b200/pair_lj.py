@@ -90,19 +90,29 @@ class PairResult:
 
 
 def lj_force_rank(store, nl: NeighborList, params: PairParams, ev: torch.Tensor, flags: torch.Tensor,
-                  zero: bool = True, virial: bool = True, mode: str = "atom") -> None:
+                  zero: bool = True, virial: bool = True, mode: str = "atom", gate: torch.Tensor | None = None,
+                  gate_limit: float = 0.0) -> None:
     """One rank's kernel launch (no host sync).
 
     Ghost force rows are zero outside a force evaluation (migrate zeroes all
     rows, reverse comm zeroes ghosts, full-list kernels write owner rows
     only), so only the half list (owner rows accumulate with atomics) needs
-    a clear.
+    a clear.  `gate` (engine-internal, device double): the launch is
+    speculative and does nothing when sqrt(gate) > gate_limit (a rebuilding
+    step, which relaunches after its rebuild).
     """
     dev = store.device
     if zero and nl.style == "half":
         store.f.zero_()
     # mode "atom": one thread per owned atom; "neighbor": a team of lanes per atom
     # splitting its list (mdkk/pair_lj.py:118-143)
+    if gate is not None:
+        _lib.check(_lib.lib().mdkk_lj_force_gated(
+            _lib.ctx(dev), store.x.data_ptr(), store.n_local, nl.table_dev.data_ptr(), nl.counts_dev.data_ptr(),
+            nl.alloc_cap, STYLES[nl.style], int(nl.newton), int(virial), int(mode == "neighbor"), params.epsilon,
+            params.sigma, params.r_c, store.f.data_ptr(), ev.data_ptr(), flags.data_ptr(), gate.data_ptr(),
+            gate_limit, _lib.stream(dev)), "mdkk_lj_force_gated")
+        return
     fn = "mdkk_lj_force_neighbor" if mode == "neighbor" else "mdkk_lj_force"
     _lib.check(getattr(_lib.lib(), fn)(
         _lib.ctx(dev), store.x.data_ptr(), store.n_local, nl.table_dev.data_ptr(), nl.counts_dev.data_ptr(),

@@ -246,3 +246,36 @@ def test_knobs_do_not_change_results(gpu):
         assert np.abs(f1 - f0).max() / fscale < 1e-12, knobs
         assert np.array_equal(u1, u0) and np.allclose(y1, y0, rtol=1e-13, atol=1e-14), knobs
         assert np.allclose(b1, b0, rtol=1e-13, atol=1e-13), knobs
+
+
+def test_one_call_pipeline_bit_identical(gpu):
+    """mdkk_snap_compute (handle workspace and caller dumps) == ui -> yi -> fused deidrj: U, Y and E bit
+    for bit; F up to the order of the FP64 atomics that fold f_k."""
+    import torch
+    from paper_2508_13523_b200 import _lib
+    from paper_2508_13523_b200.snap import compute_fused_deidrj, energy_from_y
+    bcc, L = md.lattice("bcc", 3.1803, (4, 4, 4))
+    system, store, nmap, state = _state_for(md.jittered(bcc, 0.05, 5), L, 4, np.linspace(0.05, 0.1, 55), 4.73, 0.3)
+    f_ref = compute_fused_deidrj(nmap, state, store.n_total)
+    e_ref = energy_from_y(state)
+    nl, dev, n = nmap.nlist, state.device, store.n_local
+    for dumps in (False, True):
+        f = torch.zeros((store.n_total, 4), dtype=torch.float64, device=dev)
+        e = torch.zeros(1, dtype=torch.float64, device=dev)
+        flags = torch.zeros(1, dtype=torch.int32, device=dev)
+        U = torch.zeros((n, state.index.n_flat), dtype=torch.complex128, device=dev) if dumps else None
+        Yh = torch.zeros((145, n), dtype=torch.complex128, device=dev) if dumps else None
+        for _ in range(2):      # the second call reuses the grown workspace
+            f.zero_()
+            _lib.check(_lib.lib().mdkk_snap_compute(
+                _lib.ctx(dev), state.handle().ptr, store.x.data_ptr(), n, nl.table_dev.data_ptr(),
+                nl.counts_dev.data_ptr(), nl.alloc_cap, 4.73, U.data_ptr() if dumps else None,
+                Yh.data_ptr() if dumps else None, f.data_ptr(), e.data_ptr(), flags.data_ptr(),
+                _lib.stream(dev)), "mdkk_snap_compute")
+        assert int(flags.item()) == 0
+        assert float(e.item()) == e_ref
+        assert np.abs(f[:, :3].cpu().numpy() - f_ref).max() <= 1e-13 * np.abs(f_ref).max()
+        if dumps:   # default layout "a": U rows are atoms, as the handle writes them
+            assert state._lay == 0
+            assert np.array_equal(U.cpu().numpy(), state.U_dev[:n].cpu().numpy())
+            assert np.array_equal(Yh.cpu().numpy(), state.Yh_dev[:, :n].cpu().numpy())

@@ -12,6 +12,7 @@ from paper_2508_13523_b200.driver import RunConfig, Simulation
 
 style = sys.argv[1] if len(sys.argv) > 1 else "full"
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 30
+loop = sys.argv[3] if len(sys.argv) > 3 else "advance"   # "advance" (the engine loop) or "step"
 dev = torch.device("cuda", 0)
 sim = Simulation(RunConfig(list_style=style, newton=(style == "half"), device=dev), log=None)
 sim.execute(bench.lj_script(80))
@@ -21,8 +22,11 @@ for _ in range(5):
 torch.cuda.synchronize()
 with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA], with_stack=False) as prof:
     r0 = sim.n_rebuilds
-    for _ in range(steps):
-        sim.step_device()
+    if loop == "advance":
+        sim.advance(steps)
+    else:
+        for _ in range(steps):
+            sim.step_device()
     torch.cuda.synchronize()
 path = "gpurun_out/timeline.json"
 os.makedirs("gpurun_out", exist_ok=True)
