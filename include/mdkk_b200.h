@@ -160,13 +160,14 @@ int mdkk_lj_force_neighbor(mdkk_ctx* ctx, const double* x, int n_local, const in
 /* Speculative step launch (engine-internal pipelining): as mdkk_lj_force (mode 0) or
  * mdkk_lj_force_neighbor (mode 1), but the kernel does nothing when
  * sqrt(*maxdisp2) > half_skin -- the step's skin test, evaluated on the device in the
- * host's FP64 operations, so the launch can be queued before the host has read the
- * rebuild decision; a rebuilding step relaunches after its rebuild.  ev is then
- * undefined until that relaunch. */
+ * host's FP64 operations -- or when *max_count > count_limit (the build's capacity
+ * check), so the launch can be queued before the host has read either decision; a
+ * rebuilding / regrowing step relaunches afterwards.  Either gate may be NULL.  ev
+ * is undefined after a skipped launch. */
 int mdkk_lj_force_gated(mdkk_ctx* ctx, const double* x, int n_local, const int* table, const int* counts,
                         int cap, int style, int newton, int virial, int mode, double epsilon, double sigma,
                         double rc, double* f, double* ev, int* flags, const double* maxdisp2, double half_skin,
-                        void* stream);
+                        const int* max_count, int count_limit, void* stream);
 
 /* ------------------------------------------------------------- integrator
  * Velocity Verlet (mdkk/driver/simulation.py:431-450) fused with the skin

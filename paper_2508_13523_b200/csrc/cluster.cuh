@@ -65,10 +65,4 @@ __device__ __forceinline__ long long tbl_index(int c, int capb, int k, int lane)
     return ((((long long)c * capb + (k >> 3)) * kClusterSize + lane) << 3) + (k & 7);
 }
 
-__device__ __forceinline__ double warp_min_d(double v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
-    return v;
-}
-
 }  // namespace mdkk

@@ -28,7 +28,8 @@ __device__ __forceinline__ bool in_combo(const double4& p, const double* c) {
 
 // Per-thread bit mask of the combos (<= 64 per call) the atom falls in, and the
 // block-wide OR: blocks of cell-sorted rows are compact, so most of them touch no
-// halo at all and skip every per-combo block reduction.
+// halo at all and skip every per-combo block reduction.  (Pre-testing the combos
+// against each warp's bounding box measured slower: the kernels are latency bound.)
 __device__ __forceinline__ unsigned long long combo_mask(const double4& p, const double* sc, int c0, int C,
                                                          bool valid) {
     unsigned long long m = 0ull;

@@ -18,8 +18,16 @@ constexpr int kBlock = 128;
 // Speculative launch gate: the step's skin test (mdkk/neighbor.py:73-74, the host's
 // sqrt(maxdisp2) > skin/2 in the same FP64 operations) read on the device, so the
 // force launch can be queued before the host has seen the rebuild decision.
-__device__ __forceinline__ bool gated_off(const double* gate, double limit) {
-    return gate != nullptr && sqrt(*gate) > limit;
+// The count gate is the build's capacity check (max_count > cap: the table overflowed
+// and the list is rebuilt with a grown cap before the relaunch).
+struct Gate {
+    const double* d2;
+    double half_skin;
+    const int* count;
+    int count_limit;
+};
+__device__ __forceinline__ bool gated_off(const Gate& g) {
+    return (g.d2 != nullptr && sqrt(*g.d2) > g.half_skin) || (g.count != nullptr && *g.count > g.count_limit);
 }
 
 template <int STYLE, bool NEWTON, bool VIR>
@@ -27,9 +35,8 @@ __global__ void __launch_bounds__(kBlock) k_lj(const double* __restrict__ x, int
                                                const int* __restrict__ table, const int* __restrict__ counts,
                                                int cap, double eps4, double eps24, double sig2, double rc2,
                                                double* __restrict__ f, double* __restrict__ partials,
-                                               int* __restrict__ flags, const double* __restrict__ gate,
-                                               double gate_limit) {
-    if (gated_off(gate, gate_limit)) return;   // block-uniform: the step rebuilds and relaunches
+                                               int* __restrict__ flags, Gate gate) {
+    if (gated_off(gate)) return;   // block-uniform: the step rebuilds and relaunches
     const int i = blockIdx.x * kBlock + threadIdx.x;
     double acc[7] = {0, 0, 0, 0, 0, 0, 0};  // E, Wxx, Wyy, Wzz, Wxy, Wxz, Wyz
     if (i < n_local) {
@@ -123,9 +130,8 @@ __global__ void __launch_bounds__(kBlock) k_lj_team(const double* __restrict__ x
                                                     const int* __restrict__ table, const int* __restrict__ counts,
                                                     int cap, double eps4, double eps24, double sig2, double rc2,
                                                     double* __restrict__ f, double* __restrict__ partials,
-                                                    int* __restrict__ flags, const double* __restrict__ gate,
-                                                    double gate_limit) {
-    if (gated_off(gate, gate_limit)) return;
+                                                    int* __restrict__ flags, Gate gate) {
+    if (gated_off(gate)) return;
     const int t = blockIdx.x * kBlock + threadIdx.x;
     const int i = t / T, l = t % T;
     double acc[7] = {0, 0, 0, 0, 0, 0, 0};
@@ -204,7 +210,7 @@ namespace {
 
 int lj_team_launch(mdkk_ctx* ctx, const double* x, int n_local, const int* table, const int* counts, int cap,
                    int style, int newton, int virial, double epsilon, double sigma, double rc, double* f, double* ev,
-                   int* flags, const double* gate, double gate_limit, cudaStream_t s) {
+                   int* flags, const Gate& gate, cudaStream_t s) {
     if (!ctx || n_local < 0 || cap < 1 || (style != 0 && style != 1)) return MDKK_E_ARG;
     if (n_local == 0) {
         cudaMemsetAsync(ev, 0, 7 * sizeof(double), s);
@@ -217,7 +223,7 @@ int lj_team_launch(mdkk_ctx* ctx, const double* x, int n_local, const int* table
     const double e4 = 4.0 * epsilon, e24 = 24.0 * epsilon, s2 = sigma * sigma, rc2 = rc * rc;
 #define MDKK_LJT(ST, NW, VR)                                                                                   \
     k_lj_team<ST, NW, VR, T><<<nb, kBlock, 0, s>>>(x, n_local, table, counts, cap, e4, e24, s2, rc2, f, partials, \
-                                                    flags, gate, gate_limit)
+                                                    flags, gate)
     if (style == 0) {
         if (virial) MDKK_LJT(0, false, true); else MDKK_LJT(0, false, false);
     } else if (newton) {
@@ -235,7 +241,7 @@ int lj_team_launch(mdkk_ctx* ctx, const double* x, int n_local, const int* table
 
 int lj_launch(mdkk_ctx* ctx, const double* x, int n_local, const int* table, const int* counts, int cap, int style,
               int newton, int virial, double epsilon, double sigma, double rc, double* f, double* ev, int* flags,
-              const double* gate, double gate_limit, cudaStream_t s) {
+              const Gate& gate, cudaStream_t s) {
     if (!ctx || n_local < 0 || cap < 1 || (style != 0 && style != 1)) return MDKK_E_ARG;
     if (n_local == 0) {
         cudaMemsetAsync(ev, 0, 7 * sizeof(double), s);
@@ -247,7 +253,7 @@ int lj_launch(mdkk_ctx* ctx, const double* x, int n_local, const int* table, con
     const double e4 = 4.0 * epsilon, e24 = 24.0 * epsilon, s2 = sigma * sigma, rc2 = rc * rc;
 #define MDKK_LJ(ST, NW, VR)                                                                                    \
     k_lj<ST, NW, VR><<<nb, kBlock, 0, s>>>(x, n_local, table, counts, cap, e4, e24, s2, rc2, f, partials, flags, \
-                                           gate, gate_limit)
+                                           gate)
     if (style == 0) {
         if (virial) MDKK_LJ(0, false, true); else MDKK_LJ(0, false, false);
     } else if (newton) {
@@ -269,22 +275,24 @@ extern "C" int mdkk_lj_force_neighbor(mdkk_ctx* ctx, const double* x, int n_loca
                                       const int* counts, int cap, int style, int newton, int virial, double epsilon,
                                       double sigma, double rc, double* f, double* ev, int* flags, void* stream) {
     return lj_team_launch(ctx, x, n_local, table, counts, cap, style, newton, virial, epsilon, sigma, rc, f, ev,
-                          flags, nullptr, 0.0, mdkk::as_stream(stream));
+                          flags, Gate{nullptr, 0.0, nullptr, 0}, mdkk::as_stream(stream));
 }
 
 extern "C" int mdkk_lj_force(mdkk_ctx* ctx, const double* x, int n_local, const int* table, const int* counts,
                              int cap, int style, int newton, int virial, double epsilon, double sigma, double rc,
                              double* f, double* ev, int* flags, void* stream) {
     return lj_launch(ctx, x, n_local, table, counts, cap, style, newton, virial, epsilon, sigma, rc, f, ev, flags,
-                     nullptr, 0.0, mdkk::as_stream(stream));
+                     Gate{nullptr, 0.0, nullptr, 0}, mdkk::as_stream(stream));
 }
 
 extern "C" int mdkk_lj_force_gated(mdkk_ctx* ctx, const double* x, int n_local, const int* table,
                                    const int* counts, int cap, int style, int newton, int virial, int mode,
                                    double epsilon, double sigma, double rc, double* f, double* ev, int* flags,
-                                   const double* maxdisp2, double half_skin, void* stream) {
-    if (!maxdisp2 || (mode != 0 && mode != 1)) return MDKK_E_ARG;
+                                   const double* maxdisp2, double half_skin, const int* max_count, int count_limit,
+                                   void* stream) {
+    if (mode != 0 && mode != 1) return MDKK_E_ARG;
     return (mode == 0 ? lj_launch : lj_team_launch)(ctx, x, n_local, table, counts, cap, style, newton, virial,
-                                                    epsilon, sigma, rc, f, ev, flags, maxdisp2, half_skin,
+                                                    epsilon, sigma, rc, f, ev, flags,
+                                                    Gate{maxdisp2, half_skin, max_count, count_limit},
                                                     mdkk::as_stream(stream));
 }

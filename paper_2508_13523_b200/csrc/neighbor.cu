@@ -137,6 +137,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_nbr_build(
     const double bmin_z = mdkk::warp_min_d(xi.z), bmax_z = mdkk::warp_max(xi.z);
     const int3 clo = mdkk::cell_of(g, bmin_x - bc, bmin_y - bc, bmin_z - bc);
     const int3 chi = mdkk::cell_of(g, bmax_x + bc, bmax_y + bc, bmax_z + bc);
+    const double ccx = 0.5 * (bmin_x + bmax_x), ccy = 0.5 * (bmin_y + bmax_y), ccz = 0.5 * (bmin_z + bmax_z);
+    const double hwx = 0.5 * (bmax_x - bmin_x), hwy = 0.5 * (bmax_y - bmin_y), hwz = 0.5 * (bmax_z - bmin_z);
     // 2. union of candidate rows
     int m = 0;
     for (int cx = clo.x; cx <= chi.x; ++cx) {
@@ -150,10 +152,13 @@ __global__ void __launch_bounds__(kWarps * 32) k_nbr_build(
                 if (s < s1) {
                     j = cell_atoms[s];
                     const double4 p = mdkk::ld4(x, j);
-                    const double dx = fmax(0.0, fmax(bmin_x - p.x, p.x - bmax_x));
-                    const double dy = fmax(0.0, fmax(bmin_y - p.y, p.y - bmax_y));
-                    const double dz = fmax(0.0, fmax(bmin_z - p.z, p.z - bmax_z));
-                    keep = dx * dx + dy * dy + dz * dz < bc2 * (1.0 + 1e-12);
+                    // distance to the bbox (a superset filter: the margin covers the
+                    // center/half-width rounding; every member is re-tested exactly)
+                    double dx = fabs(p.x - ccx) - hwx, dy = fabs(p.y - ccy) - hwy, dz = fabs(p.z - ccz) - hwz;
+                    dx = dx > 0.0 ? dx : 0.0;
+                    dy = dy > 0.0 ? dy : 0.0;
+                    dz = dz > 0.0 ? dz : 0.0;
+                    keep = dx * dx + dy * dy + dz * dz < bc2 * (1.0 + 1e-9);
                 }
                 const unsigned mask = __ballot_sync(0xffffffffu, keep);
                 const int pos = m + __popc(mask & ((1u << lane) - 1u));
@@ -166,8 +171,9 @@ __global__ void __launch_bounds__(kWarps * 32) k_nbr_build(
     // 3. per-lane test: FP32 prefilter on cluster-relative coordinates (rejects
     //    ~85% of candidates at twice the FP64 rate), then the exact FP64 test
     //    (strict r^2 < bc^2, reference rounding) + style predicate.
-    const double ccx = 0.5 * (bmin_x + bmax_x), ccy = 0.5 * (bmin_y + bmax_y), ccz = 0.5 * (bmin_z + bmax_z);
-    const float fxi = (float)(xi.x - ccx), fyi = (float)(xi.y - ccy), fzi = (float)(xi.z - ccz);
+    // invalid lanes sit at -1e18 and padded candidates at +1e18: no FP32 hit, no checks
+    const float fxi = valid ? (float)(xi.x - ccx) : -1e18f, fyi = valid ? (float)(xi.y - ccy) : -1e18f;
+    const float fzi = valid ? (float)(xi.z - ccz) : -1e18f;
     const unsigned long long fxi2 = f32x2(fxi, fxi), fyi2 = f32x2(fyi, fyi), fzi2 = f32x2(fzi, fzi);
     // margin >> FP32 rounding: |r2_f - r2| <~ 6 eps_f D^2 with D the farthest cluster-relative coordinate
     const double hx = 0.5 * (bmax_x - bmin_x) + bc, hy = 0.5 * (bmax_y - bmin_y) + bc, hz = 0.5 * (bmax_z - bmin_z) + bc;
@@ -214,6 +220,11 @@ __global__ void __launch_bounds__(kWarps * 32) k_nbr_build(
                     if (NEWTON) srk[t] = owner_rank[j];
                 }
             }
+            for (int t = cn + lane; t < ((cn + 31) & ~31); t += 32) {   // pad to whole groups of 32
+                sfx[t] = 1e18f;
+                sfy[t] = 1e18f;
+                sfz[t] = 1e18f;
+            }
             __syncwarp();
             // branch-free prefilter into a per-lane bit mask, then each lane visits only
             // its own survivors (in candidate order): the warp runs max-popcount exact
@@ -222,28 +233,26 @@ __global__ void __launch_bounds__(kWarps * 32) k_nbr_build(
                 unsigned bits = 0u;
                 const int lim = cn - h0;
                 if (STYLE == 0) {
-                    // full list: two-sided FP32 test; certain members are stored right here
-                    // (predicated, candidate order), only the thin shell around bc goes to
-                    // the exact FP64 test below
-                    unsigned in_bits = 0u;
+                    // full list: two-sided FP32 test.  Certain members are stored right here,
+                    // branch-free (predicated stores in candidate order: no per-lane bit loops,
+                    // whose trip count is the warp's max popcount); only the thin shell around
+                    // bc goes to the exact FP64 test below.  Overflowing lanes keep counting
+                    // and overwrite their last row (the table is rebuilt with the grown cap).
 #pragma unroll
-                    for (int t = 0; t < 32; t += 2) {   // entries past cn are stale but masked below
+                    for (int t = 0; t < 32; t += 2) {   // pads sit at +1e18: never hits
                         float r0, r1;
                         r2_pair(sfx + h0 + t, sfy + h0 + t, sfz + h0 + t, fxi2, fyi2, fzi2, r0, r1);
-                        in_bits |= ((r0 < lo2f) ? (1u << t) : 0u) | ((r1 < lo2f) ? (2u << t) : 0u);
-                        bits |= ((r0 < bc2f) ? (1u << t) : 0u) | ((r1 < bc2f) ? (2u << t) : 0u);
-                    }
-                    if (lim < 32) in_bits &= (1u << lim) - 1u;
-                    if (!valid) in_bits = 0u;
-                    bits &= ~in_bits;                    // the exact test only for the shell
-                    while (in_bits) {                    // certain members, candidate order
-                        const int t = __ffs(in_bits) - 1;
-                        in_bits &= in_bits - 1u;
-                        const int j = su[u0 + h0 + t];
-                        if (j != i) {
-                            if (cnt < cap) trow[(long long)cnt * 32] = j;
+                        const int2 jj = *reinterpret_cast<const int2*>(su + u0 + h0 + t);
+                        const bool in0 = r0 < lo2f, in1 = r1 < lo2f;
+                        if (in0 && jj.x != i) {
+                            trow[(long long)min(cnt, cap - 1) * 32] = jj.x;
                             ++cnt;
                         }
+                        if (in1 && jj.y != i) {
+                            trow[(long long)min(cnt, cap - 1) * 32] = jj.y;
+                            ++cnt;
+                        }
+                        bits |= ((!in0 && r0 < bc2f) ? (1u << t) : 0u) | ((!in1 && r1 < bc2f) ? (2u << t) : 0u);
                     }
                 } else {
 #pragma unroll

@@ -347,18 +347,29 @@ class Simulation:
         if self._d2 is None:
             self._d2 = torch.zeros(max(self.config.n_ranks, 1), dtype=torch.float64, device=self.device)
 
-    def _rebuild_lists(self):
-        """migrate + build (mdkk/driver/simulation.py:368-373)."""
+    def _rebuild_lists(self, defer: bool = False):
+        """migrate + build (mdkk/driver/simulation.py:368-373).  `defer`: the capacity
+        check is left to `_settle_lists` (after a count-gated force launch)."""
         halo = self.style.r_c + self.config.skin
         self.system.migrate(halo)
         old = self.lists if self.lists is not None and len(self.lists) == len(self.system.stores) else None
         self.lists = None   # the old lists are dead: their buffers are recycled
         self.lists = [build(s, self.system.box, self.style.r_c, self.config.skin, style=self._list_style,
                             newton=self.config.newton, cap_hint=self._cap_hint,
-                            recycle=old[k] if old is not None else None)
+                            recycle=old[k] if old is not None else None, defer=defer)
                       for k, s in enumerate(self.system.stores)]
-        self._cap_hint = max(nl.alloc_cap for nl in self.lists)
+        if not defer:
+            self._cap_hint = max(nl.alloc_cap for nl in self.lists)
         self.n_rebuilds += 1
+
+    def _settle_lists(self) -> bool:
+        """Finish deferred builds; False when a table overflowed and was regrown."""
+        ok = True
+        for k, nl in enumerate(self.lists):
+            self.lists[k], good = nl.settle()
+            ok &= good
+        self._cap_hint = max(nl.alloc_cap for nl in self.lists)
+        return ok
 
     def _forces_device(self, gate=None, gate_limit: float = 0.0):
         if gate is not None:
@@ -447,8 +458,15 @@ class Simulation:
         self._packed = False
         self._spec_e = None
         if self._half_kick_drift():
-            self._rebuild_lists()
+            # with a gated style the build's capacity check is deferred: the force launch
+            # (gated on the device-side count) queues behind the build without a host
+            # round trip, and only an overflow (rare: cap grows x1.5) repeats it
+            defer = (not self.config.distributed and getattr(self.style, "supports_gate", False)
+                     and self._cap_hint is not None)
+            self._rebuild_lists(defer=defer)
             e = self._forces_device()
+            if defer and not self._settle_lists():
+                e = self._forces_device()
         else:
             if not self._packed:
                 self.system.forward_comm()

@@ -64,6 +64,29 @@ class NeighborList:
         self.ref_dev = store.x[: max(store.n_local, 1)].clone() if ref_buf is None else _ref_into(ref_buf, store)
         self._d2 = torch.zeros(1, dtype=torch.float64, device=store.device)
         self._pairs = None
+        self._pending = None   # deferred capacity check: (device max count, build args)
+
+    @property
+    def pending(self) -> bool:
+        return self._pending is not None
+
+    def settle(self) -> "tuple[NeighborList, bool]":
+        """Complete a deferred build (`build(..., defer=True)`): read the max count
+        (one sync).  Returns (list, True) when the table held every row, else a
+        list rebuilt with the grown capacity and False (a force launch gated on
+        this list's count was a no-op and must be repeated)."""
+        if self._pending is None:
+            return self, True
+        mc, box, capacity = self._pending
+        self._pending = None
+        need = int(mc.item())
+        if need <= self.alloc_cap:
+            self.max_count = need
+            self.max_neighbors = grow_capacity(capacity, need)
+            return self, True
+        nl = build(self.store, box, self.cutoff, self.skin, self.style, self.newton, capacity,
+                   cap_hint=grow_capacity(self.alloc_cap, need), recycle=self)
+        return nl, False
 
     @property
     def build_cutoff(self) -> float:
@@ -186,7 +209,7 @@ _cache: dict = {}
 
 def build(store: AtomStore, box: Box, cutoff: float, skin: float, style: str = "full",
           newton: bool = True, capacity: int = DEFAULT_CAPACITY, cap_hint: int | None = None,
-          recycle: NeighborList | None = None, **_unused) -> NeighborList:
+          recycle: NeighborList | None = None, defer: bool = False, **_unused) -> NeighborList:
     """One rank's list from its local + ghost rows (mdkk/neighbor.py:182-219).
 
     Owned rows must be cell-sorted for compact clusters (RankedSystem keeps
@@ -195,6 +218,9 @@ def build(store: AtomStore, box: Box, cutoff: float, skin: float, style: str = "
     always follows the reference growth sequence from `capacity`.
     `recycle` (engine-internal) is a list that is dead after this call: its
     device buffers are reused instead of allocating a new ~GB table.
+    `defer` (engine-internal, with `cap_hint`): one launch, no host sync; the
+    capacity check waits for `NeighborList.settle()` so that work gated on the
+    device-side count (mdkk_lj_force_gated) can be queued first.
     """
     if style not in STYLES:
         raise NeighborError(f"unknown list style {style!r}")
@@ -227,6 +253,17 @@ def build(store: AtomStore, box: Box, cutoff: float, skin: float, style: str = "
     old_t = recycle.table_dev if recycle is not None else None
     counts = _recycled(recycle.counts_dev if recycle is not None else None, (max(n_local, 1),), torch.int32, dev)
     mc = torch.zeros(1, dtype=torch.int32, device=dev)
+    if defer and cap_hint is not None:
+        table = _recycled(old_t, ((n_local + 31) // 32 or 1, alloc, 32), torch.int32, dev)
+        _lib.check(lib.mdkk_nbr_build(ctx, store.x.data_ptr(), n_local, n_total, garr, narr, cstart.data_ptr(),
+                                      catoms.data_ptr(), store.gid.data_ptr(), store.orank.data_ptr(),
+                                      store.rank, bc, STYLES[style], int(bool(newton)), alloc,
+                                      table.data_ptr(), counts.data_ptr(), mc.data_ptr(), stream),
+                   "mdkk_nbr_build")
+        nl = NeighborList(store, style, newton, cutoff, skin, alloc, table, counts, alloc,
+                          ref_buf=recycle.ref_dev if recycle is not None else None)
+        nl._pending = (mc, box, capacity)
+        return nl
     while True:
         table = _recycled(old_t, ((n_local + 31) // 32 or 1, alloc, 32), torch.int32, dev)
         mc.zero_()

@@ -106,12 +106,17 @@ def lj_force_rank(store, nl: NeighborList, params: PairParams, ev: torch.Tensor,
         store.f.zero_()
     # mode "atom": one thread per owned atom; "neighbor": a team of lanes per atom
     # splitting its list (mdkk/pair_lj.py:118-143)
-    if gate is not None:
+    pend = nl._pending
+    if gate is not None or pend is not None:
+        # speculative launch: skipped on the device if the step rebuilds (gate) or the
+        # deferred build overflowed its table (count gate; see NeighborList.settle)
         _lib.check(_lib.lib().mdkk_lj_force_gated(
             _lib.ctx(dev), store.x.data_ptr(), store.n_local, nl.table_dev.data_ptr(), nl.counts_dev.data_ptr(),
             nl.alloc_cap, STYLES[nl.style], int(nl.newton), int(virial), int(mode == "neighbor"), params.epsilon,
-            params.sigma, params.r_c, store.f.data_ptr(), ev.data_ptr(), flags.data_ptr(), gate.data_ptr(),
-            gate_limit, _lib.stream(dev)), "mdkk_lj_force_gated")
+            params.sigma, params.r_c, store.f.data_ptr(), ev.data_ptr(), flags.data_ptr(),
+            gate.data_ptr() if gate is not None else None, gate_limit,
+            pend[0].data_ptr() if pend is not None else None, nl.alloc_cap, _lib.stream(dev)),
+            "mdkk_lj_force_gated")
         return
     fn = "mdkk_lj_force_neighbor" if mode == "neighbor" else "mdkk_lj_force"
     _lib.check(getattr(_lib.lib(), fn)(

@@ -1,0 +1,91 @@
+"""The engine's speculative launches give exactly the unpipelined results.
+
+`Simulation.step_device` queues the force launch before the host has read the
+step's skin test (mdkk_lj_force_gated skips it on the device when the step
+rebuilds) and, on rebuild steps, before the build's capacity check
+(`build(..., defer=True)` + `NeighborList.settle`).  Both must be invisible:
+same trajectory bit for bit as the synchronous path, including a table
+overflow that forces the regrow-and-relaunch branch.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+MELT = """\
+units lj
+boundary p p p
+lattice fcc 0.8442
+create_box 8 8 8
+create_atoms
+mass 1.0
+velocity 1.44 87287
+pair_style lj/cut 2.5
+pair_coeff 1.0 1.0
+timestep 0.005
+thermo 10
+"""
+
+
+def _sim(style="full"):
+    from paper_2508_13523_b200.driver import RunConfig, Simulation
+    sim = Simulation(RunConfig(list_style=style, newton=(style == "half")), log=None)
+    sim.execute(MELT)
+    return sim
+
+
+@pytest.mark.parametrize("style", ["full", "half"])
+def test_speculative_loop_matches_synchronous_loop(gpu, style):
+    a, b = _sim(style), _sim(style)
+    b.style.supports_gate = False          # the plain synchronous step
+    ra, rb = a.run_nve(60), b.run_nve(60)
+    assert ra.n_rebuilds == rb.n_rebuilds and ra.n_rebuilds >= 3
+    if style == "full":   # owner writes: bit-identical
+        assert ra.lines == rb.lines
+        assert np.array_equal(a.system.gather_positions(), b.system.gather_positions())
+    else:                 # FP64 atomics: summation order may differ
+        for (s0, *r0), (s1, *r1) in zip(ra.rows, rb.rows):
+            assert s0 == s1 and np.allclose(r0, r1, rtol=1e-12, atol=1e-12)
+
+
+def test_gated_launch_is_a_no_op_when_the_step_rebuilds(gpu):
+    import torch
+    from paper_2508_13523_b200.pair_lj import lj_force_rank
+    sim = _sim()
+    sim.run_nve(0)
+    s, nl = sim.system.stores[0], sim.lists[0]
+    before = s.f.clone()
+    ev = torch.zeros(7, dtype=torch.float64, device=s.device)
+    flags = torch.zeros(1, dtype=torch.int32, device=s.device)
+    d2 = torch.tensor([0.2 ** 2], dtype=torch.float64, device=s.device)   # sqrt = 0.2 > skin/2
+    s.f.fill_(7.0)
+    lj_force_rank(s, nl, sim.style.kernel.params, ev, flags, virial=False, gate=d2, gate_limit=0.15)
+    assert bool((s.f == 7.0).all())
+    d2.fill_(0.1 ** 2)                                                     # 0.1 <= skin/2: runs
+    s.f.copy_(before)
+    lj_force_rank(s, nl, sim.style.kernel.params, ev, flags, virial=False, gate=d2, gate_limit=0.15)
+    assert torch.equal(s.f[: s.n_local], before[: s.n_local])
+
+
+def test_deferred_build_overflow_regrows_and_relaunches(gpu):
+    sim = _sim()
+    sim.run_nve(5)
+    sim._rebuild_lists()                       # reference: synchronous build
+    e_ref = float(sim._forces_device().item())
+    f_ref = sim.system.gather_forces()
+    cap_ref = sim.lists[0].max_neighbors
+    for hint, expect_ok in ((sim._cap_hint, True), (8, False)):
+        sim._cap_hint = hint
+        sim._rebuild_lists(defer=True)
+        assert sim.lists[0].pending
+        sim._forces_device()
+        ok = sim._settle_lists()
+        assert ok is expect_ok and not sim.lists[0].pending
+        e = float(sim._forces_device().item()) if not ok else float(sim._e_dev.item())
+        assert e == e_ref
+        assert np.array_equal(sim.system.gather_forces(), f_ref)
+        assert sim.lists[0].max_neighbors == cap_ref          # the reference growth sequence
+        assert sim.lists[0].alloc_cap >= sim.lists[0].max_count
