@@ -227,6 +227,7 @@ class AtomStore:
         self.f = torch.zeros_like(x)
         self.orank = torch.full((cap,), self.rank, dtype=torch.int32, device=self.device)
         self.oidx = torch.arange(cap, dtype=torch.int32, device=self.device)
+        self.pos = None
         self.lo = self.hi = None  # brick bounds, set by RankedSystem
         self._lengths = None
         self._lanes_in = []       # lanes whose ghost rows live here (for ghost_shift)
@@ -239,11 +240,15 @@ class AtomStore:
         return self.x.shape[0]
 
     def _views(self):
-        nt = max(self.n_total, 1)
-        self.pos = DualArray((nt, 3), device=self.device, pad_last=4, storage_b=self.x[:nt], layout_b=_ROW)
-        self.vel = DualArray((max(self.n_local, 1), 3), device=self.device, pad_last=4,
-                             storage_b=self.v[: max(self.n_local, 1)], layout_b=_ROW)
-        self.force = DualArray((nt, 3), device=self.device, pad_last=4, storage_b=self.f[:nt], layout_b=_ROW)
+        nt, nl = max(self.n_total, 1), max(self.n_local, 1)
+        if getattr(self, "pos", None) is None:
+            self.pos = DualArray((nt, 3), device=self.device, pad_last=4, storage_b=self.x[:nt], layout_b=_ROW)
+            self.vel = DualArray((nl, 3), device=self.device, pad_last=4, storage_b=self.v[:nl], layout_b=_ROW)
+            self.force = DualArray((nt, 3), device=self.device, pad_last=4, storage_b=self.f[:nt], layout_b=_ROW)
+        else:   # rebuilds: re-point the existing mirrors (fresh and clean, as new ones would be)
+            self.pos.rebind((nt, 3), self.x[:nt])
+            self.vel.rebind((nl, 3), self.v[:nl])
+            self.force.rebind((nt, 3), self.f[:nt])
         self._host_cache = {}
 
     def ensure_capacity(self, rows: int) -> None:
@@ -473,14 +478,15 @@ class RankedSystem:
                 sst = self.stores[s]
                 _lib.check(lib.mdkk_gather_i64(sst.gid.data_ptr(), ix.data_ptr(), t, dst.gid[cur:].data_ptr(),
                                                stream), "mdkk_gather_i64")
-                dst.orank[cur:cur + t].fill_(s)
+                if self.n_ranks > 1:   # one rank: orank is uniformly 0 from allocation on
+                    dst.orank[cur:cur + t].fill_(s)
                 dst.oidx[cur:cur + t].copy_(ix)
                 ln = _Lane(s, dst.rank, ix, code, cur, t)
                 self.lanes.append(ln)
                 dst._lanes_in.append(ln)
                 cur += t
             dst.n_ghost = ng
-            if nl:
+            if nl and self.n_ranks > 1:
                 dst.orank[:nl].fill_(dst.rank)
             dst._views()
         self._pack_all()

@@ -166,6 +166,16 @@ class DualArray:
         self.sync(space)
         return self.view(space)
 
+    def rebind(self, shape, storage_b) -> "DualArray":
+        """Re-point this array at new device storage of a new leading extent (same
+        dtype / layouts / padding): a fresh, clean mirror without re-running the
+        constructor (the engine re-views its row buffers at every rebuild)."""
+        self.shape = tuple(int(s) for s in shape)
+        self.data_b = storage_b
+        self._data_a = None
+        self.modified_a = self.modified_b = False
+        return self
+
 
 def create_dual(shape, layout_a=None, layout_b=None, dtype=np.float64, device=None, **kw) -> DualArray:
     return DualArray(shape, layout_a=layout_a, layout_b=layout_b, dtype=dtype, device=device, **kw)

@@ -77,9 +77,10 @@ class NeighborList:
         this list's count was a no-op and must be repeated)."""
         if self._pending is None:
             return self, True
-        mc, box, capacity = self._pending
+        mc, box, capacity, pin, ready = self._pending
         self._pending = None
-        need = int(mc.item())
+        ready.synchronize()
+        need = int(pin[0])
         if need <= self.alloc_cap:
             self.max_count = need
             self.max_neighbors = grow_capacity(capacity, need)
@@ -260,9 +261,17 @@ def build(store: AtomStore, box: Box, cutoff: float, skin: float, style: str = "
                                       store.rank, bc, STYLES[style], int(bool(newton)), alloc,
                                       table.data_ptr(), counts.data_ptr(), mc.data_ptr(), stream),
                    "mdkk_nbr_build")
+        # the count read-back is queued right behind the build (pinned, async): settle()
+        # then waits on this event only, not on the work queued after it
+        pin = cache.bufs.get("mc_pin")
+        if pin is None:
+            pin = cache.bufs["mc_pin"] = torch.zeros(1, dtype=torch.int32, pin_memory=True)
+        pin.copy_(mc, non_blocking=True)
+        ready = torch.cuda.Event()
+        ready.record(torch.cuda.current_stream(dev))
         nl = NeighborList(store, style, newton, cutoff, skin, alloc, table, counts, alloc,
                           ref_buf=recycle.ref_dev if recycle is not None else None)
-        nl._pending = (mc, box, capacity)
+        nl._pending = (mc, box, capacity, pin, ready)
         return nl
     while True:
         table = _recycled(old_t, ((n_local + 31) // 32 or 1, alloc, 32), torch.int32, dev)
