@@ -22,7 +22,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .memspace import DualArray
+from .memspace import DualArray, download, upload
 
 
 class DomainError(RuntimeError):
@@ -127,7 +127,7 @@ def _rows4(n: int, device, zero: bool = True) -> torch.Tensor:
 def _to4(a: np.ndarray, device, cap: int | None = None) -> torch.Tensor:
     t = _rows4(max(cap or 0, len(a)), device)
     if len(a):
-        t[: len(a), :3] = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(device)
+        t[: len(a), :3] = upload(np.asarray(a, dtype=np.float64), device)
     return t
 
 
@@ -167,8 +167,8 @@ def device_partition(box: Box, rs: RankSet, positions, velocities, global_ids, d
     x = _rows4(cap_all, device)
     v = _rows4(n, device)
     if n:
-        x[:n, :3] = torch.from_numpy(pos).to(device)
-        v[:n, :3] = torch.from_numpy(vel).to(device)
+        x[:n, :3] = upload(pos, device)
+        v[:n, :3] = upload(vel, device)
         _lib.check(lib.mdkk_wrap(x.data_ptr(), n, _lib.dbl3(box.lengths), stream), "mdkk_wrap")
     if R == 1:
         g = torch.zeros(cap_all, dtype=torch.int64, device=device)
@@ -623,19 +623,13 @@ class RankedSystem:
         n = self.n_atoms
         if self.dense_gids:
             lib, stream = _lib.lib(), _lib.stream(self.device)
-            out = _rows4(n, self.device)
+            out = _rows4(n, self.device, zero=False)   # dense gids: every row is written
             for s in self.stores:
                 if s.n_local:
                     gi = s.gid[: s.n_local].to(torch.int32)
                     _lib.check(lib.mdkk_scatter_rows4(rows_fn(s).data_ptr(), gi.data_ptr(), s.n_local,
                                                       out.data_ptr(), stream), "scatter")
-            # device -> pinned staging (full-rate DMA) -> fresh host array
-            pin = self._scratch.get("pin")
-            if pin is None or pin.numel() < n * width:
-                pin = self._scratch["pin"] = torch.empty(max(n * width, 1), dtype=torch.float64, pin_memory=True)
-            stage = pin[: n * width].view(n, width)
-            stage.copy_(out[:n, :width])
-            return stage.numpy().copy()
+            return download(out[:n, :width])
         rows = np.concatenate([rows_fn(s)[: s.n_local, :width].cpu().numpy() for s in self.stores])
         gid = np.concatenate([s.global_ids[: s.n_local] for s in self.stores])
         return rows[np.argsort(gid, kind="stable")]
