@@ -141,29 +141,50 @@ __global__ void __launch_bounds__(kWarps * 32) k_nbr_build(
     const double hwx = 0.5 * (bmax_x - bmin_x), hwy = 0.5 * (bmax_y - bmin_y), hwz = 0.5 * (bmax_z - bmin_z);
     // 2. union of candidate rows
     int m = 0;
+    // the z-run bounds of the first 32 (cx, cy) columns are loaded up front, one per
+    // lane, so the runs' row loads do not wait on a cell_start round trip each
+    const int ny = chi.y - clo.y + 1, nrun = (chi.x - clo.x + 1) * ny;
+    int run_s0 = 0, run_s1 = 0;
+    if (lane < nrun) {
+        const int2 kr = mdkk::zrun_keys(g, clo.x + lane / ny, clo.y + lane % ny, clo.z, chi.z);
+        run_s0 = cell_start[kr.x];
+        run_s1 = cell_start[kr.y + 1];
+    }
     for (int cx = clo.x; cx <= chi.x; ++cx) {
         for (int cy = clo.y; cy <= chi.y; ++cy) {
-            const int2 kr = mdkk::zrun_keys(g, cx, cy, clo.z, chi.z);
-            const int s0 = cell_start[kr.x], s1 = cell_start[kr.y + 1];
-            for (int base = s0; base < s1; base += 32) {
-                const int s = base + lane;
-                bool keep = false;
-                int j = 0;
-                if (s < s1) {
-                    j = cell_atoms[s];
-                    const double4 p = mdkk::ld4(x, j);
-                    // distance to the bbox (a superset filter: the margin covers the
-                    // center/half-width rounding; every member is re-tested exactly)
+            const int r = (cx - clo.x) * ny + (cy - clo.y);
+            int s0 = __shfl_sync(0xffffffffu, run_s0, r & 31), s1 = __shfl_sync(0xffffffffu, run_s1, r & 31);
+            if (r >= 32) {
+                const int2 kr = mdkk::zrun_keys(g, cx, cy, clo.z, chi.z);
+                s0 = cell_start[kr.x];
+                s1 = cell_start[kr.y + 1];
+            }
+            // two 32-row batches per pass: both batches' index and position loads are in
+            // flight together (the pass is latency bound); union order is unchanged
+            for (int base = s0; base < s1; base += 64) {
+                const int sa = base + lane, sb = base + 32 + lane;
+                const int ja = sa < s1 ? cell_atoms[sa] : -1;
+                const int jb = sb < s1 ? cell_atoms[sb] : -1;
+                const double4 pa = mdkk::ld4(x, ja >= 0 ? ja : 0);
+                const double4 pb = mdkk::ld4(x, jb >= 0 ? jb : 0);
+                // distance to the bbox (a superset filter: the margin covers the
+                // center/half-width rounding; every member is re-tested exactly)
+                auto near = [&](const double4& p) {
                     double dx = fabs(p.x - ccx) - hwx, dy = fabs(p.y - ccy) - hwy, dz = fabs(p.z - ccz) - hwz;
                     dx = dx > 0.0 ? dx : 0.0;
                     dy = dy > 0.0 ? dy : 0.0;
                     dz = dz > 0.0 ? dz : 0.0;
-                    keep = dx * dx + dy * dy + dz * dz < bc2 * (1.0 + 1e-9);
-                }
-                const unsigned mask = __ballot_sync(0xffffffffu, keep);
-                const int pos = m + __popc(mask & ((1u << lane) - 1u));
-                if (keep && pos < kUnion) su[pos] = j;
-                m += __popc(mask);
+                    return dx * dx + dy * dy + dz * dz < bc2 * (1.0 + 1e-9);
+                };
+                const bool ka = ja >= 0 && near(pa), kb = jb >= 0 && near(pb);
+                const unsigned ma = __ballot_sync(0xffffffffu, ka);
+                const int posa = m + __popc(ma & ((1u << lane) - 1u));
+                if (ka && posa < kUnion) su[posa] = ja;
+                m += __popc(ma);
+                const unsigned mb = __ballot_sync(0xffffffffu, kb);
+                const int posb = m + __popc(mb & ((1u << lane) - 1u));
+                if (kb && posb < kUnion) su[posb] = jb;
+                m += __popc(mb);
             }
         }
     }
