@@ -23,4 +23,4 @@ for _ in range(10):
     sim._rebuild_lists()
 torch.cuda.synchronize()
 pr.disable()
-pstats.Stats(pr).sort_stats("tottime").print_stats(25)
+pstats.Stats(pr).sort_stats("tottime").print_stats(45)
