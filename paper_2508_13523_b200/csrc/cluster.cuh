@@ -1,21 +1,16 @@
-// Cell grid (serpentine order) and the cluster neighbour-table layout shared by
-// the build, force and SNAP kernels.
+// Cell grid (serpentine order) shared by the binning, the spatial sort and the
+// neighbour build.
 //
-// Cluster list format ("mdkk cluster list"):
-//   * owned atoms are cell-sorted; cluster c = owned rows [32c, 32c+32) (one warp)
-//   * union[c][0..ucount[c]) (int32, row stride ucap): every row within the build
-//     cutoff of the cluster's bounding box (the only rows its atoms can list)
-//   * table: uint16 local index u into union[c], blocked so one lane loads 8
-//     entries with one 16-byte load:  ((c*capb + k/8)*32 + lane)*8 + k%8,
-//     capb = cap/8.  counts[i] entries are valid for row i.
-// Positions of union[c] are staged in shared memory by the force kernels.
+// Neighbour table layout ("cluster-blocked"): owned rows are cell-sorted and
+// cluster c = rows [32c, 32c+32) (one warp in the build and force kernels);
+// table[c][k][lane] (int32, row index of the k-th partner of row 32c+lane) so
+// every per-k read of a warp is one coalesced 128-byte line; counts[i] entries
+// are valid for row i, the rest undefined.
 #pragma once
 
 #include "common.cuh"
 
 namespace mdkk {
-
-constexpr int kClusterSize = 32;
 
 struct Grid {
     double ox, oy, oz;
@@ -61,8 +56,5 @@ __device__ __forceinline__ int2 zrun_keys(const Grid& g, int cx, int cy, int z0,
                      : make_int2(col * g.nz + z0, col * g.nz + z1);
 }
 
-__device__ __forceinline__ long long tbl_index(int c, int capb, int k, int lane) {
-    return ((((long long)c * capb + (k >> 3)) * kClusterSize + lane) << 3) + (k & 7);
-}
 
 }  // namespace mdkk

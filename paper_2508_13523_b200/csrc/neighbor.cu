@@ -276,11 +276,25 @@ __global__ void __launch_bounds__(kWarps * 32) k_nbr_build(
                         bits |= ((!in0 && r0 < bc2f) ? (1u << t) : 0u) | ((!in1 && r1 < bc2f) ? (2u << t) : 0u);
                     }
                 } else {
+                    // half lists: certain members that are owned rows only need the gid
+                    // rule (mdkk/neighbor.py:146-150; gi < gj also excludes i itself) and
+                    // are stored here, branch-free; ghosts (owner-rank / zyx rules) and the
+                    // shell take the exact path below
 #pragma unroll
-                    for (int t = 0; t < 32; t += 2) {   // entries past cn are stale but masked below
+                    for (int t = 0; t < 32; t += 2) {   // pads sit at +1e18: never hits
                         float r0, r1;
                         r2_pair(sfx + h0 + t, sfy + h0 + t, sfz + h0 + t, fxi2, fyi2, fzi2, r0, r1);
-                        bits |= ((r0 < bc2f) ? (1u << t) : 0u) | ((r1 < bc2f) ? (2u << t) : 0u);
+                        const int2 jj = *reinterpret_cast<const int2*>(su + u0 + h0 + t);
+                        const bool c0 = r0 < lo2f && jj.x < n_local, c1 = r1 < lo2f && jj.y < n_local;
+                        if (c0 && gi < sgid[h0 + t]) {
+                            trow[(long long)min(cnt, cap - 1) * 32] = jj.x;
+                            ++cnt;
+                        }
+                        if (c1 && gi < sgid[h0 + t + 1]) {
+                            trow[(long long)min(cnt, cap - 1) * 32] = jj.y;
+                            ++cnt;
+                        }
+                        bits |= ((!c0 && r0 < bc2f) ? (1u << t) : 0u) | ((!c1 && r1 < bc2f) ? (2u << t) : 0u);
                     }
                 }
                 if (lim < 32) bits &= (1u << lim) - 1u;
