@@ -420,13 +420,24 @@ class Simulation:
         # the step's one host sync: a pinned 8-byte read-back, no reduction kernel for one rank
         if self._d2_host is None:
             self._d2_host = torch.zeros(1, dtype=torch.float64, pin_memory=True)
-        self._d2_host.copy_(worst, non_blocking=True)
         if self.config.distributed:
+            self._d2_host.copy_(worst, non_blocking=True)
             torch.cuda.current_stream(self.device).synchronize()
         else:
+            # the read-back runs on a side stream: the compute stream goes straight on to the
+            # speculative pack + force launch instead of waiting out the copy-engine round
+            # trip (the next step's verlet_first, which rewrites the maximum, is only issued
+            # after the host has waited for this copy)
+            main = torch.cuda.current_stream(self.device)
             if self._d2_ready is None:
                 self._d2_ready = torch.cuda.Event()
-            self._d2_ready.record(torch.cuda.current_stream(self.device))
+                self._d2_kicked = torch.cuda.Event()
+                self._side = torch.cuda.Stream(self.device)
+            self._d2_kicked.record(main)
+            self._side.wait_event(self._d2_kicked)
+            with torch.cuda.stream(self._side):
+                self._d2_host.copy_(worst, non_blocking=True)
+            self._d2_ready.record(self._side)
             # speculative halo refresh, queued behind the read-back: a plain step needs
             # it next, and a rebuild simply overwrites the ghost rows
             self.system.forward_comm()
