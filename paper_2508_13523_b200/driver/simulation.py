@@ -204,7 +204,6 @@ class Simulation:
         self.results: list[RunResult] = []
         self.n_rebuilds = 0
         self._cap_hint = None
-        self._ucap_hint = None
         self.snapshots = True
         dev = self.config.device
         self.device = torch.device(dev) if dev is not None else torch.device("cuda", torch.cuda.current_device())

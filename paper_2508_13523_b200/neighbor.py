@@ -214,8 +214,8 @@ def build(store: AtomStore, box: Box, cutoff: float, skin: float, style: str = "
     """One rank's list from its local + ghost rows (mdkk/neighbor.py:182-219).
 
     Owned rows must be cell-sorted for compact clusters (RankedSystem keeps
-    them so); any order is still correct.  `cap_hint` / `ucap_hint`
-    (engine-internal) size the first launch; the reported `max_neighbors`
+    them so); any order is still correct.  `cap_hint`
+    (engine-internal) sizes the first launch; the reported `max_neighbors`
     always follows the reference growth sequence from `capacity`.
     `recycle` (engine-internal) is a list that is dead after this call: its
     device buffers are reused instead of allocating a new ~GB table.
