@@ -85,6 +85,11 @@ int mdkk_pack_shift(const double* x, const int* idx, const int8_t* code, const d
                     int n, double* out, void* stream);
 /* Reverse-comm unpack: f[idx[k]] += buf[k] (FP64 atomics; idx may repeat). */
 int mdkk_fold_add(double* f, const int* idx, const double* buf, int n, void* stream);
+/* A lane's new ghost rows in one pass (exchange_ghosts, mdkk/domain.py:276-293):
+ * out_x[k] = x[idx[k]] + shift_table[code[k]] (as mdkk_pack_shift), out_gid[k] =
+ * gid[idx[k]], out_oidx[k] = idx[k]. */
+int mdkk_ghost_rows(const double* x, const int64_t* gid, const int* idx, const int8_t* code, const double* shifts,
+                    int n, double* out_x, int64_t* out_gid, int* out_oidx, void* stream);
 /* Gather rows by permutation: dst[i] = src[perm[i]] for double4 rows / int64 / int32. */
 int mdkk_gather_rows4(const double* src, const int* perm, int n, double* dst, void* stream);
 int mdkk_gather_i64(const int64_t* src, const int* perm, int n, int64_t* dst, void* stream);

@@ -34,6 +34,7 @@ SIGNATURES = {
     "mdkk_wrap": [_p, _i, _p, _p],
     "mdkk_halo_count": [_p, _p, _i, _p, _i, _p, _p, _p],
     "mdkk_halo_fill": [_p, _p, _i, _p, _i, _p, _p, _p, _p, _p, _p],
+    "mdkk_ghost_rows": [_p, _p, _p, _p, _p, _i, _p, _p, _p, _p],
     "mdkk_pack_shift": [_p, _p, _p, _p, _i, _p, _p],
     "mdkk_fold_add": [_p, _p, _p, _i, _p],
     "mdkk_gather_rows4": [_p, _p, _i, _p, _p],

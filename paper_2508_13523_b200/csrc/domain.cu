@@ -166,6 +166,21 @@ __global__ void k_pack_shift(const double* __restrict__ x, const int* __restrict
     mdkk::st4(out, k, make_double4(p.x + s[0], p.y + s[1], p.z + s[2], 0.0));
 }
 
+// New ghost rows in one pass: position (= pack), global id and owner index.
+__global__ void k_ghost_rows(const double* __restrict__ x, const int64_t* __restrict__ gid,
+                             const int* __restrict__ idx, const int8_t* __restrict__ code,
+                             const double* __restrict__ shifts, int n, double* __restrict__ out_x,
+                             int64_t* __restrict__ out_gid, int* __restrict__ out_oidx) {
+    int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const int i = idx[k];
+    double4 p = mdkk::ld4_nc(x, i);
+    const double* s = shifts + 3 * code[k];
+    mdkk::st4(out_x, k, make_double4(p.x + s[0], p.y + s[1], p.z + s[2], 0.0));
+    out_gid[k] = gid[i];
+    out_oidx[k] = i;
+}
+
 __global__ void k_fold_add(double* __restrict__ f, const int* __restrict__ idx,
                            const double* __restrict__ buf, int n) {
     int k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -237,6 +252,16 @@ int mdkk_pack_shift(const double* x, const int* idx, const int8_t* code, const d
     if (n == 0) return MDKK_OK;
     k_pack_shift<<<mdkk::grid_for(n, 256), 256, 0, mdkk::as_stream(stream)>>>(x, idx, code, shifts, n, out);
     MDKK_CHECK_LAUNCH("k_pack_shift");
+    return MDKK_OK;
+}
+
+int mdkk_ghost_rows(const double* x, const int64_t* gid, const int* idx, const int8_t* code, const double* shifts,
+                    int n, double* out_x, int64_t* out_gid, int* out_oidx, void* stream) {
+    if (n < 0) return MDKK_E_ARG;
+    if (n == 0) return MDKK_OK;
+    k_ghost_rows<<<mdkk::grid_for(n, 256), 256, 0, mdkk::as_stream(stream)>>>(x, gid, idx, code, shifts, n, out_x,
+                                                                              out_gid, out_oidx);
+    MDKK_CHECK_LAUNCH("k_ghost_rows");
     return MDKK_OK;
 }
 

@@ -427,6 +427,8 @@ class RankedSystem:
         ctx = _lib.ctx(self.device)
         for s in self.stores:
             s.to_device()
+        if self.n_ranks == 1 and self.stores[0].n_local and self._combos(0, halo)[0]:
+            return self._exchange_single(halo, lib, stream, ctx)
         plans = []
         for src in self.stores:
             meta, tab, codes = self._combos(src.rank, halo)
@@ -492,6 +494,39 @@ class RankedSystem:
         self._pack_all()
         for s in self.stores:
             s.device_wrote(pos=True)
+
+    def _exchange_single(self, halo, lib, stream, ctx) -> None:
+        """One rank (periodic self-images only): the same selection, lane and rows as the
+        general path with a fraction of its host work -- one pinned totals read-back and
+        one fused ghost-row kernel (position + gid + owner index)."""
+        s = self.stores[0]
+        meta, tab, codes = self._combos(0, halo)
+        C_, nl = len(meta), s.n_local
+        nb = (nl + 255) // 256
+        blk = self._buf("blk0", nb * C_, torch.int32)
+        tot = self._buf("tot0", C_, torch.int32)[:C_]
+        _lib.check(lib.mdkk_halo_count(ctx, s.x.data_ptr(), nl, tab.data_ptr(), C_, blk.data_ptr(), tot.data_ptr(),
+                                       stream), "mdkk_halo_count")
+        pin = self._scratch.get("tot_pin")
+        if pin is None or pin.numel() < C_:
+            pin = self._scratch["tot_pin"] = torch.zeros(max(C_, 64), dtype=torch.int32, pin_memory=True)
+        pin[:C_].copy_(tot, non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        ng = int(pin[:C_].numpy().astype(np.int64).sum())
+        idx = self._buf("idx0", ng + 1, torch.int32)
+        cds = self._buf("cds0", ng + 1, torch.int8)
+        _lib.check(lib.mdkk_halo_fill(ctx, s.x.data_ptr(), nl, tab.data_ptr(), C_, blk.data_ptr(), tot.data_ptr(),
+                                      idx.data_ptr(), codes.data_ptr(), cds.data_ptr(), stream), "mdkk_halo_fill")
+        s.ensure_capacity(nl + ng)
+        _lib.check(lib.mdkk_ghost_rows(s.x.data_ptr(), s.gid.data_ptr(), idx.data_ptr(), cds.data_ptr(),
+                                       self._shift_dev.data_ptr(), ng, s.x[nl:].data_ptr(), s.gid[nl:].data_ptr(),
+                                       s.oidx[nl:].data_ptr(), stream), "mdkk_ghost_rows")
+        ln = _Lane(0, 0, idx[:ng], cds[:ng], nl, ng)
+        self.lanes = [ln] if ng else []
+        s._lanes_in = list(self.lanes)
+        s.n_ghost = ng
+        s._views()
+        s.device_wrote(pos=True)
 
     def _pack_all(self):
         lib, stream = _lib.lib(), _lib.stream(self.device)
@@ -599,13 +634,12 @@ class RankedSystem:
             return
         lib, stream = _lib.lib(), _lib.stream(self.device)
         ctx = _lib.ctx(self.device)
-        g, nc = cell_grid(s.lo, s.hi, 0.0, width)   # bins tile the brick exactly: full cells everywhere
-        ncell = nc[0] * nc[1] * nc[2]
+        _, _, garr, narr, ncell = grid_args(s.lo, s.hi, 0.0, width)   # bins tile the brick exactly
         n = s.n_local
         keys = self._buf(f"sk{s.rank}", n, torch.int32)
         start = self._buf(f"ss{s.rank}", ncell + 1, torch.int32)
         order = self._buf(f"so{s.rank}", n, torch.int32)
-        _lib.check(lib.mdkk_bin_atoms(ctx, s.x.data_ptr(), n, _lib.dbl3(g), _lib.int_arr(nc),
+        _lib.check(lib.mdkk_bin_atoms(ctx, s.x.data_ptr(), n, garr, narr,
                                       keys.data_ptr(), start.data_ptr(), order.data_ptr(), stream), "bin")
         if s._alt is None or s._alt[0].shape[0] != s.capacity or s._alt[1].shape[0] < n:
             s._alt = (_rows4(s.capacity, self.device, zero=False), _rows4(s.v.shape[0], self.device, zero=False),
@@ -663,6 +697,22 @@ class RankedSystem:
             s.force.sync("b")
             s.f.zero_()
             s.device_wrote(force=True)
+
+
+_GRID_MEMO: dict = {}
+
+
+def grid_args(lo, hi, halo: float, width: float):
+    """cell_grid plus its ctypes arrays, memoised (bricks are fixed for a run): (grid,
+    ncell[3], grid_c, ncell_c, total cells)."""
+    key = (*(float(v) for v in lo), *(float(v) for v in hi), float(halo), float(width))
+    hit = _GRID_MEMO.get(key)
+    if hit is None:
+        if len(_GRID_MEMO) > 256:
+            _GRID_MEMO.clear()
+        g, nc = cell_grid(lo, hi, halo, width)
+        hit = _GRID_MEMO[key] = (g, nc, _lib.dbl3(g), _lib.int_arr(nc), nc[0] * nc[1] * nc[2])
+    return hit
 
 
 def cell_grid(lo, hi, halo: float, width: float):

@@ -16,7 +16,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .domain import AtomStore, Box, RankedSystem, cell_grid
+from .domain import AtomStore, Box, RankedSystem, grid_args
 from .memspace import DualArray, LayoutPolicy
 
 DEFAULT_CAPACITY = 16
@@ -62,7 +62,7 @@ class NeighborList:
         self.table_dev = table
         self.counts_dev = counts
         self.ref_dev = store.x[: max(store.n_local, 1)].clone() if ref_buf is None else _ref_into(ref_buf, store)
-        self._d2 = torch.zeros(1, dtype=torch.float64, device=store.device)
+        self._d2 = torch.empty(1, dtype=torch.float64, device=store.device)   # written before every read
         self._pairs = None
         self._pending = None   # deferred capacity check: (device max count, build args)
 
@@ -235,13 +235,11 @@ def build(store: AtomStore, box: Box, cutoff: float, skin: float, style: str = "
     n_local, n_total = store.n_local, store.n_total
     lo = store.lo if store.lo is not None else np.zeros(3)
     hi = store.hi if store.hi is not None else box.lengths
-    g, nc = cell_grid(lo, hi, bc, bc)
-    ncell = nc[0] * nc[1] * nc[2]
+    _, _, garr, narr, ncell = grid_args(lo, hi, bc, bc)
     cache = _cache.setdefault((str(dev), store.rank), _BuildCache())
     keys = cache.get("keys", n_total, torch.int32, dev)
     cstart = cache.get("cstart", ncell + 1, torch.int32, dev)
     catoms = cache.get("catoms", n_total, torch.int32, dev)
-    garr, narr = _lib.dbl3(g), _lib.int_arr(nc)
     _lib.check(lib.mdkk_bin_atoms(ctx, store.x.data_ptr(), n_total, garr, narr, keys.data_ptr(),
                                   cstart.data_ptr(), catoms.data_ptr(), stream), "mdkk_bin_atoms")
     if cap_hint is None and n_local:
