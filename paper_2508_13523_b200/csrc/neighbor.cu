@@ -66,6 +66,14 @@ __global__ void k_cell_sort(int ncell, const int* __restrict__ start, int* __res
     }
 }
 
+__global__ void k_cell_positions(const double* __restrict__ x, const int* __restrict__ cell_atoms, int n,
+                                 float4* __restrict__ xs) {
+    int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    const double4 p = mdkk::ld4(x, cell_atoms[s]);
+    xs[s] = make_float4((float)p.x, (float)p.y, (float)p.z, 0.f);
+}
+
 __device__ __forceinline__ bool lex_zyx_less(double ax, double ay, double az, double bx, double by, double bz) {
     // mdkk/neighbor.py:163-166: z, then y, then x
     return (az < bz) || (az == bz && (ay < by || (ay == by && ax < bx)));
@@ -107,7 +115,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_nbr_build(
     const double* __restrict__ x, int n_local, Grid g, const int* __restrict__ cell_start,
     const int* __restrict__ cell_atoms, const int64_t* __restrict__ gid, const int32_t* __restrict__ owner_rank,
     int my_rank, double bc, double bc2, int cap, int* __restrict__ table, int* __restrict__ counts,
-    int* __restrict__ max_count) {
+    int* __restrict__ max_count, const float4* __restrict__ xs) {
     __shared__ int s_union[kWarps][kUnion];
     __shared__ double s_pos[kWarps][3][kChunk];
     // cluster-relative FP32 coordinates, SoA: an aligned float2 = two candidates for the packed
@@ -139,6 +147,15 @@ __global__ void __launch_bounds__(kWarps * 32) k_nbr_build(
     const int3 chi = mdkk::cell_of(g, bmax_x + bc, bmax_y + bc, bmax_z + bc);
     const double ccx = 0.5 * (bmin_x + bmax_x), ccy = 0.5 * (bmin_y + bmax_y), ccz = 0.5 * (bmin_z + bmax_z);
     const double hwx = 0.5 * (bmax_x - bmin_x), hwy = 0.5 * (bmax_y - bmin_y), hwz = 0.5 * (bmax_z - bmin_z);
+    // FP32 union test: coordinates carry <= 1 ulp of the largest |coordinate| each (the
+    // copy, the center); the radius is widened by 16 such ulps (+ 1e-5 bc) so the union
+    // stays a superset of every member's partners
+    const float ccxf = (float)ccx, ccyf = (float)ccy, cczf = (float)ccz;
+    const float hwxf = (float)hwx, hwyf = (float)hwy, hwzf = (float)hwz;
+    const double ext = fmax(fmax(fmax(fabs(bmin_x), fabs(bmax_x)), fmax(fabs(bmin_y), fabs(bmax_y))),
+                            fmax(fabs(bmin_z), fabs(bmax_z))) + bc;
+    const double ru = bc * (1.0 + 1e-5) + 16.0 * 1.2e-7 * ext;
+    const float ru2f = (float)(ru * ru);
     // 2. union of candidate rows
     int m = 0;
     // the z-run bounds of the first 32 (cx, cy) columns are loaded up front, one per
@@ -165,16 +182,16 @@ __global__ void __launch_bounds__(kWarps * 32) k_nbr_build(
                 const int sa = base + lane, sb = base + 32 + lane;
                 const int ja = sa < s1 ? cell_atoms[sa] : -1;
                 const int jb = sb < s1 ? cell_atoms[sb] : -1;
-                const double4 pa = mdkk::ld4(x, ja >= 0 ? ja : 0);
-                const double4 pb = mdkk::ld4(x, jb >= 0 ? jb : 0);
-                // distance to the bbox (a superset filter: the margin covers the
-                // center/half-width rounding; every member is re-tested exactly)
-                auto near = [&](const double4& p) {
-                    double dx = fabs(p.x - ccx) - hwx, dy = fabs(p.y - ccy) - hwy, dz = fabs(p.z - ccz) - hwz;
-                    dx = dx > 0.0 ? dx : 0.0;
-                    dy = dy > 0.0 ? dy : 0.0;
-                    dz = dz > 0.0 ? dz : 0.0;
-                    return dx * dx + dy * dy + dz * dz < bc2 * (1.0 + 1e-9);
+                // cell-ordered FP32 copies: coalesced, and independent of the index loads
+                const float4 pa = xs[sa < s1 ? sa : s0], pb = xs[sb < s1 ? sb : s0];
+                // distance to the bbox in FP32 against a widened radius (a superset
+                // filter: every member is re-tested exactly below)
+                auto near = [&](const float4& p) {
+                    float dx = fabsf(p.x - ccxf) - hwxf, dy = fabsf(p.y - ccyf) - hwyf, dz = fabsf(p.z - cczf) - hwzf;
+                    dx = dx > 0.f ? dx : 0.f;
+                    dy = dy > 0.f ? dy : 0.f;
+                    dz = dz > 0.f ? dz : 0.f;
+                    return dx * dx + dy * dy + dz * dz < ru2f;
                 };
                 const bool ka = ja >= 0 && near(pa), kb = jb >= 0 && near(pb);
                 const unsigned ma = __ballot_sync(0xffffffffu, ka);
@@ -474,26 +491,31 @@ int mdkk_bin_atoms(mdkk_ctx* ctx, const double* x, int n, const double* grid_hos
     return mdkk_bucket_sort(ctx, keys, n, (int)ncell, cell_start, cell_atoms, stream);
 }
 
-int mdkk_nbr_build(mdkk_ctx*, const double* x, int n_local, int n_total, const double* grid_host,
+int mdkk_nbr_build(mdkk_ctx* ctx, const double* x, int n_local, int n_total, const double* grid_host,
                    const int* ncell_host, const int* cell_start, const int* cell_atoms, const int64_t* gid,
                    const int32_t* owner_rank, int my_rank, double bc, int style, int newton, int cap, int* table,
                    int* counts, int* max_count, void* stream) {
-    if (n_local < 0 || n_total < n_local || cap < 1 || (style != 0 && style != 1)) return MDKK_E_ARG;
+    if (!ctx || n_local < 0 || n_total < n_local || cap < 1 || (style != 0 && style != 1)) return MDKK_E_ARG;
     if (n_local == 0) return MDKK_OK;
     Grid g = mdkk::make_grid(grid_host, ncell_host);
     cudaStream_t s = mdkk::as_stream(stream);
+    // FP32 positions in cell order for the union pass (coalesced instead of gathered)
+    float4* xs = static_cast<float4*>(mdkk::scratch(ctx, sizeof(float4) * (size_t)std::max(n_total, 1)));
+    if (!xs) return mdkk::cuda_fail(cudaErrorMemoryAllocation, "scratch");
+    k_cell_positions<<<mdkk::grid_for(n_total, 256), 256, 0, s>>>(x, cell_atoms, n_total, xs);
+    MDKK_CHECK_LAUNCH("k_cell_positions");
     const int ncl = (n_local + 31) / 32;
     const int nb = (ncl + kWarps - 1) / kWarps;
     const double bc2 = bc * bc;
     if (style == 0)
         k_nbr_build<0, false><<<nb, kWarps * 32, 0, s>>>(x, n_local, g, cell_start, cell_atoms, gid, owner_rank,
-                                                         my_rank, bc, bc2, cap, table, counts, max_count);
+                                                         my_rank, bc, bc2, cap, table, counts, max_count, xs);
     else if (newton)
         k_nbr_build<1, true><<<nb, kWarps * 32, 0, s>>>(x, n_local, g, cell_start, cell_atoms, gid, owner_rank,
-                                                        my_rank, bc, bc2, cap, table, counts, max_count);
+                                                        my_rank, bc, bc2, cap, table, counts, max_count, xs);
     else
         k_nbr_build<1, false><<<nb, kWarps * 32, 0, s>>>(x, n_local, g, cell_start, cell_atoms, gid, owner_rank,
-                                                         my_rank, bc, bc2, cap, table, counts, max_count);
+                                                         my_rank, bc, bc2, cap, table, counts, max_count, xs);
     MDKK_CHECK_LAUNCH("k_nbr_build");
     return MDKK_OK;
 }
