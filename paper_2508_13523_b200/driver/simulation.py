@@ -419,35 +419,33 @@ class Simulation:
         # the step's one host sync: a pinned 8-byte read-back, no reduction kernel for one rank
         if self._d2_host is None:
             self._d2_host = torch.zeros(1, dtype=torch.float64, pin_memory=True)
-        if self.config.distributed:
+        # (distributed: `worst` is the all-reduced maximum, the same on every rank, so
+        # the speculative halo exchange and force launch below stay collective-matched)
+        # the read-back runs on a side stream: the compute stream goes straight on to the
+        # speculative pack + force launch instead of waiting out the copy-engine round
+        # trip (the next step's verlet_first, which rewrites the maximum, is only issued
+        # after the host has waited for this copy)
+        main = torch.cuda.current_stream(self.device)
+        if self._d2_ready is None:
+            self._d2_ready = torch.cuda.Event()
+            self._d2_kicked = torch.cuda.Event()
+            self._side = torch.cuda.Stream(self.device)
+        self._d2_kicked.record(main)
+        self._side.wait_event(self._d2_kicked)
+        with torch.cuda.stream(self._side):
             self._d2_host.copy_(worst, non_blocking=True)
-            torch.cuda.current_stream(self.device).synchronize()
-        else:
-            # the read-back runs on a side stream: the compute stream goes straight on to the
-            # speculative pack + force launch instead of waiting out the copy-engine round
-            # trip (the next step's verlet_first, which rewrites the maximum, is only issued
-            # after the host has waited for this copy)
-            main = torch.cuda.current_stream(self.device)
-            if self._d2_ready is None:
-                self._d2_ready = torch.cuda.Event()
-                self._d2_kicked = torch.cuda.Event()
-                self._side = torch.cuda.Stream(self.device)
-            self._d2_kicked.record(main)
-            self._side.wait_event(self._d2_kicked)
-            with torch.cuda.stream(self._side):
-                self._d2_host.copy_(worst, non_blocking=True)
-            self._d2_ready.record(self._side)
-            # speculative halo refresh, queued behind the read-back: a plain step needs
-            # it next, and a rebuild simply overwrites the ghost rows
-            self.system.forward_comm()
-            self._packed = True
-            if getattr(self.style, "supports_gate", False):
-                # speculative force launch, gated on the device by the same skin test:
-                # the GPU runs it while the host reads the decision (no idle gap), and
-                # it is a no-op on a rebuilding step (relaunched after the rebuild)
-                self._gate = worst
-                self._spec_e = self._forces_device(gate=worst, gate_limit=0.5 * self.config.skin)
-            self._d2_ready.synchronize()
+        self._d2_ready.record(self._side)
+        # speculative halo refresh, queued behind the read-back: a plain step needs
+        # it next, and a rebuild simply overwrites the ghost rows
+        self.system.forward_comm()
+        self._packed = True
+        if getattr(self.style, "supports_gate", False):
+            # speculative force launch, gated on the device by the same skin test:
+            # the GPU runs it while the host reads the decision (no idle gap), and
+            # it is a no-op on a rebuilding step (relaunched after the rebuild)
+            self._gate = worst
+            self._spec_e = self._forces_device(gate=worst, gate_limit=0.5 * self.config.skin)
+        self._d2_ready.synchronize()
         return math.sqrt(float(self._d2_host[0])) > 0.5 * self.config.skin
 
     def _half_kick(self):
@@ -471,8 +469,10 @@ class Simulation:
             # with a gated style the build's capacity check is deferred: the force launch
             # (gated on the device-side count) queues behind the build without a host
             # round trip, and only an overflow (rare: cap grows x1.5) repeats it
-            defer = (not self.config.distributed and getattr(self.style, "supports_gate", False)
-                     and self._cap_hint is not None)
+            # (distributed half lists excepted: a regrow on one rank would re-run the
+            # reverse-comm collective on that rank alone)
+            defer = (getattr(self.style, "supports_gate", False) and self._cap_hint is not None
+                     and not (self.config.distributed and self._list_style == "half"))
             self._rebuild_lists(defer=defer)
             e = self._forces_device()
             if defer and not self._settle_lists():
