@@ -24,7 +24,7 @@ sys.path.insert(0, REF_SRC)
 from mdkk.domain import Box, RankedSystem  # noqa: E402
 from mdkk.neighbor import build_all  # noqa: E402
 from mdkk.pair_lj import LJCut, PairParams, compute_pair  # noqa: E402
-from mdkk.driver.simulation import RunConfig, run_script, lattice_positions, seeded_velocities  # noqa: E402
+from mdkk.driver.simulation import RunConfig, run_script, lattice_positions  # noqa: E402
 from mdkk.snap import (  # noqa: E402
     SnapState, build_neighbor_map, compute_bi, compute_fused_deidrj, compute_ui,
     compute_yi, make_coupling_tables, QuantumIndex,
