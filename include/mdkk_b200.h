@@ -162,6 +162,19 @@ int mdkk_lj_force(mdkk_ctx* ctx, const double* x, int n_local, const int* table,
 int mdkk_lj_force_neighbor(mdkk_ctx* ctx, const double* x, int n_local, const int* table, const int* counts,
                            int cap, int style, int newton, int virial, double epsilon, double sigma, double rc,
                            double* f, double* ev, int* flags, void* stream);
+/* Full-list force with the velocity-Verlet update fused into its epilogue (the engine's
+ * advance loop; mdkk/driver/simulation.py:431-450): mode 1 = closing half-kick
+ * v += h f; mode 2 = closing + next opening half-kick and drift x_next = x + dt v
+ * for the owned rows (x_next must not alias x: positions are double-buffered; its
+ * ghost rows are refreshed by the next pack) and *d2_next = max |x_next - x_ref|^2
+ * (atomic max; caller-zeroed).  Bit-identical to mdkk_lj_force + mdkk_verlet_second
+ * + mdkk_verlet_first.  Gates as mdkk_lj_force_gated (a gated-off launch changes
+ * nothing). */
+int mdkk_lj_force_integrate(mdkk_ctx* ctx, const double* x, int n_local, const int* table, const int* counts,
+                            int cap, int virial, double epsilon, double sigma, double rc, double* f, double* ev,
+                            int* flags, const double* maxdisp2, double half_skin, const int* max_count,
+                            int count_limit, int mode, double* v, const double* x_ref, double* x_next,
+                            double* d2_next, double dt, double h, void* stream);
 /* Speculative step launch (engine-internal pipelining): as mdkk_lj_force (mode 0) or
  * mdkk_lj_force_neighbor (mode 1), but the kernel does nothing when
  * sqrt(*maxdisp2) > half_skin -- the step's skin test, evaluated on the device in the

@@ -49,6 +49,8 @@ SIGNATURES = {
     "mdkk_nbr_canonicalize": [_p, _p, _i, _i, _p, _p, _p],
     "mdkk_max_disp2": [_p, _p, _i, _p, _p],
     "mdkk_lj_force": [_p, _p, _i, _p, _p, _i, _i, _i, _i, _d, _d, _d, _p, _p, _p, _p],
+    "mdkk_lj_force_integrate": [_p, _p, _i, _p, _p, _i, _i, _d, _d, _d, _p, _p, _p, _p, _d, _p, _i, _i, _p, _p, _p,
+                                _p, _d, _d, _p],
     "mdkk_lj_force_gated": [_p, _p, _i, _p, _p, _i, _i, _i, _i, _i, _d, _d, _d, _p, _p, _p, _p, _d, _p, _i, _p],
     "mdkk_lj_force_neighbor": [_p, _p, _i, _p, _p, _i, _i, _i, _i, _d, _d, _d, _p, _p, _p, _p],
     "mdkk_verlet_first": [_p, _p, _p, _p, _p, _i, _d, _d, _p, _i, _p],

@@ -30,15 +30,33 @@ __device__ __forceinline__ bool gated_off(const Gate& g) {
     return (g.d2 != nullptr && sqrt(*g.d2) > g.half_skin) || (g.count != nullptr && *g.count > g.count_limit);
 }
 
-template <int STYLE, bool NEWTON, bool VIR>
+// Velocity-Verlet fused into the full-list force epilogue (mdkk_lj_force_integrate):
+// MODE 1 closes the step (v += h f); MODE 2 also opens the next one and drifts
+// (v += h f; x_next = x + dt v) and takes the next skin-test maximum
+// max |x_next - x_ref|^2 -- the same operations, in the same order, as
+// k_verlet_second + k_verlet_first<false> (or k_verlet_first<true>), so the
+// trajectory is bit-identical.  Positions are double-buffered: the kernel reads x
+// (owned + ghost rows) and writes the owned rows of x_next.
+struct Integ {
+    double* v;
+    const double* x_ref;
+    double* x_next;
+    double* d2_next;
+    double dt;
+    double h;
+};
+
+template <int STYLE, bool NEWTON, bool VIR, int MODE = 0>
 __global__ void __launch_bounds__(kBlock) k_lj(const double* __restrict__ x, int n_local,
                                                const int* __restrict__ table, const int* __restrict__ counts,
                                                int cap, double eps4, double eps24, double sig2, double rc2,
                                                double* __restrict__ f, double* __restrict__ partials,
-                                               int* __restrict__ flags, Gate gate) {
+                                               int* __restrict__ flags, Gate gate, Integ integ = Integ{}) {
+    static_assert(MODE == 0 || STYLE == 0, "integration needs the complete f_i: full lists only");
     if (gated_off(gate)) return;   // block-uniform: the step rebuilds and relaunches
     const int i = blockIdx.x * kBlock + threadIdx.x;
     double acc[7] = {0, 0, 0, 0, 0, 0, 0};  // E, Wxx, Wyy, Wzz, Wxy, Wxz, Wyz
+    double d2n = 0.0;
     if (i < n_local) {
         const double4 xi = mdkk::ld4(x, i);
         const int n = min(counts[i], cap);
@@ -104,6 +122,27 @@ __global__ void __launch_bounds__(kBlock) k_lj(const double* __restrict__ x, int
             if (k + b < n) pair(jn[b], mdkk::ld4(x, jn[b]));
         if (STYLE == 0) {
             mdkk::st4(f, i, make_double4(fx, fy, fz, 0.0));
+            if (MODE > 0) {
+                const double h = integ.h, dt = integ.dt;
+                double4 vi = mdkk::ld4_nc(integ.v, i);
+                vi.x += h * fx;   // closing half-kick of this step
+                vi.y += h * fy;
+                vi.z += h * fz;
+                if (MODE == 2) {
+                    vi.x += h * fx;   // opening half-kick of the next step
+                    vi.y += h * fy;
+                    vi.z += h * fz;
+                    double4 xn = xi;
+                    xn.x += dt * vi.x;
+                    xn.y += dt * vi.y;
+                    xn.z += dt * vi.z;
+                    xn.w = 0.0;
+                    mdkk::st4(integ.x_next, i, xn);
+                    const double4 r = mdkk::ld4_nc(integ.x_ref, i);
+                    d2n = mdkk::r2_exact(xn.x - r.x, xn.y - r.y, xn.z - r.z);
+                }
+                mdkk::st4(integ.v, i, vi);
+            }
         } else {
             double* fi = f + 4LL * i;
             atomicAdd(fi + 0, fx);
@@ -111,6 +150,10 @@ __global__ void __launch_bounds__(kBlock) k_lj(const double* __restrict__ x, int
             atomicAdd(fi + 2, fz);
         }
         if (bad) atomicOr(flags, MDKK_FLAG_COINCIDENT);
+    }
+    if (MODE == 2) {
+        d2n = mdkk::warp_max(d2n);
+        if ((threadIdx.x & 31) == 0) mdkk::atomic_max_nonneg(integ.d2_next, d2n);
     }
     if (VIR) {
         mdkk::block_sum<7, kBlock>(acc, partials + 7LL * blockIdx.x);
@@ -283,6 +326,41 @@ extern "C" int mdkk_lj_force(mdkk_ctx* ctx, const double* x, int n_local, const 
                              double* f, double* ev, int* flags, void* stream) {
     return lj_launch(ctx, x, n_local, table, counts, cap, style, newton, virial, epsilon, sigma, rc, f, ev, flags,
                      Gate{nullptr, 0.0, nullptr, 0}, mdkk::as_stream(stream));
+}
+
+extern "C" int mdkk_lj_force_integrate(mdkk_ctx* ctx, const double* x, int n_local, const int* table,
+                                       const int* counts, int cap, int virial, double epsilon, double sigma, double rc,
+                                       double* f, double* ev, int* flags, const double* maxdisp2, double half_skin,
+                                       const int* max_count, int count_limit, int mode, double* v,
+                                       const double* x_ref, double* x_next, double* d2_next, double dt, double h,
+                                       void* stream) {
+    if (!ctx || n_local < 0 || cap < 1 || mode < 1 || mode > 2 || !v) return MDKK_E_ARG;
+    if (mode == 2 && (!x_ref || !x_next || !d2_next || x_next == x)) return MDKK_E_ARG;
+    cudaStream_t s = mdkk::as_stream(stream);
+    if (n_local == 0) {
+        cudaMemsetAsync(ev, 0, 7 * sizeof(double), s);
+        return MDKK_OK;
+    }
+    const int nb = mdkk::grid_for(n_local, kBlock);
+    double* partials = static_cast<double*>(mdkk::scratch(ctx, sizeof(double) * 7 * (size_t)nb));
+    if (!partials) return mdkk::cuda_fail(cudaErrorMemoryAllocation, "scratch");
+    const double e4 = 4.0 * epsilon, e24 = 24.0 * epsilon, s2 = sigma * sigma, rc2 = rc * rc;
+    const Gate gate{maxdisp2, half_skin, max_count, count_limit};
+    const Integ integ{v, x_ref, x_next, d2_next, dt, h};
+#define MDKK_LJI(VR, MD)                                                                                        \
+    k_lj<0, false, VR, MD><<<nb, kBlock, 0, s>>>(x, n_local, table, counts, cap, e4, e24, s2, rc2, f, partials,  \
+                                                 flags, gate, integ)
+    if (mode == 1) {
+        if (virial) MDKK_LJI(true, 1); else MDKK_LJI(false, 1);
+    } else {
+        if (virial) MDKK_LJI(true, 2); else MDKK_LJI(false, 2);
+    }
+#undef MDKK_LJI
+    MDKK_CHECK_LAUNCH("k_lj (integrate)");
+    if (!virial) cudaMemsetAsync(ev, 0, 7 * sizeof(double), s);
+    mdkk::reduce_partials(partials, nb, virial ? 7 : 1, ev, s);
+    MDKK_CHECK_LAUNCH("k_reduce_partials");
+    return MDKK_OK;
 }
 
 extern "C" int mdkk_lj_force_gated(mdkk_ctx* ctx, const double* x, int n_local, const int* table,

@@ -78,7 +78,7 @@ class LJStyle:
             raise RunError("pair_coeff must be set before computing forces")
         return compute_pair(self.kernel, system, lists, mode=config.mode or self.default_mode, check=check)
 
-    def compute_device(self, system, lists, config, gate=None, gate_limit: float = 0.0
+    def compute_device(self, system, lists, config, gate=None, gate_limit: float = 0.0, integ=None
                        ) -> tuple[torch.Tensor, torch.Tensor]:
         """Engine path: no host sync; returns (device energy scalar, device flag word).
         With `gate` the launch is speculative (a no-op when sqrt(gate) > gate_limit)."""
@@ -96,12 +96,12 @@ class LJStyle:
         half = False
         for k, (s, nl) in enumerate(zip(system.stores, lists)):
             lj_force_rank(s, nl, self.kernel.params, evs[k], flags, virial=False,
-                          mode=config.mode or self.default_mode, gate=gate, gate_limit=gate_limit)
+                          mode=config.mode or self.default_mode, gate=gate, gate_limit=gate_limit, integ=integ)
             half |= nl.style == "half"
         if half:   # collective in the distributed system: every rank calls it
             system.reverse_comm()
         for s in system.stores:
-            s.device_wrote(force=True)
+            s.device_wrote(force=True, vel=integ is not None)
         return (evs[:, 0].sum() if len(system.stores) > 1 else evs[0, 0]), flags
 
 
@@ -370,9 +370,9 @@ class Simulation:
         self._cap_hint = max(nl.alloc_cap for nl in self.lists)
         return ok
 
-    def _forces_device(self, gate=None, gate_limit: float = 0.0):
-        if gate is not None:
-            e, flags = self.style.compute_device(self.system, self.lists, self.config, gate, gate_limit)
+    def _forces_device(self, gate=None, gate_limit: float = 0.0, integ=None):
+        if gate is not None or integ is not None:
+            e, flags = self.style.compute_device(self.system, self.lists, self.config, gate, gate_limit, integ)
         else:
             e, flags = self.style.compute_device(self.system, self.lists, self.config)
         self._e_dev, self._flags = e, flags
@@ -508,6 +508,8 @@ class Simulation:
         was = gc.isenabled()
         gc.disable()
         try:
+            if n_steps >= 2 and self._fusable():
+                return self._advance_fused(n_steps)
             e = None
             for _ in range(n_steps):
                 e = self.step_device(defer_kick=True)
@@ -516,6 +518,97 @@ class Simulation:
         finally:
             if was:
                 gc.enable()
+
+    def _fusable(self) -> bool:
+        """The integration fuses into the force kernel for full-list LJ (atom mode) on one
+        in-process rank: the epilogue needs each owned atom's complete force."""
+        return (isinstance(self.style, LJStyle) and getattr(self.style, "supports_gate", False)
+                and self._list_style == "full" and (self.config.mode or self.style.default_mode) == "atom"
+                and not self.config.distributed and len(self.system.stores) == 1)
+
+    def _advance_fused(self, n_steps: int) -> torch.Tensor:
+        """`advance` with velocity-Verlet fused into the force epilogue.
+
+        Step s's force kernel also closes step s and opens + drifts step s+1 into a
+        second position buffer, taking the next skin-test maximum; the last step
+        only closes.  The pipeline keeps the speculative shape of `step_device`:
+        the pack and the force launch for step s are queued, gated on step s's
+        device-side maximum, before the host has read it; a rebuilding step
+        relaunches after the rebuild.  Positions swap buffers after every drift.
+        Bit-identical to the unfused loop (tests/test_pipeline_gpu.py).
+        """
+        lib, stream = _lib.lib(), _lib.stream(self.device)
+        ctx = _lib.ctx(self.device)
+        s = self.system.stores[0]
+        h = 0.5 * self.dt / self.mass
+        half = 0.5 * self.config.skin
+        main = torch.cuda.current_stream(self.device)
+        if getattr(self, "_fz", None) is None:
+            self._fz = dict(d2=torch.zeros(2, dtype=torch.float64, device=self.device),
+                            pin=torch.zeros(2, dtype=torch.float64, pin_memory=True),
+                            ready=[torch.cuda.Event(), torch.cuda.Event()], kicked=torch.cuda.Event(),
+                            side=torch.cuda.Stream(self.device), x_alt=None)
+        fz = self._fz
+        d2 = fz["d2"]
+
+        def read_back(k):   # d2[k] -> pin[k] on the side stream, behind the work queued so far
+            fz["kicked"].record(main)
+            fz["side"].wait_event(fz["kicked"])
+            with torch.cuda.stream(fz["side"]):
+                fz["pin"][k:k + 1].copy_(d2[k:k + 1], non_blocking=True)
+            fz["ready"][k].record(fz["side"])
+
+        def x_alt():        # the drift target: same capacity, never aliasing a live buffer
+            a = fz["x_alt"]
+            live = {s.x.data_ptr()} | ({s._alt[0].data_ptr()} if s._alt is not None else set())
+            if a is None or a.shape[0] != s.x.shape[0] or a.data_ptr() in live:
+                a = fz["x_alt"] = torch.empty_like(s.x)
+            return a
+
+        # opening of step 1: the classic pass (with any deferred closing kick)
+        s.to_device()
+        _lib.check(lib.mdkk_verlet_first(ctx, s.x.data_ptr(), s.v.data_ptr(), s.f.data_ptr(),
+                                         self.lists[0].ref_dev.data_ptr(), s.n_local, self.dt, h, d2.data_ptr(),
+                                         int(self._kick_pending), stream), "mdkk_verlet_first")
+        self._kick_pending = False
+        s.device_wrote(pos=True, vel=True)
+        cur = 0
+        read_back(cur)
+        e = None
+        for step in range(1, n_steps + 1):
+            mode = 2 if step < n_steps else 1
+            nxt = 1 - cur
+            xa = x_alt() if mode == 2 else None
+
+            def launch(gated):
+                if mode == 2:
+                    d2[nxt:nxt + 1].zero_()
+                integ = dict(mode=mode, x_next=xa, d2_next=d2[nxt:nxt + 1], dt=self.dt, h=h)
+                return self._forces_device(gate=d2[cur:cur + 1] if gated else None, gate_limit=half, integ=integ)
+
+            self.system.forward_comm()                 # speculative halo refresh
+            e = launch(True)                           # speculative force + integration
+            if mode == 2:
+                read_back(nxt)
+            fz["ready"][cur].synchronize()
+            if math.sqrt(float(fz["pin"][cur])) > half:
+                defer = self._cap_hint is not None
+                self._rebuild_lists(defer=defer)
+                xa = x_alt() if mode == 2 else None     # the rebuild may have rotated buffers
+                e = launch(False)
+                if defer and not self._settle_lists():
+                    e = launch(False)
+                if mode == 2:
+                    read_back(nxt)                     # the relaunch rewrote the maximum
+            if mode == 2:
+                fz["x_alt"] = s.x                      # swap: x(s+1) becomes current
+                s.x = xa
+                s._views()
+                s.device_wrote(pos=True, vel=True, force=True)
+                cur = nxt
+            else:
+                s.device_wrote(vel=True, force=True)
+        return e
 
     def _check_finite(self, step, e_pot):
         if not np.isfinite(e_pot):

@@ -91,7 +91,7 @@ class PairResult:
 
 def lj_force_rank(store, nl: NeighborList, params: PairParams, ev: torch.Tensor, flags: torch.Tensor,
                   zero: bool = True, virial: bool = True, mode: str = "atom", gate: torch.Tensor | None = None,
-                  gate_limit: float = 0.0) -> None:
+                  gate_limit: float = 0.0, integ: dict | None = None) -> None:
     """One rank's kernel launch (no host sync).
 
     Ghost force rows are zero outside a force evaluation (migrate zeroes all
@@ -107,6 +107,17 @@ def lj_force_rank(store, nl: NeighborList, params: PairParams, ev: torch.Tensor,
     # mode "atom": one thread per owned atom; "neighbor": a team of lanes per atom
     # splitting its list (mdkk/pair_lj.py:118-143)
     pend = nl._pending
+    if integ is not None:
+        # full list + velocity-Verlet epilogue (engine advance loop; mdkk_lj_force_integrate)
+        _lib.check(_lib.lib().mdkk_lj_force_integrate(
+            _lib.ctx(dev), store.x.data_ptr(), store.n_local, nl.table_dev.data_ptr(), nl.counts_dev.data_ptr(),
+            nl.alloc_cap, int(virial), params.epsilon, params.sigma, params.r_c, store.f.data_ptr(), ev.data_ptr(),
+            flags.data_ptr(), gate.data_ptr() if gate is not None else None, gate_limit,
+            pend[0].data_ptr() if pend is not None else None, nl.alloc_cap, integ["mode"], store.v.data_ptr(),
+            nl.ref_dev.data_ptr(), integ["x_next"].data_ptr() if integ["mode"] == 2 else None,
+            integ["d2_next"].data_ptr() if integ["mode"] == 2 else None, integ["dt"], integ["h"],
+            _lib.stream(dev)), "mdkk_lj_force_integrate")
+        return
     if gate is not None or pend is not None:
         # speculative launch: skipped on the device if the step rebuilds (gate) or the
         # deferred build overflowed its table (count gate; see NeighborList.settle)
