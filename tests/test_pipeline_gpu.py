@@ -89,3 +89,20 @@ def test_deferred_build_overflow_regrows_and_relaunches(gpu):
         assert np.array_equal(sim.system.gather_forces(), f_ref)
         assert sim.lists[0].max_neighbors == cap_ref          # the reference growth sequence
         assert sim.lists[0].alloc_cap >= sim.lists[0].max_count
+
+
+def test_fused_loop_overflow_relaunch_matches_synchronous(gpu):
+    """The fused advance loop's regrow-and-relaunch branch (a rebuild whose table outgrows
+    the capacity hint) keeps the trajectory bit-identical to the synchronous loop."""
+    a, b = _sim("full"), _sim("full")
+    b.style.supports_gate = False
+    a.run_nve(0)
+    b.run_nve(0)
+    for sim in (a, b):
+        sim._cap_hint = 8            # the next deferred rebuild overflows and regrows
+    assert a._fusable() and not b._fusable()
+    ra, rb = a.run_nve(40), b.run_nve(40)
+    assert ra.n_rebuilds == rb.n_rebuilds and ra.n_rebuilds >= 2
+    assert ra.lines == rb.lines
+    assert np.array_equal(a.system.gather_positions(), b.system.gather_positions())
+    assert np.array_equal(a.system.gather()[1], b.system.gather()[1])     # velocities
