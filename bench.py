@@ -158,8 +158,9 @@ def lj_run(style, cells, steps, warmup, device, profile=True, distributed=False)
     sim.execute(lj_script(cells))
     sim._ensure_system()
     sim._forces_device()
-    for _ in range(warmup):
-        sim.step_device()
+    # warm-up through the same loop as the timed region (its buffers, pinned read-back
+    # slots and side stream are created here, not inside the timing)
+    sim.advance(max(warmup, 2))
     torch.cuda.synchronize()
     rebuild0, l0 = sim.n_rebuilds, _lib.launch_count()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
