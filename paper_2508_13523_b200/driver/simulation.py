@@ -520,11 +520,12 @@ class Simulation:
                 gc.enable()
 
     def _fusable(self) -> bool:
-        """The integration fuses into the force kernel for full-list LJ (atom mode) on one
-        in-process rank: the epilogue needs each owned atom's complete force."""
+        """The integration fuses into the force kernel for full-list LJ (atom mode) with one
+        store per process (one in-process rank, or one rank per GPU): the epilogue needs
+        each owned atom's complete force."""
         return (isinstance(self.style, LJStyle) and getattr(self.style, "supports_gate", False)
                 and self._list_style == "full" and (self.config.mode or self.style.default_mode) == "atom"
-                and not self.config.distributed and len(self.system.stores) == 1)
+                and len(self.system.stores) == 1)
 
     def _advance_fused(self, n_steps: int) -> torch.Tensor:
         """`advance` with velocity-Verlet fused into the force epilogue.
@@ -565,11 +566,18 @@ class Simulation:
                 a = fz["x_alt"] = torch.empty_like(s.x)
             return a
 
+        dist_ = self.config.distributed
+
+        def global_max(k):   # one rank per GPU: every rank gates and decides on the same maximum
+            if dist_:
+                self.system.allreduce_max(d2[k:k + 1])
+
         # opening of step 1: the classic pass (with any deferred closing kick)
         s.to_device()
         _lib.check(lib.mdkk_verlet_first(ctx, s.x.data_ptr(), s.v.data_ptr(), s.f.data_ptr(),
                                          self.lists[0].ref_dev.data_ptr(), s.n_local, self.dt, h, d2.data_ptr(),
                                          int(self._kick_pending), stream), "mdkk_verlet_first")
+        global_max(0)
         self._kick_pending = False
         s.device_wrote(pos=True, vel=True)
         cur = 0
@@ -589,16 +597,19 @@ class Simulation:
             self.system.forward_comm()                 # speculative halo refresh
             e = launch(True)                           # speculative force + integration
             if mode == 2:
+                global_max(nxt)
                 read_back(nxt)
             fz["ready"][cur].synchronize()
             if math.sqrt(float(fz["pin"][cur])) > half:
                 defer = self._cap_hint is not None
                 self._rebuild_lists(defer=defer)
+                s = self.system.stores[0]               # a distributed migrate makes a new store
                 xa = x_alt() if mode == 2 else None     # the rebuild may have rotated buffers
                 e = launch(False)
                 if defer and not self._settle_lists():
                     e = launch(False)
                 if mode == 2:
+                    global_max(nxt)
                     read_back(nxt)                     # the relaunch rewrote the maximum
             if mode == 2:
                 fz["x_alt"] = s.x                      # swap: x(s+1) becomes current
