@@ -139,6 +139,10 @@ int mdkk_nbr_build(mdkk_ctx* ctx, const double* x, int n_local, int n_total,
 int mdkk_nbr_canonicalize(const double* x, const int64_t* gid, int n_local, int cap,
                           int* table, const int* counts, void* stream);
 /* max_i |x_i - x_ref_i|^2 into *out (device double) — mdkk/neighbor.py:66-74. */
+/* Sort every row of a cluster-blocked table by the partner displacement (dz, dy, dx)
+ * = x_j - x_i (the reference's NeighborMap order, mdkk/snap/compute.py:66-104), making
+ * per-row accumulation orders label-independent.  In place. */
+int mdkk_nbr_geo_order(const double* x, int n_local, int cap, int* table, const int* counts, void* stream);
 int mdkk_max_disp2(const double* x, const double* x_ref, int n, double* out, void* stream);
 
 /* --------------------------------------------------------------------- LJ

@@ -370,6 +370,36 @@ __global__ void k_canonicalize(const double* __restrict__ x, const int64_t* __re
     }
 }
 
+// Geometric row order for the cluster-blocked table: each row's entries sorted by the
+// partner's displacement (dz, dy, dx) = x_j - x_i, the reference's NeighborMap order
+// (mdkk/snap/compute.py:66-104: lexsort (row, dz, dy, dx)), so order-dependent sums
+// over a row (compute_ui's U accumulation) do not depend on atom labels.
+__global__ void k_geo_order(const double* __restrict__ x, int n_local, int cap, int* __restrict__ table,
+                            const int* __restrict__ counts) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_local) return;
+    const int n = min(counts[i], cap);
+    int* row = table + ((long long)(i >> 5) * cap) * 32 + (i & 31);
+    const double4 xi = mdkk::ld4(x, i);
+    auto less = [&](int a, int b) {
+        const double4 pa = mdkk::ld4(x, a), pb = mdkk::ld4(x, b);
+        const double az = pa.z - xi.z, bz = pb.z - xi.z;
+        if (az != bz) return az < bz;
+        const double ay = pa.y - xi.y, by = pb.y - xi.y;
+        if (ay != by) return ay < by;
+        return (pa.x - xi.x) < (pb.x - xi.x);
+    };
+    for (int k = 1; k < n; ++k) {
+        const int v = row[(long long)k * 32];
+        int m = k - 1;
+        while (m >= 0 && less(v, row[(long long)m * 32])) {
+            row[(long long)(m + 1) * 32] = row[(long long)m * 32];
+            --m;
+        }
+        row[(long long)(m + 1) * 32] = v;
+    }
+}
+
 __global__ void k_max_disp2(const double* __restrict__ x, const double* __restrict__ xr, int n,
                             double* __restrict__ out) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -527,6 +557,14 @@ int mdkk_nbr_canonicalize(const double* x, const int64_t* gid, int n_local, int 
     k_canonicalize<<<mdkk::grid_for(n_local, 128), 128, 0, mdkk::as_stream(stream)>>>(x, gid, n_local, cap,
                                                                                        table, counts);
     MDKK_CHECK_LAUNCH("k_canonicalize");
+    return MDKK_OK;
+}
+
+int mdkk_nbr_geo_order(const double* x, int n_local, int cap, int* table, const int* counts, void* stream) {
+    if (n_local < 0 || cap < 1) return MDKK_E_ARG;
+    if (n_local == 0) return MDKK_OK;
+    k_geo_order<<<mdkk::grid_for(n_local, 128), 128, 0, mdkk::as_stream(stream)>>>(x, n_local, cap, table, counts);
+    MDKK_CHECK_LAUNCH("k_geo_order");
     return MDKK_OK;
 }
 

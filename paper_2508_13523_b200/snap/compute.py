@@ -98,6 +98,15 @@ def build_neighbor_map(store, nlist, r_c: float) -> NeighborMap:
         raise SnapError("descriptor pipeline requires a full-style neighbor list")
     if r_c > nlist.build_cutoff:
         raise SnapError(f"cutoff {r_c} exceeds neighbor build cutoff {nlist.build_cutoff}")
+    if not getattr(nlist, "_geo_order", False):
+        # the reference's pair order (row, dz, dy, dx) on the device table, once per list:
+        # the U accumulation order then follows geometry, not atom labels
+        # (mdkk tests/test_snap.py:502-520)
+        store.to_device()
+        _lib.check(_lib.lib().mdkk_nbr_geo_order(store.x.data_ptr(), store.n_local, nlist.alloc_cap,
+                                                 nlist.table_dev.data_ptr(), nlist.counts_dev.data_ptr(),
+                                                 _lib.stream(store.device)), "mdkk_nbr_geo_order")
+        nlist._geo_order = True
     return NeighborMap(store, nlist, r_c)
 
 
