@@ -14,6 +14,10 @@ import difflib
 COMMANDS = {"units": 1, "boundary": 3, "lattice": 2, "create_box": 3, "create_atoms": 0, "mass": 1,
             "velocity": 2, "pair_style": None, "pair_coeff": 2, "suffix": 1, "timestep": 1, "thermo": 1,
             "run": 1, "qeq": None}
+# per-argument kinds: a set = allowed words, "f" = number, "i" = integer, None = free word
+_ARGS = {"units": [{"lj"}], "boundary": [{"p"}] * 3, "lattice": [{"fcc", "sc", "bcc"}, "f"],
+         "create_box": ["i", "i", "i"], "mass": ["f"], "velocity": ["f", "i"], "pair_coeff": ["f", "f"],
+         "timestep": ["f"], "thermo": ["i"], "run": ["i"], "suffix": [None]}
 
 
 class ParseError(ValueError):
@@ -56,8 +60,18 @@ def _command(tokens, line_no):
     n = COMMANDS[name]
     if n is not None and len(args) != n:
         raise ParseError(line_no, f"{name} expects {n} argument(s), got {len(args)}")
-    if name == "pair_style" and not args:
-        raise ParseError(line_no, "pair_style expects a style name")
+    for kind, tok in zip(_ARGS.get(name, ()), args):
+        _check_arg(name, kind, tok, line_no)
+    if name == "pair_style":
+        if not args:
+            raise ParseError(line_no, "pair_style expects a style name")
+        base = args[0].split("/")[0]
+        if base == "snap" and len(args) != 3:
+            raise ParseError(line_no, f"pair_style {args[0]} expects: cutoff coeff_file")
+        if base == "lj" and len(args) != 2:
+            raise ParseError(line_no, f"pair_style {args[0]} expects: cutoff")
+        if len(args) > 1:
+            _check_arg(name, "f", args[1], line_no)
     if name == "qeq":   # 'qeq off' | 'qeq on gamma eta chi cutoff' (mdkk/driver/script.py:102-120)
         if not args:
             raise ParseError(line_no, "qeq expects 'on <params>' or 'off'")
@@ -75,3 +89,17 @@ def _command(tokens, line_no):
                 except ValueError:
                     raise ParseError(line_no, f"qeq: {tok!r} is not a number") from None
     return Command(name, args, line_no)
+
+
+def _check_arg(name, kind, tok, line_no):
+    if kind is None:
+        return
+    if isinstance(kind, set):
+        if tok not in kind:
+            raise ParseError(line_no, f"{name}: {tok!r}: expected one of {sorted(kind)}")
+        return
+    try:
+        int(tok) if kind == "i" else float(tok)
+    except ValueError:
+        what = "integer" if kind == "i" else "number"
+        raise ParseError(line_no, f"{name}: malformed {what} {tok!r}") from None

@@ -161,3 +161,98 @@ def test_run_errors(gpu, tmp_path):
         run_script(snap, RunConfig(list_style="half"), log=SILENT)
     with pytest.raises(RunError, match="pair_coeff does not apply"):
         run_script(MINI.replace("pair_style lj/cut 1.5", f"pair_style snap 1.6 {coeff}"), log=SILENT)
+
+
+# ------------------------------------------ more of mdkk tests/test_driver.py
+def test_parse_unknown_command_suggests_near_match():
+    with pytest.raises(ParseError) as exc:
+        parse_script("units lj\npair_stylee lj/cut 1.5\n")
+    assert exc.value.line_no == 2
+    assert "did you mean" in str(exc.value) and "pair_style" in str(exc.value)
+
+
+def test_parse_arity_and_number_validation():
+    with pytest.raises(ParseError, match="expects 2"):
+        parse_script("velocity 0.1\n")
+    with pytest.raises(ParseError, match="malformed number"):
+        parse_script("timestep fast\n")
+    with pytest.raises(ParseError, match="malformed integer"):
+        parse_script("run 1.5\n")
+    with pytest.raises(ParseError, match="expected one of"):
+        parse_script("lattice bct 0.8\n")   # (bcc is accepted here: the SNAP tungsten lattice)
+    with pytest.raises(ParseError, match="expected one of"):
+        parse_script("boundary p p f\n")
+    with pytest.raises(ParseError, match="expected one of"):
+        parse_script("units si\n")
+
+
+def test_parse_onoff_and_pair_style_shapes():
+    assert parse_script("qeq off\n")[0].args == ["off"]
+    with pytest.raises(ParseError, match="off takes no parameters"):
+        parse_script("qeq off 1.0\n")
+    with pytest.raises(ParseError, match="expects 4 parameter"):
+        parse_script("qeq on 0.8 15.0 -0.3\n")
+    assert parse_script("pair_style snap 1.6 w.coeff\n")[0].args[0] == "snap"
+    with pytest.raises(ParseError, match="cutoff coeff_file"):
+        parse_script("pair_style snap 1.6\n")
+    with pytest.raises(ParseError, match="expects: cutoff"):
+        parse_script("pair_style lj/cut 1.5 extra\n")
+    with pytest.raises(ParseError, match="style name"):
+        parse_script("pair_style\n")
+
+
+def test_run_command_ordering_errors():
+    """Raised before any device work (mdkk tests/test_driver.py:326-338)."""
+    CPU = RunConfig(device="cpu")
+    with pytest.raises(RunError, match="lattice must be set"):
+        run_script("units lj\ncreate_box 2 2 2\n", CPU, log=SILENT)
+    with pytest.raises(RunError, match="create_atoms must run"):
+        run_script("velocity 0.1 1\n", CPU, log=SILENT)
+    with pytest.raises(RunError, match="pair_style must be set"):
+        run_script("pair_coeff 1.0 1.0\n", CPU, log=SILENT)
+    with pytest.raises(RunError, match="timestep must be positive"):
+        run_script("timestep -0.1\n", CPU, log=SILENT)
+    with pytest.raises(RegistryError, match="unknown style"):
+        run_script("pair_style bogus 1.0\n", CPU, log=SILENT)
+
+
+def _coeff(tmp_path):
+    from paper_2508_13523_b200.snap import QuantumIndex
+    p = tmp_path / "snap_jmax1.coeff"
+    p.write_text("1\n" + "\n".join(["0.1"] * len(QuantumIndex(1).triples())) + "\n")
+    return str(p)
+
+
+@pytest.mark.gpu
+def test_more_run_errors_and_list_style_conflict(gpu, tmp_path):
+    coeff = _coeff(tmp_path)
+    with pytest.raises(RunError, match="pair_style must be set"):
+        run_script(MINI.replace("pair_style lj/cut 1.5\n", "").replace("pair_coeff 1.0 1.0\n", ""), log=SILENT)
+    with pytest.raises(RunError, match="pair_coeff does not apply"):
+        run_script(MINI.replace("pair_style lj/cut 1.5", f"pair_style snap 1.6 {coeff}"), log=SILENT)
+    with pytest.raises(RunError, match="requires full lists"):
+        run_script(MINI.replace("pair_style lj/cut 1.5\npair_coeff 1.0 1.0", f"pair_style snap 1.6 {coeff}"),
+                   RunConfig(list_style="half"), log=SILENT)
+
+
+@pytest.mark.gpu
+def test_strategy_and_mode_agree_through_driver(gpu):
+    base = run_script(MINI, RunConfig(), log=SILENT).results[-1]
+    for config in (RunConfig(strategy="duplicate", mode="neighbor", workers=3),
+                   RunConfig(strategy="atomic", mode="neighbor", workers=2),
+                   RunConfig(list_style="full", newton=False)):
+        other = run_script(MINI, config, log=SILENT).results[-1]
+        for (s0, *r0), (s1, *r1) in zip(base.rows, other.rows):
+            assert s0 == s1 and np.allclose(r0, r1, rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.gpu
+def test_snap_script_runs_with_suffix(gpu, tmp_path):
+    """A SNAP input through the driver, `suffix kk` resolving snap/kk (mdkk tests/test_driver.py:302-310)."""
+    coeff = _coeff(tmp_path)
+    text = (f"units lj\nboundary p p p\nlattice fcc 0.8\ncreate_box 3 3 3\ncreate_atoms\nmass 1.0\n"
+            f"velocity 0.05 7\nsuffix kk\npair_style snap 1.6 {coeff}\ntimestep 0.002\nthermo 5\nrun 10\n")
+    sim = run_script(text, log=SILENT)
+    assert sim.style.name == "snap/kk"
+    rows = np.array(sim.results[-1].rows)
+    assert rows.shape[0] == 3 and np.isfinite(rows).all()
