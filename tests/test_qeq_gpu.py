@@ -108,3 +108,26 @@ def test_qeq_thermo_diagnostic(gpu):
     assert [r[0] for r in log] == [0, 10, 20]
     for step, its, itt, sq, e in log:
         assert its >= 0 and itt > 0 and abs(sq) < 1e-10 and np.isfinite(e)
+
+
+def test_energy_stationary_net_charge_target_and_order(gpu):
+    """mdkk tests/test_qeq.py:147-184: constrained minimum (perturbations preserving the
+    net charge do not lower the energy), a nonzero net-charge target, energy before solve."""
+    from paper_2508_13523_b200.qeq import QeqError, QeqSystem, qeq_energy, solve_qeq
+    g = golden("qeq.npz")
+    H, _, gid = _setup(g["b_pos"], g["b_L"])
+    Hd = g["b_H"][np.ix_(gid, gid)]
+    chi = np.full(H.n_rows, CHI)
+    with pytest.raises(QeqError):
+        qeq_energy(QeqSystem(H, chi))
+    qs = QeqSystem(H, chi, tol=1e-10)
+    q = solve_qeq(qs)
+    e = qeq_energy(qs)
+    rng = np.random.default_rng(1)
+    for _ in range(5):
+        d = rng.normal(size=H.n_rows)
+        d -= d.mean()
+        d *= 1e-4 / np.linalg.norm(d)
+        assert chi @ (q + d) + 0.5 * (q + d) @ (Hd @ (q + d)) >= e - 1e-9
+    q5 = solve_qeq(QeqSystem(H, chi, net_charge=0.5, tol=1e-10))
+    assert q5.sum() == pytest.approx(0.5, abs=1e-10)
