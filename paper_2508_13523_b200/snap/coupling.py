@@ -45,6 +45,14 @@ class QuantumIndex:
             raise SnapIndexError(f"(p, q) = ({p}, {q}) out of block range for tj {tj}")
         return int(self.block_offset[tj] + p * (tj + 1) + q)
 
+    def unflatten(self, idx: int) -> tuple[int, int, int]:
+        """Inverse of flat (mdkk/snap/indexing.py:42-50)."""
+        if not (0 <= idx < self.n_flat):
+            raise SnapIndexError(f"flat index {idx} out of range [0, {self.n_flat})")
+        tj = int(np.searchsorted(self.block_offset, idx, side="right")) - 1
+        p, q = divmod(int(idx - self.block_offset[tj]), tj + 1)
+        return tj, p, q
+
     def block(self, tj: int) -> slice:
         return slice(int(self.block_offset[tj]), int(self.block_offset[tj + 1]))
 

@@ -4,7 +4,8 @@ Mirrors mdkk tests/test_snap.py case by case (same inputs, assertions and
 tolerances): pair levels unitary (:247-258), level 1 the seed matrix
 (:261-269), forces vs central finite differences of the energy (:436-454),
 periodic force balance (:457-462), atom relabelling bit-exact per atom
-(:502-520).  Energies take the descriptor route E = sum beta . B like the
+(:502-520), map validation (:288-307), rotation / translation invariance
+(:398-418), state validation (:523-531).  Energies take the descriptor route E = sum beta . B like the
 reference's helper (mdkk tests/test_snap.py:93-115).
 """
 
@@ -154,3 +155,57 @@ def test_atom_relabeling_is_bit_exact_per_atom(gpu):
     assert np.array_equal(compute_bi(states0[0])[g0], compute_bi(states1[0])[g1])
     assert e1 == pytest.approx(e0, rel=1e-12)
     assert np.allclose(f1, f0, rtol=1e-12, atol=1e-12)
+
+
+def test_neighbor_map_requires_full_list_and_reach(gpu):
+    """mdkk tests/test_snap.py:288-307."""
+    from paper_2508_13523_b200 import Box, RankedSystem, build, build_all
+    from paper_2508_13523_b200.snap import SnapError, build_neighbor_map
+    pos = _cluster(6, 3)
+    box = Box((BOX_L,) * 3)
+    system = RankedSystem.distribute(box, 1, pos, np.zeros_like(pos))
+    system.exchange_ghosts(R_C + 0.2)
+    half = build(system.stores[0], box, R_C, 0.2, style="half", newton=True)
+    with pytest.raises(SnapError):
+        build_neighbor_map(system.stores[0], half, R_C)
+    full = build(system.stores[0], box, R_C, 0.2, style="full", newton=False)
+    with pytest.raises(SnapError):
+        build_neighbor_map(system.stores[0], full, R_C + 1.0)
+    z = RankedSystem.distribute(box, 1, np.full((2, 3), 5.0), np.zeros((2, 3)))
+    (zl,) = build_all(z, R_C, 0.2, style="full", newton=False)
+    with pytest.raises(SnapError):
+        build_neighbor_map(z.stores[0], zl, R_C).n_pairs
+
+
+def test_rotation_and_translation_invariance(gpu):
+    """mdkk tests/test_snap.py:398-418: E and B invariant under rotations (1e-8) and
+    translations (1e-12)."""
+    from paper_2508_13523_b200.snap import compute_bi
+    pos = _cluster(10, 29)
+    beta = _beta_for(2)
+    e0, _, states, sys0 = _pipeline(pos, BOX_L, 2, beta)
+    g0 = np.argsort(sys0.stores[0].global_ids[: sys0.stores[0].n_local])
+    b0 = compute_bi(states[0])[g0]
+    rng = np.random.default_rng(31)
+    center = pos.mean(axis=0)
+    for _ in range(3):
+        q, _ = np.linalg.qr(rng.standard_normal((3, 3)))
+        if np.linalg.det(q) < 0:
+            q[:, 0] = -q[:, 0]
+        e1, _, states1, sys1 = _pipeline((pos - center) @ q.T + center, BOX_L, 2, beta)
+        g1 = np.argsort(sys1.stores[0].global_ids[: sys1.stores[0].n_local])
+        assert e1 == pytest.approx(e0, rel=1e-8)
+        assert np.allclose(compute_bi(states1[0])[g1], b0, rtol=1e-8, atol=1e-10)
+    e2 = _pipeline(pos + np.array([0.4, -0.9, 1.7]), BOX_L, 2, beta)[0]
+    assert e2 == pytest.approx(e0, rel=1e-12)
+
+
+def test_state_validation(gpu):
+    """mdkk tests/test_snap.py:523-531."""
+    from paper_2508_13523_b200.snap import SnapError, SnapState, compute_energy, make_coupling_tables
+    tables = make_coupling_tables(1)
+    with pytest.raises(SnapError):
+        SnapState(tables, 4, np.zeros(3))
+    with pytest.raises(SnapError):
+        SnapState(tables, 4, np.zeros(5), layout="c")
+    assert compute_energy(SnapState(tables, 0, np.zeros(5))) == 0.0
