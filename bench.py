@@ -410,7 +410,7 @@ def main():
                                     else "k_lj<full> (+ partial reduce)"),
                          "achieved": achieved,
                          "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic_from_profiles("k_lj"),
+                         "traffic": traffic_from_profiles("k_lj_fused" if fused else "k_lj"),
                          "bytes_model": (f"n_local*(28*nn+52+128), nn={nn:.2f} measured" if fused
                                          else f"n_local*(28*nn+52), nn={nn:.2f} measured")},
             "snap": (None if snapr is None else {
