@@ -412,7 +412,10 @@ def main():
                          "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic_from_profiles("k_lj_fused" if fused else "k_lj"),
                          "bytes_model": (f"n_local*(28*nn+52+128), nn={nn:.2f} measured" if fused
-                                         else f"n_local*(28*nn+52), nn={nn:.2f} measured")},
+                                         else f"n_local*(28*nn+52), nn={nn:.2f} measured"),
+                         "note": ("pair-stream model (SURVEY 8(d)): x_j reuse in L1/L2 lets it exceed the HBM "
+                                  "peak; actual DRAM per launch is `traffic`; the kernel's limiter is the L1TEX "
+                                  "data pipe (92-93 % wavefronts, profiles/r1h_klj_ncu_full_summary.txt)")},
             "snap": (None if snapr is None else {
                 "workload": f"SNAP W bcc a=3.1803, 2J=8, rc=4.73, skin 0.3, T=0.01, dt=0.001, "
                             f"{snapr['n_atoms']} atoms (configs[4] at N=1)",
