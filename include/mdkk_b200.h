@@ -127,7 +127,9 @@ int mdkk_bin_atoms(mdkk_ctx* ctx, const double* x, int n, const double* grid_hos
  * both sides (newton off).  table is the cluster-blocked int32 layout above
  * (ceil(n_local/32)*cap*32 ints), entries beyond counts[i] undefined; counts[i] is the true count even when
  * > cap and *max_count (device int, caller-zeroed) the max, so the caller
- * grows cap x1.5 and relaunches — never truncates (mdkk/neighbor.py:199-205). */
+ * grows cap x1.5 and relaunches — never truncates (mdkk/neighbor.py:199-205);
+ * after an overflow the table's contents are undefined.  ctx's scratch holds a
+ * cell-ordered FP32 copy of the positions for the (superset) union test. */
 int mdkk_nbr_build(mdkk_ctx* ctx, const double* x, int n_local, int n_total,
                    const double* grid_host, const int* ncell_host, const int* cell_start,
                    const int* cell_atoms, const int64_t* gid, const int32_t* owner_rank, int my_rank,
