@@ -116,6 +116,15 @@ int mdkk_bucket_sort(mdkk_ctx* ctx, const int* keys, int n, int nbuckets, int* b
 int mdkk_bin_atoms(mdkk_ctx* ctx, const double* x, int n, const double* grid_host, const int* ncell_host,
                    int* keys, int* cell_start, int* cell_atoms, void* stream);
 
+/* Cell lists for a build whose owned rows [0, n_local) are already sorted by cell on
+ * this grid with bucket starts owned_start[ncell + 1] (the engine's spatial sort):
+ * bins only the ghost rows [n_local, n_total) and merges, giving exactly
+ * mdkk_bin_atoms over all rows (owned then ghost rows per cell, each ascending).
+ * keys: int[n_total - n_local] scratch; cell_start int[ncell + 1]; cell_atoms
+ * int[n_total]. */
+int mdkk_bin_merge(mdkk_ctx* ctx, const double* x, int n_local, int n_total, const double* grid_host,
+                   const int* ncell_host, const int* owned_start, int* keys, int* cell_start, int* cell_atoms,
+                   void* stream);
 /* -------------------------------------------------------------- neighbour
  * Cluster-scan neighbour build (replaces mdkk/neighbor.py:83-219 +
  * _apply_style :134-179).  Owned rows should be cell-sorted (any order is

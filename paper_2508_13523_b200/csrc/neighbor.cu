@@ -74,6 +74,40 @@ __global__ void k_cell_positions(const double* __restrict__ x, const int* __rest
     xs[s] = make_float4((float)p.x, (float)p.y, (float)p.z, 0.f);
 }
 
+// Binning merge (engine rebuilds): the owned rows are already sorted by cell on this
+// grid (the spatial sort, bucket starts owned_start), the ghost rows binned on their
+// own (ghost_start, ghost_order over rows n_local..n_total): the combined cell lists
+// are owned rows then ghost rows per cell, both ascending -- exactly mdkk_bin_atoms
+// over all rows, without re-sorting the owned ones.
+__global__ void k_merge_starts(const int* __restrict__ owned_start, const int* __restrict__ ghost_start, int ncell,
+                               int* __restrict__ cell_start) {
+    int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c <= ncell) cell_start[c] = owned_start[c] + ghost_start[c];
+}
+
+__global__ void k_merge_owned(const double* __restrict__ x, int n_local, Grid g, const int* __restrict__ owned_start,
+                              const int* __restrict__ cell_start, int* __restrict__ cell_atoms) {
+    int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n_local) return;
+    const double4 p = mdkk::ld4(x, r);
+    const int3 cc = mdkk::cell_of(g, p.x, p.y, p.z);
+    const int c = mdkk::cell_key(g, cc.x, cc.y, cc.z);
+    cell_atoms[cell_start[c] + (r - owned_start[c])] = r;
+}
+
+__global__ void k_merge_ghosts(const double* __restrict__ x, int n_local, int n_ghost, Grid g,
+                               const int* __restrict__ owned_start, const int* __restrict__ ghost_start,
+                               const int* __restrict__ ghost_order, const int* __restrict__ cell_start,
+                               int* __restrict__ cell_atoms) {
+    int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n_ghost) return;
+    const int row = n_local + ghost_order[k];
+    const double4 p = mdkk::ld4(x, row);
+    const int3 cc = mdkk::cell_of(g, p.x, p.y, p.z);
+    const int c = mdkk::cell_key(g, cc.x, cc.y, cc.z);
+    cell_atoms[cell_start[c] + (owned_start[c + 1] - owned_start[c]) + (k - ghost_start[c])] = row;
+}
+
 __device__ __forceinline__ bool lex_zyx_less(double ax, double ay, double az, double bx, double by, double bz) {
     // mdkk/neighbor.py:163-166: z, then y, then x
     return (az < bz) || (az == bz && (ay < by || (ay == by && ax < bx)));
@@ -557,6 +591,43 @@ int mdkk_nbr_canonicalize(const double* x, const int64_t* gid, int n_local, int 
     k_canonicalize<<<mdkk::grid_for(n_local, 128), 128, 0, mdkk::as_stream(stream)>>>(x, gid, n_local, cap,
                                                                                        table, counts);
     MDKK_CHECK_LAUNCH("k_canonicalize");
+    return MDKK_OK;
+}
+
+int mdkk_bin_merge(mdkk_ctx* ctx, const double* x, int n_local, int n_total, const double* grid_host,
+                   const int* ncell_host, const int* owned_start, int* keys, int* cell_start, int* cell_atoms,
+                   void* stream) {
+    if (!ctx || n_local < 0 || n_total < n_local || !grid_host || !ncell_host || !owned_start) return MDKK_E_ARG;
+    const long long ncl = (long long)ncell_host[0] * ncell_host[1] * ncell_host[2];
+    if (ncl < 1 || ncl >= (1LL << 30)) return MDKK_E_ARG;
+    const int ncell = (int)ncl, n_ghost = n_total - n_local;
+    Grid g = mdkk::make_grid(grid_host, ncell_host);
+    cudaStream_t s = mdkk::as_stream(stream);
+    // ghost bins in ctx scratch after the ghost sort's own use of it: [ghost_start | ghost_order]
+    int* gstart = static_cast<int*>(mdkk::scratch(ctx, sizeof(int) * ((size_t)ncell + 2 + (size_t)n_ghost + 64)));
+    if (!gstart) return mdkk::cuda_fail(cudaErrorMemoryAllocation, "scratch");
+    // the ghost rows' own binning writes into caller buffers first (it uses the scratch itself)
+    int* gorder = cell_atoms + n_local;   // free until the merge below fills cell_atoms
+    int st = mdkk_bin_atoms(ctx, x + 4LL * n_local, n_ghost, grid_host, ncell_host, keys, cell_start, gorder,
+                            stream);
+    if (st != MDKK_OK) return st;
+    if (n_ghost == 0) cudaMemsetAsync(cell_start, 0, sizeof(int) * ((size_t)ncell + 1), s);
+    gstart = static_cast<int*>(mdkk::scratch(ctx, sizeof(int) * ((size_t)ncell + 2 + (size_t)n_ghost + 64)));
+    if (!gstart) return mdkk::cuda_fail(cudaErrorMemoryAllocation, "scratch");
+    int* gord = gstart + ncell + 2;
+    cudaMemcpyAsync(gstart, cell_start, sizeof(int) * ((size_t)ncell + 1), cudaMemcpyDeviceToDevice, s);
+    if (n_ghost) cudaMemcpyAsync(gord, gorder, sizeof(int) * (size_t)n_ghost, cudaMemcpyDeviceToDevice, s);
+    k_merge_starts<<<mdkk::grid_for(ncell + 1, 256), 256, 0, s>>>(owned_start, gstart, ncell, cell_start);
+    MDKK_CHECK_LAUNCH("k_merge_starts");
+    if (n_local) {
+        k_merge_owned<<<mdkk::grid_for(n_local, 256), 256, 0, s>>>(x, n_local, g, owned_start, cell_start, cell_atoms);
+        MDKK_CHECK_LAUNCH("k_merge_owned");
+    }
+    if (n_ghost) {
+        k_merge_ghosts<<<mdkk::grid_for(n_ghost, 256), 256, 0, s>>>(x, n_local, n_ghost, g, owned_start, gstart, gord,
+                                                                    cell_start, cell_atoms);
+        MDKK_CHECK_LAUNCH("k_merge_ghosts");
+    }
     return MDKK_OK;
 }
 

@@ -232,6 +232,7 @@ class AtomStore:
         self._lengths = None
         self._lanes_in = []       # lanes whose ghost rows live here (for ghost_shift)
         self._alt = None          # double buffers for the spatial sort
+        self._bins = None         # (width, n_local, bucket starts) of the last spatial sort
         self._views()
         self.device_wrote(pos=True, vel=True)   # the rows were uploaded: HBM holds the current data
 
@@ -634,7 +635,9 @@ class RankedSystem:
             return
         lib, stream = _lib.lib(), _lib.stream(self.device)
         ctx = _lib.ctx(self.device)
-        _, _, garr, narr, ncell = grid_args(s.lo, s.hi, 0.0, width)   # bins tile the brick exactly
+        # the brick's cells plus a shell layer: the owned rows' sort order and bucket starts
+        # are then reused by the neighbour build's binning (mdkk_bin_merge)
+        _, _, garr, narr, ncell = shell_grid_args(s.lo, s.hi, width)
         n = s.n_local
         keys = self._buf(f"sk{s.rank}", n, torch.int32)
         start = self._buf(f"ss{s.rank}", ncell + 1, torch.int32)
@@ -650,6 +653,7 @@ class RankedSystem:
         _lib.check(lib.mdkk_gather_i64(s.gid.data_ptr(), order.data_ptr(), n, g2.data_ptr(), stream), "g64")
         s._alt = (s.x, s.v, s.gid)
         s.x, s.v, s.gid = x2, v2, g2
+        s._bins = (float(width), n, start)   # owned rows sorted on shell_grid_args(lo, hi, width)
 
     # -------------------------------------------------------------- gather
     def _gid_order(self, rows_fn, width):
@@ -711,6 +715,22 @@ def grid_args(lo, hi, halo: float, width: float):
         if len(_GRID_MEMO) > 256:
             _GRID_MEMO.clear()
         g, nc = cell_grid(lo, hi, halo, width)
+        hit = _GRID_MEMO[key] = (g, nc, _lib.dbl3(g), _lib.int_arr(nc), nc[0] * nc[1] * nc[2])
+    return hit
+
+
+def shell_grid_args(lo, hi, width: float):
+    """grid_args for the brick's own cells (width >= `width`, tiling [lo, hi) exactly) plus
+    one shell layer on each side, so the same grid bins the owned rows (interior cells)
+    and the ghosts within one cell width of the faces (the shell).  Memoised."""
+    key = ("shell", *(float(v) for v in lo), *(float(v) for v in hi), float(width))
+    hit = _GRID_MEMO.get(key)
+    if hit is None:
+        g, nc = cell_grid(lo, hi, 0.0, width)
+        inv = np.asarray(g[3:], dtype=np.float64)
+        w = 1.0 / inv
+        g = [*(np.asarray(g[:3]) - w).tolist(), *inv.tolist()]
+        nc = [int(v) + 2 for v in nc]
         hit = _GRID_MEMO[key] = (g, nc, _lib.dbl3(g), _lib.int_arr(nc), nc[0] * nc[1] * nc[2])
     return hit
 

@@ -16,7 +16,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .domain import AtomStore, Box, RankedSystem, grid_args
+from .domain import AtomStore, Box, RankedSystem, grid_args, shell_grid_args
 from .memspace import DualArray, LayoutPolicy
 
 DEFAULT_CAPACITY = 16
@@ -86,7 +86,7 @@ class NeighborList:
             self.max_neighbors = grow_capacity(capacity, need)
             return self, True
         nl = build(self.store, box, self.cutoff, self.skin, self.style, self.newton, capacity,
-                   cap_hint=grow_capacity(self.alloc_cap, need), recycle=self)
+                   cap_hint=grow_capacity(self.alloc_cap, need), recycle=self, rebin=False)
         return nl, False
 
     @property
@@ -197,6 +197,7 @@ class _BuildCache:
 
     def __init__(self):
         self.bufs = {}
+        self.last = None   # ((n_total, bc), (grid args)) of the last binning
 
     def get(self, name, n, dtype, device):
         t = self.bufs.get(name)
@@ -210,7 +211,8 @@ _cache: dict = {}
 
 def build(store: AtomStore, box: Box, cutoff: float, skin: float, style: str = "full",
           newton: bool = True, capacity: int = DEFAULT_CAPACITY, cap_hint: int | None = None,
-          recycle: NeighborList | None = None, defer: bool = False, **_unused) -> NeighborList:
+          recycle: NeighborList | None = None, defer: bool = False, rebin: bool = True,
+          **_unused) -> NeighborList:
     """One rank's list from its local + ghost rows (mdkk/neighbor.py:182-219).
 
     Owned rows must be cell-sorted for compact clusters (RankedSystem keeps
@@ -222,6 +224,8 @@ def build(store: AtomStore, box: Box, cutoff: float, skin: float, style: str = "
     `defer` (engine-internal, with `cap_hint`): one launch, no host sync; the
     capacity check waits for `NeighborList.settle()` so that work gated on the
     device-side count (mdkk_lj_force_gated) can be queued first.
+    `rebin=False` (engine-internal, a regrow right after a build of the same rows)
+    reuses that build's cell lists, so the table comes out in the same order.
     """
     if style not in STYLES:
         raise NeighborError(f"unknown list style {style!r}")
@@ -235,13 +239,30 @@ def build(store: AtomStore, box: Box, cutoff: float, skin: float, style: str = "
     n_local, n_total = store.n_local, store.n_total
     lo = store.lo if store.lo is not None else np.zeros(3)
     hi = store.hi if store.hi is not None else box.lengths
-    _, _, garr, narr, ncell = grid_args(lo, hi, bc, bc)
+    bins = getattr(store, "_bins", None)
+    merged = bins is not None and bins[0] == bc and bins[1] == n_local and store.lo is not None
+    store._bins = None   # one-shot: valid only for the build right after the sort (positions move)
     cache = _cache.setdefault((str(dev), store.rank), _BuildCache())
+    if not rebin and getattr(cache, "last", None) is not None and cache.last[0] == (n_total, bc):
+        merged = None                       # the previous build's cell lists, as they are
+        garr, narr, ncell = cache.last[1]
+    elif merged:   # owned rows come sorted from the spatial sort on this grid: bin only the ghosts
+        _, _, garr, narr, ncell = shell_grid_args(lo, hi, bc)
+    else:
+        _, _, garr, narr, ncell = grid_args(lo, hi, bc, bc)
+    cache.last = ((n_total, bc), (garr, narr, ncell))
     keys = cache.get("keys", n_total, torch.int32, dev)
     cstart = cache.get("cstart", ncell + 1, torch.int32, dev)
     catoms = cache.get("catoms", n_total, torch.int32, dev)
-    _lib.check(lib.mdkk_bin_atoms(ctx, store.x.data_ptr(), n_total, garr, narr, keys.data_ptr(),
-                                  cstart.data_ptr(), catoms.data_ptr(), stream), "mdkk_bin_atoms")
+    if merged is None:
+        pass
+    elif merged:
+        _lib.check(lib.mdkk_bin_merge(ctx, store.x.data_ptr(), n_local, n_total, garr, narr, bins[2].data_ptr(),
+                                      keys.data_ptr(), cstart.data_ptr(), catoms.data_ptr(), stream),
+                   "mdkk_bin_merge")
+    else:
+        _lib.check(lib.mdkk_bin_atoms(ctx, store.x.data_ptr(), n_total, garr, narr, keys.data_ptr(),
+                                      cstart.data_ptr(), catoms.data_ptr(), stream), "mdkk_bin_atoms")
     if cap_hint is None and n_local:
         # first build: size the table from the density (mean partners 4/3 pi bc^3 rho,
         # halved for half lists, +25 % for fluctuations) instead of growing by retries
