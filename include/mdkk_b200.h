@@ -74,10 +74,18 @@ int mdkk_wrap(double* x, int n, const double* lengths_host, void* stream);
  * out_code (optional, int8[total]) each selected row also gets its combo's
  * shift code combo_code[c] (device int8[C]). */
 int mdkk_halo_count(mdkk_ctx* ctx, const double* x, int n, const double* combos_dev, int C,
-                    int* block_scratch, int* totals, void* stream);
+                    int* block_scratch, int* totals, const int* rows, const int* n_dev, void* stream);
 int mdkk_halo_fill(mdkk_ctx* ctx, const double* x, int n, const double* combos_dev, int C,
                    const int* block_scratch, const int* totals, int* out_idx, const int8_t* combo_code,
-                   int8_t* out_code, void* stream);
+                   int8_t* out_code, const int* rows, const int* n_dev, void* stream);
+/* rows / n_dev (both optional, for count and fill alike): scan only rows[k], k < *n_dev
+ * (ascending; n then bounds k) instead of every row -- mdkk_boundary_rows' output for a
+ * cell-sorted brick whose cells are at least the halo wide. */
+/* Rows of the cells within `layer` cells of the faces of a (serpentine-keyed) grid,
+ * ascending, for owned rows sorted by cell with bucket starts cell_start[ncell + 1];
+ * *count (device) = their number. */
+int mdkk_boundary_rows(mdkk_ctx* ctx, const int* cell_start, const int* ncell_host, int layer, int* rows,
+                       int* count, void* stream);
 
 /* Forward-comm pack: out[k] = x[idx[k]] + shift_table[code[k]] (shift_table is
  * double[27][3] device, code int8 in 0..26).  `out` may alias ghost rows of x. */

@@ -32,8 +32,9 @@ SIGNATURES = {
     "mdkk_ctx_destroy": [_p],
     "mdkk_fp64_probe": [_i, _i, _p, _p],
     "mdkk_wrap": [_p, _i, _p, _p],
-    "mdkk_halo_count": [_p, _p, _i, _p, _i, _p, _p, _p],
-    "mdkk_halo_fill": [_p, _p, _i, _p, _i, _p, _p, _p, _p, _p, _p],
+    "mdkk_halo_count": [_p, _p, _i, _p, _i, _p, _p, _p, _p, _p],
+    "mdkk_boundary_rows": [_p, _p, _p, _i, _p, _p, _p],
+    "mdkk_halo_fill": [_p, _p, _i, _p, _i, _p, _p, _p, _p, _p, _p, _p, _p],
     "mdkk_ghost_rows": [_p, _p, _p, _p, _p, _i, _p, _p, _p, _p],
     "mdkk_pack_shift": [_p, _p, _p, _p, _i, _p, _p],
     "mdkk_fold_add": [_p, _p, _p, _i, _p],

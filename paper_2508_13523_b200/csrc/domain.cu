@@ -1,6 +1,8 @@
 // Domain kernels: wrap, halo selection (stable multi-way compaction),
 // forward-comm pack with periodic shift, reverse-comm fold, row permutes.
 // Reference: mdkk/domain.py:56-63, :246-334.
+#include <cub/device/device_scan.cuh>
+
 #include "common.cuh"
 
 namespace {
@@ -48,17 +50,31 @@ __device__ __forceinline__ unsigned long long block_or(unsigned long long m, uns
     return *s_or;
 }
 
+// rows / n_dev (optional): scan only rows[k] for k < *n_dev (ascending: the boundary-layer
+// rows of a cell-sorted brick, the only ones a halo no wider than a cell can select);
+// blocks past the device count contribute empty counts.
+__device__ __forceinline__ int halo_row(int k, int n, const int* rows, const int* n_dev, bool& ok) {
+    ok = k < n && (n_dev == nullptr || k < *n_dev);
+    return ok ? (rows ? rows[k] : k) : 0;
+}
+
 __global__ void k_halo_count(const double* __restrict__ x, int n, const double* __restrict__ combos,
-                             int C, int* __restrict__ block_counts) {
+                             int C, int* __restrict__ block_counts, const int* __restrict__ rows,
+                             const int* __restrict__ n_dev) {
     extern __shared__ double sc[];
     __shared__ unsigned long long s_or;
+    if (n_dev && (long long)blockIdx.x * blockDim.x >= *n_dev) {   // block-uniform: nothing to select
+        for (int c = threadIdx.x; c < C; c += blockDim.x) block_counts[(long long)blockIdx.x * C + c] = 0;
+        return;
+    }
     for (int t = threadIdx.x; t < 9 * C; t += blockDim.x) sc[t] = combos[t];
     __syncthreads();
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    bool ok;
+    const int i = halo_row(blockIdx.x * blockDim.x + threadIdx.x, n, rows, n_dev, ok);
     double4 p = make_double4(0, 0, 0, 0);
-    if (i < n) p = mdkk::ld4(x, i);
+    if (ok) p = mdkk::ld4(x, i);
     for (int c0 = 0; c0 < C; c0 += 64) {   // combos in groups of 64 (one mask word)
-        const unsigned long long mine = combo_mask(p, sc, c0, C, i < n);
+        const unsigned long long mine = combo_mask(p, sc, c0, C, ok);
         const unsigned long long any = block_or(mine, &s_or);
         for (int c = c0; c < min(C, c0 + 64); ++c) {
             int cnt = 0;
@@ -112,11 +128,13 @@ __global__ void k_halo_scan(int* __restrict__ block_counts, int nb, int C, int* 
 __global__ void k_halo_fill(const double* __restrict__ x, int n, const double* __restrict__ combos, int C,
                             const int* __restrict__ block_off, const int* __restrict__ totals,
                             int* __restrict__ out, const int8_t* __restrict__ combo_code,
-                            int8_t* __restrict__ out_code) {
+                            int8_t* __restrict__ out_code, const int* __restrict__ rows,
+                            const int* __restrict__ n_dev) {
     extern __shared__ double sc[];
     int* base = reinterpret_cast<int*>(sc + 9 * C);
     __shared__ int warp_cnt[kHaloBlock / 32];
     __shared__ unsigned long long s_or;
+    if (n_dev && (long long)blockIdx.x * blockDim.x >= *n_dev) return;
     for (int t = threadIdx.x; t < 9 * C; t += blockDim.x) sc[t] = combos[t];
     if (threadIdx.x == 0) {
         int s = 0;
@@ -127,11 +145,12 @@ __global__ void k_halo_fill(const double* __restrict__ x, int n, const double* _
     }
     __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    bool ok;
+    const int i = halo_row(blockIdx.x * blockDim.x + threadIdx.x, n, rows, n_dev, ok);
     double4 p = make_double4(0, 0, 0, 0);
-    if (i < n) p = mdkk::ld4(x, i);
+    if (ok) p = mdkk::ld4(x, i);
     for (int c0 = 0; c0 < C; c0 += 64) {   // combos in groups of 64 (one mask word)
-    const unsigned long long mine = combo_mask(p, sc, c0, C, i < n);
+    const unsigned long long mine = combo_mask(p, sc, c0, C, ok);
     unsigned long long any = block_or(mine, &s_or);
     while (any) {   // block-uniform: only the combos some row of this block falls in
         const int cb = __ffsll((long long)any) - 1;
@@ -154,6 +173,36 @@ __global__ void k_halo_fill(const double* __restrict__ x, int n, const double* _
     }
 }
 
+
+// Rows of the cells within `layer` cells of the grid's faces, ascending (cells in key
+// order, each a contiguous ascending row range of a cell-sorted brick).  Keys follow
+// the serpentine order of csrc/cluster.cuh.
+__global__ void k_boundary_counts(const int* __restrict__ cell_start, int nx, int ny, int nz, int layer,
+                                  int* __restrict__ cnt) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    const int ncell = nx * ny * nz;
+    if (c > ncell) return;
+    if (c == ncell) {
+        cnt[c] = 0;
+        return;
+    }
+    const int col = c / nz, czs = c - col * nz;
+    const int cz = (col & 1) ? nz - 1 - czs : czs;
+    const int cx = col / ny, cys = col - cx * ny;
+    const int cy = (cx & 1) ? ny - 1 - cys : cys;
+    const bool edge = cx <= layer || cx >= nx - 1 - layer || cy <= layer || cy >= ny - 1 - layer ||
+                      cz <= layer || cz >= nz - 1 - layer;
+    cnt[c] = edge ? cell_start[c + 1] - cell_start[c] : 0;
+}
+
+__global__ void k_boundary_fill(const int* __restrict__ cell_start, int ncell, const int* __restrict__ cnt,
+                                const int* __restrict__ off, int* __restrict__ rows, int* __restrict__ count) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c == 0) *count = off[ncell];
+    if (c >= ncell || cnt[c] == 0) return;
+    const int r0 = cell_start[c], o = off[c];
+    for (int t = 0; t < cnt[c]; ++t) rows[o + t] = r0 + t;
+}
 
 __global__ void k_pack_shift(const double* __restrict__ x, const int* __restrict__ idx,
                              const int8_t* __restrict__ code, const double* __restrict__ shifts, int n,
@@ -221,13 +270,13 @@ int mdkk_wrap(double* x, int n, const double* L, void* stream) {
 }
 
 int mdkk_halo_count(mdkk_ctx*, const double* x, int n, const double* combos, int C, int* block_scratch,
-                    int* totals, void* stream) {
+                    int* totals, const int* rows, const int* n_dev, void* stream) {
     if (n < 0 || C < 0 || C > kMaxCombos) return MDKK_E_ARG;
     if (C == 0) return MDKK_OK;
     cudaStream_t s = mdkk::as_stream(stream);
     int nb = mdkk::grid_for(n, kHaloBlock);
     size_t sm = sizeof(double) * 9 * C;
-    k_halo_count<<<nb, kHaloBlock, sm, s>>>(x, n, combos, C, block_scratch);
+    k_halo_count<<<nb, kHaloBlock, sm, s>>>(x, n, combos, C, block_scratch, rows, n_dev);
     MDKK_CHECK_LAUNCH("k_halo_count");
     k_halo_scan<<<C, 1024, 0, s>>>(block_scratch, nb, C, totals);
     MDKK_CHECK_LAUNCH("k_halo_scan");
@@ -235,14 +284,38 @@ int mdkk_halo_count(mdkk_ctx*, const double* x, int n, const double* combos, int
 }
 
 int mdkk_halo_fill(mdkk_ctx*, const double* x, int n, const double* combos, int C, const int* block_scratch,
-                   const int* totals, int* out_idx, const int8_t* combo_code, int8_t* out_code, void* stream) {
+                   const int* totals, int* out_idx, const int8_t* combo_code, int8_t* out_code, const int* rows,
+                   const int* n_dev, void* stream) {
     if (n < 0 || C < 0 || C > kMaxCombos || (out_code && !combo_code)) return MDKK_E_ARG;
     if (C == 0 || n == 0) return MDKK_OK;
     int nb = mdkk::grid_for(n, kHaloBlock);
     size_t sm = sizeof(double) * 9 * C + sizeof(int) * C;
     k_halo_fill<<<nb, kHaloBlock, sm, mdkk::as_stream(stream)>>>(x, n, combos, C, block_scratch, totals,
-                                                                  out_idx, combo_code, out_code);
+                                                                  out_idx, combo_code, out_code, rows, n_dev);
     MDKK_CHECK_LAUNCH("k_halo_fill");
+    return MDKK_OK;
+}
+
+int mdkk_boundary_rows(mdkk_ctx* ctx, const int* cell_start, const int* ncell_host, int layer, int* rows,
+                       int* count, void* stream) {
+    if (!ctx || !cell_start || !ncell_host || !rows || !count || layer < 0) return MDKK_E_ARG;
+    const long long ncl = (long long)ncell_host[0] * ncell_host[1] * ncell_host[2];
+    if (ncl < 1 || ncl >= (1LL << 30)) return MDKK_E_ARG;
+    const int ncell = (int)ncl;
+    cudaStream_t s = mdkk::as_stream(stream);
+    size_t scan_bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (int*)nullptr, (int*)nullptr, ncell + 1, s);
+    const size_t off_cnt = 0, off_tmp = ((sizeof(int) * ((size_t)ncell + 2) * 2) + 255) & ~size_t(255);
+    char* base = static_cast<char*>(mdkk::scratch(ctx, off_tmp + scan_bytes + 256));
+    if (!base) return mdkk::cuda_fail(cudaErrorMemoryAllocation, "scratch");
+    int* cnt = reinterpret_cast<int*>(base + off_cnt);
+    int* off = cnt + ncell + 2;
+    const int nx = ncell_host[0], ny = ncell_host[1], nz = ncell_host[2];
+    k_boundary_counts<<<mdkk::grid_for(ncell + 1, 256), 256, 0, s>>>(cell_start, nx, ny, nz, layer, cnt);
+    MDKK_CHECK_LAUNCH("k_boundary_counts");
+    cub::DeviceScan::ExclusiveSum(base + off_tmp, scan_bytes, cnt, off, ncell + 1, s);
+    k_boundary_fill<<<mdkk::grid_for(ncell, 256), 256, 0, s>>>(cell_start, ncell, cnt, off, rows, count);
+    MDKK_CHECK_LAUNCH("k_boundary_fill");
     return MDKK_OK;
 }
 

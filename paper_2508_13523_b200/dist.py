@@ -75,11 +75,11 @@ class CudaOps:
         blk = torch.empty(max(nb * C_, 1), dtype=torch.int32, device=self.device)
         tot = torch.empty(max(C_, 1), dtype=torch.int32, device=self.device)
         _lib.check(lib.mdkk_halo_count(ctx, x.data_ptr(), n, tab.data_ptr(), C_, blk.data_ptr(), tot.data_ptr(),
-                                       self._s()), "mdkk_halo_count")
+                                       None, None, self._s()), "mdkk_halo_count")
         totals = tot[:C_].cpu().numpy().astype(np.int64)
         idx = torch.empty(int(totals.sum()) + 1, dtype=torch.int32, device=self.device)
         _lib.check(lib.mdkk_halo_fill(ctx, x.data_ptr(), n, tab.data_ptr(), C_, blk.data_ptr(), tot.data_ptr(),
-                                      idx.data_ptr(), None, None, self._s()), "mdkk_halo_fill")
+                                      idx.data_ptr(), None, None, None, None, self._s()), "mdkk_halo_fill")
         return idx, totals
 
     def pack(self, x, idx, code, shifts, n, out):

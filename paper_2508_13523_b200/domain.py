@@ -441,7 +441,7 @@ class RankedSystem:
             blk = self._buf(f"blk{src.rank}", nb * C_, torch.int32)
             tot = self._buf(f"tot{src.rank}", C_, torch.int32)[:C_]
             _lib.check(lib.mdkk_halo_count(ctx, src.x.data_ptr(), src.n_local, tab.data_ptr(), C_,
-                                           blk.data_ptr(), tot.data_ptr(), stream), "mdkk_halo_count")
+                                           blk.data_ptr(), tot.data_ptr(), None, None, stream), "mdkk_halo_count")
             plans.append((meta, tab, codes, blk, tot))
         live = [p for p in plans if p is not None]
         host_tot = torch.cat([p[4] for p in live]).cpu().numpy() if live else np.zeros(0, np.int64)
@@ -458,7 +458,7 @@ class RankedSystem:
             cds = self._buf(f"cds{src.rank}", int(totals.sum()) + 1, torch.int8)
             _lib.check(lib.mdkk_halo_fill(ctx, src.x.data_ptr(), src.n_local, tab.data_ptr(), C_, blk.data_ptr(),
                                           tot.data_ptr(), idx.data_ptr(), codes.data_ptr(), cds.data_ptr(),
-                                          stream), "mdkk_halo_fill")
+                                          None, None, stream), "mdkk_halo_fill")
             # combos are dst-major: each (src, dst) lane is one contiguous run of idx
             start = np.concatenate([[0], np.cumsum(totals)])
             d_of = np.array([d for d, _ in meta])
@@ -506,8 +506,20 @@ class RankedSystem:
         nb = (nl + 255) // 256
         blk = self._buf("blk0", nb * C_, torch.int32)
         tot = self._buf("tot0", C_, torch.int32)[:C_]
+        rows = nrow = None
+        bins = getattr(s, "_bins", None)
+        if bins is not None and bins[1] == nl and bins[0] >= halo:
+            # owned rows are cell-sorted on the shell grid with cells >= halo wide: only
+            # rows within two cell layers of the faces can be selected (ascending list)
+            _, _, _, narr, _ = shell_grid_args(s.lo, s.hi, bins[0])
+            rows = self._buf("brows0", nl, torch.int32)
+            nrow = self._buf("bcount0", 1, torch.int32)
+            _lib.check(lib.mdkk_boundary_rows(ctx, bins[2].data_ptr(), narr, 2, rows.data_ptr(), nrow.data_ptr(),
+                                              stream), "mdkk_boundary_rows")
+        rp = rows.data_ptr() if rows is not None else None
+        cp = nrow.data_ptr() if nrow is not None else None
         _lib.check(lib.mdkk_halo_count(ctx, s.x.data_ptr(), nl, tab.data_ptr(), C_, blk.data_ptr(), tot.data_ptr(),
-                                       stream), "mdkk_halo_count")
+                                       rp, cp, stream), "mdkk_halo_count")
         pin = self._scratch.get("tot_pin")
         if pin is None or pin.numel() < C_:
             pin = self._scratch["tot_pin"] = torch.zeros(max(C_, 64), dtype=torch.int32, pin_memory=True)
@@ -517,7 +529,8 @@ class RankedSystem:
         idx = self._buf("idx0", ng + 1, torch.int32)
         cds = self._buf("cds0", ng + 1, torch.int8)
         _lib.check(lib.mdkk_halo_fill(ctx, s.x.data_ptr(), nl, tab.data_ptr(), C_, blk.data_ptr(), tot.data_ptr(),
-                                      idx.data_ptr(), codes.data_ptr(), cds.data_ptr(), stream), "mdkk_halo_fill")
+                                      idx.data_ptr(), codes.data_ptr(), cds.data_ptr(), rp, cp, stream),
+                   "mdkk_halo_fill")
         s.ensure_capacity(nl + ng)
         _lib.check(lib.mdkk_ghost_rows(s.x.data_ptr(), s.gid.data_ptr(), idx.data_ptr(), cds.data_ptr(),
                                        self._shift_dev.data_ptr(), ng, s.x[nl:].data_ptr(), s.gid[nl:].data_ptr(),
