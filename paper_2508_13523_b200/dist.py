@@ -377,7 +377,7 @@ class DistSystem:
         s.device_wrote(force=True)
 
     # ----------------------------------------------------------- migration
-    def migrate(self, halo: float, sort_width: float | None = None) -> None:
+    def migrate(self, halo: float, sort_width: float | None = None, zero_forces: bool = True) -> None:
         """Wrap, send leavers to their bricks, append arrivals, re-sort, rebuild ghosts (mdkk/domain.py:324-334)."""
         s = self.store
         s.to_device()
@@ -429,7 +429,8 @@ class DistSystem:
         st._views()
         st.device_wrote(pos=True, vel=True, force=True)
         self.exchange_ghosts(halo)
-        st.f[: st.n_total].zero_()
+        if zero_forces:
+            st.f[: st.n_total].zero_()
 
     def _sort(self, width: float) -> None:
         s = self.store

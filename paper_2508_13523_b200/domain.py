@@ -574,8 +574,10 @@ class RankedSystem:
             s.device_wrote(force=True)
 
     # ----------------------------------------------------------- migration
-    def migrate(self, halo: float, sort_width: float | None = None) -> None:
-        """Wrap, reassign bricks, re-sort spatially, zero forces, rebuild ghosts (mdkk/domain.py:324-334)."""
+    def migrate(self, halo: float, sort_width: float | None = None, zero_forces: bool = True) -> None:
+        """Wrap, reassign bricks, re-sort spatially, zero forces, rebuild ghosts (mdkk/domain.py:324-334).
+        `zero_forces=False` (engine-internal: the forces are recomputed right away, and every
+        force path clears or overwrites the rows it reads) skips the reset."""
         lib, stream = _lib.lib(), _lib.stream(self.device)
         ctx = _lib.ctx(self.device)
         L = _lib.dbl3(self.box.lengths)
@@ -628,8 +630,9 @@ class RankedSystem:
             s._views()
             s.device_wrote(pos=True, vel=True, force=True)
         self.exchange_ghosts(halo)
-        for s in self.stores:   # the reference resets forces at migration (new AtomStores)
-            s.f[: s.n_total].zero_()
+        if zero_forces:
+            for s in self.stores:   # the reference resets forces at migration (new AtomStores)
+                s.f[: s.n_total].zero_()
 
     def sort_local(self, width: float) -> None:
         """Re-order every rank's owned rows into serpentine cell order (drops ghosts; call before exchange)."""

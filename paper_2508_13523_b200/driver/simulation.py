@@ -350,7 +350,9 @@ class Simulation:
         """migrate + build (mdkk/driver/simulation.py:368-373).  `defer`: the capacity
         check is left to `_settle_lists` (after a count-gated force launch)."""
         halo = self.style.r_c + self.config.skin
-        self.system.migrate(halo)
+        # forces are recomputed right after (full lists overwrite every owned row, half
+        # lists and SNAP clear the rows they accumulate into): no reset pass
+        self.system.migrate(halo, zero_forces=False)
         old = self.lists if self.lists is not None and len(self.lists) == len(self.system.stores) else None
         self.lists = None   # the old lists are dead: their buffers are recycled
         self.lists = [build(s, self.system.box, self.style.r_c, self.config.skin, style=self._list_style,

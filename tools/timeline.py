@@ -17,8 +17,11 @@ dev = torch.device("cuda", 0)
 sim = Simulation(RunConfig(list_style=style, newton=(style == "half"), device=dev), log=None)
 sim.execute(bench.lj_script(80))
 sim._ensure_system(); sim._forces_device()
-for _ in range(5):
-    sim.step_device()
+if loop == "advance":
+    sim.advance(5)        # warm the fused loop's buffers outside the profile
+else:
+    for _ in range(5):
+        sim.step_device()
 torch.cuda.synchronize()
 with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA], with_stack=False) as prof:
     r0 = sim.n_rebuilds
@@ -58,8 +61,10 @@ for e in ev:
 print("cpu ops (total us), top 15:")
 for n, d in cpu.most_common(15):
     print(f"  {d / 1e3:8.3f} ms  {n}")
-# per step: ops from one k_verlet_first to the next
-starts = [n for n, e in enumerate(k) if "k_verlet_first" in e["name"]]
+# per step: ops from one step delimiter to the next (the fused loop has no per-step
+# verlet pass; every step starts with its speculative halo pack)
+delim = "k_verlet_first" if loop != "advance" else "k_pack_shift"
+starts = [n for n, e in enumerate(k) if delim in e["name"]]
 rows = []
 for a, b in zip(starts, starts[1:]):
     ops = k[a:b]
