@@ -31,7 +31,7 @@ import torch
 import torch.distributed as dist
 
 from . import _lib
-from .domain import (SHIFT_UNITS, AtomStore, Box, RankSet, _rows4, _to4, cell_grid, decompose,
+from .domain import (SHIFT_UNITS, AtomStore, Box, RankSet, _rows4, _to4, decompose, shell_grid_args,
                      _dense_ids)
 
 
@@ -69,17 +69,27 @@ class CudaOps:
     def _s(self):
         return _lib.stream(self.device)
 
-    def halo_select(self, x, n, tab, C_):
+    def halo_select(self, x, n, tab, C_, bins=None, lo=None, hi=None):
+        """Per-combo ghost selection; with `bins` (the brick's cell sort on the shell grid,
+        cells >= the halo wide) only the boundary-layer rows are scanned."""
         lib, ctx = _lib.lib(), _lib.ctx(self.device)
         nb = (n + 255) // 256
         blk = torch.empty(max(nb * C_, 1), dtype=torch.int32, device=self.device)
         tot = torch.empty(max(C_, 1), dtype=torch.int32, device=self.device)
+        rp = cp = None
+        if bins is not None:
+            _, _, _, narr, _ = shell_grid_args(lo, hi, bins[0])
+            rows = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
+            cnt = torch.empty(1, dtype=torch.int32, device=self.device)
+            _lib.check(lib.mdkk_boundary_rows(ctx, bins[2].data_ptr(), narr, 2, rows.data_ptr(), cnt.data_ptr(),
+                                              self._s()), "mdkk_boundary_rows")
+            rp, cp = rows.data_ptr(), cnt.data_ptr()
         _lib.check(lib.mdkk_halo_count(ctx, x.data_ptr(), n, tab.data_ptr(), C_, blk.data_ptr(), tot.data_ptr(),
-                                       None, None, self._s()), "mdkk_halo_count")
+                                       rp, cp, self._s()), "mdkk_halo_count")
         totals = tot[:C_].cpu().numpy().astype(np.int64)
         idx = torch.empty(int(totals.sum()) + 1, dtype=torch.int32, device=self.device)
         _lib.check(lib.mdkk_halo_fill(ctx, x.data_ptr(), n, tab.data_ptr(), C_, blk.data_ptr(), tot.data_ptr(),
-                                      idx.data_ptr(), None, None, None, None, self._s()), "mdkk_halo_fill")
+                                      idx.data_ptr(), None, None, rp, cp, self._s()), "mdkk_halo_fill")
         return idx, totals
 
     def pack(self, x, idx, code, shifts, n, out):
@@ -119,15 +129,17 @@ class CudaOps:
         return start.cpu().numpy().astype(np.int64), order
 
     def cell_order(self, x, n, lo, hi, width):
-        """Permutation putting rows in serpentine cell order over the brick."""
+        """Permutation putting rows in serpentine cell order on the brick's shell grid (its
+        cells plus one shell layer: the neighbour build's grid); the bucket starts are kept
+        in `last_bins` for the build's ghost-only binning and the boundary-row halo scan."""
         lib, ctx = _lib.lib(), _lib.ctx(self.device)
-        g, nc = cell_grid(lo, hi, 0.0, width)
-        ncell = nc[0] * nc[1] * nc[2]
+        _, _, garr, narr, ncell = shell_grid_args(lo, hi, width)
         keys = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
         start = torch.empty(ncell + 1, dtype=torch.int32, device=self.device)
         order = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
-        _lib.check(lib.mdkk_bin_atoms(ctx, x.data_ptr(), n, _lib.dbl3(g), _lib.int_arr(nc), keys.data_ptr(),
+        _lib.check(lib.mdkk_bin_atoms(ctx, x.data_ptr(), n, garr, narr, keys.data_ptr(),
                                       start.data_ptr(), order.data_ptr(), self._s()), "mdkk_bin_atoms")
+        self.last_bins = (float(width), n, start)
         return order
 
 
@@ -273,7 +285,11 @@ class DistSystem:
         per_dst = np.zeros(self.world, dtype=np.int64)
         self.send_lanes = []
         if C_ and s.n_local:
-            idx, totals = self.ops.halo_select(s.x, s.n_local, tab, C_)
+            bins = getattr(s, "_bins", None)
+            if isinstance(self.ops, CudaOps) and bins is not None and bins[1] == s.n_local and bins[0] >= halo:
+                idx, totals = self.ops.halo_select(s.x, s.n_local, tab, C_, bins=bins, lo=s.lo, hi=s.hi)
+            else:
+                idx, totals = self.ops.halo_select(s.x, s.n_local, tab, C_)
             start = np.concatenate([[0], np.cumsum(totals)])
             d_of = np.array([d for d, _ in meta])
             codes_all = np.array([c for _, c in meta], dtype=np.int8)
@@ -445,6 +461,7 @@ class DistSystem:
         self.ops.gather_rows(s.v, order, n, v)
         self.ops.gather_i64(s.gid, order, n, g)
         s.x, s.v, s.gid = x, v, g
+        s._bins = getattr(self.ops, "last_bins", None)   # owned rows now sorted on the shell grid
 
     def sort_local(self, width: float) -> None:
         s = self.store
