@@ -510,6 +510,11 @@ class DistSystem:
         self.store.to_device()
         return self._gather_rows(self.store.x, 3)[0]
 
+    def gather_positions_async(self):
+        """The collective gather runs now (every rank must take part at the same step)."""
+        pos = self.gather_positions()
+        return lambda: pos
+
     def gather_forces(self) -> np.ndarray:
         self.store.force.sync("b")
         f, _ = self._gather_rows(self.store.f, 3)

@@ -22,7 +22,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .memspace import DualArray, download, upload
+from .memspace import DualArray, download, download_async, upload
 
 
 class DomainError(RuntimeError):
@@ -672,9 +672,14 @@ class RankedSystem:
         s._bins = (float(width), n, start)   # owned rows sorted on shell_grid_args(lo, hi, width)
 
     # -------------------------------------------------------------- gather
-    def _gid_order(self, rows_fn, width):
-        """Owned rows of all ranks in global-id order (device scatter when gids are 0..N-1)."""
+    def _gid_order(self, rows_fn, width, asynchronous=False):
+        """Owned rows of all ranks in global-id order (device scatter when gids are 0..N-1).
+        `asynchronous`: return a callable that finishes the read-back (dense gids: the
+        device->host copy overlaps the work queued after this call)."""
         n = self.n_atoms
+        if not self.dense_gids and asynchronous:
+            rows = self._gid_order(rows_fn, width)
+            return lambda: rows
         if self.dense_gids:
             lib, stream = _lib.lib(), _lib.stream(self.device)
             out = _rows4(n, self.device, zero=False)   # dense gids: every row is written
@@ -683,7 +688,7 @@ class RankedSystem:
                     gi = s.gid[: s.n_local].to(torch.int32)
                     _lib.check(lib.mdkk_scatter_rows4(rows_fn(s).data_ptr(), gi.data_ptr(), s.n_local,
                                                       out.data_ptr(), stream), "scatter")
-            return download(out[:n, :width])
+            return (download_async if asynchronous else download)(out[:n, :width])
         rows = np.concatenate([rows_fn(s)[: s.n_local, :width].cpu().numpy() for s in self.stores])
         gid = np.concatenate([s.global_ids[: s.n_local] for s in self.stores])
         return rows[np.argsort(gid, kind="stable")]
@@ -705,6 +710,13 @@ class RankedSystem:
         for s in self.stores:
             s.to_device()
         return self._gid_order(lambda s: s.x, 3)
+
+    def gather_positions_async(self):
+        """`gather_positions` whose device->host copy overlaps the work queued next; call
+        the returned function for the array."""
+        for s in self.stores:
+            s.to_device()
+        return self._gid_order(lambda s: s.x, 3, asynchronous=True)
 
     def gather_forces(self) -> np.ndarray:
         """Owned forces in global-id order (mdkk/domain.py:344-348)."""

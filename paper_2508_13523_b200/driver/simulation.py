@@ -646,23 +646,35 @@ class Simulation:
             self.results.append(result)
             rebuilds0 = self.n_rebuilds
 
-            def log(step, e_dev):
+            pending = []     # (step, finish): snapshots whose read-back overlaps the next stretch
+
+            def settle_snapshots():
+                while pending:
+                    at, finish = pending.pop(0)
+                    result.snapshots[at] = finish()
+
+            def log(step, e_dev, last):
                 e_pot = float(self._global_sum(e_dev.reshape(1)).item())
                 self._check_finite(step, e_pot)
                 ke, t = self._kinetic()
                 result.log(step, e_pot, ke, t)
                 if self.snapshots:
-                    result.snapshots[step] = self.system.gather_positions()
+                    if last:
+                        result.snapshots[step] = self.system.gather_positions()
+                    else:
+                        pending.append((step, self.system.gather_positions_async()))
                 self._qeq_diagnostic(step, result)
                 self.log(result.lines[-1])
 
-            log(0, self._forces_device())
+            log(0, self._forces_device(), n_steps == 0)
             step = 0
             while step < n_steps:   # device-resident stretches between thermo steps
                 k = min(self.thermo_every - step % self.thermo_every, n_steps - step)
                 e = self.advance(k)
+                settle_snapshots()
                 step += k
-                log(step, e)
+                log(step, e, step == n_steps)
+            settle_snapshots()
             result.n_rebuilds = self.n_rebuilds - rebuilds0
         return result
 

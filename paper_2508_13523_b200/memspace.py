@@ -104,6 +104,36 @@ def download(t: torch.Tensor) -> np.ndarray:
     return out
 
 
+_COPY_STREAMS: dict = {}
+
+
+def download_async(t: torch.Tensor):
+    """`download(t)` started now, finished by the returned callable: the DMA into pinned
+    staging is queued on a copy stream behind the work already on the current stream, so
+    kernels queued next overlap it; the host copy runs when the callable is invoked.
+    The caller must not write `t` afterwards (pass a private buffer)."""
+    if t.numel() * t.element_size() < _STAGE_MIN or not t.is_cuda:
+        host = t.cpu().numpy()
+        return lambda: host
+    side = _COPY_STREAMS.get(t.device)
+    if side is None:
+        side = _COPY_STREAMS[t.device] = torch.cuda.Stream(t.device)
+    side.wait_stream(torch.cuda.current_stream(t.device))
+    pin = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    with torch.cuda.stream(side):
+        pin.copy_(t, non_blocking=True)
+        done = torch.cuda.Event()
+        done.record(side)
+    t.record_stream(side)
+
+    def finish() -> np.ndarray:
+        done.synchronize()
+        out = np.empty(tuple(pin.shape), dtype=pin.numpy().dtype)
+        torch.from_numpy(out).copy_(pin)
+        return out
+    return finish
+
+
 
 class DualArray:
     """Host/device mirrored array with staleness flags (mdkk/memspace.py:77-156).

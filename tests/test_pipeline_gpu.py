@@ -106,3 +106,23 @@ def test_fused_loop_overflow_relaunch_matches_synchronous(gpu):
     assert ra.lines == rb.lines
     assert np.array_equal(a.system.gather_positions(), b.system.gather_positions())
     assert np.array_equal(a.system.gather()[1], b.system.gather()[1])     # velocities
+
+
+def test_overlapped_snapshots_match_synchronous_reads(gpu):
+    """run_nve's thermo snapshots whose read-back overlaps the next stretch (pinned DMA on
+    a copy stream, large enough for the staged path) equal positions read synchronously at
+    the same steps."""
+    from paper_2508_13523_b200.driver import RunConfig, Simulation
+    big = MELT.replace("create_box 8 8 8", "create_box 23 23 23")
+    a = Simulation(RunConfig(list_style="full", newton=False), log=None)
+    b = Simulation(RunConfig(list_style="full", newton=False), log=None)
+    a.execute(big)
+    b.execute(big)
+    assert a.snapshots and 4 * 23 ** 3 * 3 * 8 > (1 << 20)
+    ra = a.run_nve(30)
+    ref = {0: b.run_nve(0).snapshots[0]}       # the last snapshot of a run is read synchronously
+    for k in range(1, 4):
+        ref[10 * k] = b.run_nve(10).snapshots[10]
+    assert sorted(ra.snapshots) == [0, 10, 20, 30]
+    for step, snap in ra.snapshots.items():
+        assert np.array_equal(snap, ref[step]), step
