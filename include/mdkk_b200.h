@@ -209,6 +209,36 @@ int mdkk_lj_force_gated(mdkk_ctx* ctx, const double* x, int n_local, const int* 
                         int cap, int style, int newton, int virial, int mode, double epsilon, double sigma,
                         double rc, double* f, double* ev, int* flags, const double* maxdisp2, double half_skin,
                         const int* max_count, int count_limit, void* stream);
+/* Half-list force with an explicit partner-write strategy: compute_pair's
+ * `strategy` (mdkk/pair_lj.py:114-139 -> ScatterAccumulator, mdkk/memspace.py:165-254).
+ * strategy 1 = Duplicate: own and partner REDs go into staging copy
+ * (block % copies) of `copies` zeroed f-shaped ([n][4]) copies `stride` doubles apart;
+ * the caller combines them with mdkk_scatter_combine.  strategy 2 = Serial: own rows
+ * are stored into f, each partner contribution is written as double4 (g, 1) per table
+ * entry into `stage` (zeroed, the table's [ncl][cap][32] layout) and applied in entry
+ * order by mdkk_scatter_ordered (no atomics: deterministic).  Atomic is mdkk_lj_force. */
+int mdkk_lj_force_strategy(mdkk_ctx* ctx, const double* x, int n_local, const int* table, const int* counts,
+                           int cap, int newton, int virial, double epsilon, double sigma, double rc, double* f,
+                           double* ev, int* flags, int strategy, double* stage, long long stride, int copies,
+                           void* stream);
+
+/* ---------------------------------------------------------------- scatter
+ * ScatterAccumulator strategies (mdkk/memspace.py:198-257) on row-major
+ * [n_rows][ld] f64 targets; a contribution updates `width` leading entries.
+ * atomic : target[idx[e]][c] += vals[e][c] with FP64 RED (Atomic).
+ * ordered: `sorted_idx`/`perm` are the stable sort of the contribution indices;
+ *          each row's contributions are added one by one in their original order
+ *          onto its current value -- bit-identical to sequential np.add.at (Serial).
+ * combine: out[e] += ((stage[0][e] + stage[1][e]) + ...) over `copies` staging copies
+ *          `stride` doubles apart (Duplicate's finalize, np.add.reduce order).
+ * index_range: *bad = min(*bad, e) for every idx[e] outside [0, n_rows) (caller
+ *          initialises *bad to ~0): the reference's IndexError check. */
+int mdkk_scatter_atomic(double* target, int ld, int width, const long long* idx, const double* vals, long long n,
+                        void* stream);
+int mdkk_scatter_ordered(double* target, int ld, int width, const long long* sorted_idx, const long long* perm,
+                         const double* vals, long long n, void* stream);
+int mdkk_scatter_combine(const double* stage, int copies, long long stride, double* out, long long n, void* stream);
+int mdkk_index_range(const long long* idx, long long n, long long n_rows, unsigned long long* bad, void* stream);
 
 /* ------------------------------------------------------------- integrator
  * Velocity Verlet (mdkk/driver/simulation.py:431-450) fused with the skin
@@ -300,6 +330,12 @@ int mdkk_snap_deidrj_staged(mdkk_snap* snap, int n_pairs, const int* rows, const
  * terms (half indices; code = g | h << 8 | z << 16 | conj_g << 24 | conj_h << 25 |
  * conj_z << 26 | last-of-triple << 27; tri[k] = triple of term k; chunk[w] =
  * first term of warp w, output-aligned, mdkk_snap_bi_warps() + 1 entries). */
+/* pair_u_flat (mdkk/snap/compute.py:165-184): u_0..u_2J of arbitrary (a, b) (complex128
+ * [n]) by the reference's four-term recursion, out complex128 [n][n_flat]. */
+int mdkk_snap_pair_u(int n_pairs, int twojmax, const double* a, const double* b, double* out, void* stream);
+/* NeighborMap.deriv_params (mdkk/snap/compute.py:48-63,98-102): da, db complex128 [n][3]
+ * from dr f64 [n][3]. */
+int mdkk_snap_pair_grads(int n_pairs, const double* dr, double rc, double* da, double* db, void* stream);
 int mdkk_snap_bi(mdkk_snap* snap, const double* U, int n_local, const double* coef, const int* code, const int* tri,
                  const int* chunk, int n_tri, double* B, int layout, int ldu, void* stream);
 int mdkk_snap_bi_warps(void);

@@ -9,11 +9,14 @@ fallback: compute entry points raise if the library is not built.
 __version__ = "0.1.0"
 
 from .domain import AtomStore, Box, DomainError, RankedSystem, RankSet, decompose  # noqa: E402
-from .memspace import DualArray, LayoutPolicy, MemspaceError  # noqa: E402
-from .neighbor import NeighborError, NeighborList, StaleListError, any_needs_rebuild, build, build_all  # noqa: E402
+from .memspace import (Atomic, DualArray, Duplicate, LayoutPolicy, MemspaceError, ScatterAccumulator,  # noqa: E402
+                       Serial, create_dual, scatter_accumulate)
+from .neighbor import (NeighborError, NeighborList, StaleListError, any_needs_rebuild, brute_force_pairs,  # noqa: E402
+                       build, build_all)
 from .pair_lj import LJCut, PairError, PairParams, PairResult, compute_pair, u2_lj  # noqa: E402
 
 __all__ = ["AtomStore", "Box", "DomainError", "RankedSystem", "RankSet", "decompose", "DualArray",
-           "LayoutPolicy", "MemspaceError", "NeighborError", "NeighborList", "StaleListError",
-           "any_needs_rebuild", "build", "build_all", "LJCut", "PairError", "PairParams", "PairResult",
+           "LayoutPolicy", "MemspaceError", "ScatterAccumulator", "Serial", "Duplicate", "Atomic", "create_dual",
+           "scatter_accumulate", "NeighborError", "NeighborList", "StaleListError",
+           "any_needs_rebuild", "brute_force_pairs", "build", "build_all", "LJCut", "PairError", "PairParams", "PairResult",
            "compute_pair", "u2_lj"]

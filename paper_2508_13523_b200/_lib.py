@@ -21,6 +21,7 @@ FLAG_COINCIDENT, FLAG_NONFINITE = 1, 2
 _p = C.c_void_p
 _i = C.c_int
 _d = C.c_double
+_l = C.c_longlong
 
 # name -> argtypes (restype is always c_int unless listed in _RESTYPE)
 SIGNATURES = {
@@ -56,6 +57,11 @@ SIGNATURES = {
                                 _p, _d, _d, _p],
     "mdkk_lj_force_gated": [_p, _p, _i, _p, _p, _i, _i, _i, _i, _i, _d, _d, _d, _p, _p, _p, _p, _d, _p, _i, _p],
     "mdkk_lj_force_neighbor": [_p, _p, _i, _p, _p, _i, _i, _i, _i, _d, _d, _d, _p, _p, _p, _p],
+    "mdkk_lj_force_strategy": [_p, _p, _i, _p, _p, _i, _i, _i, _d, _d, _d, _p, _p, _p, _i, _p, _l, _i, _p],
+    "mdkk_scatter_atomic": [_p, _i, _i, _p, _p, _l, _p],
+    "mdkk_scatter_ordered": [_p, _i, _i, _p, _p, _p, _l, _p],
+    "mdkk_scatter_combine": [_p, _i, _l, _p, _l, _p],
+    "mdkk_index_range": [_p, _l, _l, _p, _p],
     "mdkk_verlet_first": [_p, _p, _p, _p, _p, _i, _d, _d, _p, _i, _p],
     "mdkk_verlet_second": [_p, _p, _p, _i, _d, _d, _p, _p],
     "mdkk_kinetic": [_p, _p, _i, _d, _p, _p],
@@ -73,6 +79,8 @@ SIGNATURES = {
     "mdkk_snap_deidrj_staged": [_p, _i, _p, _p, _p, _p, _p, _p],
     "mdkk_snap_bi": [_p, _p, _i, _p, _p, _p, _p, _i, _p, _i, _i, _p],
     "mdkk_snap_bi_warps": [],
+    "mdkk_snap_pair_u": [_i, _i, _p, _p, _p, _p],
+    "mdkk_snap_pair_grads": [_i, _p, _d, _p, _p, _p],
     "mdkk_qeq_offsets": [_p, _p, _i, _i, _p, _p, _p],
     "mdkk_qeq_build": [_p, _i, _p, _p, _i, _p, _p, _d, _d, _d, _p, _p, _p, _p],
     "mdkk_qeq_spmv": [_p, _p, _p, _p, _p, _i, _p, _p, _p, _p, _p, _p],

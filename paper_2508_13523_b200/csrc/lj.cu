@@ -46,13 +46,30 @@ struct Integ {
     double h;
 };
 
-template <int STYLE, bool NEWTON, bool VIR, int MODE = 0>
+// Half-list partner-write deconfliction (compute_pair's `strategy`, the
+// reference's ScatterAccumulator strategies, mdkk/memspace.py:165-254):
+// SCAT 0 Atomic    -- FP64 RED straight into f (the default engine path);
+// SCAT 1 Duplicate -- RED into staging copy (blockIdx % copies), combined afterwards
+//                     in a fixed order by mdkk_scatter_combine;
+// SCAT 2 Serial    -- no atomics: own rows stored, each partner contribution staged
+//                     per table entry (double4 (g, 1) in the table's blocked layout)
+//                     and applied in entry order by mdkk_scatter_ordered -- run-to-run
+//                     deterministic.
+struct Scat {
+    double* stage;
+    long long stride;
+    int copies;
+};
+
+template <int STYLE, bool NEWTON, bool VIR, int MODE = 0, int SCAT = 0>
 __global__ void __launch_bounds__(kBlock) k_lj(const double* __restrict__ x, int n_local,
                                                const int* __restrict__ table, const int* __restrict__ counts,
                                                int cap, double eps4, double eps24, double sig2, double rc2,
                                                double* __restrict__ f, double* __restrict__ partials,
-                                               int* __restrict__ flags, Gate gate, Integ integ = Integ{}) {
+                                               int* __restrict__ flags, Gate gate, Integ integ = Integ{},
+                                               Scat scat = Scat{}) {
     static_assert(MODE == 0 || STYLE == 0, "integration needs the complete f_i: full lists only");
+    static_assert(SCAT == 0 || STYLE == 1, "strategies apply to half lists (full lists write owner rows only)");
     if (gated_off(gate)) return;   // block-uniform: the step rebuilds and relaunches
     const int i = blockIdx.x * kBlock + threadIdx.x;
     double acc[7] = {0, 0, 0, 0, 0, 0, 0};  // E, Wxx, Wyy, Wzz, Wxy, Wxz, Wyz
@@ -63,7 +80,9 @@ __global__ void __launch_bounds__(kBlock) k_lj(const double* __restrict__ x, int
         double fx = 0.0, fy = 0.0, fz = 0.0;
         bool bad = false;
         const int* col = table + ((long long)(i >> 5) * cap) * 32 + (i & 31);
-        auto pair = [&](int j, const double4& xj) {
+        double* fw = f;   // partner / own-row RED target
+        if (SCAT == 1) fw = scat.stage + (long long)(blockIdx.x % scat.copies) * scat.stride;
+        auto pair = [&](int j, const double4& xj, int kk) {
             const double dx = xj.x - xi.x, dy = xj.y - xi.y, dz = xj.z - xi.z;
             const double r2 = mdkk::r2_exact(dx, dy, dz);
             if (r2 < rc2) {
@@ -80,10 +99,15 @@ __global__ void __launch_bounds__(kBlock) k_lj(const double* __restrict__ x, int
                 fy -= gy;
                 fz -= gz;
                 if (wj) {
-                    double* fj = f + 4LL * j;
-                    atomicAdd(fj + 0, gx);
-                    atomicAdd(fj + 1, gy);
-                    atomicAdd(fj + 2, gz);
+                    if (SCAT == 2) {
+                        mdkk::st4(scat.stage, ((long long)(i >> 5) * cap + kk) * 32 + (i & 31),
+                                  make_double4(gx, gy, gz, 1.0));
+                    } else {
+                        double* fj = fw + 4LL * j;
+                        atomicAdd(fj + 0, gx);
+                        atomicAdd(fj + 1, gy);
+                        atomicAdd(fj + 2, gz);
+                    }
                 }
                 acc[0] += wgt * (eps4 * (s12 - s6));
                 if (VIR) {
@@ -115,11 +139,11 @@ __global__ void __launch_bounds__(kBlock) k_lj(const double* __restrict__ x, int
 #pragma unroll
             for (int b = 0; b < kB; ++b) jn[b] = (k + kB + b < n) ? __ldg(col + (long long)(k + kB + b) * 32) : i;
 #pragma unroll
-            for (int b = 0; b < kB; ++b) pair(jc[b], xc[b]);
+            for (int b = 0; b < kB; ++b) pair(jc[b], xc[b], k + b);
         }
 #pragma unroll
         for (int b = 0; b < kB; ++b)
-            if (k + b < n) pair(jn[b], mdkk::ld4(x, jn[b]));
+            if (k + b < n) pair(jn[b], mdkk::ld4(x, jn[b]), k + b);
         if (STYLE == 0) {
             mdkk::st4(f, i, make_double4(fx, fy, fz, 0.0));
             if (MODE > 0) {
@@ -143,8 +167,10 @@ __global__ void __launch_bounds__(kBlock) k_lj(const double* __restrict__ x, int
                 }
                 mdkk::st4(integ.v, i, vi);
             }
+        } else if (SCAT == 2) {
+            mdkk::st4(f, i, make_double4(fx, fy, fz, 0.0));   // partners are applied afterwards
         } else {
-            double* fi = f + 4LL * i;
+            double* fi = fw + 4LL * i;
             atomicAdd(fi + 0, fx);
             atomicAdd(fi + 1, fy);
             atomicAdd(fi + 2, fz);
@@ -373,4 +399,49 @@ extern "C" int mdkk_lj_force_gated(mdkk_ctx* ctx, const double* x, int n_local, 
                                                     epsilon, sigma, rc, f, ev, flags,
                                                     Gate{maxdisp2, half_skin, max_count, count_limit},
                                                     mdkk::as_stream(stream));
+}
+
+// Half-list force with an explicit partner-write strategy (compute_pair's
+// `strategy`; see Scat above).  strategy 1 = Duplicate (`stage` holds `copies`
+// zeroed f-shaped copies `stride` doubles apart; the caller combines them),
+// 2 = Serial (`stage` is a zeroed double4 per table entry, [ncl][cap][32]).
+extern "C" int mdkk_lj_force_strategy(mdkk_ctx* ctx, const double* x, int n_local, const int* table,
+                                      const int* counts, int cap, int newton, int virial, double epsilon,
+                                      double sigma, double rc, double* f, double* ev, int* flags, int strategy,
+                                      double* stage, long long stride, int copies, void* stream) {
+    if (!ctx || n_local < 0 || cap < 1 || !stage || (strategy != 1 && strategy != 2)) return MDKK_E_ARG;
+    if (strategy == 1 && (copies < 1 || stride < 4LL * n_local)) return MDKK_E_ARG;
+    cudaStream_t s = mdkk::as_stream(stream);
+    if (n_local == 0) {
+        cudaMemsetAsync(ev, 0, 7 * sizeof(double), s);
+        return MDKK_OK;
+    }
+    const int nb = mdkk::grid_for(n_local, kBlock);
+    double* partials = static_cast<double*>(mdkk::scratch(ctx, sizeof(double) * 7 * (size_t)nb));
+    if (!partials) return mdkk::cuda_fail(cudaErrorMemoryAllocation, "scratch");
+    const double e4 = 4.0 * epsilon, e24 = 24.0 * epsilon, s2 = sigma * sigma, rc2 = rc * rc;
+    const Gate gate{nullptr, 0.0, nullptr, 0};
+    const Scat scat{stage, stride, copies};
+#define MDKK_LJS(NW, VR, SC)                                                                                  \
+    k_lj<1, NW, VR, 0, SC><<<nb, kBlock, 0, s>>>(x, n_local, table, counts, cap, e4, e24, s2, rc2, f, partials, \
+                                                 flags, gate, Integ{}, scat)
+    if (strategy == 1) {
+        if (newton) {
+            if (virial) MDKK_LJS(true, true, 1); else MDKK_LJS(true, false, 1);
+        } else {
+            if (virial) MDKK_LJS(false, true, 1); else MDKK_LJS(false, false, 1);
+        }
+    } else {
+        if (newton) {
+            if (virial) MDKK_LJS(true, true, 2); else MDKK_LJS(true, false, 2);
+        } else {
+            if (virial) MDKK_LJS(false, true, 2); else MDKK_LJS(false, false, 2);
+        }
+    }
+#undef MDKK_LJS
+    MDKK_CHECK_LAUNCH("k_lj (strategy)");
+    if (!virial) cudaMemsetAsync(ev, 0, 7 * sizeof(double), s);
+    mdkk::reduce_partials(partials, nb, virial ? 7 : 1, ev, s);
+    MDKK_CHECK_LAUNCH("k_reduce_partials");
+    return MDKK_OK;
 }

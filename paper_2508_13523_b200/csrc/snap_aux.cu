@@ -241,9 +241,98 @@ __global__ void __launch_bounds__(kBW * 32) k_snap_bi(const double2* __restrict_
     }
 }
 
+
+// ------------------------------------------------------------ pair levels
+// pair_u_flat (mdkk/snap/compute.py:165-184): unweighted levels u_0..u_2J of
+// arbitrary (a, b) by the reference's four-term recursion (:138-147), every
+// (tj+1)^2 block in full (no mirror: (a, b) need not be unitary here).  One warp
+// per pair, levels ping-ponged in shared memory; the terms are added in the
+// reference's order with explicit roundings.
+constexpr int kUW = 4;
+
+__device__ __forceinline__ cplx cmul_rn(cplx x, cplx y) {
+    return {__dsub_rn(__dmul_rn(x.re, y.re), __dmul_rn(x.im, y.im)),
+            __dadd_rn(__dmul_rn(x.re, y.im), __dmul_rn(x.im, y.re))};
+}
+__device__ __forceinline__ cplx cacc_rn(cplx acc, double c, cplx v) {
+    return {__dadd_rn(acc.re, __dmul_rn(c, v.re)), __dadd_rn(acc.im, __dmul_rn(c, v.im))};
+}
+
+__global__ void __launch_bounds__(kUW * 32) k_snap_pair_u(int n_pairs, int twojmax, const double2* __restrict__ a_in,
+                                                          const double2* __restrict__ b_in, double2* __restrict__ out) {
+    __shared__ cplx s_l[kUW][2][kLevelMax];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const long long p = (long long)blockIdx.x * kUW + w;
+    if (p >= n_pairs) return;
+    const int nf = block_offset(twojmax + 1);
+    const cplx a = {a_in[p].x, a_in[p].y}, b = {b_in[p].x, b_in[p].y};
+    const cplx ac = {a.re, -a.im}, nbc = {-b.re, b.im};
+    double2* o = out + p * nf;
+    if (lane == 0) {
+        s_l[w][0][0] = {1.0, 0.0};
+        o[0] = make_double2(1.0, 0.0);
+    }
+    __syncwarp();
+    for (int tj = 1; tj <= twojmax; ++tj) {
+        const cplx* v = s_l[w][(tj - 1) & 1];   // previous level, row-major tj x tj
+        cplx* nw = s_l[w][tj & 1];
+        const double itj = (double)tj;
+        for (int e = lane; e < (tj + 1) * (tj + 1); e += 32) {
+            const int P = e / (tj + 1), Q = e % (tj + 1);
+            cplx acc = {0.0, 0.0};
+            if (P >= 1 && Q >= 1) acc = cacc_rn(acc, sqrt((double)(P * Q)) / itj, cmul_rn(v[(P - 1) * tj + Q - 1], a));
+            if (P >= 1 && Q < tj) acc = cacc_rn(acc, sqrt((double)(P * (tj - Q))) / itj, cmul_rn(v[(P - 1) * tj + Q], b));
+            if (P < tj && Q >= 1) acc = cacc_rn(acc, sqrt((double)((tj - P) * Q)) / itj, cmul_rn(v[P * tj + Q - 1], nbc));
+            if (P < tj && Q < tj) acc = cacc_rn(acc, sqrt((double)((tj - P) * (tj - Q))) / itj, cmul_rn(v[P * tj + Q], ac));
+            nw[e] = acc;
+            o[block_offset(tj) + e] = make_double2(acc.re, acc.im);
+        }
+        __syncwarp();
+    }
+}
+
+// NeighborMap.deriv_params (mdkk/snap/compute.py:48-63,98-102): (da, db) per pair,
+// [n][3] complex each, from the same device geometry the force kernels use.
+__global__ void k_snap_pair_grads(int n_pairs, const double* __restrict__ dr, double rc, double2* __restrict__ da_out,
+                                  double2* __restrict__ db_out) {
+    const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n_pairs) return;
+    const double d[3] = {dr[3 * p + 0], dr[3 * p + 1], dr[3 * p + 2]};
+    PairGeo g;
+    double z0, r0;
+    pair_geometry(d[0], d[1], d[2], mdkk::r2_exact(d[0], d[1], d[2]), rc, g, z0, r0);
+    cplx da[3], db[3];
+    pair_grads(d, g, rc, z0, r0, da, db);
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        da_out[3 * p + q] = make_double2(da[q].re, da[q].im);
+        db_out[3 * p + q] = make_double2(db[q].re, db[q].im);
+    }
+}
+
 }  // namespace
 
 extern "C" {
+
+int mdkk_snap_pair_u(int n_pairs, int twojmax, const double* a, const double* b, double* out, void* stream) {
+    if (n_pairs < 0 || twojmax < 0 || twojmax > kMaxTwoJ || (n_pairs && (!a || !b || !out))) return MDKK_E_ARG;
+    if (n_pairs == 0) return MDKK_OK;
+    k_snap_pair_u<<<(n_pairs + kUW - 1) / kUW, kUW * 32, 0, mdkk::as_stream(stream)>>>(
+        n_pairs, twojmax, reinterpret_cast<const double2*>(a), reinterpret_cast<const double2*>(b),
+        reinterpret_cast<double2*>(out));
+    MDKK_CHECK_LAUNCH("k_snap_pair_u");
+    return MDKK_OK;
+}
+
+int mdkk_snap_pair_grads(int n_pairs, const double* dr, double rc, double* da, double* db, void* stream) {
+    if (n_pairs < 0 || (n_pairs && (!dr || !da || !db))) return MDKK_E_ARG;
+    if (n_pairs == 0) return MDKK_OK;
+    upload_weights();
+    k_snap_pair_grads<<<mdkk::grid_for(n_pairs, 128), 128, 0, mdkk::as_stream(stream)>>>(
+        n_pairs, dr, rc, reinterpret_cast<double2*>(da), reinterpret_cast<double2*>(db));
+    MDKK_CHECK_LAUNCH("k_snap_pair_grads");
+    return MDKK_OK;
+}
 
 int mdkk_snap_pair_count(mdkk_ctx* ctx, const double* x, int n_local, const int* table, const int* counts, int cap,
                          double rc, int* npair, int* offsets, int* flags, void* stream) {

@@ -24,6 +24,7 @@ import torch
 
 from .. import _lib
 from ..domain import Box, RankedSystem
+from ..memspace import Atomic, Duplicate, Serial
 from ..neighbor import build, build_all
 from ..pair_lj import LJCut, PairParams, PairResult, compute_pair, lj_force_rank
 from .registry import StyleRegistry
@@ -37,12 +38,15 @@ class RunError(RuntimeError):
 class RunConfig:
     """Harness knobs (mdkk/driver/simulation.py:36-62) plus `device`."""
 
-    def __init__(self, n_ranks: int = 1, strategy: str = "serial", mode: str | None = None,
+    def __init__(self, n_ranks: int = 1, strategy: str | None = None, mode: str | None = None,
                  list_style: str | None = None, newton: bool = True, skin: float = 0.3,
                  workers: int | None = None, batch_u: int | None = None, batch_y: int | None = None,
                  tile_v: int | None = None, layout: str | None = None, rng_seed: int | None = None,
                  device=None, distributed: bool = False):
-        if strategy not in ("serial", "duplicate", "atomic"):
+        # None = the device default (owner writes for full lists, FP64 RED for half
+        # lists); an explicit name selects that ScatterAccumulator strategy for the
+        # half list's partner writes (the reference defaults to "serial")
+        if strategy is not None and strategy not in ("serial", "duplicate", "atomic"):
             raise RunError(f"unknown strategy {strategy!r}; choose from ['atomic', 'duplicate', 'serial']")
         self.n_ranks = int(n_ranks)
         self.strategy = strategy
@@ -56,6 +60,12 @@ class RunConfig:
         self.device = device
         # one brick per process over torch.distributed (NCCL) instead of in-process logical ranks
         self.distributed = bool(distributed)
+
+    def make_strategy(self):
+        """The strategy object compute_pair receives (mdkk/driver/simulation.py:58-59)."""
+        if self.strategy is None:
+            return None
+        return {"serial": Serial, "atomic": Atomic}.get(self.strategy, lambda: Duplicate(self.workers))()
 
 
 class LJStyle:
@@ -76,7 +86,8 @@ class LJStyle:
     def compute(self, system, lists, config: RunConfig, check: bool = True) -> PairResult:
         if self.kernel is None:
             raise RunError("pair_coeff must be set before computing forces")
-        return compute_pair(self.kernel, system, lists, mode=config.mode or self.default_mode, check=check)
+        return compute_pair(self.kernel, system, lists, mode=config.mode or self.default_mode,
+                            strategy=config.make_strategy(), n_workers=config.workers, check=check)
 
     def compute_device(self, system, lists, config, gate=None, gate_limit: float = 0.0, integ=None
                        ) -> tuple[torch.Tensor, torch.Tensor]:
@@ -96,7 +107,8 @@ class LJStyle:
         half = False
         for k, (s, nl) in enumerate(zip(system.stores, lists)):
             lj_force_rank(s, nl, self.kernel.params, evs[k], flags, virial=False,
-                          mode=config.mode or self.default_mode, gate=gate, gate_limit=gate_limit, integ=integ)
+                          mode=config.mode or self.default_mode, gate=gate, gate_limit=gate_limit, integ=integ,
+                          strategy=config.make_strategy())
             half |= nl.style == "half"
         if half:   # collective in the distributed system: every rank calls it
             system.reverse_comm()
@@ -441,7 +453,7 @@ class Simulation:
         # it next, and a rebuild simply overwrites the ghost rows
         self.system.forward_comm()
         self._packed = True
-        if getattr(self.style, "supports_gate", False):
+        if self._speculative():
             # speculative force launch, gated on the device by the same skin test:
             # the GPU runs it while the host reads the decision (no idle gap), and
             # it is a no-op on a rebuilding step (relaunched after the rebuild)
@@ -473,7 +485,7 @@ class Simulation:
             # round trip, and only an overflow (rare: cap grows x1.5) repeats it
             # (distributed half lists excepted: a regrow on one rank would re-run the
             # reverse-comm collective on that rank alone)
-            defer = (getattr(self.style, "supports_gate", False) and self._cap_hint is not None
+            defer = (self._speculative() and self._cap_hint is not None
                      and not (self.config.distributed and self._list_style == "half"))
             self._rebuild_lists(defer=defer)
             e = self._forces_device()
@@ -521,11 +533,17 @@ class Simulation:
             if was:
                 gc.enable()
 
+    def _speculative(self) -> bool:
+        """Gated (speculative) force launches: LJ with the default or Atomic half-list
+        writes; an explicit Serial / Duplicate strategy runs the staged kernels unguarded."""
+        return (getattr(self.style, "supports_gate", False)
+                and not (self._list_style == "half" and self.config.strategy in ("serial", "duplicate")))
+
     def _fusable(self) -> bool:
         """The integration fuses into the force kernel for full-list LJ (atom mode) with one
         store per process (one in-process rank, or one rank per GPU): the epilogue needs
         each owned atom's complete force."""
-        return (isinstance(self.style, LJStyle) and getattr(self.style, "supports_gate", False)
+        return (isinstance(self.style, LJStyle) and self._speculative()
                 and self._list_style == "full" and (self.config.mode or self.style.default_mode) == "atom"
                 and len(self.system.stores) == 1)
 

@@ -6,13 +6,18 @@ copies), but space "b" is real HBM.  Device rows may be padded: positions and
 forces are stored as AoS double4 (x, y, z, pad) so one neighbour gather is one
 32-byte sector, while the logical (n, 3) view is what both spaces expose.
 
-Scatter strategies (Serial / Duplicate / Atomic, mdkk/memspace.py:165-254)
-are accepted for signature compatibility; on the GPU the deconfliction is
-fixed by the list style: full lists are owner-writes (no atomics), half lists
-use FP64 atomics (`RED.E.ADD.F64`).
+Scatter strategies (Serial / Duplicate / Atomic) and `ScatterAccumulator`
+(mdkk/memspace.py:165-257) run on the device (csrc/scatter.cu): Serial is an
+ordered segmented sum (bit-identical to sequential np.add.at), Atomic is
+FP64 RED, Duplicate stages one copy per worker and combines them in a fixed
+order.  `compute_pair` maps the same strategies onto the half-list force
+kernel's partner writes (full lists write owner rows only: nothing to
+deconflict).
 """
 
 from __future__ import annotations
+
+import os
 
 import numpy as np
 import torch
@@ -241,14 +246,196 @@ def create_dual(shape, layout_a=None, layout_b=None, dtype=np.float64, device=No
     return DualArray(shape, layout_a=layout_a, layout_b=layout_b, dtype=dtype, device=device, **kw)
 
 
+DEFAULT_WORKERS = 4
+
+
+def worker_count(requested: int | None = None) -> int:
+    """Logical worker count honouring the MDKK_THREADS cap (mdkk/parallel.py:15-26).
+
+    On the GPU the workers are Duplicate's staging copies (one per worker)."""
+    n = requested if requested is not None else DEFAULT_WORKERS
+    cap = os.environ.get("MDKK_THREADS")
+    if cap is not None:
+        try:
+            cap_n = int(cap)
+        except ValueError as exc:
+            raise ValueError(f"MDKK_THREADS must be an integer, got {cap!r}") from exc
+        if cap_n < 1:
+            raise ValueError(f"MDKK_THREADS must be >= 1, got {cap_n}")
+        n = min(n, cap_n)
+    return max(1, int(n))
+
+
 class Serial:
+    """Ordered sequential accumulation (mdkk/memspace.py:165-171): a deterministic
+    segmented sum on the device, bit-identical to np.add.at in contribution order."""
+
     copies = 1
+
+    def __repr__(self):
+        return "Serial()"
 
 
 class Duplicate:
+    """Per-worker staging copies plus a fixed-order combine (mdkk/memspace.py:174-183)."""
+
     def __init__(self, copies: int | None = None):
-        self.copies = int(copies or 1)
+        self.copies = worker_count(copies)
+        if self.copies < 1:
+            raise ValueError("Duplicate requires at least one copy")
+
+    def __repr__(self):
+        return f"Duplicate(copies={self.copies})"
 
 
 class Atomic:
+    """Concurrent FP64 RED adds on shared storage (mdkk/memspace.py:186-192)."""
+
     copies = 1
+
+    def __repr__(self):
+        return "Atomic()"
+
+
+STRATEGIES = (Serial, Duplicate, Atomic)
+
+
+def _lib():
+    from . import _lib as lib_mod
+    return lib_mod
+
+
+def ordered_scatter(target: torch.Tensor, ld: int, width: int, idx: torch.Tensor, vals: torch.Tensor) -> None:
+    """target[idx[e], :width] += vals[e] one contribution at a time in e order (Serial)."""
+    n = int(idx.numel())
+    if n == 0:
+        return
+    sorted_idx, perm = torch.sort(idx, stable=True)
+    L = _lib()
+    L.call("mdkk_scatter_ordered", target.data_ptr(), ld, width, sorted_idx.data_ptr(), perm.data_ptr(),
+           vals.data_ptr(), n, L.stream(target.device))
+
+
+def atomic_scatter(target: torch.Tensor, ld: int, width: int, idx: torch.Tensor, vals: torch.Tensor) -> None:
+    n = int(idx.numel())
+    if n:
+        L = _lib()
+        L.call("mdkk_scatter_atomic", target.data_ptr(), ld, width, idx.data_ptr(), vals.data_ptr(), n,
+               L.stream(target.device))
+
+
+def combine_copies(stage: torch.Tensor, out: torch.Tensor) -> None:
+    """out += ((stage[0] + stage[1]) + ...) element-wise (Duplicate's finalize)."""
+    copies = int(stage.shape[0])
+    n = int(out.numel())
+    if n:
+        L = _lib()
+        L.call("mdkk_scatter_combine", stage.data_ptr(), copies, int(stage[0].numel()), out.data_ptr(), n,
+               L.stream(out.device))
+
+
+class ScatterAccumulator:
+    """Indexed accumulation into a dense device target (mdkk/memspace.py:198-254).
+
+    Contributions index the first axis of ``target_shape``; values carry the
+    remaining axes.  ``finalize`` is a barrier and returns the host array (the
+    reference's return type); ``finalize_device`` returns the device tensor.
+    FP64 only (the kernels accumulate in double).
+    """
+
+    def __init__(self, target_shape, strategy=None, dtype=np.float64, device=None):
+        self.target_shape = tuple(int(s) for s in target_shape)
+        if any(s < 0 for s in self.target_shape):
+            raise ValueError(f"invalid target shape {self.target_shape}")
+        self.strategy = strategy if strategy is not None else Serial()
+        if not isinstance(self.strategy, STRATEGIES):
+            raise TypeError(f"unknown scatter strategy {self.strategy!r}")
+        if np.dtype(dtype) != np.float64:
+            raise TypeError("ScatterAccumulator accumulates in float64 on the device")
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self._n = self.target_shape[0] if self.target_shape else 0
+        self._width = int(np.prod(self.target_shape[1:])) if len(self.target_shape) > 1 else 1
+        rows = max(self._n, 0)
+        if isinstance(self.strategy, Duplicate):
+            self._staging = torch.zeros((self.strategy.copies, rows * self._width), dtype=torch.float64,
+                                        device=self.device)
+            self._pending = [[] for _ in range(self.strategy.copies)]
+        else:
+            self._staging = None
+            self._pending = [[]]
+        self._data = torch.zeros(rows * self._width, dtype=torch.float64, device=self.device)
+        self._bad = torch.empty(1, dtype=torch.int64, device=self.device)
+        self._finalized = False
+
+    def _check_indices(self, idx: torch.Tensor) -> None:
+        if idx.numel() == 0:
+            return
+        self._bad.fill_(-1)   # all ones = no bad index
+        L = _lib()
+        L.call("mdkk_index_range", idx.data_ptr(), int(idx.numel()), self._n, self._bad.data_ptr(),
+               L.stream(self.device))
+        e = int(self._bad.item())
+        if e != -1:
+            raise IndexError(f"scatter index {int(idx[e].item())} out of range [0, {self._n})")
+
+    def add(self, indices, values, worker: int = 0) -> None:
+        """Accumulate ``values`` at first-axis ``indices`` on behalf of ``worker``."""
+        if self._finalized:
+            raise MemspaceError("accumulator already finalized")
+        idx = torch.as_tensor(np.asarray(indices) if not torch.is_tensor(indices) else indices)
+        idx = idx.to(device=self.device, dtype=torch.int64).reshape(-1).contiguous()
+        vals = torch.as_tensor(np.asarray(values, dtype=np.float64) if not torch.is_tensor(values) else values)
+        vals = vals.to(device=self.device, dtype=torch.float64).reshape(idx.numel(), self._width).contiguous()
+        self._check_indices(idx)
+        if isinstance(self.strategy, Atomic):
+            atomic_scatter(self._data, self._width, self._width, idx, vals)
+        elif isinstance(self.strategy, Serial):
+            self._pending[0].append((idx, vals))
+        else:
+            self._pending[worker % self.strategy.copies].append((idx, vals))
+
+    def finalize_device(self) -> torch.Tensor:
+        """Barrier: combine staged contributions; the dense result stays on the device."""
+        if self._finalized:
+            raise MemspaceError("accumulator already finalized")
+        self._finalized = True
+        if isinstance(self.strategy, Serial):
+            self._flush(self._data, self._pending[0])
+        elif isinstance(self.strategy, Duplicate):
+            for c, chunks in enumerate(self._pending):
+                self._flush(self._staging[c], chunks)
+            combine_copies(self._staging, self._data)
+            self._staging = None
+        self._pending = None
+        return self._data.view(self.target_shape) if self.target_shape else self._data
+
+    def finalize(self) -> np.ndarray:
+        """Barrier: combine staged contributions and return the dense (host) result."""
+        return self.finalize_device().cpu().numpy()
+
+    def _flush(self, target, chunks):
+        if not chunks:
+            return
+        idx = torch.cat([c[0] for c in chunks])
+        vals = torch.cat([c[1] for c in chunks])
+        ordered_scatter(target, self._width, self._width, idx, vals)
+
+
+def scatter_accumulate(acc: ScatterAccumulator, contributions) -> np.ndarray:
+    """Apply ``(index, value)`` contributions and finalize (mdkk/memspace.py:257-276):
+    Duplicate splits the list into one contiguous chunk per copy; Serial and
+    Atomic apply it in the given order."""
+    contributions = list(contributions)
+    if contributions:
+        idx = np.asarray([c[0] for c in contributions])
+        vals = np.asarray([c[1] for c in contributions])
+        copies = acc.strategy.copies
+        if copies <= 1 or len(contributions) < copies:
+            acc.add(idx, vals, worker=0)
+        else:
+            bounds = np.linspace(0, len(contributions), copies + 1).astype(int)
+            for w in range(copies):
+                lo, hi = bounds[w], bounds[w + 1]
+                if hi > lo:
+                    acc.add(idx[lo:hi], vals[lo:hi], worker=w)
+    return acc.finalize()

@@ -328,3 +328,29 @@ def any_needs_rebuild(lists: list[NeighborList]) -> bool:
         return False
     worst = float(torch.stack([t[0] for t in d2]).max().item())
     return math.sqrt(worst) > 0.5 * lists[0].skin
+
+
+def brute_force_pairs(pos, box: Box, cutoff: float, device=None) -> set[tuple[int, int]]:
+    """O(N^2) minimum-image pair set, unordered index pairs (i, j), i < j (mdkk/neighbor.py:234-245).
+
+    The test oracle the reference exports, evaluated on the GPU in row blocks
+    with the reference's operations (min image L*floor(d/L + 0.5), r^2 in the
+    einsum order (dx^2 + dz^2) + dy^2, strict <)."""
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    x = torch.as_tensor(np.asarray(pos, dtype=np.float64), device=dev)
+    n = int(x.shape[0])
+    L = torch.as_tensor(np.asarray(box.lengths, dtype=np.float64), device=dev)
+    per = torch.as_tensor(np.asarray(box.periodic, dtype=bool), device=dev)
+    out: set[tuple[int, int]] = set()
+    cut2 = float(cutoff) * float(cutoff)
+    step = max(1, (1 << 24) // max(n, 1))
+    for lo in range(0, n, step):
+        hi = min(n, lo + step)
+        d = x[None, :, :] - x[lo:hi, None, :]
+        d = torch.where(per, d - L * torch.floor(d / L + 0.5), d)
+        r2 = (d[..., 0] * d[..., 0] + d[..., 2] * d[..., 2]) + d[..., 1] * d[..., 1]
+        j = torch.arange(n, device=dev)[None, :]
+        i = torch.arange(lo, hi, device=dev)[:, None]
+        hit = torch.nonzero((r2 < cut2) & (j > i)).cpu().numpy()
+        out.update((int(a) + lo, int(b)) for a, b in hit)
+    return out

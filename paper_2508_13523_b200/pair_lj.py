@@ -3,8 +3,9 @@
 `PairParams`, `LJCut`, `PairResult`, `u2_lj` and `compute_pair` keep the
 reference signatures (mdkk/pair_lj.py:29-179).  `compute_pair` launches the
 sm_100a kernel `mdkk_lj_force` per rank — owner-writes for full lists, FP64
-atomics for half lists — then the device reverse comm; energy and the six
-virial components come from a deterministic on-device reduction.
+atomics for half lists (or the Serial / Duplicate ScatterAccumulator
+strategies, `mdkk_lj_force_strategy`) — then the device reverse comm; energy
+and the six virial components come from a deterministic on-device reduction.
 """
 
 from __future__ import annotations
@@ -14,6 +15,7 @@ import torch
 
 from . import _lib
 from .domain import RankedSystem
+from .memspace import STRATEGIES, Duplicate, Serial, combine_copies, ordered_scatter, worker_count
 from .neighbor import STYLES, NeighborList
 
 
@@ -51,6 +53,25 @@ class LJCut:
     def __init__(self, params: PairParams):
         self.params = params
         self.r_c = params.r_c
+
+    def pair_energy_force(self, r2):
+        """(e, fpair) on squared distances, all < r_c^2 (mdkk/pair_lj.py:81-91).
+
+        Element-wise on whatever it is given: a numpy array returns numpy
+        arrays, a device tensor stays on the device.  The force engine does not
+        call this; csrc/lj.cu evaluates the same expressions in the same order."""
+        is_t = torch.is_tensor(r2)
+        x = r2 if is_t else np.asarray(r2, dtype=np.float64)
+        if x.numel() if is_t else x.size:
+            if float(x.min()) <= 0.0:
+                raise PairError("coincident atoms (r = 0)")
+        p = self.params
+        s2 = (p.sigma * p.sigma) / x
+        s6 = s2 * s2 * s2
+        s12 = s6 * s6
+        e = 4.0 * p.epsilon * (s12 - s6)
+        fp = 24.0 * p.epsilon * (2.0 * s12 - s6) / x
+        return e, fp
 
 
 class PairResult:
@@ -91,7 +112,7 @@ class PairResult:
 
 def lj_force_rank(store, nl: NeighborList, params: PairParams, ev: torch.Tensor, flags: torch.Tensor,
                   zero: bool = True, virial: bool = True, mode: str = "atom", gate: torch.Tensor | None = None,
-                  gate_limit: float = 0.0, integ: dict | None = None) -> None:
+                  gate_limit: float = 0.0, integ: dict | None = None, strategy=None) -> None:
     """One rank's kernel launch (no host sync).
 
     Ghost force rows are zero outside a force evaluation (migrate zeroes all
@@ -129,11 +150,48 @@ def lj_force_rank(store, nl: NeighborList, params: PairParams, ev: torch.Tensor,
             pend[0].data_ptr() if pend is not None else None, nl.alloc_cap, _lib.stream(dev)),
             "mdkk_lj_force_gated")
         return
+    if nl.style == "half" and isinstance(strategy, (Serial, Duplicate)):
+        _half_with_strategy(store, nl, params, ev, flags, virial, strategy)
+        return
     fn = "mdkk_lj_force_neighbor" if mode == "neighbor" else "mdkk_lj_force"
     _lib.check(getattr(_lib.lib(), fn)(
         _lib.ctx(dev), store.x.data_ptr(), store.n_local, nl.table_dev.data_ptr(), nl.counts_dev.data_ptr(),
         nl.alloc_cap, STYLES[nl.style], int(nl.newton), int(virial), params.epsilon, params.sigma, params.r_c,
         store.f.data_ptr(), ev.data_ptr(), flags.data_ptr(), _lib.stream(dev)), fn)
+
+
+def _half_with_strategy(store, nl: NeighborList, params: PairParams, ev, flags, virial: bool, strategy) -> None:
+    """Half-list force with the partner writes deconflicted by `strategy`
+    (mdkk/pair_lj.py:138-165 through ScatterAccumulator, mdkk/memspace.py:198-254).
+
+    Duplicate: the kernel's REDs go into `copies` staging copies (copy = block %
+    copies), combined in a fixed order into f.  Serial: the kernel stores own rows
+    and stages every partner contribution per table entry (no atomics); they are
+    applied in (row, slot) order by the ordered scatter -- run-to-run deterministic.
+    The strategy kernels run the atom-parallel schedule."""
+    dev = store.device
+    L = _lib.lib()
+    f = store.f
+    if isinstance(strategy, Duplicate):
+        stage = torch.zeros((strategy.copies,) + tuple(f.shape), dtype=torch.float64, device=dev)
+        _lib.check(L.mdkk_lj_force_strategy(
+            _lib.ctx(dev), store.x.data_ptr(), store.n_local, nl.table_dev.data_ptr(), nl.counts_dev.data_ptr(),
+            nl.alloc_cap, int(nl.newton), int(virial), params.epsilon, params.sigma, params.r_c, f.data_ptr(),
+            ev.data_ptr(), flags.data_ptr(), 1, stage.data_ptr(), int(f.numel()), strategy.copies,
+            _lib.stream(dev)), "mdkk_lj_force_strategy")
+        combine_copies(stage, f)
+        return
+    ncl, cap = nl.table_dev.shape[0], nl.alloc_cap
+    stage = torch.zeros((ncl, cap, 32, 4), dtype=torch.float64, device=dev)
+    _lib.check(L.mdkk_lj_force_strategy(
+        _lib.ctx(dev), store.x.data_ptr(), store.n_local, nl.table_dev.data_ptr(), nl.counts_dev.data_ptr(),
+        cap, int(nl.newton), int(virial), params.epsilon, params.sigma, params.r_c, f.data_ptr(), ev.data_ptr(),
+        flags.data_ptr(), 2, stage.data_ptr(), 0, 1, _lib.stream(dev)), "mdkk_lj_force_strategy")
+    n = store.n_local * cap
+    ent = stage.permute(0, 2, 1, 3).reshape(-1, 4)[:n]           # (row, slot) order
+    tab = nl.table_dev.permute(0, 2, 1).reshape(-1)[:n]
+    used = ent[:, 3] != 0
+    ordered_scatter(f, 4, 3, tab[used].long(), ent[used, :3].contiguous())
 
 
 def compute_pair(kernel, system: RankedSystem, lists: list[NeighborList], mode: str = "atom", strategy=None,
@@ -142,14 +200,22 @@ def compute_pair(kernel, system: RankedSystem, lists: list[NeighborList], mode: 
 
     `mode` picks the GPU schedule: "atom" = one thread per owned atom,
     "neighbor" = a team of lanes per atom over its list (the reference's
-    mid-row split).  `strategy` / `n_workers` are accepted for signature
-    parity; the write-deconfliction is fixed by the list style (owner writes
-    for full lists, FP64 atomics for half lists).  `check=False` (engine-internal) skips the
+    mid-row split).  `strategy` deconflicts the half list's partner writes
+    (Serial = staged + ordered, deterministic; Duplicate = staging copies;
+    Atomic = FP64 RED; None = Atomic, the engine default); full lists write
+    owner rows only, so every strategy is the same owner-write kernel there.
+    `n_workers` (capped by MDKK_THREADS as in mdkk/parallel.py) sizes a
+    Duplicate without an explicit copy count.  `check=False` (engine-internal) skips the
     synchronous stale-list and coincident-atom checks; the error word is then
     read when the result is first inspected.
     """
     if mode not in ("atom", "neighbor"):
         raise PairError(f"unknown execution mode {mode!r}")
+    if strategy is not None and not isinstance(strategy, STRATEGIES):
+        raise PairError(f"unknown scatter strategy {strategy!r}")
+    workers = worker_count(n_workers)
+    if isinstance(strategy, Duplicate) and n_workers is not None:
+        strategy = Duplicate(min(strategy.copies, workers))
     params = kernel.params
     dev = system.device
     evs = torch.zeros((len(system.stores), 7), dtype=torch.float64, device=dev)
@@ -163,7 +229,7 @@ def compute_pair(kernel, system: RankedSystem, lists: list[NeighborList], mode: 
             nl.check_current()
         store.to_device()
         half |= nl.style == "half"
-        lj_force_rank(store, nl, params, evs[k], flags, mode=mode)
+        lj_force_rank(store, nl, params, evs[k], flags, mode=mode, strategy=strategy)
         store.device_wrote(force=True)
     if half and any(s.n_ghost for s in system.stores):
         system.reverse_comm()

@@ -27,6 +27,36 @@ class SnapError(RuntimeError):
     pass
 
 
+def cutoff_switch(r, r_c: float):
+    """f_c(r) = (1 + cos(pi r / r_c)) / 2 and its derivative (mdkk/snap/compute.py:27-32).
+
+    Element-wise on the input's own side: numpy in, numpy out; a device tensor
+    stays on the device.  The kernels evaluate the same switch inline
+    (snap_common.cuh pair_geometry)."""
+    if torch.is_tensor(r):
+        x = r.to(torch.float64)
+        return 0.5 * (1.0 + torch.cos(np.pi * x / r_c)), -np.pi / (2.0 * r_c) * torch.sin(np.pi * x / r_c)
+    x = np.asarray(r, dtype=np.float64)
+    return 0.5 * (1.0 + np.cos(np.pi * x / r_c)), -np.pi / (2.0 * r_c) * np.sin(np.pi * x / r_c)
+
+
+def pair_u_flat(a, b, twojmax: int, device=None) -> np.ndarray:
+    """Unweighted levels u_0..u_2J of each (a, b), flattened to (n, n_flat)
+    (mdkk/snap/compute.py:165-184), computed on the GPU (mdkk_snap_pair_u, the
+    reference's four-term recursion; (a, b) need not be unitary)."""
+    a = np.atleast_1d(np.asarray(a, dtype=np.complex128))
+    b = np.atleast_1d(np.asarray(b, dtype=np.complex128))
+    twojmax = int(twojmax)
+    nf = sum((t + 1) ** 2 for t in range(twojmax + 1))
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    at = torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    bt = torch.from_numpy(np.ascontiguousarray(b)).to(dev)
+    out = torch.empty((max(len(a), 1), nf), dtype=torch.complex128, device=dev)
+    _lib.check(_lib.lib().mdkk_snap_pair_u(len(a), twojmax, at.data_ptr(), bt.data_ptr(), out.data_ptr(),
+                                           _lib.stream(dev)), "mdkk_snap_pair_u")
+    return out[: len(a)].cpu().numpy()
+
+
 class NeighborMap:
     """The pairs of a full list with r < r_c (mdkk/snap/compute.py:66-119).
 
@@ -81,6 +111,18 @@ class NeighborMap:
     @property
     def n_pairs(self) -> int:
         return int(self.device_arrays()["rows"].shape[0])
+
+    def deriv_params(self, sel: slice):
+        """(da, db), each (n, 3) complex, for one pair block (mdkk/snap/compute.py:98-102),
+        from the device geometry the force kernels use (mdkk_snap_pair_grads)."""
+        d = self.device_arrays()
+        dr = d["dr"][sel].contiguous()
+        n = int(dr.shape[0])
+        da = torch.empty((max(n, 1), 3), dtype=torch.complex128, device=dr.device)
+        db = torch.empty_like(da)
+        _lib.check(_lib.lib().mdkk_snap_pair_grads(n, dr.data_ptr(), self.r_c, da.data_ptr(), db.data_ptr(),
+                                                   _lib.stream(dr.device)), "mdkk_snap_pair_grads")
+        return da[:n].cpu().numpy(), db[:n].cpu().numpy()
 
     def __getattr__(self, name):
         if name in NeighborMap._FIELDS:
@@ -270,6 +312,24 @@ def _tiles(state: SnapState):
 def _u_at(state: SnapState, a0: int) -> int:
     """Device address of atom a0's U entries in the state's layout."""
     return state.U_dev.data_ptr() + 16 * (a0 if state._lay else a0 * state.index.n_flat)
+
+
+def compute_zi(state: SnapState, it: int) -> np.ndarray:
+    """Dense Z block of coupled triple `it` for every atom, (n, tj+1, tj+1)
+    (mdkk/snap/compute.py:343-351; an oracle helper there): Z[iz] += c U[iu1] U[iu2]
+    over the triple's terms, formed on the device from the resident U."""
+    tt = state.tables.terms[it]
+    tj = tt.tj
+    n = state.n_atoms
+    state.U.sync("b")
+    u = state.U_dev[:, :n].T if state._lay else state.U_dev[:n]
+    dev = state.device
+    iz = torch.from_numpy(tt.iz - state.index.block_offset[tj]).to(dev)
+    i1, i2 = torch.from_numpy(tt.iu1).to(dev), torch.from_numpy(tt.iu2).to(dev)
+    c = torch.from_numpy(tt.coeff).to(dev).to(torch.complex128)
+    z = torch.zeros(((tj + 1) * (tj + 1), max(n, 1)), dtype=torch.complex128, device=dev)
+    z.index_add_(0, iz, (c[:, None] * u[:, i1].T * u[:, i2].T))
+    return z[:, :n].T.reshape(n, tj + 1, tj + 1).cpu().numpy()
 
 
 def compute_bi_complex(state: SnapState) -> np.ndarray:

@@ -91,14 +91,53 @@ def clebsch_gordan(tj1: int, tm1: int, tj2: int, tm2: int, tj: int, tm: int) -> 
     return math.copysign(math.sqrt(float(acc * acc * pref)), float(acc))
 
 
+class TripleTerms:
+    """Flattened contraction terms of one (tj, tj1, tj2) triple (mdkk/snap/coupling.py:69-91).
+
+    Term k couples U[iu1[k]] * U[iu2[k]] into slot iz[k] of the tj block with
+    weight coeff[k] = C(m1, m2) C(m1', m2'); `order_*` / `starts_*` /
+    `unique_*` group the terms by iz, iu1 and iu2 (stable sorts, reduceat
+    boundaries), as in the reference.  Host-side setup data: the device kernels
+    consume the Z-list built from these terms (`device_product_list`).
+    Iterating yields (iz, iu1, iu2, coeff).
+    """
+
+    def __init__(self, tj: int, tj1: int, tj2: int, iz, iu1, iu2, coeff):
+        self.tj, self.tj1, self.tj2 = int(tj), int(tj1), int(tj2)
+        self.iz = np.asarray(iz, dtype=np.int64)
+        self.iu1 = np.asarray(iu1, dtype=np.int64)
+        self.iu2 = np.asarray(iu2, dtype=np.int64)
+        self.coeff = np.asarray(coeff, dtype=np.float64)
+        self.n_terms = len(self.coeff)
+        for key in ("iz", "iu1", "iu2"):
+            idx = getattr(self, key)
+            order = np.argsort(idx, kind="stable")
+            srt = idx[order]
+            firsts = np.flatnonzero(np.concatenate([[True], srt[1:] != srt[:-1]])) if len(srt) else \
+                np.zeros(0, np.int64)
+            setattr(self, f"order_{key}", order)
+            setattr(self, f"starts_{key}", firsts)
+            setattr(self, f"unique_{key}", srt[firsts])
+
+    def __iter__(self):
+        return iter((self.iz, self.iu1, self.iu2, self.coeff))
+
+    def __getitem__(self, k):
+        return (self.iz, self.iu1, self.iu2, self.coeff)[k]
+
+    def __len__(self):
+        return 4
+
+
 class CouplingTables:
-    """Per-triple term lists (iz, iu1, iu2, coeff) for every coupled triple (mdkk/snap/coupling.py:136)."""
+    """CG blocks and per-triple `TripleTerms` for every coupled triple (mdkk/snap/coupling.py:94-133)."""
 
     def __init__(self, jmax):
         self.index = QuantumIndex(jmax)
         self.triples = self.index.triples()
         off = self.index.block_offset
-        self.terms = []
+        self.cg = {}      # (tj1, tj2, tj) -> cg[p1, p2]
+        self.terms = []   # TripleTerms, parallel to self.triples
         for (tj, tj1, tj2) in self.triples:
             cg = np.zeros((tj1 + 1, tj2 + 1))
             for p1 in range(tj1 + 1):
@@ -113,8 +152,10 @@ class CouplingTables:
             p, q = p1 + p2 - sh, q1 + q2 - sh
             c = cg[p1, p2] * cg[q1, q2]
             k = (p >= 0) & (p <= tj) & (q >= 0) & (q <= tj) & (c != 0.0)
-            self.terms.append((off[tj] + p[k] * (tj + 1) + q[k], off[tj1] + p1[k] * (tj1 + 1) + q1[k],
-                               off[tj2] + p2[k] * (tj2 + 1) + q2[k], c[k]))
+            self.cg[(tj1, tj2, tj)] = cg
+            self.terms.append(TripleTerms(tj, tj1, tj2, off[tj] + p[k] * (tj + 1) + q[k],
+                                          off[tj1] + p1[k] * (tj1 + 1) + q1[k],
+                                          off[tj2] + p2[k] * (tj2 + 1) + q2[k], c[k]))
 
     @property
     def n_terms(self) -> int:

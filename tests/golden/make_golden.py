@@ -198,8 +198,100 @@ def qeq_fixtures():
     np.savez_compressed(os.path.join(HERE, "qeq.npz"), **out)
 
 
+def canonical_keys(pairs, n_atoms):
+    """Directed entries -> sorted int64 keys ((gid_i·n + gid_j)·27 + shift code).
+
+    `pairs` is `directed_set`'s (gid_i, gid_j, sx, sy, sz, rank, 2w, wj) array.
+    The test side (tests/test_parity_scale_gpu.py) encodes its own lists the
+    same way, so a SHA-256 of the sorted key bytes pins the exact directed set.
+    """
+    code = (pairs[:, 2] + 1) * 9 + (pairs[:, 3] + 1) * 3 + (pairs[:, 4] + 1)
+    keys = (pairs[:, 0] * n_atoms + pairs[:, 1]) * 27 + code
+    keys.sort()
+    return keys
+
+
+def _set_digest(system, lists, n_atoms):
+    import hashlib
+    pairs = directed_set(system, lists)
+    keys = canonical_keys(pairs, n_atoms)
+    counts = np.zeros(n_atoms, np.int64)
+    np.add.at(counts, pairs[:, 0], 1)
+    return (hashlib.sha256(keys.astype("<i8").tobytes()).hexdigest(), len(keys),
+            counts.astype(np.uint8))
+
+
+def lj_sets(cells, tag, n_ranks_list=(1,), sub=997, counts_every=1):
+    """Exact directed neighbour sets at the benchmarked LJ configs (C1 32k / C2 2M).
+
+    fcc rho* 0.8442 + N(0, 0.02) jitter from default_rng(1), rc 2.5, skin 0.3;
+    full/newton-off and half/newton-on lists; the set's SHA-256 and per-gid row
+    counts, plus the step-0 E, W, max|F|, sum F and a 1/`sub` force subsample.
+    """
+    import hashlib
+    pos, box = lattice_positions("fcc", 0.8442, cells)
+    pos = pos + np.random.default_rng(1).normal(0.0, 0.02, pos.shape)
+    n = len(pos)
+    out = {"lengths": box.lengths, "n": n}
+    for style, newton in (("full", False), ("half", True)):
+        for n_ranks in n_ranks_list:
+            t0 = time.time()
+            system = RankedSystem.distribute(box, n_ranks, pos, np.zeros_like(pos))
+            lists = build_all(system, 2.5, 0.3, style=style, newton=newton)
+            t1 = time.time()
+            digest, n_entries, counts = _set_digest(system, lists, n)
+            res = compute_pair(LJCut(PairParams(1.0, 1.0, 2.5)), system, lists)
+            k = f"{style}_{n_ranks}"
+            out[f"sha_{k}"] = digest
+            out[f"nentries_{k}"] = n_entries
+            out[f"counts_{k}"] = counts[::counts_every]
+            out[f"counts_sha_{k}"] = hashlib.sha256(counts.tobytes()).hexdigest()
+            out[f"cap_{k}"] = np.array([nl.max_neighbors for nl in lists])
+            out[f"nghost_{k}"] = np.array([s.n_ghost for s in system.stores])
+            out[f"E_{k}"] = res.energy
+            out[f"W_{k}"] = res.virial
+            out[f"Fmax_{k}"] = float(np.abs(res.forces).max())
+            out[f"Fsum_{k}"] = res.forces.sum(axis=0)
+            out[f"F_sub_{k}"] = res.forces[::sub]
+            print(f"{tag} {k}: build {t1 - t0:.1f}s total {time.time() - t0:.1f}s "
+                  f"entries {n_entries} E {res.energy!r}", flush=True)
+            del system, lists, res
+    np.savez_compressed(os.path.join(HERE, f"{tag}.npz"), **out)
+
+
+def snap_c4_run():
+    """C4: 2,000 bcc, 2J=8, rc 4.73, skin 0.3, beta linspace(0.05, 0.1, 55),
+    m 1, T 0.01 seed 4928459, dt 0.001, 100 NVE steps through the reference's own
+    Simulation (bcc sites built here in the reference's cell-major x basis order,
+    mdkk/driver/simulation.py:156-178, because mdkk has no bcc lattice)."""
+    from mdkk.driver.simulation import Simulation, SnapStyle, seeded_velocities
+    a = 3.1803
+    grid = np.stack(np.meshgrid(*[np.arange(10)] * 3, indexing="ij"), -1).reshape(-1, 3).astype(float)
+    basis = np.array([[0, 0, 0], [0.5, 0.5, 0.5]])
+    pos = (grid[:, None, :] + basis[None]).reshape(-1, 3) * a
+    sim = Simulation(RunConfig(list_style="full", newton=False), log=lambda *_: None)
+    sim.box = Box((10 * a,) * 3)
+    sim._positions = pos
+    sim._velocities = seeded_velocities(len(pos), 0.01, 1.0, 4928459)
+    sim.style = SnapStyle(4.73, 4.0, np.linspace(0.05, 0.1, 55))
+    sim.dt = 0.001
+    sim.thermo_every = 10
+    t0 = time.time()
+    res = sim.run_nve(100)
+    print(f"C4 run: {time.time() - t0:.1f}s", flush=True)
+    out = {"rows": np.array(res.rows), "final_pos_sub": res.snapshots[100][::7],
+           "pos10_sub": res.snapshots[10][::7]}
+    np.savez_compressed(os.path.join(HERE, "snap_run.npz"), **out)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["lj_small", "lj_32k", "snap", "runs", "qeq"]
+    if "lj_sets_c1" in which:
+        lj_sets((20, 20, 20), "lj_c1_sets", n_ranks_list=(1, 8), sub=37)
+    if "lj_sets_c2" in which:
+        lj_sets((80, 80, 80), "lj_c2_sets", sub=997, counts_every=97)
+    if "snap_run" in which:
+        snap_c4_run()
     if "lj_small" in which:
         lj_small()
     if "lj_32k" in which:

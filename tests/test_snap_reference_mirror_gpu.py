@@ -209,3 +209,98 @@ def test_state_validation(gpu):
     with pytest.raises(SnapError):
         SnapState(tables, 4, np.zeros(5), layout="c")
     assert compute_energy(SnapState(tables, 0, np.zeros(5))) == 0.0
+
+
+# ------------------------------------------- exported helpers (mdkk/snap/__init__.py:3-21)
+def test_pair_u_flat_unitary_seed_and_oracle(gpu):
+    """pair_u_flat: unitary blocks for unit (a, b) (mdkk tests/test_snap.py:247-258), the seed
+    matrix at level 1 (:261-269), and the four-term recursion for arbitrary (a, b)."""
+    from oracle import snap as osnap
+    from paper_2508_13523_b200.snap import QuantumIndex, pair_u_flat
+    rng = np.random.default_rng(7)
+    n = 6
+    th = rng.uniform(0, np.pi, n)
+    a = np.cos(th / 2) * np.exp(1j * rng.uniform(0, 2 * np.pi, n))
+    b = np.sin(th / 2) * np.exp(1j * rng.uniform(0, 2 * np.pi, n))
+    qi = QuantumIndex(4)
+    flat = pair_u_flat(a, b, qi.twojmax)
+    for tj in range(qi.twojmax + 1):
+        blk = flat[:, qi.block(tj)].reshape(n, tj + 1, tj + 1)
+        assert np.allclose(np.einsum("npq,nrq->npr", blk, np.conj(blk)), np.eye(tj + 1), atol=1e-12)
+    a1, b1 = np.array([0.6 + 0.3j]), np.array([0.2 - 0.7j])
+    lvl = pair_u_flat(a1, b1, 2)
+    assert np.array_equal(lvl[0, 1:5].reshape(2, 2), np.array([[np.conj(a1[0]), -np.conj(b1[0])], [b1[0], a1[0]]]))
+    assert lvl[0, 0] == 1.0 + 0.0j
+    a2 = rng.normal(size=50) + 1j * rng.normal(size=50)
+    b2 = rng.normal(size=50) + 1j * rng.normal(size=50)
+    ref, _ = osnap.pair_levels(a2, b2, 8)
+    got = pair_u_flat(a2, b2, 8)
+    assert np.abs(got - ref).max() <= 1e-13 * np.abs(ref).max()
+
+
+def test_cutoff_switch_endpoints_and_slope(gpu):
+    """mdkk tests/test_snap.py:272-284."""
+    from paper_2508_13523_b200.snap import cutoff_switch
+    fc, dfc = cutoff_switch(np.array([0.0, 1.5, 3.0]), 3.0)
+    assert fc[0] == pytest.approx(1.0) and fc[1] == pytest.approx(0.5) and fc[2] == pytest.approx(0.0, abs=1e-16)
+    assert dfc[0] == pytest.approx(0.0, abs=1e-16) and dfc[2] == pytest.approx(0.0, abs=1e-15)
+    r, h = np.linspace(0.3, 2.7, 9), 1e-6
+    fp, _ = cutoff_switch(r + h, 3.0)
+    fm, _ = cutoff_switch(r - h, 3.0)
+    _, d = cutoff_switch(r, 3.0)
+    assert np.allclose((fp - fm) / (2 * h), d, atol=1e-8)
+
+
+def test_zi_route_consistent_with_descriptors(gpu):
+    """compute_zi: Re sum Z conj(U) per triple == B (mdkk tests/test_snap.py:348-361)."""
+    from paper_2508_13523_b200.snap import compute_bi, compute_zi
+    for layout in ("a", "b"):
+        _, _, states, _ = _pipeline(_cluster(8, 17), BOX_L, 1, _beta_for(1), layout=layout)
+        state = states[0]
+        bi = compute_bi(state)
+        u = state.u_view()
+        qi = state.index
+        for it, (tj, _, _) in enumerate(state.tables.triples):
+            z = compute_zi(state, it)
+            ublk = u[:, qi.block(tj)].reshape(len(u), tj + 1, tj + 1)
+            via_z = np.einsum("npq,npq->n", z, np.conj(ublk)).real
+            assert np.allclose(via_z, bi[:, it], rtol=1e-12, atol=1e-13)
+
+
+def test_triple_terms_groupings(gpu):
+    """TripleTerms (mdkk/snap/coupling.py:69-91): the grouping orders reproduce the terms."""
+    from paper_2508_13523_b200.snap import TripleTerms, make_coupling_tables
+    tables = make_coupling_tables(2)
+    for tt in tables.terms:
+        assert isinstance(tt, TripleTerms) and tt.n_terms == len(tt.coeff)
+        for key in ("iz", "iu1", "iu2"):
+            idx = getattr(tt, key)
+            srt = idx[getattr(tt, f"order_{key}")]
+            assert np.all(np.diff(srt) >= 0)
+            assert np.array_equal(srt[getattr(tt, f"starts_{key}")], getattr(tt, f"unique_{key}"))
+        assert tables.cg[(tt.tj1, tt.tj2, tt.tj)].shape == (tt.tj1 + 1, tt.tj2 + 1)
+
+
+def test_neighbor_map_deriv_params_match_oracle(gpu):
+    """NeighborMap.deriv_params (mdkk/snap/compute.py:98-102) vs the analytic gradients."""
+    from oracle import snap as osnap
+    from paper_2508_13523_b200 import Box, RankedSystem, build_all
+    from paper_2508_13523_b200.snap import build_neighbor_map
+    pos = _cluster(12, 5)
+    system = RankedSystem.distribute(Box((BOX_L,) * 3), 1, pos, np.zeros_like(pos))
+    (nl,) = build_all(system, R_C, 0.2, style="full", newton=False)
+    nmap = build_neighbor_map(system.stores[0], nl, R_C)
+    sel = slice(1, nmap.n_pairs - 1)
+    da, db = nmap.deriv_params(sel)
+    dr = nmap.dr[sel]
+    r, a, b, _, _, z0, r0 = osnap.pair_params(dr, R_C)
+    rda, rdb = osnap.pair_grads(dr, r, R_C, a, b, z0, r0)
+    assert np.allclose(da, rda, rtol=1e-12, atol=1e-13) and np.allclose(db, rdb, rtol=1e-12, atol=1e-13)
+
+
+def test_brute_force_pairs_matches_oracle(gpu):
+    """brute_force_pairs (mdkk/neighbor.py:234-245; mdkk tests/test_neighbor.py:126-128)."""
+    from oracle import md
+    from paper_2508_13523_b200 import Box, brute_force_pairs
+    pos, lengths = md.random_config(300, 0.8, seed=9)
+    assert brute_force_pairs(pos, Box(lengths), 1.6) == md.pair_set_brute(pos, lengths, 1.6)
