@@ -102,6 +102,13 @@ class CudaOps:
             _lib.check(_lib.lib().mdkk_fold_add(f.data_ptr(), idx.data_ptr(), buf.data_ptr(), n, self._s()),
                        "mdkk_fold_add")
 
+    def fold_ordered(self, f, idx, buf, n):
+        """As fold, but each owner row takes its contributions one by one in lane order
+        (no atomics: the Serial strategy's deterministic reverse comm)."""
+        if n:
+            from .memspace import ordered_scatter
+            ordered_scatter(f, 4, 3, idx[:n].long(), buf[:n, :3].contiguous())
+
     def gather_rows(self, src, idx, n, out):
         if n:
             _lib.check(_lib.lib().mdkk_gather_rows4(src.data_ptr(), idx.data_ptr(), n, out.data_ptr(), self._s()),
@@ -369,10 +376,12 @@ class DistSystem:
         if s.n_ghost:
             s.device_wrote(pos=True)
 
-    def reverse_comm(self) -> None:
-        """Ghost forces back to owners, folded with atomics; ghost rows zeroed (mdkk/domain.py:307-322)."""
+    def reverse_comm(self, ordered: bool = False) -> None:
+        """Ghost forces back to owners, folded with atomics; ghost rows zeroed (mdkk/domain.py:307-322).
+        `ordered` (the Serial strategy): a deterministic ordered fold instead of atomics."""
         s = self.store
         s.to_device()
+        fold = self.ops.fold_ordered if ordered and hasattr(self.ops, "fold_ordered") else self.ops.fold
         sends, recvs, folds = [], [], []
         for ln in self.recv_lanes:
             if ln.src != self.rank:
@@ -380,14 +389,14 @@ class DistSystem:
         for ln in self.send_lanes:
             if ln.dst == self.rank:
                 rl = next(r for r in self.recv_lanes if r.src == self.rank)
-                self.ops.fold(s.f, ln.idx, s.f[rl.start:], ln.count)
+                fold(s.f, ln.idx, s.f[rl.start:], ln.count)
             else:
                 buf = torch.empty((ln.count, 4), dtype=torch.float64, device=self.device)
                 recvs.append((buf, ln.dst))
                 folds.append((ln, buf))
         self._p2p(sends, recvs)
         for ln, buf in folds:
-            self.ops.fold(s.f, ln.idx, buf, ln.count)
+            fold(s.f, ln.idx, buf, ln.count)
         if s.n_ghost:
             s.f[s.n_local:s.n_total].zero_()
         s.device_wrote(force=True)

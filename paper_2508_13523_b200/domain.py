@@ -559,13 +559,23 @@ class RankedSystem:
             if s.n_ghost:
                 s.device_wrote(pos=True)
 
-    def reverse_comm(self) -> None:
-        """Fold ghost forces onto owners, zero ghost rows (mdkk/domain.py:307-322)."""
+    def reverse_comm(self, ordered: bool = False) -> None:
+        """Fold ghost forces onto owners, zero ghost rows (mdkk/domain.py:307-322).
+
+        FP64 RED folds; `ordered` (the Serial strategy) folds each owner row's
+        contributions one by one in lane order instead -- deterministic, like the
+        reference's np.add.at."""
         lib, stream = _lib.lib(), _lib.stream(self.device)
         for s in self.stores:
             s.to_device()
         for ln in self.lanes:
             s, d = self.stores[ln.src], self.stores[ln.dst]
+            if ordered:
+                from .memspace import ordered_scatter
+                if ln.count:
+                    ordered_scatter(s.f, 4, 3, ln.idx[: ln.count].long(),
+                                    d.f[ln.start:ln.start + ln.count, :3].contiguous())
+                continue
             _lib.check(lib.mdkk_fold_add(s.f.data_ptr(), ln.idx.data_ptr(), d.f[ln.start:].data_ptr(),
                                          ln.count, stream), "mdkk_fold_add")
         for s in self.stores:

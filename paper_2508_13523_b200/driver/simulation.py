@@ -111,7 +111,7 @@ class LJStyle:
                           strategy=config.make_strategy())
             half |= nl.style == "half"
         if half:   # collective in the distributed system: every rank calls it
-            system.reverse_comm()
+            system.reverse_comm(ordered=config.strategy == "serial")
         for s in system.stores:
             s.device_wrote(force=True, vel=integ is not None)
         return (evs[:, 0].sum() if len(system.stores) > 1 else evs[0, 0]), flags

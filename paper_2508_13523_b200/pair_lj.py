@@ -232,7 +232,10 @@ def compute_pair(kernel, system: RankedSystem, lists: list[NeighborList], mode: 
         lj_force_rank(store, nl, params, evs[k], flags, mode=mode, strategy=strategy)
         store.device_wrote(force=True)
     if half and any(s.n_ghost for s in system.stores):
-        system.reverse_comm()
+        if isinstance(strategy, Serial):
+            system.reverse_comm(ordered=True)
+        else:
+            system.reverse_comm()
     if prev is not None:
         for s, p in zip(system.stores, prev):
             s.f[: s.n_local] += p[: s.n_local]
