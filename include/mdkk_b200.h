@@ -336,6 +336,12 @@ int mdkk_snap_pair_u(int n_pairs, int twojmax, const double* a, const double* b,
 /* NeighborMap.deriv_params (mdkk/snap/compute.py:48-63,98-102): da, db complex128 [n][3]
  * from dr f64 [n][3]. */
 int mdkk_snap_pair_grads(int n_pairs, const double* dr, double rc, double* da, double* db, void* stream);
+/* Per-pair force contraction of staged derivatives, no scatter (the drop-in's
+ * compute_fused_deidrj / compute_deidrj over the reference's pair arrays,
+ * mdkk/snap/compute.py:390-436): t_out[p][d] = Re sum_f Y[rows[p]][f] conj(wdu[p][d][f]),
+ * Y complex128 [n][n_flat] (layout "a"), wdu complex128 [n_pairs][3][n_flat]. */
+int mdkk_snap_pair_dedr(mdkk_snap* snap, int n_pairs, const int* rows, const double* Y, const double* wdu,
+                        double* t_out, void* stream);
 int mdkk_snap_bi(mdkk_snap* snap, const double* U, int n_local, const double* coef, const int* code, const int* tri,
                  const int* chunk, int n_tri, double* B, int layout, int ldu, void* stream);
 int mdkk_snap_bi_warps(void);

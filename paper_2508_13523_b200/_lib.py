@@ -81,6 +81,7 @@ SIGNATURES = {
     "mdkk_snap_bi_warps": [],
     "mdkk_snap_pair_u": [_i, _i, _p, _p, _p, _p],
     "mdkk_snap_pair_grads": [_i, _p, _d, _p, _p, _p],
+    "mdkk_snap_pair_dedr": [_p, _i, _p, _p, _p, _p, _p],
     "mdkk_qeq_offsets": [_p, _p, _i, _i, _p, _p, _p],
     "mdkk_qeq_build": [_p, _i, _p, _p, _i, _p, _p, _d, _d, _d, _p, _p, _p, _p],
     "mdkk_qeq_spmv": [_p, _p, _p, _p, _p, _i, _p, _p, _p, _p, _p, _p],

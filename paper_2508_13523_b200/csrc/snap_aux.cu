@@ -200,6 +200,33 @@ __global__ void k_snap_deidrj_staged(int n_pairs, int nf, const int* __restrict_
     }
 }
 
+// Per-pair contraction only (no scatter): t[p][d] = Re sum_f Y[row][f] conj(wdu[p][d][f]).
+// The caller applies F[row] += t, F[col] -= t with the ordered scatter
+// (np.add.at / np.subtract.at order, mdkk/snap/compute.py:405-408): deterministic.
+__global__ void k_snap_pair_dedr(int n_pairs, int nf, const int* __restrict__ rows, const double2* __restrict__ Y,
+                                 const double2* __restrict__ wdu, double* __restrict__ t_out) {
+    const int lane = threadIdx.x & 31;
+    const long long p = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (p >= n_pairs) return;
+    const double2* y = Y + (long long)rows[p] * nf;
+    const double2* w = wdu + p * 3 * nf;
+    double t[3] = {0.0, 0.0, 0.0};
+    for (int e = lane; e < nf; e += 32) {
+        const double2 yv = y[e];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            const double2 wv = w[q * nf + e];
+            t[q] += yv.x * wv.x + yv.y * wv.y;
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 3; ++q) t[q] = mdkk::warp_sum(t[q]);
+    if (lane == 0) {
+#pragma unroll
+        for (int q = 0; q < 3; ++q) t_out[3 * p + q] = t[q];
+    }
+}
+
 // ------------------------------------------------------------- descriptors
 // B[i][t] = sum over the triple's terms of c * op(U[g]) * op(U[h]) * op(U[z]),
 // U from the half set (mirrored operands conj'ed, signs in c; op_z is conj
@@ -386,6 +413,18 @@ int mdkk_snap_deidrj_staged(mdkk_snap* s, int n_pairs, const int* rows, const in
         n_pairs, s->n_flat, rows, cols, reinterpret_cast<const double2*>(Y), reinterpret_cast<const double2*>(wdu),
         f);
     MDKK_CHECK_LAUNCH("k_snap_deidrj_staged");
+    return MDKK_OK;
+}
+
+int mdkk_snap_pair_dedr(mdkk_snap* s, int n_pairs, const int* rows, const double* Y, const double* wdu,
+                        double* t_out, void* stream) {
+    if (!s || n_pairs < 0 || (n_pairs && (!rows || !Y || !wdu || !t_out))) return MDKK_E_ARG;
+    if (n_pairs == 0) return MDKK_OK;
+    const long long threads = (long long)n_pairs * 32;
+    k_snap_pair_dedr<<<(unsigned)((threads + 127) / 128), 128, 0, mdkk::as_stream(stream)>>>(
+        n_pairs, s->n_flat, rows, reinterpret_cast<const double2*>(Y), reinterpret_cast<const double2*>(wdu),
+        t_out);
+    MDKK_CHECK_LAUNCH("k_snap_pair_dedr");
     return MDKK_OK;
 }
 
