@@ -7,6 +7,10 @@ velocity-Verlet NVE with skin rebuilds — both the full/newton-off list (no
 atomics, headline `value`) and the half/newton-on list (FP64 atomics).  A
 "step" is one full velocity-Verlet step (kick+drift+skin test, halo refresh
 or rebuild, force, kick).  Inputs (x, v, f, table: ~1 GB) exceed the 126 MB L2.
+At N = 1 the configs[2] melt (16,384,000 atoms) is timed too, as a variant:
+the baseline of the strong-scaling curve.  Under torchrun (N > 1) the headline
+is configs[2] split over the N GPUs (strong scaling; `--weak` = an 80^3 brick
+per GPU) and the SNAP line is configs[4] (1,024,000 atoms) over the N GPUs.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 """
@@ -100,8 +104,11 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------- CPU oracle
-def cpu_lj_sample(steps=20, cells=20, style="full"):
-    """Oracle (numpy port of mdkk) on a bounded sample: 32k atoms, same physics, `steps` timed steps."""
+def cpu_lj_sample(steps=3, cells=40, style="full"):
+    """Oracle (numpy port of mdkk) on a bounded sample of configs[1]: the same melt at 40^3 cells
+    (256,000 atoms, 1/8 of configs[1]), initial build untimed, `steps` timed NVE steps.  The
+    per-atom CPU rate grows with N up to ~256k (numpy overheads amortise: 32k runs 1.33x slower
+    per atom here), so this sample is the closest bounded stand-in for the 2M configuration."""
     from oracle import md
     pos, L = md.lattice("fcc", LJ["rho"], (cells, cells, cells))
     vel = md.seeded_velocities(len(pos), LJ["T"], 1.0, LJ["seed"])
@@ -146,8 +153,11 @@ def run_reference(args):
     import multiprocessing as mp
     # bounded sample: 20^3 cells (32,000 atoms, ~0.3 s per step on one core) for up to
     # 200 timed steps, smaller cubes beyond so the whole run stays within a few minutes
+    # bounded sample of configs[1]: 40^3 cells (256,000 atoms, ~4 s per step on one core) for runs
+    # of up to 60 steps, 20^3 (32,000 atoms, ~0.6 s per step) up to 400, smaller cubes beyond,
+    # so the whole run stays within a few minutes
     total = max(1, args.steps + args.warmup)
-    cells = 20 if total <= 200 else max(6, int(20 * (200.0 / total) ** (1.0 / 3.0)))
+    cells = 40 if total <= 60 else 20 if total <= 400 else max(6, int(20 * (400.0 / total) ** (1.0 / 3.0)))
     n_rep = max(1, min(os.cpu_count() or 1, 32))
     ctx = mp.get_context("fork")
     q = ctx.Queue()
@@ -256,7 +266,7 @@ def fp64_peak(device):
     return blocks * 256 * iters * 8 * 2 / (a.elapsed_time(b) * 1e-3) / 1e12
 
 
-def snap_run(cells, steps, warmup, device):
+def snap_run(cells, steps, warmup, device, distributed=False):
     import tempfile
     import torch
     from paper_2508_13523_b200 import _lib
@@ -264,7 +274,7 @@ def snap_run(cells, steps, warmup, device):
     coeff = os.path.join(tempfile.mkdtemp(), "w_2j8.coeff")
     with open(coeff, "w") as fh:
         fh.write("4\n" + "\n".join(repr(float(b)) for b in np.linspace(0.05, 0.1, 55)) + "\n")
-    sim = Simulation(RunConfig(skin=SNAP["skin"], device=device), log=None)
+    sim = Simulation(RunConfig(skin=SNAP["skin"], device=device, distributed=distributed), log=None)
     sim.execute(f"units lj\nboundary p p p\nlattice bcc {SNAP['a']}\ncreate_box {cells} {cells} {cells}\n"
                 f"create_atoms\nmass 1.0\nvelocity {SNAP['T']} {SNAP['seed']}\nsuffix kk\n"
                 f"pair_style snap {SNAP['rc']} {coeff}\ntimestep {SNAP['dt']}\nthermo 1000000000\n")
@@ -289,10 +299,15 @@ def snap_run(cells, steps, warmup, device):
     l0 = _lib.launch_count()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
+    if distributed:
+        import torch.distributed as dist
+        dist.barrier()
     start.record()
     sim.advance(steps)
     end.record()
     torch.cuda.synchronize()
+    if distributed:
+        dist.barrier()
     ms = start.elapsed_time(end) / steps
     st, nl = sim.system.stores[0], sim.lists[0]
     # pairs within rc per atom (the descriptor neighbours), counted on device from the list
@@ -327,12 +342,11 @@ def lj_e2e(style, cells, steps, device, distributed=False):
     return dict(value=n * steps / dt / 1e6, h2d=h2d / steps, d2h=d2h / steps)
 
 
-def traffic_from_profiles(kernel="k_lj"):
-    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(p):
-        d = json.load(open(p))
-        return d.get(kernel)
-    return None
+def ncu_metrics():
+    """Per-kernel ncu figures committed under profiles/ (tools/ncu_metrics.py): DRAM bytes,
+    L1TEX wavefront %, executed FP64 instructions, per launch, with the launch's atom count."""
+    p = os.path.join(ROOT, "profiles", "ncu_metrics.json")
+    return json.load(open(p)) if os.path.exists(p) else {}
 
 
 def main():
@@ -345,10 +359,13 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-snap", action="store_true")
+    ap.add_argument("--no-16m", action="store_true", help="skip the configs[2] point at N=1")
     ap.add_argument("--snap-cells", type=int, default=SNAP["cells"])
     ap.add_argument("--snap-steps", type=int, default=5)
     ap.add_argument("--strong", action="store_true",
-                    help="configs[2]: a fixed 160^3-cell (16,384,000-atom) melt split over the N GPUs")
+                    help="configs[2] headline: the fixed 160^3-cell (16,384,000-atom) melt over the N GPUs "
+                         "(the default when WORLD_SIZE > 1)")
+    ap.add_argument("--weak", action="store_true", help="N > 1: an 80^3-cell brick per GPU instead")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -363,39 +380,50 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=device)
 
-    # weak scaling: an 80^3-cell fcc brick (2,048,000 atoms) per GPU, bricks tiled by decompose(N)
     from paper_2508_13523_b200.domain import Box as _Box, decompose as _decompose
     grid = _decompose(_Box((1.0, 1.0, 1.0)), world).grid
-    cells = (160, 160, 160) if args.strong else tuple(args.cells * g for g in grid)
-    scaling = "strong" if args.strong else "weak"
+    # N = 1: configs[1] (2,048,000 atoms) headline + the configs[2] point (16,384,000 atoms) as a
+    # variant; N > 1: configs[2] strong scaling (the north star's 80 % target), or --weak bricks
+    strong = args.strong or (world > 1 and not args.weak)
+    cells = (160, 160, 160) if strong else tuple(args.cells * g for g in grid)
+    scaling = "strong" if strong else "weak"
     workload = ("LJ 12-6 melt fcc rho*=0.8442, rc=2.5, skin=0.3, T=1.44, dt=0.005, full list newton-off "
-                + ("(configs[2]: 16,384,000 atoms, strong scaling over the GPUs)" if args.strong else
-                   "(configs[1]; weak scaling: 80^3 fcc cells per GPU)"))
+                + ("(configs[2]: 16,384,000 atoms, strong scaling over the GPUs)" if strong else
+                   "(configs[1]: 2,048,000 atoms per GPU)"))
     distributed = world > 1
 
     def max_over_ranks(v):
-        if not distributed:
+        if not distributed or v is None:
             return v
         import torch.distributed as dist
         t = torch.tensor([v], device=device, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    with ClockSampler(local) as clk:   # sampled in a child process across both timed LJ runs
+    with ClockSampler(local) as clk:   # sampled in a child process across the timed LJ runs
         full = lj_run("full", cells, args.steps, args.warmup, device, distributed=distributed)
         half = lj_run("half", cells, args.steps, args.warmup, device, distributed=distributed)
+        big = None
+        if world == 1 and not strong and not args.no_16m:
+            big = lj_run("full", (160, 160, 160), min(args.steps, 20), max(args.warmup, 3), device, profile=False)
     ms = max_over_ranks(full["ms"])
     half_ms = max_over_ranks(half["ms"])
+    force_ms = max_over_ranks(full["force_ms"])
     n_atoms = full["n_atoms"]           # global atom count (all bricks)
     value = n_atoms / (ms * 1e-3) / 1e6
     peak, peak_kind = _peaks()
     nn = full["nn"]
+    prof = ncu_metrics()
     # pair-stream model per launch: 28 B per listed partner + 52 B per atom;
     # the fused integration epilogue adds v read+write, x_ref read, x_next write (128 B)
     fused = bool(full.get("fused"))
     per_atom = 28.0 * nn + 52.0 + (128.0 if fused else 0.0)
-    bytes_per_launch = full["n_atoms"] / world * per_atom
-    achieved = bytes_per_launch / (full["force_ms"] * 1e-3) / 1e9
+    n_rank = full["n_atoms"] / world
+    bytes_per_launch = n_rank * per_atom
+    achieved = bytes_per_launch / (force_ms * 1e-3) / 1e9
+    kname = "k_lj_fused" if fused else "k_lj"
+    kp = prof.get(kname, {})
+    traffic = kp.get("dram_bytes") * n_rank / kp["n_atoms"] if kp.get("dram_bytes") else None
     # e2e: the user's call `run 100` (the configs' run length) from host arrays, thermo + snapshots back
     e2e_steps = 100
     if not args.no_e2e:
@@ -404,16 +432,41 @@ def main():
     if e2e is not None and distributed:
         e2e["value"] = n_atoms * e2e_steps / max_over_ranks(n_atoms * e2e_steps / e2e["value"])
     snapr, fp64 = None, None
-    if not args.no_snap and not distributed:
+    if not args.no_snap:
         fp64 = fp64_peak(device)
-        snapr = snap_run(args.snap_cells, args.snap_steps, 2, device)
+        snapr = snap_run(args.snap_cells, args.snap_steps, 2, device, distributed)
+        snapr["ms"] = max_over_ranks(snapr["ms"])
+        snapr["force_ms"] = max_over_ranks(snapr["force_ms"])
     cpu = None
-    if rank == 0 and not args.no_cpu and not distributed:
+    if rank == 0 and not args.no_cpu:
         v, secs, n = cpu_lj_sample()
         cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "port",
-               "sample": f"numpy oracle port, LJ melt {n} atoms (same rho/rc/skin/T/dt, full list), 20 steps "
-                         f"after initial build, {secs:.1f} s, 1 thread of {os.cpu_count()}"}
+               "sample": f"numpy oracle port of mdkk (oracle/md.py), the configs[1] melt at 40^3 cells ({n:,} "
+                         f"atoms; same rho/rc/skin/T/dt, full list), 3 NVE steps after the initial build, "
+                         f"{secs:.1f} s, 1 thread of {os.cpu_count()}"}
     if rank == 0:
+        snap_block = None
+        if snapr is not None:
+            flop_model = snap_flops_per_atom_step(snapr["nn"]) * snapr["n_atoms"] / (snapr["force_ms"] * 1e-3) / 1e12
+            ex = prof.get("snap_pipeline", {})
+            executed = (ex["dflop_per_atom"] * snapr["n_atoms"] / (snapr["force_ms"] * 1e-3) / 1e12
+                        if ex.get("dflop_per_atom") else None)
+            snap_block = {
+                "workload": f"SNAP W bcc a=3.1803, 2J=8, rc=4.73, skin 0.3, T=0.01, dt=0.001, "
+                            f"{snapr['n_atoms']:,} atoms (configs[4]"
+                            + (f", strong scaling over {world} GPUs)" if distributed else " at N=1)"),
+                "value": snapr["n_atoms"] / (snapr["ms"] * 1e-3) / 1e6, "unit": UNIT,
+                "scaling": "strong" if distributed else None,
+                "ms_per_step": snapr["ms"], "force_ms": snapr["force_ms"], "steps": args.snap_steps,
+                "pairs_within_rc_per_atom": snapr["nn"],
+                "roofline": {"bound": "fp64", "kernel": "ui + yi + fused deidrj (+ reverse comm)",
+                             "achieved": flop_model, "peak": fp64 * world,
+                             "peak_kind": "measured live (DFMA probe) x GPUs", "unit": "TFLOP/s",
+                             "frac": flop_model / (fp64 * world),
+                             "flops_model": "canonical mdkk formulation nn*(9260+60518)+36*32578 per atom",
+                             "executed_tflops": executed,
+                             "executed_frac": executed / (fp64 * world) if executed else None,
+                             "executed_source": ex.get("source")}}
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": scaling,
@@ -422,11 +475,12 @@ def main():
                        "n_atoms": full["n_atoms"], "n_ghost_rank0": full["n_ghost"], "list": "full",
                        "grid": list(grid),
                        "rebuilds_in_timed_steps": full["rebuilds"], "mean_neighbors": nn,
-                       "l2": "inputs (x,v,f,table ~%.0f MB) larger than L2" % (full["n_atoms"] * (nn * 4 + 96) / 1e6),
+                       "l2": "inputs (x,v,f,table ~%.0f MB per GPU) larger than L2"
+                             % (n_rank * (nn * 4 + 96) / 1e6),
                        "parallelism": (f"spatial DD {grid[0]}x{grid[1]}x{grid[2]}, NCCL halo exchange"
                                        if world > 1 else "1 GPU")},
             "variants": {
-                "lj_full_newton_off": {"value": value, "ms_per_step": full["ms"], "force_ms": full["force_ms"],
+                "lj_full_newton_off": {"value": value, "ms_per_step": ms, "force_ms": force_ms,
                                        "rebuilds": full["rebuilds"]},
                 "lj_half_newton_on_atomics": {"value": half["n_atoms"] / (half_ms * 1e-3) / 1e6,
                                               "ms_per_step": half_ms, "force_ms": half["force_ms"],
@@ -437,25 +491,17 @@ def main():
                                     else "k_lj<full> (+ partial reduce)"),
                          "achieved": achieved,
                          "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic_from_profiles("k_lj_fused" if fused else "k_lj"),
+                         "traffic": traffic,
                          "bytes_model": (f"n_local*(28*nn+52+128), nn={nn:.2f} measured" if fused
                                          else f"n_local*(28*nn+52), nn={nn:.2f} measured"),
-                         "note": ("pair-stream model (SURVEY 8(d)): x_j reuse in L1/L2 lets it exceed the HBM "
-                                  "peak; actual DRAM per launch is `traffic`; the kernel's limiter is the L1TEX "
-                                  "data pipe (92-93 % wavefronts, profiles/r1h_klj_ncu_full_summary.txt)")},
-            "snap": (None if snapr is None else {
-                "workload": f"SNAP W bcc a=3.1803, 2J=8, rc=4.73, skin 0.3, T=0.01, dt=0.001, "
-                            f"{snapr['n_atoms']} atoms (configs[4] at N=1)",
-                "value": snapr["n_atoms"] / (snapr["ms"] * 1e-3) / 1e6, "unit": UNIT,
-                "ms_per_step": snapr["ms"], "force_ms": snapr["force_ms"], "steps": args.snap_steps,
-                "pairs_within_rc_per_atom": snapr["nn"],
-                "roofline": {"bound": "fp64", "kernel": "ui + yi + fused deidrj (+ reverse comm)",
-                             "achieved": snap_flops_per_atom_step(snapr["nn"]) * snapr["n_atoms"]
-                             / (snapr["force_ms"] * 1e-3) / 1e12,
-                             "peak": fp64, "peak_kind": "measured live (DFMA probe)", "unit": "TFLOP/s",
-                             "frac": snap_flops_per_atom_step(snapr["nn"]) * snapr["n_atoms"]
-                             / (snapr["force_ms"] * 1e-3) / 1e12 / fp64,
-                             "flops_model": "canonical mdkk formulation nn*(9260+60518)+36*32578 per atom"}}),
+                         "dram_frac": traffic / (force_ms * 1e-3) / 1e9 / peak if traffic else None,
+                         "l1_wavefront_pct": kp.get("l1tex_wavefront_pct"),
+                         "fp64_pipe_pct": kp.get("fp64_pipe_pct"),
+                         "profile_source": kp.get("source"),
+                         "note": ("frac = SURVEY 8(d) pair-stream model (x_j reuse in L1/L2 lets it exceed 1); "
+                                  "dram_frac = the kernel's ncu DRAM bytes per launch over the live launch time; "
+                                  "the binding limiter is the L1TEX data pipe (l1_wavefront_pct)")},
+            "snap": snap_block,
             "cpu_baseline": cpu,
             "e2e": ({"value": e2e["value"], "unit": UNIT, "h2d_bytes_per_step": e2e["h2d"],
                      "d2h_bytes_per_step": e2e["d2h"],
@@ -465,6 +511,11 @@ def main():
             "gpu_launches": full["launches"],
             "clocks": clk.summary(),
         }
+        if big is not None:
+            out["variants"]["lj_16m_full_configs2_n1"] = {
+                "value": big["n_atoms"] / (big["ms"] * 1e-3) / 1e6, "ms_per_step": big["ms"],
+                "n_atoms": big["n_atoms"], "rebuilds": big["rebuilds"],
+                "what": "configs[2] on one GPU: the strong-scaling baseline for bench.py --gpus N"}
         print(json.dumps(out))
     if world > 1:
         import torch.distributed as dist
