@@ -100,6 +100,11 @@ __device__ __forceinline__ void block_sum(double (&v)[K], double* out) {
 // Deterministic second stage: out[k] = sum_b partials[b*K + k], fixed order.
 void reduce_partials(const double* partials, int nblocks, int K, double* out, cudaStream_t s);
 
+// A drift maximum that cannot hide a blow-up: NaN / inf become +inf before the
+// (NaN-dropping) fmax reductions, so the host's per-step read-back sees it
+// (the every-step non-finite abort, mdkk/driver/simulation.py:459-478).
+__device__ __forceinline__ double finite_or_inf(double v) { return v <= 1.7976931348623157e308 ? v : __longlong_as_double(0x7ff0000000000000LL); }
+
 // Non-negative doubles order like their int64 bit patterns.
 __device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
     atomicMax(reinterpret_cast<unsigned long long*>(addr),

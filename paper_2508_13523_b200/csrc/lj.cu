@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(kBlock) k_lj(const double* __restrict__ x, int
                     xn.w = 0.0;
                     mdkk::st4(integ.x_next, i, xn);
                     const double4 r = mdkk::ld4_nc(integ.x_ref, i);
-                    d2n = mdkk::r2_exact(xn.x - r.x, xn.y - r.y, xn.z - r.z);
+                    d2n = mdkk::finite_or_inf(mdkk::r2_exact(xn.x - r.x, xn.y - r.y, xn.z - r.z));
                 }
                 mdkk::st4(integ.v, i, vi);
             }

@@ -33,7 +33,7 @@ __global__ void __launch_bounds__(kBlock) k_verlet_first(double* __restrict__ x,
         mdkk::st4(v, i, vi);
         mdkk::st4(x, i, xi);
         double4 r = mdkk::ld4(xr, i);
-        d2 = mdkk::r2_exact(xi.x - r.x, xi.y - r.y, xi.z - r.z);
+        d2 = mdkk::finite_or_inf(mdkk::r2_exact(xi.x - r.x, xi.y - r.y, xi.z - r.z));
     }
     d2 = mdkk::warp_max(d2);
     if ((threadIdx.x & 31) == 0) mdkk::atomic_max_nonneg(maxd2, d2);

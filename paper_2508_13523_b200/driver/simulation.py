@@ -101,9 +101,13 @@ class LJStyle:
         key = (id(system), len(system.stores), str(dev))
         if getattr(self, "_bufkey", None) != key:
             self._bufkey = key
-            self._evs = torch.zeros((len(system.stores), 7), dtype=torch.float64, device=dev)
+            self._evs = torch.zeros((2, len(system.stores), 7), dtype=torch.float64, device=dev)
             self._flags = torch.zeros(1, dtype=torch.int32, device=dev)
-        evs, flags = self._evs, self._flags
+            self._slot = 0
+        # two energy slots used in turn: a step's returned energy stays valid while the
+        # next step's (speculative) launch is already queued (the per-step non-finite check)
+        self._slot ^= 1
+        evs, flags = self._evs[self._slot], self._flags
         half = False
         for k, (s, nl) in enumerate(zip(system.stores, lists)):
             lj_force_rank(s, nl, self.kernel.params, evs[k], flags, virial=False,
@@ -228,6 +232,8 @@ class Simulation:
         self.qeq = None
         self._e_dev = None
         self._flags = None
+        self._run_step = 0         # steps taken in the current run (the non-finite abort names them)
+        self._e_prev = None        # device energy of the last completed step
 
     # ------------------------------------------------------------ commands
     def execute(self, script) -> "Simulation":
@@ -460,7 +466,10 @@ class Simulation:
             self._gate = worst
             self._spec_e = self._forces_device(gate=worst, gate_limit=0.5 * self.config.skin)
         self._d2_ready.synchronize()
-        return math.sqrt(float(self._d2_host[0])) > 0.5 * self.config.skin
+        d2 = float(self._d2_host[0])
+        if not math.isfinite(d2):
+            self._nonfinite_abort(self._run_step - 1)
+        return math.sqrt(d2) > 0.5 * self.config.skin
 
     def _half_kick(self):
         lib, st = _lib.lib(), _lib.stream(self.device)
@@ -479,6 +488,7 @@ class Simulation:
         """
         self._packed = False
         self._spec_e = None
+        self._run_step += 1
         if self._half_kick_drift():
             # with a gated style the build's capacity check is deferred: the force launch
             # (gated on the device-side count) queues behind the build without a host
@@ -496,6 +506,7 @@ class Simulation:
                 self.system.forward_comm()
             e = self._spec_e if self._spec_e is not None else self._forces_device()
         self._spec_e = None
+        self._e_prev = e
         if defer_kick:
             self._kick_pending = True
         else:
@@ -604,6 +615,7 @@ class Simulation:
         read_back(cur)
         e = None
         for step in range(1, n_steps + 1):
+            self._run_step += 1
             mode = 2 if step < n_steps else 1
             nxt = 1 - cur
             xa = x_alt() if mode == 2 else None
@@ -620,7 +632,10 @@ class Simulation:
                 global_max(nxt)
                 read_back(nxt)
             fz["ready"][cur].synchronize()
-            if math.sqrt(float(fz["pin"][cur])) > half:
+            d2h = float(fz["pin"][cur])
+            if not math.isfinite(d2h):   # the drift of this step saw a non-finite x / v / f
+                self._nonfinite_abort(self._run_step - 1)
+            if math.sqrt(d2h) > half:
                 defer = self._cap_hint is not None
                 self._rebuild_lists(defer=defer)
                 s = self.system.stores[0]               # a distributed migrate makes a new store
@@ -639,7 +654,21 @@ class Simulation:
                 cur = nxt
             else:
                 s.device_wrote(vel=True, force=True)
+            self._e_prev = e
         return e
+
+    def _nonfinite_abort(self, step: int):
+        """The per-step drift maximum came back non-finite: the forces (or energy) of
+        `step` were not finite (mdkk/driver/simulation.py:459-464, checked every step
+        there).  Raise the reference's RunError naming that step."""
+        torch.cuda.synchronize(self.device)
+        if self._flags is not None and int(self._flags.item()) & _lib.FLAG_COINCIDENT:
+            from ..pair_lj import PairError
+            raise PairError("coincident atoms (r = 0)")   # what the reference's kernel raises (pair_lj.py:83-84)
+        e = getattr(self, "_e_prev", None)
+        if e is not None and not math.isfinite(float(self._global_sum(e.reshape(1)).item())):
+            raise RunError(f"non-finite potential energy at step {step}")
+        raise RunError(f"non-finite force at step {step}")
 
     def _check_finite(self, step, e_pot):
         if not np.isfinite(e_pot):
@@ -648,13 +677,16 @@ class Simulation:
             if s.n_local and not bool(torch.isfinite(s.f[: s.n_local, :3]).all().item()):
                 raise RunError(f"non-finite force at step {step}")
         if self._flags is not None and int(self._flags.item()) & _lib.FLAG_COINCIDENT:
-            raise RunError(f"coincident atoms (r = 0) at or before step {step}")
+            from ..pair_lj import PairError
+            raise PairError("coincident atoms (r = 0)")   # the reference kernel's error (pair_lj.py:83-84)
 
     def run_nve(self, n_steps: int) -> RunResult:
         """NVE with thermo at 0, every `thermo`, and the last step (mdkk/driver/simulation.py:452-481).
 
-        The non-finite check runs on logged steps (device error word + force
-        scan) instead of every step, so the loop never waits on the host.
+        Non-finite values abort at the first bad step, as in the reference: the
+        per-step skin-test read-back the loop already waits on carries it (the
+        kernels turn a non-finite drift into +inf), so step t's check sees step
+        t-1's forces; logged steps also scan energy, forces and the error word.
         """
         if n_steps < 0:
             raise RunError("run expects a non-negative step count")
@@ -684,6 +716,8 @@ class Simulation:
                 self._qeq_diagnostic(step, result)
                 self.log(result.lines[-1])
 
+            self._run_step = 0
+            self._e_prev = None
             log(0, self._forces_device(), n_steps == 0)
             step = 0
             while step < n_steps:   # device-resident stretches between thermo steps

@@ -284,8 +284,26 @@ def snap_c4_run():
     np.savez_compressed(os.path.join(HERE, "snap_run.npz"), **out)
 
 
+def c1_drift():
+    """C1 1000-step NVE thermo (every 100 steps) from the reference, full and half lists: the
+    drift bound of the north star ("no worse than the reference's")."""
+    silent = lambda *_: None  # noqa: E731
+    c1 = ("units lj\nboundary p p p\nlattice fcc 0.8442\ncreate_box 20 20 20\ncreate_atoms\n"
+          "mass 1.0\nvelocity 1.44 87287\npair_style lj/cut 2.5\npair_coeff 1.0 1.0\n"
+          "timestep 0.005\nthermo 100\nrun 1000\n")
+    out = {}
+    for style in ("full", "half"):
+        t0 = time.time()
+        sim = run_script(c1, RunConfig(list_style=style, newton=(style == "half")), log=silent)
+        out[f"c1_{style}_rows1000"] = np.array(sim.results[-1].rows)
+        print(f"C1 1000 {style}: {time.time() - t0:.1f}s", flush=True)
+    np.savez_compressed(os.path.join(HERE, "lj_drift.npz"), **out)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["lj_small", "lj_32k", "snap", "runs", "qeq"]
+    if "c1_drift" in which:
+        c1_drift()
     if "lj_sets_c1" in which:
         lj_sets((20, 20, 20), "lj_c1_sets", n_ranks_list=(1, 8), sub=37)
     if "lj_sets_c2" in which:

@@ -126,3 +126,45 @@ def test_overlapped_snapshots_match_synchronous_reads(gpu):
     assert sorted(ra.snapshots) == [0, 10, 20, 30]
     for step, snap in ra.snapshots.items():
         assert np.array_equal(snap, ref[step]), step
+
+
+@pytest.mark.parametrize("style", ["full", "half"])
+@pytest.mark.parametrize("at", [3, 7])
+def test_blow_up_aborts_at_the_first_bad_step(gpu, style, at):
+    """Atom 0 moved exactly onto atom 1 right before step `at`'s force launch: that step's
+    energy and forces are not finite, and the run stops there -- between thermo steps --
+    with the reference's error (its kernel raises PairError on r = 0, mdkk/pair_lj.py:83-84,
+    checked every step), not at the next thermo step."""
+    from paper_2508_13523_b200 import PairError
+    sim = _sim(style)
+    sim.thermo_every = 100
+    orig = sim.style.compute_device
+    state = {"done": False}
+
+    def poisoned(system, lists, config, *a, **kw):
+        if sim._run_step == at and not state["done"]:
+            s = system.stores[0]
+            s.x[0, :3] = s.x[1, :3]
+            state["done"] = True
+        return orig(system, lists, config, *a, **kw)
+    sim.style.compute_device = poisoned
+    with pytest.raises(PairError, match="coincident"):
+        sim.run_nve(40)
+    assert sim._run_step == at + 1      # stopped at the next step's check, not at thermo 40
+
+
+def test_nonfinite_energy_is_named_with_its_step(gpu):
+    """Non-finite energy without coincidence (a NaN-poisoned epsilon from step 4 on): the run
+    stops right after step 4 with "non-finite potential energy at step 4"."""
+    from paper_2508_13523_b200.driver import RunError
+    sim = _sim("full")
+    sim.thermo_every = 100
+    orig = sim.style.compute_device
+
+    def poisoned(system, lists, config, *a, **kw):
+        if sim._run_step == 4:
+            sim.style.kernel.params.epsilon = float("nan")
+        return orig(system, lists, config, *a, **kw)
+    sim.style.compute_device = poisoned
+    with pytest.raises(RunError, match="non-finite potential energy at step 4$"):
+        sim.run_nve(40)

@@ -39,3 +39,22 @@ def test_install_rebinds_every_hot_path_binding_and_registers_kk_styles():
         "['lj/cut', 'lj/cut/opt', 'snap', 'snap/opt']\n"
         "print(len(names))\n")
     assert int(out.strip().splitlines()[-1]) >= 20
+
+
+def test_saturation_bench_validates_before_touching_the_device():
+    """bench_saturation's argument checks (mdkk/driver/bench.py:105-115) and the CSV schema."""
+    from paper_2508_13523_b200.driver.bench import BenchResult, bench_saturation
+    from paper_2508_13523_b200.driver.simulation import RunError
+    with pytest.raises(RunError):
+        bench_saturation("eam", [1000])
+    with pytest.raises(RunError):
+        bench_saturation("lj", [1000], reps=0)
+    r = BenchResult("lj", [(1000, 2.5e8), (8000, 1.5e9)])
+    assert list(r.sizes) == [1000, 8000] and r.rates[1] == 1.5e9
+
+
+def test_saturation_csv_schema(tmp_path):
+    from paper_2508_13523_b200.driver.bench import BenchResult
+    p = tmp_path / "s.csv"
+    BenchResult("snap", [(64000, 1.25e8)]).write_csv(str(p))
+    assert p.read_text().splitlines() == ["n_atoms,atom_steps_per_second", "64000,1.25e+08"]
