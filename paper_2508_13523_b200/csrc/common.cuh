@@ -12,16 +12,24 @@
 struct mdkk_ctx {
     int device = 0;
     int sm_count = 148;
-    void* scratch = nullptr;     // reduction partials, CUB temp storage
+    void* scratch = nullptr;     // reduction partials, sort / binning buffers
     size_t scratch_bytes = 0;
+    void* scratch_tail = nullptr;  // the prefix-sum tile totals (used while `scratch` is held)
+    size_t scratch_tail_bytes = 0;
 };
 
 namespace mdkk {
 
 void set_error(const std::string& msg);
 int cuda_fail(cudaError_t e, const char* what);
-// Grow-only scratch arena (synchronises the device only when it grows).
+// Grow-only scratch arena (synchronises the device only when it grows; a pointer
+// from an earlier call is invalid after a call that grows it).
 void* scratch(mdkk_ctx* ctx, size_t bytes);
+// A second, independent arena for the prefix sums' tile totals.
+void* scratch_tail(mdkk_ctx* ctx, size_t bytes);
+// Exclusive prefix sums (csrc/sort.cu), out[k] = in[0] + ... + in[k-1]; in != out.
+int exclusive_scan_i32(mdkk_ctx* ctx, const int* in, int* out, long long n, cudaStream_t s);
+int exclusive_scan_i64(mdkk_ctx* ctx, const long long* in, long long* out, long long n, cudaStream_t s);
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 

@@ -31,6 +31,20 @@ void* scratch(mdkk_ctx* ctx, size_t bytes) {
     return ctx->scratch;
 }
 
+void* scratch_tail(mdkk_ctx* ctx, size_t bytes) {
+    if (bytes <= ctx->scratch_tail_bytes) return ctx->scratch_tail;
+    size_t want = bytes + bytes / 2 + (1 << 16);
+    if (ctx->scratch_tail) {
+        cudaDeviceSynchronize();
+        cudaFree(ctx->scratch_tail);
+    }
+    ctx->scratch_tail = nullptr;
+    ctx->scratch_tail_bytes = 0;
+    if (cudaMalloc(&ctx->scratch_tail, want) != cudaSuccess) return nullptr;
+    ctx->scratch_tail_bytes = want;
+    return ctx->scratch_tail;
+}
+
 // One block per column k: fixed-order strided sums then a fixed tree (deterministic).
 __global__ void __launch_bounds__(1024) k_reduce_partials(const double* __restrict__ p, int nb, int K,
                                                           double* __restrict__ out) {
@@ -84,10 +98,9 @@ int mdkk_ctx_create(int device, mdkk_ctx** out_host) {
 
 int mdkk_ctx_destroy(mdkk_ctx* ctx) {
     if (!ctx) return MDKK_OK;
-    if (ctx->scratch) {
-        cudaDeviceSynchronize();
-        cudaFree(ctx->scratch);
-    }
+    if (ctx->scratch || ctx->scratch_tail) cudaDeviceSynchronize();
+    if (ctx->scratch) cudaFree(ctx->scratch);
+    if (ctx->scratch_tail) cudaFree(ctx->scratch_tail);
     delete ctx;
     return MDKK_OK;
 }

@@ -1,7 +1,6 @@
 // Domain kernels: wrap, halo selection (stable multi-way compaction),
 // forward-comm pack with periodic shift, reverse-comm fold, row permutes.
 // Reference: mdkk/domain.py:56-63, :246-334.
-#include <cub/device/device_scan.cuh>
 
 #include "common.cuh"
 
@@ -303,17 +302,14 @@ int mdkk_boundary_rows(mdkk_ctx* ctx, const int* cell_start, const int* ncell_ho
     if (ncl < 1 || ncl >= (1LL << 30)) return MDKK_E_ARG;
     const int ncell = (int)ncl;
     cudaStream_t s = mdkk::as_stream(stream);
-    size_t scan_bytes = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (int*)nullptr, (int*)nullptr, ncell + 1, s);
-    const size_t off_cnt = 0, off_tmp = ((sizeof(int) * ((size_t)ncell + 2) * 2) + 255) & ~size_t(255);
-    char* base = static_cast<char*>(mdkk::scratch(ctx, off_tmp + scan_bytes + 256));
-    if (!base) return mdkk::cuda_fail(cudaErrorMemoryAllocation, "scratch");
-    int* cnt = reinterpret_cast<int*>(base + off_cnt);
+    int* cnt = static_cast<int*>(mdkk::scratch(ctx, sizeof(int) * ((size_t)ncell + 2) * 2));
+    if (!cnt) return mdkk::cuda_fail(cudaErrorMemoryAllocation, "scratch");
     int* off = cnt + ncell + 2;
     const int nx = ncell_host[0], ny = ncell_host[1], nz = ncell_host[2];
     k_boundary_counts<<<mdkk::grid_for(ncell + 1, 256), 256, 0, s>>>(cell_start, nx, ny, nz, layer, cnt);
     MDKK_CHECK_LAUNCH("k_boundary_counts");
-    cub::DeviceScan::ExclusiveSum(base + off_tmp, scan_bytes, cnt, off, ncell + 1, s);
+    const int st = mdkk::exclusive_scan_i32(ctx, cnt, off, (long long)ncell + 1, s);
+    if (st != MDKK_OK) return st;
     k_boundary_fill<<<mdkk::grid_for(ncell, 256), 256, 0, s>>>(cell_start, ncell, cnt, off, rows, count);
     MDKK_CHECK_LAUNCH("k_boundary_fill");
     return MDKK_OK;

@@ -9,9 +9,6 @@
 //      per warp) and keeps j != i with r^2 < bc^2 (strict, same rounding as
 //      the reference) passing the style predicate (mdkk/neighbor.py:134-179).
 // Output: int32 cluster-blocked table [ncl][cap][32] of row indices + counts.
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_scan.cuh>
-
 #include "cluster.cuh"
 
 namespace {
@@ -36,34 +33,6 @@ __global__ void k_rank_keys(const double* __restrict__ x, int n, double Lx, doub
     int cy = mdkk::clampi((int)floor(p.y / Ly * (double)gy), gy);
     int cz = mdkk::clampi((int)floor(p.z / Lz * (double)gz), gz);
     key[i] = (cx * gy + cy) * gz + cz;
-}
-
-__global__ void k_key_count(int n, const int* __restrict__ key, int* __restrict__ counts) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) atomicAdd(counts + key[i], 1);
-}
-
-__global__ void k_cell_scatter(int n, const int* __restrict__ cid, const int* __restrict__ start,
-                               int* __restrict__ cursor, int* __restrict__ atoms) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    int c = cid[i];
-    atoms[start[c] + atomicAdd(cursor + c, 1)] = i;
-}
-
-// Deterministic order inside a bucket: ascending row index (insertion sort).
-__global__ void k_cell_sort(int ncell, const int* __restrict__ start, int* __restrict__ atoms) {
-    int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= ncell) return;
-    int b = start[c], e = start[c + 1];
-    for (int k = b + 1; k < e; ++k) {
-        int v = atoms[k], m = k - 1;
-        while (m >= b && atoms[m] > v) {
-            atoms[m + 1] = atoms[m];
-            --m;
-        }
-        atoms[m + 1] = v;
-    }
 }
 
 __global__ void k_cell_positions(const double* __restrict__ x, const int* __restrict__ cell_atoms, int n,
@@ -449,80 +418,6 @@ __global__ void k_max_disp2(const double* __restrict__ x, const double* __restri
 }  // namespace
 
 extern "C" {
-
-__global__ void k_iota(int n, int* __restrict__ v) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) v[i] = i;
-}
-
-// Stable LSD radix sort of (key, row) over ceil(log2(nbuckets)) bits: rows
-// ascending within a bucket, the same order as the scatter + per-bucket
-// insertion sort below (which is kept for huge bucket counts, where the
-// radix passes over 2^bits keys would dominate).  For rank partitions the
-// insertion sort would be O(n^2); for cells its one-thread-per-cell serial
-// loops cost ~3x the radix passes (2.3M rows, 110k cells).
-constexpr int kRadixMaxBuckets = 1 << 24;
-static int bucket_sort_radix(mdkk_ctx* ctx, const int* keys, int n, int nbuckets, int* bucket_start, int* order,
-                             cudaStream_t s) {
-    int bits = 1;
-    while ((1 << bits) < nbuckets) ++bits;
-    size_t sort_bytes = 0, scan_bytes = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, (const int*)nullptr, (int*)nullptr, (const int*)nullptr,
-                                    (int*)nullptr, n, 0, bits, s);
-    cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (int*)nullptr, (int*)nullptr, nbuckets + 1, s);
-    auto al = [](size_t v) { return (v + 255) & ~size_t(255); };
-    const size_t off_cnt = 0;
-    const size_t off_ko = al(off_cnt + sizeof(int) * ((size_t)nbuckets + 64));
-    const size_t off_vi = al(off_ko + sizeof(int) * (size_t)n);
-    const size_t off_tmp = al(off_vi + sizeof(int) * (size_t)n);
-    char* base = static_cast<char*>(mdkk::scratch(ctx, off_tmp + std::max(sort_bytes, scan_bytes) + 256));
-    if (!base) return mdkk::cuda_fail(cudaErrorMemoryAllocation, "scratch");
-    int* cnt = reinterpret_cast<int*>(base + off_cnt);
-    int* kout = reinterpret_cast<int*>(base + off_ko);
-    int* vin = reinterpret_cast<int*>(base + off_vi);
-    void* tmp = base + off_tmp;
-    cudaMemsetAsync(cnt, 0, sizeof(int) * ((size_t)nbuckets + 1), s);
-    k_key_count<<<mdkk::grid_for(n, 256), 256, 0, s>>>(n, keys, cnt);
-    MDKK_CHECK_LAUNCH("k_key_count");
-    cub::DeviceScan::ExclusiveSum(tmp, scan_bytes, cnt, bucket_start, nbuckets + 1, s);
-    k_iota<<<mdkk::grid_for(n, 256), 256, 0, s>>>(n, vin);
-    MDKK_CHECK_LAUNCH("k_iota");
-    cub::DeviceRadixSort::SortPairs(tmp, sort_bytes, keys, kout, vin, order, n, 0, bits, s);
-    MDKK_CHECK_LAUNCH("cub radix sort");
-    return MDKK_OK;
-}
-
-int mdkk_bucket_sort(mdkk_ctx* ctx, const int* keys, int n, int nbuckets, int* bucket_start, int* order,
-                     void* stream) {
-    if (!ctx || n < 0 || nbuckets < 1 || nbuckets > (1 << 30)) return MDKK_E_ARG;
-    cudaStream_t s = mdkk::as_stream(stream);
-    if (n > 0 && nbuckets <= kRadixMaxBuckets) return bucket_sort_radix(ctx, keys, n, nbuckets, bucket_start, order, s);
-    size_t cub_bytes = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, cub_bytes, (int*)nullptr, (int*)nullptr, nbuckets + 1, s);
-    size_t off_cnt = 0;
-    size_t off_cur = off_cnt + sizeof(int) * ((size_t)nbuckets + 64);
-    size_t off_cub = off_cur + sizeof(int) * ((size_t)nbuckets + 64);
-    off_cub = (off_cub + 255) & ~size_t(255);
-    char* base = static_cast<char*>(mdkk::scratch(ctx, off_cub + cub_bytes + 256));
-    if (!base) return mdkk::cuda_fail(cudaErrorMemoryAllocation, "scratch");
-    int* cnt = reinterpret_cast<int*>(base + off_cnt);
-    int* cur = reinterpret_cast<int*>(base + off_cur);
-    void* tmp = base + off_cub;
-    cudaMemsetAsync(cnt, 0, sizeof(int) * ((size_t)nbuckets + 1), s);
-    cudaMemsetAsync(cur, 0, sizeof(int) * (size_t)nbuckets, s);
-    if (n > 0) {
-        k_key_count<<<mdkk::grid_for(n, 256), 256, 0, s>>>(n, keys, cnt);
-        MDKK_CHECK_LAUNCH("k_key_count");
-    }
-    cub::DeviceScan::ExclusiveSum(tmp, cub_bytes, cnt, bucket_start, nbuckets + 1, s);
-    if (n > 0) {
-        k_cell_scatter<<<mdkk::grid_for(n, 256), 256, 0, s>>>(n, keys, bucket_start, cur, order);
-        MDKK_CHECK_LAUNCH("k_cell_scatter");
-        k_cell_sort<<<mdkk::grid_for(nbuckets, 128), 128, 0, s>>>(nbuckets, bucket_start, order);
-        MDKK_CHECK_LAUNCH("k_cell_sort");
-    }
-    return MDKK_OK;
-}
 
 int mdkk_cell_keys(const double* x, int n, const double* grid_host, const int* ncell_host, int* keys,
                    void* stream) {

@@ -4,7 +4,6 @@
 // two-stage sum, so a fused two-system solve reproduces two sequential solves
 // bit for bit (mdkk/qeq.py:233-274): the per-row SpMV sums and the dot
 // partials do not depend on how many systems share the traversal.
-#include <cub/device/device_scan.cuh>
 
 #include "common.cuh"
 
@@ -148,13 +147,7 @@ int mdkk_qeq_offsets(mdkk_ctx* ctx, const int* counts, int n, int cap, long long
     cudaStream_t s = mdkk::as_stream(stream);
     k_qeq_caps<<<mdkk::grid_for(n + 1, kBlock), kBlock, 0, s>>>(counts, n, cap, caps);
     MDKK_CHECK_LAUNCH("k_qeq_caps");
-    size_t bytes = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, bytes, caps, offsets, n + 1, s);
-    void* tmp = mdkk::scratch(ctx, bytes + 256);
-    if (!tmp) return mdkk::cuda_fail(cudaErrorMemoryAllocation, "scratch");
-    cub::DeviceScan::ExclusiveSum(tmp, bytes, caps, offsets, n + 1, s);
-    MDKK_CHECK_LAUNCH("qeq offsets scan");
-    return MDKK_OK;
+    return mdkk::exclusive_scan_i64(ctx, caps, offsets, (long long)n + 1, s);
 }
 
 int mdkk_qeq_build(const double* x, int n_local, const int* table, const int* counts, int cap, const int* oidx,

@@ -8,7 +8,6 @@
 //     B_t = sum_terms c U[iu1] U[iu2] conj(U[iz]) per atom and triple.
 // The engine never calls these (its forces come from the fused reverse-mode
 // kernel in snap.cu); they serve the reference's staged API and its tests.
-#include <cub/device/device_scan.cuh>
 
 #include "snap_common.cuh"
 
@@ -371,13 +370,7 @@ int mdkk_snap_pair_count(mdkk_ctx* ctx, const double* x, int n_local, const int*
         MDKK_CHECK_LAUNCH("k_snap_pair_count");
     }
     cudaMemsetAsync(npair + n_local, 0, sizeof(int), st);
-    size_t bytes = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, bytes, npair, offsets, n_local + 1, st);
-    void* tmp = mdkk::scratch(ctx, bytes + 256);
-    if (!tmp) return mdkk::cuda_fail(cudaErrorMemoryAllocation, "scratch");
-    cub::DeviceScan::ExclusiveSum(tmp, bytes, npair, offsets, n_local + 1, st);
-    MDKK_CHECK_LAUNCH("pair offsets scan");
-    return MDKK_OK;
+    return mdkk::exclusive_scan_i32(ctx, npair, offsets, (long long)n_local + 1, st);
 }
 
 int mdkk_snap_pair_fill(const double* x, int n_local, const int* table, const int* counts, int cap, double rc,
