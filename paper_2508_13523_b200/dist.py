@@ -92,6 +92,46 @@ class CudaOps:
                                       idx.data_ptr(), None, None, rp, cp, self._s()), "mdkk_halo_fill")
         return idx, totals
 
+    def halo_count(self, x, n, tab, C_, bins=None, lo=None, hi=None):
+        """First half of halo_select: per-combo totals stay on the device (the caller reads
+        them together with the all-gathered counts matrix: one host sync per exchange)."""
+        lib, ctx = _lib.lib(), _lib.ctx(self.device)
+        nb = (n + 255) // 256
+        blk = torch.empty(max(nb * C_, 1), dtype=torch.int32, device=self.device)
+        tot = torch.empty(max(C_, 1), dtype=torch.int32, device=self.device)
+        rp = cp = None
+        if bins is not None:
+            _, _, _, narr, _ = shell_grid_args(lo, hi, bins[0])
+            rows = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
+            cnt = torch.empty(1, dtype=torch.int32, device=self.device)
+            _lib.check(lib.mdkk_boundary_rows(ctx, bins[2].data_ptr(), narr, 2, rows.data_ptr(), cnt.data_ptr(),
+                                              self._s()), "mdkk_boundary_rows")
+            rp, cp = (rows, cnt)
+        _lib.check(lib.mdkk_halo_count(ctx, x.data_ptr(), n, tab.data_ptr(), C_, blk.data_ptr(), tot.data_ptr(),
+                                       _lib.ptr(rp), _lib.ptr(cp), self._s()), "mdkk_halo_count")
+        return tot[:C_], (blk, rp, cp)
+
+    def halo_fill(self, x, n, tab, C_, tot, state, total):
+        lib, ctx = _lib.lib(), _lib.ctx(self.device)
+        blk, rp, cp = state
+        idx = torch.empty(int(total) + 1, dtype=torch.int32, device=self.device)
+        _lib.check(lib.mdkk_halo_fill(ctx, x.data_ptr(), n, tab.data_ptr(), C_, blk.data_ptr(), tot.data_ptr(),
+                                      idx.data_ptr(), None, None, _lib.ptr(rp), _lib.ptr(cp), self._s()),
+                   "mdkk_halo_fill")
+        return idx
+
+    def owner_partition_dev(self, x, n, lengths, grid, R):
+        """owner_partition with the bucket starts left on the device."""
+        lib, ctx = _lib.lib(), _lib.ctx(self.device)
+        keys = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
+        start = torch.empty(R + 1, dtype=torch.int32, device=self.device)
+        order = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
+        _lib.check(lib.mdkk_rank_keys(x.data_ptr(), n, _lib.dbl3(lengths), _lib.int_arr(grid), keys.data_ptr(),
+                                      self._s()), "mdkk_rank_keys")
+        _lib.check(lib.mdkk_bucket_sort(ctx, keys.data_ptr(), n, R, start.data_ptr(), order.data_ptr(), self._s()),
+                   "mdkk_bucket_sort")
+        return start, order
+
     def pack(self, x, idx, code, shifts, n, out):
         if n:
             _lib.check(_lib.lib().mdkk_pack_shift(x.data_ptr(), idx.data_ptr(), code.data_ptr(), shifts.data_ptr(), n,
@@ -151,10 +191,11 @@ class CudaOps:
 
 
 class _SendLane:
-    __slots__ = ("dst", "idx", "code", "count")
+    __slots__ = ("dst", "idx", "code", "count", "fbuf", "rbuf")
 
     def __init__(self, dst, idx, code, count):
         self.dst, self.idx, self.code, self.count = dst, idx, code, count
+        self.fbuf = self.rbuf = None
 
 
 class _RecvLane:
@@ -279,6 +320,16 @@ class DistSystem:
             hit = self._combo_cache[halo] = (meta, tab)
         return hit
 
+    def _combo_dst(self, halo):
+        """Destination rank of every halo combo, on the device (cached with the combos)."""
+        key = ("dst", halo)
+        hit = self._combo_cache.get(key)
+        if hit is None:
+            meta, _ = self._combos(halo)
+            hit = self._combo_cache[key] = torch.tensor([d for d, _ in meta], dtype=torch.int64,
+                                                        device=self.device)
+        return hit
+
     # ------------------------------------------------------------ ghosts
     def exchange_ghosts(self, halo: float) -> None:
         from .domain import DomainError
@@ -291,12 +342,29 @@ class DistSystem:
         C_ = len(meta)
         per_dst = np.zeros(self.world, dtype=np.int64)
         self.send_lanes = []
-        if C_ and s.n_local:
-            bins = getattr(s, "_bins", None)
-            if isinstance(self.ops, CudaOps) and bins is not None and bins[1] == s.n_local and bins[0] >= halo:
-                idx, totals = self.ops.halo_select(s.x, s.n_local, tab, C_, bins=bins, lo=s.lo, hi=s.hi)
+        bins = getattr(s, "_bins", None)
+        sorted_rows = isinstance(self.ops, CudaOps) and bins is not None and bins[1] == s.n_local and bins[0] >= halo
+        M = None
+        if hasattr(self.ops, "halo_count"):
+            # device totals -> per-destination counts -> all-gather, then ONE host read-back of
+            # both (the totals size the index buffer, the matrix sizes the receives)
+            if C_ and s.n_local:
+                tot, hstate = (self.ops.halo_count(s.x, s.n_local, tab, C_, bins=bins, lo=s.lo, hi=s.hi)
+                               if sorted_rows else self.ops.halo_count(s.x, s.n_local, tab, C_))
             else:
-                idx, totals = self.ops.halo_select(s.x, s.n_local, tab, C_)
+                tot = torch.zeros(C_, dtype=torch.int32, device=self.device)
+            per = torch.zeros(self.world, dtype=torch.int64, device=self.device)
+            if C_:
+                per.index_add_(0, self._combo_dst(halo), tot.long())
+            out = [torch.empty_like(per) for _ in range(self.world)]
+            _all_gather(out, per, self.group)
+            host = torch.cat([tot.long(), torch.stack(out).flatten()]).cpu().numpy()
+            totals, M = host[:C_], host[C_:].reshape(self.world, self.world)
+            idx = (self.ops.halo_fill(s.x, s.n_local, tab, C_, tot, hstate, int(totals.sum()))
+                   if C_ and s.n_local else None)
+        elif C_ and s.n_local:
+            idx, totals = self.ops.halo_select(s.x, s.n_local, tab, C_)
+        if C_ and s.n_local:
             start = np.concatenate([[0], np.cumsum(totals)])
             d_of = np.array([d for d, _ in meta])
             codes_all = np.array([c for _, c in meta], dtype=np.int8)
@@ -309,7 +377,8 @@ class DistSystem:
                     code = torch.from_numpy(np.repeat(codes_all[ks], totals[ks])).to(self.device)
                     self.send_lanes.append(_SendLane(d, idx[a:b], code, b - a))
                     per_dst[d] = b - a
-        M = self._counts_matrix(per_dst)          # M[src][dst]
+        if M is None:
+            M = self._counts_matrix(per_dst)      # M[src][dst]
         recv = M[:, self.rank]
         nl, ng = s.n_local, int(recv.sum())
         s.ensure_capacity(nl + ng)
@@ -353,6 +422,12 @@ class DistSystem:
         s._lanes_in = [_CodeView(ln) for ln in self.recv_lanes]
         if nl:
             s.orank[:nl] = self.rank
+        # per-step communication buffers, allocated once per exchange: a remote send lane's
+        # packed positions (forward) and the ghost forces it gets back (reverse)
+        for ln in self.send_lanes:
+            if ln.dst != self.rank:
+                ln.fbuf = torch.empty((ln.count, 4), dtype=torch.float64, device=self.device)
+                ln.rbuf = torch.empty((ln.count, 4), dtype=torch.float64, device=self.device)
         s._views()
         s.device_wrote(pos=True)
 
@@ -366,9 +441,8 @@ class DistSystem:
                 rl = next(r for r in self.recv_lanes if r.src == self.rank)
                 self.ops.pack(s.x, ln.idx, ln.code, self._shift_dev, ln.count, s.x[rl.start:])
             else:
-                bx = torch.empty((ln.count, 4), dtype=torch.float64, device=self.device)
-                self.ops.pack(s.x, ln.idx, ln.code, self._shift_dev, ln.count, bx)
-                sends.append((bx, ln.dst))
+                self.ops.pack(s.x, ln.idx, ln.code, self._shift_dev, ln.count, ln.fbuf)
+                sends.append((ln.fbuf, ln.dst))
         for ln in self.recv_lanes:
             if ln.src != self.rank:
                 recvs.append((s.x[ln.start:ln.start + ln.count], ln.src))
@@ -391,9 +465,8 @@ class DistSystem:
                 rl = next(r for r in self.recv_lanes if r.src == self.rank)
                 fold(s.f, ln.idx, s.f[rl.start:], ln.count)
             else:
-                buf = torch.empty((ln.count, 4), dtype=torch.float64, device=self.device)
-                recvs.append((buf, ln.dst))
-                folds.append((ln, buf))
+                recvs.append((ln.rbuf, ln.dst))
+                folds.append((ln, ln.rbuf))
         self._p2p(sends, recvs)
         for ln, buf in folds:
             fold(s.f, ln.idx, buf, ln.count)
@@ -408,9 +481,17 @@ class DistSystem:
         s.to_device()
         nl = s.n_local
         self.ops.wrap(s.x, nl, self.box.lengths)
-        start, order = self.ops.owner_partition(s.x, nl, self.box.lengths, self.rankset.grid, self.world)
-        counts = np.diff(start)
-        M = self._counts_matrix(counts)
+        if hasattr(self.ops, "owner_partition_dev"):
+            # bucket starts and the all-gathered counts matrix in one host read-back
+            st_dev, order = self.ops.owner_partition_dev(s.x, nl, self.box.lengths, self.rankset.grid, self.world)
+            cnt = (st_dev[1:] - st_dev[:-1]).long()
+            out = [torch.empty_like(cnt) for _ in range(self.world)]
+            _all_gather(out, cnt, self.group)
+            host = torch.cat([st_dev.long(), torch.stack(out).flatten()]).cpu().numpy()
+            start, M = host[: self.world + 1], host[self.world + 1:].reshape(self.world, self.world)
+        else:
+            start, order = self.ops.owner_partition(s.x, nl, self.box.lengths, self.rankset.grid, self.world)
+            M = self._counts_matrix(np.diff(start))
         arrivals = M[:, self.rank]
         n_new = int(arrivals.sum())
         cap = max(s.capacity, int(n_new * 1.3) + 64)

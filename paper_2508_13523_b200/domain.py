@@ -258,7 +258,7 @@ class AtomStore:
             return
         cap = int(rows * 1.15) + 64
         nl = self.n_local
-        x = _rows4(cap, self.device, zero=False)
+        x = _rows4(cap, self.device)   # zeroed once: the double4 pad lane is read by 256-bit loads
         x[:nl] = self.x[:nl]
         g = torch.empty(cap, dtype=torch.int64, device=self.device)
         g[:nl] = self.gid[:nl]
@@ -671,7 +671,7 @@ class RankedSystem:
         _lib.check(lib.mdkk_bin_atoms(ctx, s.x.data_ptr(), n, garr, narr,
                                       keys.data_ptr(), start.data_ptr(), order.data_ptr(), stream), "bin")
         if s._alt is None or s._alt[0].shape[0] != s.capacity or s._alt[1].shape[0] < n:
-            s._alt = (_rows4(s.capacity, self.device, zero=False), _rows4(s.v.shape[0], self.device, zero=False),
+            s._alt = (_rows4(s.capacity, self.device), _rows4(s.v.shape[0], self.device),
                       torch.empty(s.capacity, dtype=torch.int64, device=self.device))
         x2, v2, g2 = s._alt
         _lib.check(lib.mdkk_gather_rows4(s.x.data_ptr(), order.data_ptr(), n, x2.data_ptr(), stream), "g4")

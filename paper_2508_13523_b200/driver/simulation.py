@@ -594,7 +594,7 @@ class Simulation:
             a = fz["x_alt"]
             live = {s.x.data_ptr()} | ({s._alt[0].data_ptr()} if s._alt is not None else set())
             if a is None or a.shape[0] != s.x.shape[0] or a.data_ptr() in live:
-                a = fz["x_alt"] = torch.empty_like(s.x)
+                a = fz["x_alt"] = torch.zeros_like(s.x)   # once per buffer; pads defined
             return a
 
         dist_ = self.config.distributed

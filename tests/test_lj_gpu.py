@@ -211,29 +211,27 @@ def test_c1_32k_trajectory_matches_reference(gpu, style):
     assert np.abs(snap - g[f"c1_{style}_final_pos_sub"]).max() < 1e-7
 
 
-# The reference's energy drift over 1000 NVE steps of the C1 melt (32,000 atoms, full
-# list, 1 rank), measured by running mdkk itself (SURVEY.md §8(c) "Parity tolerances",
-# BASELINE.md §2): max |E_tot - E_0| / |E_0| = 1.97e-3 (mostly steps 0-100, pairs
-# crossing the truncated, unshifted cutoff), final -1.51e-3.
-C1_REF_MAX_DRIFT = 1.97e-3
-
-
 @pytest.mark.parametrize("style", ["full", "half"])
 def test_c1_1000_step_drift_no_worse_than_reference(gpu, style):
-    """north_star: "energy-conservation drift over 1000 NVE steps no worse than the reference's"."""
+    """north_star: "energy-conservation drift over 1000 NVE steps no worse than the reference's".
+
+    The bound is the reference's own 1000-step run (tests/golden/lj_drift.npz, the C1 melt
+    through mdkk's Simulation): max |E_tot - E_0| / |E_0| = 1.9706e-3, reached at step 200,
+    where the two trajectories still agree point-wise.  The comparison allows 1e-9 relative
+    -- the measured point-wise agreement of the thermo rows over those steps -- instead of
+    the 2 % slack of round 1."""
     from paper_2508_13523_b200.driver import RunConfig, run_script
     c1 = ("units lj\nboundary p p p\nlattice fcc 0.8442\ncreate_box 20 20 20\ncreate_atoms\n"
           "mass 1.0\nvelocity 1.44 87287\npair_style lj/cut 2.5\npair_coeff 1.0 1.0\n"
           "timestep 0.005\nthermo 100\nrun 1000\n")
     sim = run_script(c1, RunConfig(list_style=style, newton=(style == "half")), log=None)
     rows = np.array(sim.results[-1].rows)
-    assert rows.shape[0] == 11 and np.isfinite(rows).all()
-    e0 = rows[0, 3]
-    drift = np.abs(rows[:, 3] - e0) / abs(e0)
-    assert drift.max() <= C1_REF_MAX_DRIFT   # north star: no worse than the reference's
-    # the first 100 steps are the reference's trajectory (pointwise, test above)
-    ref = golden("lj_runs.npz")[f"c1_{style}_rows"]
-    assert rows[1, 3] == pytest.approx(ref[-1, 3], rel=1e-8)
+    ref = golden("lj_drift.npz")[f"c1_{style}_rows1000"]
+    assert rows.shape == ref.shape == (11, 5) and np.isfinite(rows).all()
+    assert np.allclose(rows[:4, 1:], ref[:4, 1:], rtol=1e-9)     # steps 0-300: the same trajectory
+    drift = np.abs(rows[:, 3] - rows[0, 3]) / abs(rows[0, 3])
+    ref_drift = np.abs(ref[:, 3] - ref[0, 3]) / abs(ref[0, 3])
+    assert drift.max() <= ref_drift.max() * (1.0 + 1e-9)
 
 
 def test_distributed_system_single_rank_nccl_matches_in_process(gpu):
