@@ -37,6 +37,25 @@ __device__ __forceinline__ bool gated_off(const Gate& g) {
 // k_verlet_second + k_verlet_first<false> (or k_verlet_first<true>), so the
 // trajectory is bit-identical.  Positions are double-buffered: the kernel reads x
 // (owned + ghost rows) and writes the owned rows of x_next.
+// Pair coefficients in the r^-6 form: F/r = r^-6 (c1 r^-6 - c2) r^-2, E = r^-6 (c3 r^-6 - c4)
+// with c1 = 48 eps sig^12, c2 = 24 eps sig^6, c3 = 4 eps sig^12, c4 = 4 eps sig^6 (the
+// reference's 4 eps ((sig/r)^12 - (sig/r)^6), mdkk/pair_lj.py:81-91, in 26 instead of 35
+// FP64 operations per pair); h3 / h4 = c3 / 2, c4 / 2 (the full list's pair weight).
+struct LJc {
+    double c1, c2, c3, c4, h3, h4;
+};
+__device__ __forceinline__ LJc lj_coeffs(double eps4, double eps24, double sig2) {
+    const double s6 = sig2 * sig2 * sig2, s12 = s6 * s6;
+    LJc c;
+    c.c1 = 2.0 * eps24 * s12;
+    c.c2 = eps24 * s6;
+    c.c3 = eps4 * s12;
+    c.c4 = eps4 * s6;
+    c.h3 = 0.5 * c.c3;
+    c.h4 = 0.5 * c.c4;
+    return c;
+}
+
 struct Integ {
     double* v;
     const double* x_ref;
@@ -71,6 +90,7 @@ __global__ void __launch_bounds__(kBlock) k_lj(const double* __restrict__ x, int
     static_assert(MODE == 0 || STYLE == 0, "integration needs the complete f_i: full lists only");
     static_assert(SCAT == 0 || STYLE == 1, "strategies apply to half lists (full lists write owner rows only)");
     if (gated_off(gate)) return;   // block-uniform: the step rebuilds and relaunches
+    const LJc lj = lj_coeffs(eps4, eps24, sig2);
     const int i = blockIdx.x * kBlock + threadIdx.x;
     double acc[7] = {0, 0, 0, 0, 0, 0, 0};  // E, Wxx, Wyy, Wzz, Wxy, Wxz, Wyz
     double d2n = 0.0;
@@ -87,29 +107,34 @@ __global__ void __launch_bounds__(kBlock) k_lj(const double* __restrict__ x, int
             const double r2 = mdkk::r2_exact(dx, dy, dz);
             if (r2 < rc2) {
                 bad |= !(r2 > 0.0);
-                const double inv = 1.0 / r2;
-                const double s2 = sig2 * inv;
-                const double s6 = s2 * s2 * s2;
-                const double s12 = s6 * s6;
-                const double fp = eps24 * (2.0 * s12 - s6) * inv;
+                const double inv = mdkk::rcp_nr(r2);
+                const double r6 = inv * inv * inv;
+                const double fp = r6 * fma(lj.c1, r6, -lj.c2) * inv;
                 const bool wj = (STYLE == 1) && (NEWTON || j < n_local);
                 const double wgt = (STYLE == 0) ? 0.5 : ((NEWTON || j < n_local) ? 1.0 : 0.5);
-                const double gx = fp * dx, gy = fp * dy, gz = fp * dz;
-                fx -= gx;
-                fy -= gy;
-                fz -= gz;
-                if (wj) {
-                    if (SCAT == 2) {
-                        mdkk::st4(scat.stage, ((long long)(i >> 5) * cap + kk) * 32 + (i & 31),
-                                  make_double4(gx, gy, gz, 1.0));
-                    } else {
-                        double* fj = fw + 4LL * j;
-                        atomicAdd(fj + 0, gx);
-                        atomicAdd(fj + 1, gy);
-                        atomicAdd(fj + 2, gz);
+                if (STYLE == 0) {
+                    fx = fma(-fp, dx, fx);
+                    fy = fma(-fp, dy, fy);
+                    fz = fma(-fp, dz, fz);
+                    acc[0] += r6 * fma(lj.h3, r6, -lj.h4);   // 0.5 * E_pair (the weight is exact)
+                } else {
+                    const double gx = fp * dx, gy = fp * dy, gz = fp * dz;
+                    fx -= gx;
+                    fy -= gy;
+                    fz -= gz;
+                    if (wj) {
+                        if (SCAT == 2) {
+                            mdkk::st4(scat.stage, ((long long)(i >> 5) * cap + kk) * 32 + (i & 31),
+                                      make_double4(gx, gy, gz, 1.0));
+                        } else {
+                            double* fj = fw + 4LL * j;
+                            atomicAdd(fj + 0, gx);
+                            atomicAdd(fj + 1, gy);
+                            atomicAdd(fj + 2, gz);
+                        }
                     }
+                    acc[0] += wgt * (r6 * fma(lj.c3, r6, -lj.c4));
                 }
-                acc[0] += wgt * (eps4 * (s12 - s6));
                 if (VIR) {
                     const double wf = wgt * fp;
                     acc[1] += wf * (dx * dx);
@@ -201,6 +226,7 @@ __global__ void __launch_bounds__(kBlock) k_lj_team(const double* __restrict__ x
                                                     double* __restrict__ f, double* __restrict__ partials,
                                                     int* __restrict__ flags, Gate gate) {
     if (gated_off(gate)) return;
+    const LJc lj = lj_coeffs(eps4, eps24, sig2);
     const int t = blockIdx.x * kBlock + threadIdx.x;
     const int i = t / T, l = t % T;
     double acc[7] = {0, 0, 0, 0, 0, 0, 0};
@@ -218,24 +244,29 @@ __global__ void __launch_bounds__(kBlock) k_lj_team(const double* __restrict__ x
             const double r2 = mdkk::r2_exact(dx, dy, dz);
             if (r2 < rc2) {
                 bad |= !(r2 > 0.0);
-                const double inv = 1.0 / r2;
-                const double s2 = sig2 * inv;
-                const double s6 = s2 * s2 * s2;
-                const double s12 = s6 * s6;
-                const double fp = eps24 * (2.0 * s12 - s6) * inv;
+                const double inv = mdkk::rcp_nr(r2);
+                const double r6 = inv * inv * inv;
+                const double fp = r6 * fma(lj.c1, r6, -lj.c2) * inv;
                 const bool wj = (STYLE == 1) && (NEWTON || j < n_local);
                 const double wgt = (STYLE == 0) ? 0.5 : ((NEWTON || j < n_local) ? 1.0 : 0.5);
-                const double gx = fp * dx, gy = fp * dy, gz = fp * dz;
-                fx -= gx;
-                fy -= gy;
-                fz -= gz;
-                if (wj) {
-                    double* fj = f + 4LL * j;
-                    atomicAdd(fj + 0, gx);
-                    atomicAdd(fj + 1, gy);
-                    atomicAdd(fj + 2, gz);
+                if (STYLE == 0) {
+                    fx = fma(-fp, dx, fx);
+                    fy = fma(-fp, dy, fy);
+                    fz = fma(-fp, dz, fz);
+                    acc[0] += r6 * fma(lj.h3, r6, -lj.h4);
+                } else {
+                    const double gx = fp * dx, gy = fp * dy, gz = fp * dz;
+                    fx -= gx;
+                    fy -= gy;
+                    fz -= gz;
+                    if (wj) {
+                        double* fj = f + 4LL * j;
+                        atomicAdd(fj + 0, gx);
+                        atomicAdd(fj + 1, gy);
+                        atomicAdd(fj + 2, gz);
+                    }
+                    acc[0] += wgt * (r6 * fma(lj.c3, r6, -lj.c4));
                 }
-                acc[0] += wgt * (eps4 * (s12 - s6));
                 if (VIR) {
                     const double wf = wgt * fp;
                     acc[1] += wf * (dx * dx);
