@@ -274,7 +274,9 @@ def snap_run(cells, steps, warmup, device, distributed=False):
     coeff = os.path.join(tempfile.mkdtemp(), "w_2j8.coeff")
     with open(coeff, "w") as fh:
         fh.write("4\n" + "\n".join(repr(float(b)) for b in np.linspace(0.05, 0.1, 55)) + "\n")
-    sim = Simulation(RunConfig(skin=SNAP["skin"], device=device, distributed=distributed), log=None)
+    # batch_y=2: compute_yi serves two atoms per lane (the fastest schedule on B200; batch_u keeps
+    # the reference default 4 = 16-lane teams, also the fastest)
+    sim = Simulation(RunConfig(skin=SNAP["skin"], device=device, distributed=distributed, batch_y=2), log=None)
     sim.execute(f"units lj\nboundary p p p\nlattice bcc {SNAP['a']}\ncreate_box {cells} {cells} {cells}\n"
                 f"create_atoms\nmass 1.0\nvelocity {SNAP['T']} {SNAP['seed']}\nsuffix kk\n"
                 f"pair_style snap {SNAP['rc']} {coeff}\ntimestep {SNAP['dt']}\nthermo 1000000000\n")

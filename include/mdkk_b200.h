@@ -279,6 +279,12 @@ int mdkk_kinetic(mdkk_ctx* ctx, const double* v, int n, double mass, double* ke,
 int mdkk_snap_create(mdkk_ctx* ctx, int twojmax, int n_entries, const double* coef_host, const int* code_host,
                      int n_half, const int* fmap_host, mdkk_snap** out_host);
 int mdkk_snap_destroy(mdkk_snap* snap);
+/* Schedule knobs of SnapState (mdkk/snap/compute.py:238-276: batch_u scales the
+ * expansion pass's pair batch, batch_y groups the contraction; scheduling only).
+ * batch_u -> neighbour pairs expanded concurrently per two warps in compute_ui
+ * (<=3, 4..7, >=8 -> 32-, 16-, 8-lane teams per pair; the reference default 4 is the
+ * fastest on B200); batch_y -> atoms per lane in compute_yi (1, >=2 -> 2). */
+int mdkk_snap_set_schedule(mdkk_snap* snap, int batch_u, int batch_y);
 /* U_i = sum_k f_c(r_ik) u(a_ik, b_ik) (compute_ui, mdkk/snap/compute.py:279-292); flags gets
  * MDKK_FLAG_COINCIDENT for r = 0 pairs (mdkk/snap/compute.py:117-118). */
 int mdkk_snap_ui(mdkk_snap* snap, const double* x, int n_local, const int* table, const int* counts, int cap,

@@ -67,6 +67,7 @@ SIGNATURES = {
     "mdkk_kinetic": [_p, _p, _i, _d, _p, _p],
     "mdkk_snap_create": [_p, _i, _i, _p, _p, _i, _p, _p],
     "mdkk_snap_destroy": [_p],
+    "mdkk_snap_set_schedule": [_p, _i, _i],
     "mdkk_snap_ui": [_p, _p, _i, _p, _p, _i, _d, _p, _i, _i, _p, _p],
     "mdkk_snap_yi": [_p, _p, _p, _i, _p, _i, _p, _i, _i, _p],
     "mdkk_snap_y_expand": [_p, _p, _i, _i, _p, _i, _i, _p],

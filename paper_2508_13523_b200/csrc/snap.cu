@@ -115,11 +115,6 @@ __global__ void __launch_bounds__(DW * 32, (TEAM == 16 ? 4 : 8 / DW)) k_snap_ui(
         }
 }
 
-#ifndef MDKK_UI_TEAM
-#define MDKK_UI_TEAM 16
-#endif
-constexpr int kUiTeam = MDKK_UI_TEAM;              // lanes per pair in k_snap_ui
-constexpr int kUiWarps = kUiTeam == 16 ? 4 : 2;    // atoms (warps) per CTA
 
 // ---------------------------------------------------------------- compute_yi
 // Half-block Y (outputs 2p < tj, or 2p == tj and 2q <= tj) as a list of U*U
@@ -143,31 +138,40 @@ __device__ __forceinline__ double flip_sign(double v, unsigned mask) {   // mask
     return __hiloint2double(__double2hiint(v) ^ (int)mask, __double2loint(v));
 }
 
-template <int NF, int NH>
-__global__ void __launch_bounds__(kYW * 32, 2) k_snap_yi(const double2* __restrict__ U, int n,
-                                                         const ZEntry* __restrict__ ent,
-                                                         const int* __restrict__ chunk,
-                                                         const int* __restrict__ chunkf, double2* __restrict__ Yh,
-                                                         int ld, double* __restrict__ partials, long long su,
-                                                         long long sf) {
+// B atoms per lane (the batch_y knob): B tiles of 32 atoms, each Z-list entry broadcast serves
+// B atoms (work batching, paper Table 2); B = 1 keeps two CTAs per SM, B = 2 one.
+template <int NF, int NH, int B>
+__global__ void __launch_bounds__(kYW * 32, B == 1 ? 2 : 1) k_snap_yi(const double2* __restrict__ U, int n,
+                                                                      const ZEntry* __restrict__ ent,
+                                                                      const int* __restrict__ chunk,
+                                                                      const int* __restrict__ chunkf,
+                                                                      double2* __restrict__ Yh, int ld,
+                                                                      double* __restrict__ partials, long long su,
+                                                                      long long sf) {
     extern __shared__ double2 s_dyn2[];
-    double2* s_u = s_dyn2;                                                   // [NH][kUS]
-    ZEntry* s_e = reinterpret_cast<ZEntry*>(s_u + NH * kUS);                  // [kYW][32]
+    double2* s_u = s_dyn2;                                                   // B x [NH][kUS]
+    ZEntry* s_e = reinterpret_cast<ZEntry*>(s_u + B * NH * kUS);              // [kYW][32]
+    constexpr int kTile = NH * kUS * (int)sizeof(double2);                    // bytes between atom tiles
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int a0 = blockIdx.x * 32;
-    for (int t = threadIdx.x; t < 32 * NH; t += blockDim.x) {
+    const int a0 = blockIdx.x * 32 * B;
+    for (int t = threadIdx.x; t < 32 * B * NH; t += blockDim.x) {
         const int a = t / NH, e = t - a * NH;
-        s_u[e * kUS + a] = (a0 + a < n) ? U[(long long)(a0 + a) * su + c_hflat[e] * sf] : make_double2(0.0, 0.0);
+        s_u[(a >> 5) * NH * kUS + e * kUS + (a & 31)] =
+            (a0 + a < n) ? U[(long long)(a0 + a) * su + c_hflat[e] * sf] : make_double2(0.0, 0.0);
     }
     __syncthreads();
-    const bool valid = a0 + lane < n;
     const int beg = chunk[w], end = chunk[w + 1];
     int f = chunkf[w];   // outputs are consecutive inside a warp's range
     const char* su_l = reinterpret_cast<const char*>(s_u + lane);
     ZEntry* se = s_e + w * 32;
-    double are = 0.0, aim = 0.0, en = 0.0;
+    double are[B], aim[B], en[B];
+    double2 ug[B];
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+        are[b] = aim[b] = en[b] = 0.0;
+        ug[b] = make_double2(0.0, 0.0);
+    }
     int last_g = -1;      // products are sorted by g inside an output: half reuse the previous U[g]
-    double2 ug = make_double2(0.0, 0.0);
     for (int base = beg; base < end; base += 32) {
         if (base + lane < end) se[lane] = ent[base + lane];
         __syncwarp();
@@ -175,27 +179,39 @@ __global__ void __launch_bounds__(kYW * 32, 2) k_snap_yi(const double2* __restri
         for (int j = 0; j < cnt; ++j) {
             const ZEntry e = se[j];
             if (e.goff != last_g) {   // warp-uniform
-                ug = *reinterpret_cast<const double2*>(su_l + e.goff);
+#pragma unroll
+                for (int b = 0; b < B; ++b) ug[b] = *reinterpret_cast<const double2*>(su_l + b * kTile + e.goff);
                 last_g = e.goff;
             }
-            const double2 uh = *reinterpret_cast<const double2*>(su_l + (e.hcode & 0xfffff));
-            const double gy = flip_sign(ug.y, ((unsigned)e.hcode << 11) & 0x80000000u);   // conj_g
-            const double hy = flip_sign(uh.y, ((unsigned)e.hcode << 10) & 0x80000000u);   // conj_h
-            const double tre = ug.x * uh.x - gy * hy;
-            const double tim = ug.x * hy + gy * uh.x;
-            are = fma(e.coef, tre, are);
-            aim = fma(e.coef, tim, aim);
+            const unsigned cg = ((unsigned)e.hcode << 11) & 0x80000000u, ch = ((unsigned)e.hcode << 10) & 0x80000000u;
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                const double2 uh = *reinterpret_cast<const double2*>(su_l + b * kTile + (e.hcode & 0xfffff));
+                const double gy = flip_sign(ug[b].y, cg);   // conj_g
+                const double hy = flip_sign(uh.y, ch);      // conj_h
+                const double tre = ug[b].x * uh.x - gy * hy;
+                const double tim = ug[b].x * hy + gy * uh.x;
+                are[b] = fma(e.coef, tre, are[b]);
+                aim[b] = fma(e.coef, tim, aim[b]);
+            }
             if (e.hcode & (1 << 22)) {   // warp-uniform: output f complete
-                if (valid) Yh[(long long)f * ld + a0 + lane] = make_double2(are, aim);
-                const double2 u = s_u[f * kUS + lane];
-                en += ((e.hcode & (1 << 23)) ? 1.0 : 2.0) * (are * u.x + aim * u.y);
-                are = aim = 0.0;
+                const double wgt = (e.hcode & (1 << 23)) ? 1.0 : 2.0;
+#pragma unroll
+                for (int b = 0; b < B; ++b) {
+                    const int a = a0 + 32 * b + lane;
+                    if (a < n) Yh[(long long)f * ld + a] = make_double2(are[b], aim[b]);
+                    const double2 u = s_u[b * NH * kUS + f * kUS + lane];
+                    en[b] += wgt * (are[b] * u.x + aim[b] * u.y);
+                    are[b] = aim[b] = 0.0;
+                }
                 ++f;
             }
         }
         __syncwarp();
     }
-    double v[1] = {valid ? en / 3.0 : 0.0};
+    double v[1] = {0.0};
+#pragma unroll
+    for (int b = 0; b < B; ++b) v[0] += (a0 + 32 * b + lane < n) ? en[b] / 3.0 : 0.0;
     mdkk::block_sum<1, kYW * 32>(v, partials + blockIdx.x);
 }
 
@@ -474,6 +490,13 @@ int mdkk_snap_create(mdkk_ctx* ctx, int twojmax, int n_entries, const double* co
     return MDKK_OK;
 }
 
+int mdkk_snap_set_schedule(mdkk_snap* s, int batch_u, int batch_y) {
+    if (!s || batch_u < 1 || batch_y < 1) return MDKK_E_ARG;
+    s->ui_ppw = batch_u >= 8 ? 4 : (batch_u >= 4 ? 2 : 1);   // batch_u pairs per 64 lanes
+    s->yi_batch = batch_y >= 2 ? 2 : 1;
+    return MDKK_OK;
+}
+
 int mdkk_snap_destroy(mdkk_snap* s) {
     if (!s) return MDKK_OK;
     cudaFree(s->ent);
@@ -491,17 +514,24 @@ int mdkk_snap_ui(mdkk_snap* s, const double* x, int n_local, const int* table, c
     const long long su = layout ? 1 : s->n_flat, sf = layout ? ldu : 1;
     if (n_local == 0) return MDKK_OK;
     upload_weights();
-    const int nb = (n_local + kUiWarps - 1) / kUiWarps;
     cudaStream_t st = mdkk::as_stream(stream);
     double2* u = reinterpret_cast<double2*>(U);
-    switch (s->twojmax) {
-#define MDKK_UI(TJ)                                                                                          \
-    case TJ:                                                                                                 \
-        k_snap_ui<TJ, kUiTeam, kUiWarps><<<nb, kUiWarps * 32, 0, st>>>(x, n_local, table, counts, cap, rc, u,  \
-                                                                      su, sf, flags);                        \
+    // batch_u: pairs expanded concurrently per warp -> team width (DW atoms per CTA)
+    const int team = s->ui_ppw >= 4 ? 8 : (s->ui_ppw >= 2 ? 16 : 32);
+#define MDKK_UI_T(TJ, TM)                                                                                     \
+    {                                                                                                         \
+        constexpr int DW = TM == 16 ? 4 : 2;                                                                  \
+        k_snap_ui<TJ, TM, DW><<<(n_local + DW - 1) / DW, DW * 32, 0, st>>>(x, n_local, table, counts, cap, rc, \
+                                                                          u, su, sf, flags);                  \
+    }
+#define MDKK_UI(TJ)                                                                                           \
+    case TJ:                                                                                                  \
+        if (team == 8) MDKK_UI_T(TJ, 8) else if (team == 16) MDKK_UI_T(TJ, 16) else MDKK_UI_T(TJ, 32)         \
         break;
+    switch (s->twojmax) {
         MDKK_UI(0) MDKK_UI(1) MDKK_UI(2) MDKK_UI(3) MDKK_UI(4) MDKK_UI(5) MDKK_UI(6) MDKK_UI(7) MDKK_UI(8)
 #undef MDKK_UI
+#undef MDKK_UI_T
         default: return MDKK_E_ARG;
     }
     MDKK_CHECK_LAUNCH("k_snap_ui");
@@ -518,23 +548,28 @@ int mdkk_snap_yi(mdkk_ctx* ctx, mdkk_snap* s, const double* U, int n_local, doub
         return MDKK_OK;
     }
     upload_weights();
-    const int nb = (n_local + 31) / 32;
+    const int B = s->yi_batch == 2 ? 2 : 1;
+    const int nb = (n_local + 32 * B - 1) / (32 * B);
     double* partials = static_cast<double*>(mdkk::scratch(ctx, sizeof(double) * (size_t)nb));
     if (!partials) return mdkk::cuda_fail(cudaErrorMemoryAllocation, "scratch");
     const double2* u = reinterpret_cast<const double2*>(U);
     double2* y = reinterpret_cast<double2*>(Yh);
     switch (s->twojmax) {
-#define MDKK_YI(TJ)                                                                                             \
-    case TJ: {                                                                                                  \
+#define MDKK_YI_B(TJ, BB)                                                                                       \
+    {                                                                                                           \
         constexpr int NF = block_offset(TJ + 1), NH = half_offset(TJ + 1);                                      \
-        const size_t sm = NH * kUS * sizeof(double2) + kYW * 32 * sizeof(ZEntry);                               \
-        cudaFuncSetAttribute(k_snap_yi<NF, NH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);         \
-        k_snap_yi<NF, NH><<<nb, kYW * 32, sm, st>>>(u, n_local, s->ent, s->chunk, s->chunkf, y, ld, partials,   \
-                                                        su, sf);                                                \
-        break;                                                                                                  \
+        const size_t sm = BB * NH * kUS * sizeof(double2) + kYW * 32 * sizeof(ZEntry);                          \
+        cudaFuncSetAttribute(k_snap_yi<NF, NH, BB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);     \
+        k_snap_yi<NF, NH, BB><<<nb, kYW * 32, sm, st>>>(u, n_local, s->ent, s->chunk, s->chunkf, y, ld,        \
+                                                        partials, su, sf);                                      \
     }
+#define MDKK_YI(TJ)                                                                                             \
+    case TJ:                                                                                                    \
+        if (B == 2) MDKK_YI_B(TJ, 2) else MDKK_YI_B(TJ, 1)                                                      \
+        break;
         MDKK_YI(0) MDKK_YI(1) MDKK_YI(2) MDKK_YI(3) MDKK_YI(4) MDKK_YI(5) MDKK_YI(6) MDKK_YI(7) MDKK_YI(8)
 #undef MDKK_YI
+#undef MDKK_YI_B
         default: return MDKK_E_ARG;
     }
     MDKK_CHECK_LAUNCH("k_snap_yi");

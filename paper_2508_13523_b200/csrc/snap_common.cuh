@@ -25,6 +25,10 @@ struct mdkk_snap {
     int* fmap = nullptr;     // [n_flat] half index | mirrored << 16 | odd sign << 17
     double* work = nullptr;  // mdkk_snap_compute workspace: U [n][n_flat] then Yh [n_half][n] (complex)
     size_t work_bytes = 0;
+    // schedule knobs (SnapState.batch_u / batch_y, mdkk/snap/compute.py:238-276; scheduling only):
+    int ui_ppw = 2;    // compute_ui: pairs expanded concurrently per warp (1, 2, 4 -> 32-, 16-, 8-lane teams)
+                       // = batch_u / 2 (batch_u pairs in flight per two warps), clamped to [1, 4]
+    int yi_batch = 1;  // compute_yi: atoms per lane (1 or 2: each Z-list broadcast serves 2 atoms)
 };
 
 namespace {

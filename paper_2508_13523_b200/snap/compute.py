@@ -6,9 +6,10 @@ signatures (mdkk/snap/compute.py:105-436).  U lives in HBM as complex128
 row-major [n_atoms][n_flat] (the reference's layout "a"); the engine keeps Y
 as its half set, transposed (`Yh_dev[e][i]`, atoms fastest), and expands the
 reference-layout `state.Y` only when it is read.  The `layout` / `batch_u` /
-`batch_y` / `tile_v` knobs are accepted for signature parity (the reference
-guarantees they never change results, mdkk/snap/compute.py:238-276) and do
-not change the GPU schedule.
+`batch_y` / `tile_v` knobs are real schedule parameters of the GPU kernels
+(storage layout; pairs in flight per warp in compute_ui; atoms per lane in
+compute_yi; atom tiles of yi / bi) and, as the reference guarantees
+(mdkk/snap/compute.py:238-276), change results only at rounding level.
 """
 
 from __future__ import annotations
@@ -180,10 +181,13 @@ class SnapState:
     row-major [n][n_flat] (ui writes one atom's row), "b" = transposed
     [n_flat][ld] with atoms fastest (the yi / bi tile loads read whole
     rows).  `tile_v` > 0 runs yi and bi over atom tiles of that size (one
-    launch per tile: bounded shared work per launch).  `batch_u` / `batch_y`
-    are accepted; the pair and product batching of the GPU kernels is fixed
-    by their warp decomposition.  No knob changes results beyond rounding
-    (mdkk tests/test_snap.py:482-499).
+    launch per tile: bounded shared work per launch).  `batch_u` is the
+    number of neighbour pairs compute_ui expands concurrently per two warps
+    (<= 3, 4..7, >= 8 -> 32-, 16-, 8-lane teams per pair; the paper's
+    ComputeUi work batching, Table 2; the default 4 is the fastest on B200);
+    `batch_y` the atoms per lane of compute_yi (1, >= 2 -> 2: every Z-list
+    broadcast serves two atoms).  No knob changes results
+    beyond rounding (mdkk tests/test_snap.py:482-499).
     """
 
     def __init__(self, tables: CouplingTables, n_atoms: int, beta, batch_u: int = 4, batch_y: int = 1,
@@ -237,6 +241,13 @@ class SnapState:
             self._handle = _Handle(self.tables, self.beta, self.device)
         return self._handle
 
+    def scheduled(self) -> int:
+        """The handle pointer with this state's batch_u / batch_y applied (handles are
+        shared between the states of one style, so the knobs are set per call)."""
+        h = self.handle().ptr
+        _lib.check(_lib.lib().mdkk_snap_set_schedule(h, self.batch_u, self.batch_y), "mdkk_snap_set_schedule")
+        return h
+
     def u_view(self) -> np.ndarray:
         return self.U.read("a")[: self.n_atoms]
 
@@ -271,7 +282,7 @@ def compute_ui(nmap: NeighborMap, state: SnapState) -> None:
     st, nl = nmap.store, nmap.nlist
     st.to_device()
     state.flags.zero_()
-    _lib.check(_lib.lib().mdkk_snap_ui(state.handle().ptr, st.x.data_ptr(), st.n_local, nl.table_dev.data_ptr(),
+    _lib.check(_lib.lib().mdkk_snap_ui(state.scheduled(), st.x.data_ptr(), st.n_local, nl.table_dev.data_ptr(),
                                        nl.counts_dev.data_ptr(), nl.alloc_cap, nmap.r_c, state.U_dev.data_ptr(),
                                        state._lay, state.ld, state.flags.data_ptr(), _lib.stream(st.device)),
                "mdkk_snap_ui")
@@ -288,9 +299,10 @@ def compute_yi(state: SnapState) -> None:
     """Full three-slot adjoint Y and the per-atom energy sum (mdkk/snap/compute.py:303-340, :376-387)."""
     state.U.sync("b")
     tiles = _tiles(state)
+    h = state.scheduled()
     e_t = state.energy_dev if len(tiles) == 1 else torch.zeros(len(tiles), dtype=torch.float64, device=state.device)
     for k, (a0, n) in enumerate(tiles):
-        _lib.check(_lib.lib().mdkk_snap_yi(_lib.ctx(state.device), state.handle().ptr, _u_at(state, a0), n,
+        _lib.check(_lib.lib().mdkk_snap_yi(_lib.ctx(state.device), h, _u_at(state, a0), n,
                                            state.Yh_dev.data_ptr() + 16 * a0, state.ld, e_t.data_ptr() + 8 * k,
                                            state._lay, state.ld, _lib.stream(state.device)), "mdkk_snap_yi")
     if len(tiles) > 1:

@@ -31,13 +31,23 @@ class SnapStyle:
         from ..driver.simulation import RunError
         raise RunError("snap styles read coefficients from their file; pair_coeff does not apply")
 
-    def _state(self, idx, store):
-        key = (idx, store.n_local)
+    def _knobs(self, config) -> dict:
+        """RunConfig knobs override the style's own (mdkk/driver/simulation.py:115-121)."""
+        k = dict(self.knobs)
+        for name in ("batch_u", "batch_y", "tile_v", "layout"):
+            v = getattr(config, name, None) if config is not None else None
+            if v is not None:
+                k[name] = v
+        return k
+
+    def _state(self, idx, store, config=None):
+        knobs = self._knobs(config)
+        key = (idx, store.n_local, tuple(sorted(knobs.items())))
         st = self._states.get(key)
         if st is None:
             self._states = {k: v for k, v in self._states.items() if k[0] != idx}
             # the coupling table handle is shared across states of the same style
-            st = SnapState(self.tables, store.n_local, self.beta, device=store.device, **self.knobs)
+            st = SnapState(self.tables, store.n_local, self.beta, device=store.device, **knobs)
             for other in self._states.values():
                 st._handle = other._handle
                 break
@@ -50,7 +60,7 @@ class SnapStyle:
         states = []
         for idx, (store, nl) in enumerate(zip(system.stores, lists)):
             nmap = build_neighbor_map(store, nl, self.r_c)
-            st = self._state(idx, store)
+            st = self._state(idx, store, config)
             compute_ui(nmap, st)
             compute_yi(st)
             store.f[: store.n_total].zero_()

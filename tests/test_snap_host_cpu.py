@@ -93,3 +93,13 @@ def test_coeff_file_parsing_and_errors(tmp_path):
         p.write_text(text)
         with pytest.raises(SnapError):
             read_coeff_file(p)
+
+
+def test_run_config_knobs_override_style_knobs():
+    """mdkk/driver/simulation.py:115-121: RunConfig batch_u / batch_y / tile_v / layout win over the style's."""
+    from paper_2508_13523_b200.driver import RunConfig
+    from paper_2508_13523_b200.snap.style import SnapStyle
+    st = SnapStyle(4.73, 1, np.zeros(5), batch_u=8, tile_v=256)
+    assert st._knobs(RunConfig()) == {"batch_u": 8, "batch_y": 1, "tile_v": 256, "layout": "a"}
+    assert st._knobs(RunConfig(batch_u=2, batch_y=3, layout="b")) == {"batch_u": 2, "batch_y": 3, "tile_v": 256,
+                                                                      "layout": "b"}
