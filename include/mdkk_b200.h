@@ -192,12 +192,22 @@ int mdkk_lj_force_neighbor(mdkk_ctx* ctx, const double* x, int n_local, const in
  * ghost rows are refreshed by the next pack) and *d2_next = max |x_next - x_ref|^2
  * (atomic max; caller-zeroed).  Bit-identical to mdkk_lj_force + mdkk_verlet_second
  * + mdkk_verlet_first.  Gates as mdkk_lj_force_gated (a gated-off launch changes
- * nothing). */
+ * nothing).  Halo overlap (one rank per GPU): part 1 computes only the clusters with
+ * part_flags[c] == 0 (launched while the ghost exchange is in flight; no reduction),
+ * part 2 the others and the energy reduction (same gate / arguments); part 0 = all. */
 int mdkk_lj_force_integrate(mdkk_ctx* ctx, const double* x, int n_local, const int* table, const int* counts,
                             int cap, int virial, double epsilon, double sigma, double rc, double* f, double* ev,
                             int* flags, const double* maxdisp2, double half_skin, const int* max_count,
                             int count_limit, int mode, double* v, const double* x_ref, double* x_next,
-                            double* d2_next, double dt, double h, void* stream);
+                            double* d2_next, double dt, double h, const unsigned char* part_flags, int part,
+                            void* stream);
+/* Boundary flags per 32-row cluster for the halo overlap (engine-internal; no reference
+ * counterpart): flags[c] = 1 when the cluster's bounding box lies within `halo` of a
+ * brick face [lo, hi) in a dimension of dims_mask (bit d: the neighbour bricks along d
+ * are other ranks).  halo = list cutoff + skin/2 keeps the flags valid until the next
+ * rebuild. */
+int mdkk_cluster_flags(const double* x, int n_local, const double* lo_host, const double* hi_host, double halo,
+                       int dims_mask, unsigned char* flags, void* stream);
 /* Speculative step launch (engine-internal pipelining): as mdkk_lj_force (mode 0) or
  * mdkk_lj_force_neighbor (mode 1), but the kernel does nothing when
  * sqrt(*maxdisp2) > half_skin -- the step's skin test, evaluated on the device in the

@@ -95,8 +95,9 @@ __device__ __forceinline__ double warp_min_d(double v) {
 }
 
 // Block-wide sum of K doubles per thread into out[K] (thread 0 holds result).
+// acc: add to out[k] (a second pass over the same blocks) instead of storing.
 template <int K, int BLOCK>
-__device__ __forceinline__ void block_sum(double (&v)[K], double* out) {
+__device__ __forceinline__ void block_sum(double (&v)[K], double* out, bool acc = false) {
     __shared__ double sm[BLOCK / 32][K];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
@@ -111,7 +112,7 @@ __device__ __forceinline__ void block_sum(double (&v)[K], double* out) {
         for (int k = 0; k < K; ++k) {
             double s = 0.0;
             for (int w = 0; w < BLOCK / 32; ++w) s += sm[w][k];
-            out[k] = s;
+            out[k] = acc ? out[k] + s : s;
         }
     }
 }

@@ -56,6 +56,11 @@ __device__ __forceinline__ LJc lj_coeffs(double eps4, double eps24, double sig2)
     return c;
 }
 
+//
+// Halo overlap (one rank per GPU): `part` 1 runs only the clusters whose flag is 0
+// (no partner can be a ghost from another rank: launched while the halo exchange is
+// in flight), `part` 2 the flagged ones once it has landed (its block partials add to
+// part 1's); part 0 = every cluster.  Each atom is computed in exactly one part.
 struct Integ {
     double* v;
     const double* x_ref;
@@ -63,6 +68,8 @@ struct Integ {
     double* d2_next;
     double dt;
     double h;
+    const unsigned char* part_flags;   // per 32-row cluster (mdkk_cluster_flags), parts 1 / 2
+    int part;
 };
 
 // Half-list partner-write deconfliction (compute_pair's `strategy`, the
@@ -94,7 +101,9 @@ __global__ void __launch_bounds__(kBlock) k_lj(const double* __restrict__ x, int
     const int i = blockIdx.x * kBlock + threadIdx.x;
     double acc[7] = {0, 0, 0, 0, 0, 0, 0};  // E, Wxx, Wyy, Wzz, Wxy, Wxz, Wyz
     double d2n = 0.0;
-    if (i < n_local) {
+    bool mine = true;   // warp-uniform: this warp's cluster belongs to the launched part
+    if (MODE > 0 && integ.part != 0 && i < n_local) mine = (integ.part_flags[i >> 5] != 0) == (integ.part == 2);
+    if (i < n_local && mine) {
         const double4 xi = mdkk::ld4(x, i);
         const int n = min(counts[i], cap);
         double fx = 0.0, fy = 0.0, fz = 0.0;
@@ -206,12 +215,36 @@ __global__ void __launch_bounds__(kBlock) k_lj(const double* __restrict__ x, int
         d2n = mdkk::warp_max(d2n);
         if ((threadIdx.x & 31) == 0) mdkk::atomic_max_nonneg(integ.d2_next, d2n);
     }
+    const bool add = MODE > 0 && integ.part == 2;
     if (VIR) {
-        mdkk::block_sum<7, kBlock>(acc, partials + 7LL * blockIdx.x);
+        mdkk::block_sum<7, kBlock>(acc, partials + 7LL * blockIdx.x, add);
     } else {
         double e1[1] = {acc[0]};
-        mdkk::block_sum<1, kBlock>(e1, partials + blockIdx.x);
+        mdkk::block_sum<1, kBlock>(e1, partials + blockIdx.x, add);
     }
+}
+
+// Boundary flags of the 32-row clusters for the halo overlap: 1 when the cluster's
+// bounding box comes within `halo` of a brick face in a dimension whose neighbour
+// bricks are other ranks (dims_mask bit d) -- only such clusters can list ghosts that
+// arrive by the exchange (mdkk/domain.py:246-293 selects ghosts within the halo of
+// the faces).  With halo = list cutoff + skin/2 the flags hold from any positions
+// between the build and the next rebuild (no atom has moved more than skin/2).
+__global__ void k_cluster_flags(const double* __restrict__ x, int n_local, double lox, double loy, double loz,
+                                double hix, double hiy, double hiz, double halo, int dims_mask,
+                                unsigned char* __restrict__ flags) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int c = i >> 5;
+    if (c * 32 >= n_local) return;
+    const double4 p = mdkk::ld4(x, i < n_local ? i : c * 32);
+    const double bnx = mdkk::warp_min_d(p.x), bxx = mdkk::warp_max(p.x);
+    const double bny = mdkk::warp_min_d(p.y), bxy = mdkk::warp_max(p.y);
+    const double bnz = mdkk::warp_min_d(p.z), bxz = mdkk::warp_max(p.z);
+    bool f = false;
+    if (dims_mask & 1) f |= bnx - halo < lox || bxx + halo >= hix;
+    if (dims_mask & 2) f |= bny - halo < loy || bxy + halo >= hiy;
+    if (dims_mask & 4) f |= bnz - halo < loz || bxz + halo >= hiz;
+    if ((threadIdx.x & 31) == 0) flags[c] = f ? 1 : 0;
 }
 
 // Neighbour-parallel variant (mode "neighbor", the lj/cut/opt default,
@@ -390,20 +423,23 @@ extern "C" int mdkk_lj_force_integrate(mdkk_ctx* ctx, const double* x, int n_loc
                                        double* f, double* ev, int* flags, const double* maxdisp2, double half_skin,
                                        const int* max_count, int count_limit, int mode, double* v,
                                        const double* x_ref, double* x_next, double* d2_next, double dt, double h,
-                                       void* stream) {
+                                       const unsigned char* part_flags, int part, void* stream) {
     if (!ctx || n_local < 0 || cap < 1 || mode < 1 || mode > 2 || !v) return MDKK_E_ARG;
+    if (part < 0 || part > 2 || (part && !part_flags)) return MDKK_E_ARG;
     if (mode == 2 && (!x_ref || !x_next || !d2_next || x_next == x)) return MDKK_E_ARG;
     cudaStream_t s = mdkk::as_stream(stream);
     if (n_local == 0) {
-        cudaMemsetAsync(ev, 0, 7 * sizeof(double), s);
+        if (part != 1) cudaMemsetAsync(ev, 0, 7 * sizeof(double), s);
         return MDKK_OK;
     }
     const int nb = mdkk::grid_for(n_local, kBlock);
+    // part 1 leaves its block partials in the scratch arena for part 2 (same launch shape, same
+    // stream, nothing in between uses the arena)
     double* partials = static_cast<double*>(mdkk::scratch(ctx, sizeof(double) * 7 * (size_t)nb));
     if (!partials) return mdkk::cuda_fail(cudaErrorMemoryAllocation, "scratch");
     const double e4 = 4.0 * epsilon, e24 = 24.0 * epsilon, s2 = sigma * sigma, rc2 = rc * rc;
     const Gate gate{maxdisp2, half_skin, max_count, count_limit};
-    const Integ integ{v, x_ref, x_next, d2_next, dt, h};
+    const Integ integ{v, x_ref, x_next, d2_next, dt, h, part_flags, part};
 #define MDKK_LJI(VR, MD)                                                                                        \
     k_lj<0, false, VR, MD><<<nb, kBlock, 0, s>>>(x, n_local, table, counts, cap, e4, e24, s2, rc2, f, partials,  \
                                                  flags, gate, integ)
@@ -414,9 +450,21 @@ extern "C" int mdkk_lj_force_integrate(mdkk_ctx* ctx, const double* x, int n_loc
     }
 #undef MDKK_LJI
     MDKK_CHECK_LAUNCH("k_lj (integrate)");
+    if (part == 1) return MDKK_OK;   // the reduction follows part 2
     if (!virial) cudaMemsetAsync(ev, 0, 7 * sizeof(double), s);
     mdkk::reduce_partials(partials, nb, virial ? 7 : 1, ev, s);
     MDKK_CHECK_LAUNCH("k_reduce_partials");
+    return MDKK_OK;
+}
+
+extern "C" int mdkk_cluster_flags(const double* x, int n_local, const double* lo_host, const double* hi_host,
+                                  double halo, int dims_mask, unsigned char* flags, void* stream) {
+    if (n_local < 0 || !lo_host || !hi_host || !(halo >= 0.0)) return MDKK_E_ARG;
+    if (n_local == 0) return MDKK_OK;
+    const long long nthreads = ((long long)n_local + 31) / 32 * 32;
+    k_cluster_flags<<<mdkk::grid_for(nthreads, 128), 128, 0, mdkk::as_stream(stream)>>>(
+        x, n_local, lo_host[0], lo_host[1], lo_host[2], hi_host[0], hi_host[1], hi_host[2], halo, dims_mask, flags);
+    MDKK_CHECK_LAUNCH("k_cluster_flags");
     return MDKK_OK;
 }
 

@@ -277,6 +277,12 @@ class DistSystem:
 
     def _p2p(self, sends, recvs):
         """One batched group of isend/irecv (tensor, peer) pairs; waits for completion."""
+        self._p2p_end(self._p2p_begin(sends, recvs))
+
+    def _p2p_begin(self, sends, recvs):
+        """Post the batched group; returns what `_p2p_end` completes.  Over NCCL the
+        transfers run on NCCL's stream behind the work queued so far, so kernels queued
+        before `_p2p_end` overlap them."""
         staged = _staged(self.group) and any(t.is_cuda for t, _ in list(sends) + list(recvs))
         if staged:
             sends = [(t.cpu(), p) for t, p in sends]
@@ -285,13 +291,37 @@ class DistSystem:
             host_recvs = recvs
         ops = [dist.P2POp(dist.isend, t, p, self.group) for t, p in sends if t.numel()]
         ops += [dist.P2POp(dist.irecv, t, p, self.group) for t, p in host_recvs if t.numel()]
-        if ops:
-            for req in dist.batch_isend_irecv(ops):
-                req.wait()
+        reqs = dist.batch_isend_irecv(ops) if ops else []
+        return reqs, (recvs, host_recvs) if staged else None
+
+    def _p2p_end(self, pending) -> None:
+        reqs, staged = pending
+        for req in reqs:
+            req.wait()   # NCCL: the current stream waits for the transfers (no host block)
         if staged:
+            recvs, host_recvs = staged
             for (t, _), (h, _) in zip(recvs, host_recvs):
                 if t.numel():
                     t.copy_(h)
+
+    def remote_dims(self) -> int:
+        """Bit d set when the bricks along d are more than one (ghosts across those faces
+        come from other ranks by the exchange; along the others they are periodic
+        self-images packed locally)."""
+        return sum(1 << d for d in range(3) if int(self.rankset.grid[d]) > 1)
+
+    def cluster_flags(self, nl, halo: float) -> torch.Tensor:
+        """Per-cluster boundary flags of `nl` for the halo overlap (mdkk_cluster_flags)."""
+        s = self.store
+        ncl = (s.n_local + 31) // 32
+        fl = getattr(nl, "_part_flags", None)
+        if fl is None:
+            fl = torch.ones(max(ncl, 1), dtype=torch.uint8, device=self.device)
+            _lib.check(_lib.lib().mdkk_cluster_flags(s.x.data_ptr(), s.n_local, _lib.dbl3(s.lo), _lib.dbl3(s.hi),
+                                                     float(halo), self.remote_dims(), fl.data_ptr(),
+                                                     _lib.stream(self.device)), "mdkk_cluster_flags")
+            nl._part_flags = fl
+        return fl
 
     def _counts_matrix(self, mine: np.ndarray) -> np.ndarray:
         """All-gather of every rank's per-destination counts -> [src][dst]."""
@@ -433,6 +463,16 @@ class DistSystem:
 
     def forward_comm(self) -> None:
         """ghost x = owner x + shift: pack -> NCCL send/recv into ghost rows (mdkk/domain.py:295-305)."""
+        self.forward_comm_end(self.forward_comm_begin())
+
+    def forward_comm_end(self, pending) -> None:
+        self._p2p_end(pending)
+        if self.store.n_ghost:
+            self.store.device_wrote(pos=True)
+
+    def forward_comm_begin(self):
+        """Pack and post the halo exchange; `forward_comm_end` completes it (kernels
+        queued in between overlap the transfers)."""
         s = self.store
         s.to_device()
         sends, recvs = [], []
@@ -446,9 +486,7 @@ class DistSystem:
         for ln in self.recv_lanes:
             if ln.src != self.rank:
                 recvs.append((s.x[ln.start:ln.start + ln.count], ln.src))
-        self._p2p(sends, recvs)
-        if s.n_ghost:
-            s.device_wrote(pos=True)
+        return self._p2p_begin(sends, recvs)
 
     def reverse_comm(self, ordered: bool = False) -> None:
         """Ghost forces back to owners, folded with atomics; ghost rows zeroed (mdkk/domain.py:307-322).

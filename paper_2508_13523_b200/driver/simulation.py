@@ -105,8 +105,10 @@ class LJStyle:
             self._flags = torch.zeros(1, dtype=torch.int32, device=dev)
             self._slot = 0
         # two energy slots used in turn: a step's returned energy stays valid while the
-        # next step's (speculative) launch is already queued (the per-step non-finite check)
-        self._slot ^= 1
+        # next step's (speculative) launch is already queued (the per-step non-finite check);
+        # a halo-overlap part 1 writes no energy (part 2 reduces both) and keeps the slot
+        if integ is None or integ.get("part", 0) != 1:
+            self._slot ^= 1
         evs, flags = self._evs[self._slot], self._flags
         half = False
         for k, (s, nl) in enumerate(zip(system.stores, lists)):
@@ -598,6 +600,9 @@ class Simulation:
             return a
 
         dist_ = self.config.distributed
+        # one rank per GPU with other ranks across some faces: overlap the halo exchange
+        overlap = bool(dist_ and getattr(self.system, "world", 1) > 1 and self.system.remote_dims())
+        overlap_halo = self.style.r_c + self.config.skin + 0.5 * self.config.skin * (1.0 + 1e-9) + 1e-12
 
         def global_max(k):   # one rank per GPU: every rank gates and decides on the same maximum
             if dist_:
@@ -620,14 +625,24 @@ class Simulation:
             nxt = 1 - cur
             xa = x_alt() if mode == 2 else None
 
-            def launch(gated):
-                if mode == 2:
+            def launch(gated, part=0):
+                if mode == 2 and part != 2:
                     d2[nxt:nxt + 1].zero_()
-                integ = dict(mode=mode, x_next=xa, d2_next=d2[nxt:nxt + 1], dt=self.dt, h=h)
+                integ = dict(mode=mode, x_next=xa, d2_next=d2[nxt:nxt + 1], dt=self.dt, h=h, part=part)
+                if part:
+                    integ["flags"] = self.system.cluster_flags(self.lists[0], overlap_halo)
                 return self._forces_device(gate=d2[cur:cur + 1] if gated else None, gate_limit=half, integ=integ)
 
-            self.system.forward_comm()                 # speculative halo refresh
-            e = launch(True)                           # speculative force + integration
+            if overlap:
+                # halo overlap: the clusters that list no exchanged ghost run while the
+                # exchange is in flight, the boundary clusters once it has landed
+                pending = self.system.forward_comm_begin()
+                launch(True, part=1)
+                self.system.forward_comm_end(pending)
+                e = launch(True, part=2)
+            else:
+                self.system.forward_comm()             # speculative halo refresh
+                e = launch(True)                       # speculative force + integration
             if mode == 2:
                 global_max(nxt)
                 read_back(nxt)

@@ -137,6 +137,7 @@ def lj_force_rank(store, nl: NeighborList, params: PairParams, ev: torch.Tensor,
             pend[0].data_ptr() if pend is not None else None, nl.alloc_cap, integ["mode"], store.v.data_ptr(),
             nl.ref_dev.data_ptr(), integ["x_next"].data_ptr() if integ["mode"] == 2 else None,
             integ["d2_next"].data_ptr() if integ["mode"] == 2 else None, integ["dt"], integ["h"],
+            integ["flags"].data_ptr() if integ.get("part") else None, int(integ.get("part", 0)),
             _lib.stream(dev)), "mdkk_lj_force_integrate")
         return
     if gate is not None or pend is not None:

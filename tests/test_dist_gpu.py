@@ -21,7 +21,7 @@ pytestmark = pytest.mark.gpu
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
-LJ = ("units lj\nboundary p p p\nlattice fcc 0.8442\ncreate_box 8 8 8\ncreate_atoms\nmass 1.0\n"
+LJ = ("units lj\nboundary p p p\nlattice fcc 0.8442\ncreate_box 16 16 16\ncreate_atoms\nmass 1.0\n"
       "velocity 1.44 87287\npair_style lj/cut 2.5\npair_coeff 1.0 1.0\ntimestep 0.005\nthermo 10\nrun 40\n")
 
 
@@ -51,6 +51,9 @@ def _worker(rank, world, port, coeff, out):
             sim = run_script(LJ, RunConfig(list_style=style, newton=(style == "half"),
                                                                    distributed=True, device="cuda:0"), log=None)
             res[f"lj_{style}"] = np.array(sim.results[-1].rows)
+            if style == "full":   # the halo-overlap path ran: interior clusters, then boundary ones
+                fl = getattr(sim.lists[0], "_part_flags", None)
+                res["overlap"] = np.array([-1.0 if fl is None else float(fl.float().mean().item())])
         sim = run_script(_snap_script(coeff), RunConfig(distributed=True, device="cuda:0"), log=None)
         res["snap"] = np.array(sim.results[-1].rows)
         if rank == 0:
@@ -74,6 +77,9 @@ def test_distributed_two_ranks_on_one_gpu(gpu, tmp_path):
         p.join(300)
         assert p.exitcode == 0
     got = np.load(out)
+    # full-list LJ took the split (interior while the exchange is in flight, then boundary)
+    # launch: flags exist and both parts are non-empty for the 16^3-cell brick pair
+    assert 0.0 < got["overlap"][0] < 1.0, got["overlap"]
     for style in ("full", "half"):
         ref = np.array(run_script(LJ, RunConfig(n_ranks=2, list_style=style,
                                                                         newton=(style == "half")),
