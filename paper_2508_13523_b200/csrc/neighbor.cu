@@ -8,7 +8,12 @@
 //   3. each lane scans the union (broadcast loads: one wavefront per candidate
 //      per warp) and keeps j != i with r^2 < bc^2 (strict, same rounding as
 //      the reference) passing the style predicate (mdkk/neighbor.py:134-179).
+// Full lists use the streaming variant k_nbr_build_full (union members in a
+// 128-entry ring, tested block by block while the cell rows stream); half lists
+// use k_nbr_build (whole union staged, gids / owner ranks in shared memory).
 // Output: int32 cluster-blocked table [ncl][cap][32] of row indices + counts.
+#include <type_traits>
+
 #include "cluster.cuh"
 
 namespace {
@@ -39,8 +44,9 @@ __global__ void k_cell_positions(const double* __restrict__ x, const int* __rest
                                  float4* __restrict__ xs) {
     int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= n) return;
-    const double4 p = mdkk::ld4(x, cell_atoms[s]);
-    xs[s] = make_float4((float)p.x, (float)p.y, (float)p.z, 0.f);
+    const int j = cell_atoms[s];
+    const double4 p = mdkk::ld4(x, j);
+    xs[s] = make_float4((float)p.x, (float)p.y, (float)p.z, __int_as_float(j));   // .w = the row
 }
 
 // Binning merge (engine rebuilds): the owned rows are already sorted by cell on this
@@ -94,6 +100,22 @@ __device__ __forceinline__ void r2_pair(const float* px, const float* py, const 
     const unsigned long long x = *reinterpret_cast<const unsigned long long*>(px);
     const unsigned long long y = *reinterpret_cast<const unsigned long long*>(py);
     const unsigned long long z = *reinterpret_cast<const unsigned long long*>(pz);
+    unsigned long long dx, dy, dz, r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(dx) : "l"(x), "l"(xi2));
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(dy) : "l"(y), "l"(yi2));
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(dz) : "l"(z), "l"(zi2));
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(dx), "l"(dx));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(dy), "l"(dy), "l"(r));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(dz), "l"(dz), "l"(r));
+    asm("mov.b64 {%0,%1}, %2;" : "=f"(r0), "=f"(r1) : "l"(r));
+}
+
+// the same on register operands (an LDS.128 of a pair-interleaved union entry
+// already holds (x0, x1) and (y0, y1) as register pairs)
+__device__ __forceinline__ void r2_pair_v(float x0, float x1, float y0, float y1, float z0, float z1,
+                                          unsigned long long xi2, unsigned long long yi2, unsigned long long zi2,
+                                          float& r0, float& r1) {
+    const unsigned long long x = f32x2(x0, x1), y = f32x2(y0, y1), z = f32x2(z0, z1);
     unsigned long long dx, dy, dz, r;
     asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(dx) : "l"(x), "l"(xi2));
     asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(dy) : "l"(y), "l"(yi2));
@@ -347,6 +369,252 @@ __global__ void __launch_bounds__(kWarps * 32) k_nbr_build(
     if (lane == 0 && mc > 0) atomicMax(max_count, mc);
 }
 
+// ---------------------------------------------------------------------------
+// Full-list build (streaming): the cluster / union scheme of k_nbr_build with its
+// two stalls removed (half lists keep k_nbr_build: their ghost-partner rules need
+// the staged gids / owner ranks).
+//  * The cell rows stream through a two-deep software pipeline of 64-row
+//    batches (the next batch's loads are in flight while the current one is
+//    filtered and tested), reading only the cell-ordered FP32 copy xs (.w = the
+//    row), so no load waits on another.
+//  * Union members go to a 128-member ring in shared memory with their FP32
+//    cluster-relative coordinates and row (16 B, pair-interleaved: one LDS.128
+//    per coordinate pair); every full 32-member block is tested as soon as it
+//    exists, so the per-lane test overlaps the union scan and shared memory per
+//    warp stays at 2 KB (occupancy is set by registers).  FP64 positions are
+//    read only for the thin shell |r^2 - bc^2| < M that FP32 cannot decide.
+//  * The cluster's own rows are not union members: a 32-step shuffle pass tests
+//    them first, so the union test needs no j != i check.
+// Table rows: own-cluster partners first, then union members in union (cell)
+// order, each 32-member block's certain partners before its exactly-tested shell.
+constexpr int kW2 = 4;       // clusters (warps) per CTA
+constexpr int kRing = 128;   // union ring per warp (a block of 32 + two batches of 32 pending)
+
+struct __align__(16) UxY {   // union members 2p, 2p+1: x0, x1, y0, y1
+    float x0, x1, y0, y1;
+};
+struct __align__(16) UzJ {   // z0, z1, row0, row1
+    float z0, z1;
+    int j0, j1;
+};
+
+__global__ void __launch_bounds__(kW2 * 32, 1) k_nbr_build_full(
+    const double* __restrict__ x, int n_local, Grid g, const int* __restrict__ cell_start, double bc, double bc2,
+    int cap, int* __restrict__ table, int* __restrict__ counts, int* __restrict__ max_count,
+    const float4* __restrict__ xs) {
+    __shared__ UxY s_ra[kW2][kRing / 2];
+    __shared__ UzJ s_rb[kW2][kRing / 2];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    UxY* sa = s_ra[w];
+    UzJ* sb = s_rb[w];
+    float* fa = reinterpret_cast<float*>(sa);
+    float* fb = reinterpret_cast<float*>(sb);
+    int* jb = reinterpret_cast<int*>(sb);
+    const int c = blockIdx.x * kW2 + w;
+    const int ncl = (n_local + 31) >> 5;
+    if (c >= ncl) return;
+    const int c0 = c * 32;
+    const int nown = min(32, n_local - c0);   // the cluster's owned rows [c0, c0 + nown)
+    const int i = c0 + lane;
+    const bool valid = lane < nown;
+    const double4 xi = mdkk::ld4(x, valid ? i : c0);
+    // 1. cluster bounding box, the cells it can reach, FP32 frame at its center
+    const double bmin_x = mdkk::warp_min_d(xi.x), bmax_x = mdkk::warp_max(xi.x);
+    const double bmin_y = mdkk::warp_min_d(xi.y), bmax_y = mdkk::warp_max(xi.y);
+    const double bmin_z = mdkk::warp_min_d(xi.z), bmax_z = mdkk::warp_max(xi.z);
+    const int3 clo = mdkk::cell_of(g, bmin_x - bc, bmin_y - bc, bmin_z - bc);
+    const int3 chi = mdkk::cell_of(g, bmax_x + bc, bmax_y + bc, bmax_z + bc);
+    const double ccx = 0.5 * (bmin_x + bmax_x), ccy = 0.5 * (bmin_y + bmax_y), ccz = 0.5 * (bmin_z + bmax_z);
+    const double hwx = 0.5 * (bmax_x - bmin_x), hwy = 0.5 * (bmax_y - bmin_y), hwz = 0.5 * (bmax_z - bmin_z);
+    const float ccxf = (float)ccx, ccyf = (float)ccy, cczf = (float)ccz;
+    const float hwxf = (float)hwx, hwyf = (float)hwy, hwzf = (float)hwz;
+    const double ext = fmax(fmax(fmax(fabs(bmin_x), fabs(bmax_x)), fmax(fabs(bmin_y), fabs(bmax_y))),
+                            fmax(fabs(bmin_z), fabs(bmax_z))) + bc;
+    const double ru = bc * (1.0 + 1e-5) + 16.0 * 1.2e-7 * ext;
+    const float ru2f = (float)(ru * ru);
+    // FP32 decision margins.  A relative coordinate u = fl(fl(x) - fl(cc)) is within
+    // 2^-24 (2 ext + D) of x - cc (D >= |u|); a packed difference within
+    // e_d = 2^-23 (2 ext + D) + 2^-23 D; r^2 (FMA chain) within
+    // 2 sqrt(3) |d| e_d + 3 e_d^2 + 2e-7 r^2.  M doubles that bound.
+    const double dmax = fmax(fmax(hwx, hwy), hwz) * 2.0 + ru;
+    const double e_d = 1.2e-7 * (2.0 * ext + 2.0 * dmax);
+    const double rmax = sqrt(bc2) * 1.01;
+    const double M = 2.0 * (3.4642 * rmax * e_d + 3.0 * e_d * e_d + 2e-7 * bc2) + 1e-5 * bc2;
+    const float lo2f = (float)(bc2 - M), bc2f = (float)(bc2 + M);
+    const float fxi = valid ? (float)xi.x - ccxf : -1e18f, fyi = valid ? (float)xi.y - ccyf : -1e18f;
+    const float fzi = valid ? (float)xi.z - cczf : -1e18f;
+    const unsigned long long fxi2 = f32x2(fxi, fxi), fyi2 = f32x2(fyi, fyi), fzi2 = f32x2(fzi, fzi);
+    // exact FP64 test (strict r^2 < bc^2 in the reference's rounding, mdkk/neighbor.py:121-126)
+    // for the candidates FP32 cannot decide
+    int cnt = 0;
+    int* const trow = table + ((long long)c * cap) * 32 + lane;
+    auto visit = [&](int j) {
+        if (!valid || j == i) return;
+        const double4 p = mdkk::ld4(x, j);
+        const double r2 = mdkk::r2_exact(p.x - xi.x, p.y - xi.y, p.z - xi.z);
+        if (!(r2 < bc2)) return;
+        trow[(long long)min(cnt, cap - 1) * 32] = j;
+        ++cnt;
+    };
+    // 2. the cluster's own rows, broadcast by shuffles
+    for (int k = 0; k < 32; ++k) {
+        const float dx = __shfl_sync(0xffffffffu, fxi, k) - fxi, dy = __shfl_sync(0xffffffffu, fyi, k) - fyi;
+        const float dz = __shfl_sync(0xffffffffu, fzi, k) - fzi;
+        const float r2f = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+        const bool own = valid && k < nown && k != lane;
+        const bool cert = own && r2f < lo2f;
+        if (cert) {
+            trow[(long long)min(cnt, cap - 1) * 32] = c0 + k;
+            ++cnt;
+        }
+        if (own && !cert && r2f < bc2f) visit(c0 + k);
+    }
+    // 3. stream the cell rows within bc of the bbox through the ring, testing every full block
+    int m = 0, done = 0;   // members put / tested
+    auto put = [&](const float4& p, bool keep) {
+        const unsigned mk = __ballot_sync(0xffffffffu, keep);
+        if (keep) {
+            const int pos = (m + __popc(mk & ((1u << lane) - 1u))) & (kRing - 1);
+            const int o = (pos >> 1) * 4 + (pos & 1);
+            fa[o] = p.x - ccxf;
+            fa[o + 2] = p.y - ccyf;
+            fb[o] = p.z - cczf;
+            jb[o + 2] = __float_as_int(p.w);
+        }
+        m += __popc(mk);
+    };
+    auto near = [&](const float4& p) {
+        float dx = fabsf(p.x - ccxf) - hwxf, dy = fabsf(p.y - ccyf) - hwyf, dz = fabsf(p.z - cczf) - hwzf;
+        dx = dx > 0.f ? dx : 0.f;
+        dy = dy > 0.f ? dy : 0.f;
+        dz = dz > 0.f ? dz : 0.f;
+        return dx * dx + dy * dy + dz * dz < ru2f;
+    };
+    auto test = [&](const float4& p, bool in_range) {
+        return in_range && (unsigned)(__float_as_int(p.w) - c0) >= (unsigned)nown && near(p);
+    };
+    // one 32-member block at ring offset h (certain partners: branch-free predicated
+    // stores in member order; the shell is flagged and tested exactly after the block)
+    auto run_block = [&](int h) {
+        __syncwarp();
+        unsigned bits = 0u;
+        const UxY* ra = sa + (h >> 1);   // a block never wraps the ring (h is a multiple of 32)
+        const UzJ* rb = sb + (h >> 1);
+        auto body = [&](auto roomy_tag) {
+            constexpr bool kRoomy = decltype(roomy_tag)::value;
+            int off = cnt * 32;   // roomy: cnt + 32 <= cap
+#pragma unroll
+            for (int t = 0; t < 32; t += 2) {
+                const UxY a = ra[t >> 1];
+                const UzJ b = rb[t >> 1];
+                float r0, r1;
+                r2_pair_v(a.x0, a.x1, a.y0, a.y1, b.z0, b.z1, fxi2, fyi2, fzi2, r0, r1);
+                const bool k0 = r0 < lo2f, k1 = r1 < lo2f;
+                const bool e0 = r0 < bc2f && !k0, e1 = r1 < bc2f && !k1;
+                if (kRoomy) {
+                    if (k0) {
+                        trow[off] = b.j0;
+                        off += 32;
+                    }
+                    if (k1) {
+                        trow[off] = b.j1;
+                        off += 32;
+                    }
+                } else {
+                    if (k0) {
+                        trow[(long long)min(cnt, cap - 1) * 32] = b.j0;
+                        ++cnt;
+                    }
+                    if (k1) {
+                        trow[(long long)min(cnt, cap - 1) * 32] = b.j1;
+                        ++cnt;
+                    }
+                }
+                bits |= (e0 ? (1u << t) : 0u) | (e1 ? (2u << t) : 0u);
+            }
+            if (kRoomy) cnt = off >> 5;
+        };
+        if (__all_sync(0xffffffffu, cnt + 32 <= cap))
+            body(std::true_type{});
+        else
+            body(std::false_type{});
+        while (bits) {
+            const int t = h + __ffs(bits) - 1;
+            bits &= bits - 1u;
+            visit(jb[(t >> 1) * 4 + 2 + (t & 1)]);
+        }
+        __syncwarp();   // the ring slots are refilled next
+    };
+    const int ny = chi.y - clo.y + 1, nrun = (chi.x - clo.x + 1) * ny;
+    int run_s0 = 0, run_s1 = 0;
+    if (lane < nrun) {
+        const int2 kr = mdkk::zrun_keys(g, clo.x + lane / ny, clo.y + lane % ny, clo.z, chi.z);
+        run_s0 = cell_start[kr.x];
+        run_s1 = cell_start[kr.y + 1];
+    }
+    int r = -1, bs = 0, be = 0;
+    auto advance = [&]() -> bool {   // to the next 64-row batch (warp-uniform state)
+        bs += 64;
+        while (bs >= be) {
+            if (++r >= nrun) return false;
+            if (r < 32) {
+                bs = __shfl_sync(0xffffffffu, run_s0, r);
+                be = __shfl_sync(0xffffffffu, run_s1, r);
+            } else {
+                const int2 kr = mdkk::zrun_keys(g, clo.x + r / ny, clo.y + r % ny, clo.z, chi.z);
+                bs = cell_start[kr.x];
+                be = cell_start[kr.y + 1];
+            }
+        }
+        return true;
+    };
+    {
+        float4 pa = make_float4(0.f, 0.f, 0.f, 0.f), pb = pa;
+        int n_cur = 0;
+        if (advance()) {
+            pa = xs[min(bs + lane, be - 1)];
+            pb = xs[min(bs + 32 + lane, be - 1)];
+            n_cur = be - bs;
+        }
+        bool more = n_cur > 0 && advance();
+        while (n_cur > 0) {
+            float4 qa = pa, qb = pb;
+            int n_next = 0;
+            if (more) {   // the next batch's loads go out before this batch is filtered and tested
+                qa = xs[min(bs + lane, be - 1)];
+                qb = xs[min(bs + 32 + lane, be - 1)];
+                n_next = be - bs;
+                more = advance();
+            }
+            put(pa, test(pa, lane < n_cur));
+            put(pb, test(pb, lane + 32 < n_cur));
+            while (m - done >= 32) {
+                run_block(done & (kRing - 1));
+                done += 32;
+            }
+            pa = qa;
+            pb = qb;
+            n_cur = n_next;
+        }
+    }
+    if (m > done) {   // the last partial block, padded (pads sit at +1e18: never a hit)
+        const int pos = (m + lane) & (kRing - 1);
+        if (m + lane < done + 32) {
+            const int o = (pos >> 1) * 4 + (pos & 1);
+            fa[o] = 1e18f;
+            fa[o + 2] = 1e18f;
+            fb[o] = 1e18f;
+            jb[o + 2] = -1;
+        }
+        run_block(done & (kRing - 1));
+    }
+    if (valid) counts[i] = cnt;
+    int mc = cnt;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mc = max(mc, __shfl_xor_sync(0xffffffffu, mc, o));
+    if (lane == 0 && mc > 0) atomicMax(max_count, mc);
+}
+
 // Canonical per-row order: (gid[j], z_j, y_j, x_j) ascending (mdkk/neighbor.py:192-197).
 __device__ __forceinline__ bool canon_less(int a, int b, const double* x, const int64_t* gid) {
     int64_t ga = gid[a], gb = gid[b];
@@ -466,6 +734,13 @@ int mdkk_nbr_build(mdkk_ctx* ctx, const double* x, int n_local, int n_total, con
     const int ncl = (n_local + 31) / 32;
     const int nb = (ncl + kWarps - 1) / kWarps;
     const double bc2 = bc * bc;
+    static const bool v1 = getenv("MDKK_NB_V1") && getenv("MDKK_NB_V1")[0] == '1';   // A/B switch
+    if (style == 0 && !v1) {
+        k_nbr_build_full<<<(ncl + kW2 - 1) / kW2, kW2 * 32, 0, s>>>(x, n_local, g, cell_start, bc, bc2, cap, table,
+                                                                    counts, max_count, xs);
+        MDKK_CHECK_LAUNCH("k_nbr_build_full");
+        return MDKK_OK;
+    }
     if (style == 0)
         k_nbr_build<0, false><<<nb, kWarps * 32, 0, s>>>(x, n_local, g, cell_start, cell_atoms, gid, owner_rank,
                                                          my_rank, bc, bc2, cap, table, counts, max_count, xs);
