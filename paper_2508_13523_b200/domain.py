@@ -270,6 +270,10 @@ class AtomStore:
 
     def to_device(self):
         """Make device storage current before a kernel reads it."""
+        if self.pos.modified_a:
+            # host-written positions: the last spatial sort's cell order no longer holds,
+            # so the boundary-row halo scan and ghost-only binning must not reuse it
+            self._bins = None
         self.pos.sync("b")
         self.vel.sync("b")
         self.force.sync("b")

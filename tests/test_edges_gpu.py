@@ -89,3 +89,31 @@ def test_partial_last_cluster(gpu, n):
     for style, newton in (("full", False), ("half", True)):
         _, _, res = _forces(pos, lengths, 1.8, 0.3, 1, style, newton)
         _check(res, pos, lengths, 1.8)
+
+
+def test_host_position_write_after_sort_drops_stale_cell_order(gpu):
+    """sort_local() leaves the owned rows cell-sorted and the halo selection scans
+    only the boundary-layer rows of that order; a host-side position write through
+    the DualArray protocol afterwards must invalidate it, or an atom moved into
+    the halo layer would be missed as a ghost (mdkk/domain.py:246-293)."""
+    from paper_2508_13523_b200 import Box, RankedSystem
+    pos, lengths = md.lattice("fcc", 0.8442, (6, 6, 6))
+    pos = md.jittered(pos, 0.02, 3)
+    system = RankedSystem.distribute(Box(lengths), 1, pos, np.zeros_like(pos))
+    system.sort_local(2.8)
+    s = system.stores[0]
+    a = s.pos.read("a")
+    gids = s.gid[: s.n_local].cpu().numpy()
+    k = int(np.argmin(np.abs(a[: s.n_local] - 0.5 * np.asarray(lengths)).sum(axis=1)))  # the most interior atom
+    a[k] = (0.05, 0.5 * lengths[1], 0.5 * lengths[2])   # now within the halo of the x = 0 face
+    s.pos.mark_modified("a")
+    system.exchange_ghosts(2.8)
+    by_gid = np.empty_like(pos)
+    by_gid[gids] = a[: s.n_local]
+    ref = md.Ranked(lengths, 1, by_gid, np.zeros_like(by_gid))
+    ref.exchange_ghosts(2.8)
+    r0 = ref.ranks[0]
+    ours = np.sort(s.gid[s.n_local: s.n_total].cpu().numpy())
+    assert s.n_ghost == len(r0.gid) - r0.n_local
+    assert np.array_equal(ours, np.sort(r0.gid[r0.n_local:]))
+    assert gids[k] in ours
