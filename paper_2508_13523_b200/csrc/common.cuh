@@ -117,8 +117,9 @@ __device__ __forceinline__ void block_sum(double (&v)[K], double* out, bool acc 
     }
 }
 
-// Deterministic second stage: out[k] = sum_b partials[b*K + k], fixed order.
-void reduce_partials(const double* partials, int nblocks, int K, double* out, cudaStream_t s);
+// Deterministic second stage: out[k] = sum_b partials[b*K + k], fixed order;
+// out[K .. zero_to) are cleared in the same launch.
+void reduce_partials(const double* partials, int nblocks, int K, double* out, cudaStream_t s, int zero_to = 0);
 
 // A drift maximum that cannot hide a blow-up: NaN / inf become +inf before the
 // (NaN-dropping) fmax reductions, so the host's per-step read-back sees it

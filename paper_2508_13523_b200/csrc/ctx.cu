@@ -46,12 +46,24 @@ void* scratch_tail(mdkk_ctx* ctx, size_t bytes) {
 }
 
 // One block per column k: fixed-order strided sums then a fixed tree (deterministic).
+// Four independent accumulators per thread keep four loads in flight (the sum is
+// latency bound: one block per column); out[K .. zero_to) are cleared by block 0
+// (the energy/virial slots a K = 1 reduction does not write), so callers need no
+// separate memset launch.
 __global__ void __launch_bounds__(1024) k_reduce_partials(const double* __restrict__ p, int nb, int K,
-                                                          double* __restrict__ out) {
+                                                          double* __restrict__ out, int zero_to) {
     __shared__ double sm[32];
     const int k = blockIdx.x;
-    double s = 0.0;
-    for (int b = threadIdx.x; b < nb; b += blockDim.x) s += p[(long long)b * K + k];
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int b = threadIdx.x;
+    for (; b + 3 * 1024 < nb; b += 4 * 1024) {
+        s0 += p[(long long)b * K + k];
+        s1 += p[(long long)(b + 1024) * K + k];
+        s2 += p[(long long)(b + 2048) * K + k];
+        s3 += p[(long long)(b + 3072) * K + k];
+    }
+    for (; b < nb; b += 1024) s0 += p[(long long)b * K + k];
+    double s = (s0 + s1) + (s2 + s3);
     s = warp_sum(s);
     if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = s;
     __syncthreads();
@@ -60,10 +72,11 @@ __global__ void __launch_bounds__(1024) k_reduce_partials(const double* __restri
         v = warp_sum(v);
         if (threadIdx.x == 0) out[k] = v;
     }
+    if (k == 0 && threadIdx.x >= K && threadIdx.x < zero_to) out[threadIdx.x] = 0.0;
 }
 
-void reduce_partials(const double* partials, int nblocks, int K, double* out, cudaStream_t s) {
-    k_reduce_partials<<<K, 1024, 0, s>>>(partials, nblocks, K, out);
+void reduce_partials(const double* partials, int nblocks, int K, double* out, cudaStream_t s, int zero_to) {
+    k_reduce_partials<<<K, 1024, 0, s>>>(partials, nblocks, K, out, zero_to);
 }
 
 }  // namespace mdkk

@@ -366,8 +366,7 @@ int lj_team_launch(mdkk_ctx* ctx, const double* x, int n_local, const int* table
     }
 #undef MDKK_LJT
     MDKK_CHECK_LAUNCH("k_lj_team");
-    if (!virial) cudaMemsetAsync(ev, 0, 7 * sizeof(double), s);
-    mdkk::reduce_partials(partials, nb, virial ? 7 : 1, ev, s);
+    mdkk::reduce_partials(partials, nb, virial ? 7 : 1, ev, s, 7);   // clears the unused virial slots
     MDKK_CHECK_LAUNCH("k_reduce_partials");
     return MDKK_OK;
 }
@@ -396,8 +395,7 @@ int lj_launch(mdkk_ctx* ctx, const double* x, int n_local, const int* table, con
     }
 #undef MDKK_LJ
     MDKK_CHECK_LAUNCH("k_lj");
-    if (!virial) cudaMemsetAsync(ev, 0, 7 * sizeof(double), s);
-    mdkk::reduce_partials(partials, nb, virial ? 7 : 1, ev, s);
+    mdkk::reduce_partials(partials, nb, virial ? 7 : 1, ev, s, 7);   // clears the unused virial slots
     MDKK_CHECK_LAUNCH("k_reduce_partials");
     return MDKK_OK;
 }
@@ -451,8 +449,7 @@ extern "C" int mdkk_lj_force_integrate(mdkk_ctx* ctx, const double* x, int n_loc
 #undef MDKK_LJI
     MDKK_CHECK_LAUNCH("k_lj (integrate)");
     if (part == 1) return MDKK_OK;   // the reduction follows part 2
-    if (!virial) cudaMemsetAsync(ev, 0, 7 * sizeof(double), s);
-    mdkk::reduce_partials(partials, nb, virial ? 7 : 1, ev, s);
+    mdkk::reduce_partials(partials, nb, virial ? 7 : 1, ev, s, 7);   // clears the unused virial slots
     MDKK_CHECK_LAUNCH("k_reduce_partials");
     return MDKK_OK;
 }
@@ -519,8 +516,7 @@ extern "C" int mdkk_lj_force_strategy(mdkk_ctx* ctx, const double* x, int n_loca
     }
 #undef MDKK_LJS
     MDKK_CHECK_LAUNCH("k_lj (strategy)");
-    if (!virial) cudaMemsetAsync(ev, 0, 7 * sizeof(double), s);
-    mdkk::reduce_partials(partials, nb, virial ? 7 : 1, ev, s);
+    mdkk::reduce_partials(partials, nb, virial ? 7 : 1, ev, s, 7);   // clears the unused virial slots
     MDKK_CHECK_LAUNCH("k_reduce_partials");
     return MDKK_OK;
 }
