@@ -162,11 +162,14 @@ __host__ __device__ constexpr int half_offset(int tj) {
     return s;
 }
 // Compact column-major level storage for the recursion: level t keeps columns
-// 0..(t+1)>>1 (all the next level reads: C_t plus the mirror of its last column).
+// 0..(t+1)>>1 (all the next level reads: C_t plus the mirror of its last column),
+// followed by one spare slot: rec2's branch-free read of the element below the
+// last column (weight 0) lands there instead of on the next level's first slot,
+// which the same pass writes.
 __host__ __device__ constexpr int lvl_size(int t) { return (t + 1) * (((t + 1) >> 1) + 1); }
 __host__ __device__ constexpr int lvl_offset(int t) {
     int s = 0;
-    for (int k = 0; k < t; ++k) s += lvl_size(k);
+    for (int k = 0; k < t; ++k) s += lvl_size(k) + 1;
     return s;
 }
 
