@@ -434,6 +434,7 @@ class RankedSystem:
             s.to_device()
         if self.n_ranks == 1 and self.stores[0].n_local and self._combos(0, halo)[0]:
             return self._exchange_single(halo, lib, stream, ctx)
+        self._run_tails()
         plans = []
         for src in self.stores:
             meta, tab, codes = self._combos(src.rank, halo)
@@ -528,7 +529,12 @@ class RankedSystem:
         if pin is None or pin.numel() < C_:
             pin = self._scratch["tot_pin"] = torch.zeros(max(C_, 64), dtype=torch.int32, pin_memory=True)
         pin[:C_].copy_(tot, non_blocking=True)
-        torch.cuda.current_stream(self.device).synchronize()
+        ev = self._scratch.get("tot_ev")
+        if ev is None:
+            ev = self._scratch["tot_ev"] = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(self.device))
+        self._run_tails()   # deferred sort gathers: device work while the host waits for the totals
+        ev.synchronize()
         ng = int(pin[:C_].numpy().astype(np.int64).sum())
         idx = self._buf("idx0", ng + 1, torch.int32)
         cds = self._buf("cds0", ng + 1, torch.int8)
@@ -545,6 +551,13 @@ class RankedSystem:
         s.n_ghost = ng
         s._views()
         s.device_wrote(pos=True)
+
+    def _run_tails(self):
+        for s in self.stores:
+            t = getattr(s, "_tail", None)
+            if t is not None:
+                s._tail = None
+                t()
 
     def _pack_all(self):
         lib, stream = _lib.lib(), _lib.stream(self.device)
@@ -638,7 +651,8 @@ class RankedSystem:
         w = sort_width or self.sort_width
         if w:
             for s in self.stores:
-                self._spatial_sort(s, w, halo)
+                # one rank: the v / gid gathers go behind the exchange's totals read-back
+                self._spatial_sort(s, w, halo, defer_tail=R == 1)
         for s in self.stores:
             s.n_ghost = 0
             s._views()
@@ -659,8 +673,11 @@ class RankedSystem:
             s.device_wrote(pos=True, vel=True, force=True)
         self.lanes = []
 
-    def _spatial_sort(self, s: AtomStore, width: float, halo: float):
-        """Reorder owned rows by cell (double-buffered) so neighbour gathers are local; gids travel."""
+    def _spatial_sort(self, s: AtomStore, width: float, halo: float, defer_tail: bool = False):
+        """Reorder owned rows by cell (double-buffered) so neighbour gathers are local; gids travel.
+        `defer_tail`: the velocity / gid gathers are left in `s._tail` for the caller to queue
+        later (the one-rank exchange queues them behind its totals read-back, so the device
+        has work while the host waits for the totals)."""
         if s.n_local < 2:
             return
         lib, stream = _lib.lib(), _lib.stream(self.device)
@@ -679,8 +696,15 @@ class RankedSystem:
                       torch.empty(s.capacity, dtype=torch.int64, device=self.device))
         x2, v2, g2 = s._alt
         _lib.check(lib.mdkk_gather_rows4(s.x.data_ptr(), order.data_ptr(), n, x2.data_ptr(), stream), "g4")
-        _lib.check(lib.mdkk_gather_rows4(s.v.data_ptr(), order.data_ptr(), n, v2.data_ptr(), stream), "g4")
-        _lib.check(lib.mdkk_gather_i64(s.gid.data_ptr(), order.data_ptr(), n, g2.data_ptr(), stream), "g64")
+        vp, gp, op = s.v.data_ptr(), s.gid.data_ptr(), order.data_ptr()
+
+        def tail():
+            _lib.check(lib.mdkk_gather_rows4(vp, op, n, v2.data_ptr(), stream), "g4")
+            _lib.check(lib.mdkk_gather_i64(gp, op, n, g2.data_ptr(), stream), "g64")
+        if defer_tail:
+            s._tail = tail
+        else:
+            tail()
         s._alt = (s.x, s.v, s.gid)
         s.x, s.v, s.gid = x2, v2, g2
         s._bins = (float(width), n, start)   # owned rows sorted on shell_grid_args(lo, hi, width)

@@ -374,10 +374,19 @@ class Simulation:
         # lists and SNAP clear the rows they accumulate into): no reset pass
         self.system.migrate(halo, zero_forces=False)
         old = self.lists if self.lists is not None and len(self.lists) == len(self.system.stores) else None
+        ready = False
+        if old is not None and all(o.ref_dev.shape[0] >= max(s.n_local, 1)
+                                   for o, s in zip(old, self.system.stores)):
+            # the new lists' skin-test reference = the owned positions now: copied here, so the
+            # device does it while the host prepares the build (not after the build kernel)
+            for o, s in zip(old, self.system.stores):
+                n = max(s.n_local, 1)
+                o.ref_dev[:n].copy_(s.x[:n])
+            ready = True
         self.lists = None   # the old lists are dead: their buffers are recycled
         self.lists = [build(s, self.system.box, self.style.r_c, self.config.skin, style=self._list_style,
                             newton=self.config.newton, cap_hint=self._cap_hint,
-                            recycle=old[k] if old is not None else None, defer=defer)
+                            recycle=old[k] if old is not None else None, defer=defer, ref_ready=ready)
                       for k, s in enumerate(self.system.stores)]
         if not defer:
             self._cap_hint = max(nl.alloc_cap for nl in self.lists)

@@ -49,7 +49,8 @@ class NeighborList:
     """
 
     def __init__(self, store: AtomStore, style: str, newton: bool, cutoff: float, skin: float,
-                 cap: int, table: torch.Tensor, counts: torch.Tensor, max_count: int, ref_buf=None):
+                 cap: int, table: torch.Tensor, counts: torch.Tensor, max_count: int, ref_buf=None,
+                 ref_ready: bool = False):
         self.store = store
         self.style = style
         self.newton = bool(newton)
@@ -61,7 +62,10 @@ class NeighborList:
         self.max_count = int(max_count)
         self.table_dev = table
         self.counts_dev = counts
-        self.ref_dev = store.x[: max(store.n_local, 1)].clone() if ref_buf is None else _ref_into(ref_buf, store)
+        if ref_ready:   # the caller already holds the build-time positions in ref_buf
+            self.ref_dev = ref_buf[: max(store.n_local, 1)]
+        else:
+            self.ref_dev = store.x[: max(store.n_local, 1)].clone() if ref_buf is None else _ref_into(ref_buf, store)
         self._d2 = torch.empty(1, dtype=torch.float64, device=store.device)   # written before every read
         self._pairs = None
         self._pending = None   # deferred capacity check: (device max count, build args)
@@ -212,7 +216,7 @@ _cache: dict = {}
 def build(store: AtomStore, box: Box, cutoff: float, skin: float, style: str = "full",
           newton: bool = True, capacity: int = DEFAULT_CAPACITY, cap_hint: int | None = None,
           recycle: NeighborList | None = None, defer: bool = False, rebin: bool = True,
-          **_unused) -> NeighborList:
+          ref_ready: bool = False, **_unused) -> NeighborList:
     """One rank's list from its local + ghost rows (mdkk/neighbor.py:182-219).
 
     Owned rows must be cell-sorted for compact clusters (RankedSystem keeps
@@ -226,6 +230,9 @@ def build(store: AtomStore, box: Box, cutoff: float, skin: float, style: str = "
     device-side count (mdkk_lj_force_gated) can be queued first.
     `rebin=False` (engine-internal, a regrow right after a build of the same rows)
     reuses that build's cell lists, so the table comes out in the same order.
+    `ref_ready` (engine-internal, with `recycle`): the recycled list's reference
+    buffer already holds the current owned positions (the engine copies them
+    while the host is still preparing the build).
     """
     if style not in STYLES:
         raise NeighborError(f"unknown list style {style!r}")
@@ -289,7 +296,8 @@ def build(store: AtomStore, box: Box, cutoff: float, skin: float, style: str = "
         ready = torch.cuda.Event()
         ready.record(torch.cuda.current_stream(dev))
         nl = NeighborList(store, style, newton, cutoff, skin, alloc, table, counts, alloc,
-                          ref_buf=recycle.ref_dev if recycle is not None else None)
+                          ref_buf=recycle.ref_dev if recycle is not None else None,
+                          ref_ready=ref_ready and recycle is not None)
         nl._pending = (mc, box, capacity, pin, ready)
         return nl
     while True:
@@ -306,7 +314,8 @@ def build(store: AtomStore, box: Box, cutoff: float, skin: float, style: str = "
         alloc = grow_capacity(alloc, need)  # never truncate: grow and rebuild
     cap = grow_capacity(capacity, need)
     return NeighborList(store, style, newton, cutoff, skin, cap, table, counts, need,
-                        ref_buf=recycle.ref_dev if recycle is not None else None)
+                        ref_buf=recycle.ref_dev if recycle is not None else None,
+                          ref_ready=ref_ready and recycle is not None)
 
 
 def build_all(system: RankedSystem, cutoff: float, skin: float, style: str = "full",
