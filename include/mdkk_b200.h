@@ -124,6 +124,21 @@ int mdkk_bucket_sort(mdkk_ctx* ctx, const int* keys, int n, int nbuckets, int* b
 int mdkk_bin_atoms(mdkk_ctx* ctx, const double* x, int n, const double* grid_host, const int* ncell_host,
                    int* keys, int* cell_start, int* cell_atoms, void* stream);
 
+/* One-rank engine rebuild, selection phase (RankedSystem.migrate's single-rank path,
+ * mdkk/domain.py:324-334, with the halo selection of exchange_ghosts :246-293) in one
+ * call: wrap x[0, n), counting-sort the rows by cell of the shell grid (keys / cell_start
+ * / order as mdkk_bin_atoms), gather x into x_sorted, list the boundary-layer rows
+ * (mdkk_boundary_rows, 2 layers) and count the halo entries per combo (mdkk_halo_count
+ * over x_sorted); the totals are copied into totals_host (pinned, int[C]) and the
+ * velocity / gid gathers are queued behind that copy; returns once the totals have
+ * arrived, with their sum in *n_ghost_host.  The caller then fills the ghost rows
+ * (mdkk_halo_fill with the same block_scratch / totals / brows / bcount). */
+int mdkk_rebuild1_select(mdkk_ctx* ctx, double* x, int n, const double* lengths_host, const double* grid_host,
+                         const int* ncell_host, int* keys, int* cell_start, int* order, double* x_sorted,
+                         const double* v, double* v_sorted, const int64_t* gid, int64_t* gid_sorted, int* brows,
+                         int* bcount, const double* combos_dev, int C, int* block_scratch, int* totals,
+                         int* totals_host, int* n_ghost_host, void* stream);
+
 /* Cell lists for a build whose owned rows [0, n_local) are already sorted by cell on
  * this grid with bucket starts owned_start[ncell + 1] (the engine's spatial sort):
  * bins only the ghost rows [n_local, n_total) and merges, giving exactly

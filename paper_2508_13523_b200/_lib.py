@@ -52,6 +52,8 @@ SIGNATURES = {
     "mdkk_max_disp2": [_p, _p, _i, _p, _p],
     "mdkk_nbr_geo_order": [_p, _i, _i, _p, _p, _p],
     "mdkk_bin_merge": [_p, _p, _i, _i, _p, _p, _p, _p, _p, _p, _p],
+    "mdkk_rebuild1_select": [_p, _p, _i, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _i, _p, _p, _p,
+                             _p, _p],
     "mdkk_lj_force": [_p, _p, _i, _p, _p, _i, _i, _i, _i, _d, _d, _d, _p, _p, _p, _p],
     "mdkk_lj_force_integrate": [_p, _p, _i, _p, _p, _i, _i, _d, _d, _d, _p, _p, _p, _p, _d, _p, _i, _i, _p, _p, _p,
                                 _p, _d, _d, _p, _i, _p],
@@ -153,7 +155,20 @@ def ctx(device: torch.device) -> int:
     return h
 
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def stream(device: torch.device | None = None) -> int:
+    """The current stream of `device` as a raw cudaStream_t (what every C entry point takes).
+    Called several times per step: torch's raw accessor skips building a Stream object."""
+    if _raw_stream is not None:
+        if device is None:
+            idx = torch.cuda.current_device()
+        else:
+            idx = device if isinstance(device, int) else device.index
+            if idx is None:
+                idx = torch.cuda.current_device()
+        return _raw_stream(idx)
     return torch.cuda.current_stream(device).cuda_stream
 
 

@@ -1,0 +1,68 @@
+// One-rank engine rebuild, selection phase: the device sequence of
+// RankedSystem.migrate's single-rank path (mdkk/domain.py:324-334: wrap, then the
+// ghost selection of exchange_ghosts, :246-293) issued from one host call.
+//
+// The rebuild is a chain of ~25 short kernels ahead of one host read-back (the
+// ghost totals); issued one ctypes call at a time, the host was slower than the
+// device and the GPU idled between launches.  Here the whole chain up to the
+// read-back is queued back to back, the velocity / gid gathers go behind the
+// totals' copy (device work while the host waits), and the host waits on an
+// event for that copy only.
+#include "common.cuh"
+
+namespace {
+cudaEvent_t g_totals_ev[64];   // per device, created lazily
+}
+
+extern "C" {
+
+int mdkk_wrap(double* x, int n, const double* lengths_host, void* stream);
+int mdkk_bin_atoms(mdkk_ctx* ctx, const double* x, int n, const double* grid_host, const int* ncell_host,
+                   int* keys, int* cell_start, int* cell_atoms, void* stream);
+int mdkk_gather_rows4(const double* src, const int* perm, int n, double* dst, void* stream);
+int mdkk_gather_i64(const int64_t* src, const int* perm, int n, int64_t* dst, void* stream);
+int mdkk_boundary_rows(mdkk_ctx* ctx, const int* cell_start, const int* ncell_host, int layer, int* rows,
+                       int* count, void* stream);
+int mdkk_halo_count(mdkk_ctx* ctx, const double* x, int n, const double* combos, int C, int* block_scratch,
+                    int* totals, const int* rows, const int* n_dev, void* stream);
+
+int mdkk_rebuild1_select(mdkk_ctx* ctx, double* x, int n, const double* lengths_host, const double* grid_host,
+                         const int* ncell_host, int* keys, int* cell_start, int* order, double* x_sorted,
+                         const double* v, double* v_sorted, const int64_t* gid, int64_t* gid_sorted, int* brows,
+                         int* bcount, const double* combos_dev, int C, int* block_scratch, int* totals,
+                         int* totals_host, int* n_ghost_host, void* stream) {
+    if (!ctx || n < 2 || C < 1 || !totals_host || !n_ghost_host || x_sorted == x || v_sorted == v ||
+        gid_sorted == gid)
+        return MDKK_E_ARG;
+    cudaStream_t s = mdkk::as_stream(stream);
+    int st = mdkk_wrap(x, n, lengths_host, stream);
+    if (st == MDKK_OK) st = mdkk_bin_atoms(ctx, x, n, grid_host, ncell_host, keys, cell_start, order, stream);
+    if (st == MDKK_OK) st = mdkk_gather_rows4(x, order, n, x_sorted, stream);
+    // owned rows are now cell-sorted on the shell grid (cells >= halo wide): only rows within
+    // two cell layers of the faces can be selected
+    if (st == MDKK_OK) st = mdkk_boundary_rows(ctx, cell_start, ncell_host, 2, brows, bcount, stream);
+    if (st == MDKK_OK)
+        st = mdkk_halo_count(ctx, x_sorted, n, combos_dev, C, block_scratch, totals, brows, bcount, stream);
+    if (st != MDKK_OK) return st;
+    cudaEvent_t& ev = g_totals_ev[ctx->device & 63];
+    cudaError_t e = cudaSuccess;
+    if (!ev) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(totals_host, totals, sizeof(int) * (size_t)C, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaEventRecord(ev, s);
+    if (e != cudaSuccess) return mdkk::cuda_fail(e, "mdkk_rebuild1_select");
+    st = mdkk_gather_rows4(v, order, n, v_sorted, stream);
+    if (st == MDKK_OK) st = mdkk_gather_i64(gid, order, n, gid_sorted, stream);
+    if (st != MDKK_OK) return st;
+    e = cudaEventSynchronize(ev);
+    if (e != cudaSuccess) return mdkk::cuda_fail(e, "mdkk_rebuild1_select (totals)");
+    long long ng = 0;
+    for (int c = 0; c < C; ++c) ng += totals_host[c];
+    if (ng > 0x7fffffffLL) {
+        mdkk::set_error("mdkk_rebuild1_select: ghost count overflows int");
+        return MDKK_E_ARG;
+    }
+    *n_ghost_host = (int)ng;
+    return MDKK_OK;
+}
+
+}  // extern "C"

@@ -535,7 +535,7 @@ class RankedSystem:
         ev.record(torch.cuda.current_stream(self.device))
         self._run_tails()   # deferred sort gathers: device work while the host waits for the totals
         ev.synchronize()
-        ng = int(pin[:C_].numpy().astype(np.int64).sum())
+        ng = sum(pin[:C_].tolist())
         idx = self._buf("idx0", ng + 1, torch.int32)
         cds = self._buf("cds0", ng + 1, torch.int8)
         _lib.check(lib.mdkk_halo_fill(ctx, s.x.data_ptr(), nl, tab.data_ptr(), C_, blk.data_ptr(), tot.data_ptr(),
@@ -551,6 +551,69 @@ class RankedSystem:
         s.n_ghost = ng
         s._views()
         s.device_wrote(pos=True)
+
+    def _migrate_single(self, halo: float, width: float, zero_forces: bool) -> bool:
+        """One rank, periodic self-images only: migrate = wrap + spatial sort + ghost
+        selection + ghost rows, with everything up to the ghost totals issued by one
+        library call (mdkk_rebuild1_select).  The same kernels in the same order as the
+        general path (bit-identical rows, ghosts and bins); False (nothing done) when
+        the fast path does not apply."""
+        if halo <= 0 or halo > 0.5 * self.box.min_periodic_length():
+            return False   # the general path raises the reference's DomainError
+        s = self.stores[0]
+        meta, tab, codes = self._combos(0, halo)
+        C_ = len(meta)
+        if C_ == 0:
+            return False
+        lib, stream, ctx = _lib.lib(), _lib.stream(self.device), _lib.ctx(self.device)
+        s.to_device()
+        n = s.n_local
+        s.n_ghost = 0
+        s._lanes_in = []
+        _, _, garr, narr, ncell = shell_grid_args(s.lo, s.hi, width)
+        keys = self._buf("sk0", n, torch.int32)
+        start = self._buf("ss0", ncell + 1, torch.int32)
+        order = self._buf("so0", n, torch.int32)
+        if s._alt is None or s._alt[0].shape[0] != s.capacity or s._alt[1].shape[0] < n:
+            s._alt = (_rows4(s.capacity, self.device), _rows4(s.v.shape[0], self.device),
+                      torch.empty(s.capacity, dtype=torch.int64, device=self.device))
+        x2, v2, g2 = s._alt
+        rows = self._buf("brows0", n, torch.int32)
+        nrow = self._buf("bcount0", 1, torch.int32)
+        blk = self._buf("blk0", ((n + 255) // 256) * C_, torch.int32)
+        tot = self._buf("tot0", C_, torch.int32)
+        pin = self._scratch.get("tot_pin")
+        if pin is None or pin.numel() < C_:
+            pin = self._scratch["tot_pin"] = torch.zeros(max(C_, 64), dtype=torch.int32, pin_memory=True)
+        ngh = _lib.C.c_int(0)
+        _lib.check(lib.mdkk_rebuild1_select(
+            ctx, s.x.data_ptr(), n, _lib.dbl3(self.box.lengths), garr, narr, keys.data_ptr(), start.data_ptr(),
+            order.data_ptr(), x2.data_ptr(), s.v.data_ptr(), v2.data_ptr(), s.gid.data_ptr(), g2.data_ptr(),
+            rows.data_ptr(), nrow.data_ptr(), tab.data_ptr(), C_, blk.data_ptr(), tot.data_ptr(), pin.data_ptr(),
+            _lib.C.byref(ngh), stream), "mdkk_rebuild1_select")
+        ng = ngh.value
+        s._alt = (s.x, s.v, s.gid)
+        s.x, s.v, s.gid = x2, v2, g2
+        s._bins = (float(width), n, start)   # owned rows sorted on shell_grid_args(lo, hi, width)
+        self.halo = float(halo)
+        idx = self._buf("idx0", ng + 1, torch.int32)
+        cds = self._buf("cds0", ng + 1, torch.int8)
+        _lib.check(lib.mdkk_halo_fill(ctx, s.x.data_ptr(), n, tab.data_ptr(), C_, blk.data_ptr(), tot.data_ptr(),
+                                      idx.data_ptr(), codes.data_ptr(), cds.data_ptr(), rows.data_ptr(),
+                                      nrow.data_ptr(), stream), "mdkk_halo_fill")
+        s.ensure_capacity(n + ng)
+        xp, gp, op = s.x.data_ptr(), s.gid.data_ptr(), s.oidx.data_ptr()
+        _lib.check(lib.mdkk_ghost_rows(xp, gp, idx.data_ptr(), cds.data_ptr(), self._shift_dev.data_ptr(), ng,
+                                       xp + 32 * n, gp + 8 * n, op + 4 * n, stream), "mdkk_ghost_rows")
+        ln = _Lane(0, 0, idx[:ng], cds[:ng], n, ng)
+        self.lanes = [ln] if ng else []
+        s._lanes_in = list(self.lanes)
+        s.n_ghost = ng
+        s._views()
+        s.device_wrote(pos=True, vel=True, force=True)
+        if zero_forces:
+            s.f[: s.n_total].zero_()
+        return True
 
     def _run_tails(self):
         for s in self.stores:
@@ -608,8 +671,11 @@ class RankedSystem:
         lib, stream = _lib.lib(), _lib.stream(self.device)
         ctx = _lib.ctx(self.device)
         L = _lib.dbl3(self.box.lengths)
-        grid = _lib.int_arr(self.rankset.grid)
         R = self.n_ranks
+        w = sort_width or self.sort_width
+        if R == 1 and w and w >= halo and self.stores[0].n_local >= 2 and self._migrate_single(halo, w, zero_forces):
+            return
+        grid = _lib.int_arr(self.rankset.grid)
         for s in self.stores:
             s.to_device()
             _lib.check(lib.mdkk_wrap(s.x.data_ptr(), s.n_local, L, stream), "mdkk_wrap")
@@ -648,7 +714,6 @@ class RankedSystem:
             s = self.stores[0]
             s.n_ghost = 0
             s._lanes_in = []
-        w = sort_width or self.sort_width
         if w:
             for s in self.stores:
                 # one rank: the v / gid gathers go behind the exchange's totals read-back

@@ -279,7 +279,8 @@ def build(store: AtomStore, box: Box, cutoff: float, skin: float, style: str = "
     alloc = max(grow_capacity(capacity, 0), int(cap_hint or 0))
     old_t = recycle.table_dev if recycle is not None else None
     counts = _recycled(recycle.counts_dev if recycle is not None else None, (max(n_local, 1),), torch.int32, dev)
-    mc = torch.zeros(1, dtype=torch.int32, device=dev)
+    mc = cache.get("mc", 1, torch.int32, dev)   # one element; stream-ordered reuse across builds
+    mc.zero_()
     if defer and cap_hint is not None:
         table = _recycled(old_t, ((n_local + 31) // 32 or 1, alloc, 32), torch.int32, dev)
         _lib.check(lib.mdkk_nbr_build(ctx, store.x.data_ptr(), n_local, n_total, garr, narr, cstart.data_ptr(),
