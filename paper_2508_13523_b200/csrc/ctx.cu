@@ -45,38 +45,66 @@ void* scratch_tail(mdkk_ctx* ctx, size_t bytes) {
     return ctx->scratch_tail;
 }
 
-// One block per column k: fixed-order strided sums then a fixed tree (deterministic).
-// Four independent accumulators per thread keep four loads in flight (the sum is
-// latency bound: one block per column); out[K .. zero_to) are cleared by block 0
-// (the energy/virial slots a K = 1 reduction does not write), so callers need no
-// separate memset launch.
+// Deterministic two-level sum, one launch: column k is split over kRedG blocks; each
+// block sums its slice in a fixed order (strided loads, four in flight per thread,
+// then a fixed tree) into g_red_stage, and the block that finishes last (a
+// per-column counter, reset by that block) adds the kRedG slice sums in block order.
+// The partial sums are latency bound; kRedG blocks run their loads in parallel
+// instead of one block walking all of them.  out[K .. zero_to) are cleared by the
+// last block of column 0, so callers need no separate memset launch.  Reductions on
+// one device are issued from one stream at a time (the stage / counters are shared).
+constexpr int kRedG = 8;
+constexpr int kRedMaxK = 8;
+__device__ double g_red_stage[kRedMaxK * kRedG];
+__device__ unsigned g_red_count[kRedMaxK];
+
+__device__ __forceinline__ double block_tree_sum(double s, double* sm) {
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = s;
+    __syncthreads();
+    double v = 0.0;
+    if (threadIdx.x < 32) {
+        v = threadIdx.x < (blockDim.x >> 5) ? sm[threadIdx.x] : 0.0;
+        v = warp_sum(v);
+    }
+    return v;   // valid in thread 0
+}
+
 __global__ void __launch_bounds__(1024) k_reduce_partials(const double* __restrict__ p, int nb, int K,
                                                           double* __restrict__ out, int zero_to) {
     __shared__ double sm[32];
-    const int k = blockIdx.x;
+    __shared__ bool last;
+    const int k = blockIdx.y, g = blockIdx.x;
+    const int per = (nb + kRedG - 1) / kRedG, b0 = g * per, b1 = min(nb, b0 + per);
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-    int b = threadIdx.x;
-    for (; b + 3 * 1024 < nb; b += 4 * 1024) {
+    int b = b0 + threadIdx.x;
+    for (; b + 3 * 1024 < b1; b += 4 * 1024) {
         s0 += p[(long long)b * K + k];
         s1 += p[(long long)(b + 1024) * K + k];
         s2 += p[(long long)(b + 2048) * K + k];
         s3 += p[(long long)(b + 3072) * K + k];
     }
-    for (; b < nb; b += 1024) s0 += p[(long long)b * K + k];
-    double s = (s0 + s1) + (s2 + s3);
-    s = warp_sum(s);
-    if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = s;
+    for (; b < b1; b += 1024) s0 += p[(long long)b * K + k];
+    const double v = block_tree_sum((s0 + s1) + (s2 + s3), sm);
+    if (threadIdx.x == 0) {
+        g_red_stage[k * kRedG + g] = v;
+        __threadfence();
+        last = atomicAdd(&g_red_count[k], 1u) == kRedG - 1;
+    }
     __syncthreads();
-    if (threadIdx.x < 32) {
-        double v = threadIdx.x < (blockDim.x >> 5) ? sm[threadIdx.x] : 0.0;
-        v = warp_sum(v);
-        if (threadIdx.x == 0) out[k] = v;
+    if (!last) return;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        double t = 0.0;
+        for (int q = 0; q < kRedG; ++q) t += *((volatile double*)&g_red_stage[k * kRedG + q]);
+        out[k] = t;
+        g_red_count[k] = 0u;
     }
     if (k == 0 && threadIdx.x >= K && threadIdx.x < zero_to) out[threadIdx.x] = 0.0;
 }
 
 void reduce_partials(const double* partials, int nblocks, int K, double* out, cudaStream_t s, int zero_to) {
-    k_reduce_partials<<<K, 1024, 0, s>>>(partials, nblocks, K, out, zero_to);
+    k_reduce_partials<<<dim3(kRedG, K), 1024, 0, s>>>(partials, nblocks, K, out, zero_to);
 }
 
 }  // namespace mdkk
