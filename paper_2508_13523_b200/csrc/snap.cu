@@ -334,7 +334,7 @@ __global__ void __launch_bounds__(DW * 32, (TEAM == 16 ? 4 : 10 / DW)) k_snap_de
                     if (c < half_size(tj)) {
                         int P, Q;
                         col_elem(tj, c, P, Q);
-                        const cplx v = rec2(ul + lvl_offset(tj - 1), tj, P, Q, rs, ab, g.b);
+                        const cplx v = rec2(ul + lvl_offset(tj - 1), tj, P, Q, rs, ab, g.b, lvl_size(tj - 1) - 1);
                         if (tj < TWOJ) store_for_next(ul + lvl_offset(tj), tj, P, Q, v);
                         const cplx yv = sy[half_offset(tj) + c];
                         const double wgt = (2 * P == tj && 2 * Q == tj) ? 1.0 : 2.0;

@@ -115,8 +115,12 @@ __device__ __forceinline__ void pair_grads(const double d[3], const PairGeo& g, 
 // Branch-free at the column ends: the weights vanish there (sqrt(0) for P == tj
 // resp. P == 0) and the out-of-column operand is a finite neighbour (clamped
 // index, buffers zero-initialised), so both terms are always evaluated.
-__device__ __forceinline__ cplx rec2(const cplx* v, int tj, int P, int Q, const RS& rs, cplx ab, cplx b) {
-    const cplx v0 = v[Q * tj + P], v1 = v[max(Q * tj + P - 1, 0)];
+// `vmax` (compact level storage): the last readable slot of the level, so the
+// zero-weight read below the last column (P == tj) stays inside it instead of
+// touching the next level's first slot, which the same pass writes.
+__device__ __forceinline__ cplx rec2(const cplx* v, int tj, int P, int Q, const RS& rs, cplx ab, cplx b,
+                                     int vmax = 0x7fffffff) {
+    const cplx v0 = v[min(Q * tj + P, vmax)], v1 = v[max(Q * tj + P - 1, 0)];
     const cplx t0 = cmul(ab, v0), t1 = cmul(b, v1);
     const double w0 = rs.v[tj - P][tj - Q], w1 = rs.v[P][tj - Q];
     return {fma(w0, t0.re, w1 * t1.re), fma(w0, t0.im, w1 * t1.im)};
@@ -162,14 +166,11 @@ __host__ __device__ constexpr int half_offset(int tj) {
     return s;
 }
 // Compact column-major level storage for the recursion: level t keeps columns
-// 0..(t+1)>>1 (all the next level reads: C_t plus the mirror of its last column),
-// followed by one spare slot: rec2's branch-free read of the element below the
-// last column (weight 0) lands there instead of on the next level's first slot,
-// which the same pass writes.
+// 0..(t+1)>>1 (all the next level reads: C_t plus the mirror of its last column).
 __host__ __device__ constexpr int lvl_size(int t) { return (t + 1) * (((t + 1) >> 1) + 1); }
 __host__ __device__ constexpr int lvl_offset(int t) {
     int s = 0;
-    for (int k = 0; k < t; ++k) s += lvl_size(k) + 1;
+    for (int k = 0; k < t; ++k) s += lvl_size(k);
     return s;
 }
 
