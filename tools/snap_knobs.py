@@ -36,7 +36,7 @@ def timed(fn, reps=5):
 
 
 print(f"atoms {store.n_local}")
-for bu in (1, 2, 4):
+for bu in (1, 2, 4, 8):
     st = SnapState(tables, store.n_local, beta, batch_u=bu)
     print(f"batch_u={bu}: compute_ui {timed(lambda: compute_ui(nmap, st)):.3f} ms")
 for by in (1, 2):
