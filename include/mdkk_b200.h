@@ -131,13 +131,15 @@ int mdkk_bin_atoms(mdkk_ctx* ctx, const double* x, int n, const double* grid_hos
  * (mdkk_boundary_rows, 2 layers) and count the halo entries per combo (mdkk_halo_count
  * over x_sorted); the totals are copied into totals_host (pinned, int[C]) and the
  * velocity / gid gathers are queued behind that copy; returns once the totals have
- * arrived, with their sum in *n_ghost_host.  The caller then fills the ghost rows
- * (mdkk_halo_fill with the same block_scratch / totals / brows / bcount). */
+ * arrived, with their sum in *n_ghost_host.  x_ref (optional, double4[n]): also receives
+ * the sorted rows (the next lists' skin-test reference, mdkk/neighbor.py:66-80).  The
+ * caller then fills the ghost rows (mdkk_halo_fill with the same block_scratch / totals /
+ * brows / bcount). */
 int mdkk_rebuild1_select(mdkk_ctx* ctx, double* x, int n, const double* lengths_host, const double* grid_host,
                          const int* ncell_host, int* keys, int* cell_start, int* order, double* x_sorted,
                          const double* v, double* v_sorted, const int64_t* gid, int64_t* gid_sorted, int* brows,
                          int* bcount, const double* combos_dev, int C, int* block_scratch, int* totals,
-                         int* totals_host, int* n_ghost_host, void* stream);
+                         int* totals_host, int* n_ghost_host, double* x_ref, void* stream);
 
 /* Cell lists for a build whose owned rows [0, n_local) are already sorted by cell on
  * this grid with bucket starts owned_start[ncell + 1] (the engine's spatial sort):

@@ -53,7 +53,7 @@ SIGNATURES = {
     "mdkk_nbr_geo_order": [_p, _i, _i, _p, _p, _p],
     "mdkk_bin_merge": [_p, _p, _i, _i, _p, _p, _p, _p, _p, _p, _p],
     "mdkk_rebuild1_select": [_p, _p, _i, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _i, _p, _p, _p,
-                             _p, _p],
+                             _p, _p, _p],
     "mdkk_lj_force": [_p, _p, _i, _p, _p, _i, _i, _i, _i, _d, _d, _d, _p, _p, _p, _p],
     "mdkk_lj_force_integrate": [_p, _p, _i, _p, _p, _i, _i, _d, _d, _d, _p, _p, _p, _p, _d, _p, _i, _i, _p, _p, _p,
                                 _p, _d, _d, _p, _i, _p],

@@ -63,7 +63,7 @@ __global__ void k_halo_count(const double* __restrict__ x, int n, const double* 
     extern __shared__ double sc[];
     __shared__ unsigned long long s_or;
     if (n_dev && (long long)blockIdx.x * blockDim.x >= *n_dev) {   // block-uniform: nothing to select
-        for (int c = threadIdx.x; c < C; c += blockDim.x) block_counts[(long long)blockIdx.x * C + c] = 0;
+        for (int c = threadIdx.x; c < C; c += blockDim.x) block_counts[(long long)c * gridDim.x + blockIdx.x] = 0;
         return;
     }
     for (int t = threadIdx.x; t < 9 * C; t += blockDim.x) sc[t] = combos[t];
@@ -79,46 +79,59 @@ __global__ void k_halo_count(const double* __restrict__ x, int n, const double* 
             int cnt = 0;
             if ((any >> (c - c0)) & 1ull)   // block-uniform branch
                 cnt = __syncthreads_count((int)((mine >> (c - c0)) & 1ull));
-            if (threadIdx.x == 0) block_counts[(long long)blockIdx.x * C + c] = cnt;
+            if (threadIdx.x == 0) block_counts[(long long)c * gridDim.x + blockIdx.x] = cnt;   // combo-major
         }
         __syncthreads();
     }
 }
 
-// One block per combo: exclusive scan over blocks (stride C) in place; totals[c].
-__global__ void k_halo_scan(int* __restrict__ block_counts, int nb, int C, int* __restrict__ totals) {
+// One block per combo: exclusive scan of that combo's per-block counts in place
+// (combo-major [C][nb]: contiguous, four consecutive entries per thread per pass);
+// totals[c].
+__global__ void __launch_bounds__(1024) k_halo_scan(int* __restrict__ block_counts, int nb, int C,
+                                                    int* __restrict__ totals) {
     __shared__ int warp_tot[32];
     __shared__ int carry;
     const int c = blockIdx.x;
+    int* col = block_counts + (long long)c * nb;
     if (threadIdx.x == 0) carry = 0;
     __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int base = 0; base < nb; base += blockDim.x) {
-        int b = base + threadIdx.x;
-        int v = b < nb ? block_counts[(long long)b * C + c] : 0;
-        int incl = v;
+    for (int base = 0; base < nb; base += 4 * blockDim.x) {
+        const int b = base + 4 * threadIdx.x;
+        int v[4], s = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            v[q] = b + q < nb ? col[b + q] : 0;
+            s += v[q];
+        }
+        int incl = s;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            int t = __shfl_up_sync(0xffffffffu, incl, o);
+            const int t = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += t;
         }
         if (lane == 31) warp_tot[wid] = incl;
         __syncthreads();
         if (wid == 0) {
-            int w = lane < nw ? warp_tot[lane] : 0;
+            const int w = lane < nw ? warp_tot[lane] : 0;
             int wi = w;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-                int t = __shfl_up_sync(0xffffffffu, wi, o);
+                const int t = __shfl_up_sync(0xffffffffu, wi, o);
                 if (lane >= o) wi += t;
             }
-            if (lane < nw) warp_tot[lane] = wi - w;  // exclusive warp offsets
+            if (lane < nw) warp_tot[lane] = wi - w;   // exclusive warp offsets
         }
         __syncthreads();
-        int excl = carry + warp_tot[wid] + incl - v;
-        if (b < nb) block_counts[(long long)b * C + c] = excl;
+        int run = carry + warp_tot[wid] + incl - s;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (b + q < nb) col[b + q] = run;
+            run += v[q];
+        }
         __syncthreads();
-        if (threadIdx.x == blockDim.x - 1) carry = excl + v;
+        if (threadIdx.x == blockDim.x - 1) carry = run;
         __syncthreads();
     }
     if (threadIdx.x == 0) totals[c] = carry;
@@ -163,7 +176,7 @@ __global__ void k_halo_fill(const double* __restrict__ x, int n, const double* _
         for (int w = 0; w < wid; ++w) before += warp_cnt[w];
         if (flag) {
             int r = before + __popc(m & ((1u << lane) - 1u));
-            const int o = base[c] + block_off[(long long)blockIdx.x * C + c] + r;
+            const int o = base[c] + block_off[(long long)c * gridDim.x + blockIdx.x] + r;
             out[o] = i;
             if (out_code) out_code[o] = combo_code[c];
         }

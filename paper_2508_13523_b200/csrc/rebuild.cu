@@ -12,6 +12,17 @@
 
 namespace {
 cudaEvent_t g_totals_ev[64];   // per device, created lazily
+
+// The sort's position gather, also writing the rows into the new lists' skin-test
+// reference (the build-time positions) -- one pass over x instead of a later copy.
+__global__ void k_gather4_ref(const double* __restrict__ src, const int* __restrict__ perm, int n,
+                              double* __restrict__ dst, double* __restrict__ ref) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double4 p = mdkk::ld4(src, perm[i]);
+    mdkk::st4(dst, i, p);
+    mdkk::st4(ref, i, p);
+}
 }
 
 extern "C" {
@@ -30,14 +41,21 @@ int mdkk_rebuild1_select(mdkk_ctx* ctx, double* x, int n, const double* lengths_
                          const int* ncell_host, int* keys, int* cell_start, int* order, double* x_sorted,
                          const double* v, double* v_sorted, const int64_t* gid, int64_t* gid_sorted, int* brows,
                          int* bcount, const double* combos_dev, int C, int* block_scratch, int* totals,
-                         int* totals_host, int* n_ghost_host, void* stream) {
+                         int* totals_host, int* n_ghost_host, double* x_ref, void* stream) {
     if (!ctx || n < 2 || C < 1 || !totals_host || !n_ghost_host || x_sorted == x || v_sorted == v ||
         gid_sorted == gid)
         return MDKK_E_ARG;
     cudaStream_t s = mdkk::as_stream(stream);
     int st = mdkk_wrap(x, n, lengths_host, stream);
     if (st == MDKK_OK) st = mdkk_bin_atoms(ctx, x, n, grid_host, ncell_host, keys, cell_start, order, stream);
-    if (st == MDKK_OK) st = mdkk_gather_rows4(x, order, n, x_sorted, stream);
+    if (st == MDKK_OK) {
+        if (x_ref) {
+            k_gather4_ref<<<mdkk::grid_for(n, 256), 256, 0, s>>>(x, order, n, x_sorted, x_ref);
+            MDKK_CHECK_LAUNCH("k_gather4_ref");
+        } else {
+            st = mdkk_gather_rows4(x, order, n, x_sorted, stream);
+        }
+    }
     // owned rows are now cell-sorted on the shell grid (cells >= halo wide): only rows within
     // two cell layers of the faces can be selected
     if (st == MDKK_OK) st = mdkk_boundary_rows(ctx, cell_start, ncell_host, 2, brows, bcount, stream);

@@ -513,8 +513,10 @@ class DistSystem:
         s.device_wrote(force=True)
 
     # ----------------------------------------------------------- migration
-    def migrate(self, halo: float, sort_width: float | None = None, zero_forces: bool = True) -> None:
-        """Wrap, send leavers to their bricks, append arrivals, re-sort, rebuild ghosts (mdkk/domain.py:324-334)."""
+    def migrate(self, halo: float, sort_width: float | None = None, zero_forces: bool = True,
+                ref_out=None) -> bool:
+        """Wrap, send leavers to their bricks, append arrivals, re-sort, rebuild ghosts (mdkk/domain.py:324-334).
+        `ref_out` is the one-rank engine hint of RankedSystem.migrate (not used here: returns False)."""
         s = self.store
         s.to_device()
         nl = s.n_local

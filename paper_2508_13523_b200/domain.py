@@ -552,19 +552,21 @@ class RankedSystem:
         s._views()
         s.device_wrote(pos=True)
 
-    def _migrate_single(self, halo: float, width: float, zero_forces: bool) -> bool:
+    def _migrate_single(self, halo: float, width: float, zero_forces: bool, ref_out=None) -> int:
         """One rank, periodic self-images only: migrate = wrap + spatial sort + ghost
         selection + ghost rows, with everything up to the ghost totals issued by one
         library call (mdkk_rebuild1_select).  The same kernels in the same order as the
-        general path (bit-identical rows, ghosts and bins); False (nothing done) when
-        the fast path does not apply."""
+        general path (bit-identical rows, ghosts and bins); 0 when the fast path does
+        not apply (nothing done), 1 when done, 2 when `ref_out` was also written."""
         if halo <= 0 or halo > 0.5 * self.box.min_periodic_length():
-            return False   # the general path raises the reference's DomainError
+            return 0   # the general path raises the reference's DomainError
         s = self.stores[0]
         meta, tab, codes = self._combos(0, halo)
         C_ = len(meta)
         if C_ == 0:
-            return False
+            return 0
+        if ref_out is not None and (ref_out.shape[0] < s.n_local or ref_out.device != self.device):
+            ref_out = None
         lib, stream, ctx = _lib.lib(), _lib.stream(self.device), _lib.ctx(self.device)
         s.to_device()
         n = s.n_local
@@ -590,7 +592,7 @@ class RankedSystem:
             ctx, s.x.data_ptr(), n, _lib.dbl3(self.box.lengths), garr, narr, keys.data_ptr(), start.data_ptr(),
             order.data_ptr(), x2.data_ptr(), s.v.data_ptr(), v2.data_ptr(), s.gid.data_ptr(), g2.data_ptr(),
             rows.data_ptr(), nrow.data_ptr(), tab.data_ptr(), C_, blk.data_ptr(), tot.data_ptr(), pin.data_ptr(),
-            _lib.C.byref(ngh), stream), "mdkk_rebuild1_select")
+            _lib.C.byref(ngh), ref_out.data_ptr() if ref_out is not None else None, stream), "mdkk_rebuild1_select")
         ng = ngh.value
         s._alt = (s.x, s.v, s.gid)
         s.x, s.v, s.gid = x2, v2, g2
@@ -613,7 +615,7 @@ class RankedSystem:
         s.device_wrote(pos=True, vel=True, force=True)
         if zero_forces:
             s.f[: s.n_total].zero_()
-        return True
+        return 2 if ref_out is not None else 1
 
     def _run_tails(self):
         for s in self.stores:
@@ -664,17 +666,22 @@ class RankedSystem:
             s.device_wrote(force=True)
 
     # ----------------------------------------------------------- migration
-    def migrate(self, halo: float, sort_width: float | None = None, zero_forces: bool = True) -> None:
+    def migrate(self, halo: float, sort_width: float | None = None, zero_forces: bool = True,
+                ref_out: torch.Tensor | None = None) -> bool:
         """Wrap, reassign bricks, re-sort spatially, zero forces, rebuild ghosts (mdkk/domain.py:324-334).
         `zero_forces=False` (engine-internal: the forces are recomputed right away, and every
-        force path clears or overwrites the rows it reads) skips the reset."""
+        force path clears or overwrites the rows it reads) skips the reset.  `ref_out`
+        (engine-internal, one rank): rows4 buffer that also receives the sorted owned
+        positions (the next lists' skin-test reference); returns whether it was written."""
         lib, stream = _lib.lib(), _lib.stream(self.device)
         ctx = _lib.ctx(self.device)
         L = _lib.dbl3(self.box.lengths)
         R = self.n_ranks
         w = sort_width or self.sort_width
-        if R == 1 and w and w >= halo and self.stores[0].n_local >= 2 and self._migrate_single(halo, w, zero_forces):
-            return
+        if R == 1 and w and w >= halo and self.stores[0].n_local >= 2:
+            done = self._migrate_single(halo, w, zero_forces, ref_out)
+            if done:
+                return done == 2
         grid = _lib.int_arr(self.rankset.grid)
         for s in self.stores:
             s.to_device()
@@ -726,6 +733,7 @@ class RankedSystem:
         if zero_forces:
             for s in self.stores:   # the reference resets forces at migration (new AtomStores)
                 s.f[: s.n_total].zero_()
+        return False
 
     def sort_local(self, width: float) -> None:
         """Re-order every rank's owned rows into serpentine cell order (drops ghosts; call before exchange)."""

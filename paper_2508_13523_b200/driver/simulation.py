@@ -372,11 +372,15 @@ class Simulation:
         halo = self.style.r_c + self.config.skin
         # forces are recomputed right after (full lists overwrite every owned row, half
         # lists and SNAP clear the rows they accumulate into): no reset pass
-        self.system.migrate(halo, zero_forces=False)
         old = self.lists if self.lists is not None and len(self.lists) == len(self.system.stores) else None
-        ready = False
-        if old is not None and all(o.ref_dev.shape[0] >= max(s.n_local, 1)
-                                   for o, s in zip(old, self.system.stores)):
+        # one rank: the sort's position gather also fills the recycled skin-test reference
+        ready = bool(self.system.migrate(halo, zero_forces=False,
+                                         ref_out=old[0].ref_dev if old is not None and len(old) == 1 else None))
+        old = self.lists if self.lists is not None and len(self.lists) == len(self.system.stores) else None
+        if ready and old is None:
+            ready = False
+        if not ready and old is not None and all(o.ref_dev.shape[0] >= max(s.n_local, 1)
+                                                 for o, s in zip(old, self.system.stores)):
             # the new lists' skin-test reference = the owned positions now: copied here, so the
             # device does it while the host prepares the build (not after the build kernel)
             for o, s in zip(old, self.system.stores):
