@@ -8,10 +8,25 @@
 // read-back is queued back to back, the velocity / gid gathers go behind the
 // totals' copy (device work while the host waits), and the host waits on an
 // event for that copy only.
-#include "common.cuh"
+#include "cluster.cuh"
 
 namespace {
 cudaEvent_t g_totals_ev[64];   // per device, created lazily
+
+// Wrap (pos - L floor(pos / L) with explicit roundings, as k_wrap / mdkk/domain.py:62)
+// and the cell key of the wrapped row (as k_cell_keys), one pass over x.
+__global__ void k_wrap_keys(double* __restrict__ x, int n, double Lx, double Ly, double Lz, mdkk::Grid g,
+                            int* __restrict__ key) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double4 p = mdkk::ld4_nc(x, i);
+    p.x = __dsub_rn(p.x, __dmul_rn(Lx, floor(p.x / Lx)));
+    p.y = __dsub_rn(p.y, __dmul_rn(Ly, floor(p.y / Ly)));
+    p.z = __dsub_rn(p.z, __dmul_rn(Lz, floor(p.z / Lz)));
+    mdkk::st4(x, i, p);
+    const int3 c = mdkk::cell_of(g, p.x, p.y, p.z);
+    key[i] = mdkk::cell_key(g, c.x, c.y, c.z);
+}
 
 // The sort's position gather, also writing the rows into the new lists' skin-test
 // reference (the build-time positions) -- one pass over x instead of a later copy.
@@ -27,9 +42,8 @@ __global__ void k_gather4_ref(const double* __restrict__ src, const int* __restr
 
 extern "C" {
 
-int mdkk_wrap(double* x, int n, const double* lengths_host, void* stream);
-int mdkk_bin_atoms(mdkk_ctx* ctx, const double* x, int n, const double* grid_host, const int* ncell_host,
-                   int* keys, int* cell_start, int* cell_atoms, void* stream);
+int mdkk_bucket_sort(mdkk_ctx* ctx, const int* keys, int n, int nbuckets, int* bucket_start, int* order,
+                     void* stream);
 int mdkk_gather_rows4(const double* src, const int* perm, int n, double* dst, void* stream);
 int mdkk_gather_i64(const int64_t* src, const int* perm, int n, int64_t* dst, void* stream);
 int mdkk_boundary_rows(mdkk_ctx* ctx, const int* cell_start, const int* ncell_host, int layer, int* rows,
@@ -46,8 +60,13 @@ int mdkk_rebuild1_select(mdkk_ctx* ctx, double* x, int n, const double* lengths_
         gid_sorted == gid)
         return MDKK_E_ARG;
     cudaStream_t s = mdkk::as_stream(stream);
-    int st = mdkk_wrap(x, n, lengths_host, stream);
-    if (st == MDKK_OK) st = mdkk_bin_atoms(ctx, x, n, grid_host, ncell_host, keys, cell_start, order, stream);
+    const long long ncl = (long long)ncell_host[0] * ncell_host[1] * ncell_host[2];
+    if (ncl < 1 || ncl > (1LL << 30)) return MDKK_E_ARG;
+    const mdkk::Grid g = mdkk::make_grid(grid_host, ncell_host);
+    k_wrap_keys<<<mdkk::grid_for(n, 256), 256, 0, s>>>(x, n, lengths_host[0], lengths_host[1], lengths_host[2], g,
+                                                       keys);
+    MDKK_CHECK_LAUNCH("k_wrap_keys");
+    int st = mdkk_bucket_sort(ctx, keys, n, (int)ncl, cell_start, order, stream);
     if (st == MDKK_OK) {
         if (x_ref) {
             k_gather4_ref<<<mdkk::grid_for(n, 256), 256, 0, s>>>(x, order, n, x_sorted, x_ref);
