@@ -360,6 +360,7 @@ class RankedSystem:
         self.dense_gids = dense_gids
         self.n_atoms = sum(s.n_local for s in stores)
         self._shift_dev = torch.from_numpy(SHIFT_UNITS * box.lengths).to(self.device)
+        self._lengths_c = _lib.dbl3(box.lengths)   # ctypes double[3] for the per-rebuild calls
         self._combo_cache = {}
         self._scratch = {}
         self.sort_width = None  # spatial-sort bin width (set by the first neighbour build)
@@ -589,7 +590,7 @@ class RankedSystem:
             pin = self._scratch["tot_pin"] = torch.zeros(max(C_, 64), dtype=torch.int32, pin_memory=True)
         ngh = _lib.C.c_int(0)
         _lib.check(lib.mdkk_rebuild1_select(
-            ctx, s.x.data_ptr(), n, _lib.dbl3(self.box.lengths), garr, narr, keys.data_ptr(), start.data_ptr(),
+            ctx, s.x.data_ptr(), n, self._lengths_c, garr, narr, keys.data_ptr(), start.data_ptr(),
             order.data_ptr(), x2.data_ptr(), s.v.data_ptr(), v2.data_ptr(), s.gid.data_ptr(), g2.data_ptr(),
             rows.data_ptr(), nrow.data_ptr(), tab.data_ptr(), C_, blk.data_ptr(), tot.data_ptr(), pin.data_ptr(),
             _lib.C.byref(ngh), ref_out.data_ptr() if ref_out is not None else None, stream), "mdkk_rebuild1_select")

@@ -261,15 +261,6 @@ def build(store: AtomStore, box: Box, cutoff: float, skin: float, style: str = "
     keys = cache.get("keys", n_total, torch.int32, dev)
     cstart = cache.get("cstart", ncell + 1, torch.int32, dev)
     catoms = cache.get("catoms", n_total, torch.int32, dev)
-    if merged is None:
-        pass
-    elif merged:
-        _lib.check(lib.mdkk_bin_merge(ctx, store.x.data_ptr(), n_local, n_total, garr, narr, bins[2].data_ptr(),
-                                      keys.data_ptr(), cstart.data_ptr(), catoms.data_ptr(), stream),
-                   "mdkk_bin_merge")
-    else:
-        _lib.check(lib.mdkk_bin_atoms(ctx, store.x.data_ptr(), n_total, garr, narr, keys.data_ptr(),
-                                      cstart.data_ptr(), catoms.data_ptr(), stream), "mdkk_bin_atoms")
     if cap_hint is None and n_local:
         # first build: size the table from the density (mean partners 4/3 pi bc^3 rho,
         # halved for half lists, +25 % for fluctuations) instead of growing by retries
@@ -281,8 +272,21 @@ def build(store: AtomStore, box: Box, cutoff: float, skin: float, style: str = "
     counts = _recycled(recycle.counts_dev if recycle is not None else None, (max(n_local, 1),), torch.int32, dev)
     mc = cache.get("mc", 1, torch.int32, dev)   # one element; stream-ordered reuse across builds
     mc.zero_()
-    if defer and cap_hint is not None:
+    deferred = defer and cap_hint is not None
+    if deferred:
         table = _recycled(old_t, ((n_local + 31) // 32 or 1, alloc, 32), torch.int32, dev)
+    # the list buffers are ready before the binning is queued: binning and build go out
+    # back to back (no host work between their launches while the device waits)
+    if merged is None:
+        pass
+    elif merged:
+        _lib.check(lib.mdkk_bin_merge(ctx, store.x.data_ptr(), n_local, n_total, garr, narr, bins[2].data_ptr(),
+                                      keys.data_ptr(), cstart.data_ptr(), catoms.data_ptr(), stream),
+                   "mdkk_bin_merge")
+    else:
+        _lib.check(lib.mdkk_bin_atoms(ctx, store.x.data_ptr(), n_total, garr, narr, keys.data_ptr(),
+                                      cstart.data_ptr(), catoms.data_ptr(), stream), "mdkk_bin_atoms")
+    if deferred:
         _lib.check(lib.mdkk_nbr_build(ctx, store.x.data_ptr(), n_local, n_total, garr, narr, cstart.data_ptr(),
                                       catoms.data_ptr(), store.gid.data_ptr(), store.orank.data_ptr(),
                                       store.rank, bc, STYLES[style], int(bool(newton)), alloc,
