@@ -13,7 +13,9 @@ import threading
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmdkk_b200.so")
+_DEFAULT_LIB = os.path.join(HERE, "libmdkk_b200.so")
+# MDKK_LIB: an alternative build of the same library (A/B experiments on the GPU box)
+LIB_PATH = os.environ.get("MDKK_LIB") or _DEFAULT_LIB
 
 OK, E_CAPACITY, E_COINCIDENT, E_NONFINITE, E_ARG, E_CUDA = range(6)
 FLAG_COINCIDENT, FLAG_NONFINITE = 1, 2
