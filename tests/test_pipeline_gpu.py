@@ -168,3 +168,36 @@ def test_nonfinite_energy_is_named_with_its_step(gpu):
     sim.style.compute_device = poisoned
     with pytest.raises(RunError, match="non-finite potential energy at step 4$"):
         sim.run_nve(40)
+
+
+def test_single_rank_migrate_fast_path_matches_general_path(gpu):
+    """RankedSystem.migrate's one-rank fast path (mdkk_rebuild1_select: wrap, cell sort,
+    boundary rows, halo count in one call; the sort's gather also fills a skin-test
+    reference) gives bit for bit the rows, ghosts and bins of the general path."""
+    import torch
+    from oracle import md
+    from paper_2508_13523_b200 import Box, RankedSystem
+    from paper_2508_13523_b200.domain import shell_grid_args
+
+    pos, lengths = md.lattice("fcc", 0.8442, (10, 10, 10))
+    pos = md.jittered(pos, 0.3, 7) + 0.37 * lengths   # drifted past the box: wrap has work
+    vel = md.jittered(np.zeros_like(pos), 1.0, 8)
+    out = {}
+    for fast in (True, False):
+        system = RankedSystem.distribute(Box(lengths), 1, pos, vel)
+        system.sort_width = 2.8
+        if not fast:
+            system._migrate_single = lambda *a, **k: 0   # force the general path
+        ref = torch.zeros_like(system.stores[0].x)
+        wrote = system.migrate(2.8, zero_forces=False, ref_out=ref)
+        s = system.stores[0]
+        nt = s.n_total
+        ncell = shell_grid_args(s.lo, s.hi, 2.8)[4]
+        out[fast] = (s.x[:nt].cpu(), s.v[: s.n_local].cpu(), s.gid[:nt].cpu(), s.oidx[nt - s.n_ghost:nt].cpu(),
+                     s._bins[2][: ncell + 1].cpu(), s.n_ghost, wrote, ref[: s.n_local].cpu())
+    a, b = out[True], out[False]
+    assert a[5] == b[5] and a[5] > 0
+    for k in range(5):
+        assert torch.equal(a[k], b[k]), k
+    assert a[6] is True and b[6] is False
+    assert torch.equal(a[7], a[0][: a[7].shape[0]])   # the reference rows are the sorted owned rows
