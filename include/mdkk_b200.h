@@ -19,6 +19,10 @@
  *  - `stream` is a cudaStream_t (may be NULL = legacy default stream).
  *  - Every function returns an mdkk_status; calls are asynchronous on
  *    `stream` unless documented otherwise.  No C++ exception crosses the ABI.
+ *  - One host thread and one stream per device at a time (the reference
+ *    driver is single-threaded): a context's scratch arena and the
+ *    energy/virial reductions' device-side stage are shared by the calls
+ *    issued on a device.
  */
 #ifndef MDKK_B200_H
 #define MDKK_B200_H
