@@ -34,6 +34,7 @@ METRICS = {
     "dfma": "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum",
     "dadd": "smsp__sass_thread_inst_executed_op_dadd_pred_on.sum",
     "dmul": "smsp__sass_thread_inst_executed_op_dmul_pred_on.sum",
+    "l2_sectors": "lts__t_sectors.sum",
 }
 SCALE = {"usecond": 1.0, "msecond": 1e3, "nsecond": 1e-3, "us": 1.0, "ms": 1e3, "ns": 1e-3, "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6,
          "Gbyte": 1e9, "%": 1.0, "": 1.0, "inst": 1.0, "Kinst": 1e3, "Minst": 1e6, "Ginst": 1e9}
@@ -59,7 +60,7 @@ def summarize(recs, atoms):
     out = {"launches": n, "n_atoms": atoms, "duration_us": avg["duration_us"],
            "dram_bytes": avg["dram_read"] + avg["dram_write"], "l1tex_wavefront_pct": avg["l1tex_wavefront_pct"],
            "fp64_pipe_pct": avg["fp64_pipe_pct"], "warps_active_pct": avg["warps_active_pct"],
-           "dflop": 2 * avg["dfma"] + avg["dadd"] + avg["dmul"]}
+           "dflop": 2 * avg["dfma"] + avg["dadd"] + avg["dmul"], "l2_bytes": 32.0 * avg["l2_sectors"]}
     return out
 
 
