@@ -13,7 +13,7 @@ from .coupling import make_coupling_tables, read_coeff_file
 class SnapStyle:
     list_style = "full"  # the expansion needs every neighbour of every atom
 
-    def __init__(self, r_c: float, jmax: float, beta, name: str = "snap/kk", batch_u: int = 4, batch_y: int = 1,
+    def __init__(self, r_c: float, jmax: float, beta, name: str = "snap/kk", batch_u: int = 4, batch_y: int = 2,
                  tile_v: int = 0, layout: str = "a"):
         self.name = name
         self.r_c = float(r_c)
