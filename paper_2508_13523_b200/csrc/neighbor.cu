@@ -49,38 +49,25 @@ __global__ void k_cell_positions(const double* __restrict__ x, const int* __rest
     xs[s] = make_float4((float)p.x, (float)p.y, (float)p.z, __int_as_float(j));   // .w = the row
 }
 
-// Binning merge (engine rebuilds): the owned rows are already sorted by cell on this
-// grid (the spatial sort, bucket starts owned_start), the ghost rows binned on their
-// own (ghost_start, ghost_order over rows n_local..n_total): the combined cell lists
-// are owned rows then ghost rows per cell, both ascending -- exactly mdkk_bin_atoms
-// over all rows, without re-sorting the owned ones.
-__global__ void k_merge_starts(const int* __restrict__ owned_start, const int* __restrict__ ghost_start, int ncell,
-                               int* __restrict__ cell_start) {
-    int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c <= ncell) cell_start[c] = owned_start[c] + ghost_start[c];
-}
-
-__global__ void k_merge_owned(const double* __restrict__ x, int n_local, Grid g, const int* __restrict__ owned_start,
-                              const int* __restrict__ cell_start, int* __restrict__ cell_atoms) {
-    int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= n_local) return;
-    const double4 p = mdkk::ld4(x, r);
-    const int3 cc = mdkk::cell_of(g, p.x, p.y, p.z);
-    const int c = mdkk::cell_key(g, cc.x, cc.y, cc.z);
-    cell_atoms[cell_start[c] + (r - owned_start[c])] = r;
-}
-
-__global__ void k_merge_ghosts(const double* __restrict__ x, int n_local, int n_ghost, Grid g,
-                               const int* __restrict__ owned_start, const int* __restrict__ ghost_start,
-                               const int* __restrict__ ghost_order, const int* __restrict__ cell_start,
-                               int* __restrict__ cell_atoms) {
-    int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= n_ghost) return;
-    const int row = n_local + ghost_order[k];
-    const double4 p = mdkk::ld4(x, row);
-    const int3 cc = mdkk::cell_of(g, p.x, p.y, p.z);
-    const int c = mdkk::cell_key(g, cc.x, cc.y, cc.z);
-    cell_atoms[cell_start[c] + (owned_start[c + 1] - owned_start[c]) + (k - ghost_start[c])] = row;
+// Merged cell lists (mdkk_bin_merge), one warp per cell: cell_start[c] = owned_start[c] +
+// ghost_start[c]; the cell's owned rows (rows owned_start[c] .. owned_start[c+1] of the
+// cell-sorted brick) then its ghost rows (n_local + ghost_order[...]) -- exactly the
+// bin_atoms order over all rows (owned then ghost rows per cell, each ascending).
+__global__ void k_merge_cells(const int* __restrict__ owned_start, const int* __restrict__ ghost_start,
+                              const int* __restrict__ ghost_order, int ncell, int n_local, int n_total,
+                              int* __restrict__ cell_start, int* __restrict__ cell_atoms) {
+    const int c = (int)(((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
+    if (c >= ncell) return;
+    const int os = owned_start[c], no = owned_start[c + 1] - os;
+    const int gs = ghost_start[c], ng = ghost_start[c + 1] - gs;
+    const int b = os + gs;
+    if (lane == 0) {
+        cell_start[c] = b;
+        if (c == ncell - 1) cell_start[ncell] = n_total;
+    }
+    for (int t = lane; t < no; t += 32) cell_atoms[b + t] = os + t;
+    for (int t = lane; t < ng; t += 32) cell_atoms[b + no + t] = n_local + ghost_order[gs + t];
 }
 
 __device__ __forceinline__ bool lex_zyx_less(double ax, double ay, double az, double bx, double by, double bz) {
@@ -773,31 +760,25 @@ int mdkk_bin_merge(mdkk_ctx* ctx, const double* x, int n_local, int n_total, con
     const int ncell = (int)ncl, n_ghost = n_total - n_local;
     Grid g = mdkk::make_grid(grid_host, ncell_host);
     cudaStream_t s = mdkk::as_stream(stream);
-    // ghost bins in ctx scratch after the ghost sort's own use of it: [ghost_start | ghost_order]
-    int* gstart = static_cast<int*>(mdkk::scratch(ctx, sizeof(int) * ((size_t)ncell + 2 + (size_t)n_ghost + 64)));
-    if (!gstart) return mdkk::cuda_fail(cudaErrorMemoryAllocation, "scratch");
-    // the ghost rows' own binning writes into caller buffers first (it uses the scratch itself)
-    int* gorder = cell_atoms + n_local;   // free until the merge below fills cell_atoms
-    int st = mdkk_bin_atoms(ctx, x + 4LL * n_local, n_ghost, grid_host, ncell_host, keys, cell_start, gorder,
-                            stream);
+    // ghost bins in ctx scratch, after the bucket sort's own counters: [cnt | ghost_start | ghost_order]
+    // (the whole arena is requested first, so the sort's smaller request does not move it)
+    // (the bucket sort's footprint: ncell + 1 counters, or the few-bucket path's block table)
+    const size_t nbk = ((size_t)n_ghost + 255) / 256;
+    const size_t sort_words = ncell > 64 ? (size_t)ncell + 1 : 2 * ((size_t)ncell * nbk + 1);
+    const size_t cnt_words = (sort_words + 63) & ~(size_t)63;
+    int* base = static_cast<int*>(
+        mdkk::scratch(ctx, sizeof(int) * (cnt_words + (size_t)ncell + 64 + (size_t)n_ghost + 64)));
+    if (!base) return mdkk::cuda_fail(cudaErrorMemoryAllocation, "scratch");
+    int* gstart = base + cnt_words;
+    int* gord = gstart + ncell + 64;
+    int st = mdkk_cell_keys(x + 4LL * n_local, n_ghost, grid_host, ncell_host, keys, stream);
+    if (st == MDKK_OK) st = mdkk_bucket_sort(ctx, keys, n_ghost, ncell, gstart, gord, stream);
     if (st != MDKK_OK) return st;
-    if (n_ghost == 0) cudaMemsetAsync(cell_start, 0, sizeof(int) * ((size_t)ncell + 1), s);
-    gstart = static_cast<int*>(mdkk::scratch(ctx, sizeof(int) * ((size_t)ncell + 2 + (size_t)n_ghost + 64)));
-    if (!gstart) return mdkk::cuda_fail(cudaErrorMemoryAllocation, "scratch");
-    int* gord = gstart + ncell + 2;
-    cudaMemcpyAsync(gstart, cell_start, sizeof(int) * ((size_t)ncell + 1), cudaMemcpyDeviceToDevice, s);
-    if (n_ghost) cudaMemcpyAsync(gord, gorder, sizeof(int) * (size_t)n_ghost, cudaMemcpyDeviceToDevice, s);
-    k_merge_starts<<<mdkk::grid_for(ncell + 1, 256), 256, 0, s>>>(owned_start, gstart, ncell, cell_start);
-    MDKK_CHECK_LAUNCH("k_merge_starts");
-    if (n_local) {
-        k_merge_owned<<<mdkk::grid_for(n_local, 256), 256, 0, s>>>(x, n_local, g, owned_start, cell_start, cell_atoms);
-        MDKK_CHECK_LAUNCH("k_merge_owned");
-    }
-    if (n_ghost) {
-        k_merge_ghosts<<<mdkk::grid_for(n_ghost, 256), 256, 0, s>>>(x, n_local, n_ghost, g, owned_start, gstart, gord,
-                                                                    cell_start, cell_atoms);
-        MDKK_CHECK_LAUNCH("k_merge_ghosts");
-    }
+    // one warp per cell: its owned rows (a contiguous range of the sorted brick) then its ghost rows
+    k_merge_cells<<<mdkk::grid_for((long long)ncell * 32, 256), 256, 0, s>>>(owned_start, gstart, gord, ncell,
+                                                                              n_local, n_total, cell_start,
+                                                                              cell_atoms);
+    MDKK_CHECK_LAUNCH("k_merge_cells");
     return MDKK_OK;
 }
 
