@@ -70,11 +70,10 @@ __device__ __forceinline__ double block_tree_sum(double s, double* sm) {
     return v;   // valid in thread 0
 }
 
-__global__ void __launch_bounds__(1024) k_reduce_partials(const double* __restrict__ p, int nb, int K,
-                                                          double* __restrict__ out, int zero_to) {
+__device__ __forceinline__ void reduce_block(const double* __restrict__ p, int nb, int K, double* __restrict__ out,
+                                             int zero_to, int k, int g) {
     __shared__ double sm[32];
     __shared__ bool last;
-    const int k = blockIdx.y, g = blockIdx.x;
     const int per = (nb + kRedG - 1) / kRedG, b0 = g * per, b1 = min(nb, b0 + per);
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
     int b = b0 + threadIdx.x;
@@ -103,8 +102,40 @@ __global__ void __launch_bounds__(1024) k_reduce_partials(const double* __restri
     if (k == 0 && threadIdx.x >= K && threadIdx.x < zero_to) out[threadIdx.x] = 0.0;
 }
 
+__global__ void __launch_bounds__(1024) k_reduce_partials(const double* __restrict__ p, int nb, int K,
+                                                          double* __restrict__ out, int zero_to) {
+    reduce_block(p, nb, K, out, zero_to, blockIdx.y, blockIdx.x);
+}
+
+// The same reduction with the next step's halo pack in extra blocks of the same launch
+// (both only wait for the force kernel): blocks [0, kRedG K) reduce, the rest write
+// ghost rows out[k] = x[idx[k]] + shift[code[k]] (k_pack_shift's rounding).
+__global__ void __launch_bounds__(1024) k_reduce_pack(const double* __restrict__ p, int nb, int K,
+                                                      double* __restrict__ out, int zero_to,
+                                                      const double* __restrict__ x, const int* __restrict__ idx,
+                                                      const int8_t* __restrict__ code, const double* __restrict__ shifts,
+                                                      int n_pack, double* __restrict__ x_ghost) {
+    const int nred = kRedG * K;
+    if ((int)blockIdx.x < nred) {
+        reduce_block(p, nb, K, out, zero_to, blockIdx.x / kRedG, blockIdx.x % kRedG);
+        return;
+    }
+    const int t = (blockIdx.x - nred) * 1024 + threadIdx.x;
+    if (t >= n_pack) return;
+    const double4 q = ld4_nc(x, idx[t]);
+    const double* sh = shifts + 3 * code[t];
+    st4(x_ghost, t, make_double4(q.x + sh[0], q.y + sh[1], q.z + sh[2], 0.0));
+}
+
 void reduce_partials(const double* partials, int nblocks, int K, double* out, cudaStream_t s, int zero_to) {
     k_reduce_partials<<<dim3(kRedG, K), 1024, 0, s>>>(partials, nblocks, K, out, zero_to);
+}
+
+void reduce_partials_pack(const double* partials, int nblocks, int K, double* out, int zero_to, const double* x,
+                          const int* idx, const int8_t* code, const double* shifts, int n_pack, double* x_ghost,
+                          cudaStream_t s) {
+    const int blocks = kRedG * K + (n_pack + 1023) / 1024;
+    k_reduce_pack<<<blocks, 1024, 0, s>>>(partials, nblocks, K, out, zero_to, x, idx, code, shifts, n_pack, x_ghost);
 }
 
 }  // namespace mdkk

@@ -621,6 +621,8 @@ class Simulation:
             if dist_:
                 self.system.allreduce_max(d2[k:k + 1])
 
+        fuse_pack = (not dist_) and isinstance(self.system, RankedSystem) and self.system.n_ranks == 1
+        packed = False   # the ghost rows of the current x were written by the previous launch
         # opening of step 1: the classic pass (with any deferred closing kick)
         s.to_device()
         _lib.check(lib.mdkk_verlet_first(ctx, s.x.data_ptr(), s.v.data_ptr(), s.f.data_ptr(),
@@ -639,11 +641,22 @@ class Simulation:
             xa = x_alt() if mode == 2 else None
 
             def launch(gated, part=0):
+                nonlocal packed
                 if mode == 2 and part != 2:
                     d2[nxt:nxt + 1].zero_()
                 integ = dict(mode=mode, x_next=xa, d2_next=d2[nxt:nxt + 1], dt=self.dt, h=h, part=part)
                 if part:
                     integ["flags"] = self.system.cluster_flags(self.lists[0], overlap_halo)
+                packed = False
+                if mode == 2 and fuse_pack:
+                    # one rank: step s+1's periodic ghost rows are written from x(s+1) in the
+                    # force launch's reduction blocks (the separate pack of the next step is skipped)
+                    lanes = self.system.lanes
+                    if not lanes:
+                        packed = True
+                    elif len(lanes) == 1 and lanes[0].start == s.n_local:
+                        integ["pack"] = (lanes[0], self.system._shift_dev)
+                        packed = True
                 return self._forces_device(gate=d2[cur:cur + 1] if gated else None, gate_limit=half, integ=integ)
 
             if overlap:
@@ -654,7 +667,8 @@ class Simulation:
                 self.system.forward_comm_end(pending)
                 e = launch(True, part=2)
             else:
-                self.system.forward_comm()             # speculative halo refresh
+                if not packed:
+                    self.system.forward_comm()         # speculative halo refresh
                 e = launch(True)                       # speculative force + integration
             if mode == 2:
                 global_max(nxt)

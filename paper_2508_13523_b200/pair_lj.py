@@ -128,6 +128,18 @@ def lj_force_rank(store, nl: NeighborList, params: PairParams, ev: torch.Tensor,
     # mode "atom": one thread per owned atom; "neighbor": a team of lanes per atom
     # splitting its list (mdkk/pair_lj.py:118-143)
     pend = nl._pending
+    if integ is not None and integ.get("pack") is not None:
+        # ... + the next step's periodic ghost rows in the reduction's launch (one rank)
+        ln, shifts = integ["pack"]
+        _lib.check(_lib.lib().mdkk_lj_force_integrate_pack(
+            _lib.ctx(dev), store.x.data_ptr(), store.n_local, nl.table_dev.data_ptr(), nl.counts_dev.data_ptr(),
+            nl.alloc_cap, int(virial), params.epsilon, params.sigma, params.r_c, store.f.data_ptr(), ev.data_ptr(),
+            flags.data_ptr(), gate.data_ptr() if gate is not None else None, gate_limit,
+            pend[0].data_ptr() if pend is not None else None, nl.alloc_cap, store.v.data_ptr(),
+            nl.ref_dev.data_ptr(), integ["x_next"].data_ptr(), integ["d2_next"].data_ptr(), integ["dt"], integ["h"],
+            ln.idx.data_ptr(), ln.code.data_ptr(), shifts.data_ptr(), ln.count, _lib.stream(dev)),
+            "mdkk_lj_force_integrate_pack")
+        return
     if integ is not None:
         # full list + velocity-Verlet epilogue (engine advance loop; mdkk_lj_force_integrate)
         _lib.check(_lib.lib().mdkk_lj_force_integrate(

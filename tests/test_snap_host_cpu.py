@@ -100,6 +100,6 @@ def test_run_config_knobs_override_style_knobs():
     from paper_2508_13523_b200.driver import RunConfig
     from paper_2508_13523_b200.snap.style import SnapStyle
     st = SnapStyle(4.73, 1, np.zeros(5), batch_u=8, tile_v=256)
-    assert st._knobs(RunConfig()) == {"batch_u": 8, "batch_y": 1, "tile_v": 256, "layout": "a"}
+    assert st._knobs(RunConfig()) == {"batch_u": 8, "batch_y": 2, "tile_v": 256, "layout": "a"}
     assert st._knobs(RunConfig(batch_u=2, batch_y=3, layout="b")) == {"batch_u": 2, "batch_y": 3, "tile_v": 256,
                                                                       "layout": "b"}
