@@ -62,14 +62,31 @@ print("cpu ops (total us), top 15:")
 for n, d in cpu.most_common(15):
     print(f"  {d / 1e3:8.3f} ms  {n}")
 # per step: ops from one step delimiter to the next (the fused loop has no per-step
-# verlet pass; every step starts with its speculative halo pack)
+# verlet pass; each step starts with its speculative halo pack -- on one rank the pack
+# rides in the previous force launch's reduction, k_reduce_pack, which then delimits)
 delim = "k_verlet_first" if loop != "advance" else "k_pack_shift"
+if loop == "advance" and any("k_reduce_pack" in e["name"] for e in k):
+    delim = "k_reduce_pack"
 starts = [n for n, e in enumerate(k) if delim in e["name"]]
 rows = []
+def _union(iv):
+    tot, cur_s, cur_e = 0.0, None, None
+    for s0, e0 in sorted(iv):
+        if cur_e is None or s0 > cur_e:
+            if cur_e is not None:
+                tot += cur_e - cur_s
+            cur_s, cur_e = s0, e0
+        else:
+            cur_e = max(cur_e, e0)
+    return tot + ((cur_e - cur_s) if cur_e is not None else 0.0)
+
+
 for a, b in zip(starts, starts[1:]):
     ops = k[a:b]
-    idle = sum(max(0.0, y["ts"] - (x["ts"] + x["dur"])) for x, y in zip(ops, ops[1:] + [k[b]]))
-    busy = sum(e["dur"] for e in ops)
+    # device busy = union of the ops' intervals (side-stream copies overlap kernels);
+    # idle = the step's span (to the next step's first op) minus that union
+    busy = _union([(e["ts"], e["ts"] + e["dur"]) for e in ops])
+    idle = max(0.0, (k[b]["ts"] - ops[0]["ts"]) - busy)
     rebuild = any("nbr_build" in e["name"] for e in ops)
     rows.append((rebuild, busy, idle, a, b))
 for reb in (False, True):
