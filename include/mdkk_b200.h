@@ -226,13 +226,14 @@ int mdkk_lj_force_integrate(mdkk_ctx* ctx, const double* x, int n_local, const i
  * writes step s+1's periodic ghost rows (forward_comm, mdkk/domain.py:295-305):
  * x_next[n_local + k] = x_next[pack_idx[k]] + pack_shifts[pack_code[k]] for k < pack_n, in
  * the reduction's launch -- one rank with its own periodic images (the engine's fused
- * loop, which then skips the separate pack). */
+ * loop, which then skips the separate pack).  d2_zero (optional): a drift-maximum slot
+ * cleared in the same launch (the engine's three-slot ring: the slot two steps ahead). */
 int mdkk_lj_force_integrate_pack(mdkk_ctx* ctx, const double* x, int n_local, const int* table, const int* counts,
                                  int cap, int virial, double epsilon, double sigma, double rc, double* f, double* ev,
                                  int* flags, const double* maxdisp2, double half_skin, const int* max_count,
                                  int count_limit, double* v, const double* x_ref, double* x_next, double* d2_next,
                                  double dt, double h, const int* pack_idx, const int8_t* pack_code,
-                                 const double* pack_shifts, int pack_n, void* stream);
+                                 const double* pack_shifts, int pack_n, double* d2_zero, void* stream);
 /* Boundary flags per 32-row cluster for the halo overlap (engine-internal; no reference
  * counterpart): flags[c] = 1 when the cluster's bounding box lies within `halo` of a
  * brick face [lo, hi) in a dimension of dims_mask (bit d: the neighbour bricks along d

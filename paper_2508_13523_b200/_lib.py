@@ -60,7 +60,7 @@ SIGNATURES = {
     "mdkk_lj_force_integrate": [_p, _p, _i, _p, _p, _i, _i, _d, _d, _d, _p, _p, _p, _p, _d, _p, _i, _i, _p, _p, _p,
                                 _p, _d, _d, _p, _i, _p],
     "mdkk_lj_force_integrate_pack": [_p, _p, _i, _p, _p, _i, _i, _d, _d, _d, _p, _p, _p, _p, _d, _p, _i, _p, _p, _p,
-                                     _p, _d, _d, _p, _p, _p, _i, _p],
+                                     _p, _d, _d, _p, _p, _p, _i, _p, _p],
     "mdkk_cluster_flags": [_p, _i, _p, _p, _d, _i, _p, _p],
     "mdkk_lj_force_gated": [_p, _p, _i, _p, _p, _i, _i, _i, _i, _i, _d, _d, _d, _p, _p, _p, _p, _d, _p, _i, _p],
     "mdkk_lj_force_neighbor": [_p, _p, _i, _p, _p, _i, _i, _i, _i, _d, _d, _d, _p, _p, _p, _p],

@@ -120,10 +120,11 @@ __device__ __forceinline__ void block_sum(double (&v)[K], double* out, bool acc 
 // Deterministic second stage: out[k] = sum_b partials[b*K + k], fixed order;
 // out[K .. zero_to) are cleared in the same launch.
 void reduce_partials(const double* partials, int nblocks, int K, double* out, cudaStream_t s, int zero_to = 0);
-// The same, with a halo pack (x_ghost[k] = x[idx[k]] + shifts[code[k]], k < n_pack) in the same launch.
+// The same, with a halo pack (x_ghost[k] = x[idx[k]] + shifts[code[k]], k < n_pack) in the same
+// launch; *zero_slot (optional) is cleared too.
 void reduce_partials_pack(const double* partials, int nblocks, int K, double* out, int zero_to, const double* x,
                           const int* idx, const int8_t* code, const double* shifts, int n_pack, double* x_ghost,
-                          cudaStream_t s);
+                          double* zero_slot, cudaStream_t s);
 
 // A drift maximum that cannot hide a blow-up: NaN / inf become +inf before the
 // (NaN-dropping) fmax reductions, so the host's per-step read-back sees it

@@ -114,8 +114,10 @@ __global__ void __launch_bounds__(1024) k_reduce_pack(const double* __restrict__
                                                       double* __restrict__ out, int zero_to,
                                                       const double* __restrict__ x, const int* __restrict__ idx,
                                                       const int8_t* __restrict__ code, const double* __restrict__ shifts,
-                                                      int n_pack, double* __restrict__ x_ghost) {
+                                                      int n_pack, double* __restrict__ x_ghost,
+                                                      double* __restrict__ zero_slot) {
     const int nred = kRedG * K;
+    if (zero_slot && blockIdx.x == 0 && threadIdx.x == 0) *zero_slot = 0.0;
     if ((int)blockIdx.x < nred) {
         reduce_block(p, nb, K, out, zero_to, blockIdx.x / kRedG, blockIdx.x % kRedG);
         return;
@@ -133,9 +135,10 @@ void reduce_partials(const double* partials, int nblocks, int K, double* out, cu
 
 void reduce_partials_pack(const double* partials, int nblocks, int K, double* out, int zero_to, const double* x,
                           const int* idx, const int8_t* code, const double* shifts, int n_pack, double* x_ghost,
-                          cudaStream_t s) {
+                          double* zero_slot, cudaStream_t s) {
     const int blocks = kRedG * K + (n_pack + 1023) / 1024;
-    k_reduce_pack<<<blocks, 1024, 0, s>>>(partials, nblocks, K, out, zero_to, x, idx, code, shifts, n_pack, x_ghost);
+    k_reduce_pack<<<blocks, 1024, 0, s>>>(partials, nblocks, K, out, zero_to, x, idx, code, shifts, n_pack, x_ghost,
+                                          zero_slot);
 }
 
 }  // namespace mdkk

@@ -421,7 +421,7 @@ static int lj_integrate(mdkk_ctx* ctx, const double* x, int n_local, const int* 
                         const double* maxdisp2, double half_skin, const int* max_count, int count_limit, int mode,
                         double* v, const double* x_ref, double* x_next, double* d2_next, double dt, double h,
                         const unsigned char* part_flags, int part, const int* pack_idx, const int8_t* pack_code,
-                        const double* pack_shifts, int pack_n, void* stream) {
+                        const double* pack_shifts, int pack_n, double* d2_zero, void* stream) {
     if (!ctx || n_local < 0 || cap < 1 || mode < 1 || mode > 2 || !v) return MDKK_E_ARG;
     if (part < 0 || part > 2 || (part && !part_flags)) return MDKK_E_ARG;
     if (mode == 2 && (!x_ref || !x_next || !d2_next || x_next == x)) return MDKK_E_ARG;
@@ -451,7 +451,7 @@ static int lj_integrate(mdkk_ctx* ctx, const double* x, int n_local, const int* 
     if (part == 1) return MDKK_OK;   // the reduction follows part 2
     if (pack_n > 0 && mode == 2) {   // + the next step's halo pack from x_next, same launch
         mdkk::reduce_partials_pack(partials, nb, virial ? 7 : 1, ev, 7, x_next, pack_idx, pack_code, pack_shifts,
-                                   pack_n, x_next + 4LL * n_local, s);
+                                   pack_n, x_next + 4LL * n_local, d2_zero, s);
         MDKK_CHECK_LAUNCH("k_reduce_pack");
         return MDKK_OK;
     }
@@ -468,7 +468,7 @@ extern "C" int mdkk_lj_force_integrate(mdkk_ctx* ctx, const double* x, int n_loc
                                        const unsigned char* part_flags, int part, void* stream) {
     return lj_integrate(ctx, x, n_local, table, counts, cap, virial, epsilon, sigma, rc, f, ev, flags, maxdisp2,
                         half_skin, max_count, count_limit, mode, v, x_ref, x_next, d2_next, dt, h, part_flags, part,
-                        nullptr, nullptr, nullptr, 0, stream);
+                        nullptr, nullptr, nullptr, 0, nullptr, stream);
 }
 
 extern "C" int mdkk_lj_force_integrate_pack(mdkk_ctx* ctx, const double* x, int n_local, const int* table,
@@ -477,11 +477,11 @@ extern "C" int mdkk_lj_force_integrate_pack(mdkk_ctx* ctx, const double* x, int 
                                             double half_skin, const int* max_count, int count_limit, double* v,
                                             const double* x_ref, double* x_next, double* d2_next, double dt, double h,
                                             const int* pack_idx, const int8_t* pack_code, const double* pack_shifts,
-                                            int pack_n, void* stream) {
+                                            int pack_n, double* d2_zero, void* stream) {
     if (pack_n < 0 || (pack_n > 0 && (!pack_idx || !pack_code || !pack_shifts))) return MDKK_E_ARG;
     return lj_integrate(ctx, x, n_local, table, counts, cap, virial, epsilon, sigma, rc, f, ev, flags, maxdisp2,
                         half_skin, max_count, count_limit, 2, v, x_ref, x_next, d2_next, dt, h, nullptr, 0, pack_idx,
-                        pack_code, pack_shifts, pack_n, stream);
+                        pack_code, pack_shifts, pack_n, d2_zero, stream);
 }
 
 extern "C" int mdkk_cluster_flags(const double* x, int n_local, const double* lo_host, const double* hi_host,

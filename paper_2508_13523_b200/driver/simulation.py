@@ -591,10 +591,12 @@ class Simulation:
         half = 0.5 * self.config.skin
         main = torch.cuda.current_stream(self.device)
         if getattr(self, "_fz", None) is None:
-            self._fz = dict(d2=torch.zeros(2, dtype=torch.float64, device=self.device),
-                            pin=torch.zeros(2, dtype=torch.float64, pin_memory=True),
-                            ready=[torch.cuda.Event(), torch.cuda.Event()], kicked=torch.cuda.Event(),
-                            side=torch.cuda.Stream(self.device), x_alt=None)
+            # drift maxima in a three-slot ring: step s writes slot s+1 and its (pack-fused)
+            # reduction clears slot s+2, whose previous read-back the host has already waited on
+            self._fz = dict(d2=torch.zeros(3, dtype=torch.float64, device=self.device),
+                            pin=torch.zeros(3, dtype=torch.float64, pin_memory=True),
+                            ready=[torch.cuda.Event(), torch.cuda.Event(), torch.cuda.Event()],
+                            kicked=torch.cuda.Event(), side=torch.cuda.Stream(self.device), x_alt=None)
         fz = self._fz
         d2 = fz["d2"]
 
@@ -623,6 +625,7 @@ class Simulation:
 
         fuse_pack = (not dist_) and isinstance(self.system, RankedSystem) and self.system.n_ranks == 1
         packed = False   # the ghost rows of the current x were written by the previous launch
+        cleared = None   # the d2 slot the previous launch's reduction cleared
         # opening of step 1: the classic pass (with any deferred closing kick)
         s.to_device()
         _lib.check(lib.mdkk_verlet_first(ctx, s.x.data_ptr(), s.v.data_ptr(), s.f.data_ptr(),
@@ -634,16 +637,15 @@ class Simulation:
         cur = 0
         read_back(cur)
         e = None
+        d2[1:].zero_()
         for step in range(1, n_steps + 1):
             self._run_step += 1
             mode = 2 if step < n_steps else 1
-            nxt = 1 - cur
+            nxt, aft = (cur + 1) % 3, (cur + 2) % 3
             xa = x_alt() if mode == 2 else None
 
             def launch(gated, part=0):
-                nonlocal packed
-                if mode == 2 and part != 2:
-                    d2[nxt:nxt + 1].zero_()
+                nonlocal packed, cleared
                 integ = dict(mode=mode, x_next=xa, d2_next=d2[nxt:nxt + 1], dt=self.dt, h=h, part=part)
                 if part:
                     integ["flags"] = self.system.cluster_flags(self.lists[0], overlap_halo)
@@ -656,8 +658,14 @@ class Simulation:
                         packed = True
                     elif len(lanes) == 1 and lanes[0].start == s.n_local:
                         integ["pack"] = (lanes[0], self.system._shift_dev)
+                        integ["d2_zero"] = d2[aft:aft + 1]   # the slot step s+2 writes
                         packed = True
-                return self._forces_device(gate=d2[cur:cur + 1] if gated else None, gate_limit=half, integ=integ)
+                if mode == 2 and part != 2 and cleared != nxt:
+                    d2[nxt:nxt + 1].zero_()
+                e_ = self._forces_device(gate=d2[cur:cur + 1] if gated else None, gate_limit=half, integ=integ)
+                # the slot this launch's reduction cleared (a relaunch of this step refills d2[nxt])
+                cleared = aft if "d2_zero" in integ else None
+                return e_
 
             if overlap:
                 # halo overlap: the clusters that list no exchanged ghost run while the

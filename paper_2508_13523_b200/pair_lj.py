@@ -137,7 +137,8 @@ def lj_force_rank(store, nl: NeighborList, params: PairParams, ev: torch.Tensor,
             flags.data_ptr(), gate.data_ptr() if gate is not None else None, gate_limit,
             pend[0].data_ptr() if pend is not None else None, nl.alloc_cap, store.v.data_ptr(),
             nl.ref_dev.data_ptr(), integ["x_next"].data_ptr(), integ["d2_next"].data_ptr(), integ["dt"], integ["h"],
-            ln.idx.data_ptr(), ln.code.data_ptr(), shifts.data_ptr(), ln.count, _lib.stream(dev)),
+            ln.idx.data_ptr(), ln.code.data_ptr(), shifts.data_ptr(), ln.count,
+            integ["d2_zero"].data_ptr() if integ.get("d2_zero") is not None else None, _lib.stream(dev)),
             "mdkk_lj_force_integrate_pack")
         return
     if integ is not None:
