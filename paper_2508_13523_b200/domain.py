@@ -338,6 +338,9 @@ def _init_layout():
 _init_layout()
 
 
+_COMBO_MEMO: dict = {}   # (device, src, halo, box, grid) -> (meta, combo table, codes)
+
+
 class _Lane:
     """One (src rank -> dst rank) forward/reverse lane: ghost rows [start, start+count) of dst."""
 
@@ -397,6 +400,14 @@ class RankedSystem:
         hit = self._combo_cache.get(key)
         if hit is not None:
             return hit
+        # the table depends only on the box, the brick grid and the halo: shared by every
+        # system on this device with the same decomposition (a new Simulation reuses it)
+        gkey = (str(self.device), src, float(halo), tuple(float(v) for v in self.box.lengths),
+                tuple(self.rankset.grid))
+        hit = _COMBO_MEMO.get(gkey)
+        if hit is not None:
+            self._combo_cache[key] = hit
+            return hit
         L = self.box.lengths
         rs = self.rankset
         meta, rows = [], []
@@ -414,7 +425,7 @@ class RankedSystem:
                 rows.append(np.concatenate([lo, hi, shift]))
         tab = torch.from_numpy(np.array(rows) if rows else np.zeros((0, 9))).to(self.device)
         codes = torch.tensor([c for _, c in meta], dtype=torch.int8, device=self.device)
-        hit = self._combo_cache[key] = (meta, tab, codes)
+        hit = self._combo_cache[key] = _COMBO_MEMO[gkey] = (meta, tab, codes)
         return hit
 
     def exchange_ghosts(self, halo: float) -> None:

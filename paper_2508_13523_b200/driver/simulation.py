@@ -748,8 +748,8 @@ class Simulation:
 
             pending = []     # (step, finish): snapshots whose read-back overlaps the next stretch
 
-            def settle_snapshots():
-                while pending:
+            def settle_snapshots(keep: int = 0):
+                while len(pending) > keep:
                     at, finish = pending.pop(0)
                     result.snapshots[at] = finish()
 
@@ -759,10 +759,8 @@ class Simulation:
                 ke, t = self._kinetic()
                 result.log(step, e_pot, ke, t)
                 if self.snapshots:
-                    if last:
-                        result.snapshots[step] = self.system.gather_positions()
-                    else:
-                        pending.append((step, self.system.gather_positions_async()))
+                    # queued on the copy stream; the host copy of an earlier snapshot overlaps it
+                    pending.append((step, self.system.gather_positions_async()))
                 self._qeq_diagnostic(step, result)
                 self.log(result.lines[-1])
 
@@ -773,9 +771,9 @@ class Simulation:
             while step < n_steps:   # device-resident stretches between thermo steps
                 k = min(self.thermo_every - step % self.thermo_every, n_steps - step)
                 e = self.advance(k)
-                settle_snapshots()
                 step += k
                 log(step, e, step == n_steps)
+                settle_snapshots(keep=1)   # earlier snapshots finish while this one is in flight
             settle_snapshots()
             result.n_rebuilds = self.n_rebuilds - rebuilds0
         return result

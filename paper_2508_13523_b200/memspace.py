@@ -91,9 +91,16 @@ def upload(a: np.ndarray, device) -> torch.Tensor:
     src = torch.from_numpy(np.ascontiguousarray(a))
     if src.numel() * src.element_size() < _STAGE_MIN or torch.device(device).type != "cuda":
         return src.to(device)
+    # staged in ~8 MB chunks: chunk k's DMA overlaps the host copy of chunk k+1
     pin = torch.empty(src.shape, dtype=src.dtype, pin_memory=True)
-    pin.copy_(src)
-    return pin.to(device, non_blocking=True)
+    dst = torch.empty(src.shape, dtype=src.dtype, device=device)
+    fs, fp, fd = src.reshape(-1), pin.reshape(-1), dst.reshape(-1)
+    step = max(1, (8 << 20) // src.element_size())
+    for a0 in range(0, fs.numel(), step):
+        a1 = min(fs.numel(), a0 + step)
+        fp[a0:a1].copy_(fs[a0:a1])
+        fd[a0:a1].copy_(fp[a0:a1], non_blocking=True)
+    return dst
 
 
 def download(t: torch.Tensor) -> np.ndarray:
