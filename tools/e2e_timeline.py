@@ -46,3 +46,11 @@ gaps.sort(reverse=True)
 print("largest device-idle gaps (us, before -> after, at ms):")
 for g in gaps[:20]:
     print(f"  {g[0]:9.1f}  {g[1]} -> {g[2]}  @{g[3]:.2f}")
+if len(sys.argv) > 1 and sys.argv[1] == "--head":
+    t0 = k[0]["ts"]
+    print("first ops (start ms, dur us, name):")
+    for e in k:
+        if (e["ts"] - t0) / 1e3 > float(sys.argv[2] if len(sys.argv) > 2 else 9.0):
+            break
+        if e["dur"] > 20:
+            print(f"  {(e['ts'] - t0) / 1e3:7.3f}  {e['dur']:8.1f}  {e['name'][:70]}")
