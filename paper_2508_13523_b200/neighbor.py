@@ -188,6 +188,8 @@ def _ref_into(buf: torch.Tensor, store: AtomStore) -> torch.Tensor:
 
 def _recycled(t: torch.Tensor | None, shape, dtype, device) -> torch.Tensor:
     """View of a dead list's storage when it is large enough (engine rebuilds), else a new tensor."""
+    if t is not None and t.shape == shape and t.dtype == dtype and t.device == device:
+        return t   # the usual engine rebuild: same rows, same capacity (no view ops on the host path)
     numel = 1
     for d in shape:
         numel *= d
@@ -268,15 +270,9 @@ def build(store: AtomStore, box: Box, cutoff: float, skin: float, style: str = "
         mean = n_local / max(vol, 1e-300) * (4.0 / 3.0) * math.pi * bc ** 3 * (0.5 if style == "half" else 1.0)
         cap_hint = grow_capacity(capacity, int(1.25 * mean) + 8)
     alloc = max(grow_capacity(capacity, 0), int(cap_hint or 0))
-    old_t = recycle.table_dev if recycle is not None else None
-    counts = _recycled(recycle.counts_dev if recycle is not None else None, (max(n_local, 1),), torch.int32, dev)
-    mc = cache.get("mc", 1, torch.int32, dev)   # one element; stream-ordered reuse across builds
-    mc.zero_()
-    deferred = defer and cap_hint is not None
-    if deferred:
-        table = _recycled(old_t, ((n_local + 31) // 32 or 1, alloc, 32), torch.int32, dev)
-    # the list buffers are ready before the binning is queued: binning and build go out
-    # back to back (no host work between their launches while the device waits)
+    # the binning is queued first (on a rebuild the device is idle until it arrives); the
+    # list buffers are prepared while it runs, in less host time than its ~70 us of device
+    # work, so the build launch still follows it back to back
     if merged is None:
         pass
     elif merged:
@@ -286,6 +282,13 @@ def build(store: AtomStore, box: Box, cutoff: float, skin: float, style: str = "
     else:
         _lib.check(lib.mdkk_bin_atoms(ctx, store.x.data_ptr(), n_total, garr, narr, keys.data_ptr(),
                                       cstart.data_ptr(), catoms.data_ptr(), stream), "mdkk_bin_atoms")
+    old_t = recycle.table_dev if recycle is not None else None
+    counts = _recycled(recycle.counts_dev if recycle is not None else None, (max(n_local, 1),), torch.int32, dev)
+    mc = cache.get("mc", 1, torch.int32, dev)   # one element; stream-ordered reuse across builds
+    mc.zero_()
+    deferred = defer and cap_hint is not None
+    if deferred:
+        table = _recycled(old_t, ((n_local + 31) // 32 or 1, alloc, 32), torch.int32, dev)
     if deferred:
         _lib.check(lib.mdkk_nbr_build(ctx, store.x.data_ptr(), n_local, n_total, garr, narr, cstart.data_ptr(),
                                       catoms.data_ptr(), store.gid.data_ptr(), store.orank.data_ptr(),

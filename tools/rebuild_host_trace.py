@@ -47,3 +47,56 @@ for rep in range(3):
             print(f"{(t - prev) * 1e6:8.1f} us before {n}")
             prev = t
         print(f"{(t1 - prev) * 1e6:8.1f} us to the end of _rebuild_lists; total host {(t1 - t0) * 1e6:.1f} us")
+
+if "--cprofile" in sys.argv:
+    # where the host time between the library calls goes (function-level, one rebuild)
+    import cProfile, pstats
+    for rep in range(3):
+        torch.cuda.synchronize()
+        pr = cProfile.Profile()
+        pr.enable()
+        sim._rebuild_lists(defer=True)
+        sim._forces_device()
+        pr.disable()
+        sim._settle_lists()
+        torch.cuda.synchronize()
+    pstats.Stats(pr).sort_stats("tottime").print_stats(30)
+
+if "--fine" in sys.argv:
+    # entry / exit stamps of the Python functions between the library calls
+    import functools
+    from paper_2508_13523_b200 import domain, neighbor
+    from paper_2508_13523_b200.driver import simulation
+
+    def stamp(owner, name):
+        f = getattr(owner, name)
+
+        @functools.wraps(f)
+        def g(*a, **k):
+            T.append((time.perf_counter(), f"> {name}"))
+            r = f(*a, **k)
+            T.append((time.perf_counter(), f"< {name}"))
+            return r
+        setattr(owner, name, g)
+    for owner, names in ((domain.AtomStore, ["ensure_capacity", "_views", "device_wrote", "to_device"]),
+                         (domain.RankedSystem, ["migrate", "_migrate_single", "_buf", "_combos"]),
+                         (neighbor, ["build", "_recycled"]),
+                         (neighbor.NeighborList, ["__init__"]),
+                         (simulation.Simulation, ["_forces_device"])):
+        for nm in names:
+            if hasattr(owner, nm):
+                stamp(owner, nm)
+    simulation.build = neighbor.build
+    for rep in range(3):
+        torch.cuda.synchronize()
+        T.clear()
+        t0 = time.perf_counter()
+        sim._rebuild_lists(defer=True)
+        sim._forces_device()
+        t1 = time.perf_counter()
+        sim._settle_lists()
+        torch.cuda.synchronize()
+    prev = t0
+    for t, n in T:
+        print(f"{(t - prev) * 1e6:8.1f} us before {n}")
+        prev = t
