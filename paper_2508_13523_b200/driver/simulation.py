@@ -24,7 +24,7 @@ import torch
 
 from .. import _lib
 from ..domain import Box, RankedSystem
-from ..memspace import Atomic, Duplicate, Serial
+from ..memspace import Atomic, Duplicate, Serial, pinned_array
 from ..neighbor import build, build_all
 from ..pair_lj import LJCut, PairParams, PairResult, compute_pair, lj_force_rank
 from .registry import StyleRegistry
@@ -270,8 +270,9 @@ class Simulation:
     def _cmd_create_atoms(self, a):
         if self.cells is None:
             raise RunError("create_box must run before create_atoms")
-        self._positions, self.box = lattice_positions(self.lattice_spec[0], self.lattice_spec[1], self.cells)
-        self._velocities = np.zeros_like(self._positions)
+        pos, self.box = lattice_positions(self.lattice_spec[0], self.lattice_spec[1], self.cells)
+        self._positions = pinned_array(pos)   # the run's upload is then one DMA per array
+        self._velocities = pinned_array(np.zeros_like(pos))
         self.system = None
 
     def _cmd_mass(self, a):
@@ -286,7 +287,7 @@ class Simulation:
         t, seed = float(a[0]), int(a[1])
         if self.config.rng_seed is not None:
             seed = self.config.rng_seed
-        self._velocities = seeded_velocities(len(self._positions), t, self.mass, seed)
+        self._velocities = pinned_array(seeded_velocities(len(self._positions), t, self.mass, seed))
         self.system = None
 
     def _cmd_pair_style(self, a):

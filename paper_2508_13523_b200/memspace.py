@@ -83,13 +83,31 @@ class LayoutPolicy:
 _STAGE_MIN = 1 << 20   # bytes: larger host<->device copies go through pinned staging
 
 
+def pinned_array(a: np.ndarray) -> np.ndarray:
+    """A copy of `a` in page-locked host memory (a numpy view of a pinned torch block), so
+    that `upload` DMAs it directly; `a` itself when it is small or there is no GPU.  The
+    engine keeps the host-side state it generates (lattice positions, seeded velocities)
+    this way: the run's first upload is then a plain DMA."""
+    a = np.ascontiguousarray(a)
+    if a.nbytes < _STAGE_MIN or a.dtype not in _TORCH_DTYPE or not torch.cuda.is_available():
+        return a
+    pin = torch.empty(a.shape, dtype=_TORCH_DTYPE[a.dtype], pin_memory=True)
+    out = pin.numpy()
+    torch.from_numpy(out).copy_(torch.from_numpy(a))
+    return out
+
+
 def upload(a: np.ndarray, device) -> torch.Tensor:
-    """Host array -> device tensor.  Large arrays are staged through pinned memory
-    with torch's multi-threaded host copy, then DMA'd asynchronously (the caching
-    host allocator keeps the staging block until the copy completes): ~2x the
-    pageable path, whose single-threaded staging is the bottleneck."""
+    """Host array -> device tensor.  Pinned arrays (`pinned_array`) are one DMA; large
+    pageable arrays are staged through pinned memory with torch's multi-threaded host
+    copy, then DMA'd asynchronously (the caching host allocator keeps the staging block
+    until the copy completes): ~2x the pageable path, whose single-threaded staging is
+    the bottleneck."""
     src = torch.from_numpy(np.ascontiguousarray(a))
     if src.numel() * src.element_size() < _STAGE_MIN or torch.device(device).type != "cuda":
+        return src.to(device)
+    if src.is_pinned():
+        # direct DMA; blocking, so the caller may free or rewrite the host array on return
         return src.to(device)
     # staged in ~8 MB chunks: chunk k's DMA overlaps the host copy of chunk k+1
     pin = torch.empty(src.shape, dtype=src.dtype, pin_memory=True)
