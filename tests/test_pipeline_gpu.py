@@ -126,6 +126,12 @@ def test_overlapped_snapshots_match_synchronous_reads(gpu):
     assert sorted(ra.snapshots) == [0, 10, 20, 30]
     for step, snap in ra.snapshots.items():
         assert np.array_equal(snap, ref[step]), step
+    # each snapshot owns its (pinned) block: later steps and later snapshots leave it alone
+    snaps = list(ra.snapshots.values())
+    assert not any(np.shares_memory(p, q) for i, p in enumerate(snaps) for q in snaps[i + 1:])
+    keep = {k: v.copy() for k, v in ra.snapshots.items()}
+    a.run_nve(20)
+    assert all(np.array_equal(ra.snapshots[k], keep[k]) for k in keep)
 
 
 @pytest.mark.parametrize("style", ["full", "half"])
@@ -201,3 +207,20 @@ def test_single_rank_migrate_fast_path_matches_general_path(gpu):
         assert torch.equal(a[k], b[k]), k
     assert a[6] is True and b[6] is False
     assert torch.equal(a[7], a[0][: a[7].shape[0]])   # the reference rows are the sorted owned rows
+
+
+def test_generated_inputs_are_pinned_and_upload_directly(gpu):
+    """The engine keeps the positions / velocities it generates in pinned host memory
+    (memspace.pinned_array), so the run's upload is a single DMA; values are unchanged."""
+    import torch
+    from paper_2508_13523_b200 import memspace
+    from paper_2508_13523_b200.driver import RunConfig, Simulation
+    a = np.random.default_rng(3).random((100_000, 3))
+    p = memspace.pinned_array(a)
+    assert torch.from_numpy(p).is_pinned() and np.array_equal(p, a) and not np.shares_memory(p, a)
+    assert np.array_equal(memspace.upload(p, torch.device("cuda", 0)).cpu().numpy(), a)
+    small = np.arange(6.0).reshape(2, 3)
+    assert memspace.pinned_array(small) is small or np.array_equal(memspace.pinned_array(small), small)
+    sim = Simulation(RunConfig(list_style="full", newton=False), log=None)
+    sim.execute(MELT.replace("create_box 8 8 8", "create_box 23 23 23"))
+    assert torch.from_numpy(sim._positions).is_pinned() and torch.from_numpy(sim._velocities).is_pinned()
