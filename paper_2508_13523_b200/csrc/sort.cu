@@ -113,17 +113,33 @@ int scan_impl(mdkk_ctx* ctx, const T* in, T* out, long long n, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------ many buckets
+// Warp-aggregated: the engine's keys are nearly sorted (rows keep the previous cell
+// order), so a warp's 32 rows fall in ~2 cells and per-row atomics would serialise on
+// the same counters; one atomic per distinct key per warp instead.
 __global__ void k_key_count(int n, const int* __restrict__ key, int* __restrict__ counts) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) atomicAdd(counts + key[i], 1);
+    const bool valid = i < n;
+    const unsigned act = __ballot_sync(0xffffffffu, valid);
+    if (!valid) return;
+    const int c = key[i];
+    const unsigned same = __match_any_sync(act, c);
+    if ((threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(counts + c, __popc(same));
 }
 
 __global__ void k_key_scatter(int n, const int* __restrict__ key, const int* __restrict__ start,
                               int* __restrict__ cursor, int* __restrict__ order) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
+    const bool valid = i < n;
+    const unsigned act = __ballot_sync(0xffffffffu, valid);
+    if (!valid) return;
     const int c = key[i];
-    order[start[c] + atomicAdd(cursor + c, 1)] = i;
+    const int lane = threadIdx.x & 31;
+    const unsigned same = __match_any_sync(act, c);
+    const int leader = __ffs(same) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(cursor + c, __popc(same));
+    base = __shfl_sync(same, base, leader);
+    order[start[c] + base + __popc(same & ((1u << lane) - 1u))] = i;
 }
 
 // kRsG lanes per bucket (32 / kRsG buckets per warp): the rows the scatter placed in
