@@ -30,6 +30,11 @@ void* scratch_tail(mdkk_ctx* ctx, size_t bytes);
 // Exclusive prefix sums (csrc/sort.cu), out[k] = in[0] + ... + in[k-1]; in != out.
 int exclusive_scan_i32(mdkk_ctx* ctx, const int* in, int* out, long long n, cudaStream_t s);
 int exclusive_scan_i64(mdkk_ctx* ctx, const long long* in, long long* out, long long n, cudaStream_t s);
+// mdkk_bucket_sort (many buckets) from counts the caller already took: cnt[nbuckets + 1]
+// (zeroed, then one increment per key; cnt[nbuckets] = 0), reused as the scatter cursors.
+int bucket_sort_counted(mdkk_ctx* ctx, const int* keys, int n, int nbuckets, int* cnt, int* bucket_start,
+                        int* order, cudaStream_t s);
+constexpr int kSortSmallBuckets = 64;   // mdkk_bucket_sort's few-bucket path (per-block tables) up to here
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 

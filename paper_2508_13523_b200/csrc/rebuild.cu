@@ -13,23 +13,56 @@
 namespace {
 cudaEvent_t g_totals_ev[64];   // per device, created lazily
 
+__device__ __forceinline__ double4 wrapped(double4 p, double Lx, double Ly, double Lz) {
+    p.x = __dsub_rn(p.x, __dmul_rn(Lx, floor(p.x / Lx)));
+    p.y = __dsub_rn(p.y, __dmul_rn(Ly, floor(p.y / Ly)));
+    p.z = __dsub_rn(p.z, __dmul_rn(Lz, floor(p.z / Lz)));
+    return p;
+}
+
+
 // Wrap (pos - L floor(pos / L) with explicit roundings, as k_wrap / mdkk/domain.py:62)
-// and the cell key of the wrapped row (as k_cell_keys), one pass over x.
+// and the cell key of the wrapped row (as k_cell_keys), one pass over x (few cells).
 __global__ void k_wrap_keys(double* __restrict__ x, int n, double Lx, double Ly, double Lz, mdkk::Grid g,
                             int* __restrict__ key) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    double4 p = mdkk::ld4_nc(x, i);
-    p.x = __dsub_rn(p.x, __dmul_rn(Lx, floor(p.x / Lx)));
-    p.y = __dsub_rn(p.y, __dmul_rn(Ly, floor(p.y / Ly)));
-    p.z = __dsub_rn(p.z, __dmul_rn(Lz, floor(p.z / Lz)));
+    const double4 p = wrapped(mdkk::ld4_nc(x, i), Lx, Ly, Lz);
     mdkk::st4(x, i, p);
     const int3 c = mdkk::cell_of(g, p.x, p.y, p.z);
     key[i] = mdkk::cell_key(g, c.x, c.y, c.z);
 }
 
-// The sort's position gather, also writing the rows into the new lists' skin-test
-// reference (the build-time positions) -- one pass over x instead of a later copy.
+// The many-cell form: the wrapped row's cell key plus the sort's count pass (one atomic per
+// distinct key per warp), without writing x back -- the gather below wraps the rows it
+// moves, with the same operations, so the sorted positions are bit-identical.
+__global__ void k_wrap_keys_count(const double* __restrict__ x, int n, double Lx, double Ly, double Lz,
+                                  mdkk::Grid g, int* __restrict__ key, int* __restrict__ cnt) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool valid = i < n;
+    const unsigned act = __ballot_sync(0xffffffffu, valid);
+    if (!valid) return;
+    const double4 p = wrapped(mdkk::ld4(x, i), Lx, Ly, Lz);
+    const int3 c = mdkk::cell_of(g, p.x, p.y, p.z);
+    const int k = mdkk::cell_key(g, c.x, c.y, c.z);
+    key[i] = k;
+    const unsigned same = __match_any_sync(act, k);
+    if ((threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(cnt + k, __popc(same));
+}
+
+// The sort's position gather of unwrapped rows, wrapping each; with `ref` it also writes
+// the rows into the new lists' skin-test reference (the build-time positions) -- one
+// pass over x instead of a later copy.
+__global__ void k_gather4_wrap(const double* __restrict__ src, const int* __restrict__ perm, int n, double Lx,
+                               double Ly, double Lz, double* __restrict__ dst, double* __restrict__ ref) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double4 p = wrapped(mdkk::ld4(src, perm[i]), Lx, Ly, Lz);
+    mdkk::st4(dst, i, p);
+    if (ref) mdkk::st4(ref, i, p);
+}
+
+// As k_gather4_wrap for rows x already wrapped in place (the few-cell path).
 __global__ void k_gather4_ref(const double* __restrict__ src, const int* __restrict__ perm, int n,
                               double* __restrict__ dst, double* __restrict__ ref) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -63,16 +96,32 @@ int mdkk_rebuild1_select(mdkk_ctx* ctx, double* x, int n, const double* lengths_
     const long long ncl = (long long)ncell_host[0] * ncell_host[1] * ncell_host[2];
     if (ncl < 1 || ncl > (1LL << 30)) return MDKK_E_ARG;
     const mdkk::Grid g = mdkk::make_grid(grid_host, ncell_host);
-    k_wrap_keys<<<mdkk::grid_for(n, 256), 256, 0, s>>>(x, n, lengths_host[0], lengths_host[1], lengths_host[2], g,
-                                                       keys);
-    MDKK_CHECK_LAUNCH("k_wrap_keys");
-    int st = mdkk_bucket_sort(ctx, keys, n, (int)ncl, cell_start, order, stream);
-    if (st == MDKK_OK) {
-        if (x_ref) {
-            k_gather4_ref<<<mdkk::grid_for(n, 256), 256, 0, s>>>(x, order, n, x_sorted, x_ref);
-            MDKK_CHECK_LAUNCH("k_gather4_ref");
-        } else {
-            st = mdkk_gather_rows4(x, order, n, x_sorted, stream);
+    const double Lx = lengths_host[0], Ly = lengths_host[1], Lz = lengths_host[2];
+    int st = MDKK_OK;
+    if (ncl > mdkk::kSortSmallBuckets) {
+        // wrap folded into the key / count pass and the gather (x itself is not rewritten:
+        // after the sort it is the spare buffer)
+        int* cnt = static_cast<int*>(mdkk::scratch(ctx, sizeof(int) * ((size_t)ncl + 1)));
+        if (!cnt) return mdkk::cuda_fail(cudaErrorMemoryAllocation, "sort scratch");
+        cudaMemsetAsync(cnt, 0, sizeof(int) * ((size_t)ncl + 1), s);
+        k_wrap_keys_count<<<mdkk::grid_for(n, 256), 256, 0, s>>>(x, n, Lx, Ly, Lz, g, keys, cnt);
+        MDKK_CHECK_LAUNCH("k_wrap_keys_count");
+        st = mdkk::bucket_sort_counted(ctx, keys, n, (int)ncl, cnt, cell_start, order, s);
+        if (st == MDKK_OK) {
+            k_gather4_wrap<<<mdkk::grid_for(n, 256), 256, 0, s>>>(x, order, n, Lx, Ly, Lz, x_sorted, x_ref);
+            MDKK_CHECK_LAUNCH("k_gather4_wrap");
+        }
+    } else {
+        k_wrap_keys<<<mdkk::grid_for(n, 256), 256, 0, s>>>(x, n, Lx, Ly, Lz, g, keys);
+        MDKK_CHECK_LAUNCH("k_wrap_keys");
+        st = mdkk_bucket_sort(ctx, keys, n, (int)ncl, cell_start, order, stream);
+        if (st == MDKK_OK) {
+            if (x_ref) {
+                k_gather4_ref<<<mdkk::grid_for(n, 256), 256, 0, s>>>(x, order, n, x_sorted, x_ref);
+                MDKK_CHECK_LAUNCH("k_gather4_ref");
+            } else {
+                st = mdkk_gather_rows4(x, order, n, x_sorted, stream);
+            }
         }
     }
     // owned rows are now cell-sorted on the shell grid (cells >= halo wide): only rows within

@@ -136,8 +136,11 @@ __global__ void k_key_scatter(int n, const int* __restrict__ key, const int* __r
     const int lane = threadIdx.x & 31;
     const unsigned same = __match_any_sync(act, c);
     const int leader = __ffs(same) - 1;
+    // the counts count down as the cursors (each warp's run of a bucket lands ascending;
+    // the row sort orders the runs)
+    const int m = __popc(same);
     int base = 0;
-    if (lane == leader) base = atomicAdd(cursor + c, __popc(same));
+    if (lane == leader) base = atomicSub(cursor + c, m) - m;
     base = __shfl_sync(same, base, leader);
     order[start[c] + base + __popc(same & ((1u << lane) - 1u))] = i;
 }
@@ -289,9 +292,18 @@ extern "C" int mdkk_bucket_sort(mdkk_ctx* ctx, const int* keys, int n, int nbuck
     cudaMemsetAsync(cnt, 0, sizeof(int) * ((size_t)nbuckets + 1), s);
     k_key_count<<<mdkk::grid_for(n, 256), 256, 0, s>>>(n, keys, cnt);
     MDKK_CHECK_LAUNCH("k_key_count");
+    return mdkk::bucket_sort_counted(ctx, keys, n, nbuckets, cnt, bucket_start, order, s);
+}
+
+namespace mdkk {
+
+// The many-bucket sort after its count pass: cnt[nbuckets + 1] holds the per-bucket
+// counts (cnt[nbuckets] = 0), e.g. taken by the producer of the keys.
+int bucket_sort_counted(mdkk_ctx* ctx, const int* keys, int n, int nbuckets, int* cnt, int* bucket_start,
+                        int* order, cudaStream_t s) {
     int st = mdkk::exclusive_scan_i32(ctx, cnt, bucket_start, (long long)nbuckets + 1, s);
     if (st != MDKK_OK) return st;
-    cudaMemsetAsync(cnt, 0, sizeof(int) * (size_t)nbuckets, s);   // now the per-bucket cursors
+    // the counts themselves are the per-bucket cursors (counted down by the scatter)
     k_key_scatter<<<mdkk::grid_for(n, 256), 256, 0, s>>>(n, keys, bucket_start, cnt, order);
     MDKK_CHECK_LAUNCH("k_key_scatter");
     const long long threads = (long long)nbuckets * kRsG;
@@ -299,3 +311,5 @@ extern "C" int mdkk_bucket_sort(mdkk_ctx* ctx, const int* keys, int n, int nbuck
     MDKK_CHECK_LAUNCH("k_bucket_rowsort");
     return MDKK_OK;
 }
+
+}  // namespace mdkk
