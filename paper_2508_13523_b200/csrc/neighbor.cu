@@ -28,6 +28,38 @@ __global__ void k_cell_keys(const double* __restrict__ x, int n, Grid g, int* __
     key[i] = mdkk::cell_key(g, c.x, c.y, c.z);
 }
 
+// k_cell_keys + the counting sort's count pass (one atomic per distinct key per warp).
+__global__ void k_cell_keys_count(const double* __restrict__ x, int n, Grid g, int* __restrict__ key,
+                                  int* __restrict__ cnt) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool valid = i < n;
+    const unsigned act = __ballot_sync(0xffffffffu, valid);
+    if (!valid) return;
+    const double4 p = mdkk::ld4(x, i);
+    const int3 c = mdkk::cell_of(g, p.x, p.y, p.z);
+    const int k = mdkk::cell_key(g, c.x, c.y, c.z);
+    key[i] = k;
+    const unsigned same = __match_any_sync(act, k);
+    if ((threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(cnt + k, __popc(same));
+}
+
+// Binning = cell keys + stable counting sort; with many cells the key pass also counts.
+int bin_rows(mdkk_ctx* ctx, const double* x, int n, const double* grid_host, const int* ncell_host, int ncell,
+             int* keys, int* cell_start, int* cell_atoms, cudaStream_t s) {
+    if (n == 0 || ncell <= mdkk::kSortSmallBuckets) {
+        int st = mdkk_cell_keys(x, n, grid_host, ncell_host, keys, s);
+        if (st != MDKK_OK) return st;
+        return mdkk_bucket_sort(ctx, keys, n, ncell, cell_start, cell_atoms, s);
+    }
+    int* cnt = static_cast<int*>(mdkk::scratch(ctx, sizeof(int) * ((size_t)ncell + 1)));
+    if (!cnt) return mdkk::cuda_fail(cudaErrorMemoryAllocation, "sort scratch");
+    cudaMemsetAsync(cnt, 0, sizeof(int) * ((size_t)ncell + 1), s);
+    k_cell_keys_count<<<mdkk::grid_for(n, 256), 256, 0, s>>>(x, n, mdkk::make_grid(grid_host, ncell_host), keys,
+                                                             cnt);
+    MDKK_CHECK_LAUNCH("k_cell_keys_count");
+    return mdkk::bucket_sort_counted(ctx, keys, n, ncell, cnt, cell_start, cell_atoms, s);
+}
+
 // Owning brick: floor(pos / L * grid) clipped (mdkk/domain.py:89-95).
 __global__ void k_rank_keys(const double* __restrict__ x, int n, double Lx, double Ly, double Lz, int gx,
                             int gy, int gz, int* __restrict__ key) {
@@ -700,9 +732,8 @@ int mdkk_bin_atoms(mdkk_ctx* ctx, const double* x, int n, const double* grid_hos
     if (!ctx || n < 0 || !grid_host || !ncell_host) return MDKK_E_ARG;
     long long ncell = (long long)ncell_host[0] * ncell_host[1] * ncell_host[2];
     if (ncell < 1 || ncell > (1LL << 30)) return MDKK_E_ARG;
-    int st = mdkk_cell_keys(x, n, grid_host, ncell_host, keys, stream);
-    if (st != MDKK_OK) return st;
-    return mdkk_bucket_sort(ctx, keys, n, (int)ncell, cell_start, cell_atoms, stream);
+    return bin_rows(ctx, x, n, grid_host, ncell_host, (int)ncell, keys, cell_start, cell_atoms,
+                    mdkk::as_stream(stream));
 }
 
 int mdkk_nbr_build(mdkk_ctx* ctx, const double* x, int n_local, int n_total, const double* grid_host,
@@ -771,8 +802,8 @@ int mdkk_bin_merge(mdkk_ctx* ctx, const double* x, int n_local, int n_total, con
     if (!base) return mdkk::cuda_fail(cudaErrorMemoryAllocation, "scratch");
     int* gstart = base + cnt_words;
     int* gord = gstart + ncell + 64;
-    int st = mdkk_cell_keys(x + 4LL * n_local, n_ghost, grid_host, ncell_host, keys, stream);
-    if (st == MDKK_OK) st = mdkk_bucket_sort(ctx, keys, n_ghost, ncell, gstart, gord, stream);
+    // (the sort's counters are the arena's first ncell + 1 words: `base`)
+    int st = bin_rows(ctx, x + 4LL * n_local, n_ghost, grid_host, ncell_host, ncell, keys, gstart, gord, s);
     if (st != MDKK_OK) return st;
     // one warp per cell: its owned rows (a contiguous range of the sorted brick) then its ghost rows
     k_merge_cells<<<mdkk::grid_for((long long)ncell * 32, 256), 256, 0, s>>>(owned_start, gstart, gord, ncell,
