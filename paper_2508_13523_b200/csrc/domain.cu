@@ -72,14 +72,23 @@ __global__ void k_halo_count(const double* __restrict__ x, int n, const double* 
     const int i = halo_row(blockIdx.x * blockDim.x + threadIdx.x, n, rows, n_dev, ok);
     double4 p = make_double4(0, 0, 0, 0);
     if (ok) p = mdkk::ld4(x, i);
+    __shared__ int s_wc[kHaloBlock / 32][64];   // per-warp counts of the group's combos
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     for (int c0 = 0; c0 < C; c0 += 64) {   // combos in groups of 64 (one mask word)
         const unsigned long long mine = combo_mask(p, sc, c0, C, ok);
         const unsigned long long any = block_or(mine, &s_or);
-        for (int c = c0; c < min(C, c0 + 64); ++c) {
-            int cnt = 0;
-            if ((any >> (c - c0)) & 1ull)   // block-uniform branch
-                cnt = __syncthreads_count((int)((mine >> (c - c0)) & 1ull));
-            if (threadIdx.x == 0) block_counts[(long long)c * gridDim.x + blockIdx.x] = cnt;   // combo-major
+        // one ballot per present combo per warp, one barrier for the group (not one per combo)
+        for (unsigned long long a = any; a; a &= a - 1ull) {   // block-uniform
+            const int cb = __ffsll((long long)a) - 1;
+            const int cnt = __popc(__ballot_sync(0xffffffffu, (mine >> cb) & 1ull));
+            if (lane == 0) s_wc[wid][cb] = cnt;
+        }
+        __syncthreads();
+        for (int cb = threadIdx.x; cb < min(64, C - c0); cb += blockDim.x) {
+            int t = 0;
+            if ((any >> cb) & 1ull)
+                for (int q = 0; q < kHaloBlock / 32; ++q) t += s_wc[q][cb];
+            block_counts[(long long)(c0 + cb) * gridDim.x + blockIdx.x] = t;   // combo-major
         }
         __syncthreads();
     }
@@ -144,7 +153,7 @@ __global__ void k_halo_fill(const double* __restrict__ x, int n, const double* _
                             const int* __restrict__ n_dev) {
     extern __shared__ double sc[];
     int* base = reinterpret_cast<int*>(sc + 9 * C);
-    __shared__ int warp_cnt[kHaloBlock / 32];
+    __shared__ unsigned s_bal[kHaloBlock / 32][64];   // per-warp ballots of the group's combos
     __shared__ unsigned long long s_or;
     if (n_dev && (long long)blockIdx.x * blockDim.x >= *n_dev) return;
     for (int t = threadIdx.x; t < 9 * C; t += blockDim.x) sc[t] = combos[t];
@@ -162,26 +171,27 @@ __global__ void k_halo_fill(const double* __restrict__ x, int n, const double* _
     double4 p = make_double4(0, 0, 0, 0);
     if (ok) p = mdkk::ld4(x, i);
     for (int c0 = 0; c0 < C; c0 += 64) {   // combos in groups of 64 (one mask word)
-    const unsigned long long mine = combo_mask(p, sc, c0, C, ok);
-    unsigned long long any = block_or(mine, &s_or);
-    while (any) {   // block-uniform: only the combos some row of this block falls in
-        const int cb = __ffsll((long long)any) - 1;
-        const int c = c0 + cb;
-        any &= any - 1ull;
-        const bool flag = (mine >> cb) & 1ull;
-        unsigned m = __ballot_sync(0xffffffffu, flag);
-        if (lane == 0) warp_cnt[wid] = __popc(m);
+        const unsigned long long mine = combo_mask(p, sc, c0, C, ok);
+        const unsigned long long any = block_or(mine, &s_or);
+        // the ballots of every present combo, then one barrier: each row's rank in its combo
+        // = rows of earlier warps + earlier lanes (rows ascending, as the one-barrier-per-combo
+        // form had it)
+        for (unsigned long long a = any; a; a &= a - 1ull) {   // block-uniform
+            const int cb = __ffsll((long long)a) - 1;
+            const unsigned m = __ballot_sync(0xffffffffu, (mine >> cb) & 1ull);
+            if (lane == 0) s_bal[wid][cb] = m;
+        }
         __syncthreads();
-        int before = 0;
-        for (int w = 0; w < wid; ++w) before += warp_cnt[w];
-        if (flag) {
-            int r = before + __popc(m & ((1u << lane) - 1u));
+        for (unsigned long long a = mine; a; a &= a - 1ull) {
+            const int cb = __ffsll((long long)a) - 1;
+            const int c = c0 + cb;
+            int r = __popc(s_bal[wid][cb] & ((1u << lane) - 1u));
+            for (int q = 0; q < wid; ++q) r += __popc(s_bal[q][cb]);
             const int o = base[c] + block_off[(long long)c * gridDim.x + blockIdx.x] + r;
             out[o] = i;
             if (out_code) out_code[o] = combo_code[c];
         }
         __syncthreads();
-    }
     }
 }
 
