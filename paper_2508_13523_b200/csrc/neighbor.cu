@@ -81,25 +81,28 @@ __global__ void k_cell_positions(const double* __restrict__ x, const int* __rest
     xs[s] = make_float4((float)p.x, (float)p.y, (float)p.z, __int_as_float(j));   // .w = the row
 }
 
-// Merged cell lists (mdkk_bin_merge), one warp per cell: cell_start[c] = owned_start[c] +
+// Merged cell lists (mdkk_bin_merge), eight lanes per cell: cell_start[c] = owned_start[c] +
 // ghost_start[c]; the cell's owned rows (rows owned_start[c] .. owned_start[c+1] of the
 // cell-sorted brick) then its ghost rows (n_local + ghost_order[...]) -- exactly the
 // bin_atoms order over all rows (owned then ghost rows per cell, each ascending).
 __global__ void k_merge_cells(const int* __restrict__ owned_start, const int* __restrict__ ghost_start,
                               const int* __restrict__ ghost_order, int ncell, int n_local, int n_total,
                               int* __restrict__ cell_start, int* __restrict__ cell_atoms) {
-    const int c = (int)(((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-    const int lane = threadIdx.x & 31;
+    // eight lanes per cell (cells hold ~20 rows: a warp per cell left most lanes idle and
+    // the kernel latency bound on one cell's loads per warp)
+    constexpr int G = 8;
+    const int c = (int)(((long long)blockIdx.x * blockDim.x + threadIdx.x) / G);
+    const int sl = threadIdx.x & (G - 1);
     if (c >= ncell) return;
     const int os = owned_start[c], no = owned_start[c + 1] - os;
     const int gs = ghost_start[c], ng = ghost_start[c + 1] - gs;
     const int b = os + gs;
-    if (lane == 0) {
+    if (sl == 0) {
         cell_start[c] = b;
         if (c == ncell - 1) cell_start[ncell] = n_total;
     }
-    for (int t = lane; t < no; t += 32) cell_atoms[b + t] = os + t;
-    for (int t = lane; t < ng; t += 32) cell_atoms[b + no + t] = n_local + ghost_order[gs + t];
+    for (int t = sl; t < no; t += G) cell_atoms[b + t] = os + t;
+    for (int t = sl; t < ng; t += G) cell_atoms[b + no + t] = n_local + ghost_order[gs + t];
 }
 
 __device__ __forceinline__ bool lex_zyx_less(double ax, double ay, double az, double bx, double by, double bz) {
@@ -805,8 +808,8 @@ int mdkk_bin_merge(mdkk_ctx* ctx, const double* x, int n_local, int n_total, con
     // (the sort's counters are the arena's first ncell + 1 words: `base`)
     int st = bin_rows(ctx, x + 4LL * n_local, n_ghost, grid_host, ncell_host, ncell, keys, gstart, gord, s);
     if (st != MDKK_OK) return st;
-    // one warp per cell: its owned rows (a contiguous range of the sorted brick) then its ghost rows
-    k_merge_cells<<<mdkk::grid_for((long long)ncell * 32, 256), 256, 0, s>>>(owned_start, gstart, gord, ncell,
+    // per cell: its owned rows (a contiguous range of the sorted brick) then its ghost rows
+    k_merge_cells<<<mdkk::grid_for((long long)ncell * 8, 256), 256, 0, s>>>(owned_start, gstart, gord, ncell,
                                                                               n_local, n_total, cell_start,
                                                                               cell_atoms);
     MDKK_CHECK_LAUNCH("k_merge_cells");
